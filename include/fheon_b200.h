@@ -1,0 +1,159 @@
+/* fheon_b200.h -- C ABI of the B200-native RNS-CKKS engine for FHEON's
+ * encrypted-CNN hot path (arXiv 2510.03996).
+ *
+ * The reference (slotcnn, /root/reference/proj) is a C++ library with no FFI:
+ * its "plug point" is the backend free functions of
+ * proj/include/slotcnn/backend.hpp:134-153 and the layer API of
+ * proj/include/slotcnn/layers.hpp:83-158, replaced at link time
+ * (SURVEY.md section 8(b)).  Each entry point below names the reference
+ * interface it replaces.  INTEGRATION.md shows the C++ shim a maintainer
+ * links into slotcnn (and the ctypes stub used by this repo's tests).
+ *
+ * Conventions
+ *   - every function returns 0 on success, else the reference ErrorCategory
+ *     (errors.hpp:18-22): 1 usage, 2 data, 3 internal; fheon_last_error()
+ *     returns the message (thread-local), fheon_last_error_kind() the
+ *     exception class (1 InvalidRotationError, 2 DepthExhaustedError,
+ *     3 ShapeError, 4 CapacityError, 5 ModelError, 6 InternalError, 7 CUDA,
+ *     8 not implemented).
+ *   - ciphertext handles are immutable values (backend.hpp:106-131); every op
+ *     returns a fresh handle the caller releases with fheon_ct_free().
+ *   - all work is enqueued on the context's CUDA stream (fheon_ctx_stream);
+ *     calls that return host data synchronise it.
+ *   - levels follow the reference: level = limbs - 1; add/sub -> min level,
+ *     mult_plain -> level - 1, mult_cipher -> min - 1 (backend.hpp:10-16).
+ */
+#ifndef FHEON_B200_H
+#define FHEON_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fheon_ctx fheon_ctx;
+typedef struct fheon_ct fheon_ct;
+
+/* Replaces ContextConfig + CryptoMetadata (backend.hpp:34-59), which the
+ * reference only carries as metadata; here they define the RNS chain. */
+typedef struct {
+  int log_n;          /* ring degree N = 2^log_n (10..16); slots S = N/2 */
+  int limbs;          /* L: Q-chain limbs (levels 0..L-1) */
+  int special_limbs;  /* K: special primes for hybrid key switching */
+  int dnum;           /* key-switching digits */
+  int first_mod_bits; /* bits of q_0 (CryptoMetadata::first_modulus_bits) */
+  int scale_bits;     /* scaling-prime bits (CryptoMetadata::rescale_bits) */
+  int special_bits;   /* special-prime bits */
+  int depth_budget;   /* ContextConfig::depth_budget; -1 = limbs - 1 */
+  uint64_t seed;      /* key / encryption randomness seed */
+} fheon_params;
+
+/* ---- errors / version */
+const char* fheon_last_error(void);
+int fheon_last_error_kind(void);
+int fheon_version(void);
+
+/* ---- context (SlotContext::create, backend.hpp:69) */
+int fheon_ctx_create(const fheon_params* p, fheon_ctx** out);
+void fheon_ctx_destroy(fheon_ctx* ctx);
+/* primes[L+K], scales[L] (scale target per level), slots */
+int fheon_ctx_info(const fheon_ctx* ctx, uint64_t* primes, double* scales, int* slots);
+void* fheon_ctx_stream(fheon_ctx* ctx); /* cudaStream_t */
+int fheon_ctx_sync(fheon_ctx* ctx);
+/* op counters: rotations, keyswitches, mult_plain, mult_cipher, rescales, ntt_limbs, encodes, adds */
+int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* out8);
+int fheon_ctx_reset_stats(fheon_ctx* ctx);
+
+/* ---- trace (TraceRecorder, trace.hpp:37-103; SlotContext::attach_recorder)
+ * events: pairs (kind, value); kind 0 rotation (index), 1 mult_plain
+ * (level_after), 2 mult_cipher (level_after), 3 bootstrap (level_after). */
+int fheon_set_tracing(fheon_ctx* ctx, int on);
+int fheon_trace(fheon_ctx* ctx, long* events, size_t cap, size_t* n);
+int fheon_trace_clear(fheon_ctx* ctx);
+
+/* ---- keys (keyplan.hpp KeySet: rotation keys resident in HBM) */
+uint64_t fheon_galois_elt(const fheon_ctx* ctx, long t); /* 5^t mod 2N */
+int fheon_keygen_rotations(fheon_ctx* ctx, const long* steps, size_t n);
+int fheon_keygen_relin(fheon_ctx* ctx);
+int fheon_set_strict_keys(fheon_ctx* ctx, int strict); /* 1: missing key is an error */
+/* key_id: 0 = relinearisation, else Galois element; out [dnum][2][L+K][N] standard form */
+int fheon_key_download(fheon_ctx* ctx, uint64_t key_id, uint64_t* out);
+size_t fheon_key_count(const fheon_ctx* ctx);
+
+/* ---- ciphertexts (SlotVector, backend.hpp:108-132) */
+void fheon_ct_free(fheon_ct* ct);
+int fheon_ct_level(const fheon_ct* ct);
+int fheon_ct_limbs(const fheon_ct* ct);
+double fheon_ct_scale(const fheon_ct* ct);
+/* SlotVector::encode (backend.cpp:148-161): encode + encrypt at the depth budget */
+int fheon_encrypt(fheon_ctx* ctx, const double* values, size_t n, fheon_ct** out);
+/* encode + encrypt at the top of the chain (L limbs) */
+int fheon_encrypt_top(fheon_ctx* ctx, const double* values, size_t n, fheon_ct** out);
+/* decrypt + decode all S slots into out[n >= S] */
+int fheon_decrypt(fheon_ctx* ctx, const fheon_ct* ct, double* out, size_t n);
+/* raw RNS words, layout [2][limbs][N] */
+int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* words, int limbs, double scale, fheon_ct** out);
+int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);
+
+/* ---- backend ops (backend.hpp:134-153) */
+int fheon_rotate(fheon_ctx* ctx, const fheon_ct* x, long t, fheon_ct** out);
+/* hoisted rotation set sharing one ModUp of x (layers_conv.cpp:102-113 tap_rotations) */
+int fheon_rotate_hoisted(fheon_ctx* ctx, const fheon_ct* x, const long* ts, size_t n, fheon_ct** outs);
+int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
+int fheon_sub(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
+int fheon_add_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, size_t n, fheon_ct** out);
+int fheon_mult_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, size_t n, fheon_ct** out);
+int fheon_mult_cipher(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
+int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out);
+int fheon_rescale(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out);
+int fheon_level_down(fheon_ctx* ctx, const fheon_ct* a, int limbs, fheon_ct** out);
+/* key switch of a's c1 (as d) with key key_id under automorphism g (1 = none); out = (ks0, ks1) */
+int fheon_keyswitch_raw(fheon_ctx* ctx, const fheon_ct* a, uint64_t key_id, uint64_t g, fheon_ct** out);
+
+/* ---- RNS primitives on host buffers (parity checking / microbench).
+ * words [npolys][nlimbs][N]; limb i uses prime i. */
+int fheon_ntt_host(fheon_ctx* ctx, uint64_t* words, int npolys, int nlimbs, int inverse);
+int fheon_automorph_host(fheon_ctx* ctx, uint64_t* words, int npolys, int nlimbs, uint64_t g);
+
+/* ---- device-resident microbench (config 2): times `iters` launches of a
+ * primitive with CUDA events on the context stream; returns mean ms.
+ * kind: 0 NTT fwd, 1 iNTT, 2 automorphism, 3 rotation (single key switch),
+ * 4 hoisted rotations (n_rot), 5 pt x ct MAC term, 6 rescale, 7 add */
+int fheon_microbench(fheon_ctx* ctx, int kind, int batch, int limbs, int n_rot, int iters, double* ms);
+
+/* ---- layers (layers.hpp:83-158).  Tensors are packed channel-major
+ * (slot c*W^2 + i*W + j, packing.hpp:8-10). */
+typedef struct {
+  size_t in_channels, out_channels, kernel, stride, padding;
+  int mode;           /* 0 generic, 1 special3x3, 2 grouped (ConvMode) */
+  int stride_variant; /* 0 extract, 1 masked (StrideVariant) */
+} fheon_conv_cfg;
+
+/* convolution (layers_conv.cpp:577-594); weights (F, C or 1, k, k), bias F (may be NULL) */
+int fheon_convolution(fheon_ctx* ctx, const fheon_ct* x, size_t channels, size_t width, const fheon_conv_cfg* cfg,
+                      const double* weights, const double* bias, fheon_ct** out, size_t* out_channels,
+                      size_t* out_width);
+/* avg_pool (layers_misc.cpp:99-144): kind 0 average(k, stride, variant), 1 global, 2 whole-channel(k) */
+int fheon_pool(fheon_ctx* ctx, const fheon_ct* x, size_t channels, size_t width, int kind, size_t kernel,
+               size_t stride, int stride_variant, fheon_ct** out, size_t* out_channels, size_t* out_width);
+/* fully_connected (layers_misc.cpp:197-255); weights (m, n) row-major, bias m (may be NULL) */
+int fheon_fully_connected(fheon_ctx* ctx, const fheon_ct* x, size_t inputs, size_t outputs, size_t merge_budget,
+                          const double* weights, const double* bias, fheon_ct** out);
+/* secure_relu (layers_misc.cpp:268-295): Chebyshev interpolant of max(0, scale*z), degree */
+int fheon_secure_relu(fheon_ctx* ctx, const fheon_ct* x, double scale, int degree, size_t active_slots,
+                      fheon_ct** out);
+/* stride stage (layers_conv.cpp:285-421): variant 0 extract (v1), 1 masked (v2); w_out 0 = default */
+int fheon_stride(fheon_ctx* ctx, const fheon_ct* x, size_t width, size_t stride, size_t w_out, int variant,
+                 fheon_ct** out);
+/* pad_input (layers_conv.cpp:238-283) */
+int fheon_pad_input(fheon_ctx* ctx, const fheon_ct* x, size_t channels, size_t width, size_t padding,
+                    fheon_ct** out);
+/* declared depth costs (layers_conv.cpp:596-628, layers_misc.cpp:297-322) */
+int fheon_conv_depth_cost(const fheon_conv_cfg* cfg, size_t w_in, int* cost);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHEON_B200_H */

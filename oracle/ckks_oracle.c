@@ -162,10 +162,12 @@ ock_ctx* ock_create(int logN, int L, int K, int dnum, int first_bits,
         const u64 down = base - k * M, up = base + (k + 1) * M;
         const u64 first = (tgt - down <= up - tgt) ? down : up;
         const u64 second = (first == down) ? up : down;
-        if (is_prime(first) && !used(c, np, first)) pick = first;
-        else if (is_prime(second) && !used(c, np, second)) pick = second;
-        if (pick) {
-          for (int i = L - 1; i > lv; i--) if (chosen[i] == pick) pick = 0;
+        const u64 cand[2] = {first, second};
+        for (int ci = 0; ci < 2 && !pick; ci++) {
+          const u64 x = cand[ci];
+          int ok = is_prime(x) && !used(c, np, x);
+          for (int i = L - 1; ok && i > lv; i--) if (chosen[i] == x) ok = 0;
+          if (ok) pick = x;
         }
       }
       chosen[lv] = pick;

@@ -1,0 +1,129 @@
+"""ctypes binding of the C ABI (include/fheon_b200.h).
+
+The shared library is built in-tree (paper_2510_03996_b200/_lib/libfheon_b200.so,
+see csrc/Makefile or __graft_entry__.build()).  There is no CPU fallback: if
+the library is missing, or no CUDA device is visible, every call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libfheon_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "fheon_b200.h")
+
+_lib = None
+
+
+class fheon_params(C.Structure):
+    _fields_ = [
+        ("log_n", C.c_int),
+        ("limbs", C.c_int),
+        ("special_limbs", C.c_int),
+        ("dnum", C.c_int),
+        ("first_mod_bits", C.c_int),
+        ("scale_bits", C.c_int),
+        ("special_bits", C.c_int),
+        ("depth_budget", C.c_int),
+        ("seed", C.c_uint64),
+    ]
+
+
+class fheon_conv_cfg(C.Structure):
+    _fields_ = [
+        ("in_channels", C.c_size_t),
+        ("out_channels", C.c_size_t),
+        ("kernel", C.c_size_t),
+        ("stride", C.c_size_t),
+        ("padding", C.c_size_t),
+        ("mode", C.c_int),
+        ("stride_variant", C.c_int),
+    ]
+
+
+vp = C.c_void_p
+pp = C.POINTER(C.c_void_p)
+dp = C.POINTER(C.c_double)
+u64p = C.POINTER(C.c_uint64)
+szp = C.POINTER(C.c_size_t)
+lp = C.POINTER(C.c_long)
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "fheon_last_error": (C.c_char_p, []),
+    "fheon_last_error_kind": (C.c_int, []),
+    "fheon_version": (C.c_int, []),
+    "fheon_ctx_create": (C.c_int, [C.POINTER(fheon_params), pp]),
+    "fheon_ctx_destroy": (None, [vp]),
+    "fheon_ctx_info": (C.c_int, [vp, u64p, dp, C.POINTER(C.c_int)]),
+    "fheon_ctx_stream": (vp, [vp]),
+    "fheon_ctx_sync": (C.c_int, [vp]),
+    "fheon_ctx_stats": (C.c_int, [vp, u64p]),
+    "fheon_ctx_reset_stats": (C.c_int, [vp]),
+    "fheon_set_tracing": (C.c_int, [vp, C.c_int]),
+    "fheon_trace": (C.c_int, [vp, lp, C.c_size_t, szp]),
+    "fheon_trace_clear": (C.c_int, [vp]),
+    "fheon_galois_elt": (C.c_uint64, [vp, C.c_long]),
+    "fheon_keygen_rotations": (C.c_int, [vp, lp, C.c_size_t]),
+    "fheon_keygen_relin": (C.c_int, [vp]),
+    "fheon_set_strict_keys": (C.c_int, [vp, C.c_int]),
+    "fheon_key_download": (C.c_int, [vp, C.c_uint64, u64p]),
+    "fheon_key_count": (C.c_size_t, [vp]),
+    "fheon_ct_free": (None, [vp]),
+    "fheon_ct_level": (C.c_int, [vp]),
+    "fheon_ct_limbs": (C.c_int, [vp]),
+    "fheon_ct_scale": (C.c_double, [vp]),
+    "fheon_encrypt": (C.c_int, [vp, dp, C.c_size_t, pp]),
+    "fheon_encrypt_top": (C.c_int, [vp, dp, C.c_size_t, pp]),
+    "fheon_decrypt": (C.c_int, [vp, vp, dp, C.c_size_t]),
+    "fheon_ct_upload": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
+    "fheon_ct_download": (C.c_int, [vp, vp, u64p]),
+    "fheon_rotate": (C.c_int, [vp, vp, C.c_long, pp]),
+    "fheon_rotate_hoisted": (C.c_int, [vp, vp, lp, C.c_size_t, pp]),
+    "fheon_add": (C.c_int, [vp, vp, vp, pp]),
+    "fheon_sub": (C.c_int, [vp, vp, vp, pp]),
+    "fheon_add_plain": (C.c_int, [vp, vp, dp, C.c_size_t, pp]),
+    "fheon_mult_plain": (C.c_int, [vp, vp, dp, C.c_size_t, pp]),
+    "fheon_mult_cipher": (C.c_int, [vp, vp, vp, pp]),
+    "fheon_bootstrap": (C.c_int, [vp, vp, pp]),
+    "fheon_rescale": (C.c_int, [vp, vp, pp]),
+    "fheon_level_down": (C.c_int, [vp, vp, C.c_int, pp]),
+    "fheon_keyswitch_raw": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, pp]),
+    "fheon_ntt_host": (C.c_int, [vp, u64p, C.c_int, C.c_int, C.c_int]),
+    "fheon_automorph_host": (C.c_int, [vp, u64p, C.c_int, C.c_int, C.c_uint64]),
+    "fheon_microbench": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp]),
+    "fheon_convolution": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.POINTER(fheon_conv_cfg), dp, dp, pp, szp,
+                                    szp]),
+    "fheon_pool": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.c_int, C.c_size_t, C.c_size_t, C.c_int, pp, szp,
+                             szp]),
+    "fheon_fully_connected": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.c_size_t, dp, dp, pp]),
+    "fheon_secure_relu": (C.c_int, [vp, vp, C.c_double, C.c_int, C.c_size_t, pp]),
+    "fheon_stride": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, pp]),
+    "fheon_pad_input": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.c_size_t, pp]),
+    "fheon_conv_depth_cost": (C.c_int, [C.POINTER(fheon_conv_cfg), C.c_size_t, C.POINTER(C.c_int)]),
+}
+
+
+def lib():
+    """Load the in-tree shared library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"B200 engine library not built: {LIB_PATH} (run `make -C paper_2510_03996_b200/csrc` "
+                "or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def header_symbols():
+    """Function names declared in include/fheon_b200.h."""
+    import re
+    text = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(fheon_[a-z0-9_]+)\s*\(", text)))

@@ -1,0 +1,363 @@
+// extern "C" boundary (include/fheon_b200.h): opaque handles, int status,
+// thread-local error message.  Exceptions never cross this boundary.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "../../include/fheon_b200.h"
+#include "engine.hpp"
+#include "layers.hpp"
+
+struct fheon_ctx {
+  fheon::Context* impl;
+};
+struct fheon_ct {
+  fheon::Ciphertext ct;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_kind = 0;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const fheon::Error& e) {
+    g_err = e.what();
+    g_kind = static_cast<int>(e.kind);
+    return fheon::category_of(e.kind);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_kind = static_cast<int>(fheon::ErrKind::internal);
+    return 3;
+  }
+}
+
+fheon_ct* wrap(const fheon::Ciphertext& c) { return new fheon_ct{c}; }
+
+void need(const void* p, const char* what) {
+  if (!p) throw fheon::Error(fheon::ErrKind::internal, std::string(what) + " is null");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fheon_last_error(void) { return g_err.c_str(); }
+int fheon_last_error_kind(void) { return g_kind; }
+int fheon_version(void) { return 1; }
+
+int fheon_ctx_create(const fheon_params* p, fheon_ctx** out) {
+  return guard([&] {
+    need(p, "params");
+    need(out, "out");
+    fheon::Params prm;
+    prm.logN = p->log_n;
+    prm.L = p->limbs;
+    prm.K = p->special_limbs;
+    prm.dnum = p->dnum;
+    prm.first_bits = p->first_mod_bits;
+    prm.scale_bits = p->scale_bits;
+    prm.special_bits = p->special_bits;
+    prm.depth_budget = p->depth_budget;
+    prm.seed = p->seed;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      throw fheon::Error(fheon::ErrKind::cuda, "no CUDA device visible: the B200 engine has no CPU fallback");
+    try {
+      *out = new fheon_ctx{new fheon::Context(prm)};
+    } catch (const std::invalid_argument& e) {
+      throw fheon::Error(fheon::ErrKind::shape, e.what());
+    }
+  });
+}
+
+void fheon_ctx_destroy(fheon_ctx* ctx) {
+  if (!ctx) return;
+  delete ctx->impl;
+  delete ctx;
+}
+
+int fheon_ctx_info(const fheon_ctx* ctx, uint64_t* primes, double* scales, int* slots) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const fheon::HostTables& h = ctx->impl->host();
+    if (primes)
+      for (std::size_t i = 0; i < h.q.size(); ++i) primes[i] = h.q[i];
+    if (scales)
+      for (std::size_t i = 0; i < h.T.size(); ++i) scales[i] = h.T[i];
+    if (slots) *slots = h.S;
+  });
+}
+
+void* fheon_ctx_stream(fheon_ctx* ctx) { return ctx ? static_cast<void*>(ctx->impl->stream()) : nullptr; }
+
+int fheon_ctx_sync(fheon_ctx* ctx) {
+  return guard([&] { FHEON_CUDA(cudaStreamSynchronize(ctx->impl->stream())); });
+}
+
+int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* o) {
+  return guard([&] {
+    const fheon::OpStats& s = ctx->impl->stats;
+    o[0] = s.rotations;
+    o[1] = s.keyswitches;
+    o[2] = s.mult_plain;
+    o[3] = s.mult_cipher;
+    o[4] = s.rescales;
+    o[5] = s.ntt_limbs;
+    o[6] = s.encodes;
+    o[7] = s.adds;
+  });
+}
+int fheon_ctx_reset_stats(fheon_ctx* ctx) {
+  return guard([&] { ctx->impl->stats = fheon::OpStats{}; });
+}
+
+int fheon_set_tracing(fheon_ctx* ctx, int on) {
+  return guard([&] { ctx->impl->set_tracing(on != 0); });
+}
+int fheon_trace(fheon_ctx* ctx, long* ev, size_t cap, size_t* n) {
+  return guard([&] {
+    std::size_t k = 0;
+    for (const fheon::TraceEvent& e : ctx->impl->trace_snapshot()) {
+      if (e.kind > 3) continue;
+      if (ev && k < cap) {
+        ev[2 * k] = e.kind;
+        ev[2 * k + 1] = e.value;
+      }
+      ++k;
+    }
+    if (n) *n = k;
+  });
+}
+int fheon_trace_clear(fheon_ctx* ctx) {
+  return guard([&] { ctx->impl->clear_trace(); });
+}
+
+uint64_t fheon_galois_elt(const fheon_ctx* ctx, long t) { return ctx->impl->galois(t); }
+
+int fheon_keygen_rotations(fheon_ctx* ctx, const long* steps, size_t n) {
+  return guard([&] {
+    for (size_t i = 0; i < n; ++i) {
+      const fheon::u64 g = ctx->impl->galois(steps[i]);
+      if (g != 1) ctx->impl->gen_key(g);
+    }
+    FHEON_CUDA(cudaStreamSynchronize(ctx->impl->stream()));
+  });
+}
+int fheon_keygen_relin(fheon_ctx* ctx) {
+  return guard([&] { ctx->impl->gen_key(0); });
+}
+int fheon_set_strict_keys(fheon_ctx* ctx, int strict) {
+  return guard([&] { ctx->impl->strict_keys = strict != 0; });
+}
+size_t fheon_key_count(const fheon_ctx* ctx) { return ctx->impl->num_keys(); }
+
+int fheon_key_download(fheon_ctx* ctx, uint64_t key_id, uint64_t* out) {
+  return guard([&] {
+    fheon::Context& c = *ctx->impl;
+    const fheon::u64* k = c.key(key_id);
+    const std::size_t words = c.key_words();
+    fheon::BufPtr tmp = c.alloc(words);
+    const int NP = c.L() + c.K();
+    const std::size_t LN = (std::size_t)NP * c.N();
+    for (std::size_t blk = 0; blk < words / LN; ++blk)
+      fheon::convert_mont(c.dev(), tmp->ptr + blk * LN, k + blk * LN, NP, NP, false, c.stream());
+    FHEON_CUDA(cudaMemcpyAsync(out, tmp->ptr, words * sizeof(uint64_t), cudaMemcpyDeviceToHost, c.stream()));
+    FHEON_CUDA(cudaStreamSynchronize(c.stream()));
+  });
+}
+
+void fheon_ct_free(fheon_ct* ct) { delete ct; }
+int fheon_ct_level(const fheon_ct* ct) { return ct ? ct->ct.level() : -1; }
+int fheon_ct_limbs(const fheon_ct* ct) { return ct ? ct->ct.limbs : 0; }
+double fheon_ct_scale(const fheon_ct* ct) { return ct ? ct->ct.scale : 0.0; }
+
+int fheon_encrypt(fheon_ctx* ctx, const double* v, size_t n, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::encrypt(*ctx->impl, v, n)); });
+}
+int fheon_encrypt_top(fheon_ctx* ctx, const double* v, size_t n, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::encrypt_top(*ctx->impl, v, n)); });
+}
+int fheon_decrypt(fheon_ctx* ctx, const fheon_ct* ct, double* out, size_t n) {
+  return guard([&] {
+    need(ct, "ciphertext");
+    if (n < (size_t)ctx->impl->S()) throw fheon::Error(fheon::ErrKind::capacity, "output buffer smaller than S");
+    fheon::decrypt(*ctx->impl, ct->ct, out);
+  });
+}
+int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* w, int limbs, double scale, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::upload_ct(*ctx->impl, w, limbs, scale)); });
+}
+int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* w) {
+  return guard([&] { fheon::download_ct(*ctx->impl, ct->ct, w); });
+}
+
+int fheon_rotate(fheon_ctx* ctx, const fheon_ct* x, long t, fheon_ct** out) {
+  return guard([&] {
+    need(x, "ciphertext");
+    *out = wrap(fheon::rotate(*ctx->impl, x->ct, t));
+  });
+}
+int fheon_rotate_hoisted(fheon_ctx* ctx, const fheon_ct* x, const long* ts, size_t n, fheon_ct** outs) {
+  return guard([&] {
+    need(x, "ciphertext");
+    std::vector<long> v(ts, ts + n);
+    std::vector<fheon::Ciphertext> r = fheon::rotate_hoisted(*ctx->impl, x->ct, v);
+    for (size_t i = 0; i < n; ++i) outs[i] = wrap(r[i]);
+  });
+}
+int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::add(*ctx->impl, a->ct, b->ct)); });
+}
+int fheon_sub(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::sub(*ctx->impl, a->ct, b->ct)); });
+}
+int fheon_add_plain(fheon_ctx* ctx, const fheon_ct* a, const double* v, size_t n, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::add_plain(*ctx->impl, a->ct, v, n)); });
+}
+int fheon_mult_plain(fheon_ctx* ctx, const fheon_ct* a, const double* v, size_t n, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::mult_plain(*ctx->impl, a->ct, v, n)); });
+}
+int fheon_mult_cipher(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::mult_cipher(*ctx->impl, a->ct, b->ct)); });
+}
+int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::bootstrap(*ctx->impl, a->ct)); });
+}
+int fheon_rescale(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::rescale(*ctx->impl, a->ct)); });
+}
+int fheon_level_down(fheon_ctx* ctx, const fheon_ct* a, int limbs, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::level_down(*ctx->impl, a->ct, limbs)); });
+}
+int fheon_keyswitch_raw(fheon_ctx* ctx, const fheon_ct* a, uint64_t key_id, uint64_t g, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::keyswitch_raw(*ctx->impl, a->ct, key_id, g)); });
+}
+
+int fheon_ntt_host(fheon_ctx* ctx, uint64_t* w, int npolys, int nlimbs, int inverse) {
+  return guard([&] {
+    fheon::Context& c = *ctx->impl;
+    const std::size_t words = (std::size_t)npolys * nlimbs * c.N();
+    fheon::BufPtr b = c.alloc(words);
+    FHEON_CUDA(cudaMemcpyAsync(b->ptr, w, words * sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream()));
+    fheon::LimbSet s{};
+    s.base[0] = b->ptr;
+    s.nbase = 1;
+    s.blocks_per_base = npolys;
+    s.block_stride = (long long)nlimbs * c.N();
+    s.E = nlimbs;
+    s.ell = nlimbs;
+    s.L = c.L();
+    if (inverse) fheon::ntt_inverse(c.dev(), s, c.stream());
+    else fheon::ntt_forward(c.dev(), s, c.stream());
+    FHEON_CUDA(cudaMemcpyAsync(w, b->ptr, words * sizeof(uint64_t), cudaMemcpyDeviceToHost, c.stream()));
+    FHEON_CUDA(cudaStreamSynchronize(c.stream()));
+  });
+}
+
+int fheon_automorph_host(fheon_ctx* ctx, uint64_t* w, int npolys, int nlimbs, uint64_t g) {
+  return guard([&] {
+    fheon::Context& c = *ctx->impl;
+    const std::size_t words = (std::size_t)npolys * nlimbs * c.N();
+    fheon::BufPtr in = c.alloc(words), out = c.alloc(words);
+    FHEON_CUDA(cudaMemcpyAsync(in->ptr, w, words * sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream()));
+    fheon::PolyList o{}, i{};
+    for (int p = 0; p < npolys; ++p) {
+      o.p[p] = out->ptr + (std::size_t)p * nlimbs * c.N();
+      o.g[p] = g;
+      i.p[p] = in->ptr + (std::size_t)p * nlimbs * c.N();
+    }
+    o.n = i.n = npolys;
+    fheon::automorph(c.dev(), o, i, nlimbs, c.stream());
+    FHEON_CUDA(cudaMemcpyAsync(w, out->ptr, words * sizeof(uint64_t), cudaMemcpyDeviceToHost, c.stream()));
+    FHEON_CUDA(cudaStreamSynchronize(c.stream()));
+  });
+}
+
+int fheon_microbench(fheon_ctx* ctx, int kind, int batch, int limbs, int n_rot, int iters, double* ms) {
+  return guard([&] { *ms = fheon::microbench(*ctx->impl, kind, batch, limbs, n_rot, iters); });
+}
+
+// ---------------------------------------------------------------- layers
+int fheon_convolution(fheon_ctx* ctx, const fheon_ct* x, size_t C, size_t W, const fheon_conv_cfg* cfg,
+                      const double* w, const double* bias, fheon_ct** out, size_t* oc, size_t* ow) {
+  return guard([&] {
+    need(x, "ciphertext");
+    need(cfg, "config");
+    fheon::ConvConfig c{cfg->in_channels, cfg->out_channels, cfg->kernel, cfg->stride, cfg->padding, cfg->mode,
+                        cfg->stride_variant};
+    fheon::PackedTensor in{x->ct, C, W};
+    fheon::KernelTensor kt = fheon::KernelTensor::from(c, w, bias);
+    fheon::PackedTensor r = fheon::convolution(*ctx->impl, in, c, kt);
+    *out = wrap(r.data);
+    if (oc) *oc = r.channels;
+    if (ow) *ow = r.width;
+  });
+}
+
+int fheon_pool(fheon_ctx* ctx, const fheon_ct* x, size_t C, size_t W, int kind, size_t k, size_t stride,
+               int variant, fheon_ct** out, size_t* oc, size_t* ow) {
+  return guard([&] {
+    need(x, "ciphertext");
+    fheon::PackedTensor in{x->ct, C, W};
+    if (kind == 0) {
+      fheon::PackedTensor r = fheon::avg_pool(*ctx->impl, in, k, stride, variant);
+      *out = wrap(r.data);
+      if (oc) *oc = r.channels;
+      if (ow) *ow = r.width;
+    } else {
+      fheon::Ciphertext r = kind == 1 ? fheon::global_avg_pool(*ctx->impl, in)
+                                      : fheon::whole_channel_pool(*ctx->impl, in, k);
+      *out = wrap(r);
+      if (oc) *oc = C;
+      if (ow) *ow = 1;
+    }
+  });
+}
+
+int fheon_fully_connected(fheon_ctx* ctx, const fheon_ct* x, size_t n, size_t m, size_t merge_budget,
+                          const double* w, const double* bias, fheon_ct** out) {
+  return guard([&] {
+    need(x, "ciphertext");
+    *out = wrap(fheon::fully_connected(*ctx->impl, x->ct, n, m, merge_budget, w, bias));
+  });
+}
+
+int fheon_secure_relu(fheon_ctx* ctx, const fheon_ct* x, double scale, int degree, size_t active, fheon_ct** out) {
+  return guard([&] {
+    need(x, "ciphertext");
+    *out = wrap(fheon::secure_relu(*ctx->impl, x->ct, scale, degree, active));
+  });
+}
+
+int fheon_stride(fheon_ctx* ctx, const fheon_ct* x, size_t W, size_t S, size_t w_out, int variant, fheon_ct** out) {
+  return guard([&] {
+    need(x, "ciphertext");
+    const size_t wo = w_out ? w_out : (W + S - 1) / S;
+    *out = wrap(variant == 1 ? fheon::stride_extract_v2(*ctx->impl, x->ct, W, S, wo)
+                             : fheon::stride_extract_v1(*ctx->impl, x->ct, W, S, wo));
+  });
+}
+
+int fheon_pad_input(fheon_ctx* ctx, const fheon_ct* x, size_t C, size_t W, size_t P, fheon_ct** out) {
+  return guard([&] {
+    need(x, "ciphertext");
+    fheon::PackedTensor r = fheon::pad_input(*ctx->impl, fheon::PackedTensor{x->ct, C, W}, P);
+    *out = wrap(r.data);
+  });
+}
+
+int fheon_conv_depth_cost(const fheon_conv_cfg* cfg, size_t w_in, int* cost) {
+  return guard([&] {
+    fheon::ConvConfig c{cfg->in_channels, cfg->out_channels, cfg->kernel, cfg->stride, cfg->padding, cfg->mode,
+                        cfg->stride_variant};
+    *cost = fheon::conv_depth_cost(c, w_in);
+  });
+}
+
+}  // extern "C"

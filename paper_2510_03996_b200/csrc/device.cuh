@@ -1,0 +1,145 @@
+// Device-side 64-bit modular arithmetic for sm_100a, built from the 32-bit
+// IMAD datapath (nvcc lowers mul.lo/mul.hi.u64 to IMAD.WIDE.U32 chains).
+//
+//  * Shoup multiplication by a precomputed constant w (w' = floor(w 2^64 / q))
+//    for NTT twiddles and per-limb scalars.
+//  * Montgomery REDC (R = 2^64) for variable x variable products and 128-bit
+//    lazy accumulations (basis conversion, key inner product): any sum
+//    x < q * 2^64 reduces with one REDC.  Keys and multiplicand plaintexts are
+//    held in Montgomery form so REDC(sum a_i * (b_i R)) = sum a_i b_i mod q.
+//  * All ciphertext words are canonical in [0, q) between kernels, so every
+//    kernel output is directly comparable word-for-word with the oracle.
+#pragma once
+
+#include <cstdint>
+
+namespace fheon {
+
+using u64 = std::uint64_t;
+
+struct PrimeConst {
+  u64 q;
+  u64 qinv_neg;  // -q^{-1} mod 2^64
+  u64 r2;        // R^2 mod q
+  u64 mu64;      // floor(2^64 / q)
+  u64 ninv, ninv_sh;
+  u64 rmod;      // R mod q
+  u64 pad;
+};
+
+constexpr int kMaxBases = 32;
+
+// A set of limb-polynomials addressed as base[b] + blk * block_stride + t * N
+// with blk < blocks_per_base and t < E; prime of limb t is p0 + t (t < ell) or
+// L + (t - ell) (special primes).  skip_alpha > 0 skips t in digit blk's own
+// range [blk*alpha, min((blk+1)*alpha, ell)) (ModUp outputs).
+struct LimbSet {
+  u64* base[kMaxBases];
+  int nbase;
+  int blocks_per_base;
+  long long block_stride;
+  int E;
+  int ell;
+  int L;
+  int skip_alpha;
+  int p0;  // prime index of limb t = 0 (q limbs)
+  int count() const { return nbase * blocks_per_base * E; }
+};
+
+#ifdef __CUDACC__
+
+__device__ __forceinline__ u64 mulhi(u64 a, u64 b) { return __umul64hi(a, b); }
+
+__device__ __forceinline__ u64 csub(u64 x, u64 q) { return x >= q ? x - q : x; }
+__device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 q) { return csub(a + b, q); }
+__device__ __forceinline__ u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+
+// a * w mod q for canonical-or-lazy a < 2^64 and constant w < q.
+__device__ __forceinline__ u64 shoup_mul(u64 a, u64 w, u64 wsh, u64 q) {
+  const u64 h = mulhi(a, wsh);
+  return csub(a * w - h * q, q);
+}
+
+// x = hi:lo < q * 2^64  ->  x * 2^-64 mod q (canonical).
+__device__ __forceinline__ u64 redc(u64 hi, u64 lo, u64 q, u64 qneg) {
+  const u64 m = lo * qneg;
+  const u64 t = hi + mulhi(m, q) + (lo != 0 ? 1ULL : 0ULL);
+  return csub(t, q);
+}
+
+struct Acc128 {
+  u64 lo = 0, hi = 0;
+  __device__ __forceinline__ void mac(u64 a, u64 b) {
+    const u64 l = a * b;
+    const u64 h = mulhi(a, b);
+    lo += l;
+    hi += h + (lo < l ? 1ULL : 0ULL);
+  }
+};
+
+__device__ __forceinline__ u64 mont_mul(u64 a, u64 b_mont, const PrimeConst& p) {
+  return redc(mulhi(a, b_mont), a * b_mont, p.q, p.qinv_neg);
+}
+// standard-form product of two canonical values
+__device__ __forceinline__ u64 mul_mod(u64 a, u64 b, const PrimeConst& p) {
+  const u64 t = redc(mulhi(a, b), a * b, p.q, p.qinv_neg);
+  return redc(mulhi(t, p.r2), t * p.r2, p.q, p.qinv_neg);
+}
+__device__ __forceinline__ u64 to_mont_d(u64 a, const PrimeConst& p) {
+  return redc(mulhi(a, p.r2), a * p.r2, p.q, p.qinv_neg);
+}
+// x mod q for any 64-bit x
+__device__ __forceinline__ u64 reduce64(u64 x, const PrimeConst& p) {
+  return csub(x - mulhi(x, p.mu64) * p.q, p.q);
+}
+__device__ __forceinline__ u64 reduce_signed(long long v, const PrimeConst& p) {
+  if (v >= 0) return reduce64((u64)v, p);
+  const u64 r = reduce64((u64)(-(v + 1)), p);
+  return p.q - 1 - r;
+}
+
+__device__ __forceinline__ bool limbset_get(const LimbSet& s, int idx, std::size_t N,
+                                            u64*& ptr, int& prime) {
+  const int per_base = s.blocks_per_base * s.E;
+  const int b = idx / per_base;
+  const int r = idx - b * per_base;
+  const int blk = r / s.E;
+  const int t = r - blk * s.E;
+  if (s.skip_alpha > 0) {
+    const int lo = blk * s.skip_alpha;
+    const int hi = min(lo + s.skip_alpha, s.ell);
+    if (t >= lo && t < hi) return false;
+  }
+  ptr = s.base[b] + (long long)blk * s.block_stride + (long long)t * (long long)N;
+  prime = t < s.ell ? s.p0 + t : s.L + (t - s.ell);
+  return true;
+}
+
+// ---- counter-based PRNG (spec: DESIGN.md section 3; mirrored by the oracle)
+__device__ __forceinline__ u64 mix64_d(u64 z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ u64 prng_d(u64 stream_key, u64 idx) {
+  return mix64_d(stream_key ^ (idx * 0xD1B54A32D192ED03ULL + 0x8CB92BA72F3D8DD7ULL));
+}
+__device__ __forceinline__ int cbd21_d(u64 r) {
+  return __popcll(r & 0x1FFFFFULL) - __popcll((r >> 21) & 0x1FFFFFULL);
+}
+
+__device__ __forceinline__ unsigned brev_bits(unsigned x, int bits) {
+  return __brev(x) >> (32 - bits);
+}
+
+// NTT-domain automorphism source index: out[i] = in[auto_src(i)]
+__device__ __forceinline__ unsigned auto_src(unsigned i, u64 g, int logN) {
+  const u64 M = 2ULL << logN;
+  const u64 e = 2ULL * brev_bits(i, logN) + 1ULL;
+  const u64 eg = (e * g) & (M - 1);
+  return brev_bits((unsigned)((eg - 1) >> 1), logN);
+}
+
+#endif  // __CUDACC__
+
+}  // namespace fheon

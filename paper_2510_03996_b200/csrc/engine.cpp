@@ -1,0 +1,491 @@
+// Context construction (device constant tables), allocator, keys, encoder,
+// trace.  See engine.hpp.
+#include "engine.hpp"
+
+#include <cmath>
+#include <cstring>
+
+namespace fheon {
+
+int category_of(ErrKind k) {
+  switch (k) {
+    case ErrKind::invalid_rotation:
+    case ErrKind::shape:
+    case ErrKind::capacity:
+    case ErrKind::model:
+      return 2;
+    case ErrKind::not_implemented:
+      return 1;
+    default:
+      return 3;
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Error(ErrKind::cuda, std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
+  }
+}
+
+void launch_check(const char* what) {
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(ErrKind::cuda, std::string("kernel launch failed: ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+// ------------------------------------------------------------- buffers
+DevBuffer::DevBuffer(Context* c, std::size_t w) : ctx(c), words(w) {
+  if (w == 0) return;
+  FHEON_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), c->stream()));
+}
+DevBuffer::~DevBuffer() {
+  if (ptr) cudaFreeAsync(ptr, ctx->stream());
+}
+
+BufPtr Context::alloc(std::size_t words) { return std::make_shared<DevBuffer>(this, words); }
+
+Ciphertext Context::new_ct(int limbs) {
+  Ciphertext c;
+  c.buf = alloc(2 * static_cast<std::size_t>(limbs) * N());
+  c.c0 = c.buf->ptr;
+  c.c1 = c.buf->ptr + static_cast<std::size_t>(limbs) * N();
+  c.limbs = limbs;
+  c.id = next_id();
+  return c;
+}
+
+// ------------------------------------------------------------- context
+namespace {
+
+u64 neg_inv64(u64 q) {
+  u64 inv = q;  // q * q = 1 mod 8 for odd q
+  for (int i = 0; i < 6; ++i) inv *= 2 - q * inv;
+  return ~inv + 1;  // -q^{-1}
+}
+
+template <class T>
+T* upload(std::vector<void*>& track, const std::vector<T>& v, cudaStream_t st) {
+  T* d = nullptr;
+  FHEON_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), std::max<std::size_t>(1, v.size()) * sizeof(T)));
+  track.push_back(d);
+  if (!v.empty()) FHEON_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return d;
+}
+
+u64 prod_mod(const std::vector<u64>& primes, int lo, int hi, int skip, u64 m) {
+  u64 r = 1 % m;
+  for (int i = lo; i < hi; ++i)
+    if (i != skip) r = mulmod(r, primes[i] % m, m);
+  return r;
+}
+
+}  // namespace
+
+Context::Context(const Params& p) : ht_(make_tables(p)) {
+  if (ht_.alpha > kMaxAlpha - 1) throw Error(ErrKind::shape, "alpha = ceil(L/dnum) must be < 16");
+  if (p.K > kMaxK - 1) throw Error(ErrKind::shape, "K must be < 16");
+  if (p.L > 64) throw Error(ErrKind::shape, "L must be <= 64");
+  depth_budget_ = p.depth_budget < 0 ? p.L - 1 : p.depth_budget;
+  if (depth_budget_ < 1 || depth_budget_ > p.L - 1)
+    throw Error(ErrKind::shape, "depth budget must lie in [1, L-1]");
+  int dev = 0;
+  FHEON_CUDA(cudaGetDevice(&dev));
+  FHEON_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  {
+    cudaMemPool_t pool;
+    FHEON_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    std::uint64_t thr = UINT64_MAX;
+    FHEON_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  for (int i = 0; i < kStaging; ++i) {
+    FHEON_CUDA(cudaMallocHost(reinterpret_cast<void**>(&staging_[i]), ht_.N * sizeof(long long)));
+    FHEON_CUDA(cudaEventCreateWithFlags(&staging_ev_[i], cudaEventDisableTiming));
+  }
+  build_device_tables();
+}
+
+Context::~Context() {
+  keys_.clear();
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (void* d : dev_allocs_) cudaFree(d);
+  for (int i = 0; i < kStaging; ++i) {
+    if (staging_[i]) cudaFreeHost(staging_[i]);
+    if (staging_ev_[i]) cudaEventDestroy(staging_ev_[i]);
+  }
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Context::build_device_tables() {
+  const Params& p = ht_.p;
+  const int L = p.L, K = p.K, NP = L + K, dnum = p.dnum, alpha = ht_.alpha;
+  const std::size_t N = ht_.N;
+  const std::vector<u64>& q = ht_.q;
+  DevTables& t = dt_;
+  t.logN = p.logN;
+  t.n1 = p.logN / 2;
+  t.n2 = p.logN - t.n1;
+  t.N = N;
+  t.L = L;
+  t.K = K;
+  t.dnum = dnum;
+  t.alpha = alpha;
+
+  std::vector<PrimeConst> pcs(NP);
+  for (int i = 0; i < NP; ++i) {
+    PrimeConst& c = pcs[i];
+    c.q = q[i];
+    c.qinv_neg = neg_inv64(q[i]);
+    const u64 rmod = (u64)(((u128)1 << 64) % q[i]);
+    c.rmod = rmod;
+    c.r2 = mulmod(rmod, rmod, q[i]);
+    c.mu64 = (u64)(((u128)1 << 64) / q[i]);
+    c.ninv = invmod(N % q[i], q[i]);
+    c.ninv_sh = shoup(c.ninv, q[i]);
+    c.pad = 0;
+  }
+  t.pc = upload(dev_allocs_, pcs, stream_);
+
+  // twiddles [NP][4][N]
+  std::vector<u64> tw((std::size_t)NP * 4 * N);
+#pragma omp parallel for
+  for (int i = 0; i < NP; ++i) {
+    const u64 qi = q[i];
+    const u64 psi = ht_.psi[i], ipsi = invmod(psi, qi);
+    std::vector<u64> pw(N), ipw(N);
+    pw[0] = ipw[0] = 1;
+    for (std::size_t e = 1; e < N; ++e) {
+      pw[e] = mulmod(pw[e - 1], psi, qi);
+      ipw[e] = mulmod(ipw[e - 1], ipsi, qi);
+    }
+    u64* base = tw.data() + (std::size_t)i * 4 * N;
+    for (std::size_t k = 0; k < N; ++k) {
+      const unsigned e = bitrev((unsigned)k, p.logN);
+      base[k] = pw[e];
+      base[N + k] = shoup(pw[e], qi);
+      base[2 * N + k] = ipw[e];
+      base[3 * N + k] = shoup(ipw[e], qi);
+    }
+  }
+  t.tw = upload(dev_allocs_, tw, stream_);
+
+  // ModUp tables
+  std::vector<u64> qhinv((std::size_t)L * dnum * kMaxAlpha * 2, 0);
+  std::vector<u64> qhat((std::size_t)L * dnum * NP * kMaxAlpha, 0);
+  for (int limbs = 1; limbs <= L; ++limbs) {
+    for (int j = 0; j < dnum; ++j) {
+      const int lo = j * alpha, hi = std::min(lo + alpha, limbs);
+      if (lo >= hi) continue;
+      const int tab = (limbs - 1) * dnum + j;
+      for (int i = lo; i < hi; ++i) {
+        const u64 h = prod_mod(q, lo, hi, i, q[i]);
+        const u64 hi_inv = invmod(h, q[i]);
+        qhinv[((std::size_t)tab * kMaxAlpha + (i - lo)) * 2] = hi_inv;
+        qhinv[((std::size_t)tab * kMaxAlpha + (i - lo)) * 2 + 1] = shoup(hi_inv, q[i]);
+        for (int pt = 0; pt < NP; ++pt) {
+          const u64 m = q[pt];
+          qhat[((std::size_t)tab * NP + pt) * kMaxAlpha + (i - lo)] = to_mont(prod_mod(q, lo, hi, i, m), m);
+        }
+      }
+    }
+  }
+  t.modup_qhinv = upload(dev_allocs_, qhinv, stream_);
+  t.modup_qhat = upload(dev_allocs_, qhat, stream_);
+
+  // ModDown tables
+  std::vector<u64> pk((std::size_t)K * 4, 0);
+  std::vector<double> pinv(K);
+  std::vector<u64> phat((std::size_t)L * kMaxK, 0);
+  std::vector<u64> mq((std::size_t)L * 4, 0);
+  auto half_P = [&](u64 m) {
+    const u64 Pm = prod_mod(q, L, L + K, -1, m);
+    return mulmod(submod(Pm, 1 % m, m), (m + 1) / 2, m);
+  };
+  for (int k = 0; k < K; ++k) {
+    const u64 pkv = q[L + k];
+    const u64 h = prod_mod(q, L, L + K, L + k, pkv);
+    const u64 hinv = invmod(h, pkv);
+    pk[k * 4] = hinv;
+    pk[k * 4 + 1] = shoup(hinv, pkv);
+    pk[k * 4 + 2] = half_P(pkv);
+    pinv[k] = 1.0 / (double)pkv;
+  }
+  for (int i = 0; i < L; ++i) {
+    for (int k = 0; k < K; ++k) phat[(std::size_t)i * kMaxK + k] = to_mont(prod_mod(q, L, L + K, L + k, q[i]), q[i]);
+    const u64 Pm = prod_mod(q, L, L + K, -1, q[i]);
+    const u64 Pinv = invmod(Pm, q[i]);
+    mq[i * 4] = to_mont(Pm, q[i]);
+    mq[i * 4 + 1] = half_P(q[i]);
+    mq[i * 4 + 2] = Pinv;
+    mq[i * 4 + 3] = shoup(Pinv, q[i]);
+  }
+  t.md_pk = upload(dev_allocs_, pk, stream_);
+  t.md_pinv = upload(dev_allocs_, pinv, stream_);
+  t.md_phat = upload(dev_allocs_, phat, stream_);
+  t.md_q = upload(dev_allocs_, mq, stream_);
+
+  // Rescale tables
+  std::vector<u64> rs((std::size_t)L * L * 4, 0);
+  for (int l = 1; l < L; ++l)
+    for (int i = 0; i < l; ++i) {
+      const u64 qlm = q[l] % q[i];
+      const u64 inv = invmod(qlm, q[i]);
+      u64* c = rs.data() + ((std::size_t)l * L + i) * 4;
+      c[0] = inv;
+      c[1] = shoup(inv, q[i]);
+      c[2] = qlm;
+    }
+  t.rs = upload(dev_allocs_, rs, stream_);
+
+  // secret key: ternary from the counter PRNG, NTT domain over all L+K primes
+  {
+    std::vector<long long> s(N);
+    const u64 key = prng_stream_key(p.seed, kStreamSecret);
+    for (std::size_t k = 0; k < N; ++k) {
+      const u64 r = mix64(key ^ (k * 0xD1B54A32D192ED03ULL + 0x8CB92BA72F3D8DD7ULL));
+      s[k] = (long long)(r % 3) - 1;
+    }
+    long long* dcoef = upload(dev_allocs_, s, stream_);
+    u64* sntt = nullptr;
+    FHEON_CUDA(cudaMalloc(reinterpret_cast<void**>(&sntt), (std::size_t)NP * N * sizeof(u64)));
+    dev_allocs_.push_back(sntt);
+    coeffs_to_rns(dt_, sntt, dcoef, NP, stream_);
+    LimbSet ls{};
+    ls.base[0] = sntt;
+    ls.nbase = 1;
+    ls.blocks_per_base = 1;
+    ls.block_stride = 0;
+    ls.E = NP;
+    ls.ell = NP;
+    ls.L = L;
+    ntt_forward(dt_, ls, stream_);
+    t.s_ntt = sntt;
+  }
+  FHEON_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// ------------------------------------------------------------- keys
+u64 Context::galois(long t) const {
+  const long S = ht_.S;
+  long r = t % S;
+  if (r < 0) r += S;
+  return powmod(5, (u64)r, 2 * (u64)ht_.N);
+}
+
+std::size_t Context::key_words() const {
+  return (std::size_t)ht_.p.dnum * 2 * (ht_.p.L + ht_.p.K) * ht_.N;
+}
+
+const u64* Context::key(u64 key_id) {
+  auto it = keys_.find(key_id);
+  if (it != keys_.end()) return it->second->ptr;
+  if (strict_keys) throw Error(ErrKind::internal, "evaluation key " + std::to_string(key_id) + " not resident");
+  gen_key(key_id);
+  return keys_.at(key_id)->ptr;
+}
+
+void Context::gen_key(u64 key_id) {
+  if (keys_.count(key_id)) return;
+  const Params& p = ht_.p;
+  const int L = p.L, K = p.K, NP = L + K;
+  const std::size_t N = ht_.N, LN = (std::size_t)NP * N;
+  BufPtr kb = alloc(key_words());
+  BufPtr sp = alloc(LN);
+  if (key_id == 0) {
+    secret_square(dt_, sp->ptr, stream_);
+  } else {
+    if ((key_id & 1) == 0) throw Error(ErrKind::internal, "Galois element must be odd");
+    PolyList o{}, in{};
+    o.p[0] = sp->ptr;
+    o.g[0] = key_id;
+    o.n = 1;
+    in.p[0] = dt_.s_ntt;
+    in.n = 1;
+    automorph(dt_, o, in, NP, stream_);
+  }
+  std::vector<u64> pmod(NP, 0);
+  for (int i = 0; i < NP; ++i) pmod[i] = prod_mod(ht_.q, L, L + K, -1, ht_.q[i]);
+  BufPtr dpm = alloc(NP);
+  FHEON_CUDA(cudaMemcpyAsync(dpm->ptr, pmod.data(), NP * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+  BufPtr e = alloc(LN);
+  LimbSet ls{};
+  ls.base[0] = e->ptr;
+  ls.nbase = 1;
+  ls.blocks_per_base = 1;
+  ls.E = NP;
+  ls.ell = NP;
+  ls.L = L;
+  for (int j = 0; j < p.dnum; ++j) {
+    const int lo = j * ht_.alpha, hi = std::min(lo + ht_.alpha, L);
+    sample_error(dt_, e->ptr, prng_stream_key(p.seed, stream_key(key_id, j, 3)), NP, NP, stream_);
+    ntt_forward(dt_, ls, stream_);
+    u64* b = kb->ptr + (std::size_t)(j * 2) * LN;
+    u64* a = b + LN;
+    keygen_digit(dt_, b, a, e->ptr, sp->ptr, prng_stream_key(p.seed, stream_key(key_id, j, 2)), lo, hi, dpm->ptr,
+                 stream_);
+  }
+  FHEON_CUDA(cudaStreamSynchronize(stream_));  // pmod host vector goes out of scope
+  keys_[key_id] = kb;
+}
+
+// ------------------------------------------------------------- encoder
+void Context::encode_coeffs(const double* vals, std::size_t n, double scale, long long* coeffs) const {
+  const int S = ht_.S;
+  if (n > (std::size_t)S) throw Error(ErrKind::capacity, "payload exceeds the slot count");
+  const u64 M = 2 * (u64)ht_.N;
+  std::vector<double> re(S, 0.0), im(S, 0.0);
+  for (std::size_t i = 0; i < n; ++i) re[i] = vals[i];
+  for (int len = S; len >= 1; len >>= 1) {
+    const int lenh = len >> 1;
+    const u64 lenq = (u64)len << 2;
+    for (int i = 0; i < S; i += len) {
+      for (int j = 0; j < lenh; ++j) {
+        const u64 idx = (lenq - (ht_.rotgroup[j] % lenq)) * (M / lenq);
+        const double ur = re[i + j] + re[i + j + lenh];
+        const double ui = im[i + j] + im[i + j + lenh];
+        const double vr0 = re[i + j] - re[i + j + lenh];
+        const double vi0 = im[i + j] - im[i + j + lenh];
+        const double wr = ht_.ksi_re[idx], wi = ht_.ksi_im[idx];
+        re[i + j] = ur;
+        im[i + j] = ui;
+        re[i + j + lenh] = vr0 * wr - vi0 * wi;
+        im[i + j + lenh] = vr0 * wi + vi0 * wr;
+      }
+    }
+  }
+  // bit reversal
+  for (int i = 1, j = 0; i < S; ++i) {
+    int bit = S >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) {
+      std::swap(re[i], re[j]);
+      std::swap(im[i], im[j]);
+    }
+  }
+  const double lim = 4611686018427387904.0;  // 2^62
+  for (int i = 0; i < S; ++i) {
+    const double a = (re[i] / (double)S) * scale, b = (im[i] / (double)S) * scale;
+    if (!(std::fabs(a) < lim) || !(std::fabs(b) < lim))
+      throw Error(ErrKind::capacity, "encoded value exceeds the 2^62 coefficient range");
+    coeffs[i] = std::llround(a);
+    coeffs[i + S] = std::llround(b);
+  }
+}
+
+void Context::decode_coeffs(const double* coeffs, double scale, double* out) const {
+  const int S = ht_.S;
+  const u64 M = 2 * (u64)ht_.N;
+  std::vector<double> re(S), im(S);
+  for (int i = 0; i < S; ++i) {
+    re[i] = coeffs[i] / scale;
+    im[i] = coeffs[i + S] / scale;
+  }
+  for (int i = 1, j = 0; i < S; ++i) {
+    int bit = S >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) {
+      std::swap(re[i], re[j]);
+      std::swap(im[i], im[j]);
+    }
+  }
+  for (int len = 2; len <= S; len <<= 1) {
+    const int lenh = len >> 1;
+    const u64 lenq = (u64)len << 2;
+    for (int i = 0; i < S; i += len) {
+      for (int j = 0; j < lenh; ++j) {
+        const u64 idx = (ht_.rotgroup[j] % lenq) * (M / lenq);
+        const double wr = ht_.ksi_re[idx], wi = ht_.ksi_im[idx];
+        const double ur = re[i + j], ui = im[i + j];
+        const double xr = re[i + j + lenh], xi = im[i + j + lenh];
+        const double vr = xr * wr - xi * wi;
+        const double vi = xr * wi + xi * wr;
+        re[i + j] = ur + vr;
+        im[i + j] = ui + vi;
+        re[i + j + lenh] = ur - vr;
+        im[i + j + lenh] = ui - vi;
+      }
+    }
+  }
+  for (int i = 0; i < S; ++i) out[i] = re[i];
+}
+
+long long* Context::staging_slot(cudaEvent_t** ev) {
+  const int i = staging_next_;
+  staging_next_ = (staging_next_ + 1) % kStaging;
+  FHEON_CUDA(cudaEventSynchronize(staging_ev_[i]));
+  *ev = &staging_ev_[i];
+  return staging_[i];
+}
+
+namespace {
+bool constant_value(const double* vals, std::size_t n, int S, double* c) {
+  if (n == 0) {
+    *c = 0.0;
+    return true;
+  }
+  for (std::size_t i = 1; i < n; ++i)
+    if (vals[i] != vals[0]) return false;
+  if (n < (std::size_t)S && vals[0] != 0.0) return false;
+  *c = vals[0];
+  return true;
+}
+}  // namespace
+
+BufPtr Context::encode(const double* vals, std::size_t n, int limbs, double scale) {
+  const std::size_t N = ht_.N;
+  BufPtr out = alloc((std::size_t)limbs * N);
+  ++stats.encodes;
+  double cv;
+  if (constant_value(vals, n, ht_.S, &cv)) {
+    const double x = cv * scale;
+    if (!(std::fabs(x) < 4611686018427387904.0)) throw Error(ErrKind::capacity, "constant exceeds 2^62");
+    const long long k = std::llround(x);
+    FHEON_CUDA(cudaMemsetAsync(out->ptr, 0, (std::size_t)limbs * N * sizeof(u64), stream_));
+    LimbConsts lc{};
+    for (int i = 0; i < limbs; ++i) {
+      const u64 q = ht_.q[i];
+      lc.c[i] = k >= 0 ? (u64)k % q : (q - 1 - (u64)(-(k + 1)) % q);
+    }
+    PolyList o{};
+    o.p[0] = out->ptr;
+    o.n = 1;
+    ew_add_const(dt_, o, o, lc, limbs, stream_);
+    return out;
+  }
+  cudaEvent_t* ev = nullptr;
+  long long* h = staging_slot(&ev);
+  encode_coeffs(vals, n, scale, h);
+  BufPtr dcoef = alloc(N);
+  FHEON_CUDA(cudaMemcpyAsync(dcoef->ptr, h, N * sizeof(long long), cudaMemcpyHostToDevice, stream_));
+  FHEON_CUDA(cudaEventRecord(*ev, stream_));
+  coeffs_to_rns(dt_, out->ptr, reinterpret_cast<const long long*>(dcoef->ptr), limbs, stream_);
+  LimbSet ls{};
+  ls.base[0] = out->ptr;
+  ls.nbase = 1;
+  ls.blocks_per_base = 1;
+  ls.E = limbs;
+  ls.ell = limbs;
+  ls.L = ht_.p.L;
+  ntt_forward(dt_, ls, stream_);
+  return out;
+}
+
+// ------------------------------------------------------------- trace
+void Context::record(int kind, long value, const std::string& label) {
+  if (!tracing_) return;
+  std::lock_guard<std::mutex> g(trace_mu_);
+  trace_.push_back({kind, value, label});
+}
+std::vector<TraceEvent> Context::trace_snapshot() const {
+  std::lock_guard<std::mutex> g(trace_mu_);
+  return trace_;
+}
+void Context::clear_trace() {
+  std::lock_guard<std::mutex> g(trace_mu_);
+  trace_.clear();
+}
+
+}  // namespace fheon

@@ -1,0 +1,186 @@
+// B200 RNS-CKKS engine: context (device tables, keys, stream, allocator),
+// device ciphertext handles and the evaluator ops that replace the
+// reference's slot-vector backend (proj/include/slotcnn/backend.hpp:134-153):
+//
+//   reference op (backend.cpp)      engine realisation
+//   rotate      :165-182            Galois automorphism + hybrid key switch
+//   add / sub   :184-198            level/scale alignment + limb-wise mod add
+//   mult_plain  :200-217            encode at the operand's scale, Hadamard, rescale
+//   mult_cipher :219-231            tensor, relinearise (key switch), rescale
+//   bootstrap   :233-249            not yet available (throws)
+//   SlotVector::encode :148-161     encode + encrypt at the depth budget
+//
+// Level semantics follow the reference exactly: level = limbs - 1, add/sub
+// give min(level), mult_plain level-1, mult_cipher min-1, multiplication at
+// level 0 throws DepthExhaustedError (backend.cpp:27-32).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "params.hpp"
+
+namespace fheon {
+
+// ---- errors (mirrors proj/include/slotcnn/errors.hpp:18-80)
+enum class ErrKind : int {
+  generic = 0,
+  invalid_rotation = 1,  // data
+  depth_exhausted = 2,   // internal
+  shape = 3,             // data
+  capacity = 4,          // data
+  model = 5,             // data
+  internal = 6,          // internal
+  cuda = 7,              // internal
+  not_implemented = 8,   // usage
+};
+int category_of(ErrKind k);  // usage 1, data 2, internal 3
+
+struct Error : std::runtime_error {
+  ErrKind kind;
+  Error(ErrKind k, const std::string& m) : std::runtime_error(m), kind(k) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define FHEON_CUDA(x) ::fheon::cuda_check((x), #x)
+
+class Context;
+
+struct DevBuffer {
+  Context* ctx = nullptr;
+  u64* ptr = nullptr;
+  std::size_t words = 0;
+  DevBuffer(Context* c, std::size_t w);
+  ~DevBuffer();
+  DevBuffer(const DevBuffer&) = delete;
+  DevBuffer& operator=(const DevBuffer&) = delete;
+};
+using BufPtr = std::shared_ptr<DevBuffer>;
+
+// Immutable ciphertext handle: (c0, c1) in the NTT domain, `limbs` active
+// limbs (q_0..q_{limbs-1}); copies share the device buffer.  Dropping limbs
+// is a zero-copy view (the tail limbs stay allocated).
+struct Ciphertext {
+  BufPtr buf;
+  u64* c0 = nullptr;
+  u64* c1 = nullptr;
+  int limbs = 0;
+  double scale = 0.0;
+  std::uint64_t id = 0;
+  bool valid() const { return static_cast<bool>(buf); }
+  int level() const { return limbs - 1; }
+};
+
+struct TraceEvent {
+  int kind;    // 0 rotation, 1 mult_plain, 2 mult_cipher, 3 bootstrap, 4 marker
+  long value;  // rotation index or level_after
+  std::string label;
+};
+
+struct OpStats {
+  std::uint64_t rotations = 0, keyswitches = 0, mult_plain = 0, mult_cipher = 0, rescales = 0, ntt_limbs = 0,
+                encodes = 0, adds = 0;
+};
+
+class Context {
+ public:
+  explicit Context(const Params& p);
+  ~Context();
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  const HostTables& host() const { return ht_; }
+  const DevTables& dev() const { return dt_; }
+  cudaStream_t stream() const { return stream_; }
+  std::size_t N() const { return ht_.N; }
+  int S() const { return ht_.S; }
+  int L() const { return ht_.p.L; }
+  int K() const { return ht_.p.K; }
+  int depth_budget() const { return depth_budget_; }
+
+  BufPtr alloc(std::size_t words);
+  Ciphertext new_ct(int limbs);
+  std::uint64_t next_id() { return ++id_counter_; }
+
+  // ---- keys: [dnum][2][L+K][N] Montgomery form on the device
+  u64 galois(long t) const;
+  const u64* key(u64 key_id);  // generates on demand unless strict_keys
+  void gen_key(u64 key_id);
+  bool has_key(u64 key_id) const { return keys_.count(key_id) != 0; }
+  void drop_keys() { keys_.clear(); }
+  std::size_t key_words() const;
+  std::size_t num_keys() const { return keys_.size(); }
+  bool strict_keys = false;
+
+  // ---- encoder (host special FFT)
+  void encode_coeffs(const double* vals, std::size_t n, double scale, long long* coeffs) const;
+  void decode_coeffs(const double* coeffs, double scale, double* out) const;
+  // encode `vals` at `scale` over `limbs` limbs into a device [limbs][N] NTT-domain buffer
+  BufPtr encode(const double* vals, std::size_t n, int limbs, double scale);
+
+  // ---- trace (mirrors slotcnn TraceRecorder, trace.hpp:22-103)
+  void set_tracing(bool on) { tracing_ = on; }
+  bool tracing() const { return tracing_; }
+  void record(int kind, long value, const std::string& label = {});
+  std::vector<TraceEvent> trace_snapshot() const;
+  void clear_trace();
+
+  OpStats stats;
+  std::uint64_t enc_counter = 0;
+
+  // staging for host -> device copies of encoded coefficients
+  long long* staging_slot(cudaEvent_t** ev);
+
+ private:
+  void build_device_tables();
+
+  HostTables ht_;
+  DevTables dt_{};
+  cudaStream_t stream_ = nullptr;
+  int depth_budget_ = 0;
+  std::uint64_t id_counter_ = 0;
+  std::vector<void*> dev_allocs_;  // table allocations
+  std::map<u64, BufPtr> keys_;
+  mutable std::mutex trace_mu_;
+  bool tracing_ = false;
+  std::vector<TraceEvent> trace_;
+  static constexpr int kStaging = 16;
+  long long* staging_[kStaging] = {};
+  cudaEvent_t staging_ev_[kStaging] = {};
+  int staging_next_ = 0;
+};
+
+// ---------------------------------------------------------------- ops
+Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n);            // at the depth budget
+Ciphertext encrypt_top(Context& ctx, const double* vals, std::size_t n);        // at L-1 (all limbs)
+void decrypt(Context& ctx, const Ciphertext& ct, double* out);                  // S slots
+Ciphertext rotate(Context& ctx, const Ciphertext& x, long t);
+std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& ts);
+std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t);
+Ciphertext add(Context& ctx, const Ciphertext& a, const Ciphertext& b);
+Ciphertext sub(Context& ctx, const Ciphertext& a, const Ciphertext& b);
+Ciphertext add_plain(Context& ctx, const Ciphertext& a, const double* vals, std::size_t n);
+Ciphertext add_const(Context& ctx, const Ciphertext& a, double c);
+Ciphertext mult_plain(Context& ctx, const Ciphertext& a, const double* vals, std::size_t n);
+Ciphertext mult_const(Context& ctx, const Ciphertext& a, double c);
+Ciphertext mult_cipher(Context& ctx, const Ciphertext& a, const Ciphertext& b);
+Ciphertext level_down(Context& ctx, const Ciphertext& a, int target_limbs);
+Ciphertext rescale(Context& ctx, const Ciphertext& a);
+Ciphertext bootstrap(Context& ctx, const Ciphertext& a);
+// raw key switch of one polynomial d ([limbs][N], NTT) for parity tests:
+// returns (ks0, ks1) as a 2-poly ciphertext without scale meaning
+Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d_as_c1, u64 key_id, u64 g);
+
+// device <-> host for parity tests
+Ciphertext upload_ct(Context& ctx, const u64* host, int limbs, double scale);
+void download_ct(Context& ctx, const Ciphertext& ct, u64* host);
+
+}  // namespace fheon

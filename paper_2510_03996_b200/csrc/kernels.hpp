@@ -1,0 +1,120 @@
+// Host-callable launchers for the sm_100a kernels.  Plain pointers, explicit
+// stream; no torch types.  Every launcher enqueues asynchronously.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace fheon {
+
+// Throws fheon::Error on a launch-configuration error (no device sync).
+void launch_check(const char* what);
+
+// Device-resident constant tables of one context (built in engine.cpp).
+struct DevTables {
+  int logN = 0, n1 = 0, n2 = 0;
+  std::size_t N = 0;
+  int L = 0, K = 0, dnum = 0, alpha = 0;
+  PrimeConst* pc = nullptr;   // [L+K]
+  u64* tw = nullptr;          // [L+K][4][N]: tw, tw', itw, itw'
+  // ModUp, indexed by tab = (limbs-1)*dnum + digit
+  u64* modup_qhinv = nullptr;     // [L*dnum][kMaxAlpha][2] (value, shoup) mod q_i
+  u64* modup_qhat = nullptr;      // [L*dnum][L+K][kMaxAlpha] Montgomery form mod target
+  // ModDown
+  u64* md_pk = nullptr;           // [K][4]: (P/p_k)^{-1} mod p_k (value, shoup), (P-1)/2 mod p_k, 0
+  double* md_pinv = nullptr;      // [K] fl(1/p_k)
+  u64* md_phat = nullptr;         // [L][kMaxK] (P/p_k) mod q_i, Montgomery form
+  u64* md_q = nullptr;            // [L][4]: P mod q_i (Montgomery), (P-1)/2 mod q_i, P^{-1} mod q_i, shoup
+  // Rescale: [l][i][4]: q_l^{-1} mod q_i, shoup, q_l mod q_i, 0
+  u64* rs = nullptr;
+  // secret key, NTT domain standard form [L+K][N]
+  u64* s_ntt = nullptr;
+};
+
+constexpr int kMaxAlpha = 16;
+constexpr int kMaxK = 16;
+constexpr int kMaxPolys = 64;
+
+// A list of polynomials (each [limbs][N], limb i uses prime p0 + i), optional
+// per-poly Galois element used by kernels that read a permuted operand.
+struct PolyList {
+  u64* p[kMaxPolys];
+  u64 g[kMaxPolys];
+  int n;
+};
+
+// ---- NTT (batched over every limb-polynomial of the set)
+void ntt_forward(const DevTables& t, const LimbSet& set, cudaStream_t st);
+void ntt_inverse(const DevTables& t, const LimbSet& set, cudaStream_t st);
+
+// ---- elementwise over the polys of a list, `limbs` limbs each, primes 0..limbs-1
+void ew_add(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& b, int limbs, cudaStream_t st);
+void ew_sub(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& b, int limbs, cudaStream_t st);
+void ew_neg(const DevTables& t, const PolyList& out, const PolyList& a, int limbs, cudaStream_t st);
+// out = a (*) pt (pt standard form, [limbs][N]); out may alias a
+void ew_mul_pt(const DevTables& t, const PolyList& out, const PolyList& a, const u64* pt, int limbs, cudaStream_t st);
+// per-limb constants (standard form value + shoup), out = a * c
+struct LimbConsts {
+  u64 c[64];
+  u64 sh[64];
+};
+void ew_mul_const(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& c, int limbs,
+                  cudaStream_t st);
+void ew_add_const(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& c, int limbs,
+                  cudaStream_t st);
+// (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1)
+void ew_tensor(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
+               const u64* b1, int limbs, cudaStream_t st);
+// out[p] = sigma_{g[p]}(in[p]) in the NTT domain
+void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int limbs, cudaStream_t st);
+
+// ---- key switching
+// ModUp basis conversion. x[b]: coefficient-domain input [limbs][N];
+// ext[b]: [beta][limbs+K][N], written for every limb outside the digit's own range.
+void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st);
+// Inner product with automorphism. For each job r: acc[r] ([2][limbs+K][N]) =
+//   sum_j sigma_g(D_j) (x) key_j   where D_j = d (own limbs, NTT c1) | ext (other limbs)
+struct KsJobs {
+  const u64* key[kMaxBases];  // [dnum][2][L+K][N] Montgomery
+  const u64* ext[kMaxBases];  // [beta][limbs+K][N]
+  const u64* d[kMaxBases];    // [limbs][N]
+  u64* acc[kMaxBases];
+  u64 g[kMaxBases];
+  int n;
+};
+void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st);
+// ModDown front half: z[p] = coefficient-domain P limbs ([K][N], prime L+k);
+// conv[p] ([limbs][N]) = centred P-residue lifted to q_0..q_{limbs-1}
+void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);
+// out[p] = (acc[p] - conv[p]) * P^{-1} + sigma_{add.g[p]}(add[p])   (add[p] may be null)
+void moddown_finish(const DevTables& t, const PolyList& out, const PolyList& acc, const PolyList& conv,
+                    const PolyList& add, int limbs, cudaStream_t st);
+// Rescale: last[p] coefficient-domain limb (limbs-1); r[p] ([limbs-1][N]) centred lift
+void rescale_lift(const DevTables& t, const PolyList& r, const PolyList& last, int limbs, cudaStream_t st);
+// out[p] = (a[p] - r[p]) * q_{limbs-1}^{-1}, limbs-1 limbs
+void rescale_finish(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& r, int limbs,
+                    cudaStream_t st);
+
+// ---- encode / encrypt / keygen / decrypt
+// signed coefficients -> RNS coefficient domain [limbs][N]
+void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st);
+// CBD21 error polynomial for `stream_key` into limbs 0..nlimbs-1 (prime rule: i < ell ? i : L + i - ell)
+void sample_error(const DevTables& t, u64* out, u64 stream_key, int nlimbs, int ell, cudaStream_t st);
+// c1 = uniform(stream); c0 = m + e - c1 s (m, e NTT domain) over q_0..q_{limbs-1}
+void encrypt_combine(const DevTables& t, u64* c0, u64* c1, const u64* m, const u64* e, u64 stream_a, int limbs,
+                     cudaStream_t st);
+// one key digit over all L+K limbs: a uniform, b = e - a s + [i in digit] (P mod q_i) sp; stored Montgomery
+void keygen_digit(const DevTables& t, u64* b, u64* a, const u64* e, const u64* sp, u64 stream_a, int lo, int hi,
+                  const u64* pmod, cudaStream_t st);
+// out = s^2 over all L+K limbs
+void secret_square(const DevTables& t, u64* out, cudaStream_t st);
+// m_i = c0_i + c1_i s_i, i < limbs
+void decrypt_core(const DevTables& t, u64* m, const u64* c0, const u64* c1, int limbs, cudaStream_t st);
+// Montgomery <-> standard for nlimbs limbs with the ell prime rule
+void convert_mont(const DevTables& t, u64* out, const u64* in, int nlimbs, int ell, bool to_mont, cudaStream_t st);
+
+}  // namespace fheon

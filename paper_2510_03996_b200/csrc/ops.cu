@@ -1,0 +1,377 @@
+// Elementwise RNS kernels, automorphism, hybrid key-switching pieces
+// (ModUp basis conversion, key inner product, ModDown), rescale, and the
+// encrypt / keygen / decrypt helpers.  Definitions: DESIGN.md section 3
+// (mirrored by oracle/ckks_oracle.c, which these must match bit for bit).
+#include <stdexcept>
+
+#include "kernels.hpp"
+
+namespace fheon {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline dim3 grid_for(std::size_t N, int y, int z = 1) {
+  return dim3((unsigned)(N / kThreads), (unsigned)y, (unsigned)z);
+}
+
+// ------------------------------------------------------------ elementwise
+__global__ void k_add(PolyList out, PolyList a, PolyList b, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 q = pc[blockIdx.y].q;
+  out.p[blockIdx.z][o] = add_mod(a.p[blockIdx.z][o], b.p[blockIdx.z][o], q);
+}
+__global__ void k_sub(PolyList out, PolyList a, PolyList b, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 q = pc[blockIdx.y].q;
+  out.p[blockIdx.z][o] = sub_mod(a.p[blockIdx.z][o], b.p[blockIdx.z][o], q);
+}
+__global__ void k_neg(PolyList out, PolyList a, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 q = pc[blockIdx.y].q;
+  const u64 v = a.p[blockIdx.z][o];
+  out.p[blockIdx.z][o] = v ? q - v : 0;
+}
+__global__ void k_mul_pt(PolyList out, PolyList a, const u64* __restrict__ pt, const PrimeConst* __restrict__ pc,
+                         int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst P = pc[blockIdx.y];
+  out.p[blockIdx.z][o] = mul_mod(a.p[blockIdx.z][o], pt[o], P);
+}
+__global__ void k_mul_const(PolyList out, PolyList a, LimbConsts c, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 q = pc[blockIdx.y].q;
+  out.p[blockIdx.z][o] = shoup_mul(a.p[blockIdx.z][o], c.c[blockIdx.y], c.sh[blockIdx.y], q);
+}
+__global__ void k_add_const(PolyList out, PolyList a, LimbConsts c, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 q = pc[blockIdx.y].q;
+  out.p[blockIdx.z][o] = add_mod(a.p[blockIdx.z][o], c.c[blockIdx.y], q);
+}
+__global__ void k_tensor(u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0, const u64* b1,
+                         const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst P = pc[blockIdx.y];
+  const u64 x0 = a0[o], x1 = a1[o], y0 = b0[o], y1 = b1[o];
+  d0[o] = mul_mod(x0, y0, P);
+  d1[o] = add_mod(mul_mod(x0, y1, P), mul_mod(x1, y0, P), P.q);
+  d2[o] = mul_mod(x1, y1, P);
+}
+__global__ void k_automorph(PolyList out, PolyList in, int logN) {
+  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
+  const std::size_t base = (std::size_t)blockIdx.y << logN;
+  const u64 g = out.g[blockIdx.z];
+  out.p[blockIdx.z][base + n] = in.p[blockIdx.z][base + auto_src(n, g, logN)];
+}
+
+// ------------------------------------------------------------ key switching
+// grid (N/256, beta, npolys)
+__global__ void k_modup_bconv(PolyList ext, PolyList x, const PrimeConst* __restrict__ pc,
+                              const u64* __restrict__ qhinv, const u64* __restrict__ qhat, int logN, int limbs,
+                              int L, int K, int dnum, int alpha) {
+  const std::size_t N = (std::size_t)1 << logN;
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int lo = j * alpha;
+  const int hi = min(lo + alpha, limbs);
+  const int a = hi - lo;
+  const int E = limbs + K;
+  const int tab = (limbs - 1) * dnum + j;
+  const u64* xin = x.p[blockIdx.z];
+  u64* out = ext.p[blockIdx.z] + (std::size_t)j * E * N;
+  u64 y[kMaxAlpha];
+#pragma unroll
+  for (int i = 0; i < kMaxAlpha; ++i) {
+    if (i < a) {
+      const u64* h = qhinv + ((std::size_t)tab * kMaxAlpha + i) * 2;
+      y[i] = shoup_mul(xin[(std::size_t)(lo + i) * N + n], h[0], h[1], pc[lo + i].q);
+    }
+  }
+  for (int t = 0; t < E; ++t) {
+    if (t >= lo && t < hi) continue;
+    const int pt = t < limbs ? t : L + (t - limbs);
+    const u64* c = qhat + ((std::size_t)tab * (L + K) + pt) * kMaxAlpha;
+    Acc128 acc;
+#pragma unroll
+    for (int i = 0; i < kMaxAlpha; ++i)
+      if (i < a) acc.mac(y[i], __ldg(c + i));
+    out[(std::size_t)t * N + n] = redc(acc.hi, acc.lo, pc[pt].q, pc[pt].qinv_neg);
+  }
+}
+
+// grid (N/256, E, jobs)
+__global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int logN, int limbs, int L, int K,
+                           int alpha) {
+  const std::size_t N = (std::size_t)1 << logN;
+  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  const int r = blockIdx.z;
+  const int E = limbs + K;
+  const int pt = t < limbs ? t : L + (t - limbs);
+  const PrimeConst P = pc[pt];
+  const u64 g = jobs.g[r];
+  const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
+  const int beta = (limbs + alpha - 1) / alpha;
+  const u64* key = jobs.key[r];
+  const u64* ext = jobs.ext[r];
+  const u64* d = jobs.d[r];
+  Acc128 a0, a1;
+  for (int j = 0; j < beta; ++j) {
+    const int lo = j * alpha;
+    const int hi = min(lo + alpha, limbs);
+    const u64 v = (t >= lo && t < hi) ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+    const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
+    a0.mac(v, kj[n]);
+    a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
+  }
+  u64* acc = jobs.acc[r];
+  acc[(std::size_t)t * N + n] = redc(a0.hi, a0.lo, P.q, P.qinv_neg);
+  acc[((std::size_t)E + t) * N + n] = redc(a1.hi, a1.lo, P.q, P.qinv_neg);
+}
+
+// grid (N/256, npolys)
+__global__ void k_moddown_conv(PolyList conv, PolyList z, const PrimeConst* __restrict__ pc,
+                               const u64* __restrict__ md_pk, const double* __restrict__ md_pinv,
+                               const u64* __restrict__ md_phat, const u64* __restrict__ md_q, int logN, int limbs,
+                               int L, int K) {
+  const std::size_t N = (std::size_t)1 << logN;
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const u64* zp = z.p[blockIdx.z];
+  u64 y[kMaxK];
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < kMaxK; ++k) {
+    if (k < K) {
+      const u64 pk = pc[L + k].q;
+      const u64* c = md_pk + (std::size_t)k * 4;
+      y[k] = shoup_mul(add_mod(zp[(std::size_t)k * N + n], c[2], pk), c[0], c[1], pk);
+      v = __dadd_rn(v, __dmul_rn(__ull2double_rn(y[k]), md_pinv[k]));
+    }
+  }
+  const u64 u = (u64)v;
+  u64* out = conv.p[blockIdx.z];
+  for (int i = 0; i < limbs; ++i) {
+    const PrimeConst P = pc[i];
+    const u64* ph = md_phat + (std::size_t)i * kMaxK;
+    Acc128 acc;
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k)
+      if (k < K) acc.mac(y[k], __ldg(ph + k));
+    u64 x = redc(acc.hi, acc.lo, P.q, P.qinv_neg);
+    const u64* mq = md_q + (std::size_t)i * 4;
+    x = sub_mod(x, redc(mulhi(u, mq[0]), u * mq[0], P.q, P.qinv_neg), P.q);
+    out[(std::size_t)i * N + n] = sub_mod(x, mq[1], P.q);
+  }
+}
+
+// grid (N/256, limbs, npolys)
+__global__ void k_moddown_finish(PolyList out, PolyList acc, PolyList conv, PolyList add,
+                                 const PrimeConst* __restrict__ pc, const u64* __restrict__ md_q, int logN) {
+  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int p = blockIdx.z;
+  const std::size_t o = ((std::size_t)i << logN) + n;
+  const u64 q = pc[i].q;
+  const u64* mq = md_q + (std::size_t)i * 4;
+  u64 v = shoup_mul(sub_mod(acc.p[p][o], conv.p[p][o], q), mq[2], mq[3], q);
+  if (add.p[p]) {
+    const u64 g = add.g[p];
+    const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
+    v = add_mod(v, add.p[p][((std::size_t)i << logN) + src], q);
+  }
+  out.p[p][o] = v;
+}
+
+// grid (N/256, npolys)
+__global__ void k_rescale_lift(PolyList r, PolyList last, const PrimeConst* __restrict__ pc,
+                               const u64* __restrict__ rs, int logN, int limbs, int L) {
+  const std::size_t N = (std::size_t)1 << logN;
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = limbs - 1;
+  const u64 ql = pc[l].q;
+  const u64 v = last.p[blockIdx.z][n];
+  const bool neg = v > ql / 2;
+  u64* out = r.p[blockIdx.z];
+  for (int i = 0; i < l; ++i) {
+    const PrimeConst P = pc[i];
+    u64 x = reduce64(v, P);
+    if (neg) x = sub_mod(x, rs[((std::size_t)l * L + i) * 4 + 2], P.q);
+    out[(std::size_t)i * N + n] = x;
+  }
+}
+
+// grid (N/256, limbs-1, npolys)
+__global__ void k_rescale_finish(PolyList out, PolyList a, PolyList r, const PrimeConst* __restrict__ pc,
+                                 const u64* __restrict__ rs, int logN, int limbs, int L) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int l = limbs - 1;
+  const u64 q = pc[i].q;
+  const u64* c = rs + ((std::size_t)l * L + i) * 4;
+  out.p[blockIdx.z][o] = shoup_mul(sub_mod(a.p[blockIdx.z][o], r.p[blockIdx.z][o], q), c[0], c[1], q);
+}
+
+// ------------------------------------------------------------ encode etc.
+__global__ void k_coeffs_to_rns(u64* out, const long long* __restrict__ coeffs, const PrimeConst* __restrict__ pc,
+                                int logN) {
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  out[((std::size_t)blockIdx.y << logN) + n] = reduce_signed(coeffs[n], pc[blockIdx.y]);
+}
+__global__ void k_sample_error(u64* out, u64 key, const PrimeConst* __restrict__ pc, int logN, int ell, int L) {
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int prime = i < ell ? i : L + (i - ell);
+  out[((std::size_t)i << logN) + n] = reduce_signed(cbd21_d(prng_d(key, n)), pc[prime]);
+}
+__global__ void k_encrypt_combine(u64* c0, u64* c1, const u64* m, const u64* e, const u64* s, u64 stream_a,
+                                  const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const std::size_t o = ((std::size_t)i << logN) + n;
+  const PrimeConst P = pc[i];
+  const u64 a = mulhi(prng_d(stream_a, (u64)o), P.q);
+  c1[o] = a;
+  c0[o] = sub_mod(add_mod(m[o], e[o], P.q), mul_mod(a, s[o], P), P.q);
+}
+__global__ void k_keygen_digit(u64* b, u64* a, const u64* e, const u64* s, const u64* sp, u64 stream_a, int lo,
+                               int hi, const u64* __restrict__ pmod, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const std::size_t o = ((std::size_t)i << logN) + n;
+  const PrimeConst P = pc[i];
+  const u64 av = mulhi(prng_d(stream_a, (u64)o), P.q);
+  u64 bv = sub_mod(e[o], mul_mod(av, s[o], P), P.q);
+  if (i >= lo && i < hi) bv = add_mod(bv, mul_mod(pmod[i], sp[o], P), P.q);
+  b[o] = to_mont_d(bv, P);
+  a[o] = to_mont_d(av, P);
+}
+__global__ void k_secret_square(u64* out, const u64* s, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  out[o] = mul_mod(s[o], s[o], pc[blockIdx.y]);
+}
+__global__ void k_decrypt_core(u64* m, const u64* c0, const u64* c1, const u64* s, const PrimeConst* __restrict__ pc,
+                               int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst P = pc[blockIdx.y];
+  m[o] = add_mod(c0[o], mul_mod(c1[o], s[o], P), P.q);
+}
+__global__ void k_convert_mont(u64* out, const u64* in, const PrimeConst* __restrict__ pc, int logN, int ell, int L,
+                               bool to) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const PrimeConst P = pc[i < ell ? i : L + (i - ell)];
+  out[o] = to ? to_mont_d(in[o], P) : redc(0, in[o], P.q, P.qinv_neg);
+}
+
+}  // namespace
+
+void ew_add(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& b, int limbs, cudaStream_t st) {
+  if (out.n == 0 || limbs == 0) return;
+  k_add<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, b, t.pc, t.logN);
+  launch_check("k_add");
+}
+void ew_sub(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& b, int limbs, cudaStream_t st) {
+  if (out.n == 0 || limbs == 0) return;
+  k_sub<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, b, t.pc, t.logN);
+  launch_check("k_sub");
+}
+void ew_neg(const DevTables& t, const PolyList& out, const PolyList& a, int limbs, cudaStream_t st) {
+  if (out.n == 0 || limbs == 0) return;
+  k_neg<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, t.pc, t.logN);
+  launch_check("k_neg");
+}
+void ew_mul_pt(const DevTables& t, const PolyList& out, const PolyList& a, const u64* pt, int limbs, cudaStream_t st) {
+  if (out.n == 0 || limbs == 0) return;
+  k_mul_pt<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, pt, t.pc, t.logN);
+  launch_check("k_mul_pt");
+}
+void ew_mul_const(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& c, int limbs,
+                  cudaStream_t st) {
+  if (out.n == 0 || limbs == 0) return;
+  k_mul_const<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, c, t.pc, t.logN);
+  launch_check("k_mul_const");
+}
+void ew_add_const(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& c, int limbs,
+                  cudaStream_t st) {
+  if (out.n == 0 || limbs == 0) return;
+  k_add_const<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, c, t.pc, t.logN);
+  launch_check("k_add_const");
+}
+void ew_tensor(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
+               const u64* b1, int limbs, cudaStream_t st) {
+  k_tensor<<<grid_for(t.N, limbs), kThreads, 0, st>>>(d0, d1, d2, a0, a1, b0, b1, t.pc, t.logN);
+  launch_check("k_tensor");
+}
+void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int limbs, cudaStream_t st) {
+  if (out.n == 0 || limbs == 0) return;
+  k_automorph<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, in, t.logN);
+  launch_check("k_automorph");
+}
+
+void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st) {
+  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  if (beta < 2 && t.K == 0) return;
+  k_modup_bconv<<<grid_for(t.N, beta, x.n), kThreads, 0, st>>>(ext, x, t.pc, t.modup_qhinv, t.modup_qhat, t.logN,
+                                                                  limbs, t.L, t.K, t.dnum, t.alpha);
+}
+void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st) {
+  if (jobs.n == 0) return;
+  k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K, t.alpha);
+  launch_check("k_ks_inner");
+}
+void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
+  if (conv.n == 0) return;
+  k_moddown_conv<<<grid_for(t.N, 1, conv.n), kThreads, 0, st>>>(conv, z, t.pc, t.md_pk, t.md_pinv, t.md_phat,
+                                                                  t.md_q, t.logN, limbs, t.L, t.K);
+}
+void moddown_finish(const DevTables& t, const PolyList& out, const PolyList& acc, const PolyList& conv,
+                    const PolyList& add, int limbs, cudaStream_t st) {
+  if (out.n == 0) return;
+  k_moddown_finish<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, acc, conv, add, t.pc, t.md_q, t.logN);
+  launch_check("k_moddown_finish");
+}
+void rescale_lift(const DevTables& t, const PolyList& r, const PolyList& last, int limbs, cudaStream_t st) {
+  if (r.n == 0) return;
+  k_rescale_lift<<<grid_for(t.N, 1, r.n), kThreads, 0, st>>>(r, last, t.pc, t.rs, t.logN, limbs, t.L);
+  launch_check("k_rescale_lift");
+}
+void rescale_finish(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& r, int limbs,
+                    cudaStream_t st) {
+  if (out.n == 0) return;
+  k_rescale_finish<<<grid_for(t.N, limbs - 1, out.n), kThreads, 0, st>>>(out, a, r, t.pc, t.rs, t.logN, limbs, t.L);
+  launch_check("k_rescale_finish");
+}
+
+void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st) {
+  k_coeffs_to_rns<<<grid_for(t.N, limbs), kThreads, 0, st>>>(out, coeffs, t.pc, t.logN);
+  launch_check("k_coeffs_to_rns");
+}
+void sample_error(const DevTables& t, u64* out, u64 stream_key, int nlimbs, int ell, cudaStream_t st) {
+  k_sample_error<<<grid_for(t.N, nlimbs), kThreads, 0, st>>>(out, stream_key, t.pc, t.logN, ell, t.L);
+  launch_check("k_sample_error");
+}
+void encrypt_combine(const DevTables& t, u64* c0, u64* c1, const u64* m, const u64* e, u64 stream_a, int limbs,
+                     cudaStream_t st) {
+  k_encrypt_combine<<<grid_for(t.N, limbs), kThreads, 0, st>>>(c0, c1, m, e, t.s_ntt, stream_a, t.pc, t.logN);
+  launch_check("k_encrypt_combine");
+}
+void keygen_digit(const DevTables& t, u64* b, u64* a, const u64* e, const u64* sp, u64 stream_a, int lo, int hi,
+                  const u64* pmod, cudaStream_t st) {
+  k_keygen_digit<<<grid_for(t.N, t.L + t.K), kThreads, 0, st>>>(b, a, e, t.s_ntt, sp, stream_a, lo, hi, pmod, t.pc,
+                                                                 t.logN);
+}
+void secret_square(const DevTables& t, u64* out, cudaStream_t st) {
+  k_secret_square<<<grid_for(t.N, t.L + t.K), kThreads, 0, st>>>(out, t.s_ntt, t.pc, t.logN);
+  launch_check("k_secret_square");
+}
+void decrypt_core(const DevTables& t, u64* m, const u64* c0, const u64* c1, int limbs, cudaStream_t st) {
+  k_decrypt_core<<<grid_for(t.N, limbs), kThreads, 0, st>>>(m, c0, c1, t.s_ntt, t.pc, t.logN);
+  launch_check("k_decrypt_core");
+}
+void convert_mont(const DevTables& t, u64* out, const u64* in, int nlimbs, int ell, bool to_mont, cudaStream_t st) {
+  k_convert_mont<<<grid_for(t.N, nlimbs), kThreads, 0, st>>>(out, in, t.pc, t.logN, ell, t.L, to_mont);
+  launch_check("k_convert_mont");
+}
+
+}  // namespace fheon

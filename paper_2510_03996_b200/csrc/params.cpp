@@ -1,0 +1,160 @@
+// Host-side parameter generation; see params.hpp and DESIGN.md section 3.
+#include "params.hpp"
+
+#include <cmath>
+#include <stdexcept>
+
+namespace fheon {
+
+u64 powmod(u64 a, u64 e, u64 q) {
+  u64 r = 1 % q;
+  a %= q;
+  while (e) {
+    if (e & 1) r = mulmod(r, a, q);
+    a = mulmod(a, a, q);
+    e >>= 1;
+  }
+  return r;
+}
+
+bool is_prime(u64 n) {
+  static const u64 bases[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (n < 2) return false;
+  for (u64 b : bases)
+    if (n % b == 0) return n == b;
+  u64 d = n - 1;
+  int r = 0;
+  while ((d & 1) == 0) {
+    d >>= 1;
+    ++r;
+  }
+  for (u64 b : bases) {
+    u64 x = powmod(b, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool composite = true;
+    for (int j = 1; j < r; ++j) {
+      x = mulmod(x, x, n);
+      if (x == n - 1) {
+        composite = false;
+        break;
+      }
+    }
+    if (composite) return false;
+  }
+  return true;
+}
+
+unsigned bitrev(unsigned x, int bits) {
+  unsigned r = 0;
+  for (int i = 0; i < bits; ++i) {
+    r = (r << 1) | (x & 1u);
+    x >>= 1;
+  }
+  return r;
+}
+
+namespace {
+
+bool contains(const std::vector<u64>& v, u64 x) {
+  for (u64 y : v)
+    if (y == x) return true;
+  return false;
+}
+
+// Largest value = 1 mod M strictly below 2^bits.
+u64 top_candidate(int bits, u64 M) {
+  u64 x = (((1ULL << bits) - 1) / M) * M + 1;
+  if (x >= (1ULL << bits)) x -= M;
+  return x;
+}
+
+}  // namespace
+
+HostTables make_tables(const Params& p) {
+  if (p.logN < 10 || p.logN > 16) throw std::invalid_argument("logN must be in [10, 16]");
+  if (p.L < 1 || p.K < 1 || p.L + p.K > kMaxPrimes || p.dnum < 1)
+    throw std::invalid_argument("bad limb counts");
+  if (p.first_bits > 60 || p.scale_bits > 60 || p.special_bits > 60 || p.scale_bits < 20)
+    throw std::invalid_argument("prime bit sizes must be in [20, 60]");
+  HostTables t;
+  t.p = p;
+  t.N = std::size_t{1} << p.logN;
+  t.S = static_cast<int>(t.N / 2);
+  t.alpha = (p.L + p.dnum - 1) / p.dnum;
+  t.nprimes = p.L + p.K;
+  const u64 M = 2 * static_cast<u64>(t.N);
+
+  std::vector<u64> q;
+  {  // q_0
+    u64 x = top_candidate(p.first_bits, M);
+    while (!is_prime(x)) x -= M;
+    q.push_back(x);
+  }
+  // Scaling primes, chosen top-down so the FLEXIBLEAUTO targets
+  // T_{lv-1} = T_lv^2 / q_lv stay at 2^scale_bits (no compounding drift).
+  t.T.assign(p.L, 0.0);
+  std::vector<u64> chosen(p.L, 0);
+  {
+    double T = std::ldexp(1.0, p.scale_bits);
+    t.T[p.L - 1] = T;
+    for (int lv = p.L - 1; lv >= 1; --lv) {
+      const double target = (T * T) / std::ldexp(1.0, p.scale_bits);
+      const u64 tgt = static_cast<u64>(target);
+      const u64 base = ((tgt - 1) / M) * M + 1;
+      u64 pick = 0;
+      auto ok = [&](u64 x) {
+        if (!is_prime(x) || contains(q, x)) return false;
+        for (int i = p.L - 1; i > lv; --i)
+          if (chosen[i] == x) return false;
+        return true;
+      };
+      for (u64 k = 0; pick == 0; ++k) {
+        const u64 down = base - k * M, up = base + (k + 1) * M;
+        const u64 first = (tgt - down <= up - tgt) ? down : up;
+        const u64 second = (first == down) ? up : down;
+        if (ok(first)) pick = first;
+        else if (ok(second)) pick = second;
+      }
+      chosen[lv] = pick;
+      T = (T * T) / static_cast<double>(pick);
+      t.T[lv - 1] = T;
+    }
+    for (int lv = 1; lv < p.L; ++lv) q.push_back(chosen[lv]);
+  }
+  {  // special primes
+    u64 x = top_candidate(p.special_bits, M);
+    for (int k = 0; k < p.K; ++k) {
+      while (!is_prime(x) || contains(q, x)) x -= M;
+      q.push_back(x);
+      x -= M;
+    }
+  }
+  t.q = q;
+  t.psi.resize(q.size());
+  for (std::size_t i = 0; i < q.size(); ++i) {
+    const u64 qi = q[i];
+    for (u64 g = 2;; ++g) {
+      const u64 psi = powmod(g, (qi - 1) / M, qi);
+      if (powmod(psi, t.N, qi) == qi - 1) {
+        t.psi[i] = psi;
+        break;
+      }
+    }
+  }
+  t.rotgroup.resize(t.S);
+  u64 g = 1;
+  for (int j = 0; j < t.S; ++j) {
+    t.rotgroup[j] = g;
+    g = (g * 5) % M;
+  }
+  t.ksi_re.resize(M + 1);
+  t.ksi_im.resize(M + 1);
+  for (u64 k = 0; k <= M; ++k) {
+    const double ang = 2.0 * 3.14159265358979323846 * static_cast<double>(k) / static_cast<double>(M);
+    t.ksi_re[k] = std::cos(ang);
+    t.ksi_im[k] = std::sin(ang);
+  }
+  return t;
+}
+
+}  // namespace fheon

@@ -1,0 +1,76 @@
+// Host-side RNS-CKKS parameter generation and precomputed constant tables.
+//
+// The reference carries crypto parameters as metadata only
+// (proj/include/slotcnn/backend.hpp:32-49, CryptoMetadata{first_modulus_bits,
+// rescale_bits, key_switch_digits}); this engine interprets them.  The prime
+// chain, roots, FLEXIBLEAUTO scale targets and PRNG streams follow the spec
+// written out in DESIGN.md section 3 (mirrored by oracle/ckks_oracle.c, the
+// test-only checker -- no code is shared between the two).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace fheon {
+
+using u64 = std::uint64_t;
+using u128 = unsigned __int128;
+
+constexpr int kMaxPrimes = 80;
+
+struct Params {
+  int logN = 14;
+  int L = 11;       // Q limbs (levels 0..L-1)
+  int K = 4;        // special P limbs
+  int dnum = 3;     // key-switching digits
+  int first_bits = 50;
+  int scale_bits = 40;
+  int special_bits = 60;
+  u64 seed = 1;
+  int depth_budget = -1;  // simulator-facing level budget (<= L-1); -1 = L-1
+};
+
+// Everything derived from Params on the host.
+struct HostTables {
+  Params p;
+  std::size_t N = 0;
+  int S = 0, alpha = 0, nprimes = 0;
+  std::vector<u64> q;        // [L+K]: q_0..q_{L-1}, p_0..p_{K-1}
+  std::vector<u64> psi;      // primitive 2N-th roots
+  std::vector<double> T;     // scale target per level (level = limbs-1)
+  std::vector<u64> rotgroup; // 5^j mod 2N
+  std::vector<double> ksi_re, ksi_im;  // e^{2 pi i k / 2N}, k in [0, 2N]
+};
+
+HostTables make_tables(const Params& p);
+
+// ---- modular helpers (host)
+inline u64 mulmod(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
+inline u64 addmod(u64 a, u64 b, u64 q) { u64 r = a + b; return r >= q ? r - q : r; }
+inline u64 submod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+u64 powmod(u64 a, u64 e, u64 q);
+inline u64 invmod(u64 a, u64 q) { return powmod(a % q, q - 2, q); }
+inline u64 shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+inline u64 to_mont(u64 a, u64 q) { return (u64)(((u128)(a % q) << 64) % q); }
+bool is_prime(u64 n);
+unsigned bitrev(unsigned x, int bits);
+
+// ---- counter-based PRNG (spec shared with the oracle)
+inline u64 mix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+inline u64 prng_stream_key(u64 seed, u64 stream) {
+  return mix64(seed + 0x9E3779B97F4A7C15ULL * (stream + 1));
+}
+constexpr u64 kStreamSecret = 1;
+inline u64 stream_key(u64 key_id, int digit, int kind) {  // kind 2 = a, 3 = e
+  return (key_id << 16) | ((u64)digit << 4) | (u64)kind;
+}
+inline u64 stream_enc(u64 counter, int kind) {  // kind 4 = a, 5 = e
+  return (1ULL << 60) | (counter << 4) | (u64)kind;
+}
+
+}  // namespace fheon

@@ -1,0 +1,283 @@
+"""GPU parity: every RNS-CKKS primitive of the sm_100a engine is bit-exact
+against the CPU oracle (oracle/ckks_oracle.c) on identical inputs and keys.
+
+Mirrors the reference's backend tests (proj/tests/test_backend.cpp:80-220:
+rotation direction/range, level rules, depth exhaustion) at the RNS level.
+"""
+import numpy as np
+import pytest
+
+import paper_2510_03996_b200 as fh
+from oracle.ckks_oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(logN=12, L=6, K=2, dnum=3, first=50, scale=40, special=60, seed=11)
+
+
+def make_pair(logN, L, K, dnum, first, scale, special, seed, depth=None):
+    cfg = fh.ContextConfig(1 << logN, 1 << (logN - 1), depth if depth is not None else L - 1,
+                           fh.CryptoMetadata(first, scale, dnum), limbs=L, special_limbs=K, special_bits=special,
+                           seed=seed)
+    ctx = fh.SlotContext(cfg)
+    orc = Oracle(logN, L, K, dnum, first, scale, special, seed)
+    return ctx, orc
+
+
+@pytest.fixture(scope="module")
+def small():
+    return make_pair(**SMALL)
+
+
+def rand_limbs(orc, nlimbs, rng, primes_idx=None):
+    idx = primes_idx if primes_idx is not None else range(nlimbs)
+    return np.stack([rng.integers(0, int(orc.primes[i]), orc.N, dtype=np.uint64) for i in idx])
+
+
+def test_params_match_oracle(small):
+    ctx, orc = small
+    assert (ctx.primes == orc.primes).all()
+    assert np.array_equal(ctx.scales, orc.T)
+
+
+@pytest.mark.parametrize("logN", [10, 11, 12, 13, 14, 15, 16])
+def test_ntt_bit_exact_all_sizes(logN):
+    ctx, orc = make_pair(logN, 3, 2, 3, 50, 40, 60, 5)
+    rng = np.random.default_rng(logN)
+    a = rand_limbs(orc, 5, rng)  # q0..q2, p0, p1 as one 5-limb poly (limb i uses prime i)
+    fwd = ctx.ntt(a)
+    want = orc.ntt_limbs(a)
+    assert np.array_equal(fwd, want)
+    back = ctx.ntt(fwd, inverse=True)
+    assert np.array_equal(back, a)
+    assert np.array_equal(back, orc.ntt_limbs(want, inverse=True))
+
+
+def test_ntt_batched_polys(small):
+    ctx, orc = small
+    rng = np.random.default_rng(1)
+    a = np.stack([rand_limbs(orc, 4, rng) for _ in range(3)])
+    got = ctx.ntt(a)
+    for p in range(3):
+        assert np.array_equal(got[p], orc.ntt_limbs(a[p]))
+
+
+@pytest.mark.parametrize("t", [1, 2, 5, -1, -7, 1000, 2047])
+def test_automorphism_bit_exact(small, t):
+    ctx, orc = small
+    rng = np.random.default_rng(t % 97)
+    a = rand_limbs(orc, 4, rng)
+    g = orc.galois(t)
+    assert ctx.galois_element(t) == g
+    assert np.array_equal(ctx.automorph(a, g), orc.automorph_ntt(a, g))
+
+
+def test_keygen_bit_exact(small):
+    ctx, orc = small
+    g = orc.galois(3)
+    assert np.array_equal(ctx.download_key(g), orc.keygen(g))
+    assert np.array_equal(ctx.download_key(0), orc.keygen(0))
+
+
+def test_encrypt_bit_exact_and_decrypt(small):
+    ctx, orc = small
+    rng = np.random.default_rng(2)
+    vals = rng.uniform(-1, 1, orc.S)
+    ct = fh.SlotVector.encode_top(ctx, vals)
+    # the engine's encryption counter starts at 0 and increments per encryption
+    want = None
+    for counter in range(0, 64):
+        cand = orc.encrypt(vals, counter)
+        if np.array_equal(cand[1], ct.words()[1]):
+            want = cand
+            break
+    assert want is not None, "no matching encryption counter"
+    assert np.array_equal(ct.words(), want)
+    assert np.abs(ct.slots() - vals).max() < 1e-6
+    assert np.abs(orc.decrypt(want, orc.T[-1]) - vals).max() < 1e-6
+
+
+def _oracle_ct(orc, rng, counter=5):
+    vals = rng.uniform(-1, 1, orc.S)
+    return vals, orc.encrypt(vals, counter)
+
+
+@pytest.mark.parametrize("t", [1, -1, 3, 64, -1000, 2047])
+def test_rotation_bit_exact(small, t):
+    ctx, orc = small
+    rng = np.random.default_rng(100 + abs(t))
+    vals, ct = _oracle_ct(orc, rng)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    got = fh.rotate(x, t)
+    want = orc.rotate(ct, t, orc.rotation_key(t))
+    assert np.array_equal(got.words(), want)
+    assert np.abs(got.slots() - np.roll(vals, -t)).max() < 1e-6
+    assert got.level() == x.level()
+
+
+@pytest.mark.parametrize("limbs", [6, 4, 3, 1])
+def test_rotation_lower_levels(small, limbs):
+    ctx, orc = small
+    rng = np.random.default_rng(limbs)
+    vals, ct = _oracle_ct(orc, rng)
+    ct = np.ascontiguousarray(ct[:, :limbs])
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    got = fh.rotate(x, 7)
+    want = orc.rotate(ct, 7, orc.rotation_key(7))
+    assert np.array_equal(got.words(), want)
+
+
+def test_hoisted_equals_single(small):
+    ctx, orc = small
+    rng = np.random.default_rng(9)
+    vals, ct = _oracle_ct(orc, rng)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    ts = [1, 2, 3, 28, 29, -5]
+    hs = fh.rotate_hoisted(x, ts)
+    for t, h in zip(ts, hs):
+        assert np.array_equal(h.words(), fh.rotate(x, t).words())
+        assert np.array_equal(h.words(), orc.rotate(ct, t, orc.rotation_key(t)))
+
+
+def test_keyswitch_modup_moddown(small):
+    ctx, orc = small
+    rng = np.random.default_rng(4)
+    _, ct = _oracle_ct(orc, rng)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    g = orc.galois(5)
+    got = fh.keyswitch_raw(x, g, g).words()
+    ks0, ks1 = orc.keyswitch(ct[1], orc.keygen(g), g)
+    assert np.array_equal(got[0], ks0)
+    assert np.array_equal(got[1], ks1)
+
+
+def test_rescale_bit_exact(small):
+    ctx, orc = small
+    rng = np.random.default_rng(5)
+    a = np.stack([rand_limbs(orc, 6, rng), rand_limbs(orc, 6, rng)])
+    x = fh.SlotVector.from_words(ctx, a, 1.0)
+    assert np.array_equal(fh.rescale(x).words(), orc.rescale(a))
+
+
+def test_mult_plain_bit_exact(small):
+    ctx, orc = small
+    rng = np.random.default_rng(6)
+    vals, ct = _oracle_ct(orc, rng)
+    pv = rng.uniform(-1, 1, orc.S)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    got = fh.mult_plain(x, pv)
+    want, s = orc.mult_plain(ct, orc.T[-1], pv)
+    assert np.array_equal(got.words(), want)
+    assert got.scale() == s
+    assert got.level() == x.level() - 1
+    assert np.abs(got.slots() - vals * pv).max() < 1e-6
+
+
+def test_mult_const_bit_exact(small):
+    ctx, orc = small
+    rng = np.random.default_rng(7)
+    vals, ct = _oracle_ct(orc, rng)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    got = fh.mult_plain(x, np.full(orc.S, -0.3125))
+    want, _ = orc.mult_plain(ct, orc.T[-1], np.full(orc.S, -0.3125))
+    assert np.array_equal(got.words(), want)
+
+
+def test_mult_cipher_bit_exact(small):
+    ctx, orc = small
+    rng = np.random.default_rng(8)
+    va, ca = _oracle_ct(orc, rng, 1)
+    vb, cb = _oracle_ct(orc, rng, 2)
+    a = fh.SlotVector.from_words(ctx, ca, orc.T[-1])
+    b = fh.SlotVector.from_words(ctx, cb, orc.T[-1])
+    got = fh.mult_cipher(a, b)
+    want = orc.mult_cipher(ca, cb, orc.relin_key())
+    assert np.array_equal(got.words(), want)
+    assert got.level() == a.level() - 1
+    assert np.abs(got.slots() - va * vb).max() < 1e-6
+
+
+def test_level_down_bit_exact(small):
+    ctx, orc = small
+    rng = np.random.default_rng(10)
+    vals, ct = _oracle_ct(orc, rng)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    got = fh.level_down(x, 3)
+    want, s = orc.level_down(ct, orc.T[-1], 3)
+    assert np.array_equal(got.words(), want)
+    assert got.scale() == s
+    assert np.abs(got.slots() - vals).max() < 1e-6
+
+
+def test_add_sub_levels_and_values(small):
+    ctx, _ = small
+    rng = np.random.default_rng(11)
+    va, vb = rng.uniform(-1, 1, ctx.slots()), rng.uniform(-1, 1, ctx.slots())
+    a = fh.SlotVector.encode(ctx, va)
+    b = fh.mult_plain(fh.SlotVector.encode(ctx, vb), np.full(ctx.slots(), 1.0))
+    s = fh.add(a, b)
+    d = fh.sub(a, b)
+    assert s.level() == min(a.level(), b.level())
+    assert np.abs(s.slots() - (va + vb)).max() < 1e-6
+    assert np.abs(d.slots() - (va - vb)).max() < 1e-6
+
+
+def test_rotation_range_errors(small):
+    ctx, _ = small
+    x = fh.SlotVector.encode(ctx, [1.0, 2.0])
+    S = ctx.slots()
+    with pytest.raises(fh.InvalidRotationError):
+        fh.rotate(x, S)
+    with pytest.raises(fh.InvalidRotationError):
+        fh.rotate(x, -S)
+    fh.rotate(x, S - 1)
+    fh.rotate(x, -(S - 1))
+
+
+def test_depth_exhaustion(small):
+    ctx, _ = small
+    x = fh.SlotVector.encode(ctx, [0.5])
+    ones = np.ones(ctx.slots())
+    while x.level() > 0:
+        x = fh.mult_plain(x, ones)
+    with pytest.raises(fh.DepthExhaustedError):
+        fh.mult_plain(x, ones)
+    with pytest.raises(fh.DepthExhaustedError):
+        fh.mult_cipher(x, x)
+
+
+def test_trace_events(small):
+    ctx, _ = small
+    rec = ctx.attach_recorder()
+    x = fh.SlotVector.encode(ctx, [1.0, 2.0, 3.0])
+    y = fh.rotate(x, 2)
+    z = fh.mult_plain(y, np.ones(ctx.slots()) * 2)
+    fh.mult_cipher(z, z)
+    ev = rec.snapshot()
+    assert [(e.kind, e.value) for e in ev] == [("rotation", 2), ("mult_plain", x.level() - 1),
+                                               ("mult_cipher", x.level() - 2)]
+    ctx.detach_recorder()
+
+
+@pytest.mark.slow
+def test_config2_rotation_bit_exact():
+    """BASELINE configs[1] parameters: N=2^16, L=24, K=8, dnum=3."""
+    ctx, orc = make_pair(16, 24, 8, 3, 60, 50, 60, 2001)
+    rng = np.random.default_rng(2001)
+    vals, ct = _oracle_ct(orc, rng)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    got = fh.rotate(x, 1)
+    assert np.array_equal(got.words(), orc.rotate(ct, 1, orc.rotation_key(1)))
+    got = fh.rescale(x)
+    assert np.array_equal(got.words(), orc.rescale(ct))
+
+
+def test_config1_rotation_bit_exact():
+    """BASELINE configs[0] parameters: N=2^14, 50-bit q0, 40-bit scaling, L=11, dnum=3."""
+    ctx, orc = make_pair(14, 11, 4, 3, 50, 40, 60, 1001)
+    rng = np.random.default_rng(1001)
+    vals, ct = _oracle_ct(orc, rng)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    got = fh.rotate(x, 28)
+    assert np.array_equal(got.words(), orc.rotate(ct, 28, orc.rotation_key(28)))
+    assert np.abs(got.slots() - np.roll(vals, -28)).max() < 1e-6
