@@ -87,6 +87,21 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
   if (ht_.alpha > kMaxAlpha - 1) throw Error(ErrKind::shape, "alpha = ceil(L/dnum) must be < 16");
   if (p.K > kMaxK - 1) throw Error(ErrKind::shape, "K must be < 16");
   if (p.L > 64) throw Error(ErrKind::shape, "L must be <= 64");
+  {
+    // Hybrid key switching needs P = prod(p_k) to dominate every digit
+    // modulus Q_j, otherwise the key-switch noise Q_j * e / P swamps the scale.
+    double logP = 0.0;
+    for (int k = 0; k < p.K; ++k) logP += std::log2((double)ht_.q[p.L + k]);
+    for (int j = 0; j < p.dnum; ++j) {
+      double logQ = 0.0;
+      for (int i = j * ht_.alpha; i < std::min((j + 1) * ht_.alpha, p.L); ++i) logQ += std::log2((double)ht_.q[i]);
+      if (logQ > logP)
+        throw Error(ErrKind::shape, "special modulus P (" + std::to_string((int)logP) +
+                                        " bits) must exceed every key-switching digit modulus (digit " +
+                                        std::to_string(j) + ": " + std::to_string((int)logQ) +
+                                        " bits); raise special_limbs or dnum");
+    }
+  }
   depth_budget_ = p.depth_budget < 0 ? p.L - 1 : p.depth_budget;
   if (depth_budget_ < 1 || depth_budget_ > p.L - 1)
     throw Error(ErrKind::shape, "depth budget must lie in [1, L-1]");

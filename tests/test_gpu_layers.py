@@ -1,0 +1,205 @@
+"""GPU parity of the layer API against the reference's own layer algorithms.
+
+The checker is the UNMODIFIED reference slotcnn core (oracle/_ref, built from
+/root/reference/proj): the same inputs are run through its cleartext slot
+simulator and through the encrypted B200 engine; the decrypted slots must
+agree within max-abs 1e-3 (the north-star tolerance), the output level must
+be identical and the trace (rotation indices, mult level_after, in order)
+must be identical.  Case generation follows acceptance criterion 1
+(proj/tests/acceptance.cpp:226-426): W in {4,6,8}, C,F in 1..4, random
+kernel/stride/padding, both striding flavours, degrees {7,27,59}.
+"""
+import numpy as np
+import pytest
+
+import paper_2510_03996_b200 as fh
+from oracle import ref as sref
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+LOGN, DEPTH = 12, 13
+
+
+@pytest.fixture(scope="module")
+def env():
+    cfg = fh.ContextConfig(1 << LOGN, 1 << (LOGN - 1), DEPTH, fh.CryptoMetadata(52, 40, 3), limbs=DEPTH + 1,
+                           special_limbs=4, special_bits=60, seed=9001)
+    ctx = fh.SlotContext(cfg)
+    return ctx, sref.Ref(1 << LOGN, 1 << (LOGN - 1), DEPTH)
+
+
+def run_both(ctx, fn_gpu, fn_ref, x):
+    rec = ctx.attach_recorder()
+    xs = fh.SlotVector.encode(ctx, np.asarray(x).reshape(-1))
+    out = fn_gpu(xs)
+    ev = [(e.kind, e.value) for e in rec.snapshot()]
+    ctx.detach_recorder()
+    r = fn_ref(np.asarray(x).reshape(-1))
+    return out, ev, r
+
+
+def check(out_ct, ev, r, tag):
+    got = out_ct.slots()
+    err = np.abs(got - r.slots).max()
+    assert err < TOL, f"{tag}: max abs error {err}"
+    assert out_ct.level() == r.level, f"{tag}: level {out_ct.level()} vs reference {r.level}"
+    assert ev == r.events, f"{tag}: trace differs"
+    return err
+
+
+def cases(seed, n):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        W = int(rng.choice([4, 6, 8]))
+        C = int(rng.integers(1, 5))
+        F = int(rng.integers(1, 5))
+        out.append((W, C, F, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("W,C,F,s", cases(9001, 8))
+def test_generic_conv(env, W, C, F, s):
+    ctx, ref = env
+    rng = np.random.default_rng(s)
+    while True:
+        k = int(rng.choice([2, 3, 5]))
+        S = int(rng.integers(1, 4))
+        P = int(rng.integers(0, 3))
+        if k <= W + 2 * P and (W + 2 * P - k) % S == 0:
+            break
+    variant = int(rng.integers(0, 2))
+    x = rng.uniform(-1, 1, (C, W, W))
+    w = rng.uniform(-1, 1, (F, C, k, k))
+    b = rng.uniform(-1, 1, F)
+    cfg = fh.ConvConfig(C, F, k, S, P, fh.ConvMode.generic, fh.StrideVariant(variant))
+    out, ev, r = run_both(ctx, lambda v: fh.convolution(fh.PackedTensor(v, C, W), cfg, fh.KernelTensor(w, b)).data,
+                          lambda v: ref.convolution(v, DEPTH, C, W, F, k, S, P, 0, variant, w, b), x)
+    check(out, ev, r, f"generic conv W={W} C={C} F={F} k={k} S={S} P={P} v={variant}")
+
+
+@pytest.mark.parametrize("W,C,F,s", cases(9002, 4))
+def test_special3x3(env, W, C, F, s):
+    ctx, ref = env
+    rng = np.random.default_rng(s)
+    x = rng.uniform(-1, 1, (C, W, W))
+    w = rng.uniform(-1, 1, (F, C, 3, 3))
+    b = rng.uniform(-1, 1, F)
+    cfg = fh.ConvConfig(C, F, 3, 1, 1, fh.ConvMode.special3x3)
+    out, ev, r = run_both(ctx, lambda v: fh.convolution(fh.PackedTensor(v, C, W), cfg, fh.KernelTensor(w, b)).data,
+                          lambda v: ref.convolution(v, DEPTH, C, W, F, 3, 1, 1, 1, 0, w, b), x)
+    check(out, ev, r, f"special3x3 W={W} C={C} F={F}")
+
+
+@pytest.mark.parametrize("W,C,F,s", [c for c in cases(9003, 6) if c[1] >= 2][:3])
+def test_grouped_conv(env, W, C, F, s):
+    ctx, ref = env
+    rng = np.random.default_rng(s)
+    Fg = C * int(rng.integers(1, 3))
+    while True:
+        k = int(rng.choice([2, 3]))
+        S = int(rng.integers(1, 3))
+        if k <= W and (W - k) % S == 0:
+            break
+    x = rng.uniform(-1, 1, (C, W, W))
+    w = rng.uniform(-1, 1, (Fg, 1, k, k))
+    b = rng.uniform(-1, 1, Fg)
+    cfg = fh.ConvConfig(C, Fg, k, S, 0, fh.ConvMode.grouped)
+    out, ev, r = run_both(ctx, lambda v: fh.convolution(fh.PackedTensor(v, C, W), cfg, fh.KernelTensor(w, b)).data,
+                          lambda v: ref.convolution(v, DEPTH, C, W, Fg, k, S, 0, 2, 0, w, b), x)
+    check(out, ev, r, f"grouped W={W} C={C} F={Fg} k={k} S={S}")
+
+
+@pytest.mark.parametrize("W,C,F,s", cases(9004, 4))
+def test_avg_pool(env, W, C, F, s):
+    ctx, ref = env
+    rng = np.random.default_rng(s)
+    while True:
+        k = int(rng.choice([2, 3]))
+        S = int(rng.integers(1, 4))
+        if k <= W and (W - k) % S == 0:
+            break
+    variant = int(rng.integers(0, 2))
+    x = rng.uniform(-1, 1, (C, W, W))
+    cfg = fh.PoolConfig(fh.PoolKind.average, k, S, fh.StrideVariant(variant))
+    out, ev, r = run_both(ctx, lambda v: fh.avg_pool(fh.PackedTensor(v, C, W), cfg).data,
+                          lambda v: ref.pool(v, DEPTH, C, W, 0, k, S, variant), x)
+    check(out, ev, r, f"avg_pool W={W} C={C} k={k} S={S} v={variant}")
+
+
+@pytest.mark.parametrize("W,C,F,s", cases(9005, 3))
+def test_global_and_whole_channel_pool(env, W, C, F, s):
+    ctx, ref = env
+    rng = np.random.default_rng(s)
+    x = rng.uniform(-1, 1, (C, W, W))
+    out, ev, r = run_both(ctx, lambda v: fh.global_avg_pool(fh.PackedTensor(v, C, W)),
+                          lambda v: ref.pool(v, DEPTH, C, W, 1), x)
+    check(out, ev, r, f"global W={W} C={C}")
+    out, ev, r = run_both(ctx, lambda v: fh.whole_channel_pool(fh.PackedTensor(v, C, W), W),
+                          lambda v: ref.pool(v, DEPTH, C, W, 2, W), x)
+    check(out, ev, r, f"whole_channel W={W} C={C}")
+
+
+@pytest.mark.parametrize("W,C,F,s", cases(9006, 4))
+def test_fully_connected(env, W, C, F, s):
+    ctx, ref = env
+    rng = np.random.default_rng(s)
+    m = int(rng.integers(1, 9))
+    B = int(rng.integers(1, 5))
+    n = C * W * W
+    x = rng.uniform(-1, 1, n)
+    w = rng.uniform(-1, 1, (m, n))
+    b = rng.uniform(-1, 1, m)
+    out, ev, r = run_both(ctx, lambda v: fh.fully_connected(v, fh.FcConfig(n, m, B), fh.FcWeights(w, b)),
+                          lambda v: ref.fully_connected(v, DEPTH, n, m, B, w, b), x)
+    check(out, ev, r, f"fc n={n} m={m} B={B}")
+
+
+@pytest.mark.parametrize("W,C,F,s", cases(9007, 3))
+def test_pad_input(env, W, C, F, s):
+    ctx, ref = env
+    rng = np.random.default_rng(s)
+    P = int(rng.integers(1, 3))
+    x = rng.uniform(-1, 1, (C, W, W))
+    out, ev, r = run_both(ctx, lambda v: fh.pad_input(fh.PackedTensor(v, C, W), P).data,
+                          lambda v: ref.pad_input(v, DEPTH, C, W, P), x)
+    check(out, ev, r, f"pad W={W} C={C} P={P}")
+
+
+@pytest.mark.parametrize("W,S,variant", [(4, 2, 0), (8, 2, 1), (8, 3, 0), (6, 2, 1), (8, 4, 1)])
+def test_striding(env, W, S, variant):
+    ctx, ref = env
+    rng = np.random.default_rng(W * 10 + S)
+    x = rng.uniform(-1, 1, (1, W, W))
+    fn = fh.stride_extract_v2 if variant else fh.stride_extract_v1
+    out, ev, r = run_both(ctx, lambda v: fn(v, W, S), lambda v: ref.stride(v, DEPTH, W, S, 0, variant), x)
+    check(out, ev, r, f"stride W={W} S={S} v={variant}")
+
+
+@pytest.mark.parametrize("degree,scale", [(7, 1.0), (27, 1.0), (59, 1.0), (59, 8.0)])
+def test_secure_relu(env, degree, scale):
+    ctx, ref = env
+    rng = np.random.default_rng(degree)
+    n = 40
+    x = rng.uniform(-1, 1, n) * scale
+    cfg = fh.ReluConfig(scale, degree, n)
+    out, ev, r = run_both(ctx, lambda v: fh.secure_relu(v, cfg), lambda v: ref.secure_relu(v, DEPTH, scale, degree, n),
+                          x)
+    check(out, ev, r, f"relu degree={degree} scale={scale}")
+
+
+def test_config1_conv_layer():
+    """BASELINE configs[0]: N=2^14, 8192 slots, 50-bit q0 + 40-bit scaling, depth 10, dnum 3;
+    1x28x28 U[0,1] input, conv 1->6 5x5 stride 1 pad 0, weights N(0, 0.1^2), bias 0."""
+    ctx = fh.SlotContext(fh.ContextConfig.preset("config1"))
+    ref = sref.Ref(16384, 8192, 10)
+    rng = np.random.default_rng(1001)
+    x = rng.uniform(0, 1, (1, 28, 28))
+    w = np.random.default_rng(1002).normal(0, 0.1, (6, 1, 5, 5))
+    cfg = fh.ConvConfig(1, 6, 5, 1, 0)
+    out, ev, r = run_both(ctx, lambda v: fh.convolution(fh.PackedTensor(v, 1, 28), cfg, fh.KernelTensor(w)).data,
+                          lambda v: ref.convolution(v, 10, 1, 28, 6, 5, 1, 0, 0, 0, w, None), x)
+    err = check(out, ev, r, "config1 conv")
+    assert r.level == 7 and len(r.rotations()) == 305
+    assert err < 1e-4
