@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py -- FHEON hot path on B200: key-switch rotation throughput.
+
+Workload (BASELINE.json configs[1], the config the `rotations/s` metric is
+quoted on): RNS-CKKS N = 2^16 (32768 slots), L = 24 limbs (60-bit q0 + 23 x
+50-bit), K = 8 special primes, dnum = 3 hybrid key switching.  One step =
+B ciphertexts at the top level (l = 24), each rotated by a power-of-two step
+with its own evaluation key (16 keys 2^0..2^15 resident in HBM, 1.5 GiB):
+full ModUp -> key inner product (automorphism fused) -> ModDown per rotation.
+
+  value  rotations/s with inputs resident in HBM (device time, CUDA events on
+         the engine stream, max over ranks; inputs 8 x 25 MiB ciphertexts and
+         1.5 GiB of keys exceed the 126 MB L2, so no flush is needed)
+  e2e    the same through the C ABI from pinned host words: upload, rotate,
+         download, every step
+  roofline  the key-switch inner-product kernel (HBM-bound: streams the key)
+         timed live with CUDA events inside the timed region
+  cpu_baseline  the repo's CPU RNS-CKKS oracle (oracle/ckks_oracle.c, OpenMP)
+         doing the same rotations on the host cores
+
+`--impl reference` times the reference's own CPU path (oracle/_ref: slotcnn's
+rotate() on its cleartext slot simulator at 32768 slots) on all host cores.
+Multi-GPU: independent replicas, weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LOGN, L, K, DNUM = 16, 24, 8, 3
+N = 1 << LOGN
+S = N // 2
+NKEYS = 16
+CONFIG = {"workload": "configs[1] CKKS key-switch rotation", "ring_dimension": N, "slots": S, "limbs": L,
+          "special_limbs": K, "dnum": DNUM, "prime_bits": "60 + 23x50, special 8x60",
+          "rotation_steps": "2^0..2^14 and -1 (16 keys, one per rotation, cycled)", "level": L - 1,
+          "l2": "inputs larger than L2 (8 x 25 MiB ciphertexts + 1.5 GiB keys), no flush"}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sms)) if sms else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def measured_peak_hbm():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def committed_traffic():
+    """dram bytes per launch of the roofline kernel from the committed ncu --set full capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        return d.get("ks_inner_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import paper_2510_03996_b200 as fh
+    from paper_2510_03996_b200 import replicas
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = args.batch
+    ctx = fh.SlotContext(fh.ContextConfig.preset("config2"))
+    steps_pow = [1 << i for i in range(NKEYS - 1)] + [-1]
+    ctx.keygen_rotations(steps_pow)
+    ctx.set_strict_keys(True)
+    rng = np.random.default_rng(2001 + rank)
+    cts = [fh.SlotVector.encode_top(ctx, rng.uniform(-1, 1, S)) for _ in range(B)]
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    counter = [0]
+
+    def step():
+        outs = []
+        for b in range(B):
+            t = steps_pow[counter[0] % NKEYS]
+            counter[0] += 1
+            outs.append(fh.rotate(cts[b], t))
+        return outs
+
+    def barrier():
+        torch.cuda.synchronize()
+        ctx.sync()
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    st0 = ctx.stats()
+    ctx.timer_arm(1)  # key-switch inner product, timed live in the region
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        keep = None
+        for _ in range(args.steps):
+            keep = step()
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    ks_ms, ks_n = ctx.timer_read()
+    ctx.timer_arm(0)
+    st1 = ctx.stats()
+    del keep
+    barrier()
+    value, ms_max = replicas.replica_throughput(ms, args.steps * B, torch.device("cuda", local))
+
+    # ---- roofline of the key-switch inner product (per launch: one rotation)
+    E = L + K
+    beta = (L + (L + DNUM - 1) // DNUM - 1) // ((L + DNUM - 1) // DNUM)
+    alg_bytes = (beta * E * N + 2 * beta * E * N + 2 * E * N) * 8  # digits + key (read), acc (write)
+    ks_avg_ms = ks_ms / max(1, ks_n)
+    achieved = alg_bytes / (ks_avg_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peak_hbm()
+
+    # ---- e2e through the C ABI with host buffers (pinned)
+    host_in = [torch.empty((2, L, N), dtype=torch.uint64, pin_memory=True).numpy() for _ in range(B)]
+    host_out = [torch.empty((2, L, N), dtype=torch.uint64, pin_memory=True).numpy() for _ in range(B)]
+    for b in range(B):
+        host_in[b][...] = cts[b].words()
+    scale = cts[0].scale()
+
+    def e2e_step():
+        for b in range(B):
+            x = fh.SlotVector.from_words(ctx, host_in[b], scale)
+            y = fh.rotate(x, steps_pow[counter[0] % NKEYS])
+            counter[0] += 1
+            y.words(out=host_out[b])
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(e2e_steps):
+        e2e_step()
+    barrier()
+    e2e_val, _ = replicas.replica_throughput((time.perf_counter() - t0) * 1e3, e2e_steps * B,
+                                             torch.device("cuda", local))
+    ct_bytes = 2 * L * N * 8
+
+    extras = {}
+    if rank == 0 and not args.quick:
+        extras = primitives(ctx, fh)
+    line = {
+        "metric": "rotations/s (CKKS key-switch rotation, N=2^16, L=24, dnum=3)",
+        "value": round(value, 1),
+        "unit": "rotations/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 (RNS limbs, <=60-bit primes)",
+        "data": "synthetic (seeded uniform slot values, encrypted; keys from seed 1)",
+        "config": dict(CONFIG, batch_per_step=B, parallelism=f"replicas x{ws}"),
+        "e2e": {"value": round(e2e_val, 1), "unit": "rotations/s", "h2d_bytes_per_step": B * ct_bytes,
+                "d2h_bytes_per_step": B * ct_bytes,
+                "path": "C ABI: fheon_ct_upload (pinned) -> fheon_rotate -> fheon_ct_download"},
+        "gpu_launches": int(st1["launches"] - st0["launches"]),
+        "roofline": {"kernel": "k_ks_inner (key inner product, automorphism fused)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": committed_traffic(),
+                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(ks_avg_ms, 5),
+                     "launches_timed": ks_n,
+                     "share_of_step": round(ks_ms / ms, 4)},
+        "clocks": clk.summary(),
+    }
+    if extras:
+        line["primitives"] = extras
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_port(args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def primitives(ctx, fh):
+    """Config-2 microbench (device time, CUDA events) + config-1 conv layer."""
+    out = {}
+    kinds = {"ntt_ms_per_ct": 0, "intt_ms_per_ct": 1, "automorphism_ms_per_ct": 2, "rotation_ms": 3,
+             "mac_term_ms_per_ct": 5, "rescale_ms_per_ct": 6, "add_ms_per_ct": 7}
+    for name, k in kinds.items():
+        batch = 1 if k == 3 else 8
+        ms = ctx.microbench(k, batch, L, 1, 10)
+        out[name] = round(ms / batch, 5)
+    for r in (8, 32):
+        ms = ctx.microbench(4, 1, L, r, 5)
+        out[f"hoisted{r}_rot_per_s"] = round(r / (ms / 1e3), 1)
+    ntt_bytes = 2 * L * N * 8 * 2
+    out["ntt_hbm_gbs"] = round(ntt_bytes / (out["ntt_ms_per_ct"] / 1e3) / 1e9, 1)
+    # config-1 conv layer (BASELINE configs[0]) through the layer API
+    try:
+        c1 = fh.SlotContext(fh.ContextConfig.preset("config1"))
+        rng = np.random.default_rng(1001)
+        x = rng.uniform(0, 1, (1, 28, 28))
+        w = np.random.default_rng(1002).normal(0, 0.1, (6, 1, 5, 5))
+        cfg = fh.ConvConfig(1, 6, 5, 1, 0)
+        xs = fh.SlotVector.encode(c1, x.reshape(-1))
+        fh.convolution(fh.PackedTensor(xs, 1, 28), cfg, fh.KernelTensor(w))  # warm + keygen
+        c1.sync()
+        t0 = time.perf_counter()
+        reps = 5
+        for _ in range(reps):
+            r = fh.convolution(fh.PackedTensor(xs, 1, 28), cfg, fh.KernelTensor(w))
+        c1.sync()
+        out["config1_conv_layer_ms"] = round((time.perf_counter() - t0) / reps * 1e3, 3)
+        del r
+    except Exception as e:  # pragma: no cover - diagnostics only
+        out["config1_conv_layer_error"] = str(e)
+    return out
+
+
+def cpu_baseline_port(args):
+    """The repo's CPU RNS-CKKS oracle doing config-2 rotations (OpenMP over limbs)."""
+    from oracle.ckks_oracle import Oracle
+    o = Oracle(LOGN, L, K, DNUM, 60, 50, 60, 1)
+    rng = np.random.default_rng(2001)
+    ct = o.encrypt(rng.uniform(-1, 1, S), 0)
+    keys = [o.rotation_key(1 << i) for i in range(2)]
+    o.rotate(ct, 1, keys[0])  # warm
+    n = args.cpu_sample
+    t0 = time.perf_counter()
+    for i in range(n):
+        o.rotate(ct, 1 << (i % 2), keys[i % 2])
+    dt = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": round(n / dt, 3), "unit": "rotations/s", "cores": cores, "kind": "port",
+            "sample": f"{n} key-switch rotations at N=2^16, L=24, dnum=3 (oracle/ckks_oracle.c, OpenMP)"}
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import ref as sref
+    if not sref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libslotcnn_ref.so not built"}))
+        return
+    r = sref.Ref(N, S, L - 1)
+    cores = os.cpu_count() or 1
+    per_thread = args.ref_iters
+
+    def one_step():
+        res = [0.0] * cores
+
+        def work(i):
+            res[i] = r.time_rotate(1 << (i % (NKEYS - 1)), per_thread)
+
+        th = [threading.Thread(target=work, args=(i,)) for i in range(cores)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        one_step()
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += one_step()
+    n_rot = args.steps * cores * per_thread
+    value = n_rot / tot
+    line = {
+        "impl": "reference",
+        "metric": "rotations/s (CKKS key-switch rotation, N=2^16, L=24, dnum=3)",
+        "value": round(value, 1),
+        "unit": "rotations/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(tot / args.steps * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 (cleartext slot simulator)",
+        "data": "synthetic",
+        "config": dict(CONFIG, reference_path="slotcnn rotate() on the cleartext SlotVector simulator"),
+        "cpu_baseline": {"value": round(value, 1), "unit": "rotations/s", "cores": cores, "kind": "reference",
+                         "sample": f"{per_thread} rotate() calls per thread x {cores} threads per step, 32768 "
+                                   "slots (reference simulator: memcpy rotation, no crypto)"},
+        "e2e": {"value": round(value, 1), "unit": "rotations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--cpu-sample", type=int, default=12)
+    ap.add_argument("--ref-iters", type=int, default=2000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip the primitive breakdown")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -55,6 +55,14 @@ const char* fheon_last_error(void);
 int fheon_last_error_kind(void);
 int fheon_version(void);
 
+/* ---- host-only helpers (no device needed) */
+/* prime chain q_0..q_{L-1}, p_0..p_{K-1} and the per-level scale targets */
+int fheon_host_primes(const fheon_params* p, uint64_t* primes, double* scales);
+/* canonical-embedding encode of n <= N/2 slot values at `scale` -> N signed coefficients */
+int fheon_host_encode(const fheon_params* p, const double* values, size_t n, double scale, int64_t* coeffs);
+/* Chebyshev interpolant coefficients of max(0, beta z) on [-1, 1] (chebyshev.cpp:33-50) */
+int fheon_cheb_relu_coefficients(double beta, int degree, double* coeffs);
+
 /* ---- context (SlotContext::create, backend.hpp:69) */
 int fheon_ctx_create(const fheon_params* p, fheon_ctx** out);
 void fheon_ctx_destroy(fheon_ctx* ctx);
@@ -62,9 +70,15 @@ void fheon_ctx_destroy(fheon_ctx* ctx);
 int fheon_ctx_info(const fheon_ctx* ctx, uint64_t* primes, double* scales, int* slots);
 void* fheon_ctx_stream(fheon_ctx* ctx); /* cudaStream_t */
 int fheon_ctx_sync(fheon_ctx* ctx);
-/* op counters: rotations, keyswitches, mult_plain, mult_cipher, rescales, ntt_limbs, encodes, adds */
-int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* out8);
+/* op counters: rotations, keyswitches, mult_plain, mult_cipher, rescales, ntt_limbs, encodes, adds,
+ * kernel launches (process-wide) */
+int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* out9);
 int fheon_ctx_reset_stats(fheon_ctx* ctx);
+/* live kernel timing with CUDA events on the context stream: arm a class
+ * (1 key-switch inner product, 2 NTT, 3 ModUp conversion, 4 ModDown
+ * conversion, 0 off), run work, read the summed milliseconds + scope count. */
+int fheon_timer_arm(fheon_ctx* ctx, int kernel_class);
+int fheon_timer_read(fheon_ctx* ctx, double* total_ms, int* count);
 
 /* ---- trace (TraceRecorder, trace.hpp:37-103; SlotContext::attach_recorder)
  * events: pairs (kind, value); kind 0 rotation (index), 1 mult_plain

@@ -54,6 +54,9 @@ SIGNATURES = {
     "fheon_last_error": (C.c_char_p, []),
     "fheon_last_error_kind": (C.c_int, []),
     "fheon_version": (C.c_int, []),
+    "fheon_host_primes": (C.c_int, [C.POINTER(fheon_params), u64p, dp]),
+    "fheon_host_encode": (C.c_int, [C.POINTER(fheon_params), dp, C.c_size_t, C.c_double, C.POINTER(C.c_int64)]),
+    "fheon_cheb_relu_coefficients": (C.c_int, [C.c_double, C.c_int, dp]),
     "fheon_ctx_create": (C.c_int, [C.POINTER(fheon_params), pp]),
     "fheon_ctx_destroy": (None, [vp]),
     "fheon_ctx_info": (C.c_int, [vp, u64p, dp, C.POINTER(C.c_int)]),
@@ -61,6 +64,8 @@ SIGNATURES = {
     "fheon_ctx_sync": (C.c_int, [vp]),
     "fheon_ctx_stats": (C.c_int, [vp, u64p]),
     "fheon_ctx_reset_stats": (C.c_int, [vp]),
+    "fheon_timer_arm": (C.c_int, [vp, C.c_int]),
+    "fheon_timer_read": (C.c_int, [vp, dp, C.POINTER(C.c_int)]),
     "fheon_set_tracing": (C.c_int, [vp, C.c_int]),
     "fheon_trace": (C.c_int, [vp, lp, C.c_size_t, szp]),
     "fheon_trace_clear": (C.c_int, [vp]),

@@ -279,13 +279,22 @@ class SlotContext:
         _check(_native.lib().fheon_ctx_sync(self._h))
 
     def stats(self) -> Dict[str, int]:
-        a = np.zeros(8, np.uint64)
+        a = np.zeros(9, np.uint64)
         _check(_native.lib().fheon_ctx_stats(self._h, _u64ptr(a)))
-        keys = ["rotations", "keyswitches", "mult_plain", "mult_cipher", "rescales", "ntt_limbs", "encodes", "adds"]
+        keys = ["rotations", "keyswitches", "mult_plain", "mult_cipher", "rescales", "ntt_limbs", "encodes", "adds",
+                "launches"]
         return {k: int(v) for k, v in zip(keys, a)}
 
     def reset_stats(self):
         _check(_native.lib().fheon_ctx_reset_stats(self._h))
+
+    def timer_arm(self, kernel_class: int):
+        _check(_native.lib().fheon_timer_arm(self._h, int(kernel_class)))
+
+    def timer_read(self):
+        ms, n = C.c_double(), C.c_int()
+        _check(_native.lib().fheon_timer_read(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def microbench(self, kind: int, batch: int, limbs: int, n_rot: int = 1, iters: int = 10) -> float:
         ms = C.c_double()
@@ -371,8 +380,12 @@ class SlotVector:
         _check(_native.lib().fheon_decrypt(self._ctx._h, self._h, _dptr(out), out.size))
         return out
 
-    def words(self) -> np.ndarray:
-        out = np.zeros((2, self.limbs(), self._ctx.N), np.uint64)
+    def words(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        shape = (2, self.limbs(), self._ctx.N)
+        if out is None:
+            out = np.zeros(shape, np.uint64)
+        elif out.shape != shape or out.dtype != np.uint64 or not out.flags.c_contiguous:
+            raise ShapeError(f"output buffer must be a contiguous uint64 array of shape {shape}", 2)
         _check(_native.lib().fheon_ct_download(self._ctx._h, self._h, _u64ptr(out)))
         return out
 
@@ -640,6 +653,31 @@ def pad_input(x: PackedTensor, padding: int) -> PackedTensor:
         return x
     v = _wrap(x.data._ctx, _native.lib().fheon_pad_input, x.data._h, x.channels, x.width, padding)
     return PackedTensor(v, x.channels, x.width + 2 * padding)
+
+
+def host_primes(config: ContextConfig):
+    """Prime chain and per-level scale targets, computed on the host (no GPU needed)."""
+    p = config.params()
+    primes = np.zeros(p.limbs + p.special_limbs, np.uint64)
+    scales = np.zeros(p.limbs, np.float64)
+    _check(_native.lib().fheon_host_primes(C.byref(p), _u64ptr(primes), _dptr(scales)))
+    return primes, scales
+
+
+def host_encode(config: ContextConfig, values, scale: float) -> np.ndarray:
+    """Canonical-embedding encode on the host -> N signed integer coefficients."""
+    p = config.params()
+    v = np.ascontiguousarray(values, np.float64)
+    out = np.zeros(config.ring_dimension, np.int64)
+    _check(_native.lib().fheon_host_encode(C.byref(p), _dptr(v), v.size, float(scale),
+                                           out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
+
+
+def cheb_relu_coefficients(beta: float, degree: int) -> np.ndarray:
+    out = np.zeros(degree + 1, np.float64)
+    _check(_native.lib().fheon_cheb_relu_coefficients(float(beta), int(degree), _dptr(out)))
+    return out
 
 
 def conv_depth_cost(cfg: ConvConfig, W_in: int) -> int:

@@ -51,6 +51,57 @@ const char* fheon_last_error(void) { return g_err.c_str(); }
 int fheon_last_error_kind(void) { return g_kind; }
 int fheon_version(void) { return 1; }
 
+static fheon::Params to_params(const fheon_params* p) {
+  fheon::Params prm;
+  prm.logN = p->log_n;
+  prm.L = p->limbs;
+  prm.K = p->special_limbs;
+  prm.dnum = p->dnum;
+  prm.first_bits = p->first_mod_bits;
+  prm.scale_bits = p->scale_bits;
+  prm.special_bits = p->special_bits;
+  prm.depth_budget = p->depth_budget;
+  prm.seed = p->seed;
+  return prm;
+}
+
+int fheon_host_primes(const fheon_params* p, uint64_t* primes, double* scales) {
+  return guard([&] {
+    need(p, "params");
+    fheon::HostTables h;
+    try {
+      h = fheon::make_tables(to_params(p));
+    } catch (const std::invalid_argument& e) {
+      throw fheon::Error(fheon::ErrKind::shape, e.what());
+    }
+    if (primes)
+      for (std::size_t i = 0; i < h.q.size(); ++i) primes[i] = h.q[i];
+    if (scales)
+      for (std::size_t i = 0; i < h.T.size(); ++i) scales[i] = h.T[i];
+  });
+}
+
+int fheon_host_encode(const fheon_params* p, const double* values, size_t n, double scale, int64_t* coeffs) {
+  return guard([&] {
+    need(p, "params");
+    fheon::HostTables h;
+    try {
+      h = fheon::make_tables(to_params(p));
+    } catch (const std::invalid_argument& e) {
+      throw fheon::Error(fheon::ErrKind::shape, e.what());
+    }
+    fheon::encode_coeffs_host(h, values, n, scale, reinterpret_cast<long long*>(coeffs));
+  });
+}
+
+int fheon_cheb_relu_coefficients(double beta, int degree, double* coeffs) {
+  return guard([&] {
+    const auto f = [beta](double z) { return z < 0.0 ? 0.0 : beta * z; };
+    const std::vector<double> c = fheon::cheb_coefficients(f, degree);
+    std::copy(c.begin(), c.end(), coeffs);
+  });
+}
+
 int fheon_ctx_create(const fheon_params* p, fheon_ctx** out) {
   return guard([&] {
     need(p, "params");
@@ -111,10 +162,20 @@ int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* o) {
     o[5] = s.ntt_limbs;
     o[6] = s.encodes;
     o[7] = s.adds;
+    o[8] = fheon::g_kernel_launches.load();
   });
 }
 int fheon_ctx_reset_stats(fheon_ctx* ctx) {
   return guard([&] { ctx->impl->stats = fheon::OpStats{}; });
+}
+int fheon_timer_arm(fheon_ctx* ctx, int kernel_class) {
+  return guard([&] {
+    ctx->impl->timer.cls = kernel_class;
+    ctx->impl->timer.reset();
+  });
+}
+int fheon_timer_read(fheon_ctx* ctx, double* total_ms, int* count) {
+  return guard([&] { *total_ms = ctx->impl->timer.total_ms(count); });
 }
 
 int fheon_set_tracing(fheon_ctx* ctx, int on) {

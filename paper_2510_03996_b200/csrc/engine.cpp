@@ -2,6 +2,7 @@
 // trace.  See engine.hpp.
 #include "engine.hpp"
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 
@@ -27,12 +28,54 @@ void cuda_check(cudaError_t e, const char* what) {
   }
 }
 
+std::atomic<std::uint64_t> g_kernel_launches{0};
+
 void launch_check(const char* what) {
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Error(ErrKind::cuda, std::string("kernel launch failed: ") + what + ": " + cudaGetErrorString(e));
   }
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// ------------------------------------------------------------- kernel timer
+KernelTimer::~KernelTimer() {
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+}
+void KernelTimer::begin(cudaStream_t st) {
+  if (depth++ > 0) return;
+  if (used + 2 > ev.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      FHEON_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+  }
+  FHEON_CUDA(cudaEventRecord(ev[used], st));
+}
+void KernelTimer::end(cudaStream_t st) {
+  if (--depth > 0) return;
+  FHEON_CUDA(cudaEventRecord(ev[used + 1], st));
+  used += 2;
+}
+double KernelTimer::total_ms(int* count) {
+  double tot = 0.0;
+  for (std::size_t i = 0; i + 1 < used; i += 2) {
+    FHEON_CUDA(cudaEventSynchronize(ev[i + 1]));
+    float ms = 0.f;
+    FHEON_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+    tot += ms;
+  }
+  if (count) *count = (int)(used / 2);
+  return tot;
+}
+
+TimedScope::TimedScope(const DevTables& t_, int c, cudaStream_t s) : t(t_), cls(c), st(s) {
+  if (t.timer && t.timer->cls == cls) t.timer->begin(st);
+}
+TimedScope::~TimedScope() {
+  if (t.timer && t.timer->cls == cls) t.timer->end(st);
 }
 
 // ------------------------------------------------------------- buffers
@@ -146,6 +189,7 @@ void Context::build_device_tables() {
   t.K = K;
   t.dnum = dnum;
   t.alpha = alpha;
+  t.timer = &timer;
 
   std::vector<PrimeConst> pcs(NP);
   for (int i = 0; i < NP; ++i) {
@@ -346,6 +390,10 @@ void Context::gen_key(u64 key_id) {
 
 // ------------------------------------------------------------- encoder
 void Context::encode_coeffs(const double* vals, std::size_t n, double scale, long long* coeffs) const {
+  encode_coeffs_host(ht_, vals, n, scale, coeffs);
+}
+
+void encode_coeffs_host(const HostTables& ht_, const double* vals, std::size_t n, double scale, long long* coeffs) {
   const int S = ht_.S;
   if (n > (std::size_t)S) throw Error(ErrKind::capacity, "payload exceeds the slot count");
   const u64 M = 2 * (u64)ht_.N;

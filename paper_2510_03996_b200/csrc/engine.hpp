@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -50,6 +51,7 @@ struct Error : std::runtime_error {
 };
 
 void cuda_check(cudaError_t e, const char* what);
+extern std::atomic<std::uint64_t> g_kernel_launches;
 #define FHEON_CUDA(x) ::fheon::cuda_check((x), #x)
 
 class Context;
@@ -87,7 +89,20 @@ struct TraceEvent {
 
 struct OpStats {
   std::uint64_t rotations = 0, keyswitches = 0, mult_plain = 0, mult_cipher = 0, rescales = 0, ntt_limbs = 0,
-                encodes = 0, adds = 0;
+                encodes = 0, adds = 0, launches = 0;
+};
+
+struct KernelTimer {
+  int cls = 0;  // armed class (0 = off)
+  std::vector<cudaEvent_t> ev;
+  std::size_t used = 0;
+  int depth = 0;
+  ~KernelTimer();
+  void begin(cudaStream_t st);
+  void end(cudaStream_t st);
+  // total milliseconds and number of timed scopes since the last reset (synchronises)
+  double total_ms(int* count);
+  void reset() { used = 0; depth = 0; }
 };
 
 class Context {
@@ -134,6 +149,7 @@ class Context {
   void clear_trace();
 
   OpStats stats;
+  KernelTimer timer;
   std::uint64_t enc_counter = 0;
 
   // staging for host -> device copies of encoded coefficients
@@ -157,6 +173,9 @@ class Context {
   cudaEvent_t staging_ev_[kStaging] = {};
   int staging_next_ = 0;
 };
+
+// canonical-embedding encode on the host (special FFT)
+void encode_coeffs_host(const HostTables& h, const double* vals, std::size_t n, double scale, long long* coeffs);
 
 // ---------------------------------------------------------------- ops
 Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n);            // at the depth budget

@@ -11,8 +11,15 @@
 
 namespace fheon {
 
-// Throws fheon::Error on a launch-configuration error (no device sync).
+// Throws fheon::Error on a launch-configuration error (no device sync);
+// also counts launches (OpStats::launches).
 void launch_check(const char* what);
+
+// Live per-kernel-class timing with CUDA events on the launching stream
+// (bench.py roofline).  Classes: 1 key-switch inner product, 2 NTT/iNTT
+// (both phases), 3 ModUp basis conversion, 4 ModDown conversion.
+struct KernelTimer;
+enum KernelClass { kKsInner = 1, kNtt = 2, kModUp = 3, kModDown = 4 };
 
 // Device-resident constant tables of one context (built in engine.cpp).
 struct DevTables {
@@ -33,6 +40,18 @@ struct DevTables {
   u64* rs = nullptr;
   // secret key, NTT domain standard form [L+K][N]
   u64* s_ntt = nullptr;
+  // optional live kernel timer (owned by the Context)
+  KernelTimer* timer = nullptr;
+};
+
+// RAII scope: records a start/stop event pair around the enclosed launches
+// when the context's timer is armed for class `cls`.
+struct TimedScope {
+  const DevTables& t;
+  int cls;
+  cudaStream_t st;
+  TimedScope(const DevTables& t_, int c, cudaStream_t s);
+  ~TimedScope();
 };
 
 constexpr int kMaxAlpha = 16;

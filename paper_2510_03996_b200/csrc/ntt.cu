@@ -178,12 +178,14 @@ void dispatch(const DevTables& t, const LimbSet& set, cudaStream_t st) {
 
 void ntt_forward(const DevTables& t, const LimbSet& set, cudaStream_t st) {
   if (set.count() == 0) return;
+  TimedScope ts(t, kNtt, st);
   dispatch<false, true>(t, set, st);
   dispatch<false, false>(t, set, st);
 }
 
 void ntt_inverse(const DevTables& t, const LimbSet& set, cudaStream_t st) {
   if (set.count() == 0) return;
+  TimedScope ts(t, kNtt, st);
   dispatch<true, false>(t, set, st);
   dispatch<true, true>(t, set, st);
 }

@@ -311,17 +311,19 @@ void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int 
 
 void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st) {
   const int beta = (limbs + t.alpha - 1) / t.alpha;
-  if (beta < 2 && t.K == 0) return;
+  TimedScope ts(t, kModUp, st);
   k_modup_bconv<<<grid_for(t.N, beta, x.n), kThreads, 0, st>>>(ext, x, t.pc, t.modup_qhinv, t.modup_qhat, t.logN,
                                                                   limbs, t.L, t.K, t.dnum, t.alpha);
 }
 void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.n == 0) return;
+  TimedScope ts(t, kKsInner, st);
   k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K, t.alpha);
   launch_check("k_ks_inner");
 }
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
   if (conv.n == 0) return;
+  TimedScope ts(t, kModDown, st);
   k_moddown_conv<<<grid_for(t.N, 1, conv.n), kThreads, 0, st>>>(conv, z, t.pc, t.md_pk, t.md_pinv, t.md_phat,
                                                                   t.md_q, t.logN, limbs, t.L, t.K);
 }

@@ -1,0 +1,153 @@
+"""CPU tests: the reference oracle, golden fixtures, host-side engine logic
+(prime chain, encoder, Chebyshev coefficients, depth costs) and the C ABI
+surface -- no device compute is invoked.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2510_03996_b200 as fh
+from paper_2510_03996_b200 import _native
+from oracle import ref as sref
+from oracle.ckks_oracle import Oracle
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+need_ref = pytest.mark.skipif(not sref.available(), reason="oracle/_ref not built")
+
+
+def _ev(events):
+    kinds = {"rotation": 0, "mult_plain": 1, "mult_cipher": 2, "bootstrap": 3}
+    return np.array([(kinds[k], v) for k, v in events], dtype=np.int64).reshape(-1, 2)
+
+
+# ------------------------------------------------------------ C ABI surface
+def test_library_exports_every_header_symbol():
+    lib = _native.lib()
+    syms = _native.header_symbols()
+    assert len(syms) >= 50
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in include/fheon_b200.h but not exported"
+    assert set(syms) <= set(_native.SIGNATURES), "ctypes signatures missing for some header symbols"
+
+
+def test_no_cpu_fallback_without_device():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("device present")
+    except ImportError:
+        pass
+    with pytest.raises(fh.CudaError, match="no CUDA device"):
+        fh.SlotContext(fh.ContextConfig.preset("config1"))
+
+
+# ------------------------------------------------------------ host logic
+@pytest.mark.parametrize("preset,logn", [("config1", 14), ("config2", 16)])
+def test_host_prime_chain_matches_oracle(preset, logn):
+    cfg = fh.ContextConfig.preset(preset)
+    primes, scales = fh.api.host_primes(cfg)
+    c = cfg.crypto
+    o = Oracle(logn, cfg.limbs, cfg.special_limbs, c.key_switch_digits, c.first_modulus_bits, c.rescale_bits,
+               cfg.special_bits, 1)
+    assert np.array_equal(primes, o.primes)
+    assert np.array_equal(scales, o.T)
+
+
+def test_host_encoder_matches_oracle_bit_exact():
+    cfg = fh.ContextConfig(4096, 2048, 5, fh.CryptoMetadata(50, 40, 3), limbs=6, special_limbs=2)
+    o = Oracle(12, 6, 2, 3, 50, 40, 60, 1)
+    rng = np.random.default_rng(0)
+    for n in (2048, 100, 1):
+        v = rng.uniform(-3, 3, n)
+        assert np.array_equal(fh.api.host_encode(cfg, v, 2.0 ** 40), o.encode_coeffs(v, 2.0 ** 40))
+
+
+def test_parameter_validation():
+    bad = fh.ContextConfig(4096, 2048, 13, fh.CryptoMetadata(50, 40, 3), limbs=14, special_limbs=1)
+    with pytest.raises(fh.ShapeError):
+        fh.api.host_primes(fh.ContextConfig(4096, 1000, 5))
+    # engine-side checks (P must dominate every digit) happen at context creation; host tables still build
+    fh.api.host_primes(bad)
+
+
+@need_ref
+@pytest.mark.parametrize("beta,degree", [(1.0, 59), (8.0, 59), (1.0, 7), (3.5, 27)])
+def test_cheb_coefficients_bit_exact_vs_reference(beta, degree):
+    assert np.array_equal(fh.api.cheb_relu_coefficients(beta, degree), sref.cheb_relu_coefficients(beta, degree))
+
+
+def test_relu_epsilon59_frozen_bound():
+    """Reference fixture proj/tests/data/relu_epsilon59.json (acceptance criterion 5)."""
+    fx = json.load(open(os.path.join(GOLDEN, "relu_epsilon59.json")))
+    c = fh.api.cheb_relu_coefficients(1.0, fx["degree"])
+    z = np.linspace(-1, 1, fx["grid_points"])
+    # Clenshaw evaluation of the series
+    b1 = np.zeros_like(z)
+    b2 = np.zeros_like(z)
+    for d in range(len(c) - 1, 0, -1):
+        b1, b2 = c[d] + 2 * z * b1 - b2, b1
+    p = c[0] + z * b1 - b2
+    err = np.abs(p - np.maximum(z, 0))
+    assert err.max() <= fx["sup_norm"]
+    assert err[np.abs(z) >= fx["deadzone"]].max() <= fx["epsilon_59"]
+
+
+@pytest.mark.parametrize("C,F,k,S,P,mode,variant,W", [(1, 6, 5, 1, 0, 0, 0, 28), (3, 4, 3, 1, 1, 1, 0, 8),
+                                                       (2, 4, 2, 2, 0, 0, 1, 8), (2, 4, 3, 1, 1, 0, 0, 6),
+                                                       (2, 4, 2, 2, 0, 2, 0, 8)])
+def test_conv_depth_cost_matches_reference(C, F, k, S, P, mode, variant, W):
+    got = fh.conv_depth_cost(fh.ConvConfig(C, F, k, S, P, fh.ConvMode(mode), fh.StrideVariant(variant)), W)
+    if sref.available():
+        assert got == sref.conv_depth_cost(C, F, k, S, P, mode, variant, W)
+    assert got >= 2
+
+
+# ------------------------------------------------------------ reference oracle + golden
+@need_ref
+def test_reference_reproduces_golden_config1():
+    g = np.load(os.path.join(GOLDEN, "conv_config1.npz"))
+    r = sref.Ref(16384, 8192, 10).convolution(g["x"], 10, 1, 28, 6, 5, 1, 0, 0, 0, g["w"], None)
+    assert np.array_equal(r.slots[: 6 * 24 * 24], g["out"])
+    assert r.level == int(g["level"]) == 7
+    assert np.array_equal(_ev(r.events), g["events"])
+    rots = [v for k, v in r.events if k == "rotation"]
+    assert len(rots) == 305 and len(set(rots)) == 52
+
+
+@need_ref
+def test_reference_golden_small_layers():
+    r = sref.Ref(4096, 2048, 13)
+    g = np.load(os.path.join(GOLDEN, "special3x3_small.npz"))
+    res = r.convolution(g["x"], 13, 3, 8, 4, 3, 1, 1, 1, 0, g["w"], g["b"])
+    assert np.array_equal(res.slots, g["out"]) and np.array_equal(_ev(res.events), g["events"])
+    g = np.load(os.path.join(GOLDEN, "relu59_beta8_small.npz"))
+    res = r.secure_relu(g["x"], 13, 8.0, 59, 40)
+    assert np.array_equal(res.slots, g["out"]) and res.level == int(g["level"])
+
+
+@need_ref
+def test_oracle_ops_agree_with_reference_simulator():
+    """Decrypted-level parity of the CPU CKKS oracle with slotcnn's backend ops
+    (rotation direction, mult_plain, mult_cipher, add; backend.cpp:165-231)."""
+    o = Oracle(12, 6, 2, 3, 50, 40, 60, 3)
+    r = sref.Ref(4096, 2048, 5)
+    rng = np.random.default_rng(12)
+    a, b = rng.uniform(-1, 1, o.S), rng.uniform(-1, 1, o.S)
+    ca, cb = o.encrypt(a, 0), o.encrypt(b, 1)
+    for t in (1, -3, 100):
+        want = r.backend_op(0, a, 5, t=t)
+        got = o.decrypt(o.rotate(ca, t, o.rotation_key(t)), o.T[-1])
+        assert np.abs(got - want.slots).max() < 1e-6 and want.level == 5
+    want = r.backend_op(3, a, 5, b=b)
+    mp, s = o.mult_plain(ca, o.T[-1], b)
+    assert np.abs(o.decrypt(mp, s) - want.slots).max() < 1e-6 and want.level == mp.shape[1] - 1
+    want = r.backend_op(4, a, 5, b=b, level_b=5)
+    mc = o.mult_cipher(ca, cb, o.relin_key())
+    assert np.abs(o.decrypt(mc, o.T[-1] ** 2 / float(o.primes[5])) - want.slots).max() < 1e-6
+    assert want.level == mc.shape[1] - 1
+    want = r.backend_op(1, a, 5, b=b, level_b=3)
+    cb3, s3 = o.level_down(cb, o.T[-1], 4)
+    ca3, _ = o.level_down(ca, o.T[-1], 4)
+    assert np.abs(o.decrypt(o.add(ca3, cb3), s3) - want.slots).max() < 1e-6 and want.level == 3
