@@ -115,6 +115,9 @@ int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);
 int fheon_rotate(fheon_ctx* ctx, const fheon_ct* x, long t, fheon_ct** out);
 /* hoisted rotation set sharing one ModUp of x (layers_conv.cpp:102-113 tap_rotations) */
 int fheon_rotate_hoisted(fheon_ctx* ctx, const fheon_ct* x, const long* ts, size_t n, fheon_ct** outs);
+/* batch: xs[i] rotated by ts[i] in one key-switch pipeline (distinct inputs batched,
+ * repeated inputs hoisted); trace events in call order */
+int fheon_rotate_many(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, size_t n, fheon_ct** outs);
 int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_sub(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_add_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, size_t n, fheon_ct** out);

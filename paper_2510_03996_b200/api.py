@@ -432,6 +432,21 @@ def rotate_hoisted(v: SlotVector, ts: Sequence[int]) -> List[SlotVector]:
     return [SlotVector(v._ctx, C.c_void_p(outs[i])) for i in range(n)]
 
 
+def rotate_many(xs: Sequence[SlotVector], ts: Sequence[int]) -> List[SlotVector]:
+    """xs[i] rotated by ts[i] in one batched key-switch pipeline."""
+    n = len(xs)
+    if n != len(ts):
+        raise ShapeError("rotate_many: xs and ts differ in length", 2)
+    if n == 0:
+        return []
+    ctx = xs[0]._ctx
+    hs = (C.c_void_p * n)(*[x._h.value if isinstance(x._h, C.c_void_p) else x._h for x in xs])
+    arr = (C.c_long * n)(*[int(t) for t in ts])
+    outs = (C.c_void_p * n)()
+    _check(_native.lib().fheon_rotate_many(ctx._h, hs, arr, n, outs))
+    return [SlotVector(ctx, C.c_void_p(outs[i])) for i in range(n)]
+
+
 def add(a: SlotVector, b: SlotVector) -> SlotVector:
     return _wrap(a._ctx, _native.lib().fheon_add, a._h, b._h)
 

@@ -272,6 +272,18 @@ int fheon_rotate_hoisted(fheon_ctx* ctx, const fheon_ct* x, const long* ts, size
     for (size_t i = 0; i < n; ++i) outs[i] = wrap(r[i]);
   });
 }
+int fheon_rotate_many(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, size_t n, fheon_ct** outs) {
+  return guard([&] {
+    std::vector<fheon::Ciphertext> in;
+    in.reserve(n);
+    for (size_t i = 0; i < n; ++i) {
+      need(xs[i], "ciphertext");
+      in.push_back(xs[i]->ct);
+    }
+    std::vector<fheon::Ciphertext> r = fheon::rotate_many(*ctx->impl, in, std::vector<long>(ts, ts + n));
+    for (size_t i = 0; i < n; ++i) outs[i] = wrap(r[i]);
+  });
+}
 int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::add(*ctx->impl, a->ct, b->ct)); });
 }

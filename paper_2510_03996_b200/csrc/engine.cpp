@@ -221,10 +221,10 @@ void Context::build_device_tables() {
     u64* base = tw.data() + (std::size_t)i * 4 * N;
     for (std::size_t k = 0; k < N; ++k) {
       const unsigned e = bitrev((unsigned)k, p.logN);
-      base[k] = pw[e];
-      base[N + k] = shoup(pw[e], qi);
-      base[2 * N + k] = ipw[e];
-      base[3 * N + k] = shoup(ipw[e], qi);
+      base[2 * k] = pw[e];  // (value, Shoup) pairs: one 16-byte load per twiddle
+      base[2 * k + 1] = shoup(pw[e], qi);
+      base[2 * N + 2 * k] = ipw[e];
+      base[2 * N + 2 * k + 1] = shoup(ipw[e], qi);
     }
   }
   t.tw = upload(dev_allocs_, tw, stream_);

@@ -184,6 +184,8 @@ void decrypt(Context& ctx, const Ciphertext& ct, double* out);                  
 Ciphertext rotate(Context& ctx, const Ciphertext& x, long t);
 std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& ts);
 std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t);
+// xs[i] rotated by ts[i]: one batched key-switch pipeline, shared ModUp for repeated inputs
+std::vector<Ciphertext> rotate_many(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<long>& ts);
 Ciphertext add(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext sub(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext add_plain(Context& ctx, const Ciphertext& a, const double* vals, std::size_t n);

@@ -3,6 +3,7 @@
 // here synchronises except decrypt/download.
 #include <cmath>
 #include <cstring>
+#include <map>
 
 #include "engine.hpp"
 
@@ -54,33 +55,54 @@ void check_scales(const Ciphertext& a, const Ciphertext& b, const char* op) {
                                        std::to_string(b.scale) + ")");
 }
 
-// Hybrid key switch of `d` ([limbs][N], NTT domain) against `jobs` keys.
-// Output r: c0 = ModDown(acc0) + sigma_{g_r}(add0) (add0 may be null),
-//           c1 = ModDown(acc1) + add1 (may be null)
+// Hybrid key switch of several NTT-domain inputs d_i ([limbs][N] each).  Job r
+// switches input `in` under key `key_id` with automorphism g (hoisting: jobs
+// sharing an input share its ModUp).  Output r:
+//   c0 = ModDown(acc0) + sigma_{add0_g}(add0)   (add0 may be null)
+//   c1 = ModDown(acc1) + add1                   (add1 may be null)
 struct KsJob {
   u64 key_id;
   u64 g;
   const u64* add0;
   u64 add0_g;
   const u64* add1;
+  int in = 0;
 };
 
-std::vector<Ciphertext> keyswitch(Context& ctx, const u64* d, int limbs, const std::vector<KsJob>& jobs) {
+std::vector<Ciphertext> keyswitch(Context& ctx, const std::vector<const u64*>& inputs, int limbs,
+                                  const std::vector<KsJob>& jobs) {
   const DevTables& t = ctx.dev();
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
   const int L = ctx.L(), K = ctx.K(), E = limbs + K;
   const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const int nin = (int)inputs.size();
   ctx.stats.keyswitches += jobs.size();
 
-  // ModUp (shared by every job: hoisting)
-  BufPtr xc = ctx.alloc((std::size_t)limbs * N);
-  FHEON_CUDA(cudaMemcpyAsync(xc->ptr, d, (std::size_t)limbs * N * sizeof(u64), cudaMemcpyDeviceToDevice, st));
-  ntt_inverse(t, limbset(xc->ptr, 1, 0, limbs, limbs, L), st);
-  BufPtr ext = ctx.alloc((std::size_t)beta * E * N);
-  modup_bconv(t, plist({ext->ptr}), plist({xc->ptr}), limbs, st);
-  ntt_forward(t, limbset(ext->ptr, beta, (std::size_t)E * N, E, limbs, L, 0, t.alpha), st);
-  ctx.stats.ntt_limbs += (std::size_t)limbs + (std::size_t)beta * (E - t.alpha);
+  // ModUp of every input, batched (one pipeline of launches per 32 inputs)
+  const std::size_t ext_words = (std::size_t)beta * E * N;
+  BufPtr xc = ctx.alloc((std::size_t)nin * limbs * N);
+  BufPtr ext = ctx.alloc((std::size_t)nin * ext_words);
+  for (int i0 = 0; i0 < nin; i0 += kMaxBases) {
+    const int ni = std::min(kMaxBases, nin - i0);
+    LimbSet dst = limbset(xc->ptr + (std::size_t)i0 * limbs * N, ni, (std::size_t)limbs * N, limbs, limbs, L);
+    LimbSet src = dst;
+    src.nbase = ni;
+    src.blocks_per_base = 1;
+    for (int i = 0; i < ni; ++i) src.base[i] = const_cast<u64*>(inputs[i0 + i]);
+    ntt_inverse(t, dst, st, &src);  // out of place: c1 stays untouched
+    PolyList xl{}, el{};
+    xl.n = el.n = ni;
+    for (int i = 0; i < ni; ++i) {
+      xl.p[i] = xc->ptr + (std::size_t)(i0 + i) * limbs * N;
+      el.p[i] = ext->ptr + (std::size_t)(i0 + i) * ext_words;
+    }
+    modup_bconv(t, el, xl, limbs, st);
+    ntt_forward(t, limbset(ext->ptr + (std::size_t)i0 * ext_words, ni * beta, (std::size_t)E * N, E, limbs, L, 0,
+                           t.alpha),
+                st);
+  }
+  ctx.stats.ntt_limbs += (std::size_t)nin * ((std::size_t)limbs + (std::size_t)beta * (E - t.alpha));
 
   std::vector<const u64*> keys(jobs.size());
   for (std::size_t r = 0; r < jobs.size(); ++r) keys[r] = ctx.key(jobs[r].key_id);
@@ -94,9 +116,10 @@ std::vector<Ciphertext> keyswitch(Context& ctx, const u64* d, int limbs, const s
     KsJobs kj{};
     kj.n = R;
     for (int r = 0; r < R; ++r) {
+      const int in = jobs[r0 + r].in;
       kj.key[r] = keys[r0 + r];
-      kj.ext[r] = ext->ptr;
-      kj.d[r] = d;
+      kj.ext[r] = ext->ptr + (std::size_t)in * ext_words;
+      kj.d[r] = inputs[in];
       kj.acc[r] = acc->ptr + (std::size_t)r * 2 * E * N;
       kj.g[r] = jobs[r0 + r].g;
     }
@@ -253,47 +276,70 @@ Ciphertext rotate(Context& ctx, const Ciphertext& x, long t) {
   return rotate_hoisted(ctx, x, std::vector<long>{t})[0];
 }
 
-std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& ts) {
-  require_valid(x, "rotate");
+// Rotation i: xs[i] by ts[i].  Distinct inputs are key-switched in one batched
+// pipeline; repeated inputs share their ModUp (hoisting).  Trace events are
+// recorded in call order, exactly as sequential rotate() calls would.
+std::vector<Ciphertext> rotate_many(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<long>& ts) {
+  if (xs.size() != ts.size()) throw Error(ErrKind::internal, "rotate_many: size mismatch");
   const long S = ctx.S();
-  for (long t : ts)
-    if (t <= -S || t >= S)
+  for (std::size_t i = 0; i < ts.size(); ++i) {
+    require_valid(xs[i], "rotate");
+    if (ts[i] <= -S || ts[i] >= S)
       throw Error(ErrKind::invalid_rotation,
-                  "rotation amount " + std::to_string(t) + " out of range for " + std::to_string(S) + " slots");
+                  "rotation amount " + std::to_string(ts[i]) + " out of range for " + std::to_string(S) + " slots");
+  }
   std::vector<Ciphertext> outs(ts.size());
-  std::vector<KsJob> jobs;
-  std::vector<std::size_t> where;
+  // group by level; within a level, dedupe inputs by their c1 pointer
+  std::map<int, std::vector<std::size_t>> by_level;
   for (std::size_t i = 0; i < ts.size(); ++i) {
     ctx.record(0, ts[i]);
     ctx.stats.rotations++;
-    const u64 g = ctx.galois(ts[i]);
-    if (g == 1) {
-      outs[i] = x;
+    if (ctx.galois(ts[i]) == 1) {
+      outs[i] = xs[i];
       outs[i].id = ctx.next_id();
       continue;
     }
-    jobs.push_back({g, g, x.c0, g, nullptr});
-    where.push_back(i);
+    by_level[xs[i].limbs].push_back(i);
   }
-  if (!jobs.empty()) {
-    std::vector<Ciphertext> r = keyswitch(ctx, x.c1, x.limbs, jobs);
+  for (auto& [limbs, idx] : by_level) {
+    std::vector<const u64*> inputs;
+    std::map<const u64*, int> slot;
+    std::vector<KsJob> jobs;
+    for (std::size_t i : idx) {
+      const Ciphertext& x = xs[i];
+      auto it = slot.find(x.c1);
+      int in;
+      if (it == slot.end()) {
+        in = (int)inputs.size();
+        slot[x.c1] = in;
+        inputs.push_back(x.c1);
+      } else {
+        in = it->second;
+      }
+      const u64 g = ctx.galois(ts[i]);
+      KsJob jb{g, g, x.c0, g, nullptr};
+      jb.in = in;
+      jobs.push_back(jb);
+    }
+    std::vector<Ciphertext> r = keyswitch(ctx, inputs, limbs, jobs);
     for (std::size_t k = 0; k < r.size(); ++k) {
-      r[k].scale = x.scale;
-      outs[where[k]] = r[k];
+      r[k].scale = xs[idx[k]].scale;
+      outs[idx[k]] = r[k];
     }
   }
   return outs;
 }
 
+std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& ts) {
+  return rotate_many(ctx, std::vector<Ciphertext>(ts.size(), x), ts);
+}
+
 std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t) {
-  std::vector<Ciphertext> outs;
-  outs.reserve(xs.size());
-  for (const Ciphertext& x : xs) outs.push_back(rotate(ctx, x, t));
-  return outs;
+  return rotate_many(ctx, xs, std::vector<long>(xs.size(), t));
 }
 
 Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d, u64 key_id, u64 g) {
-  std::vector<Ciphertext> r = keyswitch(ctx, d.c1, d.limbs, {{key_id, g, nullptr, 1, nullptr}});
+  std::vector<Ciphertext> r = keyswitch(ctx, {d.c1}, d.limbs, {{key_id, g, nullptr, 1, nullptr}});
   r[0].scale = d.scale;
   return r[0];
 }
@@ -409,7 +455,7 @@ Ciphertext mult_cipher(Context& ctx, const Ciphertext& a0, const Ciphertext& b0)
   u64* d1 = d0 + (std::size_t)l * N;
   u64* d2 = d1 + (std::size_t)l * N;
   ew_tensor(ctx.dev(), d0, d1, d2, a.c0, a.c1, b.c0, b.c1, l, ctx.stream());
-  std::vector<Ciphertext> r = keyswitch(ctx, d2, l, {{0, 1, d0, 1, d1}});
+  std::vector<Ciphertext> r = keyswitch(ctx, {d2}, l, {{0, 1, d0, 1, d1}});
   Ciphertext out = rescale(ctx, r[0]);
   out.scale = a.scale * b.scale / (double)ctx.host().q[l - 1];
   ctx.stats.mult_cipher++;

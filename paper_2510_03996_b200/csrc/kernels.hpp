@@ -67,8 +67,10 @@ struct PolyList {
 };
 
 // ---- NTT (batched over every limb-polynomial of the set)
-void ntt_forward(const DevTables& t, const LimbSet& set, cudaStream_t st);
-void ntt_inverse(const DevTables& t, const LimbSet& set, cudaStream_t st);
+// `src` (optional, same shape and primes): out-of-place -- the first phase reads
+// src and writes `set`, the second phase runs in place on `set`.
+void ntt_forward(const DevTables& t, const LimbSet& set, cudaStream_t st, const LimbSet* src = nullptr);
+void ntt_inverse(const DevTables& t, const LimbSet& set, cudaStream_t st, const LimbSet* src = nullptr);
 
 // ---- elementwise over the polys of a list, `limbs` limbs each, primes 0..limbs-1
 void ew_add(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& b, int limbs, cudaStream_t st);

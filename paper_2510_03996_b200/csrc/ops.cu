@@ -2,6 +2,7 @@
 // (ModUp basis conversion, key inner product, ModDown), rescale, and the
 // encrypt / keygen / decrypt helpers.  Definitions: DESIGN.md section 3
 // (mirrored by oracle/ckks_oracle.c, which these must match bit for bit).
+#include <algorithm>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -66,37 +67,51 @@ __global__ void k_automorph(PolyList out, PolyList in, int logN) {
 }
 
 // ------------------------------------------------------------ key switching
-// grid (N/256, beta, npolys)
-__global__ void k_modup_bconv(PolyList ext, PolyList x, const PrimeConst* __restrict__ pc,
-                              const u64* __restrict__ qhinv, const u64* __restrict__ qhat, int logN, int limbs,
-                              int L, int K, int dnum, int alpha) {
+// ModUp basis conversion for one digit j with A = |D_j| limbs (compile time).
+// grid (N/256, ceil((E - A) / kTC), npolys): each CTA converts a chunk of kTC
+// target limbs; the chunk's constants [Q_j/q_i]_t (Montgomery) sit in smem.
+constexpr int kTC = 8;
+template <int A>
+__global__ void __launch_bounds__(256) k_modup_bconv(PolyList ext, PolyList x, const PrimeConst* __restrict__ pc,
+                                                     const u64* __restrict__ qhinv, const u64* __restrict__ qhat,
+                                                     int logN, int limbs, int L, int K, int dnum, int alpha, int j) {
+  __shared__ u64 cs[kTC][A];
+  __shared__ u64 tq[kTC][2];
+  __shared__ int tdst[kTC];
   const std::size_t N = (std::size_t)1 << logN;
   const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y;
   const int lo = j * alpha;
-  const int hi = min(lo + alpha, limbs);
-  const int a = hi - lo;
   const int E = limbs + K;
   const int tab = (limbs - 1) * dnum + j;
-  const u64* xin = x.p[blockIdx.z];
-  u64* out = ext.p[blockIdx.z] + (std::size_t)j * E * N;
-  u64 y[kMaxAlpha];
-#pragma unroll
-  for (int i = 0; i < kMaxAlpha; ++i) {
-    if (i < a) {
-      const u64* h = qhinv + ((std::size_t)tab * kMaxAlpha + i) * 2;
-      y[i] = shoup_mul(xin[(std::size_t)(lo + i) * N + n], h[0], h[1], pc[lo + i].q);
+  const int nt = min(kTC, E - A - (int)blockIdx.y * kTC);
+  if (threadIdx.x < kTC * A) {
+    const int c = threadIdx.x / A, i = threadIdx.x % A;
+    if (c < nt) {
+      const int tt = blockIdx.y * kTC + c;
+      const int t = tt < lo ? tt : tt + A;
+      const int pt = t < limbs ? t : L + (t - limbs);
+      cs[c][i] = qhat[((std::size_t)tab * (L + K) + pt) * kMaxAlpha + i];
+      if (i == 0) {
+        tq[c][0] = pc[pt].q;
+        tq[c][1] = pc[pt].qinv_neg;
+        tdst[c] = t;
+      }
     }
   }
-  for (int t = 0; t < E; ++t) {
-    if (t >= lo && t < hi) continue;
-    const int pt = t < limbs ? t : L + (t - limbs);
-    const u64* c = qhat + ((std::size_t)tab * (L + K) + pt) * kMaxAlpha;
+  __syncthreads();
+  const u64* xin = x.p[blockIdx.z];
+  u64* out = ext.p[blockIdx.z] + (std::size_t)j * E * N;
+  u64 y[A];
+#pragma unroll
+  for (int i = 0; i < A; ++i) {
+    const u64* h = qhinv + ((std::size_t)tab * kMaxAlpha + i) * 2;
+    y[i] = shoup_mul(xin[(std::size_t)(lo + i) * N + n], __ldg(h), __ldg(h + 1), pc[lo + i].q);
+  }
+  for (int c = 0; c < nt; ++c) {
     Acc128 acc;
 #pragma unroll
-    for (int i = 0; i < kMaxAlpha; ++i)
-      if (i < a) acc.mac(y[i], __ldg(c + i));
-    out[(std::size_t)t * N + n] = redc(acc.hi, acc.lo, pc[pt].q, pc[pt].qinv_neg);
+    for (int i = 0; i < A; ++i) acc.mac(y[i], cs[c][i]);
+    out[(std::size_t)tdst[c] * N + n] = redc(acc.hi, acc.lo, tq[c][0], tq[c][1]);
   }
 }
 
@@ -130,38 +145,52 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
   acc[((std::size_t)E + t) * N + n] = redc(a1.hi, a1.lo, P.q, P.qinv_neg);
 }
 
-// grid (N/256, npolys)
-__global__ void k_moddown_conv(PolyList conv, PolyList z, const PrimeConst* __restrict__ pc,
-                               const u64* __restrict__ md_pk, const double* __restrict__ md_pinv,
-                               const u64* __restrict__ md_phat, const u64* __restrict__ md_q, int logN, int limbs,
-                               int L, int K) {
+// ModDown conversion with KK = K special limbs (compile time).
+// grid (N/256, ceil(limbs / kTC), npolys); the chunk's constants sit in smem.
+template <int KK>
+__global__ void __launch_bounds__(256) k_moddown_conv(PolyList conv, PolyList z, const PrimeConst* __restrict__ pc,
+                                                      const u64* __restrict__ md_pk, const double* __restrict__ md_pinv,
+                                                      const u64* __restrict__ md_phat, const u64* __restrict__ md_q,
+                                                      int logN, int limbs, int L) {
+  __shared__ u64 cs[kTC][KK];
+  __shared__ u64 tq[kTC][4];  // q, qinv_neg, P mod q (Montgomery), (P-1)/2 mod q
   const std::size_t N = (std::size_t)1 << logN;
   const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i0 = blockIdx.y * kTC;
+  const int nt = min(kTC, limbs - i0);
+  if (threadIdx.x < kTC * KK) {
+    const int c = threadIdx.x / KK, k = threadIdx.x % KK;
+    if (c < nt) {
+      cs[c][k] = md_phat[(std::size_t)(i0 + c) * kMaxK + k];
+      if (k == 0) {
+        tq[c][0] = pc[i0 + c].q;
+        tq[c][1] = pc[i0 + c].qinv_neg;
+        tq[c][2] = md_q[(std::size_t)(i0 + c) * 4];
+        tq[c][3] = md_q[(std::size_t)(i0 + c) * 4 + 1];
+      }
+    }
+  }
+  __syncthreads();
   const u64* zp = z.p[blockIdx.z];
-  u64 y[kMaxK];
+  u64 y[KK];
   double v = 0.0;
 #pragma unroll
-  for (int k = 0; k < kMaxK; ++k) {
-    if (k < K) {
-      const u64 pk = pc[L + k].q;
-      const u64* c = md_pk + (std::size_t)k * 4;
-      y[k] = shoup_mul(add_mod(zp[(std::size_t)k * N + n], c[2], pk), c[0], c[1], pk);
-      v = __dadd_rn(v, __dmul_rn(__ull2double_rn(y[k]), md_pinv[k]));
-    }
+  for (int k = 0; k < KK; ++k) {
+    const u64 pk = pc[L + k].q;
+    const u64* c = md_pk + (std::size_t)k * 4;
+    y[k] = shoup_mul(add_mod(zp[(std::size_t)k * N + n], __ldg(c + 2), pk), __ldg(c), __ldg(c + 1), pk);
+    v = __dadd_rn(v, __dmul_rn(__ull2double_rn(y[k]), md_pinv[k]));
   }
   const u64 u = (u64)v;
   u64* out = conv.p[blockIdx.z];
-  for (int i = 0; i < limbs; ++i) {
-    const PrimeConst P = pc[i];
-    const u64* ph = md_phat + (std::size_t)i * kMaxK;
+  for (int c = 0; c < nt; ++c) {
+    const u64 q = tq[c][0], qn = tq[c][1];
     Acc128 acc;
 #pragma unroll
-    for (int k = 0; k < kMaxK; ++k)
-      if (k < K) acc.mac(y[k], __ldg(ph + k));
-    u64 x = redc(acc.hi, acc.lo, P.q, P.qinv_neg);
-    const u64* mq = md_q + (std::size_t)i * 4;
-    x = sub_mod(x, redc(mulhi(u, mq[0]), u * mq[0], P.q, P.qinv_neg), P.q);
-    out[(std::size_t)i * N + n] = sub_mod(x, mq[1], P.q);
+    for (int k = 0; k < KK; ++k) acc.mac(y[k], cs[c][k]);
+    u64 x = redc(acc.hi, acc.lo, q, qn);
+    x = sub_mod(x, redc(mulhi(u, tq[c][2]), u * tq[c][2], q, qn), q);
+    out[(std::size_t)(i0 + c) * N + n] = sub_mod(x, tq[c][3], q);
   }
 }
 
@@ -312,8 +341,24 @@ void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int 
 void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st) {
   const int beta = (limbs + t.alpha - 1) / t.alpha;
   TimedScope ts(t, kModUp, st);
-  k_modup_bconv<<<grid_for(t.N, beta, x.n), kThreads, 0, st>>>(ext, x, t.pc, t.modup_qhinv, t.modup_qhat, t.logN,
-                                                                  limbs, t.L, t.K, t.dnum, t.alpha);
+  const int E = limbs + t.K;
+  for (int j = 0; j < beta; ++j) {
+    const int a = std::min(t.alpha, limbs - j * t.alpha);
+    const dim3 grid = grid_for(t.N, (E - a + kTC - 1) / kTC, x.n);
+#define FHEON_BCONV(AA)                                                                                        \
+  case AA:                                                                                                     \
+    k_modup_bconv<AA><<<grid, kThreads, 0, st>>>(ext, x, t.pc, t.modup_qhinv, t.modup_qhat, t.logN, limbs, t.L, \
+                                                 t.K, t.dnum, t.alpha, j);                                     \
+    break;
+    switch (a) {
+      FHEON_BCONV(1) FHEON_BCONV(2) FHEON_BCONV(3) FHEON_BCONV(4) FHEON_BCONV(5) FHEON_BCONV(6) FHEON_BCONV(7)
+      FHEON_BCONV(8) FHEON_BCONV(9) FHEON_BCONV(10) FHEON_BCONV(11) FHEON_BCONV(12) FHEON_BCONV(13)
+      FHEON_BCONV(14) FHEON_BCONV(15)
+      default: throw std::runtime_error("digit size out of range");
+    }
+#undef FHEON_BCONV
+    launch_check("k_modup_bconv");
+  }
 }
 void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.n == 0) return;
@@ -324,8 +369,19 @@ void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStr
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
   if (conv.n == 0) return;
   TimedScope ts(t, kModDown, st);
-  k_moddown_conv<<<grid_for(t.N, 1, conv.n), kThreads, 0, st>>>(conv, z, t.pc, t.md_pk, t.md_pinv, t.md_phat,
-                                                                  t.md_q, t.logN, limbs, t.L, t.K);
+  const dim3 grid = grid_for(t.N, (limbs + kTC - 1) / kTC, conv.n);
+#define FHEON_MDC(KK)                                                                                             \
+  case KK:                                                                                                        \
+    k_moddown_conv<KK><<<grid, kThreads, 0, st>>>(conv, z, t.pc, t.md_pk, t.md_pinv, t.md_phat, t.md_q, t.logN, \
+                                                  limbs, t.L);                                                    \
+    break;
+  switch (t.K) {
+    FHEON_MDC(1) FHEON_MDC(2) FHEON_MDC(3) FHEON_MDC(4) FHEON_MDC(5) FHEON_MDC(6) FHEON_MDC(7) FHEON_MDC(8)
+    FHEON_MDC(9) FHEON_MDC(10) FHEON_MDC(11) FHEON_MDC(12) FHEON_MDC(13) FHEON_MDC(14) FHEON_MDC(15)
+    default: throw std::runtime_error("K out of range");
+  }
+#undef FHEON_MDC
+  launch_check("k_moddown_conv");
 }
 void moddown_finish(const DevTables& t, const PolyList& out, const PolyList& acc, const PolyList& conv,
                     const PolyList& add, int limbs, cudaStream_t st) {
