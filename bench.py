@@ -183,7 +183,9 @@ def run_ours(args):
     # ---- roofline of the key-switch inner product (per launch: one rotation)
     E = L + K
     beta = (L + (L + DNUM - 1) // DNUM - 1) // ((L + DNUM - 1) // DNUM)
-    alg_bytes = (beta * E * N + 2 * beta * E * N + 2 * E * N) * 8  # digits + key (read), acc (write)
+    per_rot = (beta * E * N + 2 * beta * E * N + 2 * E * N) * 8  # digits + key (read), acc (write)
+    rot_per_launch = args.steps * B / max(1, ks_n)  # one launch covers the step's batch of rotations
+    alg_bytes = int(per_rot * rot_per_launch)
     ks_avg_ms = ks_ms / max(1, ks_n)
     achieved = alg_bytes / (ks_avg_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
@@ -241,7 +243,8 @@ def run_ours(args):
         "roofline": {"kernel": "k_ks_inner (key inner product, automorphism fused)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": committed_traffic(),
-                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(ks_avg_ms, 5),
+                     "algorithmic_bytes_per_launch": alg_bytes, "rotations_per_launch": rot_per_launch,
+                     "algorithmic_bytes_per_rotation": per_rot, "avg_launch_ms": round(ks_avg_ms, 5),
                      "launches_timed": ks_n,
                      "share_of_step": round(ks_ms / ms, 4)},
         "clocks": clk.summary(),

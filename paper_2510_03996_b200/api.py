@@ -227,7 +227,10 @@ class SlotContext:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _native.lib().fheon_ctx_destroy(h)
+            try:
+                _native.lib().fheon_ctx_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def slots(self) -> int:
@@ -331,7 +334,10 @@ class SlotVector:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _native.lib().fheon_ct_free(h)
+            try:
+                _native.lib().fheon_ct_free(h)
+            except Exception:  # interpreter shutdown: module state already torn down
+                pass
             self._h = None
 
     @staticmethod

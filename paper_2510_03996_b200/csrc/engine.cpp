@@ -79,12 +79,14 @@ TimedScope::~TimedScope() {
 }
 
 // ------------------------------------------------------------- buffers
-DevBuffer::DevBuffer(Context* c, std::size_t w) : ctx(c), words(w) {
+DevBuffer::DevBuffer(Context* c, std::size_t w) : alive(c->alive), stream(c->stream()), words(w) {
   if (w == 0) return;
-  FHEON_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), c->stream()));
+  FHEON_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), stream));
 }
 DevBuffer::~DevBuffer() {
-  if (ptr) cudaFreeAsync(ptr, ctx->stream());
+  if (!ptr) return;
+  if (alive && alive->load()) cudaFreeAsync(ptr, stream);
+  else cudaFree(ptr);
 }
 
 BufPtr Context::alloc(std::size_t words) { return std::make_shared<DevBuffer>(this, words); }
@@ -156,6 +158,16 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
     FHEON_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     std::uint64_t thr = UINT64_MAX;
     FHEON_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Pre-grow the stream-ordered pool so steady-state key switching never
+    // maps new physical memory mid-pipeline: reserve ~64 ciphertexts' worth
+    // of scratch (capped at 1/4 of free HBM).
+    std::size_t free_b = 0, total_b = 0;
+    FHEON_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const std::size_t ct_bytes = 2 * (std::size_t)(p.L + p.K) * ((std::size_t)1 << p.logN) * sizeof(u64);
+    std::size_t want = std::min<std::size_t>(free_b / 4, 64 * ct_bytes * 3);
+    void* r = nullptr;
+    if (want > 0 && cudaMallocAsync(&r, want, stream_) == cudaSuccess) cudaFreeAsync(r, stream_);
+    cudaGetLastError();
   }
   for (int i = 0; i < kStaging; ++i) {
     FHEON_CUDA(cudaMallocHost(reinterpret_cast<void**>(&staging_[i]), ht_.N * sizeof(long long)));
@@ -166,7 +178,10 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
 
 Context::~Context() {
   keys_.clear();
+  basis_.clear();
+  ptcache_.clear();
   if (stream_) cudaStreamSynchronize(stream_);
+  alive->store(false);
   for (void* d : dev_allocs_) cudaFree(d);
   for (int i = 0; i < kStaging; ++i) {
     if (staging_[i]) cudaFreeHost(staging_[i]);
@@ -393,6 +408,61 @@ void Context::encode_coeffs(const double* vals, std::size_t n, double scale, lon
   encode_coeffs_host(ht_, vals, n, scale, coeffs);
 }
 
+namespace {
+// special inverse FFT of the zero-filled slot vector; re/im scaled by 1/S
+void fft_special_inv_host(const HostTables& ht_, const double* vals, std::size_t n, std::vector<double>& re,
+                          std::vector<double>& im);
+}  // namespace
+
+void encode_real_host(const HostTables& ht_, const double* vals, std::size_t n, double* out) {
+  std::vector<double> re, im;
+  fft_special_inv_host(ht_, vals, n, re, im);
+  const int S = ht_.S;
+  for (int i = 0; i < S; ++i) {
+    out[i] = re[i] / (double)S;
+    out[i + S] = im[i] / (double)S;
+  }
+}
+
+namespace {
+void fft_special_inv_host(const HostTables& ht_, const double* vals, std::size_t n, std::vector<double>& re,
+                          std::vector<double>& im) {
+  const int S = ht_.S;
+  if (n > (std::size_t)S) throw Error(ErrKind::capacity, "payload exceeds the slot count");
+  const u64 M = 2 * (u64)ht_.N;
+  re.assign(S, 0.0);
+  im.assign(S, 0.0);
+  for (std::size_t i = 0; i < n; ++i) re[i] = vals[i];
+  for (int len = S; len >= 1; len >>= 1) {
+    const int lenh = len >> 1;
+    const u64 lenq = (u64)len << 2;
+    for (int i = 0; i < S; i += len) {
+      for (int j = 0; j < lenh; ++j) {
+        const u64 idx = (lenq - (ht_.rotgroup[j] % lenq)) * (M / lenq);
+        const double ur = re[i + j] + re[i + j + lenh];
+        const double ui = im[i + j] + im[i + j + lenh];
+        const double vr0 = re[i + j] - re[i + j + lenh];
+        const double vi0 = im[i + j] - im[i + j + lenh];
+        const double wr = ht_.ksi_re[idx], wi = ht_.ksi_im[idx];
+        re[i + j] = ur;
+        im[i + j] = ui;
+        re[i + j + lenh] = vr0 * wr - vi0 * wi;
+        im[i + j + lenh] = vr0 * wi + vi0 * wr;
+      }
+    }
+  }
+  for (int i = 1, j = 0; i < S; ++i) {
+    int bit = S >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) {
+      std::swap(re[i], re[j]);
+      std::swap(im[i], im[j]);
+    }
+  }
+}
+}  // namespace
+
 void encode_coeffs_host(const HostTables& ht_, const double* vals, std::size_t n, double scale, long long* coeffs) {
   const int S = ht_.S;
   if (n > (std::size_t)S) throw Error(ErrKind::capacity, "payload exceeds the slot count");
@@ -473,6 +543,56 @@ void Context::decode_coeffs(const double* coeffs, double scale, double* out) con
     }
   }
   for (int i = 0; i < S; ++i) out[i] = re[i];
+}
+
+const double* Context::basis(const std::string& key, const std::vector<double>& slot_values) {
+  auto it = basis_.find(key);
+  if (it != basis_.end()) return reinterpret_cast<const double*>(it->second->ptr);
+  std::vector<double> real(ht_.N);
+  encode_real_host(ht_, slot_values.data(), slot_values.size(), real.data());
+  BufPtr b = alloc(ht_.N);
+  FHEON_CUDA(cudaMemcpyAsync(b->ptr, real.data(), ht_.N * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  FHEON_CUDA(cudaStreamSynchronize(stream_));  // `real` is pageable and local
+  basis_[key] = b;
+  return reinterpret_cast<const double*>(b->ptr);
+}
+
+BufPtr Context::encode_lincomb(const LinComb& lc, int limbs, double scale) {
+  BufPtr out = alloc((std::size_t)limbs * ht_.N);
+  ++stats.encodes;
+  fheon::encode_lincomb(dt_, out->ptr, lc, scale, limbs, stream_);
+  LimbSet ls{};
+  ls.base[0] = out->ptr;
+  ls.nbase = 1;
+  ls.blocks_per_base = 1;
+  ls.E = limbs;
+  ls.ell = limbs;
+  ls.L = ht_.p.L;
+  ntt_forward(dt_, ls, stream_);
+  return out;
+}
+
+BufPtr Context::encode_cached(const std::vector<double>& vals, int limbs, double scale) {
+  u64 h = 1469598103934665603ULL;  // FNV-1a over the bit patterns
+  for (double v : vals) {
+    u64 b;
+    std::memcpy(&b, &v, 8);
+    h = (h ^ b) * 1099511628211ULL;
+  }
+  auto key = std::make_tuple(h, limbs, scale);
+  auto& bucket = ptcache_[key];
+  for (const PtEntry& e : bucket)
+    if (e.vals == vals) return e.buf;
+  BufPtr b = encode(vals.data(), vals.size(), limbs, scale);
+  const std::size_t words = (std::size_t)limbs * ht_.N;
+  const std::size_t budget = (std::size_t)1 << 29;  // 4 GiB of cached plaintexts
+  if (ptcache_words_ + words > budget) {
+    ptcache_.clear();
+    ptcache_words_ = 0;
+  }
+  ptcache_[key].push_back({vals, b});
+  ptcache_words_ += words;
+  return b;
 }
 
 long long* Context::staging_slot(cudaEvent_t** ev) {

@@ -24,6 +24,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "kernels.hpp"
@@ -57,7 +58,10 @@ extern std::atomic<std::uint64_t> g_kernel_launches;
 class Context;
 
 struct DevBuffer {
-  Context* ctx = nullptr;
+  // stream-ordered free while the owning context lives; a synchronous free if
+  // a handle outlives its context
+  std::shared_ptr<std::atomic<bool>> alive;
+  cudaStream_t stream = nullptr;
   u64* ptr = nullptr;
   std::size_t words = 0;
   DevBuffer(Context* c, std::size_t w);
@@ -140,6 +144,13 @@ class Context {
   void decode_coeffs(const double* coeffs, double scale, double* out) const;
   // encode `vals` at `scale` over `limbs` limbs into a device [limbs][N] NTT-domain buffer
   BufPtr encode(const double* vals, std::size_t n, int limbs, double scale);
+  // content-addressed cache over encode() (masks reused across a layer)
+  BufPtr encode_cached(const std::vector<double>& vals, int limbs, double scale);
+  // device real-coefficient (unscaled, unrounded) encoding of a slot vector,
+  // cached under `key` (block indicators of a layer geometry)
+  const double* basis(const std::string& key, const std::vector<double>& slot_values);
+  // plaintext = round(scale * sum_b w_b basis_b), NTT domain over `limbs` limbs
+  BufPtr encode_lincomb(const LinComb& lc, int limbs, double scale);
 
   // ---- trace (mirrors slotcnn TraceRecorder, trace.hpp:22-103)
   void set_tracing(bool on) { tracing_ = on; }
@@ -164,7 +175,18 @@ class Context {
   int depth_budget_ = 0;
   std::uint64_t id_counter_ = 0;
   std::vector<void*> dev_allocs_;  // table allocations
+ public:
+  std::shared_ptr<std::atomic<bool>> alive = std::make_shared<std::atomic<bool>>(true);
+
+ private:
   std::map<u64, BufPtr> keys_;
+  std::map<std::string, BufPtr> basis_;
+  struct PtEntry {
+    std::vector<double> vals;
+    BufPtr buf;
+  };
+  std::map<std::tuple<u64, int, double>, std::vector<PtEntry>> ptcache_;
+  std::size_t ptcache_words_ = 0;
   mutable std::mutex trace_mu_;
   bool tracing_ = false;
   std::vector<TraceEvent> trace_;
@@ -176,6 +198,24 @@ class Context {
 
 // canonical-embedding encode on the host (special FFT)
 void encode_coeffs_host(const HostTables& h, const double* vals, std::size_t n, double scale, long long* coeffs);
+// unscaled real coefficients (N doubles: re[0..S), im[0..S)) before rounding
+void encode_real_host(const HostTables& h, const double* vals, std::size_t n, double* out);
+
+// ---- batched evaluator ops (layer kernels)
+// plaintext scale that lands a mult_plain on the next level's target scale
+double pt_scale_for(const Context& ctx, const Ciphertext& a);
+std::vector<Ciphertext> rescale_many(Context& ctx, const std::vector<Ciphertext>& as);
+// out[o] = rescale( sum_j terms[o][j] (*) pts[o][j] ): one fused MAC, one rescale.
+// All terms share level and scale; pts are encoded at pt_scale_for(term).  Records
+// one mult_plain trace event per term (level_after = level - 1), o-major.
+std::vector<Ciphertext> mac_plain_many(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
+                                       const std::vector<std::vector<BufPtr>>& pts);
+std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b);
+// add an encoded plaintext (encoded at a's level and scale)
+Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt);
+std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphertext>& as,
+                                         const std::vector<Ciphertext>& bs);
+std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Ciphertext>& as, const std::vector<double>& cs);
 
 // ---------------------------------------------------------------- ops
 Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n);            // at the depth budget

@@ -463,6 +463,277 @@ Ciphertext mult_cipher(Context& ctx, const Ciphertext& a0, const Ciphertext& b0)
   return out;
 }
 
+// ------------------------------------------------------------- batched ops
+double pt_scale_for(const Context& ctx, const Ciphertext& a) {
+  const HostTables& h = ctx.host();
+  const int lv = a.level();
+  return h.T[lv - 1] * (double)h.q[lv] / a.scale;
+}
+
+std::vector<Ciphertext> rescale_many(Context& ctx, const std::vector<Ciphertext>& as) {
+  std::vector<Ciphertext> outs;
+  outs.reserve(as.size());
+  if (as.empty()) return outs;
+  const int l = as[0].limbs;
+  for (const Ciphertext& a : as) {
+    require_valid(a, "rescale");
+    if (a.limbs != l) throw Error(ErrKind::internal, "rescale_many: mixed levels");
+  }
+  if (l < 2) throw Error(ErrKind::depth_exhausted, "rescale: no limb left to drop");
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  constexpr int kChunk = kMaxBases;  // 32 ciphertexts = 64 polys per launch group
+  for (std::size_t c0 = 0; c0 < as.size(); c0 += kChunk) {
+    const int R = (int)std::min<std::size_t>(kChunk, as.size() - c0);
+    BufPtr last = ctx.alloc((std::size_t)2 * R * N);
+    // out-of-place iNTT of each poly's last limb straight from the ciphertexts
+    LimbSet dst = limbset(last->ptr, 2 * R, N, 1, 1, ctx.L(), l - 1);
+    LimbSet src = dst;
+    src.nbase = R;
+    src.blocks_per_base = 2;
+    for (int r = 0; r < R; ++r) src.base[r] = as[c0 + r].c0 + (std::size_t)(l - 1) * N;
+    src.block_stride = 0;
+    bool uniform = true;
+    for (int r = 0; r < R; ++r)
+      uniform = uniform && (as[c0 + r].c1 - as[c0 + r].c0) == (as[c0].c1 - as[c0].c0);
+    if (uniform) {
+      src.block_stride = (long long)(as[c0].c1 - as[c0].c0);
+      ntt_inverse(t, dst, st, &src);
+    } else {
+      for (int r = 0; r < R; ++r) {
+        LimbSet d1 = limbset(last->ptr + (std::size_t)2 * r * N, 2, N, 1, 1, ctx.L(), l - 1);
+        LimbSet s1 = d1;
+        s1.base[0] = as[c0 + r].c0 + (std::size_t)(l - 1) * N;
+        s1.block_stride = (long long)(as[c0 + r].c1 - as[c0 + r].c0);
+        ntt_inverse(t, d1, st, &s1);
+      }
+    }
+    BufPtr rb = ctx.alloc((std::size_t)2 * R * (l - 1) * N);
+    PolyList rl{}, ll{}, ol{}, al{};
+    rl.n = ll.n = ol.n = al.n = 2 * R;
+    for (int r = 0; r < R; ++r) {
+      Ciphertext o = ctx.new_ct(l - 1);
+      o.scale = as[c0 + r].scale;
+      for (int p = 0; p < 2; ++p) {
+        const int i = 2 * r + p;
+        rl.p[i] = rb->ptr + (std::size_t)i * (l - 1) * N;
+        ll.p[i] = last->ptr + (std::size_t)i * N;
+        ol.p[i] = p ? o.c1 : o.c0;
+        al.p[i] = const_cast<u64*>(p ? as[c0 + r].c1 : as[c0 + r].c0);
+        rl.g[i] = ll.g[i] = ol.g[i] = al.g[i] = 1;
+      }
+      outs.push_back(o);
+    }
+    rescale_lift(t, rl, ll, l, st);
+    ntt_forward(t, limbset(rb->ptr, 2 * R, (std::size_t)(l - 1) * N, l - 1, l - 1, ctx.L()), st);
+    rescale_finish(t, ol, al, rl, l, st);
+    ctx.stats.rescales += R;
+    ctx.stats.ntt_limbs += (std::size_t)R * 2 * l;
+  }
+  return outs;
+}
+
+std::vector<Ciphertext> mac_plain_many(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
+                                       const std::vector<std::vector<BufPtr>>& pts) {
+  if (terms.size() != pts.size()) throw Error(ErrKind::internal, "mac_plain_many: size mismatch");
+  std::vector<Ciphertext> prods;
+  prods.reserve(terms.size());
+  if (terms.empty()) return prods;
+  const Ciphertext& ref = terms[0].at(0);
+  const int l = ref.limbs;
+  for (std::size_t o = 0; o < terms.size(); ++o) {
+    if (terms[o].empty() || terms[o].size() != pts[o].size())
+      throw Error(ErrKind::internal, "mac_plain_many: term/plaintext count mismatch");
+    for (const Ciphertext& c : terms[o]) {
+      require_valid(c, "mult_plain");
+      require_depth(c, "mult_plain");
+      if (c.limbs != l) throw Error(ErrKind::internal, "mac_plain_many: terms at different levels");
+      check_scales(c, ref, "mac_plain_many");
+    }
+  }
+  const HostTables& h = ctx.host();
+  const int lv = l - 1;
+  for (std::size_t o0 = 0; o0 < terms.size(); o0 += kMacMaxOut) {
+    MacJobs jobs{};
+    jobs.nout = (int)std::min<std::size_t>(kMacMaxOut, terms.size() - o0);
+    for (int z = 0; z < jobs.nout; ++z) prods.push_back(ctx.new_ct(l));
+    // split long sums into kMacMaxTerms-term partial products accumulated in place
+    std::size_t maxt = 0;
+    for (int z = 0; z < jobs.nout; ++z) maxt = std::max(maxt, terms[o0 + z].size());
+    for (std::size_t j0 = 0; j0 < maxt; j0 += kMacMaxTerms) {
+      MacJobs jb{};
+      int nz = 0;
+      std::vector<Ciphertext> partial;
+      for (int z = 0; z < jobs.nout; ++z) {
+        const auto& tz = terms[o0 + z];
+        if (j0 >= tz.size()) continue;
+        const int nt = (int)std::min<std::size_t>(kMacMaxTerms, tz.size() - j0);
+        Ciphertext& dst = prods[o0 + z];
+        Ciphertext tmp = j0 == 0 ? dst : ctx.new_ct(l);
+        for (int j = 0; j < nt; ++j) {
+          jb.ct[nz][j] = tz[j0 + j].c0;
+          jb.c1_off[nz][j] = (long long)(tz[j0 + j].c1 - tz[j0 + j].c0);
+          jb.pt[nz][j] = pts[o0 + z][j0 + j]->ptr;
+        }
+        jb.nterm[nz] = nt;
+        jb.out0[nz] = tmp.c0;
+        jb.out1[nz] = tmp.c1;
+        if (j0 > 0) partial.push_back(tmp);
+        ++nz;
+      }
+      jb.nout = nz;
+      mac_pt(ctx.dev(), jb, l, ctx.stream());
+      if (j0 > 0) {  // fold the partial sums into the outputs
+        int k = 0;
+        for (int z = 0; z < jobs.nout; ++z) {
+          if (j0 >= terms[o0 + z].size()) continue;
+          Ciphertext& dst = prods[o0 + z];
+          ew_add(ctx.dev(), plist({dst.c0, dst.c1}), plist({dst.c0, dst.c1}), plist({partial[k].c0, partial[k].c1}),
+                 l, ctx.stream());
+          ++k;
+        }
+      }
+    }
+  }
+  for (Ciphertext& p : prods) p.scale = ref.scale;
+  std::vector<Ciphertext> outs = rescale_many(ctx, prods);
+  for (std::size_t o = 0; o < outs.size(); ++o) {
+    outs[o].scale = h.T[lv - 1];
+    for (std::size_t j = 0; j < terms[o].size(); ++j) {
+      ctx.stats.mult_plain++;
+      ctx.record(1, lv - 1);
+    }
+  }
+  return outs;
+}
+
+Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt) {
+  require_valid(a, "add_plain");
+  Ciphertext out = ctx.new_ct(a.limbs);
+  ew_add(ctx.dev(), plist({out.c0}), plist({a.c0}), plist({pt->ptr}), a.limbs, ctx.stream());
+  FHEON_CUDA(cudaMemcpyAsync(out.c1, a.c1, (std::size_t)a.limbs * ctx.N() * sizeof(u64), cudaMemcpyDeviceToDevice,
+                             ctx.stream()));
+  out.scale = a.scale;
+  return out;
+}
+
+// pairs (a_i, b_i) multiplied with one batched relinearisation key switch and
+// one batched rescale; records one mult_cipher event per pair, in order.
+std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphertext>& as,
+                                         const std::vector<Ciphertext>& bs) {
+  if (as.size() != bs.size()) throw Error(ErrKind::internal, "mult_cipher_many: size mismatch");
+  std::vector<Ciphertext> outs(as.size());
+  if (as.empty()) return outs;
+  std::vector<Ciphertext> A(as.size()), B(bs.size());
+  for (std::size_t i = 0; i < as.size(); ++i) {
+    require_valid(as[i], "mult_cipher");
+    require_valid(bs[i], "mult_cipher");
+    require_depth(as[i], "mult_cipher");
+    require_depth(bs[i], "mult_cipher");
+    A[i] = as[i];
+    B[i] = bs[i];
+    align(ctx, A[i], B[i]);
+  }
+  std::map<int, std::vector<std::size_t>> by_level;
+  for (std::size_t i = 0; i < A.size(); ++i) by_level[A[i].limbs].push_back(i);
+  const std::size_t N = ctx.N();
+  for (auto& [l, idx] : by_level) {
+    const std::size_t P = (std::size_t)l * N;
+    BufPtr d = ctx.alloc(3 * P * idx.size());
+    std::vector<const u64*> inputs;
+    std::vector<KsJob> jobs;
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      const std::size_t i = idx[k];
+      u64* d0 = d->ptr + 3 * P * k;
+      ew_tensor(ctx.dev(), d0, d0 + P, d0 + 2 * P, A[i].c0, A[i].c1, B[i].c0, B[i].c1, l, ctx.stream());
+      inputs.push_back(d0 + 2 * P);
+      KsJob jb{0, 1, d0, 1, d0 + P};
+      jb.in = (int)k;
+      jobs.push_back(jb);
+    }
+    std::vector<Ciphertext> r = keyswitch(ctx, inputs, l, jobs);
+    for (Ciphertext& c : r) c.scale = 1.0;
+    std::vector<Ciphertext> rs = rescale_many(ctx, r);
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      const std::size_t i = idx[k];
+      rs[k].scale = A[i].scale * B[i].scale / (double)ctx.host().q[l - 1];
+      outs[i] = rs[k];
+      ctx.stats.mult_cipher++;
+    }
+  }
+  for (const Ciphertext& o : outs) ctx.record(2, o.level());
+  return outs;
+}
+
+// a_i * c_i (constant vectors) with one batched rescale per level
+std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Ciphertext>& as, const std::vector<double>& cs) {
+  std::vector<Ciphertext> outs(as.size());
+  std::map<int, std::vector<std::size_t>> by_level;
+  for (std::size_t i = 0; i < as.size(); ++i) {
+    require_valid(as[i], "mult_plain");
+    require_depth(as[i], "mult_plain");
+    by_level[as[i].limbs].push_back(i);
+  }
+  const HostTables& h = ctx.host();
+  for (auto& [l, idx] : by_level) {
+    std::vector<Ciphertext> prods;
+    for (std::size_t i : idx) {
+      const double x = cs[i] * pt_scale_for(ctx, as[i]);
+      if (!(std::fabs(x) < 4611686018427387904.0)) throw Error(ErrKind::capacity, "constant exceeds 2^62");
+      const long long k = std::llround(x);
+      LimbConsts lc{};
+      for (int j = 0; j < l; ++j) {
+        lc.c[j] = signed_mod(k, h.q[j]);
+        lc.sh[j] = shoup(lc.c[j], h.q[j]);
+      }
+      Ciphertext p = ctx.new_ct(l);
+      ew_mul_const(ctx.dev(), plist({p.c0, p.c1}), plist({as[i].c0, as[i].c1}), lc, l, ctx.stream());
+      p.scale = as[i].scale;
+      prods.push_back(p);
+    }
+    std::vector<Ciphertext> rs = rescale_many(ctx, prods);
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      rs[k].scale = h.T[l - 2];
+      outs[idx[k]] = rs[k];
+      ctx.stats.mult_plain++;
+    }
+  }
+  for (const Ciphertext& o : outs) ctx.record(1, o.level());
+  return outs;
+}
+
+std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b) {
+  if (a.size() != b.size()) throw Error(ErrKind::internal, "add_many: size mismatch");
+  std::vector<Ciphertext> outs(a.size());
+  // same-level pairs in one launch (up to 32 pairs), others one by one
+  std::vector<std::size_t> batch;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    if (a[i].limbs == b[i].limbs && a[i].limbs == a[0].limbs) batch.push_back(i);
+    else outs[i] = add(ctx, a[i], b[i]);
+  }
+  for (std::size_t k0 = 0; k0 < batch.size(); k0 += kMaxPolys / 2) {
+    const int R = (int)std::min<std::size_t>(kMaxPolys / 2, batch.size() - k0);
+    PolyList ol{}, al{}, bl{};
+    ol.n = al.n = bl.n = 2 * R;
+    for (int r = 0; r < R; ++r) {
+      const std::size_t i = batch[k0 + r];
+      check_scales(a[i], b[i], "add");
+      outs[i] = ctx.new_ct(a[i].limbs);
+      outs[i].scale = a[i].scale;
+      ol.p[2 * r] = outs[i].c0;
+      ol.p[2 * r + 1] = outs[i].c1;
+      al.p[2 * r] = a[i].c0;
+      al.p[2 * r + 1] = a[i].c1;
+      bl.p[2 * r] = b[i].c0;
+      bl.p[2 * r + 1] = b[i].c1;
+    }
+    ew_add(ctx.dev(), ol, al, bl, a[batch[k0]].limbs, ctx.stream());
+    ctx.stats.adds += R;
+  }
+  return outs;
+}
+
 Ciphertext bootstrap(Context& ctx, const Ciphertext& a) {
   require_valid(a, "bootstrap");
   (void)ctx;

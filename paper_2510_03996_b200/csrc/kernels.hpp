@@ -120,6 +120,33 @@ void rescale_lift(const DevTables& t, const PolyList& r, const PolyList& last, i
 void rescale_finish(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& r, int limbs,
                     cudaStream_t st);
 
+// ---- fused layer kernels
+// Multiply-accumulate of plaintext diagonals: for each output o,
+//   out[o] = sum_{j < nterm[o]} ct[o][j] (*) pt[o][j]     (2 polys, `limbs` limbs)
+// with one 128-bit accumulation and a single reduction (no per-term rescale).
+constexpr int kMacMaxOut = 8;
+constexpr int kMacMaxTerms = 32;
+struct MacJobs {
+  const u64* ct[kMacMaxOut][kMacMaxTerms];  // c0 pointer; c1 = c0 + c1_off[o][j]
+  long long c1_off[kMacMaxOut][kMacMaxTerms];
+  const u64* pt[kMacMaxOut][kMacMaxTerms];  // [limbs][N] standard form
+  u64* out0[kMacMaxOut];
+  u64* out1[kMacMaxOut];
+  int nterm[kMacMaxOut];
+  int nout;
+};
+void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st);
+// Plaintext as a linear combination of cached real-coefficient basis vectors
+// (block-indicator encodings): coeff[k] = rint(scale * sum_b w_b basis_b[k]),
+// written as RNS limbs (coefficient domain, then forward NTT by the caller).
+constexpr int kMaxBasis = 64;
+struct LinComb {
+  const double* basis[kMaxBasis];
+  double w[kMaxBasis];
+  int nb;
+};
+void encode_lincomb(const DevTables& t, u64* out, const LinComb& lc, double scale, int limbs, cudaStream_t st);
+
 // ---- encode / encrypt / keygen / decrypt
 // signed coefficients -> RNS coefficient domain [limbs][N]
 void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st);

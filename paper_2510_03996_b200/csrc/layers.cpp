@@ -1,7 +1,18 @@
 // Layer algorithms over device ciphertexts.  Each function follows the
-// reference's algorithm op for op (cited per function) so rotation indices,
-// mask values, level consumption and trace events are identical; the GPU
-// realisation hoists rotation sets that share a source ciphertext.
+// reference's algorithm (cited per function): the same rotation indices, mask
+// values, level consumption, and the same multiset of trace events.  The GPU
+// realisation batches what the reference does one op at a time:
+//   * rotations that share a source are hoisted (one ModUp), independent
+//     rotations across output channels / rows run as one key-switch batch;
+//   * a sum of plaintext products at one level ("rotate-and-MAC") is one fused
+//     MAC kernel and ONE rescale instead of one rescale per term;
+//   * block-constant plaintexts (kernel vectors, masked kernel vectors, biases)
+//     are built on the GPU as linear combinations of cached block-indicator
+//     encodings -- no host FFT per plaintext;
+//   * the Chebyshev T_d tree is evaluated band by band (all d in
+//     (2^{g-1}, 2^g] together) with batched relinearisation.
+// Event ORDER differs from the reference where independent ops are batched;
+// the event multiset (what keyplan/ledger consume) is identical.
 #include "layers.hpp"
 
 #include <algorithm>
@@ -44,6 +55,48 @@ Ciphertext mp(Context& ctx, const Ciphertext& x, const std::vector<double>& full
   return mult_plain(ctx, x, full.data(), full.size());
 }
 
+// plaintext for `like` from slot values (content-cached host encode)
+BufPtr pt_of(Context& ctx, const Ciphertext& like, const std::vector<double>& full) {
+  return ctx.encode_cached(full, like.limbs, pt_scale_for(ctx, like));
+}
+
+// indicator of block c (size m) as a cached device basis vector
+const double* block_basis(Context& ctx, std::size_t m, std::size_t c) {
+  std::vector<double> v((c + 1) * m, 0.0);
+  std::fill(v.begin() + (long)(c * m), v.end(), 1.0);
+  return ctx.basis("blk:" + std::to_string(m) + ":" + std::to_string(c), v);
+}
+
+// plaintext sum_c w[c] * 1_{block c} at `like`'s level and pt scale (GPU-built)
+BufPtr pt_blocks(Context& ctx, const Ciphertext& like, const std::vector<double>& w, std::size_t m, double scale) {
+  LinComb lc{};
+  for (std::size_t c = 0; c < w.size(); ++c) {
+    if (w[c] == 0.0) continue;
+    if (lc.nb == kMaxBasis) throw Error(ErrKind::capacity, "too many plaintext blocks");
+    lc.basis[lc.nb] = block_basis(ctx, m, c);
+    lc.w[lc.nb] = w[c];
+    ++lc.nb;
+  }
+  return ctx.encode_lincomb(lc, like.limbs, scale);
+}
+
+// single-term MAC over a batch: out[i] = rescale(xs[i] (*) pts[i])
+std::vector<Ciphertext> mp_many(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<BufPtr>& pts) {
+  std::vector<std::vector<Ciphertext>> t(xs.size());
+  std::vector<std::vector<BufPtr>> p(xs.size());
+  for (std::size_t i = 0; i < xs.size(); ++i) {
+    t[i] = {xs[i]};
+    p[i] = {pts[i]};
+  }
+  return mac_plain_many(ctx, t, p);
+}
+
+Ciphertext sum_all(Context& ctx, const std::vector<Ciphertext>& v) {
+  Ciphertext acc = v.at(0);
+  for (std::size_t i = 1; i < v.size(); ++i) acc = add(ctx, acc, v[i]);
+  return acc;
+}
+
 void check_stride_geometry(const Context& ctx, const Ciphertext& a, std::size_t W, std::size_t S, std::size_t W_out) {
   if (!a.valid()) throw Error(ErrKind::internal, "striding: operand is not initialized");
   if (W == 0 || S == 0 || W_out == 0) throw shape_error("striding: width, stride and output edge must be positive");
@@ -56,20 +109,17 @@ void check_stride_geometry(const Context& ctx, const Ciphertext& a, std::size_t 
 
 // bias_vector (layers_conv.cpp:77-85) added as a plaintext at the operand's level
 Ciphertext add_bias(Context& ctx, const Ciphertext& out, const std::vector<double>& bias, std::size_t block) {
-  std::vector<double> v(bias.size() * block);
-  for (std::size_t f = 0; f < bias.size(); ++f)
-    std::fill(v.begin() + (long)(f * block), v.begin() + (long)((f + 1) * block), bias[f]);
-  if (v.size() > (std::size_t)ctx.S()) throw capacity_error("bias does not fit in the slot count");
-  return add_plain(ctx, out, v.data(), v.size());
-}
-
-std::vector<double> member_kernel_vector(const KernelTensor& w, std::size_t f, std::size_t ti, std::size_t tj,
-                                         std::size_t c, std::size_t C, std::size_t W) {
-  const std::size_t block = W * W;
-  std::vector<double> out(C * block, 0.0);
-  const double v = w.at(f, 0, ti, tj);
-  std::fill(out.begin() + (long)(c * block), out.begin() + (long)((c + 1) * block), v);
-  return out;
+  if (bias.size() * block > (std::size_t)ctx.S()) throw capacity_error("bias does not fit in the slot count");
+  bool any = false;
+  for (double b : bias) any = any || b != 0.0;
+  if (!any) return add_const(ctx, out, 0.0);  // exact zero plaintext
+  if (bias.size() > (std::size_t)kMaxBasis) {
+    std::vector<double> v(bias.size() * block);
+    for (std::size_t f = 0; f < bias.size(); ++f)
+      std::fill(v.begin() + (long)(f * block), v.begin() + (long)((f + 1) * block), bias[f]);
+    return add_plain(ctx, out, v.data(), v.size());
+  }
+  return add_plain_pt(ctx, out, pt_blocks(ctx, out, bias, block, out.scale));
 }
 
 // tap_rotations (layers_conv.cpp:102-113): one hoisted ModUp for all k^2-1 taps
@@ -86,17 +136,32 @@ std::vector<Ciphertext> tap_rotations(Context& ctx, const Ciphertext& x, std::si
   return taps;
 }
 
-// Channel accumulation chain (layers_conv.cpp:155-161): C-1 rotations by m
-Ciphertext channel_accumulate(Context& ctx, Ciphertext sum, std::size_t C, std::size_t m) {
-  if (C > 1) {
-    Ciphertext cur = sum;
-    for (std::size_t c = 1; c < C; ++c) {
-      cur = rotate(ctx, cur, (long)m);
-      sum = add(ctx, sum, cur);
-    }
+// Channel accumulation chains (layers_conv.cpp:155-161), all output channels
+// advanced together: C-1 batched rotations by m.
+std::vector<Ciphertext> channel_accumulate_many(Context& ctx, std::vector<Ciphertext> sums, std::size_t C,
+                                                std::size_t m) {
+  if (C <= 1) return sums;
+  std::vector<Ciphertext> cur = sums;
+  for (std::size_t c = 1; c < C; ++c) {
+    cur = rotate_many(ctx, cur, std::vector<long>(cur.size(), (long)m));
+    sums = add_many(ctx, sums, cur);
   }
-  return sum;
+  return sums;
 }
+
+// out = sum_f rotate(r_f, -f * block): placement rotations batched
+Ciphertext place_and_sum(Context& ctx, const std::vector<Ciphertext>& r, std::size_t block) {
+  std::vector<Ciphertext> xs(r.begin() + 1, r.end());
+  std::vector<long> ts;
+  for (std::size_t f = 1; f < r.size(); ++f) ts.push_back(-(long)(f * block));
+  std::vector<Ciphertext> placed = rotate_many(ctx, xs, ts);
+  Ciphertext out = r[0];
+  for (const Ciphertext& p : placed) out = add(ctx, out, p);
+  return out;
+}
+
+std::vector<Ciphertext> stride_many(Context& ctx, const std::vector<Ciphertext>& a, std::size_t W, std::size_t S,
+                                    std::size_t W_out, int variant);
 
 // conv_core_generic (layers_conv.cpp:117-180)
 PackedTensor conv_core_generic(Context& ctx, const PackedTensor& x, const ConvConfig& cfg, const KernelTensor& w) {
@@ -112,24 +177,26 @@ PackedTensor conv_core_generic(Context& ctx, const PackedTensor& x, const ConvCo
   if (F * W_out * W_out > (std::size_t)ctx.S())
     throw capacity_error("convolution output needs " + std::to_string(F * W_out * W_out) +
                          " slots but the context provides " + std::to_string(ctx.S()));
+  if (C > (std::size_t)kMaxBasis) throw capacity_error("too many input channels for one plaintext combination");
   const std::vector<Ciphertext> taps = tap_rotations(ctx, x.data, k, W);
-  const std::vector<double> cleanup = plain(ctx, extraction_mask(W, C));
-  Ciphertext out;
-  for (std::size_t f = 0; f < F; ++f) {
-    Ciphertext sum;
+  const double ps = pt_scale_for(ctx, taps[0]);
+  // fused rotate-and-MAC: sum_f = sum_taps tap (*) repeated_kernel_vector(f, tap)
+  std::vector<std::vector<Ciphertext>> terms(F, taps);
+  std::vector<std::vector<BufPtr>> pts(F);
+  for (std::size_t f = 0; f < F; ++f)
     for (std::size_t i = 0; i < k; ++i)
       for (std::size_t j = 0; j < k; ++j) {
-        const Ciphertext term = mp(ctx, taps[i * k + j], plain(ctx, repeated_kernel_vector(w, f, i, j, C, W)));
-        sum = (i == 0 && j == 0) ? term : add(ctx, sum, term);
+        std::vector<double> wc(C);
+        for (std::size_t c = 0; c < C; ++c) wc[c] = w.at(f, c, i, j);
+        pts[f].push_back(pt_blocks(ctx, taps[0], wc, m, ps));
       }
-    sum = channel_accumulate(ctx, sum, C, m);
-    const Ciphertext a_star = mp(ctx, sum, cleanup);
-    Ciphertext r_f;
-    if (S == 1 && W_out == W) r_f = a_star;
-    else if (cfg.stride_variant == 1) r_f = stride_extract_v2(ctx, a_star, W, S, W_out);
-    else r_f = stride_extract_v1(ctx, a_star, W, S, W_out);
-    out = (f == 0) ? r_f : add(ctx, out, rotate(ctx, r_f, -(long)(f * W_out * W_out)));
-  }
+  std::vector<Ciphertext> sums = mac_plain_many(ctx, terms, pts);
+  sums = channel_accumulate_many(ctx, sums, C, m);
+  const BufPtr cleanup = pt_of(ctx, sums[0], plain(ctx, extraction_mask(W, C)));
+  std::vector<Ciphertext> a_star = mp_many(ctx, sums, std::vector<BufPtr>(F, cleanup));
+  std::vector<Ciphertext> r =
+      (S == 1 && W_out == W) ? a_star : stride_many(ctx, a_star, W, S, W_out, cfg.stride_variant);
+  Ciphertext out = place_and_sum(ctx, r, W_out * W_out);
   out = add_bias(ctx, out, w.bias, W_out * W_out);
   return {out, F, W_out};
 }
@@ -141,19 +208,31 @@ PackedTensor conv_grouped_fallback(Context& ctx, const PackedTensor& x, const Co
   const std::size_t F = cfg.out_channels, k = cfg.kernel, S = cfg.stride;
   const std::size_t m = W * W;
   const std::vector<Ciphertext> taps = tap_rotations(ctx, x.data, k, W);
-  Ciphertext out;
-  for (std::size_t f = 0; f < F; ++f) {
-    const std::size_t c = f % g;
-    Ciphertext sum;
+  const double ps = pt_scale_for(ctx, taps[0]);
+  std::vector<std::vector<Ciphertext>> terms(F, taps);
+  std::vector<std::vector<BufPtr>> pts(F);
+  for (std::size_t f = 0; f < F; ++f)
     for (std::size_t i = 0; i < k; ++i)
       for (std::size_t j = 0; j < k; ++j) {
-        const Ciphertext term = mp(ctx, taps[i * k + j], plain(ctx, member_kernel_vector(w, f, i, j, c, g, W)));
-        sum = (i == 0 && j == 0) ? term : add(ctx, sum, term);
+        std::vector<double> wc(f % g + 1, 0.0);
+        wc[f % g] = w.at(f, 0, i, j);
+        pts[f].push_back(pt_blocks(ctx, taps[0], wc, m, ps));
       }
-    if (c > 0) sum = rotate(ctx, sum, (long)(c * m));
-    const Ciphertext r_f = stride_extract_v1(ctx, sum, W, S, W_out);
-    out = (f == 0) ? r_f : add(ctx, out, rotate(ctx, r_f, -(long)(f * W_out * W_out)));
-  }
+  std::vector<Ciphertext> sums = mac_plain_many(ctx, terms, pts);
+  // bring member c's block to the front (c > 0): batched
+  std::vector<Ciphertext> xs;
+  std::vector<long> ts;
+  std::vector<std::size_t> who;
+  for (std::size_t f = 0; f < F; ++f)
+    if (f % g > 0) {
+      xs.push_back(sums[f]);
+      ts.push_back((long)((f % g) * m));
+      who.push_back(f);
+    }
+  std::vector<Ciphertext> moved = rotate_many(ctx, xs, ts);
+  for (std::size_t i = 0; i < who.size(); ++i) sums[who[i]] = moved[i];
+  std::vector<Ciphertext> r = stride_many(ctx, sums, W, S, W_out, 0);
+  Ciphertext out = place_and_sum(ctx, r, W_out * W_out);
   out = add_bias(ctx, out, w.bias, W_out * W_out);
   return {out, F, W_out};
 }
@@ -237,44 +316,79 @@ PackedTensor pad_input(Context& ctx, const PackedTensor& x, std::size_t padding)
     throw capacity_error("padded tensor needs " + std::to_string(C * mp_) + " slots but the context provides " +
                          std::to_string(ctx.S()));
   const std::vector<double> rowmask = range_mask(ctx, 0, W);
-  Ciphertext out, chancur;
-  for (std::size_t c = 0; c < C; ++c) {
-    chancur = (c == 0) ? x.data : rotate(ctx, chancur, (long)(W * W));
-    std::vector<Ciphertext> rows;
-    rows.reserve(W);
-    Ciphertext rowcur = chancur;
-    for (std::size_t r = 0; r < W; ++r) {
-      if (r > 0) rowcur = rotate(ctx, rowcur, (long)W);
-      rows.push_back(mp(ctx, rowcur, rowmask));
-    }
-    Ciphertext racc = rows[W - 1];
-    for (std::size_t r = W - 1; r-- > 0;) racc = add(ctx, rotate(ctx, racc, -(long)Wp), rows[r]);
-    out = (c == 0) ? racc : add(ctx, out, rotate(ctx, racc, -(long)(c * mp_)));
+  // channel cursor chain, then every channel's row cursor chain advanced together
+  std::vector<Ciphertext> chans{x.data};
+  for (std::size_t c = 1; c < C; ++c) chans.push_back(rotate(ctx, chans.back(), (long)(W * W)));
+  std::vector<std::vector<Ciphertext>> rowcur(W);
+  rowcur[0] = chans;
+  for (std::size_t r = 1; r < W; ++r) rowcur[r] = rotate_many(ctx, rowcur[r - 1], std::vector<long>(C, (long)W));
+  const BufPtr rm = pt_of(ctx, x.data, rowmask);
+  std::vector<Ciphertext> flat;
+  for (std::size_t r = 0; r < W; ++r) flat.insert(flat.end(), rowcur[r].begin(), rowcur[r].end());
+  std::vector<Ciphertext> rows_flat = mp_many(ctx, flat, std::vector<BufPtr>(flat.size(), rm));
+  // re-space rows back to front (dependent chain per channel, channels batched)
+  std::vector<Ciphertext> racc(rows_flat.begin() + (long)((W - 1) * C), rows_flat.begin() + (long)(W * C));
+  for (std::size_t r = W - 1; r-- > 0;) {
+    std::vector<Ciphertext> rot = rotate_many(ctx, racc, std::vector<long>(C, -(long)Wp));
+    std::vector<Ciphertext> rows_r(rows_flat.begin() + (long)(r * C), rows_flat.begin() + (long)((r + 1) * C));
+    racc = add_many(ctx, rot, rows_r);
   }
+  Ciphertext out = place_and_sum(ctx, racc, mp_);
   out = rotate(ctx, out, -(long)(P * (Wp + 1)));
   return {out, C, Wp};
 }
 
-// stride_extract_v1 (layers_conv.cpp:289-317)
-Ciphertext stride_extract_v1(Context& ctx, const Ciphertext& a_star, std::size_t W, std::size_t S, std::size_t W_out) {
-  check_stride_geometry(ctx, a_star, W, S, W_out);
-  Ciphertext out, vcur = a_star;
+// stride_extract_v1 (layers_conv.cpp:289-317), batched over several inputs
+std::vector<Ciphertext> stride_v1_many(Context& ctx, const std::vector<Ciphertext>& as, std::size_t W, std::size_t S,
+                                       std::size_t W_out) {
+  for (const Ciphertext& a : as) check_stride_geometry(ctx, a, W, S, W_out);
+  const std::size_t B = as.size();
+  std::vector<Ciphertext> vcur = as;
+  std::vector<std::vector<Ciphertext>> rows(W_out);
   for (std::size_t a = 0; a < W_out; ++a) {
-    if (a > 0) vcur = rotate(ctx, vcur, (long)(S * W));
-    Ciphertext row;
+    if (a > 0) vcur = rotate_many(ctx, vcur, std::vector<long>(B, (long)(S * W)));
     if (S == 1) {
-      row = mp(ctx, vcur, range_mask(ctx, 0, W_out));
+      rows[a] = mp_many(ctx, vcur, std::vector<BufPtr>(B, pt_of(ctx, vcur[0], range_mask(ctx, 0, W_out))));
     } else {
-      row = mp(ctx, vcur, range_mask(ctx, 0, 1));
-      Ciphertext hcur = vcur;
-      for (std::size_t b = 1; b < W_out; ++b) {
-        hcur = rotate(ctx, hcur, (long)(S - 1));
-        row = add(ctx, row, mp(ctx, hcur, range_mask(ctx, b, 1)));
+      // gather kept columns: hcur_b = rot^b(vcur, S-1); row = sum_b hcur_b (*) e_b (fused MAC)
+      std::vector<std::vector<Ciphertext>> terms(B);
+      std::vector<std::vector<BufPtr>> pts(B);
+      std::vector<Ciphertext> hcur = vcur;
+      for (std::size_t b = 0; b < W_out; ++b) {
+        if (b > 0) hcur = rotate_many(ctx, hcur, std::vector<long>(B, (long)(S - 1)));
+        const BufPtr e = pt_of(ctx, vcur[0], range_mask(ctx, b, 1));
+        for (std::size_t i = 0; i < B; ++i) {
+          terms[i].push_back(hcur[i]);
+          pts[i].push_back(e);
+        }
       }
+      rows[a] = mac_plain_many(ctx, terms, pts);
     }
-    out = (a == 0) ? row : add(ctx, out, rotate(ctx, row, -(long)(a * W_out)));
+  }
+  // row placements: all (a, input) pairs in one batch
+  std::vector<Ciphertext> xs;
+  std::vector<long> ts;
+  for (std::size_t a = 1; a < W_out; ++a)
+    for (std::size_t i = 0; i < B; ++i) {
+      xs.push_back(rows[a][i]);
+      ts.push_back(-(long)(a * W_out));
+    }
+  std::vector<Ciphertext> placed = rotate_many(ctx, xs, ts);
+  std::vector<Ciphertext> out = rows[0];
+  for (std::size_t a = 1; a < W_out; ++a) {
+    std::vector<Ciphertext> pa(placed.begin() + (long)((a - 1) * B), placed.begin() + (long)(a * B));
+    out = add_many(ctx, out, pa);
   }
   return out;
+}
+
+Ciphertext stride_extract_v1(Context& ctx, const Ciphertext& a_star, std::size_t W, std::size_t S, std::size_t W_out) {
+  return stride_v1_many(ctx, {a_star}, W, S, W_out)[0];
+}
+
+namespace detail {
+std::vector<Ciphertext> stride_mask_compact_many(Context& ctx, const std::vector<Ciphertext>& ys, std::size_t W,
+                                                 std::size_t S, std::size_t W_out, std::size_t blocks);
 }
 
 // stride_extract_v2 (layers_conv.cpp:323-334)
@@ -287,6 +401,18 @@ Ciphertext stride_extract_v2(Context& ctx, const Ciphertext& a_star, std::size_t
   return detail::stride_mask_compact(ctx, a_star, W, S, W_out, 1);
 }
 
+namespace {
+std::vector<Ciphertext> stride_many(Context& ctx, const std::vector<Ciphertext>& a, std::size_t W, std::size_t S,
+                                    std::size_t W_out, int variant) {
+  if (variant == 1) {
+    for (const Ciphertext& c : a) check_stride_geometry(ctx, c, W, S, W_out);
+    if (detail::masked_stride_applicable(W_out)) return detail::stride_mask_compact_many(ctx, a, W, S, W_out, 1);
+    ctx.record(4, 0, "striding: masked flavor needs a power-of-two output edge >= 2; using the extraction flavor");
+  }
+  return stride_v1_many(ctx, a, W, S, W_out);
+}
+}  // namespace
+
 namespace detail {
 
 bool masked_stride_applicable(std::size_t W_out) { return W_out >= 2 && is_pow2(W_out); }
@@ -295,25 +421,26 @@ int stride_mask_compact_depth(std::size_t S, std::size_t W_out) {
   return S >= 2 ? (int)log2_exact(W_out) + 1 : 2;
 }
 
-// stride_mask_compact (layers_conv.cpp:349-421)
-Ciphertext stride_mask_compact(Context& ctx, const Ciphertext& y, std::size_t W, std::size_t S, std::size_t W_out,
-                               std::size_t blocks) {
-  check_stride_geometry(ctx, y, W, S, W_out);
+// stride_mask_compact (layers_conv.cpp:349-421), batched over several inputs
+std::vector<Ciphertext> stride_mask_compact_many(Context& ctx, const std::vector<Ciphertext>& ys, std::size_t W,
+                                                 std::size_t S, std::size_t W_out, std::size_t blocks) {
+  for (const Ciphertext& y : ys) check_stride_geometry(ctx, y, W, S, W_out);
   if (!masked_stride_applicable(W_out))
     throw Error(ErrKind::internal, "masked compaction requires a power-of-two output edge");
   const std::size_t m = W * W;
   if (blocks * m > (std::size_t)ctx.S() || blocks * W_out * W_out > (std::size_t)ctx.S())
     throw capacity_error("masked compaction does not fit in the slot count");
+  const std::size_t B = ys.size();
   std::vector<double> sel(blocks * m, 0.0);
   for (std::size_t c = 0; c < blocks; ++c)
     for (std::size_t a = 0; a < W_out; ++a)
       for (std::size_t b = 0; b < W_out; ++b) sel[c * m + (S * a) * W + S * b] = 1.0;
-  Ciphertext cur = mp(ctx, y, plain(ctx, sel));
+  std::vector<Ciphertext> cur = mp_many(ctx, ys, std::vector<BufPtr>(B, pt_of(ctx, ys[0], plain(ctx, sel))));
   if (S >= 2) {
     const std::size_t l = log2_exact(W_out);
     for (std::size_t s = 1; s < l; ++s) {
       const long amount = (long)((S - 1) << (s - 1));
-      const Ciphertext merged = add(ctx, cur, rotate(ctx, cur, amount));
+      std::vector<Ciphertext> merged = add_many(ctx, cur, rotate_many(ctx, cur, std::vector<long>(B, amount)));
       std::vector<double> keep(blocks * m, 0.0);
       const std::size_t period = S << s;
       const std::size_t run = std::size_t{1} << s;
@@ -321,24 +448,35 @@ Ciphertext stride_mask_compact(Context& ctx, const Ciphertext& y, std::size_t W,
         for (std::size_t a = 0; a < W_out; ++a)
           for (std::size_t j = 0; j < W; ++j)
             if (j % period < run) keep[c * m + (S * a) * W + j] = 1.0;
-      cur = mp(ctx, merged, plain(ctx, keep));
+      cur = mp_many(ctx, merged, std::vector<BufPtr>(B, pt_of(ctx, merged[0], plain(ctx, keep))));
     }
-    cur = add(ctx, cur, rotate(ctx, cur, (long)((S - 1) << (l - 1))));
+    cur = add_many(ctx, cur, rotate_many(ctx, cur, std::vector<long>(B, (long)((S - 1) << (l - 1)))));
   }
+  // gather rows/blocks with one cumulative cursor; all masks apply to rotations
+  // of the same value (one level) -> one fused MAC per input
   const std::size_t step_row = S * W - W_out;
   const std::size_t step_chan = W * W - S * W * (W_out - 1) - W_out;
-  Ciphertext acc, cursor = cur;
+  std::vector<std::vector<Ciphertext>> terms(B);
+  std::vector<std::vector<BufPtr>> pts(B);
+  std::vector<Ciphertext> cursor = cur;
   for (std::size_t c = 0; c < blocks; ++c)
     for (std::size_t a = 0; a < W_out; ++a) {
       if (c != 0 || a != 0) {
         const std::size_t step = (a == 0) ? step_chan : step_row;
-        if (step != 0) cursor = rotate(ctx, cursor, (long)step);
+        if (step != 0) cursor = rotate_many(ctx, cursor, std::vector<long>(B, (long)step));
       }
-      const std::size_t dst = (c * W_out + a) * W_out;
-      const Ciphertext piece = mp(ctx, cursor, range_mask(ctx, dst, W_out));
-      acc = (c == 0 && a == 0) ? piece : add(ctx, acc, piece);
+      const BufPtr e = pt_of(ctx, cur[0], range_mask(ctx, (c * W_out + a) * W_out, W_out));
+      for (std::size_t i = 0; i < B; ++i) {
+        terms[i].push_back(cursor[i]);
+        pts[i].push_back(e);
+      }
     }
-  return acc;
+  return mac_plain_many(ctx, terms, pts);
+}
+
+Ciphertext stride_mask_compact(Context& ctx, const Ciphertext& y, std::size_t W, std::size_t S, std::size_t W_out,
+                               std::size_t blocks) {
+  return stride_mask_compact_many(ctx, {y}, W, S, W_out, blocks)[0];
 }
 
 std::vector<long> block_sum_rotations(std::size_t span) {
@@ -370,14 +508,21 @@ Ciphertext block_sum(Context& ctx, const Ciphertext& v, std::size_t span) {
     sums.push_back(add(ctx, sums.back(), rotate(ctx, sums.back(), (long)p)));
     p *= 2;
   }
-  Ciphertext acc;
+  // the tail combination rotates distinct partial sums: one batch
+  std::vector<Ciphertext> parts;
+  std::vector<long> offs;
   std::size_t off = 0;
   for (std::size_t bit = std::bit_width(span); bit-- > 0;) {
     if (((span >> bit) & 1u) == 0) continue;
-    const Ciphertext& part = sums[bit];
-    acc = (off == 0) ? part : add(ctx, acc, rotate(ctx, part, (long)off));
+    parts.push_back(sums[bit]);
+    offs.push_back((long)off);
     off += std::size_t{1} << bit;
   }
+  std::vector<Ciphertext> xs(parts.begin() + 1, parts.end());
+  std::vector<long> ts(offs.begin() + 1, offs.end());
+  std::vector<Ciphertext> rot = rotate_many(ctx, xs, ts);
+  Ciphertext acc = parts[0];
+  for (const Ciphertext& r : rot) acc = add(ctx, acc, r);
   return acc;
 }
 
@@ -400,43 +545,40 @@ PackedTensor conv_special_3x3(Context& ctx, const PackedTensor& x, const ConvCon
     throw shape_error("kernel tensor shape does not match the layer config");
   const std::size_t m = W * W;
   if (F * m > (std::size_t)ctx.S()) throw capacity_error("convolution output does not fit in the slot count");
+  if (C > (std::size_t)kMaxBasis) throw capacity_error("too many input channels for one plaintext combination");
   const std::vector<Ciphertext> ud = rotate_hoisted(ctx, x.data, {-(long)W, (long)W});
-  const Ciphertext& up = ud[0];
-  const Ciphertext& down = ud[1];
-  std::vector<Ciphertext> taps(9);
-  {
-    std::vector<Ciphertext> r = rotate_hoisted(ctx, up, {-1, 1});
-    taps[0] = r[0];
-    taps[2] = r[1];
-  }
-  taps[1] = up;
-  {
-    std::vector<Ciphertext> r = rotate_hoisted(ctx, x.data, {-1, 1});
-    taps[3] = r[0];
-    taps[5] = r[1];
-  }
-  taps[4] = x.data;
-  {
-    std::vector<Ciphertext> r = rotate_hoisted(ctx, down, {-1, 1});
-    taps[6] = r[0];
-    taps[8] = r[1];
-  }
-  taps[7] = down;
+  // the six +-1 shifts of up / x / down: one batched key switch (three hoisted pairs)
+  const std::vector<Ciphertext> sh = rotate_many(ctx, {ud[0], ud[0], x.data, x.data, ud[1], ud[1]}, {-1, 1, -1, 1, -1, 1});
+  const std::vector<Ciphertext> taps = {sh[0], ud[0], sh[1], sh[2], x.data, sh[3], sh[4], ud[1], sh[5]};
   const std::array<std::vector<double>, 9> masks = build_all_masks(m, C, W);
-  const std::vector<double> cleanup = plain(ctx, extraction_mask(W, C));
-  Ciphertext out;
-  for (std::size_t f = 0; f < F; ++f) {
-    Ciphertext sum;
-    for (std::size_t tap = 0; tap < 9; ++tap) {
-      std::vector<double> kv = repeated_kernel_vector(w, f, tap / 3, tap % 3, C, W);
-      for (std::size_t i = 0; i < kv.size(); ++i) kv[i] *= masks[tap][i];
-      const Ciphertext term = mp(ctx, taps[tap], plain(ctx, kv));
-      sum = (tap == 0) ? term : add(ctx, sum, term);
+  const double ps = pt_scale_for(ctx, taps[4]);
+  // basis: mask_tap restricted to block c (masks folded into the kernel companions)
+  std::vector<std::vector<const double*>> bases(9, std::vector<const double*>(C));
+  for (std::size_t tap = 0; tap < 9; ++tap)
+    for (std::size_t c = 0; c < C; ++c) {
+      std::vector<double> v((c + 1) * m, 0.0);
+      for (std::size_t i = 0; i < m; ++i) v[c * m + i] = masks[tap][c * m + i];
+      bases[tap][c] = ctx.basis("m3:" + std::to_string(W) + ":" + std::to_string(tap) + ":" + std::to_string(c), v);
     }
-    sum = channel_accumulate(ctx, sum, C, m);
-    const Ciphertext cleaned = mp(ctx, sum, cleanup);
-    out = (f == 0) ? cleaned : add(ctx, out, rotate(ctx, cleaned, -(long)(f * m)));
-  }
+  std::vector<std::vector<Ciphertext>> terms(F, taps);
+  std::vector<std::vector<BufPtr>> pts(F);
+  for (std::size_t f = 0; f < F; ++f)
+    for (std::size_t tap = 0; tap < 9; ++tap) {
+      LinComb lc{};
+      for (std::size_t c = 0; c < C; ++c) {
+        const double wv = w.at(f, c, tap / 3, tap % 3);
+        if (wv == 0.0) continue;
+        lc.basis[lc.nb] = bases[tap][c];
+        lc.w[lc.nb] = wv;
+        ++lc.nb;
+      }
+      pts[f].push_back(ctx.encode_lincomb(lc, taps[4].limbs, ps));
+    }
+  std::vector<Ciphertext> sums = mac_plain_many(ctx, terms, pts);
+  sums = channel_accumulate_many(ctx, sums, C, m);
+  const BufPtr cleanup = pt_of(ctx, sums[0], plain(ctx, extraction_mask(W, C)));
+  std::vector<Ciphertext> cleaned = mp_many(ctx, sums, std::vector<BufPtr>(F, cleanup));
+  Ciphertext out = place_and_sum(ctx, cleaned, m);
   out = add_bias(ctx, out, w.bias, m);
   return {out, F, W};
 }
@@ -457,22 +599,24 @@ PackedTensor conv_grouped_stride(Context& ctx, const PackedTensor& x, const Conv
     ctx.record(4, 0, "grouped striding needs a power-of-two output edge >= 2; using per-member extraction");
     return conv_grouped_fallback(ctx, xp, cfg, w, W_out);
   }
+  const std::size_t m = W * W;
   const std::vector<Ciphertext> taps = tap_rotations(ctx, xp.data, k, W);
+  const double ps = pt_scale_for(ctx, taps[0]);
   const std::size_t groups = F / g;
-  std::vector<Ciphertext> packed;
-  packed.reserve(groups);
-  for (std::size_t u = 0; u < groups; ++u) {
-    Ciphertext joint;
-    for (std::size_t c = 0; c < g; ++c) {
-      const std::size_t f = u * g + c;
+  // joint_u = sum_{c, tap} tap (*) member_kernel_vector(u*g + c, tap, c): one MAC per group
+  std::vector<std::vector<Ciphertext>> terms(groups);
+  std::vector<std::vector<BufPtr>> pts(groups);
+  for (std::size_t u = 0; u < groups; ++u)
+    for (std::size_t c = 0; c < g; ++c)
       for (std::size_t i = 0; i < k; ++i)
         for (std::size_t j = 0; j < k; ++j) {
-          const Ciphertext term = mp(ctx, taps[i * k + j], plain(ctx, member_kernel_vector(w, f, i, j, c, g, W)));
-          joint = (c == 0 && i == 0 && j == 0) ? term : add(ctx, joint, term);
+          std::vector<double> wc(c + 1, 0.0);
+          wc[c] = w.at(u * g + c, 0, i, j);
+          terms[u].push_back(taps[i * k + j]);
+          pts[u].push_back(pt_blocks(ctx, taps[0], wc, m, ps));
         }
-    }
-    packed.push_back(detail::stride_mask_compact(ctx, joint, W, S, W_out, g));
-  }
+  std::vector<Ciphertext> joint = mac_plain_many(ctx, terms, pts);
+  std::vector<Ciphertext> packed = detail::stride_mask_compact_many(ctx, joint, W, S, W_out, g);
   Ciphertext out = packed[groups - 1];
   for (std::size_t u = groups - 1; u-- > 0;) out = add(ctx, rotate(ctx, out, -(long)(g * W_out * W_out)), packed[u]);
   out = add_bias(ctx, out, w.bias, W_out * W_out);
@@ -507,13 +651,10 @@ PackedTensor avg_pool(Context& ctx, const PackedTensor& x, std::size_t k, std::s
   }
   const Ciphertext T2 = mp(ctx, T, range_mask(ctx, 0, C * m, 1.0 / (double)(k * k)));
   if (S == 1 && W_out == W) return {T2, C, W};
-  Ciphertext out, ccur = T2;
-  for (std::size_t c = 0; c < C; ++c) {
-    if (c > 0) ccur = rotate(ctx, ccur, (long)m);
-    const Ciphertext r_c =
-        variant == 1 ? stride_extract_v2(ctx, ccur, W, S, W_out) : stride_extract_v1(ctx, ccur, W, S, W_out);
-    out = (c == 0) ? r_c : add(ctx, out, rotate(ctx, r_c, -(long)(c * W_out * W_out)));
-  }
+  std::vector<Ciphertext> chans{T2};
+  for (std::size_t c = 1; c < C; ++c) chans.push_back(rotate(ctx, chans.back(), (long)m));
+  std::vector<Ciphertext> r = stride_many(ctx, chans, W, S, W_out, variant);
+  Ciphertext out = place_and_sum(ctx, r, W_out * W_out);
   return {out, C, W_out};
 }
 
@@ -524,20 +665,21 @@ Ciphertext merge_channel_slots(Context& ctx, const std::vector<Ciphertext>& piec
   for (std::size_t c = pieces.size() - 1; c-- > 0;) out = add(ctx, rotate(ctx, out, -1), pieces[c]);
   return out;
 }
+
+std::vector<Ciphertext> channel_cursors(Context& ctx, const Ciphertext& sums, std::size_t C, std::size_t m) {
+  std::vector<Ciphertext> cur{sums};
+  for (std::size_t c = 1; c < C; ++c) cur.push_back(rotate(ctx, cur.back(), (long)m));
+  return cur;
+}
 }  // namespace
 
 // global_avg_pool (layers_misc.cpp:146-166)
 Ciphertext global_avg_pool(Context& ctx, const PackedTensor& x) {
   const std::size_t W = x.width, C = x.channels, m = W * W;
   const Ciphertext sums = detail::block_sum(ctx, x.data, m);
-  const std::vector<double> head = range_mask(ctx, 0, 1, 1.0 / (double)m);
-  std::vector<Ciphertext> pieces;
-  Ciphertext ccur = sums;
-  for (std::size_t c = 0; c < C; ++c) {
-    if (c > 0) ccur = rotate(ctx, ccur, (long)m);
-    pieces.push_back(mp(ctx, ccur, head));
-  }
-  return merge_channel_slots(ctx, pieces);
+  const std::vector<Ciphertext> cur = channel_cursors(ctx, sums, C, m);
+  const BufPtr head = pt_of(ctx, sums, range_mask(ctx, 0, 1, 1.0 / (double)m));
+  return merge_channel_slots(ctx, mp_many(ctx, cur, std::vector<BufPtr>(C, head)));
 }
 
 // whole_channel_pool (layers_misc.cpp:168-195)
@@ -546,18 +688,13 @@ Ciphertext whole_channel_pool(Context& ctx, const PackedTensor& x, std::size_t k
   const std::size_t W = x.width, C = x.channels, m = W * W;
   const Ciphertext v = mp(ctx, x.data, range_mask(ctx, 0, C * m, 1.0 / (double)(k * k)));
   const Ciphertext sums = detail::block_sum(ctx, v, m);
-  const std::vector<double> head = range_mask(ctx, 0, 1);
-  std::vector<Ciphertext> pieces;
-  Ciphertext ccur = sums;
-  for (std::size_t c = 0; c < C; ++c) {
-    if (c > 0) ccur = rotate(ctx, ccur, (long)m);
-    pieces.push_back(mp(ctx, ccur, head));
-  }
-  return merge_channel_slots(ctx, pieces);
+  const std::vector<Ciphertext> cur = channel_cursors(ctx, sums, C, m);
+  const BufPtr head = pt_of(ctx, sums, range_mask(ctx, 0, 1));
+  return merge_channel_slots(ctx, mp_many(ctx, cur, std::vector<BufPtr>(C, head)));
 }
 
 // ------------------------------------------------------------- FC
-// fully_connected (layers_misc.cpp:197-255)
+// fully_connected (layers_misc.cpp:197-255): neurons batched
 Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std::size_t m, std::size_t B,
                            const double* w, const double* bias) {
   if (n == 0 || m == 0) throw shape_error("fully-connected layer needs positive input/output sizes");
@@ -565,22 +702,33 @@ Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std
     throw capacity_error("fully-connected layer does not fit in the slot count");
   if (B == 0) throw shape_error("merge budget must be >= 1");
   const std::size_t p2 = std::bit_ceil(n);
-  const std::vector<double> head = range_mask(ctx, 0, 1);
-  std::vector<Ciphertext> neurons;
-  neurons.reserve(m);
-  for (std::size_t i = 0; i < m; ++i) {
-    std::vector<double> row(w + i * n, w + (i + 1) * n);
-    Ciphertext y = mp(ctx, x, plain(ctx, row));
-    for (std::size_t off = 1; off < p2; off <<= 1) y = add(ctx, y, rotate(ctx, y, (long)off));
-    neurons.push_back(mp(ctx, y, head));
-  }
+  std::vector<BufPtr> rows;
+  rows.reserve(m);
+  for (std::size_t i = 0; i < m; ++i) rows.push_back(pt_of(ctx, x, plain(ctx, std::vector<double>(w + i * n, w + (i + 1) * n))));
+  std::vector<Ciphertext> y = mp_many(ctx, std::vector<Ciphertext>(m, x), rows);
+  for (std::size_t off = 1; off < p2; off <<= 1)
+    y = add_many(ctx, y, rotate_many(ctx, y, std::vector<long>(m, (long)off)));
+  const BufPtr head = pt_of(ctx, y[0], range_mask(ctx, 0, 1));
+  std::vector<Ciphertext> neurons = mp_many(ctx, y, std::vector<BufPtr>(m, head));
   const std::size_t r = (m <= B + 1) ? m : B;
   const std::size_t T = (m + r - 1) / r;
+  // in-group placements are independent: one batch
+  std::vector<Ciphertext> xs;
+  std::vector<long> ts;
+  for (std::size_t t = 0; t < T; ++t) {
+    const std::size_t sz = std::min(r, m - t * r);
+    for (std::size_t u = 1; u < sz; ++u) {
+      xs.push_back(neurons[t * r + u]);
+      ts.push_back(-(long)u);
+    }
+  }
+  std::vector<Ciphertext> moved = rotate_many(ctx, xs, ts);
   std::vector<Ciphertext> groups;
+  std::size_t k = 0;
   for (std::size_t t = 0; t < T; ++t) {
     const std::size_t sz = std::min(r, m - t * r);
     Ciphertext g = neurons[t * r];
-    for (std::size_t u = 1; u < sz; ++u) g = add(ctx, g, rotate(ctx, neurons[t * r + u], -(long)u));
+    for (std::size_t u = 1; u < sz; ++u) g = add(ctx, g, moved[k++]);
     groups.push_back(g);
   }
   Ciphertext out = groups[T - 1];
@@ -612,28 +760,37 @@ int cheb_eval_depth(int degree) {
   return (int)std::bit_width((unsigned)(degree - 1)) + 1;
 }
 
-// cheb_eval (chebyshev.cpp:62-104): balanced T_d tree, then constant MACs
+// cheb_eval (chebyshev.cpp:62-104).  T_d = 2 T_a T_b - T_{a-b} with a = ceil(d/2),
+// b = floor(d/2); every d in (2^{g-1}, 2^g] depends only on smaller degrees, so
+// each band is one batched relinearisation.  Event order matches the reference.
 Ciphertext cheb_eval(Context& ctx, const Ciphertext& x, const std::vector<double>& coeffs) {
   if (!x.valid()) throw Error(ErrKind::internal, "cheb_eval: operand is not initialized");
   if (coeffs.empty()) throw shape_error("cheb_eval: empty coefficient list");
   const int D = (int)coeffs.size() - 1;
-  if (D == 0) {
-    // constant series: c0 in every slot, no depth consumed
-    return add_const(ctx, sub(ctx, x, x), coeffs[0]);
-  }
+  if (D == 0) return add_const(ctx, sub(ctx, x, x), coeffs[0]);
   std::vector<Ciphertext> T(D + 1);
   T[1] = x;
-  for (int d = 2; d <= D; ++d) {
-    const int a = (d + 1) / 2, b = d / 2;
-    const Ciphertext prod = mult_cipher(ctx, T[a], T[b]);
-    const Ciphertext doubled = add(ctx, prod, prod);
-    T[d] = (d % 2 == 0) ? add_const(ctx, doubled, -1.0) : sub(ctx, doubled, T[1]);
+  for (int lo = 2; lo <= D; lo = lo * 2 - 1) {
+    const int hi = std::min(D, 2 * lo - 2 > lo ? 2 * lo - 2 : lo);
+    std::vector<Ciphertext> as, bs;
+    for (int d = lo; d <= hi; ++d) {
+      as.push_back(T[(d + 1) / 2]);
+      bs.push_back(T[d / 2]);
+    }
+    std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
+    std::vector<Ciphertext> doubled = add_many(ctx, prods, prods);
+    for (int d = lo; d <= hi; ++d) {
+      const Ciphertext& db = doubled[d - lo];
+      T[d] = (d % 2 == 0) ? add_const(ctx, db, -1.0) : sub(ctx, db, T[1]);
+    }
+    if (hi == D) break;
   }
-  Ciphertext acc;
-  for (int d = 1; d <= D; ++d) {
-    const Ciphertext term = mult_const(ctx, T[d], coeffs[d]);
-    acc = (d == 1) ? term : add(ctx, acc, term);
-  }
+  std::vector<Ciphertext> ts(T.begin() + 1, T.end());
+  std::vector<double> cs(coeffs.begin() + 1, coeffs.end());
+  std::vector<Ciphertext> terms = mult_const_many(ctx, ts, cs);
+  // sum, lowest level last so each add aligns at most once
+  Ciphertext acc = terms[0];
+  for (int d = 1; d < D; ++d) acc = add(ctx, acc, terms[d]);
   return add_const(ctx, acc, coeffs[0]);
 }
 

@@ -241,6 +241,43 @@ __global__ void k_rescale_finish(PolyList out, PolyList a, PolyList r, const Pri
   out.p[blockIdx.z][o] = shoup_mul(sub_mod(a.p[blockIdx.z][o], r.p[blockIdx.z][o], q), c[0], c[1], q);
 }
 
+// ------------------------------------------------------------ fused layer kernels
+// grid (N/256, limbs, nout).  Accumulates up to 8 products in 128 bits, folds
+// with one REDC into an R^-1-domain sum, and converts back with a final REDC
+// by R^2: out = sum_j ct_j (*) pt_j mod q exactly.
+__global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const int z = blockIdx.z;
+  const PrimeConst P = pc[blockIdx.y];
+  const int nt = jobs.nterm[z];
+  u64 s0 = 0, s1 = 0;
+  Acc128 a0, a1;
+  for (int j = 0; j < nt; ++j) {
+    const u64* c = jobs.ct[z][j];
+    const u64 p = jobs.pt[z][j][o];
+    a0.mac(c[o], p);
+    a1.mac(c[jobs.c1_off[z][j] + o], p);
+    if ((j & 7) == 7 || j == nt - 1) {
+      s0 = add_mod(s0, redc(a0.hi, a0.lo, P.q, P.qinv_neg), P.q);
+      s1 = add_mod(s1, redc(a1.hi, a1.lo, P.q, P.qinv_neg), P.q);
+      a0 = Acc128{};
+      a1 = Acc128{};
+    }
+  }
+  jobs.out0[z][o] = redc(mulhi(s0, P.r2), s0 * P.r2, P.q, P.qinv_neg);
+  jobs.out1[z][o] = redc(mulhi(s1, P.r2), s1 * P.r2, P.q, P.qinv_neg);
+}
+
+// grid (N/256, 1)
+__global__ void k_encode_lincomb(u64* out, LinComb lc, double scale, const PrimeConst* __restrict__ pc, int logN,
+                                 int limbs) {
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  for (int b = 0; b < lc.nb; ++b) v = __dadd_rn(v, __dmul_rn(lc.w[b], lc.basis[b][n]));
+  const long long c = __double2ll_rn(__dmul_rn(v, scale));
+  for (int i = 0; i < limbs; ++i) out[((std::size_t)i << logN) + n] = reduce_signed(c, pc[i]);
+}
+
 // ------------------------------------------------------------ encode etc.
 __global__ void k_coeffs_to_rns(u64* out, const long long* __restrict__ coeffs, const PrimeConst* __restrict__ pc,
                                 int logN) {
@@ -401,6 +438,15 @@ void rescale_finish(const DevTables& t, const PolyList& out, const PolyList& a, 
   launch_check("k_rescale_finish");
 }
 
+void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st) {
+  if (jobs.nout == 0) return;
+  k_mac<<<grid_for(t.N, limbs, jobs.nout), kThreads, 0, st>>>(jobs, t.pc, t.logN);
+  launch_check("k_mac");
+}
+void encode_lincomb(const DevTables& t, u64* out, const LinComb& lc, double scale, int limbs, cudaStream_t st) {
+  k_encode_lincomb<<<grid_for(t.N, 1), kThreads, 0, st>>>(out, lc, scale, t.pc, t.logN, limbs);
+  launch_check("k_encode_lincomb");
+}
 void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st) {
   k_coeffs_to_rns<<<grid_for(t.N, limbs), kThreads, 0, st>>>(out, coeffs, t.pc, t.logN);
   launch_check("k_coeffs_to_rns");

@@ -44,7 +44,10 @@ def check(out_ct, ev, r, tag):
     err = np.abs(got - r.slots).max()
     assert err < TOL, f"{tag}: max abs error {err}"
     assert out_ct.level() == r.level, f"{tag}: level {out_ct.level()} vs reference {r.level}"
-    assert ev == r.events, f"{tag}: trace differs"
+    # identical event multiset (rotation indices with counts, mult level_after);
+    # batched execution may reorder independent ops (keyplan/ledger use multisets)
+    assert sorted(ev) == sorted(r.events), f"{tag}: trace differs"
+    assert len(ev) == len(r.events)
     return err
 
 
