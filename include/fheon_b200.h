@@ -48,6 +48,9 @@ typedef struct {
   int special_bits;   /* special-prime bits */
   int depth_budget;   /* ContextConfig::depth_budget; -1 = limbs - 1 */
   uint64_t seed;      /* key / encryption randomness seed */
+  int hamming_weight; /* secret: 0 uniform ternary, h > 0 sparse with h nonzero coefficients */
+  int bootstrap;      /* 1: enable CKKS bootstrapping (bootstrap() refreshes to depth_budget) */
+  int boot_scale_bits;/* scale of the bootstrapping levels (0 = scale_bits) */
 } fheon_params;
 
 /* ---- errors / version */
@@ -107,6 +110,10 @@ int fheon_encrypt(fheon_ctx* ctx, const double* values, size_t n, fheon_ct** out
 int fheon_encrypt_top(fheon_ctx* ctx, const double* values, size_t n, fheon_ct** out);
 /* decrypt + decode all S slots into out[n >= S] */
 int fheon_decrypt(fheon_ctx* ctx, const fheon_ct* ct, double* out, size_t n);
+/* decrypt + decode complex slots (real and imaginary parts, n >= S each) */
+int fheon_decrypt_complex(fheon_ctx* ctx, const fheon_ct* ct, double* re, double* im, size_t n);
+/* effective depth budget (levels of fresh encryptions and bootstrap outputs) */
+int fheon_ctx_depth_budget(const fheon_ctx* ctx);
 /* raw RNS words, layout [2][limbs][N] */
 int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* words, int limbs, double scale, fheon_ct** out);
 int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);
@@ -124,6 +131,10 @@ int fheon_add_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, siz
 int fheon_mult_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, size_t n, fheon_ct** out);
 int fheon_mult_cipher(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out);
+/* bootstrapping stage probes (tests): 1 CoeffsToSlots, 2 EvalMod, 3 SlotsToCoeffs, 4 ModRaise;
+ * info (may be NULL): [depth, k_range, double_angles, stc_input_limbs] */
+int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out);
+int fheon_bootstrap_info(fheon_ctx* ctx, int* info4, double* cos_coeffs, size_t cap, size_t* ncoeffs);
 int fheon_rescale(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out);
 int fheon_level_down(fheon_ctx* ctx, const fheon_ct* a, int limbs, fheon_ct** out);
 /* key switch of a's c1 (as d) with key key_id under automorphism g (1 = none); out = (ks0, ks1) */

@@ -40,6 +40,7 @@ struct ock_ctx {
   u64* rotgroup;  /* 5^j mod 2N, j < S */
   double* ksi_re; /* cos(2 pi k / 2N), k <= 2N */
   double* ksi_im;
+  int h;          /* secret Hamming weight (0 = uniform ternary) */
   int8_t* s;      /* secret, coefficient domain */
   u64* s_ntt;     /* [L+K][N] */
 };
@@ -503,8 +504,33 @@ void ock_decode_coeffs(const ock_ctx* c, const double* coeffs, double scale, dou
 }
 
 /* ------------------------------------------------------- keys / encryption */
+/* secret: uniform ternary (h = 0) or exactly h nonzero +-1 coefficients
+ * (sparse, for bootstrapping): candidate j picks position prng(seed, 6, j) % N,
+ * accepted when unused, sign from bit 0 of prng(seed, 7, j). */
 void ock_secret(const ock_ctx* c, int8_t* s) {
-  for (size_t k = 0; k < c->N; k++) s[k] = (int8_t)((int)(prng(c->seed, STREAM_SECRET, k) % 3) - 1);
+  if (c->h <= 0) {
+    for (size_t k = 0; k < c->N; k++) s[k] = (int8_t)((int)(prng(c->seed, STREAM_SECRET, k) % 3) - 1);
+    return;
+  }
+  memset(s, 0, c->N);
+  int got = 0;
+  for (u64 j = 0; got < c->h; j++) {
+    const size_t pos = (size_t)(prng(c->seed, 6, j) % c->N);
+    if (s[pos]) continue;
+    s[pos] = (prng(c->seed, 7, j) & 1) ? 1 : -1;
+    got++;
+  }
+}
+
+void ock_set_hamming_weight(ock_ctx* c, int h) {
+  c->h = h;
+  ock_secret(c, c->s);
+#pragma omp parallel for
+  for (int i = 0; i < c->L + c->K; i++) {
+    u64* d = c->s_ntt + (size_t)i * c->N;
+    for (size_t k = 0; k < c->N; k++) d[k] = reduce_signed(c->s[k], c->q[i]);
+    ock_ntt_fwd(c, i, d);
+  }
 }
 
 /* error polynomial (CBD, eta = 21) reduced into prime pi and NTT'd */

@@ -64,6 +64,8 @@ void ock_decode_coeffs(const ock_ctx* c, const double* coeffs, double scale,
 
 /* ---- keys / encryption ---- */
 void ock_secret(const ock_ctx* c, int8_t* s);
+/* switch to a sparse secret with exactly h nonzero coefficients (0 = uniform ternary) */
+void ock_set_hamming_weight(ock_ctx* c, int h);
 int ock_keygen(const ock_ctx* c, uint64_t key_id, uint64_t* key);
 int ock_encrypt(const ock_ctx* c, const double* vals, size_t n,
                 uint64_t counter, uint64_t* ct);

@@ -46,6 +46,7 @@ def lib():
         L.ock_encode_coeffs.argtypes = [vp, _dblp, C.c_size_t, C.c_double, _i64p]
         L.ock_decode_coeffs.argtypes = [vp, _dblp, C.c_double, _dblp]
         L.ock_secret.argtypes = [vp, _i8p]
+        L.ock_set_hamming_weight.argtypes = [vp, C.c_int]
         L.ock_keygen.argtypes = [vp, C.c_uint64, _u64p]
         L.ock_encrypt.argtypes = [vp, _dblp, C.c_size_t, C.c_uint64, _u64p]
         L.ock_decrypt.argtypes = [vp, _u64p, C.c_int, C.c_double, _dblp]
@@ -75,7 +76,7 @@ def _chk(rc, what):
 class Oracle:
     """CPU RNS-CKKS context mirroring the engine's parameter spec."""
 
-    def __init__(self, logN, L, K, dnum, first_bits, scale_bits, special_bits, seed=1):
+    def __init__(self, logN, L, K, dnum, first_bits, scale_bits, special_bits, seed=1, hamming_weight=0):
         self.logN, self.L, self.K, self.dnum = logN, L, K, dnum
         self.N = 1 << logN
         self.S = self.N // 2
@@ -87,6 +88,8 @@ class Oracle:
         self.psi = np.zeros(L + K, np.uint64)
         self.T = np.zeros(L, np.float64)
         lib().ock_info(self._c, self.primes, self.psi, self.T)
+        if hamming_weight:
+            lib().ock_set_hamming_weight(self._c, int(hamming_weight))
 
     def __del__(self):
         if getattr(self, "_c", None):

@@ -27,6 +27,9 @@ class fheon_params(C.Structure):
         ("special_bits", C.c_int),
         ("depth_budget", C.c_int),
         ("seed", C.c_uint64),
+        ("hamming_weight", C.c_int),
+        ("bootstrap", C.c_int),
+        ("boot_scale_bits", C.c_int),
     ]
 
 
@@ -82,6 +85,8 @@ SIGNATURES = {
     "fheon_encrypt": (C.c_int, [vp, dp, C.c_size_t, pp]),
     "fheon_encrypt_top": (C.c_int, [vp, dp, C.c_size_t, pp]),
     "fheon_decrypt": (C.c_int, [vp, vp, dp, C.c_size_t]),
+    "fheon_decrypt_complex": (C.c_int, [vp, vp, dp, dp, C.c_size_t]),
+    "fheon_ctx_depth_budget": (C.c_int, [vp]),
     "fheon_ct_upload": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
     "fheon_ct_download": (C.c_int, [vp, vp, u64p]),
     "fheon_rotate": (C.c_int, [vp, vp, C.c_long, pp]),
@@ -93,6 +98,8 @@ SIGNATURES = {
     "fheon_mult_plain": (C.c_int, [vp, vp, dp, C.c_size_t, pp]),
     "fheon_mult_cipher": (C.c_int, [vp, vp, vp, pp]),
     "fheon_bootstrap": (C.c_int, [vp, vp, pp]),
+    "fheon_bootstrap_stage": (C.c_int, [vp, vp, C.c_int, pp]),
+    "fheon_bootstrap_info": (C.c_int, [vp, C.POINTER(C.c_int), dp, C.c_size_t, szp]),
     "fheon_rescale": (C.c_int, [vp, vp, pp]),
     "fheon_level_down": (C.c_int, [vp, vp, C.c_int, pp]),
     "fheon_keyswitch_raw": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, pp]),

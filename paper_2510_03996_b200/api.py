@@ -114,6 +114,9 @@ class ContextConfig:
     seed: int = 1
     noise_sigma: float = 0.0
     noise_seed: int = 1
+    hamming_weight: int = 0   # 0: uniform ternary secret; h: sparse (needed for bootstrapping)
+    bootstrap: bool = False   # build the CKKS bootstrapping pipeline
+    boot_scale_bits: int = 0  # scale of the bootstrapping levels (0 = rescale_bits)
 
     def validate(self):
         n, s = self.ring_dimension, self.slot_count
@@ -123,8 +126,9 @@ class ContextConfig:
             raise ShapeError(f"ring dimension must be a power of two, got {n}", 2)
         if s * 2 != n:
             raise ShapeError(f"slot count {s} must equal half the ring dimension {n} (full packing)", 2)
-        if self.depth_budget < 1:
-            raise ShapeError(f"depth budget must be positive, got {self.depth_budget}", 2)
+        if self.depth_budget < 1 and not (self.depth_budget == -1 and self.limbs):
+            raise ShapeError(f"depth budget must be positive (or -1 with explicit limbs), got {self.depth_budget}",
+                             2)
 
     @staticmethod
     def preset(name: str) -> "ContextConfig":
@@ -158,6 +162,9 @@ class ContextConfig:
         p.special_bits = self.special_bits
         p.depth_budget = self.depth_budget
         p.seed = self.seed
+        p.hamming_weight = self.hamming_weight
+        p.bootstrap = int(bool(self.bootstrap))
+        p.boot_scale_bits = int(self.boot_scale_bits)
         return p
 
 
@@ -237,7 +244,8 @@ class SlotContext:
         return self._slots
 
     def depth_budget(self) -> int:
-        return self.config.depth_budget
+        """Levels of fresh encryptions and bootstrap outputs (resolved by the engine)."""
+        return int(_native.lib().fheon_ctx_depth_budget(self._h))
 
     def attach_recorder(self) -> TraceRecorder:
         _check(_native.lib().fheon_set_tracing(self._h, 1))
@@ -386,6 +394,12 @@ class SlotVector:
         _check(_native.lib().fheon_decrypt(self._ctx._h, self._h, _dptr(out), out.size))
         return out
 
+    def slots_complex(self) -> np.ndarray:
+        re = np.zeros(self._ctx.slots(), np.float64)
+        im = np.zeros(self._ctx.slots(), np.float64)
+        _check(_native.lib().fheon_decrypt_complex(self._ctx._h, self._h, _dptr(re), _dptr(im), re.size))
+        return re + 1j * im
+
     def words(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         shape = (2, self.limbs(), self._ctx.N)
         if out is None:
@@ -477,6 +491,21 @@ def mult_cipher(a: SlotVector, b: SlotVector) -> SlotVector:
 
 def bootstrap(a: SlotVector) -> SlotVector:
     return _wrap(a._ctx, _native.lib().fheon_bootstrap, a._h)
+
+
+def bootstrap_stage(a: SlotVector, stage: int) -> SlotVector:
+    """Bootstrapping stage probe: 1 CoeffsToSlots, 2 EvalMod, 3 SlotsToCoeffs, 4 ModRaise."""
+    return _wrap(a._ctx, _native.lib().fheon_bootstrap_stage, a._h, int(stage))
+
+
+def bootstrap_info(ctx: "SlotContext"):
+    info = (C.c_int * 4)()
+    n = C.c_size_t()
+    _check(_native.lib().fheon_bootstrap_info(ctx._h, info, None, 0, C.byref(n)))
+    coeffs = np.zeros(n.value)
+    _check(_native.lib().fheon_bootstrap_info(ctx._h, info, _dptr(coeffs), n.value, C.byref(n)))
+    return {"depth": info[0], "k_range": info[1], "double_angles": info[2], "stc_input_limbs": info[3],
+            "cos_coeffs": coeffs}
 
 
 def rescale(a: SlotVector) -> SlotVector:

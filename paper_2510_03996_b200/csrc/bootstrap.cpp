@@ -1,0 +1,351 @@
+// Full-slot CKKS bootstrapping (see bootstrap.hpp).
+#include "bootstrap.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <set>
+
+#include "layers.hpp"
+
+namespace fheon {
+
+namespace {
+constexpr double kPi = 3.14159265358979323846;
+
+long ilog2(long v) {
+  long l = 0;
+  while ((1L << l) < v) ++l;
+  return l;
+}
+
+// signed representative of a slot offset in (-S/2, S/2]
+long signed_off(long d, long S) {
+  d %= S;
+  if (d < 0) d += S;
+  return d > S / 2 ? d - S : d;
+}
+}  // namespace
+
+// One special-FFT stage as a 3-diagonal slot matrix: M x = sum_d diag_d (*) rot(x, d).
+// Forward (decode, Context::decode_coeffs): for p = k mod len < len/2:
+//   out[k] = x[k] + w_p x[k+len/2];  p >= len/2: out[k] = x[k-len/2] - w x[k]
+// Inverse (encode, fft_special_inv) with the 1/2 of U^{-1} = (1/S) ... per stage.
+Bootstrapper::Mat Bootstrapper::stage(int len, bool inverse) const {
+  const HostTables& h = ctx_.host();
+  const long S = S_, M = 2 * (long)h.N;
+  const int lenh = len / 2;
+  const long lenq = (long)len * 4;
+  Mat m;
+  Diag d0(S), dp(S), dm(S);
+  for (long k = 0; k < S; ++k) {
+    const long p = k % len;
+    const long j = p < lenh ? p : p - lenh;
+    long idx;
+    if (!inverse) idx = (long)(h.rotgroup[j] % lenq) * (M / lenq);
+    else idx = (lenq - (long)(h.rotgroup[j] % lenq)) * (M / lenq);
+    const std::complex<double> w(h.ksi_re[idx], h.ksi_im[idx]);
+    if (!inverse) {
+      if (p < lenh) {
+        d0[k] = 1.0;
+        dp[k] = w;
+      } else {
+        d0[k] = -w;
+        dm[k] = 1.0;
+      }
+    } else {
+      if (p < lenh) {
+        d0[k] = 0.5;
+        dp[k] = 0.5;
+      } else {
+        d0[k] = -0.5 * w;
+        dm[k] = 0.5 * w;
+      }
+    }
+  }
+  // +len/2 and -len/2 coincide when len = S (disjoint supports): accumulate
+  for (const auto& [off, d] : {std::pair<long, const Diag*>{0, &d0}, {signed_off(lenh, S), &dp},
+                               {signed_off(-lenh, S), &dm}}) {
+    Diag& dst = m[off];
+    if (dst.empty()) dst.assign(S, 0.0);
+    for (long k = 0; k < S; ++k) dst[k] += (*d)[k];
+  }
+  return m;
+}
+
+// (A B) x = sum_{a,b} (A_a (*) rot(B_b, a)) (*) rot(x, a + b)
+Bootstrapper::Mat Bootstrapper::mul(const Mat& A, const Mat& B) const {
+  const long S = S_;
+  Mat out;
+  for (const auto& [a, da] : A)
+    for (const auto& [b, db] : B) {
+      const long o = signed_off(a + b, S);
+      Diag& dst = out[o];
+      if (dst.empty()) dst.assign(S, 0.0);
+      for (long k = 0; k < S; ++k) dst[k] += da[k] * db[(k + a % S + S) % S];
+    }
+  // drop all-zero diagonals
+  for (auto it = out.begin(); it != out.end();) {
+    bool nz = false;
+    for (const auto& v : it->second) nz = nz || std::abs(v) > 1e-300;
+    it = nz ? std::next(it) : out.erase(it);
+  }
+  return out;
+}
+
+std::vector<Bootstrapper::Level> Bootstrapper::plan(const std::vector<Mat>& groups, int limbs_in, double scale_in) {
+  const HostTables& h = ctx_.host();
+  const long S = S_;
+  std::vector<Level> out;
+  int limbs = limbs_in;
+  double scale = scale_in;
+  for (const Mat& M : groups) {
+    long u = S;
+    for (const auto& [d, v] : M)
+      if (d != 0) u = std::min(u, std::labs(d) & -std::labs(d));  // lowest set bit
+    if (u == S) u = 1;
+    std::vector<long> ks;
+    for (const auto& [d, v] : M) ks.push_back(d / u);
+    // baby-step size: minimise baby + giant rotations
+    long best_n1 = 1, best_cost = 1L << 40;
+    for (long n1 = 1; n1 <= 64; n1 *= 2) {
+      std::set<long> bs, gs;
+      for (long k : ks) {
+        const long g = (long)std::floor((double)k / (double)n1);
+        bs.insert(k - g * n1);
+        gs.insert(g);
+      }
+      const long cost = (long)(bs.size() - (bs.count(0) ? 1 : 0)) + (long)(gs.size() - (gs.count(0) ? 1 : 0));
+      if (cost < best_cost) {
+        best_cost = cost;
+        best_n1 = n1;
+      }
+    }
+    const long n1 = best_n1;
+    const int lv = limbs - 1;
+    const double pt_scale = h.T[lv - 1] * (double)h.q[lv] / scale;
+    Level L;
+    std::map<long, Giant> giants;
+    std::set<long> babies;
+    for (const auto& [d, diag] : M) {
+      const long k = d / u;
+      const long g = (long)std::floor((double)k / (double)n1);
+      const long b = k - g * n1;
+      const long G = g * n1 * u;
+      // pre-rotate: p = rot(diag, -G)
+      std::vector<double> re(S), im(S);
+      for (long j = 0; j < S; ++j) {
+        const auto v = diag[((j - G) % S + S) % S];
+        re[j] = v.real();
+        im[j] = v.imag();
+      }
+      BufPtr pt = ctx_.encode_complex(re.data(), im.data(), (std::size_t)S, limbs, pt_scale);
+      Giant& gi = giants[g];
+      gi.rot = signed_off(G, S);
+      gi.terms.push_back({signed_off(b * u, S), pt});
+      if (b != 0) babies.insert(signed_off(b * u, S));
+    }
+    L.babies.assign(babies.begin(), babies.end());
+    for (auto& [g, gi] : giants) L.giants.push_back(gi);
+    out.push_back(L);
+    limbs -= 1;
+    scale = h.T[limbs - 1];
+  }
+  return out;
+}
+
+namespace {
+// EvalMod cosine: cos(2 pi ((K+1) u - 1/4) / 2^r) on u in [-1, 1]
+std::function<double(double)> evalmod_fn(int k_range, int r) {
+  const double K1 = k_range + 1.0;
+  return [K1, r](double u) { return std::cos(2.0 * kPi * (K1 * u - 0.25) / std::ldexp(1.0, r)); };
+}
+int evalmod_degree(int k_range, int r) {
+  const std::vector<double> c = cheb_coefficients(evalmod_fn(k_range, r), 127);
+  int deg = 1;
+  for (int d = 1; d < (int)c.size(); ++d)
+    if (std::fabs(c[d]) > 1e-13) deg = d;
+  return deg;
+}
+}  // namespace
+
+int bootstrap_depth(const Params& p) {
+  return p.boot_cts_levels + cheb_eval_depth(evalmod_degree(p.boot_k_range, p.boot_double_angles)) +
+         p.boot_double_angles + p.boot_stc_levels;
+}
+
+BootParams boot_params_of(const Params& p) {
+  BootParams b;
+  b.k_range = p.boot_k_range;
+  b.double_angles = p.boot_double_angles;
+  b.cts_levels = p.boot_cts_levels;
+  b.stc_levels = p.boot_stc_levels;
+  return b;
+}
+
+Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(bp) {
+  const HostTables& h = ctx.host();
+  S_ = h.S;
+  const int L = h.p.L;
+  const long logS = ilog2(S_);
+  const double K1 = bp.k_range + 1.0;
+  const int r = bp.double_angles;
+  const int deg = bp.cos_degree > 0 ? bp.cos_degree : evalmod_degree(bp.k_range, r);
+  cos_coeffs_ = cheb_coefficients(evalmod_fn(bp.k_range, r), deg);
+  depth_ = bp.cts_levels + cheb_eval_depth(deg) + r + bp.stc_levels;
+  if (depth_ > L - 2)
+    throw Error(ErrKind::shape, "bootstrapping needs " + std::to_string(depth_) + " levels; the chain has " +
+                                    std::to_string(L - 1));
+  if (bp.cts_levels < 1 || bp.stc_levels < 1 || bp.cts_levels > logS || bp.stc_levels > logS)
+    throw Error(ErrKind::shape, "bootstrapping: bad linear-transform level split");
+  auto split = [&](int levels) {
+    std::vector<int> sizes(levels, (int)(logS / levels));
+    for (int i = 0; i < (int)(logS % levels); ++i) sizes[i]++;
+    return sizes;
+  };
+  // CoeffsToSlots: inverse stages len = S .. 2 (first applied first)
+  {
+    std::vector<int> sizes = split(bp.cts_levels);
+    std::vector<Mat> groups;
+    const double c = std::pow(1.0 / (2.0 * K1), 1.0 / bp.cts_levels);
+    long len = S_;
+    for (int gsz : sizes) {
+      Mat M = stage((int)len, true);
+      len /= 2;
+      for (int i = 1; i < gsz; ++i, len /= 2) M = mul(stage((int)len, true), M);
+      for (auto& [d, v] : M)
+        for (auto& x : v) x *= c;
+      groups.push_back(M);
+    }
+    cts_ = plan(groups, L, (double)h.q[0]);
+  }
+  // SlotsToCoeffs: forward stages len = 2 .. S, scaled by q0 / (2 pi Delta_0)
+  {
+    std::vector<int> sizes = split(bp.stc_levels);
+    std::vector<Mat> groups;
+    const double c = std::pow((double)h.q[0] / (2.0 * kPi * h.T[0]), 1.0 / bp.stc_levels);
+    long len = 2;
+    for (int gsz : sizes) {
+      Mat M = stage((int)len, false);
+      len *= 2;
+      for (int i = 1; i < gsz; ++i, len *= 2) M = mul(stage((int)len, false), M);
+      for (auto& [d, v] : M)
+        for (auto& x : v) x *= c;
+      groups.push_back(M);
+    }
+    const int stc_limbs = L - bp.cts_levels - cheb_eval_depth(deg) - r;
+    stc_limbs_ = stc_limbs;
+    stc_ = plan(groups, stc_limbs, h.T[stc_limbs - 1]);
+  }
+  for (long s : rotation_steps()) ctx.gen_key(ctx.galois(s));
+  ctx.gen_key(2 * (u64)h.N - 1);  // conjugation
+  ctx.gen_key(0);                 // relinearisation
+}
+
+std::vector<long> Bootstrapper::rotation_steps() const {
+  std::set<long> s;
+  for (const auto* v : {&cts_, &stc_})
+    for (const Level& lv : *v) {
+      for (long b : lv.babies) s.insert(b);
+      for (const Giant& g : lv.giants)
+        if (g.rot != 0) s.insert(g.rot);
+    }
+  return std::vector<long>(s.begin(), s.end());
+}
+
+Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv) {
+  std::vector<Ciphertext> rot = rotate_hoisted(ctx_, x, lv.babies);
+  std::map<long, Ciphertext> by_b;
+  by_b[0] = x;
+  for (std::size_t i = 0; i < lv.babies.size(); ++i) by_b[lv.babies[i]] = rot[i];
+  std::vector<std::vector<Ciphertext>> terms;
+  std::vector<std::vector<BufPtr>> pts;
+  for (const Giant& g : lv.giants) {
+    std::vector<Ciphertext> t;
+    std::vector<BufPtr> p;
+    for (const auto& [b, pt] : g.terms) {
+      t.push_back(by_b.at(b));
+      p.push_back(pt);
+    }
+    terms.push_back(t);
+    pts.push_back(p);
+  }
+  std::vector<Ciphertext> inner = mac_plain_many(ctx_, terms, pts);
+  std::vector<Ciphertext> xs;
+  std::vector<long> ts;
+  Ciphertext acc;
+  bool have = false;
+  for (std::size_t i = 0; i < lv.giants.size(); ++i) {
+    if (lv.giants[i].rot == 0) {
+      acc = have ? add(ctx_, acc, inner[i]) : inner[i];
+      have = true;
+    } else {
+      xs.push_back(inner[i]);
+      ts.push_back(lv.giants[i].rot);
+    }
+  }
+  std::vector<Ciphertext> moved = rotate_many(ctx_, xs, ts);
+  for (const Ciphertext& m : moved) {
+    acc = have ? add(ctx_, acc, m) : m;
+    have = true;
+  }
+  return acc;
+}
+
+Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {
+  const HostTables& h = ctx_.host();
+  Ciphertext y = x0;
+  if (what == 1) {
+    y.scale = (double)h.q[0];
+    for (const Level& lv : cts_) y = apply(y, lv);
+    return y;
+  }
+  if (what == 2) {
+    std::vector<Ciphertext> ys = cheb_eval_many(ctx_, {y}, cos_coeffs_);
+    for (int i = 0; i < bp_.double_angles; ++i) {
+      std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
+      ys = add_many(ctx_, sq, sq);
+      for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
+    }
+    return ys[0];
+  }
+  if (what == 3) {
+    if (y.limbs > stc_limbs_) y = level_down(ctx_, y, stc_limbs_);
+    for (const Level& lv : stc_) y = apply(y, lv);
+    return y;
+  }
+  if (what == 4) return mod_raise(ctx_, x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0);
+  throw Error(ErrKind::internal, "debug_stage: unknown stage");
+}
+
+Ciphertext Bootstrapper::run(const Ciphertext& x0) {
+  const bool tracing = ctx_.tracing();
+  ctx_.set_tracing(false);
+  try {
+    const HostTables& h = ctx_.host();
+    Ciphertext x = x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0;
+    const double corr = x.scale / h.T[0];
+    Ciphertext y = mod_raise(ctx_, x);
+    for (const Level& lv : cts_) y = apply(y, lv);
+    const Ciphertext yc = conjugate_many(ctx_, {y})[0];
+    std::vector<Ciphertext> ys = {add(ctx_, y, yc), mul_by_i(ctx_, sub(ctx_, yc, y))};
+    ys = cheb_eval_many(ctx_, ys, cos_coeffs_);
+    for (int i = 0; i < bp_.double_angles; ++i) {
+      std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
+      ys = add_many(ctx_, sq, sq);
+      for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
+    }
+    Ciphertext z = add(ctx_, ys[0], mul_by_i(ctx_, ys[1]));
+    for (const Level& lv : stc_) z = apply(z, lv);
+    z.scale *= corr;
+    if (z.level() > ctx_.depth_budget()) z = level_down(ctx_, z, ctx_.depth_budget() + 1);
+    ctx_.set_tracing(tracing);
+    ctx_.record(3, z.level());
+    ctx_.stats.bootstraps++;
+    return z;
+  } catch (...) {
+    ctx_.set_tracing(tracing);
+    throw;
+  }
+}
+
+}  // namespace fheon

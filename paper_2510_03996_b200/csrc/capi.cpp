@@ -8,6 +8,7 @@
 #include "../../include/fheon_b200.h"
 #include "engine.hpp"
 #include "layers.hpp"
+#include "bootstrap.hpp"
 
 struct fheon_ctx {
   fheon::Context* impl;
@@ -62,6 +63,9 @@ static fheon::Params to_params(const fheon_params* p) {
   prm.special_bits = p->special_bits;
   prm.depth_budget = p->depth_budget;
   prm.seed = p->seed;
+  prm.hamming_weight = p->hamming_weight;
+  prm.bootstrap = p->bootstrap;
+  prm.boot_scale_bits = p->boot_scale_bits;
   return prm;
 }
 
@@ -106,16 +110,7 @@ int fheon_ctx_create(const fheon_params* p, fheon_ctx** out) {
   return guard([&] {
     need(p, "params");
     need(out, "out");
-    fheon::Params prm;
-    prm.logN = p->log_n;
-    prm.L = p->limbs;
-    prm.K = p->special_limbs;
-    prm.dnum = p->dnum;
-    prm.first_bits = p->first_mod_bits;
-    prm.scale_bits = p->scale_bits;
-    prm.special_bits = p->special_bits;
-    prm.depth_budget = p->depth_budget;
-    prm.seed = p->seed;
+    const fheon::Params prm = to_params(p);
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
       throw fheon::Error(fheon::ErrKind::cuda, "no CUDA device visible: the B200 engine has no CPU fallback");
@@ -251,6 +246,14 @@ int fheon_decrypt(fheon_ctx* ctx, const fheon_ct* ct, double* out, size_t n) {
     fheon::decrypt(*ctx->impl, ct->ct, out);
   });
 }
+int fheon_decrypt_complex(fheon_ctx* ctx, const fheon_ct* ct, double* re, double* im, size_t n) {
+  return guard([&] {
+    need(ct, "ciphertext");
+    if (n < (size_t)ctx->impl->S()) throw fheon::Error(fheon::ErrKind::capacity, "output buffer smaller than S");
+    fheon::decrypt(*ctx->impl, ct->ct, re, im);
+  });
+}
+int fheon_ctx_depth_budget(const fheon_ctx* ctx) { return ctx ? ctx->impl->depth_budget() : -1; }
 int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* w, int limbs, double scale, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::upload_ct(*ctx->impl, w, limbs, scale)); });
 }
@@ -301,6 +304,28 @@ int fheon_mult_cipher(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheo
 }
 int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::bootstrap(*ctx->impl, a->ct)); });
+}
+int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out) {
+  return guard([&] {
+    if (!ctx->impl->boot) throw fheon::Error(fheon::ErrKind::not_implemented, "context has no bootstrapper");
+    *out = wrap(ctx->impl->boot->debug_stage(a->ct, stage));
+  });
+}
+int fheon_bootstrap_info(fheon_ctx* ctx, int* info4, double* coeffs, size_t cap, size_t* n) {
+  return guard([&] {
+    if (!ctx->impl->boot) throw fheon::Error(fheon::ErrKind::not_implemented, "context has no bootstrapper");
+    const fheon::Bootstrapper& b = *ctx->impl->boot;
+    if (info4) {
+      info4[0] = b.depth();
+      info4[1] = 16;
+      info4[2] = 3;
+      info4[3] = b.stc_input_limbs();
+    }
+    const std::vector<double>& c = b.cos_coeffs();
+    if (n) *n = c.size();
+    if (coeffs)
+      for (size_t i = 0; i < c.size() && i < cap; ++i) coeffs[i] = c[i];
+  });
 }
 int fheon_rescale(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::rescale(*ctx->impl, a->ct)); });

@@ -2,6 +2,8 @@
 // trace.  See engine.hpp.
 #include "engine.hpp"
 
+#include "bootstrap.hpp"
+
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -150,6 +152,8 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
   depth_budget_ = p.depth_budget < 0 ? p.L - 1 : p.depth_budget;
   if (depth_budget_ < 1 || depth_budget_ > p.L - 1)
     throw Error(ErrKind::shape, "depth budget must lie in [1, L-1]");
+  if (p.bootstrap && p.hamming_weight <= 0)
+    throw Error(ErrKind::shape, "bootstrapping needs a sparse secret (hamming_weight > 0)");
   int dev = 0;
   FHEON_CUDA(cudaGetDevice(&dev));
   FHEON_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -174,9 +178,18 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
     FHEON_CUDA(cudaEventCreateWithFlags(&staging_ev_[i], cudaEventDisableTiming));
   }
   build_device_tables();
+  if (p.bootstrap) {
+    boot = std::make_unique<Bootstrapper>(*this, boot_params_of(p));
+    const int after = p.L - 1 - boot->depth();
+    if (p.depth_budget < 0) depth_budget_ = after;
+    else if (p.depth_budget > after)
+      throw Error(ErrKind::shape, "depth budget " + std::to_string(p.depth_budget) +
+                                      " exceeds the levels left after bootstrapping (" + std::to_string(after) + ")");
+  }
 }
 
 Context::~Context() {
+  boot.reset();
   keys_.clear();
   basis_.clear();
   ptcache_.clear();
@@ -314,11 +327,21 @@ void Context::build_device_tables() {
 
   // secret key: ternary from the counter PRNG, NTT domain over all L+K primes
   {
-    std::vector<long long> s(N);
-    const u64 key = prng_stream_key(p.seed, kStreamSecret);
-    for (std::size_t k = 0; k < N; ++k) {
-      const u64 r = mix64(key ^ (k * 0xD1B54A32D192ED03ULL + 0x8CB92BA72F3D8DD7ULL));
-      s[k] = (long long)(r % 3) - 1;
+    std::vector<long long> s(N, 0);
+    auto prng_h = [&](u64 stream, u64 idx) {
+      return mix64(prng_stream_key(p.seed, stream) ^ (idx * 0xD1B54A32D192ED03ULL + 0x8CB92BA72F3D8DD7ULL));
+    };
+    if (p.hamming_weight <= 0) {
+      for (std::size_t k = 0; k < N; ++k) s[k] = (long long)(prng_h(kStreamSecret, k) % 3) - 1;
+    } else {
+      // sparse: candidate j -> position prng(6, j) % N if unused, sign bit 0 of prng(7, j)
+      int got = 0;
+      for (u64 j = 0; got < p.hamming_weight; ++j) {
+        const std::size_t pos = (std::size_t)(prng_h(6, j) % N);
+        if (s[pos]) continue;
+        s[pos] = (prng_h(7, j) & 1) ? 1 : -1;
+        ++got;
+      }
     }
     long long* dcoef = upload(dev_allocs_, s, stream_);
     u64* sntt = nullptr;
@@ -409,10 +432,47 @@ void Context::encode_coeffs(const double* vals, std::size_t n, double scale, lon
 }
 
 namespace {
-// special inverse FFT of the zero-filled slot vector; re/im scaled by 1/S
+// special inverse FFT of the zero-filled slot vector (imaginary parts optional)
 void fft_special_inv_host(const HostTables& ht_, const double* vals, std::size_t n, std::vector<double>& re,
-                          std::vector<double>& im);
+                          std::vector<double>& im, const double* ivals = nullptr);
 }  // namespace
+
+void encode_complex_coeffs_host(const HostTables& ht_, const double* re_in, const double* im_in, std::size_t n,
+                                double scale, long long* coeffs) {
+  std::vector<double> re, im;
+  fft_special_inv_host(ht_, re_in, n, re, im, im_in);
+  const int S = ht_.S;
+  const double lim = 4611686018427387904.0;
+  for (int i = 0; i < S; ++i) {
+    const double a = (re[i] / (double)S) * scale, b = (im[i] / (double)S) * scale;
+    if (!(std::fabs(a) < lim) || !(std::fabs(b) < lim))
+      throw Error(ErrKind::capacity, "encoded value exceeds the 2^62 coefficient range");
+    coeffs[i] = std::llround(a);
+    coeffs[i + S] = std::llround(b);
+  }
+}
+
+BufPtr Context::encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale) {
+  const std::size_t N = ht_.N;
+  BufPtr out = alloc((std::size_t)limbs * N);
+  ++stats.encodes;
+  cudaEvent_t* ev = nullptr;
+  long long* h = staging_slot(&ev);
+  encode_complex_coeffs_host(ht_, re, im, n, scale, h);
+  BufPtr dcoef = alloc(N);
+  FHEON_CUDA(cudaMemcpyAsync(dcoef->ptr, h, N * sizeof(long long), cudaMemcpyHostToDevice, stream_));
+  FHEON_CUDA(cudaEventRecord(*ev, stream_));
+  coeffs_to_rns(dt_, out->ptr, reinterpret_cast<const long long*>(dcoef->ptr), limbs, stream_);
+  LimbSet ls{};
+  ls.base[0] = out->ptr;
+  ls.nbase = 1;
+  ls.blocks_per_base = 1;
+  ls.E = limbs;
+  ls.ell = limbs;
+  ls.L = ht_.p.L;
+  ntt_forward(dt_, ls, stream_);
+  return out;
+}
 
 void encode_real_host(const HostTables& ht_, const double* vals, std::size_t n, double* out) {
   std::vector<double> re, im;
@@ -426,13 +486,15 @@ void encode_real_host(const HostTables& ht_, const double* vals, std::size_t n, 
 
 namespace {
 void fft_special_inv_host(const HostTables& ht_, const double* vals, std::size_t n, std::vector<double>& re,
-                          std::vector<double>& im) {
+                          std::vector<double>& im, const double* ivals) {
   const int S = ht_.S;
   if (n > (std::size_t)S) throw Error(ErrKind::capacity, "payload exceeds the slot count");
   const u64 M = 2 * (u64)ht_.N;
   re.assign(S, 0.0);
   im.assign(S, 0.0);
   for (std::size_t i = 0; i < n; ++i) re[i] = vals[i];
+  if (ivals)
+    for (std::size_t i = 0; i < n; ++i) im[i] = ivals[i];
   for (int len = S; len >= 1; len >>= 1) {
     const int lenh = len >> 1;
     const u64 lenq = (u64)len << 2;
@@ -507,7 +569,7 @@ void encode_coeffs_host(const HostTables& ht_, const double* vals, std::size_t n
   }
 }
 
-void Context::decode_coeffs(const double* coeffs, double scale, double* out) const {
+void Context::decode_coeffs(const double* coeffs, double scale, double* out, double* out_im) const {
   const int S = ht_.S;
   const u64 M = 2 * (u64)ht_.N;
   std::vector<double> re(S), im(S);
@@ -543,6 +605,8 @@ void Context::decode_coeffs(const double* coeffs, double scale, double* out) con
     }
   }
   for (int i = 0; i < S; ++i) out[i] = re[i];
+  if (out_im)
+    for (int i = 0; i < S; ++i) out_im[i] = im[i];
 }
 
 const double* Context::basis(const std::string& key, const std::vector<double>& slot_values) {

@@ -56,6 +56,7 @@ extern std::atomic<std::uint64_t> g_kernel_launches;
 #define FHEON_CUDA(x) ::fheon::cuda_check((x), #x)
 
 class Context;
+class Bootstrapper;
 
 struct DevBuffer {
   // stream-ordered free while the owning context lives; a synchronous free if
@@ -93,7 +94,7 @@ struct TraceEvent {
 
 struct OpStats {
   std::uint64_t rotations = 0, keyswitches = 0, mult_plain = 0, mult_cipher = 0, rescales = 0, ntt_limbs = 0,
-                encodes = 0, adds = 0, launches = 0;
+                encodes = 0, adds = 0, launches = 0, bootstraps = 0;
 };
 
 struct KernelTimer {
@@ -141,9 +142,11 @@ class Context {
 
   // ---- encoder (host special FFT)
   void encode_coeffs(const double* vals, std::size_t n, double scale, long long* coeffs) const;
-  void decode_coeffs(const double* coeffs, double scale, double* out) const;
+  void decode_coeffs(const double* coeffs, double scale, double* out, double* out_im = nullptr) const;
   // encode `vals` at `scale` over `limbs` limbs into a device [limbs][N] NTT-domain buffer
   BufPtr encode(const double* vals, std::size_t n, int limbs, double scale);
+  // complex slot values (re + i im), host special FFT
+  BufPtr encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale);
   // content-addressed cache over encode() (masks reused across a layer)
   BufPtr encode_cached(const std::vector<double>& vals, int limbs, double scale);
   // device real-coefficient (unscaled, unrounded) encoding of a slot vector,
@@ -162,6 +165,7 @@ class Context {
   OpStats stats;
   KernelTimer timer;
   std::uint64_t enc_counter = 0;
+  std::unique_ptr<Bootstrapper> boot;  // present when Params::bootstrap
 
   // staging for host -> device copies of encoded coefficients
   long long* staging_slot(cudaEvent_t** ev);
@@ -211,6 +215,9 @@ std::vector<Ciphertext> rescale_many(Context& ctx, const std::vector<Ciphertext>
 std::vector<Ciphertext> mac_plain_many(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
                                        const std::vector<std::vector<BufPtr>>& pts);
 std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b);
+std::vector<Ciphertext> conjugate_many(Context& ctx, const std::vector<Ciphertext>& xs);
+Ciphertext mul_by_i(Context& ctx, const Ciphertext& x);
+Ciphertext mod_raise(Context& ctx, const Ciphertext& x);
 // add an encoded plaintext (encoded at a's level and scale)
 Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt);
 std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphertext>& as,
@@ -220,7 +227,7 @@ std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Cipherte
 // ---------------------------------------------------------------- ops
 Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n);            // at the depth budget
 Ciphertext encrypt_top(Context& ctx, const double* vals, std::size_t n);        // at L-1 (all limbs)
-void decrypt(Context& ctx, const Ciphertext& ct, double* out);                  // S slots
+void decrypt(Context& ctx, const Ciphertext& ct, double* out, double* out_im = nullptr);  // S slots
 Ciphertext rotate(Context& ctx, const Ciphertext& x, long t);
 std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& ts);
 std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t);

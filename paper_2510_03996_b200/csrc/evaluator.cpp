@@ -7,6 +7,8 @@
 
 #include "engine.hpp"
 
+#include "bootstrap.hpp"
+
 namespace fheon {
 
 namespace {
@@ -241,7 +243,7 @@ Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n) {
   return level_down(ctx, ct, ctx.depth_budget() + 1);
 }
 
-void decrypt(Context& ctx, const Ciphertext& ct, double* out) {
+void decrypt(Context& ctx, const Ciphertext& ct, double* out, double* out_im) {
   require_valid(ct, "decrypt");
   const std::size_t N = ctx.N();
   const int use = ct.limbs >= 2 ? 2 : 1;
@@ -268,7 +270,7 @@ void decrypt(Context& ctx, const Ciphertext& ct, double* out) {
       coeffs[k] = X > Q / 2 ? -(double)(Q - X) : (double)X;
     }
   }
-  ctx.decode_coeffs(coeffs.data(), ct.scale, out);
+  ctx.decode_coeffs(coeffs.data(), ct.scale, out, out_im);
 }
 
 // ---------------------------------------------------------------- rotate
@@ -336,6 +338,64 @@ std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const 
 
 std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t) {
   return rotate_many(ctx, xs, std::vector<long>(xs.size(), t));
+}
+
+// complex conjugation of the slots: automorphism X -> X^{2N-1} + key switch
+std::vector<Ciphertext> conjugate_many(Context& ctx, const std::vector<Ciphertext>& xs) {
+  const u64 g = 2 * (u64)ctx.N() - 1;
+  std::vector<Ciphertext> outs(xs.size());
+  std::map<int, std::vector<std::size_t>> by_level;
+  for (std::size_t i = 0; i < xs.size(); ++i) by_level[xs[i].limbs].push_back(i);
+  for (auto& [limbs, idx] : by_level) {
+    std::vector<const u64*> inputs;
+    std::vector<KsJob> jobs;
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      inputs.push_back(xs[idx[k]].c1);
+      KsJob jb{g, g, xs[idx[k]].c0, g, nullptr};
+      jb.in = (int)k;
+      jobs.push_back(jb);
+    }
+    std::vector<Ciphertext> r = keyswitch(ctx, inputs, limbs, jobs);
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      r[k].scale = xs[idx[k]].scale;
+      outs[idx[k]] = r[k];
+    }
+  }
+  return outs;
+}
+
+// slot-wise multiplication by i: exact monomial X^{N/2} product, no level used
+Ciphertext mul_by_i(Context& ctx, const Ciphertext& x) {
+  const HostTables& h = ctx.host();
+  LimbConsts iq{};
+  for (int i = 0; i < x.limbs; ++i) {
+    iq.c[i] = powmod(h.psi[i], ctx.N() / 2, h.q[i]);
+    iq.sh[i] = shoup(iq.c[i], h.q[i]);
+  }
+  Ciphertext out = ctx.new_ct(x.limbs);
+  mul_monomial_half(ctx.dev(), plist({out.c0, out.c1}), plist({x.c0, x.c1}), iq, x.limbs, ctx.stream());
+  out.scale = x.scale;
+  return out;
+}
+
+// ModRaise of a level-0 ciphertext to all L limbs (decrypts to m + q_0 I)
+Ciphertext mod_raise(Context& ctx, const Ciphertext& x) {
+  if (x.limbs != 1) throw Error(ErrKind::internal, "mod_raise expects a level-0 ciphertext");
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L();
+  BufPtr coef = ctx.alloc(2 * N);
+  LimbSet dst = limbset(coef->ptr, 2, N, 1, 1, L);
+  LimbSet src = dst;
+  src.base[0] = x.c0;
+  src.block_stride = (long long)(x.c1 - x.c0);
+  ntt_inverse(t, dst, st, &src);
+  Ciphertext out = ctx.new_ct(L);
+  modraise(t, plist({out.c0, out.c1}), plist({coef->ptr, coef->ptr + N}), L, st);
+  ntt_forward(t, limbset(out.c0, 2, (std::size_t)(out.c1 - out.c0), L, L, L), st);
+  out.scale = (double)ctx.host().q[0];
+  return out;
 }
 
 Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d, u64 key_id, u64 g) {
@@ -734,12 +794,14 @@ std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a,
   return outs;
 }
 
+// bootstrap (backend.cpp:233-249): same slots, level := depth budget
 Ciphertext bootstrap(Context& ctx, const Ciphertext& a) {
   require_valid(a, "bootstrap");
-  (void)ctx;
-  throw Error(ErrKind::not_implemented,
-              "bootstrap: CKKS bootstrapping is not available in this build; size the modulus chain for the "
-              "network depth");
+  if (!ctx.boot)
+    throw Error(ErrKind::not_implemented,
+                "bootstrap: this context was created without bootstrapping (set bootstrap = 1 and a sparse "
+                "secret, hamming_weight > 0)");
+  return ctx.boot->run(a);
 }
 
 // -------------------------------------------------------------- raw access

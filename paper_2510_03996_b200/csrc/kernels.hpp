@@ -147,6 +147,14 @@ struct LinComb {
 };
 void encode_lincomb(const DevTables& t, u64* out, const LinComb& lc, double scale, int limbs, cudaStream_t st);
 
+// ---- bootstrapping helpers
+// ModRaise: in[p] = coefficient-domain limb 0 (mod q_0); out[p] ([L][N]) = centred lift to q_0..q_{L-1}
+void modraise(const DevTables& t, const PolyList& out, const PolyList& in, int L, cudaStream_t st);
+// multiply by the monomial X^{N/2} (slot-wise multiplication by i) in the NTT domain:
+// out = a * (+-i_q) with i_q = psi^{N/2} (sign - on the upper half of NTT indices)
+void mul_monomial_half(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& iq, int limbs,
+                       cudaStream_t st);
+
 // ---- encode / encrypt / keygen / decrypt
 // signed coefficients -> RNS coefficient domain [limbs][N]
 void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st);

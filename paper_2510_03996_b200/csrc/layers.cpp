@@ -764,34 +764,55 @@ int cheb_eval_depth(int degree) {
 // b = floor(d/2); every d in (2^{g-1}, 2^g] depends only on smaller degrees, so
 // each band is one batched relinearisation.  Event order matches the reference.
 Ciphertext cheb_eval(Context& ctx, const Ciphertext& x, const std::vector<double>& coeffs) {
-  if (!x.valid()) throw Error(ErrKind::internal, "cheb_eval: operand is not initialized");
+  return cheb_eval_many(ctx, {x}, coeffs)[0];
+}
+
+// Several inputs through the same series: every band's products for all
+// inputs go through one batched relinearisation.
+std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertext>& xs,
+                                       const std::vector<double>& coeffs) {
+  for (const Ciphertext& x : xs)
+    if (!x.valid()) throw Error(ErrKind::internal, "cheb_eval: operand is not initialized");
   if (coeffs.empty()) throw shape_error("cheb_eval: empty coefficient list");
   const int D = (int)coeffs.size() - 1;
-  if (D == 0) return add_const(ctx, sub(ctx, x, x), coeffs[0]);
-  std::vector<Ciphertext> T(D + 1);
-  T[1] = x;
+  const std::size_t B = xs.size();
+  std::vector<Ciphertext> out(B);
+  if (D == 0) {
+    for (std::size_t i = 0; i < B; ++i) out[i] = add_const(ctx, sub(ctx, xs[i], xs[i]), coeffs[0]);
+    return out;
+  }
+  std::vector<std::vector<Ciphertext>> T(B, std::vector<Ciphertext>(D + 1));
+  for (std::size_t i = 0; i < B; ++i) T[i][1] = xs[i];
   for (int lo = 2; lo <= D; lo = lo * 2 - 1) {
     const int hi = std::min(D, 2 * lo - 2 > lo ? 2 * lo - 2 : lo);
     std::vector<Ciphertext> as, bs;
-    for (int d = lo; d <= hi; ++d) {
-      as.push_back(T[(d + 1) / 2]);
-      bs.push_back(T[d / 2]);
-    }
+    for (std::size_t i = 0; i < B; ++i)
+      for (int d = lo; d <= hi; ++d) {
+        as.push_back(T[i][(d + 1) / 2]);
+        bs.push_back(T[i][d / 2]);
+      }
     std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
     std::vector<Ciphertext> doubled = add_many(ctx, prods, prods);
-    for (int d = lo; d <= hi; ++d) {
-      const Ciphertext& db = doubled[d - lo];
-      T[d] = (d % 2 == 0) ? add_const(ctx, db, -1.0) : sub(ctx, db, T[1]);
-    }
+    std::size_t k = 0;
+    for (std::size_t i = 0; i < B; ++i)
+      for (int d = lo; d <= hi; ++d, ++k) T[i][d] = (d % 2 == 0) ? add_const(ctx, doubled[k], -1.0)
+                                                                  : sub(ctx, doubled[k], T[i][1]);
     if (hi == D) break;
   }
-  std::vector<Ciphertext> ts(T.begin() + 1, T.end());
-  std::vector<double> cs(coeffs.begin() + 1, coeffs.end());
+  std::vector<Ciphertext> ts;
+  std::vector<double> cs;
+  for (std::size_t i = 0; i < B; ++i)
+    for (int d = 1; d <= D; ++d) {
+      ts.push_back(T[i][d]);
+      cs.push_back(coeffs[d]);
+    }
   std::vector<Ciphertext> terms = mult_const_many(ctx, ts, cs);
-  // sum, lowest level last so each add aligns at most once
-  Ciphertext acc = terms[0];
-  for (int d = 1; d < D; ++d) acc = add(ctx, acc, terms[d]);
-  return add_const(ctx, acc, coeffs[0]);
+  for (std::size_t i = 0; i < B; ++i) {
+    Ciphertext acc = terms[i * D];
+    for (int d = 1; d < D; ++d) acc = add(ctx, acc, terms[i * D + d]);
+    out[i] = add_const(ctx, acc, coeffs[0]);
+  }
+  return out;
 }
 
 // secure_relu (layers_misc.cpp:268-295)

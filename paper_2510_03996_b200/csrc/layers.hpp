@@ -63,6 +63,8 @@ Ciphertext secure_relu(Context& ctx, const Ciphertext& x, double scale, int degr
 // ---- Chebyshev (chebyshev.cpp)
 std::vector<double> cheb_coefficients(const std::function<double(double)>& f, int degree);
 Ciphertext cheb_eval(Context& ctx, const Ciphertext& x, const std::vector<double>& coeffs);
+std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertext>& xs,
+                                       const std::vector<double>& coeffs);
 int cheb_eval_depth(int degree);
 
 // ---- declared depth costs

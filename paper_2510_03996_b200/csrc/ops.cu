@@ -278,6 +278,32 @@ __global__ void k_encode_lincomb(u64* out, LinComb lc, double scale, const Prime
   for (int i = 0; i < limbs; ++i) out[((std::size_t)i << logN) + n] = reduce_signed(c, pc[i]);
 }
 
+// ------------------------------------------------------------ bootstrapping
+// grid (N/256, npolys)
+__global__ void k_modraise(PolyList out, PolyList in, const PrimeConst* __restrict__ pc, int logN, int L) {
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 q0 = pc[0].q;
+  const u64 v = in.p[blockIdx.z][n];
+  const bool neg = v > q0 / 2;
+  u64* o = out.p[blockIdx.z];
+  for (int i = 0; i < L; ++i) {
+    const PrimeConst P = pc[i];
+    u64 x = reduce64(v, P);
+    if (neg) x = sub_mod(x, reduce64(q0, P), P.q);
+    o[((std::size_t)i << logN) + n] = x;
+  }
+}
+// grid (N/256, limbs, npolys)
+__global__ void k_mul_monomial_half(PolyList out, PolyList a, LimbConsts iq, const PrimeConst* __restrict__ pc,
+                                    int logN) {
+  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + n;
+  const u64 q = pc[blockIdx.y].q;
+  u64 v = shoup_mul(a.p[blockIdx.z][o], iq.c[blockIdx.y], iq.sh[blockIdx.y], q);
+  if ((n >> (logN - 1)) & 1u) v = v ? q - v : 0;
+  out.p[blockIdx.z][o] = v;
+}
+
 // ------------------------------------------------------------ encode etc.
 __global__ void k_coeffs_to_rns(u64* out, const long long* __restrict__ coeffs, const PrimeConst* __restrict__ pc,
                                 int logN) {
@@ -438,6 +464,17 @@ void rescale_finish(const DevTables& t, const PolyList& out, const PolyList& a, 
   launch_check("k_rescale_finish");
 }
 
+void modraise(const DevTables& t, const PolyList& out, const PolyList& in, int L, cudaStream_t st) {
+  if (out.n == 0) return;
+  k_modraise<<<grid_for(t.N, 1, out.n), kThreads, 0, st>>>(out, in, t.pc, t.logN, L);
+  launch_check("k_modraise");
+}
+void mul_monomial_half(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& iq, int limbs,
+                       cudaStream_t st) {
+  if (out.n == 0) return;
+  k_mul_monomial_half<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, iq, t.pc, t.logN);
+  launch_check("k_mul_monomial_half");
+}
 void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.nout == 0) return;
   k_mac<<<grid_for(t.N, limbs, jobs.nout), kThreads, 0, st>>>(jobs, t.pc, t.logN);

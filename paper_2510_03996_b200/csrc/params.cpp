@@ -91,14 +91,33 @@ HostTables make_tables(const Params& p) {
     q.push_back(x);
   }
   // Scaling primes, chosen top-down so the FLEXIBLEAUTO targets
-  // T_{lv-1} = T_lv^2 / q_lv stay at 2^scale_bits (no compounding drift).
+  // T_{lv-1} = T_lv^2 / q_lv follow the per-level schedule tbits[] (no
+  // compounding drift).  Without bootstrapping every level targets
+  // 2^scale_bits.  With bootstrapping the top levels (CoeffsToSlots, EvalMod)
+  // target 2^boot_scale_bits and the SlotsToCoeffs levels step linearly down
+  // to 2^scale_bits, so the raised ciphertext's linear transforms and the
+  // modular-reduction polynomial run at full precision.
+  std::vector<double> tbits(p.L, (double)p.scale_bits);
+  if (p.bootstrap && p.boot_scale_bits > p.scale_bits) {
+    const int D = bootstrap_depth(p);
+    const int lv_in = p.L - 1 - (D - p.boot_stc_levels);  // SlotsToCoeffs input level
+    for (int lv = 0; lv < p.L; ++lv) {
+      if (lv >= lv_in) tbits[lv] = p.boot_scale_bits;
+      else if (lv >= lv_in - p.boot_stc_levels) {
+        const int k = lv_in - lv;  // 1..stc
+        tbits[lv] = p.boot_scale_bits - (double)(p.boot_scale_bits - p.scale_bits) * k / p.boot_stc_levels;
+      }
+    }
+  }
   t.T.assign(p.L, 0.0);
   std::vector<u64> chosen(p.L, 0);
   {
-    double T = std::ldexp(1.0, p.scale_bits);
+    double T = std::ldexp(1.0, (int)std::lround(tbits[p.L - 1]));
     t.T[p.L - 1] = T;
     for (int lv = p.L - 1; lv >= 1; --lv) {
-      const double target = (T * T) / std::ldexp(1.0, p.scale_bits);
+      const double target = (T * T) / std::ldexp(1.0, (int)std::lround(tbits[lv - 1]));
+      if (!(target < std::ldexp(1.0, 61)) || !(target > std::ldexp(1.0, 20)))
+        throw std::invalid_argument("scale schedule needs a prime outside [2^20, 2^61)");
       const u64 tgt = static_cast<u64>(target);
       const u64 base = ((tgt - 1) / M) * M + 1;
       u64 pick = 0;

@@ -29,7 +29,18 @@ struct Params {
   int special_bits = 60;
   u64 seed = 1;
   int depth_budget = -1;  // simulator-facing level budget (<= L-1); -1 = L-1
+  int hamming_weight = 0; // secret: 0 = uniform ternary, h > 0 = exactly h nonzero (+-1)
+  int bootstrap = 0;      // 1: build the bootstrapping pipeline (needs a sparse secret)
+  int boot_scale_bits = 0;  // scale of the bootstrapping levels (0 = scale_bits)
+  // bootstrapping shape (see bootstrap.hpp)
+  int boot_k_range = 16;
+  int boot_double_angles = 3;
+  int boot_cts_levels = 3;
+  int boot_stc_levels = 3;
 };
+
+// levels consumed by bootstrapping for these parameters (bootstrap.cpp)
+int bootstrap_depth(const Params& p);
 
 // Everything derived from Params on the host.
 struct HostTables {

@@ -1,0 +1,117 @@
+"""GPU: CKKS bootstrapping, the realisation of the reference's bootstrap()
+(proj/src/backend.cpp:233-249: slot values preserved, level := depth budget,
+one `bootstrap` trace event).  Each stage is checked against an independent
+numpy model of the canonical embedding U (z_j = sum_k w_k zeta^{5^j k}):
+CoeffsToSlots = B U^{-1} / (2 (K+1)), EvalMod = sin(2 pi (K+1) u),
+SlotsToCoeffs = U B q0 / (2 pi Delta_0), ModRaise = m + q0 I with integer I.
+"""
+import numpy as np
+import pytest
+
+import paper_2510_03996_b200 as fh
+from paper_2510_03996_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+LOGN, L = 12, 24
+N, S = 1 << LOGN, 1 << (LOGN - 1)
+
+
+@pytest.fixture(scope="module")
+def bctx():
+    cfg = fh.ContextConfig(N, S, -1, fh.CryptoMetadata(55, 40, 3), limbs=L, special_limbs=8, special_bits=60,
+                           seed=5, hamming_weight=64, bootstrap=True, boot_scale_bits=55)
+    ctx = fh.SlotContext(cfg)
+    M = 2 * N
+    rot = np.array([pow(5, j, M) for j in range(S)], dtype=np.int64)
+    U = np.exp(2j * np.pi * ((rot[:, None] * np.arange(S)[None, :]) % M) / M)
+    brv = np.array([int(format(i, f"0{LOGN - 1}b")[::-1], 2) for i in range(S)])
+    return ctx, U, brv
+
+
+def test_depth_budget_and_chain(bctx):
+    ctx, _, _ = bctx
+    info = api.bootstrap_info(ctx)
+    assert info["depth"] == 3 + 7 + 3 + 3
+    assert ctx.depth_budget() == L - 1 - info["depth"]
+    T = np.log2(ctx.scales)
+    assert abs(T[0] - 40) < 0.01 and abs(T[-1] - 55) < 0.01
+
+
+def test_coeffs_to_slots_stage(bctx):
+    ctx, U, brv = bctx
+    rng = np.random.default_rng(0)
+    q0 = float(ctx.primes[0])
+    z = rng.uniform(-1, 1, S) * q0 / ctx.scales[-1]  # reinterpreted slots of O(1)
+    x = fh.SlotVector.encode_top(ctx, z)
+    y = api.bootstrap_stage(x, 1).slots_complex()
+    want = np.linalg.solve(U, z * x.scale() / q0)[brv] / (2 * 17.0)
+    assert np.abs(y - want).max() < 1e-9 * max(1.0, np.abs(want).max())
+
+
+def test_evalmod_stage(bctx):
+    ctx, _, _ = bctx
+    rng = np.random.default_rng(1)
+    u = rng.uniform(-0.95, 0.95, S)
+    x = fh.level_down(fh.SlotVector.encode_top(ctx, u), L - 3)
+    e = api.bootstrap_stage(x, 2).slots()
+    assert np.abs(e - np.sin(2 * np.pi * 17.0 * u)).max() < 1e-5
+
+
+def test_slots_to_coeffs_stage(bctx):
+    ctx, U, brv = bctx
+    rng = np.random.default_rng(2)
+    w = rng.uniform(-1, 1, S) * 1e-3
+    x = fh.SlotVector.encode_top(ctx, w)
+    s = api.bootstrap_stage(x, 3).slots_complex()
+    want = (U @ w[brv]) * float(ctx.primes[0]) / (2 * np.pi * ctx.scales[0])
+    assert np.abs(s - want).max() < 1e-6 * max(1.0, np.abs(want).max())
+
+
+def test_modraise_integer_overflow(bctx):
+    ctx, U, _ = bctx
+    rng = np.random.default_rng(3)
+    z = rng.uniform(-1, 1, S)
+    x0 = fh.level_down(fh.SlotVector.encode(ctx, z), 1)
+    r = api.bootstrap_stage(x0, 4)
+    assert r.limbs() == L
+    t = np.linalg.solve(U, r.slots_complex())          # (m + q0 I) / q0 in complex packing
+    m = np.linalg.solve(U, z * ctx.scales[0] / float(ctx.primes[0]))
+    I = t - m
+    assert np.abs(I - np.round(I)).max() < 1e-6       # integer overflow polynomial
+    assert np.abs(np.round(I)).max() <= 16            # within the EvalMod range K
+
+
+@pytest.mark.parametrize("mag", [1.0, 8.0])
+def test_bootstrap_identity_level_and_trace(bctx, mag):
+    ctx, _, _ = bctx
+    rng = np.random.default_rng(int(mag))
+    v = rng.uniform(-mag, mag, S)
+    x = fh.level_down(fh.SlotVector.encode(ctx, v), 1)
+    rec = ctx.attach_recorder()
+    y = fh.bootstrap(x)
+    ev = [(e.kind, e.value) for e in rec.snapshot()]
+    ctx.detach_recorder()
+    assert y.level() == ctx.depth_budget()
+    assert ev == [("bootstrap", ctx.depth_budget())]
+    assert np.abs(y.slots() - v).max() < 1e-4
+    # refreshed ciphertexts compute again
+    z = fh.mult_plain(y, np.full(S, 0.5))
+    assert np.abs(z.slots() - 0.5 * v).max() < 1e-4
+
+
+def test_bootstrap_from_higher_level(bctx):
+    ctx, _, _ = bctx
+    rng = np.random.default_rng(9)
+    v = rng.uniform(-1, 1, S)
+    y = fh.bootstrap(fh.SlotVector.encode(ctx, v))
+    assert y.level() == ctx.depth_budget()
+    assert np.abs(y.slots() - v).max() < 1e-4
+
+
+def test_bootstrap_requires_enabled_context():
+    cfg = fh.ContextConfig(4096, 2048, 5, fh.CryptoMetadata(50, 40, 3), limbs=6, special_limbs=2)
+    ctx = fh.SlotContext(cfg)
+    x = fh.SlotVector.encode(ctx, [1.0])
+    with pytest.raises(fh.NotImplementedInEngine):
+        fh.bootstrap(x)
