@@ -59,6 +59,8 @@ def lib():
         L.sref_time_convolution.argtypes = [_sz, _sz, C.c_int, _dp, _sz, _sz, _sz, _sz, _sz, _sz, C.c_int,
                                             C.c_int, _dp, C.c_void_p, C.c_int, C.POINTER(C.c_double)]
         L.sref_time_rotate.argtypes = [_sz, _sz, C.c_int, C.c_long, C.c_int, C.POINTER(C.c_double)]
+        L.sref_infer.argtypes = [C.c_char_p, _dp, _sz, _dp, _sz, _szp, C.POINTER(C.c_double), _ip, _sz, _szp,
+                                 C.c_char_p, _sz, _lp, _sz, _szp]
         _lib = L
     return _lib
 
@@ -192,6 +194,30 @@ class Ref:
         sec = C.c_double()
         self._check(lib().sref_time_rotate(self.ring, self.S, self.depth, t, iters, C.byref(sec)))
         return sec.value
+
+
+def infer(spec_path: str, x: np.ndarray, max_logits: int = 1 << 16):
+    """The reference's build_model + infer (model_spec.cpp:864, model_run.cpp:100) on a
+    spec JSON with CSV weights beside it.  Returns (logits, ledger rows
+    [(name, level_in, level_out, is_bootstrap)], events, wall_ms)."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1)
+    logits = np.zeros(max_logits)
+    n = C.c_size_t()
+    wall = C.c_double()
+    ledger = np.zeros(3 * 4096, dtype=np.int32)
+    nl = C.c_size_t()
+    names = C.create_string_buffer(1 << 16)
+    ev = np.zeros(2 * _EVCAP, dtype=np.int64)
+    nev = C.c_size_t()
+    rc = lib().sref_infer(spec_path.encode(), x, x.size, logits, max_logits, C.byref(n), C.byref(wall),
+                          ledger.ctypes.data_as(_ip), 4096, C.byref(nl), names, len(names),
+                          ev.ctypes.data_as(_lp), _EVCAP, C.byref(nev))
+    if rc:
+        raise RefError(lib().sref_last_error().decode(), rc)
+    nm = names.value.decode().split("\n")
+    rows = [(nm[i], int(ledger[3 * i]), int(ledger[3 * i + 1]), bool(ledger[3 * i + 2])) for i in range(nl.value)]
+    events = Ref._events(ev, nev)
+    return logits[: n.value].copy(), rows, events, wall.value
 
 
 def cheb_relu_coefficients(beta: float, degree: int) -> np.ndarray:

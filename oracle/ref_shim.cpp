@@ -21,6 +21,7 @@
 #include "slotcnn/backend.hpp"
 #include "slotcnn/chebyshev.hpp"
 #include "slotcnn/layers.hpp"
+#include "slotcnn/model.hpp"
 #include "slotcnn/packing.hpp"
 
 using namespace slotcnn;
@@ -286,6 +287,65 @@ int sref_depth_costs(std::size_t C, std::size_t F, std::size_t k,
                      std::size_t W_in, int* conv_cost) {
   return guard([&] {
     *conv_cost = conv_depth_cost(make_conv_cfg(C, F, k, stride, pad, mode, variant), W_in);
+  });
+}
+
+// ----------------------------------------------------------------- models
+// build_model (model_spec.cpp:864) + infer (model_run.cpp:100) on a spec JSON
+// with CSV weights next to it.  ledger: 3 ints per executed layer
+// (level_in, level_out, is_bootstrap); names: '\n'-separated layer names.
+int sref_infer(const char* spec_path, const double* input, std::size_t n_in,
+               double* logits, std::size_t cap, std::size_t* n_logits,
+               double* wall_ms, int* ledger, std::size_t ledger_cap,
+               std::size_t* n_layers, char* names, std::size_t names_cap,
+               long* ev, std::size_t ev_cap, std::size_t* n_ev) {
+  return guard([&] {
+    const ModelSpec spec = ModelSpec::from_json_file(spec_path);
+    const BuiltModel model = build_model(spec);
+    HostTensor x(model.input_shape.channels, model.input_shape.width,
+                 model.input_shape.width);
+    if (x.values.size() != n_in) throw ShapeError("input size mismatch");
+    std::copy(input, input + n_in, x.values.begin());
+    const InferResult r = infer(model, x);
+    if (n_logits) *n_logits = r.logits.size();
+    for (std::size_t i = 0; i < r.logits.size() && i < cap; ++i) logits[i] = r.logits[i];
+    if (wall_ms) *wall_ms = r.wall_ms;
+    std::string all;
+    std::size_t k = 0;
+    for (const auto& e : r.ledger) {
+      if (ledger && k < ledger_cap) {
+        ledger[3 * k] = e.level_in;
+        ledger[3 * k + 1] = e.level_out;
+        ledger[3 * k + 2] = e.bootstrap ? 1 : 0;
+      }
+      all += e.name + "\n";
+      ++k;
+    }
+    if (n_layers) *n_layers = k;
+    if (names && names_cap) {
+      std::strncpy(names, all.c_str(), names_cap - 1);
+      names[names_cap - 1] = 0;
+    }
+    if (n_ev) {
+      std::size_t m = 0;
+      for (const TraceEvent& e : r.trace->snapshot()) {
+        long kind = -1, value = 0;
+        switch (e.kind) {
+          case TraceEvent::Kind::rotation: kind = 0; value = e.rotation_index; break;
+          case TraceEvent::Kind::mult_plain: kind = 1; value = e.level_after; break;
+          case TraceEvent::Kind::mult_cipher: kind = 2; value = e.level_after; break;
+          case TraceEvent::Kind::bootstrap: kind = 3; value = e.level_after; break;
+          case TraceEvent::Kind::marker: break;
+        }
+        if (kind < 0) continue;
+        if (ev && m < ev_cap) {
+          ev[2 * m] = kind;
+          ev[2 * m + 1] = value;
+        }
+        ++m;
+      }
+      *n_ev = m;
+    }
   });
 }
 

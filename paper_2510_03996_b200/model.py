@@ -1,0 +1,500 @@
+"""Model runtime over the B200 engine.
+
+Host-side mirror of the reference's model runtime:
+  spec        proj/src/model_spec.cpp:117-272  (JSON schema of models/README.md)
+  build       proj/src/model_spec.cpp:456-904  (shape flow, declared depth costs,
+              standard bootstrap placement :746-776, ledger repair :789-851)
+  infer       proj/src/model_run.cpp:100-159   (per-layer ledger assertion)
+  calibrate   proj/src/model_run.cpp:364-403   (ReLU range bounds, safety 1.25)
+Every layer runs as one C-ABI call into the sm_100a engine; this module only
+orchestrates (shapes, levels, placement) -- no arithmetic happens here.
+
+Model builders `lenet5()` / `resnet20()` construct the BASELINE configs[2] /
+configs[3] architectures with seeded random weights (the reference ships no
+weights and the container has no datasets); `ModelSpec.write()` emits the
+reference's JSON + CSV format so the same model runs through oracle/_ref.
+"""
+from __future__ import annotations
+
+import copy
+import json
+import math
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import api as fh
+
+
+# ----------------------------------------------------------------- spec
+@dataclass
+class Layer:
+    type: str
+    name: str
+    params: Dict = field(default_factory=dict)
+    weights: Optional[np.ndarray] = None
+    bias: Optional[np.ndarray] = None
+    body: List["Layer"] = field(default_factory=list)
+    downsample: List["Layer"] = field(default_factory=list)
+
+
+@dataclass
+class ModelSpec:
+    name: str
+    ring_dimension: int
+    slot_count: int
+    depth_budget: int
+    input_channels: int
+    input_width: int
+    layers: List[Layer]
+    bootstrap_policy: str = "auto"
+
+    def write(self, directory: str) -> str:
+        """Reference JSON spec + CSV weights (models/README.md format)."""
+        os.makedirs(directory, exist_ok=True)
+
+        def enc(L: Layer) -> Dict:
+            d = {"type": L.type, "name": L.name}
+            d.update(L.params)
+            if L.weights is not None:
+                fn = f"{L.name}_weights.csv"
+                np.savetxt(os.path.join(directory, fn), L.weights.reshape(1, -1), delimiter=",", fmt="%.17g")
+                d["weights"] = fn
+            if L.bias is not None:
+                fn = f"{L.name}_bias.csv"
+                np.savetxt(os.path.join(directory, fn), L.bias.reshape(1, -1), delimiter=",", fmt="%.17g")
+                d["bias"] = fn
+            if L.type == "residual":
+                d["layers"] = [enc(b) for b in L.body]
+                if L.downsample:
+                    d["downsample"] = [enc(b) for b in L.downsample]
+            return d
+
+        spec = {"name": self.name,
+                "context": {"ring_dimension": self.ring_dimension, "slot_count": self.slot_count,
+                            "depth_budget": self.depth_budget},
+                "weight_mode": "preload", "bootstrap_policy": self.bootstrap_policy,
+                "input": {"channels": self.input_channels, "width": self.input_width},
+                "layers": [enc(L) for L in self.layers]}
+        path = os.path.join(directory, f"{self.name}.json")
+        with open(path, "w") as f:
+            json.dump(spec, f, indent=1)
+        return path
+
+
+def _conv(name, f, c, k, rng, std, stride=1, padding=0, mode="generic", bias=True):
+    w = rng.normal(0.0, std, (f, c, k, k))
+    b = rng.normal(0.0, std, f) if bias else None
+    p = {"out_channels": f, "kernel": k}
+    if stride != 1:
+        p["stride"] = stride
+    if padding:
+        p["padding"] = padding
+    if mode != "generic":
+        p["mode"] = mode
+    return Layer("conv", name, p, w, b)
+
+
+def lenet5(seed: int = 3001, ring: int = 32768, depth_budget: int = 12, relu_scale: float = 8.0) -> ModelSpec:
+    """BASELINE configs[2]: 1x28x28 input; conv 1->6 5x5, polyReLU, avgpool 2x2,
+    conv 6->16 5x5, polyReLU, avgpool 2x2, FC 256->120->84->10; weights N(0, 0.1^2);
+    degree-59 Chebyshev ReLU on inputs pre-scaled by 1/8."""
+    rng = np.random.default_rng(seed)
+    relu = lambda n: Layer("relu", n, {"degree": 59, "scale": relu_scale})  # noqa: E731
+
+    def fc(name, m, n):
+        return Layer("fc", name, {"outputs": m}, rng.normal(0, 0.1, (m, n)), rng.normal(0, 0.1, m))
+
+    layers = [_conv("conv1", 6, 1, 5, rng, 0.1), relu("relu1"),
+              Layer("avg_pool", "pool1", {"kernel": 2, "stride": 2}),
+              _conv("conv2", 16, 6, 5, rng, 0.1), relu("relu2"),
+              Layer("avg_pool", "pool2", {"kernel": 2, "stride": 2}),
+              fc("fc1", 120, 256), relu("relu3"), fc("fc2", 84, 120), relu("relu4"), fc("fc3", 10, 84)]
+    return ModelSpec("lenet5", ring, ring // 2, depth_budget, 1, 28, layers)
+
+
+def resnet20(seed: int = 4001, ring: int = 65536, depth_budget: int = 12) -> ModelSpec:
+    """BASELINE configs[3]: 3x32x32; 3x3 convs at 16/32/64 channels (special3x3),
+    three stages of three basic blocks, 2x2/s2 downsampling (conv + projection),
+    global avgpool, FC 64->10; He-normal weights, bias 0."""
+    rng = np.random.default_rng(seed)
+
+    def he(c, k):
+        return math.sqrt(2.0 / (c * k * k))
+
+    def c3(name, f, c):
+        return _conv(name, f, c, 3, rng, he(c, 3), padding=1, mode="special3x3", bias=False)
+
+    def relu(n):
+        return Layer("relu", n, {"degree": 59, "scale": 8.0})
+
+    layers = [c3("conv_in", 16, 3), relu("relu_in")]
+    C = 16
+    for stage, F in enumerate((16, 32, 64), start=1):
+        for unit in range(1, 4):
+            nm = f"unit{stage}_{unit}"
+            if stage > 1 and unit == 1:
+                body = [_conv(nm + "_conv1", F, C, 2, rng, he(C, 2), stride=2, bias=False), relu(nm + "_relu"),
+                        c3(nm + "_conv2", F, F)]
+                ds = [_conv(nm + "_proj", F, C, 2, rng, he(C, 2), stride=2, bias=False)]
+            else:
+                body = [c3(nm + "_conv1", F, C), relu(nm + "_relu"), c3(nm + "_conv2", F, F)]
+                ds = []
+            layers.append(Layer("residual", nm, {}, body=body, downsample=ds))
+            layers.append(relu(nm + "_relu_out"))
+            C = F
+    layers.append(Layer("global_avg_pool", "pool_global"))
+    layers.append(Layer("fc", "fc_out", {"outputs": 10}, rng.normal(0, math.sqrt(2.0 / 64), (10, 64)), np.zeros(10)))
+    return ModelSpec("resnet20", ring, ring // 2, depth_budget, 3, 32, layers)
+
+
+# ----------------------------------------------------------------- build
+@dataclass
+class Built:
+    type: str
+    name: str
+    src: Optional[Layer]
+    in_shape: Tuple
+    out_shape: Tuple
+    cost: int = 0
+    body: List["Built"] = field(default_factory=list)
+    downsample: List["Built"] = field(default_factory=list)
+
+
+def _conv_cfg(L: Layer, C: int) -> fh.ConvConfig:
+    p = L.params
+    mode = {"generic": fh.ConvMode.generic, "special3x3": fh.ConvMode.special3x3,
+            "grouped": fh.ConvMode.grouped}[p.get("mode", "generic")]
+    var = fh.StrideVariant.masked if p.get("stride_variant", "extract") == "masked" else fh.StrideVariant.extract
+    return fh.ConvConfig(C, p["out_channels"], p["kernel"], p.get("stride", 1), p.get("padding", 0), mode, var)
+
+
+def _pow2(v):
+    return v >= 2 and (v & (v - 1)) == 0
+
+
+def _cheb_depth(d):
+    return 0 if d <= 0 else (1 if d == 1 else int(d - 1).bit_length() + 1)
+
+
+def _cost(b: Built) -> int:
+    """Declared depth costs (layers_conv.cpp:596-628, layers_misc.cpp:297-322)."""
+    L, (packed, C, W, n) = b.src, b.in_shape
+    if b.type == "conv":
+        return fh.conv_depth_cost(_conv_cfg(L, C), W)
+    if b.type == "avg_pool":
+        k, S = L.params.get("kernel", 2), L.params.get("stride", 2)
+        Wo = fh.conv_output_width(W, k, S, 0)
+        if S == 1 and Wo == W:
+            return 1
+        if L.params.get("stride_variant") == "masked" and _pow2(Wo):
+            return 1 + (int(Wo - 1).bit_length() + 1 if S >= 2 else 2)
+        return 2
+    if b.type == "global_avg_pool":
+        return 1
+    if b.type == "whole_channel_pool":
+        return 2
+    if b.type == "fc":
+        return 2
+    if b.type == "relu":
+        return (1 if L.params.get("scale", 1.0) > 1.0 else 0) + _cheb_depth(L.params.get("degree", 59))
+    if b.type == "bootstrap":
+        return 0
+    raise fh.ModelError(f"no depth cost for layer type {b.type}", 2)
+
+
+def _resolve(layers: List[Layer], shape, slots) -> Tuple[List[Built], Tuple]:
+    out = []
+    for L in layers:
+        packed, C, W, n = shape
+        if L.type == "conv":
+            cfg = _conv_cfg(L, C)
+            Wo = fh.conv_output_width(W, cfg.kernel, cfg.stride, cfg.padding)
+            new = (True, cfg.out_channels, Wo, 0)
+            if cfg.out_channels * Wo * Wo > slots:
+                raise fh.ModelError(f"layer '{L.name}': output needs {cfg.out_channels * Wo * Wo} slots, context "
+                                    f"provides {slots}", 2)
+        elif L.type == "avg_pool":
+            Wo = fh.conv_output_width(W, L.params.get("kernel", 2), L.params.get("stride", 2), 0)
+            new = (True, C, Wo, 0)
+        elif L.type in ("global_avg_pool", "whole_channel_pool"):
+            new = (False, 0, 0, C)
+        elif L.type == "fc":
+            new = (False, 0, 0, L.params["outputs"])
+        elif L.type in ("relu", "bootstrap"):
+            new = shape
+        elif L.type == "residual":
+            body, bshape = _resolve(L.body, shape, slots)
+            ds, dshape = _resolve(L.downsample, shape, slots) if L.downsample else ([], shape)
+            if bshape != dshape:
+                raise fh.ModelError(f"residual '{L.name}': body and skip shapes differ", 2)
+            b = Built("residual", L.name, L, shape, bshape, body=body, downsample=ds)
+            out.append(b)
+            shape = bshape
+            continue
+        else:
+            raise fh.ModelError(f"unsupported layer type '{L.type}'", 2)
+        b = Built(L.type, L.name, L, shape, new)
+        b.cost = _cost(b)
+        out.append(b)
+        shape = new
+    return out, shape
+
+
+def _standard_placement(layers: List[Built], counters: List[int], inserted: List[int]):
+    """Bootstrap before every activation past the second, before the second
+    pooling layer and before every global reduction (model_spec.cpp:746-776);
+    counters run across residual nesting in execution order."""
+    i = 0
+    while i < len(layers):
+        b = layers[i]
+        want = False
+        if b.type == "relu":
+            want = counters[0] >= 2
+            counters[0] += 1
+        elif b.type == "avg_pool":
+            want = counters[1] == 1
+            counters[1] += 1
+        elif b.type in ("global_avg_pool", "whole_channel_pool"):
+            want = True
+            counters[1] += 1
+        elif b.type == "residual":
+            _standard_placement(b.body, counters, inserted)
+            i += 1
+            continue
+        if want and (i == 0 or layers[i - 1].type != "bootstrap"):
+            layers.insert(i, Built("bootstrap", f"bootstrap_auto_{inserted[0]}", None, b.in_shape, b.in_shape))
+            inserted[0] += 1
+            i += 1
+        i += 1
+
+
+def _ledger(layers: List[Built], entry: int, budget: int, inserted: List[int]) -> int:
+    """Level ledger with repair (model_spec.cpp:789-851): a layer that needs
+    more levels than remain gets a bootstrap inserted in front of it."""
+    level = entry
+    i = 0
+    while i < len(layers):
+        b = layers[i]
+        if b.type == "bootstrap":
+            level = budget
+            i += 1
+            continue
+        need = b.cost
+        if b.type == "residual":
+            need = b.downsample[0].cost if b.downsample else 0
+        if need > level:
+            if need > budget:
+                raise fh.ModelError(f"layer '{b.name}' needs {need} levels but the depth budget is only {budget}", 2)
+            layers.insert(i, Built("bootstrap", f"bootstrap_auto_{inserted[0]}", None, b.in_shape, b.in_shape))
+            inserted[0] += 1
+            level = budget
+            i += 1
+        if b.type == "residual":
+            d_skip = b.downsample[0].cost if b.downsample else 0
+            body_exit = _ledger(b.body, level, budget, inserted)
+            ex = min(body_exit, level - d_skip)
+            b.cost = level - ex
+            level = ex
+        else:
+            level -= b.cost
+        i += 1
+    return level
+
+
+def build(spec: ModelSpec) -> List[Built]:
+    shape = (True, spec.input_channels, spec.input_width, 0)
+    layers, _ = _resolve(spec.layers, shape, spec.slot_count)
+    inserted = [0]
+    if spec.bootstrap_policy == "auto":
+        _standard_placement(layers, [0, 0], inserted)
+    _ledger(layers, spec.depth_budget, spec.depth_budget, inserted)
+    return layers
+
+
+def count_bootstraps(layers: List[Built]) -> int:
+    n = 0
+    for b in layers:
+        n += b.type == "bootstrap"
+        n += count_bootstraps(b.body)
+    return n
+
+
+# ----------------------------------------------------------------- engine
+def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1) -> fh.ContextConfig:
+    """RNS chain for the spec's ring and depth budget: 55-bit q0, 40-bit
+    application primes, 55-bit bootstrapping levels (+16 levels), dnum 3."""
+    N = spec.ring_dimension
+    if spec.slot_count != N // 2:
+        raise fh.ShapeError("the engine packs fully: slot_count must be ring_dimension / 2", 2)
+    boot_depth = 16 if bootstrapping else 0
+    L = spec.depth_budget + 1 + boot_depth
+    dnum = 3
+    alpha = -(-L // dnum)
+    K = -(-alpha * 56 // 60) + 1
+    return fh.ContextConfig(N, N // 2, spec.depth_budget if not bootstrapping else -1,
+                            fh.CryptoMetadata(55, 40, dnum), limbs=L, special_limbs=K, special_bits=60, seed=seed,
+                            hamming_weight=64 if bootstrapping else 0, bootstrap=bootstrapping,
+                            boot_scale_bits=55 if bootstrapping else 0)
+
+
+@dataclass
+class InferResult:
+    logits: np.ndarray
+    ledger: List[Tuple[str, int, int, int, bool]]  # name, declared, level_in, level_out, bootstrap
+    wall_ms: float
+    layer_ms: Dict[str, float]
+    stats: Dict[str, int]
+
+
+class EncryptedModel:
+    """A built model bound to an engine context (keys generated on first use)."""
+
+    def __init__(self, spec: ModelSpec, seed: int = 1):
+        self.spec = spec
+        self.layers = build(spec)
+        self.n_boot = count_bootstraps(self.layers)
+        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed))
+        if self.ctx.depth_budget() != spec.depth_budget:
+            raise fh.InternalError("engine depth budget differs from the spec", 3)
+
+    def _run(self, b: Built, v, timings):
+        L = b.src
+        packed, C, W, n = b.in_shape
+        t0 = time.perf_counter()
+        if b.type == "conv":
+            w = fh.KernelTensor(L.weights, L.bias)
+            out = fh.convolution(fh.PackedTensor(v, C, W), _conv_cfg(L, C), w).data
+        elif b.type == "avg_pool":
+            cfg = fh.PoolConfig(fh.PoolKind.average, L.params.get("kernel", 2), L.params.get("stride", 2),
+                                fh.StrideVariant.masked if L.params.get("stride_variant") == "masked"
+                                else fh.StrideVariant.extract)
+            out = fh.avg_pool(fh.PackedTensor(v, C, W), cfg).data
+        elif b.type == "global_avg_pool":
+            out = fh.global_avg_pool(fh.PackedTensor(v, C, W))
+        elif b.type == "whole_channel_pool":
+            out = fh.whole_channel_pool(fh.PackedTensor(v, C, W), L.params.get("kernel", W))
+        elif b.type == "fc":
+            nin = C * W * W if packed else n
+            out = fh.fully_connected(v, fh.FcConfig(nin, L.params["outputs"], L.params.get("merge_budget", 1)),
+                                     fh.FcWeights(L.weights, L.bias))
+        elif b.type == "relu":
+            active = C * W * W if packed else n
+            out = fh.secure_relu(v, fh.ReluConfig(L.params.get("scale", 1.0), L.params.get("degree", 59), active))
+        elif b.type == "bootstrap":
+            out = fh.bootstrap(v)
+        elif b.type == "residual":
+            body = v
+            for c in b.body:
+                body = self._run(c, body, timings)
+            skip = v
+            for c in b.downsample:
+                skip = self._run(c, skip, timings)
+            out = fh.add(body, skip)
+        else:
+            raise fh.ModelError(f"unexecutable layer {b.type}", 2)
+        if timings is not None:
+            self.ctx.sync()
+            timings[b.name] = timings.get(b.name, 0.0) + (time.perf_counter() - t0) * 1e3
+        return out
+
+    def infer(self, x: np.ndarray, time_layers: bool = False) -> InferResult:
+        """Encrypt, run every layer on the GPU, decrypt the logits (model_run.cpp:100-159)."""
+        x = np.asarray(x, np.float64)
+        if x.shape != (self.spec.input_channels, self.spec.input_width, self.spec.input_width):
+            raise fh.ShapeError(f"input tensor is {x.shape}, the model expects "
+                                f"{(self.spec.input_channels, self.spec.input_width, self.spec.input_width)}", 2)
+        self.ctx.reset_stats()
+        t0 = time.perf_counter()
+        v = fh.SlotVector.encode(self.ctx, x.reshape(-1))
+        ledger = []
+        timings = {} if time_layers else None
+        for b in self.layers:
+            lin = v.level()
+            v = self._run(b, v, timings)
+            lout = v.level()
+            ledger.append((b.name, b.cost, lin, lout, b.type == "bootstrap"))
+            if b.type == "bootstrap":
+                if lout != self.spec.depth_budget:
+                    raise fh.InternalError(f"bootstrap '{b.name}' did not restore the depth budget", 3)
+            elif lin - lout != b.cost:
+                raise fh.InternalError(f"layer '{b.name}' declared {b.cost} levels but consumed {lin - lout}", 3)
+        packed, C, W, n = self.layers[-1].out_shape
+        count = C * W * W if packed else n
+        logits = v.slots()[:count]
+        wall = (time.perf_counter() - t0) * 1e3
+        return InferResult(logits, ledger, wall, timings or {}, self.ctx.stats())
+
+
+# ----------------------------------------------------------------- calibration
+def _forward_float(spec: ModelSpec, x: np.ndarray, maxima: List[float]) -> np.ndarray:
+    """True-ReLU float forward (model_run.cpp:161-358 semantics), recording the
+    max |pre-activation| of every ReLU site in execution order."""
+
+    def conv(L, t):
+        p = L.params
+        k, S, P = p["kernel"], p.get("stride", 1), p.get("padding", 0)
+        t = np.pad(t, ((0, 0), (P, P), (P, P)))
+        C, W, _ = t.shape
+        Wo = (W - k) // S + 1
+        w = L.weights
+        out = np.zeros((w.shape[0], Wo, Wo))
+        for i in range(k):
+            for j in range(k):
+                patch = t[:, i:i + S * (Wo - 1) + 1:S, j:j + S * (Wo - 1) + 1:S]
+                out += np.einsum("fc,cab->fab", w[:, :, i, j], patch)
+        if L.bias is not None:
+            out += L.bias[:, None, None]
+        return out
+
+    def run(layers, t):
+        for L in layers:
+            if L.type == "conv":
+                t = conv(L, t)
+            elif L.type == "relu":
+                maxima.append(float(np.abs(t).max()))
+                t = np.maximum(t, 0)
+            elif L.type == "avg_pool":
+                k, S = L.params.get("kernel", 2), L.params.get("stride", 2)
+                C, W, _ = t.shape
+                Wo = (W - k) // S + 1
+                t = np.stack([[[t[c, a * S:a * S + k, b * S:b * S + k].mean() for b in range(Wo)]
+                               for a in range(Wo)] for c in range(C)])
+            elif L.type in ("global_avg_pool", "whole_channel_pool"):
+                t = t.reshape(t.shape[0], -1).mean(axis=1)
+            elif L.type == "fc":
+                t = L.weights @ t.reshape(-1) + (L.bias if L.bias is not None else 0)
+            elif L.type == "residual":
+                body = run(L.body, t)
+                skip = run(L.downsample, t) if L.downsample else t
+                t = body + skip
+        return t
+
+    return run(spec.layers, x)
+
+
+def calibrate_relu_scales(spec: ModelSpec, batch: List[np.ndarray], safety: float = 1.25) -> ModelSpec:
+    """Frozen per-site ReLU scales = max(1, safety * max |pre-activation|) over a
+    calibration batch (model_run.cpp:381-403); returns a new spec."""
+    per = []
+    for x in batch:
+        m: List[float] = []
+        _forward_float(spec, x, m)
+        per.append(m)
+    mx = np.max(np.array(per), axis=0)
+    spec = copy.deepcopy(spec)
+    k = [0]
+
+    def assign(layers):
+        for L in layers:
+            if L.type == "relu":
+                L.params["scale"] = float(max(1.0, safety * mx[k[0]]))
+                k[0] += 1
+            elif L.type == "residual":
+                assign(L.body)
+
+    assign(spec.layers)
+    return spec

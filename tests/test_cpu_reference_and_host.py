@@ -151,3 +151,45 @@ def test_oracle_ops_agree_with_reference_simulator():
     cb3, s3 = o.level_down(cb, o.T[-1], 4)
     ca3, _ = o.level_down(ca, o.T[-1], 4)
     assert np.abs(o.decrypt(o.add(ca3, cb3), s3) - want.slots).max() < 1e-6 and want.level == 3
+
+
+# ------------------------------------------------------------ model runtime (host logic)
+def _flat_ledger(layers):
+    from paper_2510_03996_b200 import model as M
+    out = []
+    for b in layers:
+        out.append((b.name, b.type == "bootstrap"))
+    return out
+
+
+@pytest.mark.parametrize("budget,want", [(25, 3), (16, 4), (12, 5), (10, 6), (9, 8)])
+def test_lenet_bootstrap_placement_counts(budget, want):
+    """Standard placement + ledger repair (model_spec.cpp:746-851) give the
+    reference's bootstrap counts."""
+    from paper_2510_03996_b200 import model as M
+    assert M.count_bootstraps(M.build(M.lenet5(ring=8192, depth_budget=budget))) == want
+
+
+@pytest.mark.parametrize("budget,want", [(25, 18), (12, 19), (10, 22), (9, 38)])
+def test_resnet_bootstrap_placement_counts(budget, want):
+    from paper_2510_03996_b200 import model as M
+    assert M.count_bootstraps(M.build(M.resnet20(ring=65536, depth_budget=budget))) == want
+
+
+@need_ref
+@pytest.mark.parametrize("budget", [25, 12, 9])
+def test_lenet_ledger_matches_reference(budget, tmp_path):
+    """Layer order (incl. inserted bootstraps) and per-layer declared costs match
+    the reference's build; levels are checked on the GPU."""
+    from paper_2510_03996_b200 import model as M
+    spec = M.lenet5(ring=8192, depth_budget=budget)
+    path = spec.write(str(tmp_path))
+    x = np.random.default_rng(1).uniform(0, 1, (1, 28, 28))
+    _, rows, _, _ = sref.infer(path, x)
+    layers = M.build(spec)
+    assert [b.name for b in layers] == [r[0] for r in rows]
+    level = budget
+    for b, r in zip(layers, rows):
+        assert r[1] == level
+        level = budget if b.type == "bootstrap" else level - b.cost
+        assert r[2] == level

@@ -1,0 +1,47 @@
+"""GPU: encrypted end-to-end inference through the model runtime against the
+reference's own build_model() + infer() (oracle/_ref) on the same spec,
+weights and input: same bootstrap placement, same per-layer ledger, same
+event multiset, decrypted logits within max-abs 1e-3 (north-star tolerance).
+"""
+import tempfile
+
+import numpy as np
+import pytest
+
+from paper_2510_03996_b200 import model as M
+from oracle import ref as sref
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare(spec, x):
+    path = spec.write(tempfile.mkdtemp())
+    ref_logits, rows, ref_events, _ = sref.infer(path, x)
+    em = M.EncryptedModel(spec)
+    rec = em.ctx.attach_recorder()
+    r = em.infer(x)
+    ev = [(e.kind, e.value) for e in rec.snapshot()]
+    em.ctx.detach_recorder()
+    assert em.n_boot == sum(1 for row in rows if row[3])
+    assert [(a[0], a[2], a[3]) for a in r.ledger] == [(b[0], b[1], b[2]) for b in rows]
+    assert sorted(ev) == sorted(ref_events)
+    err = float(np.abs(r.logits - ref_logits).max())
+    assert err < 1e-3, f"max abs logit error {err}"
+    assert int(np.argmax(r.logits)) == int(np.argmax(ref_logits))
+    return err
+
+
+def test_lenet5_small_ring_with_bootstrapping():
+    """LeNet-5 (BASELINE configs[2] architecture) on a 2^13 ring, depth budget 12:
+    five standard-placement bootstraps."""
+    spec = M.lenet5(ring=8192, depth_budget=12)
+    x = np.random.default_rng(3002).uniform(0, 1, (1, 28, 28))
+    _compare(spec, x)
+
+
+def test_lenet5_no_bootstrap_deep_budget():
+    """Depth budget deep enough that the ledger needs no bootstrap except the
+    standard placements (policy auto)."""
+    spec = M.lenet5(ring=8192, depth_budget=25)
+    x = np.random.default_rng(3003).uniform(0, 1, (1, 28, 28))
+    _compare(spec, x)
