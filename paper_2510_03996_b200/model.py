@@ -70,7 +70,7 @@ class ModelSpec:
             if L.type == "residual":
                 d["layers"] = [enc(b) for b in L.body]
                 if L.downsample:
-                    d["downsample"] = [enc(b) for b in L.downsample]
+                    d["downsample"] = enc(L.downsample[0])  # a single conv object
             return d
 
         spec = {"name": self.name,

@@ -39,6 +39,20 @@ def test_lenet5_small_ring_with_bootstrapping():
     _compare(spec, x)
 
 
+def test_resnet20_full_ring_with_bootstrapping():
+    """ResNet-20 (BASELINE configs[3]): N = 2^16, depth budget 12 -> 19 bootstraps,
+    He-normal weights, calibrated frozen ReLU scales (beta = 8 diverges,
+    SURVEY.md section 0 item 6), per-channel normalised U[0,1] input."""
+    def norm(x):
+        return (x - 0.5) / 0.2887
+
+    spec = M.resnet20(ring=65536, depth_budget=12)
+    cal = [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
+    spec = M.calibrate_relu_scales(spec, cal)
+    x = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
+    _compare(spec, x)
+
+
 def test_lenet5_no_bootstrap_deep_budget():
     """Depth budget deep enough that the ledger needs no bootstrap except the
     standard placements (policy auto)."""
