@@ -251,6 +251,8 @@ def run_ours(args):
     }
     if extras:
         line["primitives"] = extras
+    if rank == 0 and not args.quick and not args.no_models:
+        line["models"] = model_runs(args)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(args)
     if rank == 0:
@@ -292,6 +294,52 @@ def primitives(ctx, fh):
         del r
     except Exception as e:  # pragma: no cover - diagnostics only
         out["config1_conv_layer_error"] = str(e)
+    return out
+
+
+def model_runs(args):
+    """Encrypted inference s/image (BASELINE configs[2], configs[3]) through the
+    model runtime: host image -> encrypt -> every layer on the GPU (bootstraps
+    placed as the reference places them) -> decrypt logits; the reference's own
+    infer() on the same spec/weights/input is timed beside it on one core."""
+    import tempfile
+    from paper_2510_03996_b200 import model as M
+    try:
+        from oracle import ref as sref
+        have_ref = sref.available()
+    except Exception:
+        have_ref = False
+
+    def norm(x):
+        return (x - 0.5) / 0.2887
+
+    out = {}
+    cases = [("lenet5", M.lenet5(ring=32768, depth_budget=12), np.random.default_rng(3001).uniform(0, 1, (1, 28, 28)))]
+    if not args.no_resnet:
+        spec = M.resnet20(ring=65536, depth_budget=12)
+        cal = [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
+        cases.append(("resnet20", M.calibrate_relu_scales(spec, cal),
+                      norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))))
+    for name, spec, x in cases:
+        em = M.EncryptedModel(spec)
+        em.infer(x)  # warm-up: lazy key generation, plaintext caches
+        times = []
+        for _ in range(args.model_reps):
+            r = em.infer(x)
+            times.append(r.wall_ms / 1e3)
+        rec = {"s_per_image": round(float(np.median(times)), 4), "reps": args.model_reps,
+               "ring_dimension": spec.ring_dimension, "depth_budget": spec.depth_budget,
+               "limbs": em.ctx.L, "bootstraps": em.n_boot, "rotations": r.stats["rotations"],
+               "keyswitches": r.stats["keyswitches"], "gpu_launches": r.stats["launches"],
+               "data": "synthetic seeded input, seeded random weights (no datasets/weights in the container)"}
+        if have_ref:
+            path = spec.write(tempfile.mkdtemp())
+            rl, rows, _, rwall = sref.infer(path, x)
+            rec["max_abs_logit_err_vs_reference"] = float(np.abs(r.logits - rl).max())
+            rec["argmax_match"] = bool(int(np.argmax(r.logits)) == int(np.argmax(rl)))
+            rec["reference_sim_s_per_image_1core"] = round(rwall / 1e3, 4)
+        out[name] = rec
+        del em
     return out
 
 
@@ -380,7 +428,10 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=12)
     ap.add_argument("--ref-iters", type=int, default=2000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="skip the primitive breakdown")
+    ap.add_argument("--quick", action="store_true", help="skip the primitive breakdown and the models")
+    ap.add_argument("--no-models", action="store_true", help="skip LeNet-5 / ResNet-20 s/image")
+    ap.add_argument("--no-resnet", action="store_true", help="skip ResNet-20 s/image")
+    ap.add_argument("--model-reps", type=int, default=2)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
