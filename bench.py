@@ -275,6 +275,17 @@ def primitives(ctx, fh):
         out[f"hoisted{r}_rot_per_s"] = round(r / (ms / 1e3), 1)
     ntt_bytes = 2 * L * N * 8 * 2
     out["ntt_hbm_gbs"] = round(ntt_bytes / (out["ntt_ms_per_ct"] / 1e3) / 1e9, 1)
+    # integer roofline of the NTT: (N/2) log2 N butterflies per limb-poly, 2L limb-polys
+    bfly = (N // 2) * LOGN * 2 * L
+    achieved = bfly / (out["ntt_ms_per_ct"] / 1e3)
+    try:
+        peak = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))["shoup_ct_butterflies_per_s"]
+        src = "measured (profiles/int_peak.json: lazy Shoup butterfly, IMAD.WIDE-bound)"
+    except Exception:
+        peak, src = 8.7e11, "fallback"
+    out["ntt_int_roofline"] = {"bound": "int", "achieved": round(achieved / 1e9, 1), "peak": round(peak / 1e9, 1),
+                               "unit": "Gbutterfly/s", "frac": round(achieved / peak, 4), "peak_source": src,
+                               "butterflies_per_ct": bfly}
     # config-1 conv layer (BASELINE configs[0]) through the layer API
     try:
         c1 = fh.SlotContext(fh.ContextConfig.preset("config1"))
