@@ -114,6 +114,11 @@ int fheon_decrypt(fheon_ctx* ctx, const fheon_ct* ct, double* out, size_t n);
 int fheon_decrypt_complex(fheon_ctx* ctx, const fheon_ct* ct, double* re, double* im, size_t n);
 /* effective depth budget (levels of fresh encryptions and bootstrap outputs) */
 int fheon_ctx_depth_budget(const fheon_ctx* ctx);
+/* rotation schedule of the layer functions: 0 = fast (hoisted sets, log-depth
+ * trees, baby-step giant-step striding; same values and levels), 1 = the
+ * reference's exact rotation sequence (layers_conv.cpp / layers_misc.cpp) */
+int fheon_ctx_set_schedule(fheon_ctx* ctx, int schedule);
+int fheon_ctx_schedule(const fheon_ctx* ctx);
 /* raw RNS words, layout [2][limbs][N] */
 int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* words, int limbs, double scale, fheon_ct** out);
 int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);

@@ -87,6 +87,8 @@ SIGNATURES = {
     "fheon_decrypt": (C.c_int, [vp, vp, dp, C.c_size_t]),
     "fheon_decrypt_complex": (C.c_int, [vp, vp, dp, dp, C.c_size_t]),
     "fheon_ctx_depth_budget": (C.c_int, [vp]),
+    "fheon_ctx_set_schedule": (C.c_int, [vp, C.c_int]),
+    "fheon_ctx_schedule": (C.c_int, [vp]),
     "fheon_ct_upload": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
     "fheon_ct_download": (C.c_int, [vp, vp, u64p]),
     "fheon_rotate": (C.c_int, [vp, vp, C.c_long, pp]),

@@ -98,6 +98,9 @@ class CryptoMetadata:
     rescaling_strategy: str = "flexibleauto"
 
 
+SCHEDULES = {"fast": 0, "reference": 1}
+
+
 @dataclass
 class ContextConfig:
     """backend.hpp:41-59 plus the RNS chain the reference leaves implicit.
@@ -117,6 +120,9 @@ class ContextConfig:
     hamming_weight: int = 0   # 0: uniform ternary secret; h: sparse (needed for bootstrapping)
     bootstrap: bool = False   # build the CKKS bootstrapping pipeline
     boot_scale_bits: int = 0  # scale of the bootstrapping levels (0 = rescale_bits)
+    # layer rotation schedule: "fast" (hoisted / log-depth / baby-step giant-step,
+    # same values and levels) or "reference" (the reference's exact rotation trace)
+    schedule: str = "fast"
 
     def validate(self):
         n, s = self.ring_dimension, self.slot_count
@@ -126,6 +132,8 @@ class ContextConfig:
             raise ShapeError(f"ring dimension must be a power of two, got {n}", 2)
         if s * 2 != n:
             raise ShapeError(f"slot count {s} must equal half the ring dimension {n} (full packing)", 2)
+        if self.schedule not in SCHEDULES:
+            raise ShapeError(f'schedule must be one of {sorted(SCHEDULES)}, got "{self.schedule}"', 2)
         if self.depth_budget < 1 and not (self.depth_budget == -1 and self.limbs):
             raise ShapeError(f"depth budget must be positive (or -1 with explicit limbs), got {self.depth_budget}",
                              2)
@@ -226,6 +234,7 @@ class SlotContext:
         self.primes = primes
         self.scales = scales
         self._slots = slots.value
+        _check(L.fheon_ctx_set_schedule(h, SCHEDULES[config.schedule]))
 
     @staticmethod
     def create(config: ContextConfig) -> "SlotContext":
@@ -246,6 +255,15 @@ class SlotContext:
     def depth_budget(self) -> int:
         """Levels of fresh encryptions and bootstrap outputs (resolved by the engine)."""
         return int(_native.lib().fheon_ctx_depth_budget(self._h))
+
+    def schedule(self) -> str:
+        v = int(_native.lib().fheon_ctx_schedule(self._h))
+        return {k: n for n, k in SCHEDULES.items()}[v]
+
+    def set_schedule(self, schedule: str):
+        if schedule not in SCHEDULES:
+            raise ShapeError(f'schedule must be one of {sorted(SCHEDULES)}, got "{schedule}"', 2)
+        _check(_native.lib().fheon_ctx_set_schedule(self._h, SCHEDULES[schedule]))
 
     def attach_recorder(self) -> TraceRecorder:
         _check(_native.lib().fheon_set_tracing(self._h, 1))

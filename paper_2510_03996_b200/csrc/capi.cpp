@@ -254,6 +254,16 @@ int fheon_decrypt_complex(fheon_ctx* ctx, const fheon_ct* ct, double* re, double
   });
 }
 int fheon_ctx_depth_budget(const fheon_ctx* ctx) { return ctx ? ctx->impl->depth_budget() : -1; }
+
+int fheon_ctx_set_schedule(fheon_ctx* ctx, int schedule) {
+  return guard([&] {
+    if (schedule != fheon::Context::kScheduleFast && schedule != fheon::Context::kScheduleReference)
+      throw fheon::Error(fheon::ErrKind::shape, "schedule must be 0 (fast) or 1 (reference)");
+    ctx->impl->schedule = schedule;
+  });
+}
+
+int fheon_ctx_schedule(const fheon_ctx* ctx) { return ctx ? ctx->impl->schedule : -1; }
 int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* w, int limbs, double scale, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::upload_ct(*ctx->impl, w, limbs, scale)); });
 }

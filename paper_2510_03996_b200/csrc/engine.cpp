@@ -648,15 +648,34 @@ BufPtr Context::encode_cached(const std::vector<double>& vals, int limbs, double
   for (const PtEntry& e : bucket)
     if (e.vals == vals) return e.buf;
   BufPtr b = encode(vals.data(), vals.size(), limbs, scale);
-  const std::size_t words = (std::size_t)limbs * ht_.N;
-  const std::size_t budget = (std::size_t)1 << 29;  // 4 GiB of cached plaintexts
+  ptcache_reserve((std::size_t)limbs * ht_.N);
+  ptcache_[key].push_back({vals, b});
+  return b;
+}
+
+BufPtr Context::encode_named(const std::string& name, const std::function<std::vector<double>()>& make, int limbs,
+                             double scale) {
+  auto key = std::make_tuple(name, limbs, scale);
+  auto it = namedcache_.find(key);
+  if (it != namedcache_.end()) return it->second;
+  const std::vector<double> vals = make();
+  BufPtr b = encode(vals.data(), vals.size(), limbs, scale);
+  ptcache_reserve((std::size_t)limbs * ht_.N);
+  namedcache_[key] = b;
+  return b;
+}
+
+// cached plaintexts stay resident up to 24 GiB of HBM (mask sets of the
+// baby-step giant-step schedules run to a few GiB at N = 2^16); past that the
+// caches start over
+void Context::ptcache_reserve(std::size_t words) {
+  const std::size_t budget = (std::size_t)3 << 30;
   if (ptcache_words_ + words > budget) {
     ptcache_.clear();
+    namedcache_.clear();
     ptcache_words_ = 0;
   }
-  ptcache_[key].push_back({vals, b});
   ptcache_words_ += words;
-  return b;
 }
 
 long long* Context::staging_slot(cudaEvent_t** ev) {

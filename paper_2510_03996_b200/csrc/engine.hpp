@@ -19,6 +19,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -149,6 +150,9 @@ class Context {
   BufPtr encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale);
   // content-addressed cache over encode() (masks reused across a layer)
   BufPtr encode_cached(const std::vector<double>& vals, int limbs, double scale);
+  // same cache keyed by a caller-chosen name (the slot values are built only on a miss)
+  BufPtr encode_named(const std::string& name, const std::function<std::vector<double>()>& make, int limbs,
+                      double scale);
   // device real-coefficient (unscaled, unrounded) encoding of a slot vector,
   // cached under `key` (block indicators of a layer geometry)
   const double* basis(const std::string& key, const std::vector<double>& slot_values);
@@ -161,6 +165,14 @@ class Context {
   void record(int kind, long value, const std::string& label = {});
   std::vector<TraceEvent> trace_snapshot() const;
   void clear_trace();
+
+  // rotation schedule of the layer algorithms: kScheduleFast hoists rotation
+  // chains into log-depth trees / baby-step giant-step sets (same outputs and
+  // levels, far fewer key switches); kScheduleReference replays the
+  // reference's exact rotation sequence (identical trace multiset)
+  static constexpr int kScheduleFast = 0, kScheduleReference = 1;
+  int schedule = kScheduleFast;
+  bool fast_schedule() const { return schedule == kScheduleFast; }
 
   OpStats stats;
   KernelTimer timer;
@@ -190,7 +202,9 @@ class Context {
     BufPtr buf;
   };
   std::map<std::tuple<u64, int, double>, std::vector<PtEntry>> ptcache_;
+  std::map<std::tuple<std::string, int, double>, BufPtr> namedcache_;
   std::size_t ptcache_words_ = 0;
+  void ptcache_reserve(std::size_t words);
   mutable std::mutex trace_mu_;
   bool tracing_ = false;
   std::vector<TraceEvent> trace_;
@@ -233,6 +247,10 @@ std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const 
 std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t);
 // xs[i] rotated by ts[i]: one batched key-switch pipeline, shared ModUp for repeated inputs
 std::vector<Ciphertext> rotate_many(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<long>& ts);
+// out[r] = sum_k rot(x_rk, t_rk): rotate-and-sum, one ModDown per output (the
+// rotated c0 terms are folded into the key-switch accumulator as P * c0)
+std::vector<Ciphertext> rotate_sum_many(Context& ctx,
+                                        const std::vector<std::vector<std::pair<Ciphertext, long>>>& groups);
 Ciphertext add(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext sub(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext add_plain(Context& ctx, const Ciphertext& a, const double* vals, std::size_t n);

@@ -161,7 +161,180 @@ std::vector<Ciphertext> keyswitch(Context& ctx, const std::vector<const u64*>& i
   return outs;
 }
 
+// ModUp of every input (batched), shared by keyswitch_sum
+BufPtr modup_all(Context& ctx, const std::vector<const u64*>& inputs, int limbs) {
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L(), E = limbs + ctx.K();
+  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const int nin = (int)inputs.size();
+  const std::size_t ext_words = (std::size_t)beta * E * N;
+  BufPtr xc = ctx.alloc((std::size_t)std::min(nin, kMaxBases) * limbs * N);
+  BufPtr ext = ctx.alloc((std::size_t)nin * ext_words);
+  for (int i0 = 0; i0 < nin; i0 += kMaxBases) {
+    const int ni = std::min(kMaxBases, nin - i0);
+    LimbSet dst = limbset(xc->ptr, ni, (std::size_t)limbs * N, limbs, limbs, L);
+    LimbSet src = dst;
+    src.nbase = ni;
+    src.blocks_per_base = 1;
+    for (int i = 0; i < ni; ++i) src.base[i] = const_cast<u64*>(inputs[i0 + i]);
+    ntt_inverse(t, dst, st, &src);
+    PolyList xl{}, el{};
+    xl.n = el.n = ni;
+    for (int i = 0; i < ni; ++i) {
+      xl.p[i] = xc->ptr + (std::size_t)i * limbs * N;
+      el.p[i] = ext->ptr + (std::size_t)(i0 + i) * ext_words;
+    }
+    modup_bconv(t, el, xl, limbs, st);
+    ntt_forward(t, limbset(ext->ptr + (std::size_t)i0 * ext_words, ni * beta, (std::size_t)E * N, E, limbs, L, 0,
+                           t.alpha),
+                st);
+  }
+  ctx.stats.ntt_limbs += (std::size_t)nin * ((std::size_t)limbs + (std::size_t)beta * (E - t.alpha));
+  return ext;
+}
+
+// Rotate-and-sum: output r = sum over jobs of group r of rot(input, g), with
+// ONE ModDown per output (kernels.hpp KsSumJobs).  jobs[k].in indexes `inputs`
+// (c1 pointers, ModUp shared by repeated inputs), c0s[in] is that input's c0.
+struct SumJob {
+  u64 g;
+  int in;
+  int group;
+};
+std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*>& inputs,
+                                      const std::vector<const u64*>& c0s, int limbs, const std::vector<SumJob>& jobs,
+                                      int ngroups) {
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L(), K = ctx.K(), E = limbs + K;
+  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const std::size_t ext_words = (std::size_t)beta * E * N;
+  ctx.stats.keyswitches += jobs.size();
+  BufPtr ext = modup_all(ctx, inputs, limbs);
+  std::vector<std::vector<const SumJob*>> by_group(ngroups);
+  for (const SumJob& j : jobs) by_group[j.group].push_back(&j);
+  std::vector<Ciphertext> outs;
+  outs.reserve(ngroups);
+  int r0 = 0;
+  while (r0 < ngroups) {
+    // pack whole groups into one launch (<= kMaxSumGroups groups, <= kMaxSumJobs jobs)
+    KsSumJobs kj{};
+    int nj = 0, R = 0;
+    while (r0 + R < ngroups && R < kMaxSumGroups) {
+      const int gsz = (int)by_group[r0 + R].size();
+      if (gsz > kMaxSumJobs) throw Error(ErrKind::internal, "rotate_sum: group larger than one launch");
+      if (nj + gsz > kMaxSumJobs) break;
+      kj.begin[R] = nj;
+      for (const SumJob* j : by_group[r0 + R]) {
+        kj.key[nj] = ctx.key(j->g);
+        kj.ext[nj] = ext->ptr + (std::size_t)j->in * ext_words;
+        kj.d[nj] = inputs[j->in];
+        kj.c0[nj] = c0s[j->in];
+        kj.g[nj] = j->g;
+        ++nj;
+      }
+      ++R;
+    }
+    kj.begin[R] = nj;
+    kj.ngroups = R;
+    BufPtr acc = ctx.alloc((std::size_t)R * 2 * E * N);
+    for (int r = 0; r < R; ++r) kj.acc[r] = acc->ptr + (std::size_t)r * 2 * E * N;
+    ks_inner_sum(t, kj, limbs, st);
+    LimbSet zs{};
+    zs.nbase = R;
+    for (int r = 0; r < R; ++r) zs.base[r] = kj.acc[r] + (std::size_t)limbs * N;
+    zs.blocks_per_base = 2;
+    zs.block_stride = (long long)E * N;
+    zs.E = K;
+    zs.ell = 0;
+    zs.L = L;
+    ntt_inverse(t, zs, st);
+    BufPtr conv = ctx.alloc((std::size_t)R * 2 * limbs * N);
+    PolyList cl{}, zl{}, al{}, ol{}, addl{};
+    cl.n = zl.n = al.n = ol.n = addl.n = 2 * R;
+    for (int r = 0; r < R; ++r) {
+      Ciphertext o = ctx.new_ct(limbs);
+      for (int p = 0; p < 2; ++p) {
+        const int i = 2 * r + p;
+        cl.p[i] = conv->ptr + (std::size_t)i * limbs * N;
+        zl.p[i] = kj.acc[r] + (std::size_t)p * E * N + (std::size_t)limbs * N;
+        al.p[i] = kj.acc[r] + (std::size_t)p * E * N;
+        ol.p[i] = p == 0 ? o.c0 : o.c1;
+        addl.p[i] = nullptr;
+        addl.g[i] = 1;
+      }
+      outs.push_back(o);
+    }
+    moddown_conv(t, cl, zl, limbs, st);
+    ntt_forward(t, limbset(conv->ptr, 2 * R, (std::size_t)limbs * N, limbs, limbs, L), st);
+    moddown_finish(t, ol, al, cl, addl, limbs, st);
+    ctx.stats.ntt_limbs += (std::size_t)R * 2 * (K + limbs);
+    r0 += R;
+  }
+  return outs;
+}
+
 }  // namespace
+
+// out[r] = sum_k rot(groups[r][k].first, groups[r][k].second): every group's
+// rotations share one ModDown; repeated inputs share one ModUp.  All terms of
+// a group must share level and scale.  Records one rotation event per term.
+std::vector<Ciphertext> rotate_sum_many(Context& ctx, const std::vector<std::vector<std::pair<Ciphertext, long>>>& groups) {
+  const long S = ctx.S();
+  std::vector<Ciphertext> outs(groups.size());
+  std::vector<std::vector<Ciphertext>> direct(groups.size());  // identity terms
+  std::map<int, std::vector<std::size_t>> by_level;              // groups with key-switched terms
+  for (std::size_t r = 0; r < groups.size(); ++r) {
+    if (groups[r].empty()) throw Error(ErrKind::internal, "rotate_sum: empty group");
+    const Ciphertext& x0 = groups[r][0].first;
+    bool ks = false;
+    for (const auto& [x, tt] : groups[r]) {
+      require_valid(x, "rotate");
+      if (tt <= -S || tt >= S)
+        throw Error(ErrKind::invalid_rotation,
+                    "rotation amount " + std::to_string(tt) + " out of range for " + std::to_string(S) + " slots");
+      if (x.limbs != x0.limbs) throw Error(ErrKind::internal, "rotate_sum: terms at different levels");
+      check_scales(x, x0, "rotate_sum");
+      ctx.record(0, tt);
+      ctx.stats.rotations++;
+      if (ctx.galois(tt) == 1) direct[r].push_back(x);
+      else ks = true;
+    }
+    if (ks) by_level[x0.limbs].push_back(r);
+  }
+  for (auto& [limbs, rs] : by_level) {
+    std::vector<const u64*> inputs, c0s;
+    std::map<const u64*, int> slot;
+    std::vector<SumJob> jobs;
+    for (std::size_t gi = 0; gi < rs.size(); ++gi)
+      for (const auto& [x, tt] : groups[rs[gi]]) {
+        const u64 g = ctx.galois(tt);
+        if (g == 1) continue;
+        auto it = slot.find(x.c1);
+        int in;
+        if (it == slot.end()) {
+          in = (int)inputs.size();
+          slot[x.c1] = in;
+          inputs.push_back(x.c1);
+          c0s.push_back(x.c0);
+        } else {
+          in = it->second;
+        }
+        jobs.push_back({g, in, (int)gi});
+      }
+    std::vector<Ciphertext> r = keyswitch_sum(ctx, inputs, c0s, limbs, jobs, (int)rs.size());
+    for (std::size_t gi = 0; gi < rs.size(); ++gi) {
+      r[gi].scale = groups[rs[gi]][0].first.scale;
+      outs[rs[gi]] = r[gi];
+    }
+  }
+  for (std::size_t r = 0; r < groups.size(); ++r)
+    for (const Ciphertext& d : direct[r]) outs[r] = outs[r].valid() ? add(ctx, outs[r], d) : d;
+  return outs;
+}
 
 // ---------------------------------------------------------------- rescale
 Ciphertext rescale(Context& ctx, const Ciphertext& a) {

@@ -108,6 +108,23 @@ struct KsJobs {
   int n;
 };
 void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st);
+// Rotate-and-sum inner product: group r accumulates its jobs [begin[r], begin[r+1])
+//   acc_r = sum_j ( sum_digit sigma_{g_j}(ext_j) * key_j  +  P * sigma_{g_j}(c0_j) [Q limbs, poly 0] )
+// so that ONE ModDown of acc_r yields sum_j rot(x_j): the c0 terms ride through
+// the division by P exactly (P * c0 is 0 mod every p_k).
+constexpr int kMaxSumJobs = 64;
+constexpr int kMaxSumGroups = 16;
+struct KsSumJobs {
+  const u64* key[kMaxSumJobs];
+  const u64* ext[kMaxSumJobs];
+  const u64* d[kMaxSumJobs];   // c1 of the input: the digit's own limbs pass through
+  const u64* c0[kMaxSumJobs];  // c0 of the input
+  u64 g[kMaxSumJobs];
+  int begin[kMaxSumGroups + 1];
+  u64* acc[kMaxSumGroups];  // [2][limbs+K][N]
+  int ngroups;
+};
+void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st);
 // ModDown front half: z[p] = coefficient-domain P limbs ([K][N], prime L+k);
 // conv[p] ([limbs][N]) = centred P-residue lifted to q_0..q_{limbs-1}
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);

@@ -13,6 +13,13 @@
 //     (2^{g-1}, 2^g] together) with batched relinearisation.
 // Event ORDER differs from the reference where independent ops are batched;
 // the event multiset (what keyplan/ledger consume) is identical.
+//
+// That is the reference schedule (Context::kScheduleReference).  The default
+// fast schedule (Context::kScheduleFast) computes the same slot values at the
+// same levels with far fewer key switches: rotation chains sum_i rot(x, i*s)
+// become doubling trees, chains of rotations of one value become hoisted sets,
+// Horner placement chains become one batched key switch, and stride
+// extraction becomes a baby-step giant-step transform (stride_bsgs_many).
 #include "layers.hpp"
 
 #include <algorithm>
@@ -91,12 +98,6 @@ std::vector<Ciphertext> mp_many(Context& ctx, const std::vector<Ciphertext>& xs,
   return mac_plain_many(ctx, t, p);
 }
 
-Ciphertext sum_all(Context& ctx, const std::vector<Ciphertext>& v) {
-  Ciphertext acc = v.at(0);
-  for (std::size_t i = 1; i < v.size(); ++i) acc = add(ctx, acc, v[i]);
-  return acc;
-}
-
 void check_stride_geometry(const Context& ctx, const Ciphertext& a, std::size_t W, std::size_t S, std::size_t W_out) {
   if (!a.valid()) throw Error(ErrKind::internal, "striding: operand is not initialized");
   if (W == 0 || S == 0 || W_out == 0) throw shape_error("striding: width, stride and output edge must be positive");
@@ -136,11 +137,47 @@ std::vector<Ciphertext> tap_rotations(Context& ctx, const Ciphertext& x, std::si
   return taps;
 }
 
+// sum_{i < span} rot(x, i * stride) for every x (fast schedule): a doubling
+// tree (x + rot(x, p*stride) for p = 1, 2, 4, ...) plus one batched round for
+// the binary tail of span -- floor(log2 span) + popcount(span) - 1 rotations
+// per input instead of a span-1 chain.  Same value: rotations are linear.
+std::vector<Ciphertext> strided_sum_many(Context& ctx, const std::vector<Ciphertext>& xs, std::size_t span,
+                                         std::size_t stride) {
+  if (span <= 1 || xs.empty()) return xs;
+  const std::size_t B = xs.size();
+  std::vector<std::vector<Ciphertext>> pw{xs};  // pw[k] = sum_{i < 2^k} rot(x, i * stride)
+  std::size_t p = 1;
+  while (p * 2 <= span) {
+    pw.push_back(add_many(ctx, pw.back(), rotate_many(ctx, pw.back(), std::vector<long>(B, (long)(p * stride)))));
+    p *= 2;
+  }
+  std::vector<Ciphertext> acc = pw.back();
+  std::vector<Ciphertext> rx;
+  std::vector<long> rt;
+  std::size_t off = p;
+  for (std::size_t bit = pw.size() - 1; bit-- > 0;)
+    if ((span >> bit) & 1u) {
+      for (std::size_t i = 0; i < B; ++i) {
+        rx.push_back(pw[bit][i]);
+        rt.push_back((long)(off * stride));
+      }
+      off += std::size_t{1} << bit;
+    }
+  if (!rx.empty()) {
+    const std::vector<Ciphertext> r = rotate_many(ctx, rx, rt);
+    for (std::size_t k0 = 0; k0 < r.size(); k0 += B)
+      acc = add_many(ctx, acc, std::vector<Ciphertext>(r.begin() + (long)k0, r.begin() + (long)(k0 + B)));
+  }
+  return acc;
+}
+
 // Channel accumulation chains (layers_conv.cpp:155-161), all output channels
-// advanced together: C-1 batched rotations by m.
+// advanced together: C-1 batched rotations by m (reference schedule), or the
+// log-depth strided sum (fast schedule).
 std::vector<Ciphertext> channel_accumulate_many(Context& ctx, std::vector<Ciphertext> sums, std::size_t C,
                                                 std::size_t m) {
   if (C <= 1) return sums;
+  if (ctx.fast_schedule()) return strided_sum_many(ctx, sums, C, m);
   std::vector<Ciphertext> cur = sums;
   for (std::size_t c = 1; c < C; ++c) {
     cur = rotate_many(ctx, cur, std::vector<long>(cur.size(), (long)m));
@@ -158,6 +195,20 @@ Ciphertext place_and_sum(Context& ctx, const std::vector<Ciphertext>& r, std::si
   Ciphertext out = r[0];
   for (const Ciphertext& p : placed) out = add(ctx, out, p);
   return out;
+}
+
+// cur[c] = rot(x, c*m), c < C: a chain (reference) or one hoisted set (fast)
+std::vector<Ciphertext> channel_cursors(Context& ctx, const Ciphertext& x, std::size_t C, std::size_t m) {
+  std::vector<Ciphertext> cur{x};
+  if (ctx.fast_schedule()) {
+    std::vector<long> ts;
+    for (std::size_t c = 1; c < C; ++c) ts.push_back((long)(c * m));
+    const std::vector<Ciphertext> r = rotate_hoisted(ctx, x, ts);
+    cur.insert(cur.end(), r.begin(), r.end());
+    return cur;
+  }
+  for (std::size_t c = 1; c < C; ++c) cur.push_back(rotate(ctx, cur.back(), (long)m));
+  return cur;
 }
 
 std::vector<Ciphertext> stride_many(Context& ctx, const std::vector<Ciphertext>& a, std::size_t W, std::size_t S,
@@ -338,10 +389,82 @@ PackedTensor pad_input(Context& ctx, const PackedTensor& x, std::size_t padding)
   return {out, C, Wp};
 }
 
+namespace {
+// stride_extract_v1's map as one baby-step giant-step linear transform (fast
+// schedule).  v1 computes out[a*W_out + b] = in[a*S*W + S*b] (a, b < W_out),
+// zero elsewhere, for one level.  Write the source offset as
+//   t(a, b) = g_a + h_b,  g_a = a*(S*W - W_out),  h_b = b*(S-1):
+//   out = sum_a rot( sum_b M_ab (*) rot(in, h_b), g_a ),  M_ab = 1 at slot a*S*W + b.
+// Baby steps are hoisted per input (one ModUp), each row is one fused MAC, the
+// giant steps one batched key switch: 2(W_out-1) rotations per input instead
+// of W_out^2 + W_out - 2, same level cost (one plaintext product).
+std::vector<Ciphertext> stride_bsgs_many(Context& ctx, const std::vector<Ciphertext>& as, std::size_t W,
+                                         std::size_t S, std::size_t W_out) {
+  const std::size_t B = as.size();
+  const std::size_t nb = S > 1 ? W_out : 1;  // distinct baby steps (S = 1: h_b = 0 for all b)
+  std::vector<std::vector<Ciphertext>> baby(B, std::vector<Ciphertext>(nb));
+  {
+    std::vector<Ciphertext> xs;
+    std::vector<long> ts;
+    for (std::size_t i = 0; i < B; ++i) {
+      baby[i][0] = as[i];
+      for (std::size_t b = 1; b < nb; ++b) {
+        xs.push_back(as[i]);
+        ts.push_back((long)(b * (S - 1)));
+      }
+    }
+    const std::vector<Ciphertext> r = rotate_many(ctx, xs, ts);
+    std::size_t k = 0;
+    for (std::size_t i = 0; i < B; ++i)
+      for (std::size_t b = 1; b < nb; ++b) baby[i][b] = r[k++];
+  }
+  const int limbs = as[0].limbs;
+  const double ps = pt_scale_for(ctx, as[0]);
+  const std::size_t Sl = (std::size_t)ctx.S();
+  std::vector<std::vector<Ciphertext>> terms(B * W_out);
+  std::vector<std::vector<BufPtr>> pts(B * W_out);
+  for (std::size_t a = 0; a < W_out; ++a) {
+    std::vector<BufPtr> masks(nb);
+    for (std::size_t b = 0; b < nb; ++b) {
+      const std::string name = "bsgs-stride:" + std::to_string(W) + ":" + std::to_string(S) + ":" +
+                               std::to_string(W_out) + ":" + std::to_string(a) + ":" + std::to_string(b);
+      masks[b] = ctx.encode_named(name, [&] {
+        std::vector<double> v(Sl, 0.0);
+        if (S > 1) v[a * S * W + b] = 1.0;
+        else std::fill(v.begin() + (long)(a * W), v.begin() + (long)(a * W + W_out), 1.0);
+        return v;
+      }, limbs, ps);
+    }
+    for (std::size_t i = 0; i < B; ++i)
+      for (std::size_t b = 0; b < nb; ++b) {
+        terms[i * W_out + a].push_back(baby[i][b]);
+        pts[i * W_out + a].push_back(masks[b]);
+      }
+  }
+  const std::vector<Ciphertext> rows = mac_plain_many(ctx, terms, pts);
+  std::vector<Ciphertext> xs;
+  std::vector<long> ts;
+  for (std::size_t i = 0; i < B; ++i)
+    for (std::size_t a = 1; a < W_out; ++a) {
+      xs.push_back(rows[i * W_out + a]);
+      ts.push_back((long)(a * (S * W - W_out)));
+    }
+  const std::vector<Ciphertext> moved = rotate_many(ctx, xs, ts);
+  std::vector<Ciphertext> out(B);
+  std::size_t k = 0;
+  for (std::size_t i = 0; i < B; ++i) {
+    out[i] = rows[i * W_out];
+    for (std::size_t a = 1; a < W_out; ++a) out[i] = add(ctx, out[i], moved[k++]);
+  }
+  return out;
+}
+}  // namespace
+
 // stride_extract_v1 (layers_conv.cpp:289-317), batched over several inputs
 std::vector<Ciphertext> stride_v1_many(Context& ctx, const std::vector<Ciphertext>& as, std::size_t W, std::size_t S,
                                        std::size_t W_out) {
   for (const Ciphertext& a : as) check_stride_geometry(ctx, a, W, S, W_out);
+  if (ctx.fast_schedule()) return stride_bsgs_many(ctx, as, W, S, W_out);
   const std::size_t B = as.size();
   std::vector<Ciphertext> vcur = as;
   std::vector<std::vector<Ciphertext>> rows(W_out);
@@ -651,25 +774,20 @@ PackedTensor avg_pool(Context& ctx, const PackedTensor& x, std::size_t k, std::s
   }
   const Ciphertext T2 = mp(ctx, T, range_mask(ctx, 0, C * m, 1.0 / (double)(k * k)));
   if (S == 1 && W_out == W) return {T2, C, W};
-  std::vector<Ciphertext> chans{T2};
-  for (std::size_t c = 1; c < C; ++c) chans.push_back(rotate(ctx, chans.back(), (long)m));
+  std::vector<Ciphertext> chans = channel_cursors(ctx, T2, C, m);
   std::vector<Ciphertext> r = stride_many(ctx, chans, W, S, W_out, variant);
   Ciphertext out = place_and_sum(ctx, r, W_out * W_out);
   return {out, C, W_out};
 }
 
 namespace {
-// merge_channel_slots (layers_misc.cpp:31-37)
+// merge_channel_slots (layers_misc.cpp:31-37): Horner chain by -1 (reference
+// schedule) or sum_c rot(piece_c, -c) as one batched key switch (fast)
 Ciphertext merge_channel_slots(Context& ctx, const std::vector<Ciphertext>& pieces) {
+  if (ctx.fast_schedule()) return place_and_sum(ctx, pieces, 1);
   Ciphertext out = pieces.back();
   for (std::size_t c = pieces.size() - 1; c-- > 0;) out = add(ctx, rotate(ctx, out, -1), pieces[c]);
   return out;
-}
-
-std::vector<Ciphertext> channel_cursors(Context& ctx, const Ciphertext& sums, std::size_t C, std::size_t m) {
-  std::vector<Ciphertext> cur{sums};
-  for (std::size_t c = 1; c < C; ++c) cur.push_back(rotate(ctx, cur.back(), (long)m));
-  return cur;
 }
 }  // namespace
 
@@ -732,7 +850,9 @@ Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std
     groups.push_back(g);
   }
   Ciphertext out = groups[T - 1];
-  for (std::size_t t = T - 1; t-- > 0;) out = add(ctx, rotate(ctx, out, -(long)r), groups[t]);
+  if (ctx.fast_schedule()) out = place_and_sum(ctx, groups, r);
+  else
+    for (std::size_t t = T - 1; t-- > 0;) out = add(ctx, rotate(ctx, out, -(long)r), groups[t]);
   std::vector<double> b(m, 0.0);
   if (bias) std::copy(bias, bias + m, b.begin());
   return add_plain(ctx, out, b.data(), b.size());

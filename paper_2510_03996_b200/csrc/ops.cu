@@ -145,6 +145,45 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
   acc[((std::size_t)E + t) * N + n] = redc(a1.hi, a1.lo, P.q, P.qinv_neg);
 }
 
+// grid (N/256, E, groups): rotate-and-sum accumulation (kernels.hpp KsSumJobs).
+// Each job's digit sum (<= beta + 1 products < q^2) is REDC'd on its own so the
+// 128-bit accumulator never exceeds q * 2^64; job results add mod q.
+__global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc, const u64* __restrict__ md_q,
+                               int logN, int limbs, int L, int K, int alpha) {
+  const std::size_t N = (std::size_t)1 << logN;
+  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  const int r = blockIdx.z;
+  const int E = limbs + K;
+  const int pt = t < limbs ? t : L + (t - limbs);
+  const PrimeConst P = pc[pt];
+  const int beta = (limbs + alpha - 1) / alpha;
+  const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;  // P mod q_t, Montgomery form
+  u64 s0 = 0, s1 = 0;
+  for (int jb = jobs.begin[r]; jb < jobs.begin[r + 1]; ++jb) {
+    const u64 g = jobs.g[jb];
+    const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
+    const u64* key = jobs.key[jb];
+    const u64* ext = jobs.ext[jb];
+    const u64* d = jobs.d[jb];
+    Acc128 a0, a1;
+    for (int j = 0; j < beta; ++j) {
+      const int lo = j * alpha;
+      const int hi = min(lo + alpha, limbs);
+      const u64 v = (t >= lo && t < hi) ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+      const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
+      a0.mac(v, kj[n]);
+      a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
+    }
+    if (t < limbs) a0.mac(jobs.c0[jb][(std::size_t)t * N + src], pm);
+    s0 = csub(s0 + redc(a0.hi, a0.lo, P.q, P.qinv_neg), P.q);
+    s1 = csub(s1 + redc(a1.hi, a1.lo, P.q, P.qinv_neg), P.q);
+  }
+  u64* acc = jobs.acc[r];
+  acc[(std::size_t)t * N + n] = s0;
+  acc[((std::size_t)E + t) * N + n] = s1;
+}
+
 // ModDown conversion with KK = K special limbs (compile time).
 // grid (N/256, ceil(limbs / kTC), npolys); the chunk's constants sit in smem.
 template <int KK>
@@ -428,6 +467,13 @@ void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStr
   TimedScope ts(t, kKsInner, st);
   k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K, t.alpha);
   launch_check("k_ks_inner");
+}
+void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st) {
+  if (jobs.ngroups == 0) return;
+  TimedScope ts(t, kKsInner, st);
+  k_ks_inner_sum<<<grid_for(t.N, limbs + t.K, jobs.ngroups), kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs,
+                                                                                 t.L, t.K, t.alpha);
+  launch_check("k_ks_inner_sum");
 }
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
   if (conv.n == 0) return;

@@ -324,7 +324,7 @@ def count_bootstraps(layers: List[Built]) -> int:
 
 
 # ----------------------------------------------------------------- engine
-def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1) -> fh.ContextConfig:
+def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: str = "fast") -> fh.ContextConfig:
     """RNS chain for the spec's ring and depth budget: 55-bit q0, 40-bit
     application primes, 55-bit bootstrapping levels (+16 levels), dnum 3."""
     N = spec.ring_dimension
@@ -338,7 +338,7 @@ def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1) -> fh.Conte
     return fh.ContextConfig(N, N // 2, spec.depth_budget if not bootstrapping else -1,
                             fh.CryptoMetadata(55, 40, dnum), limbs=L, special_limbs=K, special_bits=60, seed=seed,
                             hamming_weight=64 if bootstrapping else 0, bootstrap=bootstrapping,
-                            boot_scale_bits=55 if bootstrapping else 0)
+                            boot_scale_bits=55 if bootstrapping else 0, schedule=schedule)
 
 
 @dataclass
@@ -353,11 +353,11 @@ class InferResult:
 class EncryptedModel:
     """A built model bound to an engine context (keys generated on first use)."""
 
-    def __init__(self, spec: ModelSpec, seed: int = 1):
+    def __init__(self, spec: ModelSpec, seed: int = 1, schedule: str = "fast"):
         self.spec = spec
         self.layers = build(spec)
         self.n_boot = count_bootstraps(self.layers)
-        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed))
+        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule))
         if self.ctx.depth_budget() != spec.depth_budget:
             raise fh.InternalError("engine depth budget differs from the spec", 3)
 
