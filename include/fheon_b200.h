@@ -130,6 +130,11 @@ int fheon_rotate_hoisted(fheon_ctx* ctx, const fheon_ct* x, const long* ts, size
 /* batch: xs[i] rotated by ts[i] in one key-switch pipeline (distinct inputs batched,
  * repeated inputs hoisted); trace events in call order */
 int fheon_rotate_many(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, size_t n, fheon_ct** outs);
+/* rotate-and-sum: *out = sum_i rotate(xs[i], ts[i]) with ONE ModDown (the rotated
+ * c0 parts ride in the key-switch accumulator as P * c0); same level/scale terms.
+ * Replaces the reference's rotate + add accumulation loops (layers_conv.cpp:155-177,
+ * layers_misc.cpp:132-142); one rotation trace event per term */
+int fheon_rotate_sum(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, size_t n, fheon_ct** out);
 int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_sub(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_add_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, size_t n, fheon_ct** out);

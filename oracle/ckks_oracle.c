@@ -792,6 +792,52 @@ int ock_keyswitch(const ock_ctx* c, const u64* d, int limbs, const u64* key,
   return 0;
 }
 
+/* Rotate-and-sum with ONE ModDown (the engine's rotate_sum_many):
+ *   acc_p = sum_j [ sum_digit sigma_{g_j}(ModUp(c1_j))_digit * evk_{g_j, digit, p}
+ *                   + (p == 0 ? P * sigma_{g_j}(c0_j) on the Q limbs : 0) ]
+ *   out_p = ModDown(acc_p)
+ * P * c0 is 0 mod every special prime, so ModDown returns sum_j sigma(c0_j) +
+ * round(sum_j ks_j / P) exactly: one rounding instead of one per term. */
+int ock_rotate_sum(const ock_ctx* c, const u64* const* cts, const long* ts, int n, int limbs,
+                   const u64* const* keys, u64* out) {
+  const int L = c->L, K = c->K, E = limbs + K, LK = L + K;
+  const size_t N = c->N;
+  const int beta = (limbs + c->alpha - 1) / c->alpha;
+  u64* acc0 = (u64*)calloc((size_t)E * N, sizeof(u64));
+  u64* acc1 = (u64*)calloc((size_t)E * N, sizeof(u64));
+  u64* up = (u64*)malloc((size_t)beta * E * N * sizeof(u64));
+  size_t* idx = (size_t*)malloc(N * sizeof(size_t));
+  for (int j = 0; j < n; j++) {
+    const u64 g = ock_galois_elt(c, ts[j]);
+    const u64* ct = cts[j];
+    const u64* key = keys[j];
+    ock_modup(c, ct + (size_t)limbs * N, limbs, up);
+    for (size_t k = 0; k < N; k++) idx[k] = (g == 1) ? k : auto_index(c, k, g);
+#pragma omp parallel for
+    for (int t = 0; t < E; t++) {
+      const int pt = ext_prime(c, limbs, t);
+      const u64 m = c->q[pt];
+      u64 Pm = 1;
+      for (int k = 0; k < K; k++) Pm = mulmod(Pm, c->q[L + k] % m, m);
+      for (size_t k = 0; k < N; k++) {
+        u128 s0 = 0, s1 = 0;
+        for (int d = 0; d < beta; d++) {
+          const u64 dv = up[((size_t)d * E + t) * N + idx[k]];
+          s0 += (u128)dv * key[(((size_t)d * 2 + 0) * LK + pt) * N + k];
+          s1 += (u128)dv * key[(((size_t)d * 2 + 1) * LK + pt) * N + k];
+        }
+        if (t < limbs) s0 += (u128)ct[(size_t)t * N + idx[k]] * (t < limbs ? Pm : 0);
+        acc0[(size_t)t * N + k] = addmod(acc0[(size_t)t * N + k], (u64)(s0 % m), m);
+        acc1[(size_t)t * N + k] = addmod(acc1[(size_t)t * N + k], (u64)(s1 % m), m);
+      }
+    }
+  }
+  ock_moddown(c, acc0, limbs, out);
+  ock_moddown(c, acc1, limbs, out + (size_t)limbs * N);
+  free(acc0); free(acc1); free(up); free(idx);
+  return 0;
+}
+
 /* -------------------------------------------------------------- evaluator */
 int ock_rotate(const ock_ctx* c, const u64* ct, int limbs, long t, const u64* key, u64* out) {
   const size_t N = c->N;

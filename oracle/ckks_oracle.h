@@ -74,6 +74,9 @@ int ock_decrypt(const ock_ctx* c, const uint64_t* ct, int limbs, double scale,
 
 /* ---- key switching pieces ---- */
 int ock_modup(const ock_ctx* c, const uint64_t* d, int limbs, uint64_t* out);
+/* sum_j rotate(cts[j], ts[j]) with one ModDown (engine rotate_sum_many); cts[j] [2][limbs][N] */
+int ock_rotate_sum(const ock_ctx* c, const uint64_t* const* cts, const long* ts, int n, int limbs,
+                   const uint64_t* const* keys, uint64_t* out);
 int ock_moddown(const ock_ctx* c, const uint64_t* acc, int limbs, uint64_t* out);
 int ock_keyswitch(const ock_ctx* c, const uint64_t* d, int limbs,
                   const uint64_t* key, uint64_t g, uint64_t* ks0, uint64_t* ks1);

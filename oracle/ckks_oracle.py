@@ -54,6 +54,7 @@ def lib():
         L.ock_moddown.argtypes = [vp, _u64p, C.c_int, _u64p]
         L.ock_keyswitch.argtypes = [vp, _u64p, C.c_int, _u64p, C.c_uint64, _u64p, _u64p]
         L.ock_rotate.argtypes = [vp, _u64p, C.c_int, C.c_long, _u64p, _u64p]
+        L.ock_rotate_sum.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, _u64p]
         L.ock_rescale.argtypes = [vp, _u64p, C.c_int, _u64p]
         L.ock_rescale_poly.argtypes = [vp, _u64p, C.c_int, _u64p]
         L.ock_add.argtypes = [vp, _u64p, _u64p, C.c_int, C.c_int, _u64p]
@@ -221,6 +222,19 @@ class Oracle:
         ct = np.ascontiguousarray(ct, np.uint64)
         out = np.zeros_like(ct)
         _chk(lib().ock_rotate(self._c, ct, ct.shape[1], int(t), np.ascontiguousarray(key), out), "rotate")
+        return out
+
+    def rotate_sum(self, cts, ts, keys):
+        """sum_j rotate(cts[j], ts[j]) with one ModDown (ckks_oracle.c ock_rotate_sum)."""
+        cts = [np.ascontiguousarray(c, np.uint64) for c in cts]
+        keys = [np.ascontiguousarray(k, np.uint64) for k in keys]
+        n = len(cts)
+        limbs = cts[0].shape[1]
+        cp = (C.c_void_p * n)(*[c.ctypes.data for c in cts])
+        kp = (C.c_void_p * n)(*[k.ctypes.data for k in keys])
+        tp = (C.c_long * n)(*[int(t) for t in ts])
+        out = np.zeros((2, limbs, self.N), np.uint64)
+        _chk(lib().ock_rotate_sum(self._c, cp, tp, n, limbs, kp, out), "rotate_sum")
         return out
 
     def rescale(self, ct):

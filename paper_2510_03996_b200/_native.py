@@ -94,6 +94,7 @@ SIGNATURES = {
     "fheon_rotate": (C.c_int, [vp, vp, C.c_long, pp]),
     "fheon_rotate_hoisted": (C.c_int, [vp, vp, lp, C.c_size_t, pp]),
     "fheon_rotate_many": (C.c_int, [vp, pp, lp, C.c_size_t, pp]),
+    "fheon_rotate_sum": (C.c_int, [vp, pp, lp, C.c_size_t, pp]),
     "fheon_add": (C.c_int, [vp, vp, vp, pp]),
     "fheon_sub": (C.c_int, [vp, vp, vp, pp]),
     "fheon_add_plain": (C.c_int, [vp, vp, dp, C.c_size_t, pp]),

@@ -485,6 +485,19 @@ def rotate_many(xs: Sequence[SlotVector], ts: Sequence[int]) -> List[SlotVector]
     return [SlotVector(ctx, C.c_void_p(outs[i])) for i in range(n)]
 
 
+def rotate_sum(xs: Sequence[SlotVector], ts: Sequence[int]) -> SlotVector:
+    """sum_i rotate(xs[i], ts[i]) with one ModDown (rotate-and-sum key switch)."""
+    n = len(xs)
+    if n != len(ts) or n == 0:
+        raise ShapeError("rotate_sum: xs and ts must be non-empty and of equal length", 2)
+    ctx = xs[0]._ctx
+    hs = (C.c_void_p * n)(*[x._h.value if isinstance(x._h, C.c_void_p) else x._h for x in xs])
+    arr = (C.c_long * n)(*[int(t) for t in ts])
+    out = (C.c_void_p * 1)()
+    _check(_native.lib().fheon_rotate_sum(ctx._h, hs, arr, n, out))
+    return SlotVector(ctx, C.c_void_p(out[0]))
+
+
 def add(a: SlotVector, b: SlotVector) -> SlotVector:
     return _wrap(a._ctx, _native.lib().fheon_add, a._h, b._h)
 

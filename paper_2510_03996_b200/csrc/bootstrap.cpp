@@ -270,25 +270,10 @@ Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv) {
     pts.push_back(p);
   }
   std::vector<Ciphertext> inner = mac_plain_many(ctx_, terms, pts);
-  std::vector<Ciphertext> xs;
-  std::vector<long> ts;
-  Ciphertext acc;
-  bool have = false;
-  for (std::size_t i = 0; i < lv.giants.size(); ++i) {
-    if (lv.giants[i].rot == 0) {
-      acc = have ? add(ctx_, acc, inner[i]) : inner[i];
-      have = true;
-    } else {
-      xs.push_back(inner[i]);
-      ts.push_back(lv.giants[i].rot);
-    }
-  }
-  std::vector<Ciphertext> moved = rotate_many(ctx_, xs, ts);
-  for (const Ciphertext& m : moved) {
-    acc = have ? add(ctx_, acc, m) : m;
-    have = true;
-  }
-  return acc;
+  // giant steps: rotate-and-sum, one ModDown for the whole level
+  std::vector<std::pair<Ciphertext, long>> g;
+  for (std::size_t i = 0; i < lv.giants.size(); ++i) g.push_back({inner[i], lv.giants[i].rot});
+  return rotate_sum_many(ctx_, {g})[0];
 }
 
 Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {
@@ -300,7 +285,7 @@ Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {
     return y;
   }
   if (what == 2) {
-    std::vector<Ciphertext> ys = cheb_eval_many(ctx_, {y}, cos_coeffs_);
+    std::vector<Ciphertext> ys = cheb_eval_many(ctx_, {y}, cos_coeffs_, true);
     for (int i = 0; i < bp_.double_angles; ++i) {
       std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
       ys = add_many(ctx_, sq, sq);
@@ -328,7 +313,7 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0) {
     for (const Level& lv : cts_) y = apply(y, lv);
     const Ciphertext yc = conjugate_many(ctx_, {y})[0];
     std::vector<Ciphertext> ys = {add(ctx_, y, yc), mul_by_i(ctx_, sub(ctx_, yc, y))};
-    ys = cheb_eval_many(ctx_, ys, cos_coeffs_);
+    ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
     for (int i = 0; i < bp_.double_angles; ++i) {
       std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
       ys = add_many(ctx_, sq, sq);

@@ -297,6 +297,18 @@ int fheon_rotate_many(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts,
     for (size_t i = 0; i < n; ++i) outs[i] = wrap(r[i]);
   });
 }
+int fheon_rotate_sum(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, size_t n, fheon_ct** out) {
+  return guard([&] {
+    if (n == 0) throw fheon::Error(fheon::ErrKind::shape, "rotate_sum needs at least one term");
+    std::vector<std::pair<fheon::Ciphertext, long>> g;
+    g.reserve(n);
+    for (size_t i = 0; i < n; ++i) {
+      need(xs[i], "ciphertext");
+      g.push_back({xs[i]->ct, ts[i]});
+    }
+    *out = wrap(fheon::rotate_sum_many(*ctx->impl, {g})[0]);
+  });
+}
 int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::add(*ctx->impl, a->ct, b->ct)); });
 }

@@ -237,6 +237,8 @@ Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt);
 std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphertext>& as,
                                          const std::vector<Ciphertext>& bs);
 std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Ciphertext>& as, const std::vector<double>& cs);
+// sum_i cs[i] * xs[i] + c0 with one rescale (terms may sit at different levels)
+Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0);
 
 // ---------------------------------------------------------------- ops
 Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n);            // at the depth budget

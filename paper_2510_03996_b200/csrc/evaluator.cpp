@@ -40,6 +40,17 @@ PolyList plist(std::initializer_list<u64*> ps) {
 
 u64 signed_mod(long long k, u64 q) { return k >= 0 ? (u64)k % q : (q - 1 - (u64)(-(k + 1)) % q); }
 
+// round(x) mod q for |x| < 2^100 (constants past 2^62 are split at 2^32)
+u64 round_mod(double x, u64 q) {
+  if (std::fabs(x) < 4611686018427387904.0) return signed_mod(std::llround(x), q);
+  if (!(std::fabs(x) < 1.2676506002282294e30)) throw Error(ErrKind::capacity, "constant exceeds 2^100");
+  const double hi = std::floor(x / 4294967296.0);
+  const long long lo = std::llround(x - hi * 4294967296.0);
+  const u64 two32 = ((u64)1 << 32) % q;
+  const u64 h = mulmod(signed_mod((long long)hi, q), two32, q);
+  return addmod(h, signed_mod(lo, q), q);
+}
+
 void require_valid(const Ciphertext& c, const char* op) {
   if (!c.valid()) throw Error(ErrKind::internal, std::string(op) + ": operand is not initialized");
 }
@@ -55,6 +66,41 @@ void check_scales(const Ciphertext& a, const Ciphertext& b, const char* op) {
   if (!(std::fabs(r - 1.0) < 1e-6))
     throw Error(ErrKind::internal, std::string(op) + ": operand scales differ (" + std::to_string(a.scale) + " vs " +
                                        std::to_string(b.scale) + ")");
+}
+
+// ModUp of every input, batched (one pipeline of launches per 32 inputs):
+// [nin][beta][limbs+K][N] extended digits in the NTT domain
+BufPtr modup_all(Context& ctx, const std::vector<const u64*>& inputs, int limbs) {
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L(), E = limbs + ctx.K();
+  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const int nin = (int)inputs.size();
+  const std::size_t ext_words = (std::size_t)beta * E * N;
+  BufPtr xc = ctx.alloc((std::size_t)std::min(nin, kMaxBases) * limbs * N);
+  BufPtr ext = ctx.alloc((std::size_t)nin * ext_words);
+  for (int i0 = 0; i0 < nin; i0 += kMaxBases) {
+    const int ni = std::min(kMaxBases, nin - i0);
+    LimbSet dst = limbset(xc->ptr, ni, (std::size_t)limbs * N, limbs, limbs, L);
+    LimbSet src = dst;
+    src.nbase = ni;
+    src.blocks_per_base = 1;
+    for (int i = 0; i < ni; ++i) src.base[i] = const_cast<u64*>(inputs[i0 + i]);
+    ntt_inverse(t, dst, st, &src);
+    PolyList xl{}, el{};
+    xl.n = el.n = ni;
+    for (int i = 0; i < ni; ++i) {
+      xl.p[i] = xc->ptr + (std::size_t)i * limbs * N;
+      el.p[i] = ext->ptr + (std::size_t)(i0 + i) * ext_words;
+    }
+    modup_bconv(t, el, xl, limbs, st);
+    ntt_forward(t, limbset(ext->ptr + (std::size_t)i0 * ext_words, ni * beta, (std::size_t)E * N, E, limbs, L, 0,
+                           t.alpha),
+                st);
+  }
+  ctx.stats.ntt_limbs += (std::size_t)nin * ((std::size_t)limbs + (std::size_t)beta * (E - t.alpha));
+  return ext;
 }
 
 // Hybrid key switch of several NTT-domain inputs d_i ([limbs][N] each).  Job r
@@ -78,33 +124,10 @@ std::vector<Ciphertext> keyswitch(Context& ctx, const std::vector<const u64*>& i
   const std::size_t N = ctx.N();
   const int L = ctx.L(), K = ctx.K(), E = limbs + K;
   const int beta = (limbs + t.alpha - 1) / t.alpha;
-  const int nin = (int)inputs.size();
   ctx.stats.keyswitches += jobs.size();
 
-  // ModUp of every input, batched (one pipeline of launches per 32 inputs)
   const std::size_t ext_words = (std::size_t)beta * E * N;
-  BufPtr xc = ctx.alloc((std::size_t)nin * limbs * N);
-  BufPtr ext = ctx.alloc((std::size_t)nin * ext_words);
-  for (int i0 = 0; i0 < nin; i0 += kMaxBases) {
-    const int ni = std::min(kMaxBases, nin - i0);
-    LimbSet dst = limbset(xc->ptr + (std::size_t)i0 * limbs * N, ni, (std::size_t)limbs * N, limbs, limbs, L);
-    LimbSet src = dst;
-    src.nbase = ni;
-    src.blocks_per_base = 1;
-    for (int i = 0; i < ni; ++i) src.base[i] = const_cast<u64*>(inputs[i0 + i]);
-    ntt_inverse(t, dst, st, &src);  // out of place: c1 stays untouched
-    PolyList xl{}, el{};
-    xl.n = el.n = ni;
-    for (int i = 0; i < ni; ++i) {
-      xl.p[i] = xc->ptr + (std::size_t)(i0 + i) * limbs * N;
-      el.p[i] = ext->ptr + (std::size_t)(i0 + i) * ext_words;
-    }
-    modup_bconv(t, el, xl, limbs, st);
-    ntt_forward(t, limbset(ext->ptr + (std::size_t)i0 * ext_words, ni * beta, (std::size_t)E * N, E, limbs, L, 0,
-                           t.alpha),
-                st);
-  }
-  ctx.stats.ntt_limbs += (std::size_t)nin * ((std::size_t)limbs + (std::size_t)beta * (E - t.alpha));
+  BufPtr ext = modup_all(ctx, inputs, limbs);
 
   std::vector<const u64*> keys(jobs.size());
   for (std::size_t r = 0; r < jobs.size(); ++r) keys[r] = ctx.key(jobs[r].key_id);
@@ -159,40 +182,6 @@ std::vector<Ciphertext> keyswitch(Context& ctx, const std::vector<const u64*>& i
     ctx.stats.ntt_limbs += (std::size_t)R * 2 * (K + limbs);
   }
   return outs;
-}
-
-// ModUp of every input (batched), shared by keyswitch_sum
-BufPtr modup_all(Context& ctx, const std::vector<const u64*>& inputs, int limbs) {
-  const DevTables& t = ctx.dev();
-  cudaStream_t st = ctx.stream();
-  const std::size_t N = ctx.N();
-  const int L = ctx.L(), E = limbs + ctx.K();
-  const int beta = (limbs + t.alpha - 1) / t.alpha;
-  const int nin = (int)inputs.size();
-  const std::size_t ext_words = (std::size_t)beta * E * N;
-  BufPtr xc = ctx.alloc((std::size_t)std::min(nin, kMaxBases) * limbs * N);
-  BufPtr ext = ctx.alloc((std::size_t)nin * ext_words);
-  for (int i0 = 0; i0 < nin; i0 += kMaxBases) {
-    const int ni = std::min(kMaxBases, nin - i0);
-    LimbSet dst = limbset(xc->ptr, ni, (std::size_t)limbs * N, limbs, limbs, L);
-    LimbSet src = dst;
-    src.nbase = ni;
-    src.blocks_per_base = 1;
-    for (int i = 0; i < ni; ++i) src.base[i] = const_cast<u64*>(inputs[i0 + i]);
-    ntt_inverse(t, dst, st, &src);
-    PolyList xl{}, el{};
-    xl.n = el.n = ni;
-    for (int i = 0; i < ni; ++i) {
-      xl.p[i] = xc->ptr + (std::size_t)i * limbs * N;
-      el.p[i] = ext->ptr + (std::size_t)(i0 + i) * ext_words;
-    }
-    modup_bconv(t, el, xl, limbs, st);
-    ntt_forward(t, limbset(ext->ptr + (std::size_t)i0 * ext_words, ni * beta, (std::size_t)E * N, E, limbs, L, 0,
-                           t.alpha),
-                st);
-  }
-  ctx.stats.ntt_limbs += (std::size_t)nin * ((std::size_t)limbs + (std::size_t)beta * (E - t.alpha));
-  return ext;
 }
 
 // Rotate-and-sum: output r = sum over jobs of group r of rot(input, g), with
@@ -309,7 +298,9 @@ std::vector<Ciphertext> rotate_sum_many(Context& ctx, const std::vector<std::vec
     std::vector<const u64*> inputs, c0s;
     std::map<const u64*, int> slot;
     std::vector<SumJob> jobs;
-    for (std::size_t gi = 0; gi < rs.size(); ++gi)
+    std::vector<std::size_t> owner;  // sub-group -> group (groups larger than one launch are split)
+    for (std::size_t gi = 0; gi < rs.size(); ++gi) {
+      int in_sub = kMaxSumJobs;
       for (const auto& [x, tt] : groups[rs[gi]]) {
         const u64 g = ctx.galois(tt);
         if (g == 1) continue;
@@ -323,12 +314,19 @@ std::vector<Ciphertext> rotate_sum_many(Context& ctx, const std::vector<std::vec
         } else {
           in = it->second;
         }
-        jobs.push_back({g, in, (int)gi});
+        if (in_sub == kMaxSumJobs) {
+          owner.push_back(rs[gi]);
+          in_sub = 0;
+        }
+        jobs.push_back({g, in, (int)owner.size() - 1});
+        ++in_sub;
       }
-    std::vector<Ciphertext> r = keyswitch_sum(ctx, inputs, c0s, limbs, jobs, (int)rs.size());
-    for (std::size_t gi = 0; gi < rs.size(); ++gi) {
-      r[gi].scale = groups[rs[gi]][0].first.scale;
-      outs[rs[gi]] = r[gi];
+    }
+    std::vector<Ciphertext> r = keyswitch_sum(ctx, inputs, c0s, limbs, jobs, (int)owner.size());
+    for (std::size_t sg = 0; sg < owner.size(); ++sg) {
+      r[sg].scale = groups[owner[sg]][0].first.scale;
+      Ciphertext& o = outs[owner[sg]];
+      o = o.valid() ? add(ctx, o, r[sg]) : r[sg];
     }
   }
   for (std::size_t r = 0; r < groups.size(); ++r)
@@ -934,6 +932,58 @@ std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Cipherte
   }
   for (const Ciphertext& o : outs) ctx.record(1, o.level());
   return outs;
+}
+
+// out = sum_i cs[i] * xs[i] + c0 with ONE rescale: every term is read at the
+// lowest input level (limb drop, zero copy) and multiplied by the integer
+// k_i = round(c_i * T_out * q_top / scale_i), so the rescaled sum lands on the
+// target scale T_out of level (min level - 1) -- the level the reference's
+// per-term const-mults + aligned adds reach.  Records one mult_plain event per term.
+Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0) {
+  if (xs.empty() || xs.size() != cs.size()) throw Error(ErrKind::internal, "lincomb_const: bad term list");
+  int l = xs[0].limbs;
+  for (const Ciphertext& x : xs) {
+    require_valid(x, "mult_plain");
+    require_depth(x, "mult_plain");
+    l = std::min(l, x.limbs);
+  }
+  const HostTables& h = ctx.host();
+  const double t_out = h.T[l - 2];
+  const std::size_t n = xs.size();
+  std::vector<u64> kc(n * (std::size_t)l * 2);
+  for (std::size_t i = 0; i < n; ++i) {
+    const double x = cs[i] * t_out * (double)h.q[l - 1] / xs[i].scale;
+    for (int t = 0; t < l; ++t) {
+      const u64 v = round_mod(x, h.q[t]);
+      kc[(i * l + t) * 2] = v;
+      kc[(i * l + t) * 2 + 1] = shoup(v, h.q[t]);
+    }
+  }
+  BufPtr kd = ctx.alloc(kc.size());
+  FHEON_CUDA(cudaMemcpyAsync(kd->ptr, kc.data(), kc.size() * sizeof(u64), cudaMemcpyHostToDevice, ctx.stream()));
+  Ciphertext sum = ctx.new_ct(l);
+  sum.scale = t_out * (double)h.q[l - 1];
+  for (std::size_t i0 = 0; i0 < n; i0 += kMaxLincomb) {
+    LincombTerms lt{};
+    lt.n = (int)std::min<std::size_t>(kMaxLincomb, n - i0);
+    for (int j = 0; j < lt.n; ++j) {
+      lt.c0[j] = xs[i0 + j].c0;
+      lt.c1_off[j] = (long long)(xs[i0 + j].c1 - xs[i0 + j].c0);
+    }
+    if (i0 == 0) {
+      lincomb_const(ctx.dev(), sum.c0, sum.c1, lt, kd->ptr, l, ctx.stream());
+    } else {
+      Ciphertext part = ctx.new_ct(l);
+      lincomb_const(ctx.dev(), part.c0, part.c1, lt, kd->ptr + i0 * l * 2, l, ctx.stream());
+      ew_add(ctx.dev(), plist({sum.c0, sum.c1}), plist({sum.c0, sum.c1}), plist({part.c0, part.c1}), l,
+             ctx.stream());
+    }
+  }
+  Ciphertext out = rescale(ctx, sum);
+  out.scale = t_out;
+  ctx.stats.mult_plain += n;
+  for (std::size_t i = 0; i < n; ++i) ctx.record(1, out.level());
+  return c0 != 0.0 ? add_const(ctx, out, c0) : out;
 }
 
 std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b) {

@@ -87,6 +87,16 @@ void ew_mul_const(const DevTables& t, const PolyList& out, const PolyList& a, co
                   cudaStream_t st);
 void ew_add_const(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& c, int limbs,
                   cudaStream_t st);
+// out = sum_i k_i (*) x_i over `limbs` limbs of both polys (x_i may hold more
+// limbs: the tail is ignored).  kc = [n][limbs][2] (k_i mod q_t, Shoup) on the device.
+constexpr int kMaxLincomb = 64;
+struct LincombTerms {
+  const u64* c0[kMaxLincomb];
+  long long c1_off[kMaxLincomb];  // c1 - c0 in words
+  int n;
+};
+void lincomb_const(const DevTables& t, u64* out0, u64* out1, const LincombTerms& terms, const u64* kc, int limbs,
+                   cudaStream_t st);
 // (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1)
 void ew_tensor(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
                const u64* b1, int limbs, cudaStream_t st);

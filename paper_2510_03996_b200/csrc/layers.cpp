@@ -25,7 +25,9 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <map>
 #include <string>
+#include <tuple>
 
 namespace fheon {
 
@@ -137,6 +139,67 @@ std::vector<Ciphertext> tap_rotations(Context& ctx, const Ciphertext& x, std::si
   return taps;
 }
 
+using RotTerms = std::vector<std::pair<Ciphertext, long>>;
+
+bool same_level_and_scale(const RotTerms& g) {
+  for (const auto& [x, t] : g)
+    if (x.limbs != g[0].first.limbs || std::fabs(x.scale / g[0].first.scale - 1.0) > 1e-9) return false;
+  return true;
+}
+
+// out[r] = sum_k rot(x_rk, t_rk) for every group: rotate-and-sum key switches
+// (one ModDown per output) when a group's terms share level and scale, else
+// rotations + aligned additions.  Terms with t = 0 are plain additions (no
+// rotation event, as in the reference's loops).
+std::vector<Ciphertext> sum_rotations(Context& ctx, const std::vector<RotTerms>& groups) {
+  bool uniform = true;
+  for (const RotTerms& g : groups) uniform = uniform && same_level_and_scale(g);
+  if (uniform) {
+    std::vector<RotTerms> rot;
+    std::vector<std::size_t> who;
+    for (std::size_t r = 0; r < groups.size(); ++r) {
+      RotTerms g;
+      for (const auto& term : groups[r])
+        if (term.second != 0) g.push_back(term);
+      if (!g.empty()) {
+        rot.push_back(std::move(g));
+        who.push_back(r);
+      }
+    }
+    const std::vector<Ciphertext> rs = rot.empty() ? std::vector<Ciphertext>{} : rotate_sum_many(ctx, rot);
+    std::vector<Ciphertext> outs(groups.size());
+    for (std::size_t k = 0; k < who.size(); ++k) outs[who[k]] = rs[k];
+    for (std::size_t r = 0; r < groups.size(); ++r)
+      for (const auto& [x, t] : groups[r])
+        if (t == 0) outs[r] = outs[r].valid() ? add(ctx, outs[r], x) : x;
+    return outs;
+  }
+  std::vector<Ciphertext> outs;
+  for (const RotTerms& g : groups) {
+    std::vector<Ciphertext> xs;
+    std::vector<long> ts;
+    Ciphertext acc;
+    for (const auto& [x, t] : g) {
+      if (t == 0) {
+        acc = acc.valid() ? add(ctx, acc, x) : x;
+        continue;
+      }
+      xs.push_back(x);
+      ts.push_back(t);
+    }
+    for (const Ciphertext& r : rotate_many(ctx, xs, ts)) acc = acc.valid() ? add(ctx, acc, r) : r;
+    outs.push_back(acc);
+  }
+  return outs;
+}
+
+// out = sum_f rot(r_f, -f * block): placement rotations share one ModDown
+Ciphertext place_and_sum(Context& ctx, const std::vector<Ciphertext>& r, std::size_t block) {
+  RotTerms g;
+  for (std::size_t f = 0; f < r.size(); ++f) g.push_back({r[f], -(long)(f * block)});
+  return sum_rotations(ctx, {g})[0];
+}
+
 // sum_{i < span} rot(x, i * stride) for every x (fast schedule): a doubling
 // tree (x + rot(x, p*stride) for p = 1, 2, 4, ...) plus one batched round for
 // the binary tail of span -- floor(log2 span) + popcount(span) - 1 rotations
@@ -151,24 +214,16 @@ std::vector<Ciphertext> strided_sum_many(Context& ctx, const std::vector<Ciphert
     pw.push_back(add_many(ctx, pw.back(), rotate_many(ctx, pw.back(), std::vector<long>(B, (long)(p * stride)))));
     p *= 2;
   }
-  std::vector<Ciphertext> acc = pw.back();
-  std::vector<Ciphertext> rx;
-  std::vector<long> rt;
+  if (p == span) return pw.back();
+  std::vector<RotTerms> groups(B);
+  for (std::size_t i = 0; i < B; ++i) groups[i].push_back({pw.back()[i], 0});
   std::size_t off = p;
   for (std::size_t bit = pw.size() - 1; bit-- > 0;)
     if ((span >> bit) & 1u) {
-      for (std::size_t i = 0; i < B; ++i) {
-        rx.push_back(pw[bit][i]);
-        rt.push_back((long)(off * stride));
-      }
+      for (std::size_t i = 0; i < B; ++i) groups[i].push_back({pw[bit][i], (long)(off * stride)});
       off += std::size_t{1} << bit;
     }
-  if (!rx.empty()) {
-    const std::vector<Ciphertext> r = rotate_many(ctx, rx, rt);
-    for (std::size_t k0 = 0; k0 < r.size(); k0 += B)
-      acc = add_many(ctx, acc, std::vector<Ciphertext>(r.begin() + (long)k0, r.begin() + (long)(k0 + B)));
-  }
-  return acc;
+  return sum_rotations(ctx, groups);
 }
 
 // Channel accumulation chains (layers_conv.cpp:155-161), all output channels
@@ -187,16 +242,6 @@ std::vector<Ciphertext> channel_accumulate_many(Context& ctx, std::vector<Cipher
 }
 
 // out = sum_f rotate(r_f, -f * block): placement rotations batched
-Ciphertext place_and_sum(Context& ctx, const std::vector<Ciphertext>& r, std::size_t block) {
-  std::vector<Ciphertext> xs(r.begin() + 1, r.end());
-  std::vector<long> ts;
-  for (std::size_t f = 1; f < r.size(); ++f) ts.push_back(-(long)(f * block));
-  std::vector<Ciphertext> placed = rotate_many(ctx, xs, ts);
-  Ciphertext out = r[0];
-  for (const Ciphertext& p : placed) out = add(ctx, out, p);
-  return out;
-}
-
 // cur[c] = rot(x, c*m), c < C: a chain (reference) or one hoisted set (fast)
 std::vector<Ciphertext> channel_cursors(Context& ctx, const Ciphertext& x, std::size_t C, std::size_t m) {
   std::vector<Ciphertext> cur{x};
@@ -442,21 +487,10 @@ std::vector<Ciphertext> stride_bsgs_many(Context& ctx, const std::vector<Ciphert
       }
   }
   const std::vector<Ciphertext> rows = mac_plain_many(ctx, terms, pts);
-  std::vector<Ciphertext> xs;
-  std::vector<long> ts;
+  std::vector<RotTerms> giants(B);
   for (std::size_t i = 0; i < B; ++i)
-    for (std::size_t a = 1; a < W_out; ++a) {
-      xs.push_back(rows[i * W_out + a]);
-      ts.push_back((long)(a * (S * W - W_out)));
-    }
-  const std::vector<Ciphertext> moved = rotate_many(ctx, xs, ts);
-  std::vector<Ciphertext> out(B);
-  std::size_t k = 0;
-  for (std::size_t i = 0; i < B; ++i) {
-    out[i] = rows[i * W_out];
-    for (std::size_t a = 1; a < W_out; ++a) out[i] = add(ctx, out[i], moved[k++]);
-  }
-  return out;
+    for (std::size_t a = 0; a < W_out; ++a) giants[i].push_back({rows[i * W_out + a], (long)(a * (S * W - W_out))});
+  return sum_rotations(ctx, giants);
 }
 }  // namespace
 
@@ -768,9 +802,10 @@ PackedTensor avg_pool(Context& ctx, const PackedTensor& x, std::size_t k, std::s
     for (std::size_t j = 0; j < k; ++j)
       if (i != 0 || j != 0) ts.push_back((long)(i * W + j));
   Ciphertext T = x.data;
-  if (!ts.empty()) {
-    const std::vector<Ciphertext> r = rotate_hoisted(ctx, x.data, ts);
-    for (const Ciphertext& c : r) T = add(ctx, T, c);
+  if (!ts.empty()) {  // hoisted window taps summed under one ModDown
+    RotTerms g{{x.data, 0}};
+    for (long t : ts) g.push_back({x.data, t});
+    T = sum_rotations(ctx, {g})[0];
   }
   const Ciphertext T2 = mp(ctx, T, range_mask(ctx, 0, C * m, 1.0 / (double)(k * k)));
   if (S == 1 && W_out == W) return {T2, C, W};
@@ -830,25 +865,13 @@ Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std
   std::vector<Ciphertext> neurons = mp_many(ctx, y, std::vector<BufPtr>(m, head));
   const std::size_t r = (m <= B + 1) ? m : B;
   const std::size_t T = (m + r - 1) / r;
-  // in-group placements are independent: one batch
-  std::vector<Ciphertext> xs;
-  std::vector<long> ts;
+  // in-group placements are independent: one rotate-and-sum batch
+  std::vector<RotTerms> gterms(T);
   for (std::size_t t = 0; t < T; ++t) {
     const std::size_t sz = std::min(r, m - t * r);
-    for (std::size_t u = 1; u < sz; ++u) {
-      xs.push_back(neurons[t * r + u]);
-      ts.push_back(-(long)u);
-    }
+    for (std::size_t u = 0; u < sz; ++u) gterms[t].push_back({neurons[t * r + u], -(long)u});
   }
-  std::vector<Ciphertext> moved = rotate_many(ctx, xs, ts);
-  std::vector<Ciphertext> groups;
-  std::size_t k = 0;
-  for (std::size_t t = 0; t < T; ++t) {
-    const std::size_t sz = std::min(r, m - t * r);
-    Ciphertext g = neurons[t * r];
-    for (std::size_t u = 1; u < sz; ++u) g = add(ctx, g, moved[k++]);
-    groups.push_back(g);
-  }
+  std::vector<Ciphertext> groups = sum_rotations(ctx, gterms);
   Ciphertext out = groups[T - 1];
   if (ctx.fast_schedule()) out = place_and_sum(ctx, groups, r);
   else
@@ -887,10 +910,219 @@ Ciphertext cheb_eval(Context& ctx, const Ciphertext& x, const std::vector<double
   return cheb_eval_many(ctx, {x}, coeffs)[0];
 }
 
+namespace {
+// ---- Paterson-Stockmeyer in the Chebyshev basis (fast schedule).
+// Babies T_1..T_k (k = 2^lk), giants G_j = T_{k 2^j}; p is split recursively by
+// Chebyshev division p = q T_g + r (T_i = 2 T_g T_{i-g} - T_{2g-i}, g < i <= 2g)
+// down to leaves of degree < k, each a constant linear combination of babies
+// (one rescale).  Degree 59 takes 16 ciphertext products instead of the
+// T_d tree's 58, at the same depth.
+struct PsNode {
+  std::vector<double> c;  // leaf coefficients (degree < k) when leaf
+  int j = 0;              // giant index of the split (G_{j-1} = T_{k 2^{j-1}})
+  bool leaf = true;
+  std::unique_ptr<PsNode> q, r;
+};
+
+void cheb_divide(const std::vector<double>& c, int g, std::vector<double>& q, std::vector<double>& r) {
+  const int n = (int)c.size();
+  r.assign(c.begin(), c.begin() + std::min(n, g));
+  q.assign(std::max(0, n - g), 0.0);
+  for (int i = g; i < n; ++i) {
+    if (i == g) {
+      q[0] += c[i];
+      continue;
+    }
+    q[i - g] += 2.0 * c[i];
+    r[2 * g - i] -= c[i];
+  }
+}
+
+std::unique_ptr<PsNode> ps_build(const std::vector<double>& c, int j, int k) {
+  auto nd = std::make_unique<PsNode>();
+  const int g = j > 0 ? k << (j - 1) : 0;
+  if (j == 0 || (int)c.size() <= g) {
+    if (j == 0) {
+      nd->c = c;
+      return nd;
+    }
+    return ps_build(c, j - 1, k);
+  }
+  std::vector<double> q, r;
+  cheb_divide(c, g, q, r);
+  nd->leaf = false;
+  nd->j = j;
+  nd->q = ps_build(q, j - 1, k);
+  nd->r = ps_build(r, j - 1, k);
+  return nd;
+}
+
+bool nonconst(const std::vector<double>& c) {
+  for (std::size_t i = 1; i < c.size(); ++i)
+    if (c[i] != 0.0) return true;
+  return false;
+}
+
+int tdepth(int d) { return d <= 1 ? 0 : (int)std::bit_width((unsigned)(d - 1)); }
+
+// (depth, ciphertext products, max |coefficient|) of a tree; depth -1 = constant
+struct PsCost {
+  int depth = -1, mults = 0;
+  double cmax = 0.0;
+};
+PsCost ps_cost(const PsNode& nd, int lk) {
+  PsCost out;
+  if (nd.leaf) {
+    for (std::size_t i = 0; i < nd.c.size(); ++i) {
+      out.cmax = std::max(out.cmax, std::fabs(nd.c[i]));
+      if (i >= 1 && nd.c[i] != 0.0) out.depth = std::max(out.depth, tdepth((int)i) + 1);
+    }
+    return out;
+  }
+  const PsCost q = ps_cost(*nd.q, lk), r = ps_cost(*nd.r, lk);
+  const int gd = lk + nd.j - 1;  // depth of G_{j-1}
+  out.mults = q.mults + r.mults + (q.depth >= 0 ? 1 : 0);
+  out.depth = std::max(std::max(q.depth, gd) + 1, r.depth);
+  out.cmax = std::max(q.cmax, r.cmax);
+  return out;
+}
+
+struct PsVal {
+  Ciphertext ct;   // invalid: constant
+  double c = 0.0;  // constant part when ct is invalid
+};
+
+// evaluate node for every input; T[i][d] babies, G[i][j] giants
+std::vector<PsVal> ps_eval(Context& ctx, const PsNode& nd, std::vector<std::vector<Ciphertext>>& T,
+                           std::vector<std::vector<Ciphertext>>& G) {
+  const std::size_t B = T.size();
+  std::vector<PsVal> out(B);
+  if (nd.leaf) {
+    for (std::size_t i = 0; i < B; ++i) {
+      if (!nonconst(nd.c)) {
+        out[i].c = nd.c.empty() ? 0.0 : nd.c[0];
+        continue;
+      }
+      std::vector<Ciphertext> xs;
+      std::vector<double> cs;
+      for (std::size_t d = 1; d < nd.c.size(); ++d)
+        if (nd.c[d] != 0.0) {
+          xs.push_back(T[i][d]);
+          cs.push_back(nd.c[d]);
+        }
+      out[i].ct = lincomb_const(ctx, xs, cs, nd.c[0]);
+    }
+    return out;
+  }
+  const std::vector<PsVal> q = ps_eval(ctx, *nd.q, T, G);
+  const std::vector<PsVal> r = ps_eval(ctx, *nd.r, T, G);
+  std::vector<Ciphertext> as, bs;
+  for (std::size_t i = 0; i < B; ++i)
+    if (q[i].ct.valid()) {
+      as.push_back(q[i].ct);
+      bs.push_back(G[i][nd.j - 1]);
+    }
+  const std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
+  std::size_t k = 0;
+  for (std::size_t i = 0; i < B; ++i) {
+    Ciphertext p = q[i].ct.valid() ? prods[k++] : lincomb_const(ctx, {G[i][nd.j - 1]}, {q[i].c}, 0.0);
+    out[i].ct = r[i].ct.valid() ? add(ctx, p, r[i].ct) : add_const(ctx, p, r[i].c);
+  }
+  return out;
+}
+}  // namespace
+
+// Paterson-Stockmeyer evaluation of sum_d c_d T_d(x) for every input; empty
+// result when no baby size meets the T_d tree's depth (the caller falls back).
+// The output is brought to exactly the tree's level (input level - depth).
+std::vector<Ciphertext> cheb_eval_ps_many(Context& ctx, const std::vector<Ciphertext>& xs,
+                                          const std::vector<double>& coeffs) {
+  const int D = (int)coeffs.size() - 1;
+  if (D < 2 || xs.empty()) return {};
+  const int want = cheb_eval_depth(D);
+  int best_lk = -1, best_m = 0, best_mults = 1 << 30;
+  std::unique_ptr<PsNode> best;
+  for (int lk = 1; lk <= 5; ++lk) {
+    const int k = 1 << lk;
+    int m = 0;
+    while ((k << m) < D + 1) ++m;
+    std::unique_ptr<PsNode> root = ps_build(coeffs, m, k);
+    const PsCost c = ps_cost(*root, lk);
+    const int mults = c.mults + (std::min(k, D) - 1) + std::max(0, m - 1);
+    if (c.depth > want || c.cmax > 1e12) continue;
+    if (mults < best_mults) {
+      best_mults = mults;
+      best_lk = lk;
+      best_m = m;
+      best = std::move(root);
+    }
+  }
+  if (best_lk < 0) return {};
+  const int k = 1 << best_lk;
+  const std::size_t B = xs.size();
+  const int nb = std::min(k, D);  // babies T_1..T_nb
+  std::vector<std::vector<Ciphertext>> T(B, std::vector<Ciphertext>(nb + 1));
+  for (std::size_t i = 0; i < B; ++i) T[i][1] = xs[i];
+  std::map<std::tuple<std::size_t, int, int>, Ciphertext> lowered;
+  auto at = [&](std::size_t i, int d, int limbs) -> Ciphertext {
+    if (T[i][d].limbs <= limbs) return T[i][d];
+    auto key = std::make_tuple(i, d, limbs);
+    auto it = lowered.find(key);
+    if (it != lowered.end()) return it->second;
+    return lowered[key] = level_down(ctx, T[i][d], limbs);
+  };
+  for (int lo = 2; lo <= nb; lo = lo * 2 - 1) {
+    const int hi = std::min(nb, 2 * lo - 2 > lo ? 2 * lo - 2 : lo);
+    std::vector<Ciphertext> as, bs;
+    for (std::size_t i = 0; i < B; ++i)
+      for (int d = lo; d <= hi; ++d) {
+        const int a = (d + 1) / 2, b = d / 2;
+        const int l = std::min(T[i][a].limbs, T[i][b].limbs);
+        as.push_back(at(i, a, l));
+        bs.push_back(at(i, b, l));
+      }
+    std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
+    std::vector<Ciphertext> doubled = add_many(ctx, prods, prods);
+    std::size_t j = 0;
+    for (std::size_t i = 0; i < B; ++i)
+      for (int d = lo; d <= hi; ++d, ++j)
+        T[i][d] = (d % 2 == 0) ? add_const(ctx, doubled[j], -1.0) : sub(ctx, doubled[j], at(i, 1, doubled[j].limbs));
+    if (hi == nb) break;
+  }
+  // giants G_0 = T_k, G_j = 2 G_{j-1}^2 - 1
+  std::vector<std::vector<Ciphertext>> G(B);
+  if (best_m >= 1)
+    for (std::size_t i = 0; i < B; ++i) G[i].push_back(T[i][k]);
+  for (int j = 1; j < best_m; ++j) {
+    std::vector<Ciphertext> g;
+    for (std::size_t i = 0; i < B; ++i) g.push_back(G[i].back());
+    std::vector<Ciphertext> sq = mult_cipher_many(ctx, g, g);
+    std::vector<Ciphertext> dbl = add_many(ctx, sq, sq);
+    for (std::size_t i = 0; i < B; ++i) G[i].push_back(add_const(ctx, dbl[i], -1.0));
+  }
+  const std::vector<PsVal> v = ps_eval(ctx, *best, T, G);
+  std::vector<Ciphertext> out(B);
+  for (std::size_t i = 0; i < B; ++i) {
+    out[i] = v[i].ct.valid() ? v[i].ct : add_const(ctx, sub(ctx, xs[i], xs[i]), v[i].c);
+    const int target = xs[i].limbs - want;
+    if (out[i].limbs > target) out[i] = level_down(ctx, out[i], target);
+  }
+  return out;
+}
+
 // Several inputs through the same series: every band's products for all
 // inputs go through one batched relinearisation.
 std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertext>& xs,
                                        const std::vector<double>& coeffs) {
+  return cheb_eval_many(ctx, xs, coeffs, ctx.fast_schedule());
+}
+
+std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertext>& xs,
+                                       const std::vector<double>& coeffs, bool fused_sum) {
+  if (fused_sum) {
+    std::vector<Ciphertext> ps = cheb_eval_ps_many(ctx, xs, coeffs);
+    if (!ps.empty()) return ps;
+  }
   for (const Ciphertext& x : xs)
     if (!x.valid()) throw Error(ErrKind::internal, "cheb_eval: operand is not initialized");
   if (coeffs.empty()) throw shape_error("cheb_eval: empty coefficient list");
@@ -903,21 +1135,39 @@ std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertex
   }
   std::vector<std::vector<Ciphertext>> T(B, std::vector<Ciphertext>(D + 1));
   for (std::size_t i = 0; i < B; ++i) T[i][1] = xs[i];
+  // T_k brought down to a lower level once and reused (the operand alignment
+  // of mult_cipher / sub would otherwise repeat the same level_down per use)
+  std::map<std::tuple<std::size_t, int, int>, Ciphertext> lowered;
+  auto at = [&](std::size_t i, int k, int limbs) -> Ciphertext {
+    if (T[i][k].limbs <= limbs) return T[i][k];
+    auto key = std::make_tuple(i, k, limbs);
+    auto it = lowered.find(key);
+    if (it != lowered.end()) return it->second;
+    return lowered[key] = level_down(ctx, T[i][k], limbs);
+  };
   for (int lo = 2; lo <= D; lo = lo * 2 - 1) {
     const int hi = std::min(D, 2 * lo - 2 > lo ? 2 * lo - 2 : lo);
     std::vector<Ciphertext> as, bs;
     for (std::size_t i = 0; i < B; ++i)
       for (int d = lo; d <= hi; ++d) {
-        as.push_back(T[i][(d + 1) / 2]);
-        bs.push_back(T[i][d / 2]);
+        const int a = (d + 1) / 2, b = d / 2;
+        const int l = std::min(T[i][a].limbs, T[i][b].limbs);
+        as.push_back(at(i, a, l));
+        bs.push_back(at(i, b, l));
       }
     std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
     std::vector<Ciphertext> doubled = add_many(ctx, prods, prods);
     std::size_t k = 0;
     for (std::size_t i = 0; i < B; ++i)
-      for (int d = lo; d <= hi; ++d, ++k) T[i][d] = (d % 2 == 0) ? add_const(ctx, doubled[k], -1.0)
-                                                                  : sub(ctx, doubled[k], T[i][1]);
+      for (int d = lo; d <= hi; ++d, ++k)
+        T[i][d] = (d % 2 == 0) ? add_const(ctx, doubled[k], -1.0) : sub(ctx, doubled[k], at(i, 1, doubled[k].limbs));
     if (hi == D) break;
+  }
+  if (fused_sum) {  // sum_d c_d T_d: one fused constant MAC and one rescale per input
+    for (std::size_t i = 0; i < B; ++i)
+      out[i] = lincomb_const(ctx, std::vector<Ciphertext>(T[i].begin() + 1, T[i].end()),
+                             std::vector<double>(coeffs.begin() + 1, coeffs.end()), coeffs[0]);
+    return out;
   }
   std::vector<Ciphertext> ts;
   std::vector<double> cs;

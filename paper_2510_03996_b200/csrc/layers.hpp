@@ -65,6 +65,9 @@ std::vector<double> cheb_coefficients(const std::function<double(double)>& f, in
 Ciphertext cheb_eval(Context& ctx, const Ciphertext& x, const std::vector<double>& coeffs);
 std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertext>& xs,
                                        const std::vector<double>& coeffs);
+// fused_sum: the final sum_d c_d T_d as one constant MAC + one rescale
+std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertext>& xs,
+                                       const std::vector<double>& coeffs, bool fused_sum);
 int cheb_eval_depth(int degree);
 
 // ---- declared depth costs

@@ -50,6 +50,21 @@ __global__ void k_add_const(PolyList out, PolyList a, LimbConsts c, const PrimeC
   const u64 q = pc[blockIdx.y].q;
   out.p[blockIdx.z][o] = add_mod(a.p[blockIdx.z][o], c.c[blockIdx.y], q);
 }
+// grid (N/256, limbs, 2 polys)
+__global__ void k_lincomb_const(u64* out0, u64* out1, LincombTerms terms, const u64* __restrict__ kc,
+                                const PrimeConst* __restrict__ pc, int logN, int limbs) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  const u64 q = pc[t].q;
+  u64 s = 0;
+  for (int i = 0; i < terms.n; ++i) {
+    const u64* x = terms.c0[i] + (blockIdx.z ? terms.c1_off[i] : 0);
+    const u64* k = kc + ((std::size_t)i * limbs + t) * 2;
+    s = add_mod(s, shoup_mul(x[o], k[0], k[1], q), q);
+  }
+  (blockIdx.z ? out1 : out0)[o] = s;
+}
+
 __global__ void k_tensor(u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0, const u64* b1,
                          const PrimeConst* __restrict__ pc, int logN) {
   const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
@@ -428,6 +443,12 @@ void ew_add_const(const DevTables& t, const PolyList& out, const PolyList& a, co
   if (out.n == 0 || limbs == 0) return;
   k_add_const<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, c, t.pc, t.logN);
   launch_check("k_add_const");
+}
+void lincomb_const(const DevTables& t, u64* out0, u64* out1, const LincombTerms& terms, const u64* kc, int limbs,
+                   cudaStream_t st) {
+  if (terms.n == 0 || limbs == 0) return;
+  k_lincomb_const<<<grid_for(t.N, limbs, 2), kThreads, 0, st>>>(out0, out1, terms, kc, t.pc, t.logN, limbs);
+  launch_check("k_lincomb_const");
 }
 void ew_tensor(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
                const u64* b1, int limbs, cudaStream_t st) {

@@ -139,6 +139,26 @@ def test_hoisted_equals_single(small):
         assert np.array_equal(h.words(), orc.rotate(ct, t, orc.rotation_key(t)))
 
 
+@pytest.mark.parametrize("ts", [[1, -1], [3, 64, -1000, 2047, 5], [0, 7, 7]])
+def test_rotate_sum_bit_exact(small, ts):
+    """rotate-and-sum (one ModDown per output, c0 folded in as P * c0) is
+    bit-exact against the oracle's restatement ock_rotate_sum; identity terms
+    are added directly."""
+    ctx, orc = small
+    rng = np.random.default_rng(300 + len(ts))
+    cts = [_oracle_ct(orc, rng, counter=20 + i)[1] for i in range(len(ts))]
+    if len(ts) == 3:
+        cts[2] = cts[1]  # repeated input: shared ModUp
+    xs = [fh.SlotVector.from_words(ctx, c, orc.T[-1]) for c in cts]
+    got = fh.rotate_sum(xs, ts).words()
+    ks = [(c, t) for c, t in zip(cts, ts) if orc.galois(t) != 1]
+    want = orc.rotate_sum([c for c, _ in ks], [t for _, t in ks], [orc.rotation_key(t) for _, t in ks])
+    for c, t in zip(cts, ts):
+        if orc.galois(t) == 1:
+            want = orc.add(want, c)
+    assert np.array_equal(got, want)
+
+
 def test_keyswitch_modup_moddown(small):
     ctx, orc = small
     rng = np.random.default_rng(4)

@@ -164,6 +164,24 @@ def test_rotation_decrypts_to_left_shift(small):
         assert np.abs(o.decrypt(r, o.T[-1]) - np.roll(vals, -t)).max() < 1e-6
 
 
+def test_rotate_sum_decrypts_to_sum_of_shifts(small):
+    """rotate-and-sum with one ModDown (ock_rotate_sum) = sum of left shifts, with
+    no more noise than separate rotations followed by additions."""
+    o = small
+    rng = np.random.default_rng(17)
+    v1, v2 = rng.uniform(-1, 1, o.S), rng.uniform(-1, 1, o.S)
+    c1, c2 = o.encrypt(v1, 3), o.encrypt(v2, 4)
+    ts = [3, -7, 5, 0]
+    cts = [c1, c2, c1, c2]
+    out = o.rotate_sum(cts[:3], ts[:3], [o.rotation_key(t) for t in ts[:3]])
+    want = np.roll(v1, -3) + np.roll(v2, 7) + np.roll(v1, -5)
+    err = np.abs(o.decrypt(out, o.T[-1]) - want).max()
+    sep = o.add(o.add(o.rotate(c1, 3, o.rotation_key(3)), o.rotate(c2, -7, o.rotation_key(-7))),
+                o.rotate(c1, 5, o.rotation_key(5)))
+    err_sep = np.abs(o.decrypt(sep, o.T[-1]) - want).max()
+    assert err < 1e-6 and err <= 2 * err_sep
+
+
 def test_keyswitch_noise_bound(small):
     o = small
     rng = np.random.default_rng(8)
