@@ -334,7 +334,12 @@ def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: s
     L = spec.depth_budget + 1 + boot_depth
     dnum = 3
     alpha = -(-L // dnum)
-    K = -(-alpha * 56 // 60) + 1
+    # special primes (60-bit): the fewest whose product P exceeds every digit
+    # modulus Q_j by 2 bits (chain: 55-bit q0, 40-bit application primes,
+    # 55-bit bootstrapping primes); the engine re-checks P > Q_j exactly
+    bits = [55] + [40] * spec.depth_budget + [55] * boot_depth
+    widest = max(sum(bits[j:j + alpha]) + 0.1 * len(bits[j:j + alpha]) for j in range(0, L, alpha))
+    K = -(-int(widest + 2.0) // 59)
     return fh.ContextConfig(N, N // 2, spec.depth_budget if not bootstrapping else -1,
                             fh.CryptoMetadata(55, 40, dnum), limbs=L, special_limbs=K, special_bits=60, seed=seed,
                             hamming_weight=64 if bootstrapping else 0, bootstrap=bootstrapping,
