@@ -11,12 +11,15 @@
 //            (stride-N2 elements), phase ROW runs the last n2 stages on each
 //            contiguous row of N2 elements;
 //   inverse: ROW (first n2 GS stages) then COL (last n1 stages, scale N^{-1}).
-// Each CTA stages a tile of lines (16 columns, or a block of rows) in shared
-// memory; each line (sub-NTT of M <= 256 points) is owned by M/E threads that
-// hold E = 2^RB elements in registers and run RB radix-2 stages per register
-// pass (one smem exchange per RB stages, __syncwarp only: a line never spans
-// warps).  Shared-memory rows are padded by one word per 8 so the strided
-// register passes and the transposed column loads hit distinct banks.
+// Each thread owns E = 8 elements of one line (sub-NTT of M <= 256 points,
+// M/8 threads per line) and runs up to 3 radix-2 stages per register pass.
+// The first pass's layout (elements tp + e*M/8 for forward, 8 tp + e for
+// inverse) and the last pass's are read / written straight from / to global
+// memory, coalesced: in COL tiles the lanes of a warp span 16 adjacent
+// columns, in ROW tiles a line's threads are consecutive.  Only the
+// re-layouts between passes go through shared memory (line-major, one pad
+// word per 8 so both tile shapes are bank-conflict free); a line never spans
+// warps in ROW tiles (__syncwarp), it does in COL tiles (__syncthreads).
 //
 // Arithmetic: Harvey lazy butterflies.  Forward values live in [0, 4q)
 // (CT: X <- X mod 2q; T = Shoup(Y, W) in [0, 2q); X+T, X-T+2q), inverse
@@ -39,24 +42,41 @@ __device__ __forceinline__ int pad8(int k) { return k + (k >> 3); }
 // r = a * w mod q in [0, 2q) for any a < 2^64 (Shoup, no final correction)
 __device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) { return a * w - mulhi(a, wsh) * q; }
 
-template <int LOGM, bool COL, int RB>
+template <int LOGM, bool COL>
 struct Geometry {
   static constexpr int M = 1 << LOGM;
-  static constexpr int E = 1 << RB;  // elements per thread
+  static constexpr int E = 8;        // elements per thread
   static constexpr int T = M / E;    // threads per line
-  // columns: 16 per CTA (128-byte row segments); rows: ~256 threads per CTA
   static constexpr int ROWL = (256 / T) < 32 ? (256 / T) : 32;
-  static constexpr int LPC = COL ? 16 : (ROWL < 1 ? 1 : ROWL);
+  static constexpr int LPC = COL ? 16 : ROWL;  // lines per CTA
   static constexpr int THREADS = LPC * T;
   static constexpr int LS = M + M / 8 + 1;  // padded line stride (words)
+  static constexpr int NG = (LOGM + 2) / 3;  // register passes
 };
 
-template <int LOGM, bool INV, bool COL, int RB>
-__global__ void __launch_bounds__(Geometry<LOGM, COL, RB>::THREADS)
+// element positions of pass gi: idx(e) = base | (e << b)
+template <int LOGM, bool INV>
+__device__ __forceinline__ void pass_shape(int gi, int tp, int& b, int& nst, int& hb0, int& base) {
+  if (!INV) {
+    const int top = LOGM - 1 - 3 * gi;
+    nst = top + 1 < 3 ? top + 1 : 3;
+    b = top - 2 > 0 ? top - 2 : 0;
+    hb0 = top;
+  } else {
+    const int low = 3 * gi;
+    nst = LOGM - low < 3 ? LOGM - low : 3;
+    b = low < LOGM - 3 ? low : LOGM - 3;
+    hb0 = low;
+  }
+  base = ((tp >> b) << (b + 3)) | (tp & ((1 << b) - 1));
+}
+
+template <int LOGM, bool INV, bool COL>
+__global__ void __launch_bounds__(Geometry<LOGM, COL>::THREADS)
     ntt_phase_kernel(LimbSet set, LimbSet src, bool has_src, const PrimeConst* __restrict__ pc,
                      const u64* __restrict__ tw, int logN, int n1, int n2) {
-  using G = Geometry<LOGM, COL, RB>;
-  constexpr int M = G::M, E = G::E, T = G::T, LPC = G::LPC, LS = G::LS;
+  using G = Geometry<LOGM, COL>;
+  constexpr int M = G::M, E = G::E, T = G::T, LPC = G::LPC, LS = G::LS, NG = G::NG;
   // the phase that runs first (forward COL / inverse ROW) reads canonical input and
   // leaves lazy values; the second phase reduces to canonical.
   constexpr bool FIRST = (COL != INV);
@@ -79,55 +99,45 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, RB>::THREADS)
   const ulonglong2* twp = reinterpret_cast<const ulonglong2*>(tw + (std::size_t)prime * 4 * N + (INV ? 2 * N : 0));
   const int N2 = 1 << n2;
   const int line0 = blockIdx.x * LPC;
-
-  // ---- load tile (16-byte vector loads: two adjacent columns / elements)
-  for (int x = threadIdx.x; x < LPC * M / 2; x += blockDim.x) {
-    int line, k;
-    std::size_t g;
-    if (COL) {
-      k = x / (LPC / 2);
-      line = 2 * (x - k * (LPC / 2));
-      g = (std::size_t)k * N2 + line0 + line;
-      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(in + g);
-      sm[line * LS + pad8(k)] = v.x;
-      sm[(line + 1) * LS + pad8(k)] = v.y;
-    } else {
-      line = x / (M / 2);
-      k = 2 * (x - line * (M / 2));
-      g = (std::size_t)(line0 + line) * N2 + k;
-      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(in + g);
-      sm[line * LS + pad8(k)] = v.x;
-      sm[line * LS + pad8(k + 1)] = v.y;
-    }
-  }
-  __syncthreads();
-
-  const int li = threadIdx.x / T;
-  const int t = threadIdx.x - li * T;
+  // COL: lanes span the tile's 16 columns; ROW: a line's T threads are consecutive
+  const int li = COL ? (int)(threadIdx.x % LPC) : (int)(threadIdx.x / T);
+  const int tp = COL ? (int)(threadIdx.x / LPC) : (int)(threadIdx.x % T);
   u64* lsm = sm + li * LS;
+  auto gaddr = [&](int k) -> std::size_t {
+    return COL ? (std::size_t)k * N2 + line0 + li : (std::size_t)(line0 + li) * N2 + k;
+  };
 
   u64 x[E];
-  constexpr int NG = (LOGM + RB - 1) / RB;
+  int b, nst, hb0, base;
+  pass_shape<LOGM, INV>(0, tp, b, nst, hb0, base);
+  if (!COL && b == 0) {  // 8 consecutive words per thread: 16-byte loads
+    const ulonglong2* srcv = reinterpret_cast<const ulonglong2*>(in + gaddr(base));
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      const ulonglong2 v = srcv[e / 2];
+      x[e] = v.x;
+      x[e + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = in[gaddr(base | (e << b))];
+  }
+
 #pragma unroll
   for (int gi = 0; gi < NG; ++gi) {
-    int b, nst, hb0;
-    if (!INV) {
-      const int top = LOGM - 1 - RB * gi;
-      nst = top + 1 < RB ? top + 1 : RB;
-      b = top - (RB - 1) > 0 ? top - (RB - 1) : 0;
-      hb0 = top;
-    } else {
-      const int low = RB * gi;
-      nst = LOGM - low < RB ? LOGM - low : RB;
-      b = low < LOGM - RB ? low : LOGM - RB;
-      hb0 = low;
+    if (gi > 0) {  // re-layout through shared memory
+      int pb, pn, ph, pbase;
+      pass_shape<LOGM, INV>(gi - 1, tp, pb, pn, ph, pbase);
+#pragma unroll
+      for (int e = 0; e < E; ++e) lsm[pad8(pbase | (e << pb))] = x[e];
+      if (COL) __syncthreads();
+      else __syncwarp();
+      pass_shape<LOGM, INV>(gi, tp, b, nst, hb0, base);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = lsm[pad8(base | (e << b))];
     }
-    const int lowmask = (1 << b) - 1;
-    const int baseidx = ((t >> b) << (b + RB)) | (t & lowmask);
 #pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = lsm[pad8(baseidx | (e << b))];
-#pragma unroll
-    for (int st = 0; st < RB; ++st) {
+    for (int st = 0; st < 3; ++st) {
       if (st < nst) {
         const int hb = INV ? hb0 + st : hb0 - st;
         const int eb = hb - b;
@@ -136,7 +146,7 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, RB>::THREADS)
         for (int j = 0; j < E / 2; ++j) {
           if (j < (E >> (eb + 1))) {
             // twiddle of the butterflies whose e-bits above eb equal j
-            const int idx = baseidx | ((j << (eb + 1)) << b);
+            const int idx = base | ((j << (eb + 1)) << b);
             const int sj = idx >> (hb + 1);
             const ulonglong2 wv =
                 __ldg(twp + (COL ? (1 << s) + sj : (1 << (n1 + s)) + ((line0 + li) << s) + sj));
@@ -161,75 +171,46 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, RB>::THREADS)
         }
       }
     }
-#pragma unroll
-    for (int e = 0; e < E; ++e) lsm[pad8(baseidx | (e << b))] = x[e];
-    __syncwarp();
   }
-  __syncthreads();
 
-  // ---- store tile
-  for (int xi = threadIdx.x; xi < LPC * M / 2; xi += blockDim.x) {
-    int line, k;
-    std::size_t g;
-    u64 v0, v1;
-    if (COL) {
-      k = xi / (LPC / 2);
-      line = 2 * (xi - k * (LPC / 2));
-      g = (std::size_t)k * N2 + line0 + line;
-      v0 = sm[line * LS + pad8(k)];
-      v1 = sm[(line + 1) * LS + pad8(k)];
-    } else {
-      line = xi / (M / 2);
-      k = 2 * (xi - line * (M / 2));
-      g = (std::size_t)(line0 + line) * N2 + k;
-      v0 = sm[line * LS + pad8(k)];
-      v1 = sm[line * LS + pad8(k + 1)];
-    }
+  // ---- store the last pass's layout straight to global memory
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    u64 v = x[e];
     if (!FIRST) {
       if (INV) {
-        v0 = csub(shoup_lazy(v0, P.ninv, P.ninv_sh, q), q);  // [0, 2q) -> canonical
-        v1 = csub(shoup_lazy(v1, P.ninv, P.ninv_sh, q), q);
+        v = csub(shoup_lazy(v, P.ninv, P.ninv_sh, q), q);  // [0, 2q) -> canonical
       } else {
-        v0 = v0 >= q2 ? v0 - q2 : v0;  // [0, 4q) -> canonical
-        v1 = v1 >= q2 ? v1 - q2 : v1;
-        v0 = csub(v0, q);
-        v1 = csub(v1, q);
+        v = v >= q2 ? v - q2 : v;  // [0, 4q) -> canonical
+        v = csub(v, q);
       }
     }
-    *reinterpret_cast<ulonglong2*>(data + g) = make_ulonglong2(v0, v1);
+    x[e] = v;
   }
-}
-
-template <int LOGM, bool INV, bool COL, int RB>
-void launch_phase_t(const DevTables& t, const LimbSet& set, const LimbSet* src, cudaStream_t st) {
-  using G = Geometry<LOGM, COL, RB>;
-  const std::size_t smem = (std::size_t)G::LPC * G::LS * sizeof(u64);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(ntt_phase_kernel<LOGM, INV, COL, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr_set = true;
+  if (!COL && b == 0) {  // 8 consecutive words per thread: 16-byte stores
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(data + gaddr(base));
+#pragma unroll
+    for (int e = 0; e < E; e += 2) dst[e / 2] = make_ulonglong2(x[e], x[e + 1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) data[gaddr(base | (e << b))] = x[e];
   }
-  const int lines = COL ? (1 << t.n2) : (1 << t.n1);
-  dim3 grid(lines / G::LPC, set.count());
-  ntt_phase_kernel<LOGM, INV, COL, RB><<<grid, G::THREADS, smem, st>>>(set, src ? *src : set, src != nullptr, t.pc,
-                                                                       t.tw, t.logN, t.n1, t.n2);
-  launch_check("ntt_phase_kernel");
-}
-
-int radix_bits() {
-  static int rb = [] {
-    const char* e = std::getenv("FHEON_NTT_RB");
-    const int v = e ? std::atoi(e) : 3;
-    return (v == 4) ? 4 : 3;
-  }();
-  return rb;
 }
 
 template <int LOGM, bool INV, bool COL>
 void launch_phase(const DevTables& t, const LimbSet& set, const LimbSet* src, cudaStream_t st) {
-  if (radix_bits() == 4 && LOGM >= 6) launch_phase_t<LOGM, INV, COL, 4>(t, set, src, st);
-  else launch_phase_t<LOGM, INV, COL, 3>(t, set, src, st);
+  using G = Geometry<LOGM, COL>;
+  const std::size_t smem = (std::size_t)G::LPC * G::LS * sizeof(u64);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(ntt_phase_kernel<LOGM, INV, COL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  const int lines = COL ? (1 << t.n2) : (1 << t.n1);
+  dim3 grid(lines / G::LPC, set.count());
+  ntt_phase_kernel<LOGM, INV, COL><<<grid, G::THREADS, smem, st>>>(set, src ? *src : set, src != nullptr, t.pc, t.tw,
+                                                                    t.logN, t.n1, t.n2);
+  launch_check("ntt_phase_kernel");
 }
 
 template <bool INV, bool COL>
