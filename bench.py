@@ -15,6 +15,11 @@ full ModUp -> key inner product (automorphism fused) -> ModDown per rotation.
          download, every step
   roofline  the key-switch inner-product kernel (HBM-bound: streams the key)
          timed live with CUDA events inside the timed region
+  roofline_ntt  the NTT phases (the largest share of the step; integer-pipe
+         bound): butterflies/s against the measured lazy-Shoup butterfly peak
+  models  encrypted LeNet-5 / ResNet-20 s/image through the model runtime
+         (fast schedule, plus the reference's exact rotation schedule), with
+         the decrypted logits compared against the reference's infer()
   cpu_baseline  the repo's CPU RNS-CKKS oracle (oracle/ckks_oracle.c, OpenMP)
          doing the same rotations on the host cores
 
@@ -161,6 +166,12 @@ def run_ours(args):
         step()
     barrier()
     st0 = ctx.stats()
+    # FHEON_PROFILE_RANGE=1: limit an `ncu --profile-from-start off` capture to the timed steps
+    prof = None
+    if os.environ.get("FHEON_PROFILE_RANGE"):
+        import ctypes
+        prof = ctypes.CDLL("libcudart.so.12")
+        prof.cudaProfilerStart()
     ctx.timer_arm(1)  # key-switch inner product, timed live in the region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -173,12 +184,43 @@ def run_ours(args):
         e1.record(stream)
         e1.synchronize()
     ms = e0.elapsed_time(e1)
+    if prof is not None:
+        prof.cudaProfilerStop()
     ks_ms, ks_n = ctx.timer_read()
     ctx.timer_arm(0)
     st1 = ctx.stats()
     del keep
     barrier()
     value, ms_max = replicas.replica_throughput(ms, args.steps * B, torch.device("cuda", local))
+
+    # ---- the NTT's share and integer roofline inside the same step (second
+    # pass of K steps with the NTT class timed live; every limb-NTT is
+    # (N/2) log2 N lazy Shoup butterflies)
+    n0 = ctx.stats()["ntt_limbs"]
+    ctx.timer_arm(2)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        keep = step()
+    f1.record(stream)
+    f1.synchronize()
+    ms_ntt_pass = f0.elapsed_time(f1)
+    ntt_ms, ntt_n = ctx.timer_read()
+    ctx.timer_arm(0)
+    del keep
+    ntt_limbs = ctx.stats()["ntt_limbs"] - n0
+    bfly = ntt_limbs * (N // 2) * LOGN
+    try:
+        bpeak = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))["shoup_ct_butterflies_per_s"]
+        bsrc = "measured (profiles/int_peak.json: lazy Shoup butterfly, IMAD.WIDE-bound)"
+    except Exception:
+        bpeak, bsrc = 8.7e11, "fallback"
+    ntt_rate = bfly / (ntt_ms / 1e3)
+    roofline_ntt = {"kernel": "ntt_phase_kernel (COL + ROW phases, forward and inverse)", "bound": "int",
+                    "achieved": round(ntt_rate / 1e9, 1), "peak": round(bpeak / 1e9, 1), "unit": "Gbutterfly/s",
+                    "frac": round(ntt_rate / bpeak, 4), "peak_source": bsrc, "limb_ntts_per_step":
+                    ntt_limbs // max(1, args.steps), "share_of_step": round(ntt_ms / ms_ntt_pass, 4),
+                    "hbm_gbs": round(ntt_limbs * N * 8 * 4 / (ntt_ms / 1e3) / 1e9, 1)}
 
     # ---- roofline of the key-switch inner product (per launch: one rotation)
     E = L + K
@@ -247,6 +289,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_rotation": per_rot, "avg_launch_ms": round(ks_avg_ms, 5),
                      "launches_timed": ks_n,
                      "share_of_step": round(ks_ms / ms, 4)},
+        "roofline_ntt": roofline_ntt,
         "clocks": clk.summary(),
     }
     if extras:
@@ -338,7 +381,7 @@ def model_runs(args):
         for _ in range(args.model_reps):
             r = em.infer(x)
             times.append(r.wall_ms / 1e3)
-        rec = {"s_per_image": round(float(np.median(times)), 4), "reps": args.model_reps,
+        rec = {"s_per_image": round(float(np.median(times)), 4), "reps": args.model_reps, "schedule": "fast",
                "ring_dimension": spec.ring_dimension, "depth_budget": spec.depth_budget,
                "limbs": em.ctx.L, "bootstraps": em.n_boot, "rotations": r.stats["rotations"],
                "keyswitches": r.stats["keyswitches"], "gpu_launches": r.stats["launches"],
@@ -349,8 +392,18 @@ def model_runs(args):
             rec["max_abs_logit_err_vs_reference"] = float(np.abs(r.logits - rl).max())
             rec["argmax_match"] = bool(int(np.argmax(r.logits)) == int(np.argmax(rl)))
             rec["reference_sim_s_per_image_1core"] = round(rwall / 1e3, 4)
-        out[name] = rec
         del em
+        if not args.no_reference_schedule:
+            # the reference's exact rotation sequence (trace-identical), same engine
+            em = M.EncryptedModel(spec, schedule="reference")
+            em.infer(x)
+            r2 = em.infer(x)
+            rec["reference_schedule"] = {"s_per_image": round(r2.wall_ms / 1e3, 4), "rotations": r2.stats["rotations"],
+                                         "keyswitches": r2.stats["keyswitches"]}
+            if have_ref:
+                rec["reference_schedule"]["max_abs_logit_err_vs_reference"] = float(np.abs(r2.logits - rl).max())
+            del em
+        out[name] = rec
     return out
 
 
@@ -443,6 +496,8 @@ def main():
     ap.add_argument("--no-models", action="store_true", help="skip LeNet-5 / ResNet-20 s/image")
     ap.add_argument("--no-resnet", action="store_true", help="skip ResNet-20 s/image")
     ap.add_argument("--model-reps", type=int, default=2)
+    ap.add_argument("--no-reference-schedule", action="store_true",
+                    help="skip the models' reference-rotation-schedule timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfheon_b200.so")
+# FHEON_LIB_OVERRIDE: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("FHEON_LIB_OVERRIDE") or os.path.join(_HERE, "_lib", "libfheon_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "fheon_b200.h")
 
 _lib = None

@@ -37,6 +37,13 @@ namespace fheon {
 
 namespace {
 
+#ifndef FHEON_NTT_COL_LINES
+#define FHEON_NTT_COL_LINES 16
+#endif
+#ifndef FHEON_NTT_ROW_THREADS
+#define FHEON_NTT_ROW_THREADS 256
+#endif
+
 __device__ __forceinline__ int pad8(int k) { return k + (k >> 3); }
 
 // r = a * w mod q in [0, 2q) for any a < 2^64 (Shoup, no final correction)
@@ -47,8 +54,8 @@ struct Geometry {
   static constexpr int M = 1 << LOGM;
   static constexpr int E = 8;        // elements per thread
   static constexpr int T = M / E;    // threads per line
-  static constexpr int ROWL = (256 / T) < 32 ? (256 / T) : 32;
-  static constexpr int LPC = COL ? 16 : ROWL;  // lines per CTA
+  static constexpr int ROWL = (FHEON_NTT_ROW_THREADS / T) < 32 ? (FHEON_NTT_ROW_THREADS / T) : 32;
+  static constexpr int LPC = COL ? FHEON_NTT_COL_LINES : ROWL;  // lines per CTA
   static constexpr int THREADS = LPC * T;
   static constexpr int LS = M + M / 8 + 1;  // padded line stride (words)
   static constexpr int NG = (LOGM + 2) / 3;  // register passes
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL>::THREADS)
     ntt_phase_kernel(LimbSet set, LimbSet src, bool has_src, const PrimeConst* __restrict__ pc,
                      const u64* __restrict__ tw, int logN, int n1, int n2) {
   using G = Geometry<LOGM, COL>;
-  constexpr int M = G::M, E = G::E, T = G::T, LPC = G::LPC, LS = G::LS, NG = G::NG;
+  constexpr int E = G::E, T = G::T, LPC = G::LPC, LS = G::LS, NG = G::NG;
   // the phase that runs first (forward COL / inverse ROW) reads canonical input and
   // leaves lazy values; the second phase reduces to canonical.
   constexpr bool FIRST = (COL != INV);
