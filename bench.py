@@ -368,13 +368,18 @@ def model_runs(args):
         return (x - 0.5) / 0.2887
 
     out = {}
-    cases = [("lenet5", M.lenet5(ring=32768, depth_budget=12), np.random.default_rng(3001).uniform(0, 1, (1, 28, 28)))]
+    # depth 25 = the reference's own presets (backend.cpp:61-76, models/*.json); depth 12 = a shorter
+    # chain (fewer limbs per op, one more bootstrap in ResNet-20)
+    xl = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
+    cases = [("lenet5", M.lenet5(ring=32768, depth_budget=25), xl, False),
+             ("lenet5_depth12", M.lenet5(ring=32768, depth_budget=12), xl, True)]
     if not args.no_resnet:
-        spec = M.resnet20(ring=65536, depth_budget=12)
         cal = [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
-        cases.append(("resnet20", M.calibrate_relu_scales(spec, cal),
-                      norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))))
-    for name, spec, x in cases:
+        xr = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
+        cases.append(("resnet20", M.calibrate_relu_scales(M.resnet20(ring=65536, depth_budget=25), cal), xr, False))
+        cases.append(("resnet20_depth12", M.calibrate_relu_scales(M.resnet20(ring=65536, depth_budget=12), cal), xr,
+                      True))
+    for name, spec, x, with_ref_schedule in cases:
         em = M.EncryptedModel(spec)
         em.infer(x)  # warm-up: lazy key generation, plaintext caches
         times = []
@@ -393,7 +398,7 @@ def model_runs(args):
             rec["argmax_match"] = bool(int(np.argmax(r.logits)) == int(np.argmax(rl)))
             rec["reference_sim_s_per_image_1core"] = round(rwall / 1e3, 4)
         del em
-        if not args.no_reference_schedule:
+        if with_ref_schedule and not args.no_reference_schedule:
             # the reference's exact rotation sequence (trace-identical), same engine
             em = M.EncryptedModel(spec, schedule="reference")
             em.infer(x)

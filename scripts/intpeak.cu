@@ -109,6 +109,47 @@ __global__ void k_butterfly_approx(u64* out, u64 q, u64 w, u64 wsh, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// 3-product high word (drops lo x lo: result in {hi - 1, hi}), PTX carry chains
+__device__ __forceinline__ u64 mulhi3(u64 a, u64 b) {
+  const unsigned alo = (unsigned)a, ahi = (unsigned)(a >> 32), blo = (unsigned)b, bhi = (unsigned)(b >> 32);
+  unsigned rlo, rhi;
+  asm("{\n\t"
+      ".reg .u32 m0, m1, c;\n\t"
+      "mul.lo.u32 m0, %2, %5;\n\t"
+      "mul.hi.u32 m1, %2, %5;\n\t"
+      "mad.lo.cc.u32 m0, %3, %4, m0;\n\t"
+      "madc.hi.cc.u32 m1, %3, %4, m1;\n\t"
+      "addc.u32 c, 0, 0;\n\t"
+      "mad.lo.cc.u32 %0, %3, %5, m1;\n\t"
+      "madc.hi.u32 %1, %3, %5, c;\n\t"
+      "}"
+      : "=r"(rlo), "=r"(rhi)
+      : "r"(alo), "r"(ahi), "r"(blo), "r"(bhi));
+  return ((u64)rhi << 32) | rlo;
+}
+
+// lazy CT butterfly on [0, 8q) with the 3-product quotient (T in [0, 3q))
+__global__ void k_butterfly3(u64* out, u64 q, u64 w, u64 wsh, int iters) {
+  u64 x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = (threadIdx.x * 8 + i) % q;
+  const u64 q3 = 3 * q, q4 = 4 * q;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      u64 X = x[i];
+      X = X >= q4 ? X - q4 : X;
+      const u64 T = x[i + 1] * w - mulhi3(x[i + 1], wsh) * q;
+      x[i] = X + T;
+      x[i + 1] = X - T + q3;
+    }
+  }
+  u64 s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   cudaGetDevice(&dev);
@@ -162,6 +203,15 @@ int main() {
   const double bfa = thr * iters * 4 / (ms * 1e-3);
   printf("{\"approx_butterflies_per_s\": %.4e, \"approx_butterflies_per_clk_per_sm\": %.3f}\n", bfa,
          bfa / sms / (clk * 1e3));
+  k_butterfly3<<<blocks, threads>>>(out, 1152921504606846883ULL, 0x123456789ULL, 0xABCDEF12345ULL, 16);
+  cudaEventRecord(e0);
+  k_butterfly3<<<blocks, threads>>>(out, 1152921504606846883ULL, 0x123456789ULL, 0xABCDEF12345ULL, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double bf3 = thr * iters * 4 / (ms * 1e-3);
+  printf("{\"ptx3_butterflies_per_s\": %.4e, \"ptx3_butterflies_per_clk_per_sm\": %.3f}\n", bf3,
+         bf3 / sms / (clk * 1e3));
   printf("{\"sms\": %d, \"clock_khz\": %d, \"imad_per_s\": %.4e, \"imad_wide_u32_per_s\": %.4e, "
          "\"shoup_ct_butterflies_per_s\": %.4e, \"imad_per_clk_per_sm\": %.2f, \"imad_wide_per_clk_per_sm\": %.2f, "
          "\"butterflies_per_clk_per_sm\": %.3f}\n",

@@ -61,6 +61,19 @@ def test_resnet20_full_ring_with_bootstrapping(schedule):
     _compare(spec, x, schedule)
 
 
+def test_resnet20_reference_preset_depth25():
+    """ResNet-20 at the reference's own preset depth budget (25, backend.cpp:61-76) on the
+    BASELINE ring N = 2^16: 18 bootstraps, fast schedule."""
+    def norm(x):
+        return (x - 0.5) / 0.2887
+
+    spec = M.resnet20(ring=65536, depth_budget=25)
+    cal = [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
+    spec = M.calibrate_relu_scales(spec, cal)
+    x = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
+    _compare(spec, x, "fast")
+
+
 def test_lenet5_no_bootstrap_deep_budget():
     """Depth budget deep enough that the ledger needs no bootstrap except the
     standard placements (policy auto)."""
