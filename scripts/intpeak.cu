@@ -150,6 +150,49 @@ __global__ void k_butterfly3(u64* out, u64 q, u64 w, u64 wsh, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_dfma(double* out, double seed, int iters) {
+  double a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = seed + threadIdx.x * 16 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = fma(a[i], 0.999999, 1e-7);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// FP64 lazy CT butterfly for q < 2^50: values are exact integers in doubles,
+// a*w mod q via hi = fl(a w), lo = fma(a, w, -hi) (exact), quotient = rint(hi / q)
+// (magic-number rounding), r = fma(-quot, q, hi) + lo in (-q, q)
+__global__ void k_butterfly_f64(double* out, double q, double w, int iters) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = (double)((threadIdx.x * 8 + i) % 1000003);
+  const double qinv = 1.0 / q, magic = 6755399441055744.0, q2 = 2 * q;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      double X = x[i];
+      X = X >= q2 ? X - q2 : X;
+      const double y = x[i + 1];
+      const double hi = y * w;
+      const double lo = fma(y, w, -hi);
+      const double qt = fma(hi, qinv, magic) - magic;
+      double T = fma(-qt, q, hi) + lo;
+      T = T < 0 ? T + q : T;
+      x[i] = X + T;
+      x[i + 1] = X - T + q;
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   cudaGetDevice(&dev);
@@ -210,6 +253,22 @@ int main() {
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
   const double bf3 = thr * iters * 4 / (ms * 1e-3);
+  k_dfma<<<blocks, threads>>>((double*)out, 1.0, 16);
+  cudaEventRecord(e0);
+  k_dfma<<<blocks, threads>>>((double*)out, 1.0, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double dfma = thr * iters * 16 / (ms * 1e-3);
+  k_butterfly_f64<<<blocks, threads>>>((double*)out, 1099511627689.0, 123456789.0, 16);
+  cudaEventRecord(e0);
+  k_butterfly_f64<<<blocks, threads>>>((double*)out, 1099511627689.0, 123456789.0, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double bff = thr * iters * 4 / (ms * 1e-3);
+  printf("{\"dfma_per_clk_per_sm\": %.2f, \"f64_butterflies_per_s\": %.4e, \"f64_butterflies_per_clk_per_sm\": %.3f}\n",
+         dfma / sms / (clk * 1e3), bff, bff / sms / (clk * 1e3));
   printf("{\"ptx3_butterflies_per_s\": %.4e, \"ptx3_butterflies_per_clk_per_sm\": %.3f}\n", bf3,
          bf3 / sms / (clk * 1e3));
   printf("{\"sms\": %d, \"clock_khz\": %d, \"imad_per_s\": %.4e, \"imad_wide_u32_per_s\": %.4e, "
