@@ -381,12 +381,14 @@ def model_runs(args):
                       True))
     for name, spec, x, with_ref_schedule in cases:
         em = M.EncryptedModel(spec)
-        em.infer(x)  # warm-up: lazy key generation, plaintext caches
+        em.infer(x)  # warm-up x2: lazy key generation, plaintext caches, pool growth
+        em.infer(x)
         times = []
         for _ in range(args.model_reps):
             r = em.infer(x)
             times.append(r.wall_ms / 1e3)
         rec = {"s_per_image": round(float(np.median(times)), 4), "reps": args.model_reps, "schedule": "fast",
+               "rep_times_s": [round(t, 4) for t in times],
                "ring_dimension": spec.ring_dimension, "depth_budget": spec.depth_budget,
                "limbs": em.ctx.L, "bootstraps": em.n_boot, "rotations": r.stats["rotations"],
                "keyswitches": r.stats["keyswitches"], "gpu_launches": r.stats["launches"],
@@ -500,7 +502,7 @@ def main():
     ap.add_argument("--quick", action="store_true", help="skip the primitive breakdown and the models")
     ap.add_argument("--no-models", action="store_true", help="skip LeNet-5 / ResNet-20 s/image")
     ap.add_argument("--no-resnet", action="store_true", help="skip ResNet-20 s/image")
-    ap.add_argument("--model-reps", type=int, default=2)
+    ap.add_argument("--model-reps", type=int, default=3)
     ap.add_argument("--no-reference-schedule", action="store_true",
                     help="skip the models' reference-rotation-schedule timing")
     args = ap.parse_args()

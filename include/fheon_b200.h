@@ -74,7 +74,7 @@ int fheon_ctx_info(const fheon_ctx* ctx, uint64_t* primes, double* scales, int* 
 void* fheon_ctx_stream(fheon_ctx* ctx); /* cudaStream_t */
 int fheon_ctx_sync(fheon_ctx* ctx);
 /* op counters: rotations, keyswitches, mult_plain, mult_cipher, rescales, ntt_limbs, encodes, adds,
- * kernel launches (process-wide) */
+ * kernel launches (all contexts of the process) since this context's last reset */
 int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* out9);
 int fheon_ctx_reset_stats(fheon_ctx* ctx);
 /* live kernel timing with CUDA events on the context stream: arm a class

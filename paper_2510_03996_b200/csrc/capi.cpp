@@ -157,11 +157,14 @@ int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* o) {
     o[5] = s.ntt_limbs;
     o[6] = s.encodes;
     o[7] = s.adds;
-    o[8] = fheon::g_kernel_launches.load();
+    o[8] = fheon::g_kernel_launches.load() - s.launches;  // kernels launched since the last reset
   });
 }
 int fheon_ctx_reset_stats(fheon_ctx* ctx) {
-  return guard([&] { ctx->impl->stats = fheon::OpStats{}; });
+  return guard([&] {
+    ctx->impl->stats = fheon::OpStats{};
+    ctx->impl->stats.launches = fheon::g_kernel_launches.load();  // baseline
+  });
 }
 int fheon_timer_arm(fheon_ctx* ctx, int kernel_class) {
   return guard([&] {

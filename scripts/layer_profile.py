@@ -13,7 +13,8 @@ import paper_2510_03996_b200 as fh
 from paper_2510_03996_b200 import model as M
 
 which = sys.argv[1] if len(sys.argv) > 1 else "conv2"
-spec = M.resnet20(ring=65536, depth_budget=12)
+depth = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+spec = M.resnet20(ring=65536, depth_budget=depth)
 ctx = fh.SlotContext(M.ckks_config(spec, True))
 rng = np.random.default_rng(5)
 cudart = ctypes.CDLL("libcudart.so.12")

@@ -18,9 +18,11 @@ for r in rows:
         continue
     name = d["Kernel Name"]
     name = re.sub(r"\(.*", "", name)
-    m = re.search(r"ntt_phase_kernel<(\d+), (\w+), (\w+)", d["Kernel Name"])
+    m = re.search(r"ntt_phase_kernel<(\d+), \(?\w*\)?(\w+), \(?\w*\)?(\w+)", d["Kernel Name"])
     if m:
-        name = f"ntt<{m.group(1)},{'inv' if m.group(2) == 'true' else 'fwd'},{'col' if m.group(3) == 'true' else 'row'}>"
+        inv = m.group(2) in ("true", "1")
+        col = m.group(3) in ("true", "1")
+        name = f"ntt<{m.group(1)},{'inv' if inv else 'fwd'},{'col' if col else 'row'}>"
     v = float(d["Metric Value"].replace(",", ""))
     unit = d.get("Metric Unit", "ns")
     v = v / 1000.0 if unit == "ns" else (v * 1000.0 if unit == "ms" else v)  # -> us

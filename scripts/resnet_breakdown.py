@@ -9,6 +9,7 @@ import numpy as np
 from paper_2510_03996_b200 import model as M
 
 which = sys.argv[1] if len(sys.argv) > 1 else "resnet20"
+depth = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 
 
 def norm(x):
@@ -16,12 +17,12 @@ def norm(x):
 
 
 if which == "resnet20":
-    spec = M.resnet20(ring=65536, depth_budget=12)
+    spec = M.resnet20(ring=65536, depth_budget=depth)
     spec = M.calibrate_relu_scales(spec, [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32)))
                                           for i in range(6)])
     x = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
 else:
-    spec = M.lenet5(ring=32768, depth_budget=12)
+    spec = M.lenet5(ring=32768, depth_budget=depth)
     x = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
 em = M.EncryptedModel(spec)
 em.infer(x)
