@@ -1040,6 +1040,11 @@ std::vector<Ciphertext> cheb_eval_ps_many(Context& ctx, const std::vector<Cipher
   const int D = (int)coeffs.size() - 1;
   if (D < 2 || xs.empty()) return {};
   const int want = cheb_eval_depth(D);
+  for (const Ciphertext& x : xs)
+    if (x.level() < want)  // the T_d tree would exhaust the chain mid-way (chebyshev.cpp:62-104)
+      throw Error(ErrKind::depth_exhausted, "cheb_eval: degree " + std::to_string(D) + " needs " +
+                                                std::to_string(want) + " levels, operand is at level " +
+                                                std::to_string(x.level()));
   int best_lk = -1, best_m = 0, best_mults = 1 << 30;
   std::unique_ptr<PsNode> best;
   for (int lk = 1; lk <= 5; ++lk) {
