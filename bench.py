@@ -373,9 +373,19 @@ def model_runs(args):
     xl = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
     cases = [("lenet5", M.lenet5(ring=32768, depth_budget=25), xl, False),
              ("lenet5_depth12", M.lenet5(ring=32768, depth_budget=12), xl, True)]
+    # the reference's own model files (proj/models/*.json, presets "lenet5" N=2^14 and "large"
+    # N=2^15, depth 25 -- the paper's ResNet-20 setting), seeded CSV weights, calibrated ReLU scales
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from model_files import materialize
+    refspec = M.load_spec(materialize("lenet5", tempfile.mkdtemp(), seed=9))
+    refspec = M.calibrate_relu_scales(refspec, [np.random.default_rng(500 + i).uniform(0, 1, (1, 28, 28))
+                                                for i in range(4)])
+    cases.append(("lenet5_reference_spec", refspec, np.random.default_rng(501).uniform(0, 1, (1, 28, 28)), False))
     if not args.no_resnet:
         cal = [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
         xr = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
+        refspec = M.calibrate_relu_scales(M.load_spec(materialize("resnet20", tempfile.mkdtemp(), seed=9)), cal)
+        cases.append(("resnet20_reference_spec", refspec, xr, False))
         cases.append(("resnet20", M.calibrate_relu_scales(M.resnet20(ring=65536, depth_budget=25), cal), xr, False))
         cases.append(("resnet20_depth12", M.calibrate_relu_scales(M.resnet20(ring=65536, depth_budget=12), cal), xr,
                       True))
@@ -389,6 +399,8 @@ def model_runs(args):
             times.append(r.wall_ms / 1e3)
         rec = {"s_per_image": round(float(np.median(times)), 4), "reps": args.model_reps, "schedule": "fast",
                "rep_times_s": [round(t, 4) for t in times],
+               "spec": ("the reference's models/%s.json (preset, seeded weights)" % name.split("_")[0]
+                        if name.endswith("reference_spec") else "paper_2510_03996_b200.model." + name.split("_")[0]),
                "ring_dimension": spec.ring_dimension, "depth_budget": spec.depth_budget,
                "limbs": em.ctx.L, "bootstraps": em.n_boot, "rotations": r.stats["rotations"],
                "keyswitches": r.stats["keyswitches"], "gpu_launches": r.stats["launches"],

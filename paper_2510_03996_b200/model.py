@@ -85,6 +85,235 @@ class ModelSpec:
         return path
 
 
+# ----------------------------------------------------------------- spec files
+_PRESETS = {"lenet5": (16384, 8192, 25), "large": (32768, 16384, 25)}  # backend.cpp:61-76
+
+
+def _fail(msg: str):
+    raise fh.ModelError(msg, 2)
+
+
+def _size(j: Dict, key: str, where: str, default=None) -> int:
+    if key not in j:
+        if default is None:
+            _fail(f'{where}: missing required field "{key}"')
+        return default
+    v = j[key]
+    if isinstance(v, bool) or not isinstance(v, int) or v < 0:
+        _fail(f'{where}: field "{key}" must be a non-negative integer')
+    return v
+
+
+def _csv_values(path: str, expected: int, what: str) -> np.ndarray:
+    """load_csv_values (model_spec.cpp:293-337): comma/newline separated numbers,
+    blank cells skipped, exact count required."""
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        _fail(f"{what}: cannot open {path}")
+    out = []
+    for row, line in enumerate(text.splitlines(), start=1):
+        for col, tok in enumerate(line.split(","), start=1):
+            tok = tok.strip()
+            if not tok:
+                continue
+            try:
+                out.append(float(tok))
+            except ValueError:
+                _fail(f'{what}: {path} row {row} column {col}: cannot parse "{tok}" as a number')
+    if len(out) != expected:
+        _fail(f"{what}: {path}: expected {expected} values, found {len(out)}")
+    return np.array(out, np.float64)
+
+
+def _parse_layer(j, index: int, scope: str) -> Layer:
+    """parse_layer (model_spec.cpp:133-207)."""
+    where = f"{scope}layers[{index}]"
+    if not isinstance(j, dict) or not isinstance(j.get("type"), str):
+        _fail(f'{where}: every layer needs a string "type"')
+    t = j["type"]
+    name = j.get("name", f"{t}_{index}")
+    p: Dict = {}
+    if t == "conv":
+        p["out_channels"] = _size(j, "out_channels", where)
+        p["kernel"] = _size(j, "kernel", where)
+        p["stride"] = _size(j, "stride", where, 1)
+        p["padding"] = _size(j, "padding", where, 0)
+        mode = j.get("mode", "generic")
+        if mode not in ("generic", "special3x3", "grouped"):
+            _fail(f'{where}: mode must be "generic", "special3x3" or "grouped", got "{mode}"')
+        p["mode"] = mode
+    elif t == "avg_pool":
+        p["kernel"] = _size(j, "kernel", where, 2)
+        p["stride"] = _size(j, "stride", where, 2)
+    elif t == "whole_channel_pool":
+        p["kernel"] = _size(j, "kernel", where)
+    elif t == "fc":
+        p["outputs"] = _size(j, "outputs", where)
+        p["inputs"] = _size(j, "inputs", where, 0)
+        p["merge_budget"] = _size(j, "merge_budget", where, 1)
+    elif t == "relu":
+        if "degree" in j:
+            p["degree"] = int(j["degree"])
+        if "scale" in j:
+            p["scale"] = float(j["scale"])
+    elif t == "batchnorm":
+        for key in ("gamma", "beta", "mean", "var"):
+            if key not in j:
+                _fail(f'{where}: batchnorm needs field "{key}"')
+            v = j[key]
+            if not isinstance(v, (list, str)):
+                _fail(f'{where}: "{key}" must be an array of numbers or a CSV file name')
+            p[key] = v
+        p["epsilon"] = float(j.get("epsilon", 1e-5))
+    elif t in ("global_avg_pool", "bootstrap"):
+        pass
+    elif t == "residual":
+        if "layers" not in j:
+            _fail(f'{where}: residual units need a nested "layers" array')
+        L = Layer(t, name, p, body=_parse_list(j["layers"], where + "."))
+        if "downsample" in j:
+            d = _parse_layer(j["downsample"], 0, where + ".downsample.")
+            if d.type != "conv":
+                _fail(f'{where}: "downsample" must be a conv layer')
+            L.downsample = [d]
+        return L
+    else:
+        _fail(f'{where}: unknown layer type "{t}"')
+    if t in ("conv", "avg_pool"):
+        sv = j.get("stride_variant", "extract")
+        if sv not in ("extract", "masked"):
+            _fail(f'{where}: stride_variant must be "extract" or "masked", got "{sv}"')
+        p["stride_variant"] = sv
+    if t in ("conv", "fc"):
+        p["weights_file"] = j.get("weights", "")
+        p["bias_file"] = j.get("bias", "")
+    return Layer(t, name, p)
+
+
+def _parse_list(j, scope: str) -> List[Layer]:
+    if not isinstance(j, list) or not j:
+        _fail(f'{scope}: "layers" must be a non-empty array')
+    return [_parse_layer(e, i, scope) for i, e in enumerate(j)]
+
+
+def _resolve_file(base: str, f: str) -> str:
+    return f if os.path.isabs(f) else os.path.join(base, f)
+
+
+def _load_weights(layers: List[Layer], shape, base: str) -> Tuple[List[Layer], Tuple]:
+    """Read every conv / fc weight file with the flow's input sizes and fold
+    batchnorm into the convolution before it (model_spec.cpp:349-406, :643-684)."""
+    out: List[Layer] = []
+    folded = set()
+    for L in layers:
+        packed, C, W, n = shape
+        if L.type == "conv":
+            p = L.params
+            F, k, S, P = p["out_channels"], p["kernel"], p["stride"], p["padding"]
+            wc = 1 if p["mode"] == "grouped" else C
+            if not p.get("weights_file"):
+                _fail(f"layer '{L.name}': no weights file given")
+            L.weights = _csv_values(_resolve_file(base, p.pop("weights_file")), F * wc * k * k,
+                                    f"layer '{L.name}' weights").reshape(F, wc, k, k)
+            bf = p.pop("bias_file", "")
+            L.bias = _csv_values(_resolve_file(base, bf), F, f"layer '{L.name}' bias") if bf else None
+            if k == 0 or S == 0 or F == 0:
+                _fail(f"layer '{L.name}': out_channels, kernel and stride must be positive")
+            Wo = (W + 2 * P - k) // S + 1 if W + 2 * P >= k else 0
+            shape = (True, F, Wo, 0)
+        elif L.type == "batchnorm":
+            if not out or out[-1].type != "conv":
+                _fail(f"layer '{L.name}': batchnorm must directly follow a convolution")
+            conv = out[-1]
+            if conv.name in folded:
+                _fail(f"layer '{L.name}': convolution '{conv.name}' already has batchnorm folded in")
+            F = conv.params["out_channels"]
+            vec = {}
+            for key in ("gamma", "beta", "mean", "var"):
+                v = L.params[key]
+                vec[key] = (_csv_values(_resolve_file(base, v), F, f"layer '{L.name}' {key}") if isinstance(v, str)
+                            else np.asarray(v, np.float64))
+                if vec[key].size != F:
+                    _fail(f"layer '{L.name}' {key}: expected {F} values, found {vec[key].size}")
+            eps = L.params["epsilon"]
+            if not np.all(vec["var"] + eps > 0):
+                _fail(f"layer '{L.name}': variance + epsilon must be positive")
+            sc = vec["gamma"] / np.sqrt(vec["var"] + eps)
+            conv.weights = conv.weights * sc[:, None, None, None]
+            b = conv.bias if conv.bias is not None else np.zeros(F)
+            conv.bias = sc * (b - vec["mean"]) + vec["beta"]
+            folded.add(conv.name)
+            continue
+        elif L.type == "avg_pool":
+            k, S = L.params["kernel"], L.params["stride"]
+            shape = (True, C, (W - k) // S + 1 if W >= k and S else 0, 0)
+        elif L.type in ("global_avg_pool", "whole_channel_pool"):
+            shape = (False, 0, 0, C)
+        elif L.type == "fc":
+            p = L.params
+            have = C * W * W if packed else n
+            if p["inputs"] and p["inputs"] != have:
+                _fail(f"layer '{L.name}': declares {p['inputs']} inputs but receives {have}")
+            m = p["outputs"]
+            if not p.get("weights_file"):
+                _fail(f"layer '{L.name}': no weights file given")
+            L.weights = _csv_values(_resolve_file(base, p.pop("weights_file")), m * have,
+                                    f"layer '{L.name}' weights").reshape(m, have)
+            bf = p.pop("bias_file", "")
+            L.bias = _csv_values(_resolve_file(base, bf), m, f"layer '{L.name}' bias") if bf else None
+            shape = (False, 0, 0, m)
+        elif L.type == "residual":
+            L.body, bshape = _load_weights(L.body, shape, base)
+            if L.downsample:
+                L.downsample, _ = _load_weights(L.downsample, shape, base)
+            shape = bshape
+        out.append(L)
+    return out, shape
+
+
+def load_spec(path: str) -> ModelSpec:
+    """ModelSpec::from_json_file (model_spec.cpp:232-272): a reference model spec
+    (models/README.md schema) with its CSV weights, batchnorm folded.  The engine
+    packs fully, so the context's slot_count must be ring_dimension / 2."""
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        _fail(f"cannot open model spec file {path}")
+    try:
+        j = json.loads(text)
+    except json.JSONDecodeError as e:
+        _fail(f"model spec is not valid JSON: {e}")
+    base = os.path.dirname(os.path.abspath(path))
+    ctx = j.get("context", {})
+    if isinstance(ctx, str):
+        if ctx not in _PRESETS:
+            _fail(f'unknown context preset "{ctx}" (expected "lenet5" or "large")')
+        ring, slots, depth = _PRESETS[ctx]
+    elif isinstance(ctx, dict):
+        ring = ctx.get("ring_dimension", 16384)
+        slots = ctx.get("slot_count", 8192)
+        depth = ctx.get("depth_budget", 10)
+    else:
+        _fail('"context" must be a preset name or a parameter object')
+    if j.get("weight_mode", "preload") not in ("preload", "lazy"):
+        _fail(f'weight_mode must be "preload" or "lazy", got "{j.get("weight_mode")}"')
+    policy = j.get("bootstrap_policy", "auto")
+    if policy not in ("auto", "explicit"):
+        _fail(f'bootstrap_policy must be "auto" or "explicit", got "{policy}"')
+    inp = j.get("input")
+    if not isinstance(inp, dict):
+        _fail('model spec needs an "input" object with channels and width')
+    C, W = _size(inp, "channels", "input"), _size(inp, "width", "input")
+    if "layers" not in j:
+        _fail('model spec needs a "layers" array')
+    layers = _parse_list(j["layers"], "")
+    layers, _ = _load_weights(layers, (True, C, W, 0), base)
+    return ModelSpec(j.get("name", "model"), ring, slots, depth, C, W, layers, policy)
+
+
 def _conv(name, f, c, k, rng, std, stride=1, padding=0, mode="generic", bias=True):
     w = rng.normal(0.0, std, (f, c, k, k))
     b = rng.normal(0.0, std, f) if bias else None
@@ -206,37 +435,98 @@ def _cost(b: Built) -> int:
     raise fh.ModelError(f"no depth cost for layer type {b.type}", 2)
 
 
+def _width(L: Layer, W: int, k: int, S: int, P: int) -> int:
+    try:
+        return fh.conv_output_width(W, k, S, P)
+    except fh.Error as e:
+        _fail(f"layer '{L.name}': {e}")
+
+
+def _describe(shape) -> str:
+    packed, C, W, n = shape
+    return f"{C}x{W}x{W} packed" if packed else f"{n} flat"
+
+
 def _resolve(layers: List[Layer], shape, slots) -> Tuple[List[Built], Tuple]:
+    """resolve_entry (model_spec.cpp:459-716): shape flow and the reference's checks."""
     out = []
     for L in layers:
         packed, C, W, n = shape
         if L.type == "conv":
+            if not packed:
+                _fail(f"layer '{L.name}': convolution needs a packed tensor input, the flow here is "
+                      f"{_describe(shape)}")
             cfg = _conv_cfg(L, C)
-            Wo = fh.conv_output_width(W, cfg.kernel, cfg.stride, cfg.padding)
-            new = (True, cfg.out_channels, Wo, 0)
-            if cfg.out_channels * Wo * Wo > slots:
-                raise fh.ModelError(f"layer '{L.name}': output needs {cfg.out_channels * Wo * Wo} slots, context "
-                                    f"provides {slots}", 2)
+            F, k = cfg.out_channels, cfg.kernel
+            if F == 0 or k == 0 or cfg.stride == 0:
+                _fail(f"layer '{L.name}': out_channels, kernel and stride must be positive")
+            mode = L.params.get("mode", "generic")
+            if mode == "special3x3":
+                if k != 3 or cfg.stride != 1 or cfg.padding != 1:
+                    _fail(f"layer '{L.name}': special3x3 mode requires kernel 3, stride 1, padding 1")
+                if W < 2:
+                    _fail(f"layer '{L.name}': special3x3 mode requires input edge >= 2")
+            if mode == "grouped" and F % C != 0:
+                _fail(f"layer '{L.name}': grouped convolution requires out_channels ({F}) divisible by the group "
+                      f"count ({C})")
+            Wo = _width(L, W, k, cfg.stride, cfg.padding)
+            Wp = W if mode == "special3x3" else W + 2 * cfg.padding
+            if C * Wp * Wp > slots:
+                _fail(f"layer '{L.name}': padded input needs {C * Wp * Wp} slots, context provides {slots}")
+            new = (True, F, Wo, 0)
+            if F * Wo * Wo > slots:
+                _fail(f"layer '{L.name}': output needs {F * Wo * Wo} slots, context provides {slots}")
         elif L.type == "avg_pool":
-            Wo = fh.conv_output_width(W, L.params.get("kernel", 2), L.params.get("stride", 2), 0)
+            if not packed:
+                _fail(f"layer '{L.name}': pooling needs a packed tensor input")
+            k, S = L.params.get("kernel", 2), L.params.get("stride", 2)
+            if k == 0 or S == 0:
+                _fail(f"layer '{L.name}': kernel and stride must be positive")
+            Wo = _width(L, W, k, S, 0)
+            if C * Wo * Wo > slots:
+                _fail(f"layer '{L.name}': output does not fit in the slot count")
             new = (True, C, Wo, 0)
         elif L.type in ("global_avg_pool", "whole_channel_pool"):
+            if not packed:
+                _fail(f"layer '{L.name}': pooling needs a packed tensor input")
+            if L.type == "whole_channel_pool" and L.params.get("kernel") != W:
+                _fail(f"layer '{L.name}': whole-channel pooling requires kernel ({L.params.get('kernel')}) == input "
+                      f"edge ({W})")
             new = (False, 0, 0, C)
         elif L.type == "fc":
-            new = (False, 0, 0, L.params["outputs"])
-        elif L.type in ("relu", "bootstrap"):
+            have = C * W * W if packed else n
+            p = L.params
+            if p.get("inputs") and p["inputs"] != have:
+                _fail(f"layer '{L.name}': declares {p['inputs']} inputs but receives {have} ({_describe(shape)})")
+            if p["outputs"] == 0:
+                _fail(f"layer '{L.name}': outputs must be positive")
+            if p.get("merge_budget", 1) == 0:
+                _fail(f"layer '{L.name}': merge_budget must be >= 1")
+            if p["outputs"] > slots or have > slots:
+                _fail(f"layer '{L.name}': does not fit in the slot count")
+            new = (False, 0, 0, p["outputs"])
+        elif L.type == "relu":
+            if L.params.get("degree", 59) < 0:
+                _fail(f"layer '{L.name}': degree must be >= 0")
+            if not L.params.get("scale", 1.0) > 0.0:
+                _fail(f"layer '{L.name}': scale must be positive")
+            new = shape
+        elif L.type == "bootstrap":
             new = shape
         elif L.type == "residual":
+            if not packed:
+                _fail(f"layer '{L.name}': residual units need packed tensors")
             body, bshape = _resolve(L.body, shape, slots)
             ds, dshape = _resolve(L.downsample, shape, slots) if L.downsample else ([], shape)
-            if bshape != dshape:
-                raise fh.ModelError(f"residual '{L.name}': body and skip shapes differ", 2)
+            if bshape != dshape or not bshape[0]:
+                _fail(f"layer '{L.name}': body produces {_describe(bshape)} but the skip path carries "
+                      f"{_describe(dshape)}")
             b = Built("residual", L.name, L, shape, bshape, body=body, downsample=ds)
             out.append(b)
             shape = bshape
             continue
         else:
-            raise fh.ModelError(f"unsupported layer type '{L.type}'", 2)
+            _fail(f"unsupported layer type '{L.type}'")
         b = Built(L.type, L.name, L, shape, new)
         b.cost = _cost(b)
         out.append(b)
@@ -272,9 +562,10 @@ def _standard_placement(layers: List[Built], counters: List[int], inserted: List
         i += 1
 
 
-def _ledger(layers: List[Built], entry: int, budget: int, inserted: List[int]) -> int:
+def _ledger(layers: List[Built], entry: int, budget: int, inserted: List[int], repair: bool = True) -> int:
     """Level ledger with repair (model_spec.cpp:789-851): a layer that needs
-    more levels than remain gets a bootstrap inserted in front of it."""
+    more levels than remain gets a bootstrap inserted in front of it (policy
+    auto) or fails the build (policy explicit)."""
     level = entry
     i = 0
     while i < len(layers):
@@ -287,6 +578,9 @@ def _ledger(layers: List[Built], entry: int, budget: int, inserted: List[int]) -
         if b.type == "residual":
             need = b.downsample[0].cost if b.downsample else 0
         if need > level:
+            if not repair:
+                _fail(f"layer '{b.name}' needs {need} levels but only {level} remain; the explicit bootstrap "
+                      f"placement does not hold the depth budget")
             if need > budget:
                 raise fh.ModelError(f"layer '{b.name}' needs {need} levels but the depth budget is only {budget}", 2)
             layers.insert(i, Built("bootstrap", f"bootstrap_auto_{inserted[0]}", None, b.in_shape, b.in_shape))
@@ -295,7 +589,7 @@ def _ledger(layers: List[Built], entry: int, budget: int, inserted: List[int]) -
             i += 1
         if b.type == "residual":
             d_skip = b.downsample[0].cost if b.downsample else 0
-            body_exit = _ledger(b.body, level, budget, inserted)
+            body_exit = _ledger(b.body, level, budget, inserted, repair)
             ex = min(body_exit, level - d_skip)
             b.cost = level - ex
             level = ex
@@ -306,13 +600,32 @@ def _ledger(layers: List[Built], entry: int, budget: int, inserted: List[int]) -
 
 
 def build(spec: ModelSpec) -> List[Built]:
+    """build_model (model_spec.cpp:864-904)."""
+    if spec.input_channels == 0 or spec.input_width == 0:
+        _fail("model input needs positive channels and width")
+    if not spec.layers:
+        _fail("model has no layers")
+    need = spec.input_channels * spec.input_width * spec.input_width
+    if need > spec.slot_count:
+        _fail(f"model input needs {need} slots, context provides {spec.slot_count}")
     shape = (True, spec.input_channels, spec.input_width, 0)
     layers, _ = _resolve(spec.layers, shape, spec.slot_count)
     inserted = [0]
     if spec.bootstrap_policy == "auto":
         _standard_placement(layers, [0, 0], inserted)
-    _ledger(layers, spec.depth_budget, spec.depth_budget, inserted)
+    _ledger(layers, spec.depth_budget, spec.depth_budget, inserted, spec.bootstrap_policy == "auto")
     return layers
+
+
+def ledger_rows(layers: List[Built], budget: int) -> List[Tuple[str, int, int, bool]]:
+    """Top-level (name, level_in, level_out, is_bootstrap) rows the built model
+    will record (the reference infer()'s report rows), without running it."""
+    rows, level = [], budget
+    for b in layers:
+        out = budget if b.type == "bootstrap" else level - b.cost
+        rows.append((b.name, level, out, b.type == "bootstrap"))
+        level = out
+    return rows
 
 
 def count_bootstraps(layers: List[Built]) -> int:

@@ -1,7 +1,7 @@
 """Generates the golden fixtures in tests/golden/ by running the UNMODIFIED
 reference (oracle/_ref/libslotcnn_ref.so, compiled from /root/reference/proj)
 on seeded inputs, plus the reference's own frozen ReLU bound fixture
-(proj/tests/data/relu_epsilon59.json).  Run here (container) where
+(proj/tests/data/relu_epsilon59.json) and its model specs (proj/models/*.json).  Run here (container) where
 /root/reference exists:  python tests/golden/make_golden.py
 """
 import json
@@ -54,6 +54,13 @@ def main():
     d = json.load(open(src))
     json.dump({k: d[k] for k in ("degree", "grid_points", "deadzone", "epsilon_59", "sup_norm")},
               open(os.path.join(HERE, "relu_epsilon59.json"), "w"), indent=1)
+    # the reference's own model specs (models/lenet5.json, models/resnet20.json): the
+    # architecture descriptions the model runtime must drive; their CSV weights are not
+    # shipped, tests/model_files.py materialises seeded ones next to a copy
+    os.makedirs(os.path.join(HERE, "ref_models"), exist_ok=True)
+    for m in ("lenet5", "resnet20"):
+        d = json.load(open(f"/root/reference/proj/models/{m}.json"))
+        json.dump(d, open(os.path.join(HERE, "ref_models", f"{m}.json"), "w"), indent=1)
     print("golden fixtures written to", HERE)
 
 

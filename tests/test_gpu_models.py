@@ -74,6 +74,52 @@ def test_resnet20_reference_preset_depth25():
     _compare(spec, x, "fast")
 
 
+@pytest.mark.parametrize("name,shape", [("lenet5", (1, 28, 28)), ("resnet20", (3, 32, 32))])
+def test_reference_model_files_end_to_end(name, shape):
+    """The reference's own models/lenet5.json (preset "lenet5": N=2^14) and
+    models/resnet20.json (preset "large": N=2^15), depth budget 25, seeded CSV
+    weights (tests/model_files.py), ReLU scales calibrated as the reference's
+    calibrate step does, loaded by the model runtime and run encrypted."""
+    from model_files import materialize
+    spec = M.load_spec(materialize(name, tempfile.mkdtemp(), seed=9))
+    if name == "resnet20":
+        def prep(x):
+            return (x - 0.5) / 0.2887
+    else:
+        def prep(x):
+            return x
+    cal = [prep(np.random.default_rng(500 + i).uniform(0, 1, shape)) for i in range(4)]
+    spec = M.calibrate_relu_scales(spec, cal)
+    _compare(spec, prep(np.random.default_rng(501).uniform(0, 1, shape)), "fast")
+
+
+def test_batchnorm_explicit_bootstraps_end_to_end():
+    """A reference-format spec with a batchnorm folded into its conv and
+    explicitly placed bootstraps (bootstrap_policy "explicit")."""
+    import json
+    import os
+    tmp = tempfile.mkdtemp()
+    rng = np.random.default_rng(21)
+    np.savetxt(os.path.join(tmp, "c1_w.csv"), rng.normal(0, 0.3, (1, 4 * 9)), delimiter=",", fmt="%.17g")
+    np.savetxt(os.path.join(tmp, "fc_w.csv"), rng.normal(0, 0.1, (3, 4 * 36)), delimiter=",", fmt="%.17g")
+    spec = {"name": "bnnet", "context": {"ring_dimension": 8192, "slot_count": 4096, "depth_budget": 9},
+            "bootstrap_policy": "explicit", "input": {"channels": 1, "width": 8},
+            "layers": [{"type": "conv", "name": "c1", "out_channels": 4, "kernel": 3, "weights": "c1_w.csv"},
+                       {"type": "batchnorm", "gamma": [1.1, 0.9, 1.0, 1.2], "beta": [0.0, 0.1, -0.1, 0.05],
+                        "mean": [0.01, -0.02, 0.03, 0.0], "var": [1.0, 0.8, 1.3, 0.9]},
+                       {"type": "relu", "name": "r1", "degree": 7, "scale": 4.0}, {"type": "bootstrap"},
+                       {"type": "relu", "name": "r2", "degree": 27, "scale": 4.0}, {"type": "bootstrap"},
+                       {"type": "fc", "name": "fc", "outputs": 3, "weights": "fc_w.csv"}]}
+    path = os.path.join(tmp, "bnnet.json")
+    json.dump(spec, open(path, "w"))
+    x = np.random.default_rng(22).uniform(0, 1, (1, 8, 8))
+    ref_logits, rows, ref_events, _ = sref.infer(path, x)
+    em = M.EncryptedModel(M.load_spec(path))
+    r = em.infer(x)
+    assert [(a[0], a[2], a[3]) for a in r.ledger] == [(b[0], b[1], b[2]) for b in rows]
+    assert float(np.abs(r.logits - ref_logits).max()) < 1e-3
+
+
 def test_lenet5_no_bootstrap_deep_budget():
     """Depth budget deep enough that the ledger needs no bootstrap except the
     standard placements (policy auto)."""
