@@ -57,10 +57,10 @@ def main():
     # the reference's own model specs (models/lenet5.json, models/resnet20.json): the
     # architecture descriptions the model runtime must drive; their CSV weights are not
     # shipped, tests/model_files.py materialises seeded ones next to a copy
-    os.makedirs(os.path.join(HERE, "ref_models"), exist_ok=True)
-    for m in ("lenet5", "resnet20"):
-        d = json.load(open(f"/root/reference/proj/models/{m}.json"))
-        json.dump(d, open(os.path.join(HERE, "ref_models", f"{m}.json"), "w"), indent=1)
+    specs = {m: json.load(open(f"/root/reference/proj/models/{m}.json")) for m in ("lenet5", "resnet20")}
+    with open(os.path.join(HERE, "ref_model_specs.json"), "w") as f:  # one compact line per model
+        f.write("{\n" + ",\n".join(f"{json.dumps(m)}: {json.dumps(d, separators=(',', ':'))}"
+                                    for m, d in specs.items()) + "\n}\n")
     print("golden fixtures written to", HERE)
 
 

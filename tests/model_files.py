@@ -1,15 +1,14 @@
-"""Materialises a reference model spec (JSON, tests/golden/ref_models/) with
+"""Materialises a reference model spec (tests/golden/ref_model_specs.json) with
 seeded CSV weights for every file it references: the reference ships the
 architectures but not the weights (models/README.md)."""
 import json
 import math
 import os
-import shutil
 
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-REF_MODELS = os.path.join(HERE, "golden", "ref_models")
+REF_SPECS = os.path.join(HERE, "golden", "ref_model_specs.json")  # tests/golden/make_golden.py
 
 
 def _write(path, values):
@@ -18,9 +17,10 @@ def _write(path, values):
 
 
 def materialize(name: str, out_dir: str, seed: int = 1, context=None) -> str:
-    """Copy tests/golden/ref_models/<name>.json into out_dir (optionally with an
-    inline context replacing the preset) and write He-normal seeded weights."""
-    spec = json.load(open(os.path.join(REF_MODELS, f"{name}.json")))
+    """Write the reference's <name> spec (tests/golden/ref_model_specs.json) into
+    out_dir (optionally with an inline context replacing the preset) and seeded
+    He-normal weights for every CSV it names."""
+    spec = json.load(open(REF_SPECS))[name]
     if context is not None:
         spec["context"] = context
     rng = np.random.default_rng(seed)
@@ -71,4 +71,4 @@ def materialize(name: str, out_dir: str, seed: int = 1, context=None) -> str:
     return path
 
 
-__all__ = ["materialize", "REF_MODELS", "shutil"]
+__all__ = ["materialize", "REF_SPECS"]
