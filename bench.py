@@ -391,8 +391,8 @@ def model_runs(args):
                       True))
     for name, spec, x, with_ref_schedule in cases:
         em = M.EncryptedModel(spec)
-        em.infer(x)  # warm-up x2: lazy key generation, plaintext caches, pool growth
-        em.infer(x)
+        for _ in range(3):  # warm-up: lazy key generation, plaintext caches, pool growth
+            em.infer(x)
         times = []
         for _ in range(args.model_reps):
             r = em.infer(x)

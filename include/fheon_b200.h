@@ -119,6 +119,10 @@ int fheon_ctx_depth_budget(const fheon_ctx* ctx);
  * reference's exact rotation sequence (layers_conv.cpp / layers_misc.cpp) */
 int fheon_ctx_set_schedule(fheon_ctx* ctx, int schedule);
 int fheon_ctx_schedule(const fheon_ctx* ctx);
+/* HBM budget (bytes) of the resident weight-plaintext cache (conv kernel vectors encoded once at
+ * their consumer level): the reference's weight_mode "preload" (model.hpp:46-48); 0 = "lazy",
+ * re-encode per call.  Default 64 GiB. */
+int fheon_ctx_set_weight_cache(fheon_ctx* ctx, uint64_t bytes);
 /* raw RNS words, layout [2][limbs][N] */
 int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* words, int limbs, double scale, fheon_ct** out);
 int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);

@@ -90,6 +90,7 @@ SIGNATURES = {
     "fheon_ctx_depth_budget": (C.c_int, [vp]),
     "fheon_ctx_set_schedule": (C.c_int, [vp, C.c_int]),
     "fheon_ctx_schedule": (C.c_int, [vp]),
+    "fheon_ctx_set_weight_cache": (C.c_int, [vp, C.c_uint64]),
     "fheon_ct_upload": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
     "fheon_ct_download": (C.c_int, [vp, vp, u64p]),
     "fheon_rotate": (C.c_int, [vp, vp, C.c_long, pp]),

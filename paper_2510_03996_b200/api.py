@@ -265,6 +265,10 @@ class SlotContext:
             raise ShapeError(f'schedule must be one of {sorted(SCHEDULES)}, got "{schedule}"', 2)
         _check(_native.lib().fheon_ctx_set_schedule(self._h, SCHEDULES[schedule]))
 
+    def set_weight_cache(self, nbytes: int):
+        """HBM budget of resident weight plaintexts (weight_mode "preload"); 0 = "lazy"."""
+        _check(_native.lib().fheon_ctx_set_weight_cache(self._h, int(nbytes)))
+
     def attach_recorder(self) -> TraceRecorder:
         _check(_native.lib().fheon_set_tracing(self._h, 1))
         _check(_native.lib().fheon_trace_clear(self._h))

@@ -267,6 +267,10 @@ int fheon_ctx_set_schedule(fheon_ctx* ctx, int schedule) {
 }
 
 int fheon_ctx_schedule(const fheon_ctx* ctx) { return ctx ? ctx->impl->schedule : -1; }
+
+int fheon_ctx_set_weight_cache(fheon_ctx* ctx, uint64_t bytes) {
+  return guard([&] { ctx->impl->weight_cache_budget = (std::size_t)bytes; });
+}
 int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* w, int limbs, double scale, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::upload_ct(*ctx->impl, w, limbs, scale)); });
 }

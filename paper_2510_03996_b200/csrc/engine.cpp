@@ -169,6 +169,9 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
     FHEON_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const std::size_t ct_bytes = 2 * (std::size_t)(p.L + p.K) * ((std::size_t)1 << p.logN) * sizeof(u64);
     std::size_t want = std::min<std::size_t>(free_b / 4, 64 * ct_bytes * 3);
+    // resident weight plaintexts: up to a fifth of the free HBM (64 GiB cap); the
+    // keys, bootstrapping diagonals and masks need the rest
+    weight_cache_budget = std::min<std::size_t>(weight_cache_budget, free_b / 5);
     void* r = nullptr;
     if (want > 0 && cudaMallocAsync(&r, want, stream_) == cudaSuccess) cudaFreeAsync(r, stream_);
     cudaGetLastError();
@@ -193,6 +196,8 @@ Context::~Context() {
   keys_.clear();
   basis_.clear();
   ptcache_.clear();
+  namedcache_.clear();
+  weightcache_.clear();
   if (stream_) cudaStreamSynchronize(stream_);
   alive->store(false);
   for (void* d : dev_allocs_) cudaFree(d);
@@ -662,6 +667,20 @@ BufPtr Context::encode_named(const std::string& name, const std::function<std::v
   BufPtr b = encode(vals.data(), vals.size(), limbs, scale);
   ptcache_reserve((std::size_t)limbs * ht_.N);
   namedcache_[key] = b;
+  return b;
+}
+
+BufPtr Context::weight_pt(const std::string& key, int limbs, double scale, const std::function<BufPtr()>& make) {
+  if (weight_cache_budget == 0) return make();
+  auto k = std::make_tuple(key, limbs, scale);
+  auto it = weightcache_.find(k);
+  if (it != weightcache_.end()) return it->second;
+  BufPtr b = make();
+  const std::size_t bytes = (std::size_t)limbs * ht_.N * sizeof(u64);
+  if (weightcache_bytes_ + bytes <= weight_cache_budget) {
+    weightcache_[k] = b;
+    weightcache_bytes_ += bytes;
+  }
   return b;
 }
 

@@ -153,6 +153,11 @@ class Context {
   // same cache keyed by a caller-chosen name (the slot values are built only on a miss)
   BufPtr encode_named(const std::string& name, const std::function<std::vector<double>()>& make, int limbs,
                       double scale);
+  // weight plaintexts (conv kernel vectors) kept resident across calls, the
+  // reference's weight_mode "preload" (model.hpp:46-48): built once by `make`
+  // under `key`, then reused; past the budget new entries are built but not kept
+  BufPtr weight_pt(const std::string& key, int limbs, double scale, const std::function<BufPtr()>& make);
+  std::size_t weight_cache_budget = (std::size_t)64 << 30;  // bytes (<= free HBM / 5 at creation); 0 disables
   // device real-coefficient (unscaled, unrounded) encoding of a slot vector,
   // cached under `key` (block indicators of a layer geometry)
   const double* basis(const std::string& key, const std::vector<double>& slot_values);
@@ -203,6 +208,8 @@ class Context {
   };
   std::map<std::tuple<u64, int, double>, std::vector<PtEntry>> ptcache_;
   std::map<std::tuple<std::string, int, double>, BufPtr> namedcache_;
+  std::map<std::tuple<std::string, int, double>, BufPtr> weightcache_;
+  std::size_t weightcache_bytes_ = 0;
   std::size_t ptcache_words_ = 0;
   void ptcache_reserve(std::size_t words);
   mutable std::mutex trace_mu_;

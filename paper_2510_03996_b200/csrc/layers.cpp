@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <cstring>
 #include <map>
 #include <string>
 #include <tuple>
@@ -67,6 +68,18 @@ Ciphertext mp(Context& ctx, const Ciphertext& x, const std::vector<double>& full
 // plaintext for `like` from slot values (content-cached host encode)
 BufPtr pt_of(Context& ctx, const Ciphertext& like, const std::vector<double>& full) {
   return ctx.encode_cached(full, like.limbs, pt_scale_for(ctx, like));
+}
+
+// FNV-1a over a weight tensor's bit patterns (keys the resident weight plaintexts)
+std::string weight_key(const char* tag, const KernelTensor& w, std::size_t W) {
+  u64 h = 1469598103934665603ULL;
+  for (double v : w.weights) {
+    u64 b;
+    std::memcpy(&b, &v, 8);
+    h = (h ^ b) * 1099511628211ULL;
+  }
+  return std::string(tag) + ":" + std::to_string(h) + ":" + std::to_string(w.out_channels) + "x" +
+         std::to_string(w.in_channels) + "x" + std::to_string(w.kernel) + ":" + std::to_string(W);
 }
 
 // indicator of block c (size m) as a cached device basis vector
@@ -279,12 +292,14 @@ PackedTensor conv_core_generic(Context& ctx, const PackedTensor& x, const ConvCo
   // fused rotate-and-MAC: sum_f = sum_taps tap (*) repeated_kernel_vector(f, tap)
   std::vector<std::vector<Ciphertext>> terms(F, taps);
   std::vector<std::vector<BufPtr>> pts(F);
+  const std::string wk = weight_key("g", w, W);
   for (std::size_t f = 0; f < F; ++f)
     for (std::size_t i = 0; i < k; ++i)
       for (std::size_t j = 0; j < k; ++j) {
         std::vector<double> wc(C);
         for (std::size_t c = 0; c < C; ++c) wc[c] = w.at(f, c, i, j);
-        pts[f].push_back(pt_blocks(ctx, taps[0], wc, m, ps));
+        const std::string key = wk + ":" + std::to_string(f) + ":" + std::to_string(i * k + j);
+        pts[f].push_back(ctx.weight_pt(key, taps[0].limbs, ps, [&] { return pt_blocks(ctx, taps[0], wc, m, ps); }));
       }
   std::vector<Ciphertext> sums = mac_plain_many(ctx, terms, pts);
   sums = channel_accumulate_many(ctx, sums, C, m);
@@ -719,6 +734,7 @@ PackedTensor conv_special_3x3(Context& ctx, const PackedTensor& x, const ConvCon
     }
   std::vector<std::vector<Ciphertext>> terms(F, taps);
   std::vector<std::vector<BufPtr>> pts(F);
+  const std::string wk = weight_key("s3", w, W);
   for (std::size_t f = 0; f < F; ++f)
     for (std::size_t tap = 0; tap < 9; ++tap) {
       LinComb lc{};
@@ -729,7 +745,8 @@ PackedTensor conv_special_3x3(Context& ctx, const PackedTensor& x, const ConvCon
         lc.w[lc.nb] = wv;
         ++lc.nb;
       }
-      pts[f].push_back(ctx.encode_lincomb(lc, taps[4].limbs, ps));
+      pts[f].push_back(ctx.weight_pt(wk + ":" + std::to_string(f) + ":" + std::to_string(tap), taps[4].limbs, ps,
+                                     [&] { return ctx.encode_lincomb(lc, taps[4].limbs, ps); }));
     }
   std::vector<Ciphertext> sums = mac_plain_many(ctx, terms, pts);
   sums = channel_accumulate_many(ctx, sums, C, m);

@@ -51,6 +51,7 @@ class ModelSpec:
     input_width: int
     layers: List[Layer]
     bootstrap_policy: str = "auto"
+    weight_mode: str = "preload"  # "lazy": no resident weight plaintexts (model.hpp:46-48)
 
     def write(self, directory: str) -> str:
         """Reference JSON spec + CSV weights (models/README.md format)."""
@@ -76,7 +77,7 @@ class ModelSpec:
         spec = {"name": self.name,
                 "context": {"ring_dimension": self.ring_dimension, "slot_count": self.slot_count,
                             "depth_budget": self.depth_budget},
-                "weight_mode": "preload", "bootstrap_policy": self.bootstrap_policy,
+                "weight_mode": self.weight_mode, "bootstrap_policy": self.bootstrap_policy,
                 "input": {"channels": self.input_channels, "width": self.input_width},
                 "layers": [enc(L) for L in self.layers]}
         path = os.path.join(directory, f"{self.name}.json")
@@ -298,8 +299,9 @@ def load_spec(path: str) -> ModelSpec:
         depth = ctx.get("depth_budget", 10)
     else:
         _fail('"context" must be a preset name or a parameter object')
-    if j.get("weight_mode", "preload") not in ("preload", "lazy"):
-        _fail(f'weight_mode must be "preload" or "lazy", got "{j.get("weight_mode")}"')
+    weight_mode = j.get("weight_mode", "preload")
+    if weight_mode not in ("preload", "lazy"):
+        _fail(f'weight_mode must be "preload" or "lazy", got "{weight_mode}"')
     policy = j.get("bootstrap_policy", "auto")
     if policy not in ("auto", "explicit"):
         _fail(f'bootstrap_policy must be "auto" or "explicit", got "{policy}"')
@@ -311,7 +313,7 @@ def load_spec(path: str) -> ModelSpec:
         _fail('model spec needs a "layers" array')
     layers = _parse_list(j["layers"], "")
     layers, _ = _load_weights(layers, (True, C, W, 0), base)
-    return ModelSpec(j.get("name", "model"), ring, slots, depth, C, W, layers, policy)
+    return ModelSpec(j.get("name", "model"), ring, slots, depth, C, W, layers, policy, weight_mode)
 
 
 def _conv(name, f, c, k, rng, std, stride=1, padding=0, mode="generic", bias=True):
@@ -676,6 +678,8 @@ class EncryptedModel:
         self.layers = build(spec)
         self.n_boot = count_bootstraps(self.layers)
         self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule))
+        if spec.weight_mode == "lazy":
+            self.ctx.set_weight_cache(0)
         if self.ctx.depth_budget() != spec.depth_budget:
             raise fh.InternalError("engine depth budget differs from the spec", 3)
 
