@@ -269,11 +269,12 @@ Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv) {
     terms.push_back(t);
     pts.push_back(p);
   }
-  std::vector<Ciphertext> inner = mac_plain_many(ctx_, terms, pts);
-  // giant steps: rotate-and-sum, one ModDown for the whole level
+  // giant steps: rotate-and-sum of the unrescaled inner sums -- one ModDown and one
+  // rescale for the whole level
+  std::vector<Ciphertext> inner = mac_plain_many_unrescaled(ctx_, terms, pts);
   std::vector<std::pair<Ciphertext, long>> g;
   for (std::size_t i = 0; i < lv.giants.size(); ++i) g.push_back({inner[i], lv.giants[i].rot});
-  return rotate_sum_many(ctx_, {g})[0];
+  return rescale_to_target(ctx_, rotate_sum_many(ctx_, {g}))[0];
 }
 
 Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {

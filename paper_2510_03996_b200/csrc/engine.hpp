@@ -235,6 +235,13 @@ std::vector<Ciphertext> rescale_many(Context& ctx, const std::vector<Ciphertext>
 // one mult_plain trace event per term (level_after = level - 1), o-major.
 std::vector<Ciphertext> mac_plain_many(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
                                        const std::vector<std::vector<BufPtr>>& pts);
+// the same fused MAC without the rescale: outputs stay at `limbs` with scale
+// T_{lv-1} q_lv (rotations commute with the deferred rescale, so a rotate-and-sum
+// over such outputs needs one rescale instead of one per term); trace as above
+std::vector<Ciphertext> mac_plain_many_unrescaled(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
+                                                  const std::vector<std::vector<BufPtr>>& pts);
+// rescale unrescaled MAC outputs onto the next level's target scale
+std::vector<Ciphertext> rescale_to_target(Context& ctx, const std::vector<Ciphertext>& prods);
 std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b);
 std::vector<Ciphertext> conjugate_many(Context& ctx, const std::vector<Ciphertext>& xs);
 Ciphertext mul_by_i(Context& ctx, const Ciphertext& x);

@@ -767,6 +767,20 @@ std::vector<Ciphertext> rescale_many(Context& ctx, const std::vector<Ciphertext>
 
 std::vector<Ciphertext> mac_plain_many(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
                                        const std::vector<std::vector<BufPtr>>& pts) {
+  std::vector<Ciphertext> prods = mac_plain_many_unrescaled(ctx, terms, pts);
+  return rescale_to_target(ctx, prods);
+}
+
+std::vector<Ciphertext> rescale_to_target(Context& ctx, const std::vector<Ciphertext>& prods) {
+  if (prods.empty()) return {};
+  const int lv = prods[0].limbs - 1;
+  std::vector<Ciphertext> outs = rescale_many(ctx, prods);
+  for (Ciphertext& o : outs) o.scale = ctx.host().T[lv - 1];
+  return outs;
+}
+
+std::vector<Ciphertext> mac_plain_many_unrescaled(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
+                                                  const std::vector<std::vector<BufPtr>>& pts) {
   if (terms.size() != pts.size()) throw Error(ErrKind::internal, "mac_plain_many: size mismatch");
   std::vector<Ciphertext> prods;
   prods.reserve(terms.size());
@@ -827,16 +841,14 @@ std::vector<Ciphertext> mac_plain_many(Context& ctx, const std::vector<std::vect
       }
     }
   }
-  for (Ciphertext& p : prods) p.scale = ref.scale;
-  std::vector<Ciphertext> outs = rescale_many(ctx, prods);
-  for (std::size_t o = 0; o < outs.size(); ++o) {
-    outs[o].scale = h.T[lv - 1];
+  // plaintexts were encoded at T_{lv-1} q_lv / scale: the products sit at T_{lv-1} q_lv
+  for (Ciphertext& p : prods) p.scale = h.T[lv - 1] * (double)h.q[lv];
+  for (std::size_t o = 0; o < prods.size(); ++o)
     for (std::size_t j = 0; j < terms[o].size(); ++j) {
       ctx.stats.mult_plain++;
       ctx.record(1, lv - 1);
     }
-  }
-  return outs;
+  return prods;
 }
 
 Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt) {

@@ -102,16 +102,21 @@ BufPtr pt_blocks(Context& ctx, const Ciphertext& like, const std::vector<double>
   return ctx.encode_lincomb(lc, like.limbs, scale);
 }
 
-// single-term MAC over a batch: out[i] = rescale(xs[i] (*) pts[i])
-std::vector<Ciphertext> mp_many(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<BufPtr>& pts) {
+// single-term MAC over a batch: out[i] = rescale(xs[i] (*) pts[i]); with `defer`
+// the rescale is left to the caller (rescale_to_target after a rotate-and-sum:
+// one rescale for the sum instead of one per term)
+std::vector<Ciphertext> mp_many(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<BufPtr>& pts,
+                                bool defer = false) {
   std::vector<std::vector<Ciphertext>> t(xs.size());
   std::vector<std::vector<BufPtr>> p(xs.size());
   for (std::size_t i = 0; i < xs.size(); ++i) {
     t[i] = {xs[i]};
     p[i] = {pts[i]};
   }
-  return mac_plain_many(ctx, t, p);
+  return defer ? mac_plain_many_unrescaled(ctx, t, p) : mac_plain_many(ctx, t, p);
 }
+
+Ciphertext rescale_one(Context& ctx, const Ciphertext& c) { return rescale_to_target(ctx, {c})[0]; }
 
 void check_stride_geometry(const Context& ctx, const Ciphertext& a, std::size_t W, std::size_t S, std::size_t W_out) {
   if (!a.valid()) throw Error(ErrKind::internal, "striding: operand is not initialized");
@@ -304,10 +309,12 @@ PackedTensor conv_core_generic(Context& ctx, const PackedTensor& x, const ConvCo
   std::vector<Ciphertext> sums = mac_plain_many(ctx, terms, pts);
   sums = channel_accumulate_many(ctx, sums, C, m);
   const BufPtr cleanup = pt_of(ctx, sums[0], plain(ctx, extraction_mask(W, C)));
-  std::vector<Ciphertext> a_star = mp_many(ctx, sums, std::vector<BufPtr>(F, cleanup));
-  std::vector<Ciphertext> r =
-      (S == 1 && W_out == W) ? a_star : stride_many(ctx, a_star, W, S, W_out, cfg.stride_variant);
+  const bool strided = !(S == 1 && W_out == W);
+  const bool defer = ctx.fast_schedule() && !strided;  // the placement sum rescales once
+  std::vector<Ciphertext> a_star = mp_many(ctx, sums, std::vector<BufPtr>(F, cleanup), defer);
+  std::vector<Ciphertext> r = strided ? stride_many(ctx, a_star, W, S, W_out, cfg.stride_variant) : a_star;
   Ciphertext out = place_and_sum(ctx, r, W_out * W_out);
+  if (defer) out = rescale_one(ctx, out);
   out = add_bias(ctx, out, w.bias, W_out * W_out);
   return {out, F, W_out};
 }
@@ -501,11 +508,12 @@ std::vector<Ciphertext> stride_bsgs_many(Context& ctx, const std::vector<Ciphert
         pts[i * W_out + a].push_back(masks[b]);
       }
   }
-  const std::vector<Ciphertext> rows = mac_plain_many(ctx, terms, pts);
+  // rows stay unrescaled through the giant-step rotate-and-sum: one rescale per input
+  const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, terms, pts);
   std::vector<RotTerms> giants(B);
   for (std::size_t i = 0; i < B; ++i)
     for (std::size_t a = 0; a < W_out; ++a) giants[i].push_back({rows[i * W_out + a], (long)(a * (S * W - W_out))});
-  return sum_rotations(ctx, giants);
+  return rescale_to_target(ctx, sum_rotations(ctx, giants));
 }
 }  // namespace
 
@@ -751,8 +759,10 @@ PackedTensor conv_special_3x3(Context& ctx, const PackedTensor& x, const ConvCon
   std::vector<Ciphertext> sums = mac_plain_many(ctx, terms, pts);
   sums = channel_accumulate_many(ctx, sums, C, m);
   const BufPtr cleanup = pt_of(ctx, sums[0], plain(ctx, extraction_mask(W, C)));
-  std::vector<Ciphertext> cleaned = mp_many(ctx, sums, std::vector<BufPtr>(F, cleanup));
+  const bool defer = ctx.fast_schedule();
+  std::vector<Ciphertext> cleaned = mp_many(ctx, sums, std::vector<BufPtr>(F, cleanup), defer);
   Ciphertext out = place_and_sum(ctx, cleaned, m);
+  if (defer) out = rescale_one(ctx, out);
   out = add_bias(ctx, out, w.bias, m);
   return {out, F, W};
 }
@@ -849,7 +859,9 @@ Ciphertext global_avg_pool(Context& ctx, const PackedTensor& x) {
   const Ciphertext sums = detail::block_sum(ctx, x.data, m);
   const std::vector<Ciphertext> cur = channel_cursors(ctx, sums, C, m);
   const BufPtr head = pt_of(ctx, sums, range_mask(ctx, 0, 1, 1.0 / (double)m));
-  return merge_channel_slots(ctx, mp_many(ctx, cur, std::vector<BufPtr>(C, head)));
+  const bool defer = ctx.fast_schedule();
+  const Ciphertext out = merge_channel_slots(ctx, mp_many(ctx, cur, std::vector<BufPtr>(C, head), defer));
+  return defer ? rescale_one(ctx, out) : out;
 }
 
 // whole_channel_pool (layers_misc.cpp:168-195)
@@ -860,7 +872,9 @@ Ciphertext whole_channel_pool(Context& ctx, const PackedTensor& x, std::size_t k
   const Ciphertext sums = detail::block_sum(ctx, v, m);
   const std::vector<Ciphertext> cur = channel_cursors(ctx, sums, C, m);
   const BufPtr head = pt_of(ctx, sums, range_mask(ctx, 0, 1));
-  return merge_channel_slots(ctx, mp_many(ctx, cur, std::vector<BufPtr>(C, head)));
+  const bool defer = ctx.fast_schedule();
+  const Ciphertext out = merge_channel_slots(ctx, mp_many(ctx, cur, std::vector<BufPtr>(C, head), defer));
+  return defer ? rescale_one(ctx, out) : out;
 }
 
 // ------------------------------------------------------------- FC
@@ -879,7 +893,8 @@ Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std
   for (std::size_t off = 1; off < p2; off <<= 1)
     y = add_many(ctx, y, rotate_many(ctx, y, std::vector<long>(m, (long)off)));
   const BufPtr head = pt_of(ctx, y[0], range_mask(ctx, 0, 1));
-  std::vector<Ciphertext> neurons = mp_many(ctx, y, std::vector<BufPtr>(m, head));
+  const bool defer = ctx.fast_schedule();
+  std::vector<Ciphertext> neurons = mp_many(ctx, y, std::vector<BufPtr>(m, head), defer);
   const std::size_t r = (m <= B + 1) ? m : B;
   const std::size_t T = (m + r - 1) / r;
   // in-group placements are independent: one rotate-and-sum batch
@@ -893,6 +908,7 @@ Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std
   if (ctx.fast_schedule()) out = place_and_sum(ctx, groups, r);
   else
     for (std::size_t t = T - 1; t-- > 0;) out = add(ctx, rotate(ctx, out, -(long)r), groups[t]);
+  if (defer) out = rescale_one(ctx, out);
   std::vector<double> b(m, 0.0);
   if (bias) std::copy(bias, bias + m, b.begin());
   return add_plain(ctx, out, b.data(), b.size());
