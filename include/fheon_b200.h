@@ -51,6 +51,7 @@ typedef struct {
   int hamming_weight; /* secret: 0 uniform ternary, h > 0 sparse with h nonzero coefficients */
   int bootstrap;      /* 1: enable CKKS bootstrapping (bootstrap() refreshes to depth_budget) */
   int boot_scale_bits;/* scale of the bootstrapping levels (0 = scale_bits) */
+  int digit_split;    /* key-switching digits: 0 uniform ceil(limbs/dnum), 1 balanced by bit size */
 } fheon_params;
 
 /* ---- errors / version */

@@ -29,6 +29,8 @@ typedef unsigned __int128 u128;
 
 struct ock_ctx {
   int logN, L, K, dnum, alpha, S;
+  int dig[MAXP + 1]; /* key-switching digit boundaries: D_j = [dig[j], dig[j+1]) */
+  int ndig;
   size_t N;
   u64 seed;
   u64 q[MAXP];
@@ -138,6 +140,9 @@ ock_ctx* ock_create(int logN, int L, int K, int dnum, int first_bits,
   c->K = K;
   c->dnum = dnum;
   c->alpha = (L + dnum - 1) / dnum;
+  c->ndig = 0;
+  for (int j = 0; j * c->alpha < L; j++) c->dig[c->ndig++] = j * c->alpha;
+  c->dig[c->ndig] = L;
   c->seed = seed;
   const u64 M = 2 * (u64)c->N;
   int np = 0;
@@ -554,8 +559,8 @@ int ock_keygen(const ock_ctx* c, u64 key_id, u64* key) {
     if ((key_id & 1) == 0) { free(sp); return -1; }
     ock_automorph_ntt(c, key_id, c->s_ntt, sp, LK);
   }
-  for (int j = 0; j < c->dnum; j++) {
-    const int lo = j * c->alpha, hi = (lo + c->alpha < L) ? lo + c->alpha : L;
+  for (int j = 0; j < c->dnum; j++) { /* digits past ndig stay empty */
+    const int lo = j < c->ndig ? c->dig[j] : L, hi = j < c->ndig ? c->dig[j + 1] : L;
     u64* b = key + ((size_t)j * 2 + 0) * LK * N;
     u64* a = key + ((size_t)j * 2 + 1) * LK * N;
 #pragma omp parallel for
@@ -637,6 +642,66 @@ int ock_decrypt(const ock_ctx* c, const u64* ct, int limbs, double scale, double
 }
 
 /* --------------------------------------------------------- key switching */
+/* digits with an active limb at `limbs` limbs */
+static int digit_count(const ock_ctx* c, int limbs) {
+  int k = 0;
+  while (k < c->ndig && c->dig[k] < limbs) k++;
+  return k;
+}
+
+/* Contiguous digits balanced by bit size (engine params.cpp balanced_digits):
+ * bisection on the widest digit's bit sum, greedy packing under it, <= 15 limbs
+ * per digit, at most dnum digits. */
+static int split_digits(const double* bits, int L, int dnum, double cap, int* d) {
+  int n = 0, size = 0;
+  double acc = 0.0;
+  d[n++] = 0;
+  for (int i = 0; i < L; i++) {
+    if (bits[i] > cap) return -1;
+    if (size == 15 || acc + bits[i] > cap) {
+      d[n++] = i;
+      acc = 0.0;
+      size = 0;
+    }
+    acc += bits[i];
+    size++;
+  }
+  d[n] = L;
+  return n > dnum ? -1 : n;
+}
+
+int ock_set_digit_split(ock_ctx* c, int balanced) {
+  if (!balanced) {
+    c->ndig = 0;
+    for (int j = 0; j * c->alpha < c->L; j++) c->dig[c->ndig++] = j * c->alpha;
+    c->dig[c->ndig] = c->L;
+    return 0;
+  }
+  double bits[MAXP];
+  double lo = 0.0, hi = 0.0;
+  for (int i = 0; i < c->L; i++) {
+    bits[i] = log2((double)c->q[i]);
+    hi += bits[i];
+  }
+  int best[MAXP + 1], tmp[MAXP + 1];
+  int nb = split_digits(bits, c->L, c->dnum, hi + 1.0, best);
+  if (nb < 0) return -1;
+  for (int it = 0; it < 60; it++) {
+    const double mid = 0.5 * (lo + hi);
+    const int n = split_digits(bits, c->L, c->dnum, mid, tmp);
+    if (n >= 0) {
+      hi = mid;
+      nb = n;
+      memcpy(best, tmp, sizeof(int) * (size_t)(n + 1));
+    } else {
+      lo = mid;
+    }
+  }
+  c->ndig = nb;
+  memcpy(c->dig, best, sizeof(int) * (size_t)(nb + 1));
+  return 0;
+}
+
 static inline int ext_prime(const ock_ctx* c, int limbs, int t) {
   return t < limbs ? t : c->L + (t - limbs);
 }
@@ -645,12 +710,12 @@ static inline int ext_prime(const ock_ctx* c, int limbs, int t) {
 int ock_modup(const ock_ctx* c, const u64* d, int limbs, u64* out) {
   const int K = c->K, E = limbs + K;
   const size_t N = c->N;
-  const int beta = (limbs + c->alpha - 1) / c->alpha;
+  const int beta = digit_count(c, limbs);
   u64* x = (u64*)malloc((size_t)limbs * N * sizeof(u64));
   memcpy(x, d, (size_t)limbs * N * sizeof(u64));
   ock_ntt_inv_limbs(c, x, limbs, NULL);
   for (int j = 0; j < beta; j++) {
-    const int lo = j * c->alpha, hi = (lo + c->alpha < limbs) ? lo + c->alpha : limbs;
+    const int lo = c->dig[j], hi = c->dig[j + 1] < limbs ? c->dig[j + 1] : limbs;
     const int a = hi - lo;
     u64* y = (u64*)malloc((size_t)a * N * sizeof(u64));
     for (int i = lo; i < hi; i++) {
@@ -764,7 +829,7 @@ int ock_keyswitch(const ock_ctx* c, const u64* d, int limbs, const u64* key,
                   u64 g, u64* ks0, u64* ks1) {
   const int L = c->L, K = c->K, E = limbs + K, LK = L + K;
   const size_t N = c->N;
-  const int beta = (limbs + c->alpha - 1) / c->alpha;
+  const int beta = digit_count(c, limbs);
   u64* up = (u64*)malloc((size_t)beta * E * N * sizeof(u64));
   ock_modup(c, d, limbs, up);
   size_t* idx = (size_t*)malloc(N * sizeof(size_t));
@@ -802,7 +867,7 @@ int ock_rotate_sum(const ock_ctx* c, const u64* const* cts, const long* ts, int 
                    const u64* const* keys, u64* out) {
   const int L = c->L, K = c->K, E = limbs + K, LK = L + K;
   const size_t N = c->N;
-  const int beta = (limbs + c->alpha - 1) / c->alpha;
+  const int beta = digit_count(c, limbs);
   u64* acc0 = (u64*)calloc((size_t)E * N, sizeof(u64));
   u64* acc1 = (u64*)calloc((size_t)E * N, sizeof(u64));
   u64* up = (u64*)malloc((size_t)beta * E * N * sizeof(u64));

@@ -74,6 +74,8 @@ int ock_decrypt(const ock_ctx* c, const uint64_t* ct, int limbs, double scale,
 
 /* ---- key switching pieces ---- */
 int ock_modup(const ock_ctx* c, const uint64_t* d, int limbs, uint64_t* out);
+/* 1: key-switching digits balanced by bit size (engine Params::digit_split), 0: uniform */
+int ock_set_digit_split(ock_ctx* c, int balanced);
 /* sum_j rotate(cts[j], ts[j]) with one ModDown (engine rotate_sum_many); cts[j] [2][limbs][N] */
 int ock_rotate_sum(const ock_ctx* c, const uint64_t* const* cts, const long* ts, int n, int limbs,
                    const uint64_t* const* keys, uint64_t* out);

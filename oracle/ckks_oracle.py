@@ -47,6 +47,7 @@ def lib():
         L.ock_decode_coeffs.argtypes = [vp, _dblp, C.c_double, _dblp]
         L.ock_secret.argtypes = [vp, _i8p]
         L.ock_set_hamming_weight.argtypes = [vp, C.c_int]
+        L.ock_set_digit_split.argtypes = [vp, C.c_int]
         L.ock_keygen.argtypes = [vp, C.c_uint64, _u64p]
         L.ock_encrypt.argtypes = [vp, _dblp, C.c_size_t, C.c_uint64, _u64p]
         L.ock_decrypt.argtypes = [vp, _u64p, C.c_int, C.c_double, _dblp]
@@ -77,7 +78,8 @@ def _chk(rc, what):
 class Oracle:
     """CPU RNS-CKKS context mirroring the engine's parameter spec."""
 
-    def __init__(self, logN, L, K, dnum, first_bits, scale_bits, special_bits, seed=1, hamming_weight=0):
+    def __init__(self, logN, L, K, dnum, first_bits, scale_bits, special_bits, seed=1, hamming_weight=0,
+                 digit_split=0):
         self.logN, self.L, self.K, self.dnum = logN, L, K, dnum
         self.N = 1 << logN
         self.S = self.N // 2
@@ -91,6 +93,8 @@ class Oracle:
         lib().ock_info(self._c, self.primes, self.psi, self.T)
         if hamming_weight:
             lib().ock_set_hamming_weight(self._c, int(hamming_weight))
+        if digit_split:
+            _chk(lib().ock_set_digit_split(self._c, 1), "set_digit_split")
 
     def __del__(self):
         if getattr(self, "_c", None):

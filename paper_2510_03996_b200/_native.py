@@ -31,6 +31,7 @@ class fheon_params(C.Structure):
         ("hamming_weight", C.c_int),
         ("bootstrap", C.c_int),
         ("boot_scale_bits", C.c_int),
+        ("digit_split", C.c_int),
     ]
 
 

@@ -120,6 +120,7 @@ class ContextConfig:
     hamming_weight: int = 0   # 0: uniform ternary secret; h: sparse (needed for bootstrapping)
     bootstrap: bool = False   # build the CKKS bootstrapping pipeline
     boot_scale_bits: int = 0  # scale of the bootstrapping levels (0 = rescale_bits)
+    digit_split: int = 0      # key-switching digits: 0 uniform, 1 balanced by prime bit size
     # layer rotation schedule: "fast" (hoisted / log-depth / baby-step giant-step,
     # same values and levels) or "reference" (the reference's exact rotation trace)
     schedule: str = "fast"
@@ -173,6 +174,7 @@ class ContextConfig:
         p.hamming_weight = self.hamming_weight
         p.bootstrap = int(bool(self.bootstrap))
         p.boot_scale_bits = int(self.boot_scale_bits)
+        p.digit_split = int(self.digit_split)
         return p
 
 

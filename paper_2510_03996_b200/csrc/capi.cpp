@@ -66,6 +66,7 @@ static fheon::Params to_params(const fheon_params* p) {
   prm.hamming_weight = p->hamming_weight;
   prm.bootstrap = p->bootstrap;
   prm.boot_scale_bits = p->boot_scale_bits;
+  prm.digit_split = p->digit_split;
   return prm;
 }
 

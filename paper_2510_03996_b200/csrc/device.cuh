@@ -28,11 +28,27 @@ struct PrimeConst {
 };
 
 constexpr int kMaxBases = 32;
+constexpr int kMaxDigits = 16;
+
+// Key-switching digits D_j = [b[j], b[j+1]) (contiguous, b[0] = 0, b[n] = L);
+// at `limbs` active limbs digit j holds [b[j], min(b[j+1], limbs)).
+struct DigitTable {
+  int b[kMaxDigits + 1];
+  int n;
+  __host__ __device__ int lo(int j) const { return b[j]; }
+  __host__ __device__ int hi(int j, int limbs) const { return b[j + 1] < limbs ? b[j + 1] : limbs; }
+  __host__ __device__ int beta(int limbs) const {  // digits with an active limb
+    int k = 0;
+    while (k < n && b[k] < limbs) ++k;
+    return k;
+  }
+};
 
 // A set of limb-polynomials addressed as base[b] + blk * block_stride + t * N
 // with blk < blocks_per_base and t < E; prime of limb t is p0 + t (t < ell) or
-// L + (t - ell) (special primes).  skip_alpha > 0 skips t in digit blk's own
-// range [blk*alpha, min((blk+1)*alpha, ell)) (ModUp outputs).
+// L + (t - ell) (special primes).  skip_digits = beta > 0 skips t in digit
+// j = blk mod beta's own range [dig.b[j], min(dig.b[j+1], ell)) (ModUp outputs of
+// several inputs, beta digits each: the digit's own limbs pass through).
 struct LimbSet {
   u64* base[kMaxBases];
   int nbase;
@@ -41,7 +57,8 @@ struct LimbSet {
   int E;
   int ell;
   int L;
-  int skip_alpha;
+  int skip_digits;
+  DigitTable dig;
   int p0;  // prime index of limb t = 0 (q limbs)
   int count() const { return nbase * blocks_per_base * E; }
 };
@@ -105,10 +122,9 @@ __device__ __forceinline__ bool limbset_get(const LimbSet& s, int idx, std::size
   const int r = idx - b * per_base;
   const int blk = r / s.E;
   const int t = r - blk * s.E;
-  if (s.skip_alpha > 0) {
-    const int lo = blk * s.skip_alpha;
-    const int hi = min(lo + s.skip_alpha, s.ell);
-    if (t >= lo && t < hi) return false;
+  if (s.skip_digits > 0) {
+    const int j = blk % s.skip_digits;
+    if (t >= s.dig.lo(j) && t < s.dig.hi(j, s.ell)) return false;
   }
   ptr = s.base[b] + (long long)blk * s.block_stride + (long long)t * (long long)N;
   prime = t < s.ell ? s.p0 + t : s.L + (t - s.ell);

@@ -131,7 +131,8 @@ u64 prod_mod(const std::vector<u64>& primes, int lo, int hi, int skip, u64 m) {
 }  // namespace
 
 Context::Context(const Params& p) : ht_(make_tables(p)) {
-  if (ht_.alpha > kMaxAlpha - 1) throw Error(ErrKind::shape, "alpha = ceil(L/dnum) must be < 16");
+  if (ht_.alpha > kMaxAlpha - 1) throw Error(ErrKind::shape, "a key-switching digit must hold < 16 limbs");
+  if (ht_.ndig > kMaxDigits) throw Error(ErrKind::shape, "at most 16 key-switching digits");
   if (p.K > kMaxK - 1) throw Error(ErrKind::shape, "K must be < 16");
   if (p.L > 64) throw Error(ErrKind::shape, "L must be <= 64");
   {
@@ -139,9 +140,9 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
     // modulus Q_j, otherwise the key-switch noise Q_j * e / P swamps the scale.
     double logP = 0.0;
     for (int k = 0; k < p.K; ++k) logP += std::log2((double)ht_.q[p.L + k]);
-    for (int j = 0; j < p.dnum; ++j) {
+    for (int j = 0; j < ht_.ndig; ++j) {
       double logQ = 0.0;
-      for (int i = j * ht_.alpha; i < std::min((j + 1) * ht_.alpha, p.L); ++i) logQ += std::log2((double)ht_.q[i]);
+      for (int i = ht_.dig[j]; i < ht_.dig[j + 1]; ++i) logQ += std::log2((double)ht_.q[i]);
       if (logQ > logP)
         throw Error(ErrKind::shape, "special modulus P (" + std::to_string((int)logP) +
                                         " bits) must exceed every key-switching digit modulus (digit " +
@@ -210,7 +211,7 @@ Context::~Context() {
 
 void Context::build_device_tables() {
   const Params& p = ht_.p;
-  const int L = p.L, K = p.K, NP = L + K, dnum = p.dnum, alpha = ht_.alpha;
+  const int L = p.L, K = p.K, NP = L + K, dnum = p.dnum;
   const std::size_t N = ht_.N;
   const std::vector<u64>& q = ht_.q;
   DevTables& t = dt_;
@@ -221,7 +222,9 @@ void Context::build_device_tables() {
   t.L = L;
   t.K = K;
   t.dnum = dnum;
-  t.alpha = alpha;
+  t.alpha = ht_.alpha;
+  t.dig.n = ht_.ndig;
+  for (int j = 0; j <= ht_.ndig; ++j) t.dig.b[j] = ht_.dig[j];
   t.timer = &timer;
 
   std::vector<PrimeConst> pcs(NP);
@@ -266,8 +269,8 @@ void Context::build_device_tables() {
   std::vector<u64> qhinv((std::size_t)L * dnum * kMaxAlpha * 2, 0);
   std::vector<u64> qhat((std::size_t)L * dnum * NP * kMaxAlpha, 0);
   for (int limbs = 1; limbs <= L; ++limbs) {
-    for (int j = 0; j < dnum; ++j) {
-      const int lo = j * alpha, hi = std::min(lo + alpha, limbs);
+    for (int j = 0; j < ht_.ndig; ++j) {
+      const int lo = ht_.dig[j], hi = std::min(ht_.dig[j + 1], limbs);
       if (lo >= hi) continue;
       const int tab = (limbs - 1) * dnum + j;
       for (int i = lo; i < hi; ++i) {
@@ -418,8 +421,8 @@ void Context::gen_key(u64 key_id) {
   ls.E = NP;
   ls.ell = NP;
   ls.L = L;
-  for (int j = 0; j < p.dnum; ++j) {
-    const int lo = j * ht_.alpha, hi = std::min(lo + ht_.alpha, L);
+  for (int j = 0; j < p.dnum; ++j) {  // digits past ndig stay empty (lo = hi = L)
+    const int lo = j < ht_.ndig ? ht_.dig[j] : L, hi = j < ht_.ndig ? ht_.dig[j + 1] : L;
     sample_error(dt_, e->ptr, prng_stream_key(p.seed, stream_key(key_id, j, 3)), NP, NP, stream_);
     ntt_forward(dt_, ls, stream_);
     u64* b = kb->ptr + (std::size_t)(j * 2) * LN;

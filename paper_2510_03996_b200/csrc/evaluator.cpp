@@ -13,7 +13,8 @@ namespace fheon {
 
 namespace {
 
-LimbSet limbset(u64* base, int blocks, std::size_t stride, int E, int ell, int L, int p0 = 0, int skip_alpha = 0) {
+LimbSet limbset(u64* base, int blocks, std::size_t stride, int E, int ell, int L, int p0 = 0,
+                const DigitTable* skip = nullptr) {
   LimbSet s{};
   s.base[0] = base;
   s.nbase = 1;
@@ -23,7 +24,8 @@ LimbSet limbset(u64* base, int blocks, std::size_t stride, int E, int ell, int L
   s.ell = ell;
   s.L = L;
   s.p0 = p0;
-  s.skip_alpha = skip_alpha;
+  s.skip_digits = skip != nullptr ? skip->beta(ell) : 0;
+  if (skip) s.dig = *skip;
   return s;
 }
 
@@ -75,7 +77,7 @@ BufPtr modup_all(Context& ctx, const std::vector<const u64*>& inputs, int limbs)
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
   const int L = ctx.L(), E = limbs + ctx.K();
-  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const int beta = t.dig.beta(limbs);
   const int nin = (int)inputs.size();
   const std::size_t ext_words = (std::size_t)beta * E * N;
   BufPtr xc = ctx.alloc((std::size_t)std::min(nin, kMaxBases) * limbs * N);
@@ -96,10 +98,12 @@ BufPtr modup_all(Context& ctx, const std::vector<const u64*>& inputs, int limbs)
     }
     modup_bconv(t, el, xl, limbs, st);
     ntt_forward(t, limbset(ext->ptr + (std::size_t)i0 * ext_words, ni * beta, (std::size_t)E * N, E, limbs, L, 0,
-                           t.alpha),
+                           &t.dig),
                 st);
   }
-  ctx.stats.ntt_limbs += (std::size_t)nin * ((std::size_t)limbs + (std::size_t)beta * (E - t.alpha));
+  std::size_t own = 0;  // limbs the digits pass through un-NTT'd
+  for (int j = 0; j < beta; ++j) own += (std::size_t)(t.dig.hi(j, limbs) - t.dig.lo(j));
+  ctx.stats.ntt_limbs += (std::size_t)nin * ((std::size_t)limbs + (std::size_t)beta * E - own);
   return ext;
 }
 
@@ -123,7 +127,7 @@ std::vector<Ciphertext> keyswitch(Context& ctx, const std::vector<const u64*>& i
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
   const int L = ctx.L(), K = ctx.K(), E = limbs + K;
-  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const int beta = t.dig.beta(limbs);
   ctx.stats.keyswitches += jobs.size();
 
   const std::size_t ext_words = (std::size_t)beta * E * N;
@@ -199,7 +203,7 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
   const int L = ctx.L(), K = ctx.K(), E = limbs + K;
-  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const int beta = t.dig.beta(limbs);
   const std::size_t ext_words = (std::size_t)beta * E * N;
   ctx.stats.keyswitches += jobs.size();
   BufPtr ext = modup_all(ctx, inputs, limbs);

@@ -89,13 +89,12 @@ constexpr int kTC = 8;
 template <int A>
 __global__ void __launch_bounds__(256) k_modup_bconv(PolyList ext, PolyList x, const PrimeConst* __restrict__ pc,
                                                      const u64* __restrict__ qhinv, const u64* __restrict__ qhat,
-                                                     int logN, int limbs, int L, int K, int dnum, int alpha, int j) {
+                                                     int logN, int limbs, int L, int K, int dnum, int lo, int j) {
   __shared__ u64 cs[kTC][A];
   __shared__ u64 tq[kTC][2];
   __shared__ int tdst[kTC];
   const std::size_t N = (std::size_t)1 << logN;
   const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lo = j * alpha;
   const int E = limbs + K;
   const int tab = (limbs - 1) * dnum + j;
   const int nt = min(kTC, E - A - (int)blockIdx.y * kTC);
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(256) k_modup_bconv(PolyList ext, PolyList x, c
 
 // grid (N/256, E, jobs)
 __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int logN, int limbs, int L, int K,
-                           int alpha) {
+                           DigitTable dig) {
   const std::size_t N = (std::size_t)1 << logN;
   const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y;
@@ -142,14 +141,14 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
   const PrimeConst P = pc[pt];
   const u64 g = jobs.g[r];
   const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
-  const int beta = (limbs + alpha - 1) / alpha;
+  const int beta = dig.beta(limbs);
   const u64* key = jobs.key[r];
   const u64* ext = jobs.ext[r];
   const u64* d = jobs.d[r];
   Acc128 a0, a1;
   for (int j = 0; j < beta; ++j) {
-    const int lo = j * alpha;
-    const int hi = min(lo + alpha, limbs);
+    const int lo = dig.lo(j);
+    const int hi = dig.hi(j, limbs);
     const u64 v = (t >= lo && t < hi) ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
     const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
     a0.mac(v, kj[n]);
@@ -164,7 +163,7 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
 // Each job's digit sum (<= beta + 1 products < q^2) is REDC'd on its own so the
 // 128-bit accumulator never exceeds q * 2^64; job results add mod q.
 __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc, const u64* __restrict__ md_q,
-                               int logN, int limbs, int L, int K, int alpha) {
+                               int logN, int limbs, int L, int K, DigitTable dig) {
   const std::size_t N = (std::size_t)1 << logN;
   const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y;
@@ -172,7 +171,7 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
   const int E = limbs + K;
   const int pt = t < limbs ? t : L + (t - limbs);
   const PrimeConst P = pc[pt];
-  const int beta = (limbs + alpha - 1) / alpha;
+  const int beta = dig.beta(limbs);
   const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;  // P mod q_t, Montgomery form
   u64 s0 = 0, s1 = 0;
   for (int jb = jobs.begin[r]; jb < jobs.begin[r + 1]; ++jb) {
@@ -183,8 +182,8 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
     const u64* d = jobs.d[jb];
     Acc128 a0, a1;
     for (int j = 0; j < beta; ++j) {
-      const int lo = j * alpha;
-      const int hi = min(lo + alpha, limbs);
+      const int lo = dig.lo(j);
+      const int hi = dig.hi(j, limbs);
       const u64 v = (t >= lo && t < hi) ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
       const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
       a0.mac(v, kj[n]);
@@ -462,16 +461,17 @@ void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int 
 }
 
 void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st) {
-  const int beta = (limbs + t.alpha - 1) / t.alpha;
+  const int beta = t.dig.beta(limbs);
   TimedScope ts(t, kModUp, st);
   const int E = limbs + t.K;
   for (int j = 0; j < beta; ++j) {
-    const int a = std::min(t.alpha, limbs - j * t.alpha);
+    const int lo = t.dig.lo(j);
+    const int a = t.dig.hi(j, limbs) - lo;
     const dim3 grid = grid_for(t.N, (E - a + kTC - 1) / kTC, x.n);
 #define FHEON_BCONV(AA)                                                                                        \
   case AA:                                                                                                     \
     k_modup_bconv<AA><<<grid, kThreads, 0, st>>>(ext, x, t.pc, t.modup_qhinv, t.modup_qhat, t.logN, limbs, t.L, \
-                                                 t.K, t.dnum, t.alpha, j);                                     \
+                                                 t.K, t.dnum, lo, j);                                          \
     break;
     switch (a) {
       FHEON_BCONV(1) FHEON_BCONV(2) FHEON_BCONV(3) FHEON_BCONV(4) FHEON_BCONV(5) FHEON_BCONV(6) FHEON_BCONV(7)
@@ -486,14 +486,14 @@ void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int
 void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.n == 0) return;
   TimedScope ts(t, kKsInner, st);
-  k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K, t.alpha);
+  k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K, t.dig);
   launch_check("k_ks_inner");
 }
 void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.ngroups == 0) return;
   TimedScope ts(t, kKsInner, st);
   k_ks_inner_sum<<<grid_for(t.N, limbs + t.K, jobs.ngroups), kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs,
-                                                                                 t.L, t.K, t.alpha);
+                                                                                 t.L, t.K, t.dig);
   launch_check("k_ks_inner_sum");
 }
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {

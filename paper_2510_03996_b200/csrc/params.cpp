@@ -70,6 +70,44 @@ u64 top_candidate(int bits, u64 M) {
 
 }  // namespace
 
+std::vector<int> balanced_digits(const std::vector<double>& bits, int dnum, int max_size) {
+  const int L = (int)bits.size();
+  auto split = [&](double cap, std::vector<int>* out) {  // greedy: fewest digits under cap
+    std::vector<int> d{0};
+    double acc = 0.0;
+    int size = 0;
+    for (int i = 0; i < L; ++i) {
+      if (bits[i] > cap) return false;
+      if (size == max_size || acc + bits[i] > cap) {
+        d.push_back(i);
+        acc = 0.0;
+        size = 0;
+      }
+      acc += bits[i];
+      ++size;
+    }
+    d.push_back(L);
+    if ((int)d.size() - 1 > dnum) return false;
+    if (out) *out = d;
+    return true;
+  };
+  double lo = 0.0, hi = 0.0;
+  for (double b : bits) hi += b;
+  std::vector<int> best;
+  if (!split(hi + 1.0, &best)) throw std::invalid_argument("digit split: too many limbs for dnum digits");
+  for (int it = 0; it < 60; ++it) {  // bisection on the widest digit's bits
+    const double mid = 0.5 * (lo + hi);
+    std::vector<int> d;
+    if (split(mid, &d)) {
+      hi = mid;
+      best = d;
+    } else {
+      lo = mid;
+    }
+  }
+  return best;
+}
+
 HostTables make_tables(const Params& p) {
   if (p.logN < 10 || p.logN > 16) throw std::invalid_argument("logN must be in [10, 16]");
   if (p.L < 1 || p.K < 1 || p.L + p.K > kMaxPrimes || p.dnum < 1)
@@ -149,6 +187,17 @@ HostTables make_tables(const Params& p) {
     }
   }
   t.q = q;
+  if (p.digit_split) {
+    std::vector<double> bits(p.L);
+    for (int i = 0; i < p.L; ++i) bits[i] = std::log2((double)q[i]);
+    t.dig = balanced_digits(bits, p.dnum, 15);
+  } else {
+    for (int j = 0; j * t.alpha < p.L; ++j) t.dig.push_back(j * t.alpha);
+    t.dig.push_back(p.L);
+  }
+  t.ndig = (int)t.dig.size() - 1;
+  t.alpha = 0;
+  for (int j = 0; j < t.ndig; ++j) t.alpha = std::max(t.alpha, t.dig[j + 1] - t.dig[j]);
   t.psi.resize(q.size());
   for (std::size_t i = 0; i < q.size(); ++i) {
     const u64 qi = q[i];

@@ -37,7 +37,15 @@ struct Params {
   int boot_double_angles = 3;
   int boot_cts_levels = 3;
   int boot_stc_levels = 3;
+  // key-switching digits: 0 = uniform alpha = ceil(L / dnum) limbs each; 1 = contiguous
+  // digits balanced by bit size (the widest digit decides how many special primes
+  // P needs, so a chain of mixed 40/55-bit primes wants unequal limb counts)
+  int digit_split = 0;
 };
+
+// contiguous split of per-limb bit sizes into at most `dnum` digits minimising the
+// widest digit's bit sum (each digit <= max_size limbs); returns boundaries 0 = d_0 < ... < d_n = L
+std::vector<int> balanced_digits(const std::vector<double>& bits, int dnum, int max_size);
 
 // levels consumed by bootstrapping for these parameters (bootstrap.cpp)
 int bootstrap_depth(const Params& p);
@@ -46,7 +54,9 @@ int bootstrap_depth(const Params& p);
 struct HostTables {
   Params p;
   std::size_t N = 0;
-  int S = 0, alpha = 0, nprimes = 0;
+  int S = 0, alpha = 0, nprimes = 0;  // alpha = widest digit (limbs)
+  std::vector<int> dig;                 // digit boundaries d_0 = 0 < ... < d_ndig = L
+  int ndig = 0;
   std::vector<u64> q;        // [L+K]: q_0..q_{L-1}, p_0..p_{K-1}
   std::vector<u64> psi;      // primitive 2N-th roots
   std::vector<double> T;     // scale target per level (level = limbs-1)

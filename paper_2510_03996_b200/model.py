@@ -648,17 +648,48 @@ def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: s
     boot_depth = 16 if bootstrapping else 0
     L = spec.depth_budget + 1 + boot_depth
     dnum = 3
-    alpha = -(-L // dnum)
-    # special primes (60-bit): the fewest whose product P exceeds every digit
-    # modulus Q_j by 2 bits (chain: 55-bit q0, 40-bit application primes,
-    # 55-bit bootstrapping primes); the engine re-checks P > Q_j exactly
-    bits = [55] + [40] * spec.depth_budget + [55] * boot_depth
-    widest = max(sum(bits[j:j + alpha]) + 0.1 * len(bits[j:j + alpha]) for j in range(0, L, alpha))
-    K = -(-int(widest + 2.0) // 59)
-    return fh.ContextConfig(N, N // 2, spec.depth_budget if not bootstrapping else -1,
-                            fh.CryptoMetadata(55, 40, dnum), limbs=L, special_limbs=K, special_bits=60, seed=seed,
-                            hamming_weight=64 if bootstrapping else 0, bootstrap=bootstrapping,
-                            boot_scale_bits=55 if bootstrapping else 0, schedule=schedule)
+
+    def config(K):
+        return fh.ContextConfig(N, N // 2, spec.depth_budget if not bootstrapping else -1,
+                                fh.CryptoMetadata(55, 40, dnum), limbs=L, special_limbs=K, special_bits=60, seed=seed,
+                                hamming_weight=64 if bootstrapping else 0, bootstrap=bootstrapping,
+                                boot_scale_bits=55 if bootstrapping else 0, schedule=schedule, digit_split=1)
+
+    # digits balanced by bit size over the real Q chain (the special primes are
+    # chosen after it, so K does not change it); K = the fewest 60-bit special
+    # primes whose product exceeds the widest digit by 2 bits (the engine re-checks)
+    qbits = [math.log2(float(q)) for q in fh.host_primes(config(1))[0][:L]]
+    K = -(-int(balanced_widest(qbits, dnum) + 2.0) // 59) + 0
+    while True:
+        cfg = config(K)
+        pbits = sum(math.log2(float(q)) for q in fh.host_primes(cfg)[0][L:])
+        if pbits > balanced_widest(qbits, dnum):
+            return cfg
+        K += 1
+
+
+def balanced_widest(bits: List[float], dnum: int, max_size: int = 15) -> float:
+    """Widest digit (bits) of the balanced contiguous digit split -- the same
+    bisection + greedy packing as params.cpp balanced_digits."""
+    def split(cap):
+        n, acc, size = 1, 0.0, 0
+        for b in bits:
+            if b > cap:
+                return None
+            if size == max_size or acc + b > cap:
+                n, acc, size = n + 1, 0.0, 0
+            acc += b
+            size += 1
+        return n if n <= dnum else None
+
+    lo, hi = 0.0, sum(bits)
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if split(mid) is not None:
+            hi = mid
+        else:
+            lo = mid
+    return hi
 
 
 @dataclass

@@ -15,12 +15,12 @@ pytestmark = pytest.mark.gpu
 SMALL = dict(logN=12, L=6, K=2, dnum=3, first=50, scale=40, special=60, seed=11)
 
 
-def make_pair(logN, L, K, dnum, first, scale, special, seed, depth=None):
+def make_pair(logN, L, K, dnum, first, scale, special, seed, depth=None, digit_split=0):
     cfg = fh.ContextConfig(1 << logN, 1 << (logN - 1), depth if depth is not None else L - 1,
                            fh.CryptoMetadata(first, scale, dnum), limbs=L, special_limbs=K, special_bits=special,
-                           seed=seed)
+                           seed=seed, digit_split=digit_split)
     ctx = fh.SlotContext(cfg)
-    orc = Oracle(logN, L, K, dnum, first, scale, special, seed)
+    orc = Oracle(logN, L, K, dnum, first, scale, special, seed, digit_split=digit_split)
     return ctx, orc
 
 
@@ -301,3 +301,25 @@ def test_config1_rotation_bit_exact():
     got = fh.rotate(x, 28)
     assert np.array_equal(got.words(), orc.rotate(ct, 28, orc.rotation_key(28)))
     assert np.abs(got.slots() - np.roll(vals, -28)).max() < 1e-6
+
+
+@pytest.mark.parametrize("L,t", [(7, 3), (9, -17), (13, 100)])
+def test_balanced_digits_keyswitch_bit_exact(L, t):
+    """Key-switching digits balanced by prime bit size (60-bit q0, 40-bit rest:
+    unequal limb counts per digit): keys, rotation and rotate-and-sum stay
+    bit-exact against the oracle's restatement (ock_set_digit_split)."""
+    ctx, orc = make_pair(12, L, 4, 3, 60, 40, 60, 23, digit_split=1)
+    rng = np.random.default_rng(L)
+    vals, ct = _oracle_ct(orc, rng, counter=40)
+    x = fh.SlotVector.from_words(ctx, ct, orc.T[-1])
+    g = orc.galois(t)
+    assert np.array_equal(ctx.download_key(g), orc.keygen(g))
+    assert np.array_equal(fh.rotate(x, t).words(), orc.rotate(ct, t, orc.rotation_key(t)))
+    for limbs in (L - 2, 3):  # lower levels: fewer active digits
+        xs = fh.level_down(x, limbs)
+        c2 = xs.words()
+        assert np.array_equal(fh.rotate(xs, t).words(), orc.rotate(c2, t, orc.rotation_key(t)))
+    y = fh.rotate_sum([x, x], [t, 1])
+    want = orc.rotate_sum([ct, ct], [t, 1], [orc.rotation_key(t), orc.rotation_key(1)])
+    assert np.array_equal(y.words(), want)
+
