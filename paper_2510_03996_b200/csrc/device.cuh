@@ -42,6 +42,19 @@ struct DigitTable {
     while (k < n && b[k] < limbs) ++k;
     return k;
   }
+  __host__ __device__ int digit_of(int t) const {  // digit holding Q limb t
+    int k = 0;
+    while (k + 1 < n && b[k + 1] <= t) ++k;
+    return k;
+  }
+};
+
+// Key-switch inner-product launch facts: beta active digits (host-resolved) and
+// the device table owner[t] = digit of Q limb t (a broadcast load per CTA; a
+// dynamically indexed kernel-parameter array would spill to local memory).
+struct DigitOwner {
+  const unsigned char* owner;
+  int beta;
 };
 
 // A set of limb-polynomials addressed as base[b] + blk * block_stride + t * N

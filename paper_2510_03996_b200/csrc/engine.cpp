@@ -225,6 +225,11 @@ void Context::build_device_tables() {
   t.alpha = ht_.alpha;
   t.dig.n = ht_.ndig;
   for (int j = 0; j <= ht_.ndig; ++j) t.dig.b[j] = ht_.dig[j];
+  {
+    std::vector<unsigned char> own(L);
+    for (int i = 0; i < L; ++i) own[i] = (unsigned char)t.dig.digit_of(i);
+    t.digit_owner = upload(dev_allocs_, own, stream_);
+  }
   t.timer = &timer;
 
   std::vector<PrimeConst> pcs(NP);

@@ -27,6 +27,7 @@ struct DevTables {
   std::size_t N = 0;
   int L = 0, K = 0, dnum = 0, alpha = 0;
   DigitTable dig{};  // key-switching digit boundaries
+  unsigned char* digit_owner = nullptr;  // [L]: digit of each Q limb
   PrimeConst* pc = nullptr;   // [L+K]
   u64* tw = nullptr;          // [L+K][4][N]: tw, tw', itw, itw'
   // ModUp, indexed by tab = (limbs-1)*dnum + digit

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) k_modup_bconv(PolyList ext, PolyList x, c
 
 // grid (N/256, E, jobs)
 __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int logN, int limbs, int L, int K,
-                           DigitTable dig) {
+                           DigitOwner dig) {
   const std::size_t N = (std::size_t)1 << logN;
   const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y;
@@ -141,15 +141,14 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
   const PrimeConst P = pc[pt];
   const u64 g = jobs.g[r];
   const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
-  const int beta = dig.beta(limbs);
+  const int beta = dig.beta;
+  const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;  // CTA-uniform: limb t's own digit passes d through
   const u64* key = jobs.key[r];
   const u64* ext = jobs.ext[r];
   const u64* d = jobs.d[r];
   Acc128 a0, a1;
   for (int j = 0; j < beta; ++j) {
-    const int lo = dig.lo(j);
-    const int hi = dig.hi(j, limbs);
-    const u64 v = (t >= lo && t < hi) ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+    const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
     const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
     a0.mac(v, kj[n]);
     a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
@@ -163,7 +162,7 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
 // Each job's digit sum (<= beta + 1 products < q^2) is REDC'd on its own so the
 // 128-bit accumulator never exceeds q * 2^64; job results add mod q.
 __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc, const u64* __restrict__ md_q,
-                               int logN, int limbs, int L, int K, DigitTable dig) {
+                               int logN, int limbs, int L, int K, DigitOwner dig) {
   const std::size_t N = (std::size_t)1 << logN;
   const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y;
@@ -171,7 +170,8 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
   const int E = limbs + K;
   const int pt = t < limbs ? t : L + (t - limbs);
   const PrimeConst P = pc[pt];
-  const int beta = dig.beta(limbs);
+  const int beta = dig.beta;
+  const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;
   const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;  // P mod q_t, Montgomery form
   u64 s0 = 0, s1 = 0;
   for (int jb = jobs.begin[r]; jb < jobs.begin[r + 1]; ++jb) {
@@ -182,9 +182,7 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
     const u64* d = jobs.d[jb];
     Acc128 a0, a1;
     for (int j = 0; j < beta; ++j) {
-      const int lo = dig.lo(j);
-      const int hi = dig.hi(j, limbs);
-      const u64 v = (t >= lo && t < hi) ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+      const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
       const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
       a0.mac(v, kj[n]);
       a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
@@ -486,14 +484,15 @@ void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int
 void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.n == 0) return;
   TimedScope ts(t, kKsInner, st);
-  k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K, t.dig);
+  k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K,
+                                                                       DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner");
 }
 void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.ngroups == 0) return;
   TimedScope ts(t, kKsInner, st);
   k_ks_inner_sum<<<grid_for(t.N, limbs + t.K, jobs.ngroups), kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs,
-                                                                                 t.L, t.K, t.dig);
+                                                                                 t.L, t.K, DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner_sum");
 }
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
