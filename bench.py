@@ -497,7 +497,11 @@ def run_reference(args):
                          "sample": f"{per_thread} rotate() calls per thread x {cores} threads per step, 32768 "
                                    "slots (reference simulator: memcpy rotation, no crypto)"},
         "e2e": {"value": round(value, 1), "unit": "rotations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference's rotate() is a cleartext memcpy simulator (backend.cpp:165-182); the same CKKS "
+                "key-switch rotation on this host's CPU cores is ckks_cpu_port",
     }
+    if not args.no_cpu_baseline:
+        line["ckks_cpu_port"] = cpu_baseline_port(args)
     print(json.dumps(line), flush=True)
 
 
