@@ -382,6 +382,28 @@ def resnet20(seed: int = 4001, ring: int = 65536, depth_budget: int = 12) -> Mod
     return ModelSpec("resnet20", ring, ring // 2, depth_budget, 3, 32, layers)
 
 
+def vgg16(seed: int = 5001, ring: int = 65536, depth_budget: int = 25) -> ModelSpec:
+    """BASELINE configs[4]: 3x32x32 input, thirteen 3x3 convs (64-64-128-128-256x3-
+    512x3-512x3, pad 1), 2x2 average pooling after each block, FC 512->512->10,
+    He-normal weights.  With full packing the first block's 64x32x32 output
+    needs 65536 slots: at N = 2^16 (32768 slots) the build fails exactly as the
+    reference's does ("output needs 65536 slots")."""
+    rng = np.random.default_rng(seed)
+    layers, C, i = [], 3, 0
+    for block, (F, n) in enumerate(((64, 2), (128, 2), (256, 3), (512, 3), (512, 3)), start=1):
+        for u in range(n):
+            i += 1
+            layers.append(_conv(f"conv{block}_{u + 1}", F, C, 3, rng, math.sqrt(2.0 / (C * 9)), padding=1,
+                                mode="special3x3", bias=False))
+            layers.append(Layer("relu", f"relu{block}_{u + 1}", {"degree": 59}))
+            C = F
+        layers.append(Layer("avg_pool", f"pool{block}", {"kernel": 2, "stride": 2}))
+    layers.append(Layer("fc", "fc1", {"outputs": 512}, rng.normal(0, math.sqrt(2.0 / 512), (512, 512)), np.zeros(512)))
+    layers.append(Layer("relu", "relu_fc1", {"degree": 59}))
+    layers.append(Layer("fc", "fc2", {"outputs": 10}, rng.normal(0, math.sqrt(2.0 / 512), (10, 512)), np.zeros(10)))
+    return ModelSpec("vgg16", ring, ring // 2, depth_budget, 3, 32, layers)
+
+
 # ----------------------------------------------------------------- build
 @dataclass
 class Built:

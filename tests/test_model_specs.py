@@ -135,3 +135,20 @@ def test_invalid_specs_fail_like_the_reference(mutate, fragment):
     with pytest.raises(sref.RefError) as r:
         sref.infer(path, x)
     assert r.value.category == e.value.category
+
+
+@needs_ref
+def test_vgg16_does_not_fit_32768_slots_like_the_reference():
+    """BASELINE configs[4] VGG-16 at N=2^16: the first block's 64x32x32 output
+    needs 65536 slots; the reference's build fails with ModelError (BASELINE.md
+    section 2) and so does ours, with the same message and category."""
+    spec = M.vgg16(ring=65536)
+    with pytest.raises(fh.ModelError) as e:
+        M.build(spec)
+    assert "output needs 65536 slots, context provides 32768" in str(e.value)
+    path = spec.write(tempfile.mkdtemp())
+    with pytest.raises(sref.RefError) as r:
+        sref.infer(path, np.zeros((3, 32, 32)))
+    assert "output needs 65536 slots, context provides 32768" in str(r.value)
+    assert r.value.category == e.value.category
+
