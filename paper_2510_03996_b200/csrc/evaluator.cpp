@@ -70,6 +70,34 @@ void check_scales(const Ciphertext& a, const Ciphertext& b, const char* op) {
                                        std::to_string(b.scale) + ")");
 }
 
+// ModDown's finish (acc - conv) P^-1 + sigma(add) fused into the conv's forward NTT
+NttEpilogue moddown_epilogue(const DevTables& t, const PolyList& out, const PolyList& acc, const PolyList& add) {
+  NttEpilogue e{};
+  for (int i = 0; i < out.n; ++i) {
+    e.out[i] = out.p[i];
+    e.src[i] = acc.p[i];
+    e.add[i] = add.p[i];
+    e.add_g[i] = add.g[i];
+  }
+  e.cst = t.md_q + 2;  // md_q[i * 4 + 2] = P^-1 mod q_i, + 3 Shoup
+  e.cst_stride = 4;
+  return e;
+}
+
+// rescale's finish (a - lift) q_l^-1 fused into the lift's forward NTT
+NttEpilogue rescale_epilogue(const DevTables& t, const PolyList& out, const PolyList& a, int limbs) {
+  NttEpilogue e{};
+  for (int i = 0; i < out.n; ++i) {
+    e.out[i] = out.p[i];
+    e.src[i] = a.p[i];
+    e.add[i] = nullptr;
+    e.add_g[i] = 1;
+  }
+  e.cst = t.rs + (std::size_t)(limbs - 1) * t.L * 4;  // rs[(l * L + i) * 4] = q_l^-1 mod q_i, + 1 Shoup
+  e.cst_stride = 4;
+  return e;
+}
+
 // ModUp of every input, batched (one pipeline of launches per 32 inputs):
 // [nin][beta][limbs+K][N] extended digits in the NTT domain
 BufPtr modup_all(Context& ctx, const std::vector<const u64*>& inputs, int limbs) {
@@ -181,8 +209,8 @@ std::vector<Ciphertext> keyswitch(Context& ctx, const std::vector<const u64*>& i
       outs.push_back(o);
     }
     moddown_conv(t, cl, zl, limbs, st);
-    ntt_forward(t, limbset(conv->ptr, 2 * R, (std::size_t)limbs * N, limbs, limbs, L), st);
-    moddown_finish(t, ol, al, cl, addl, limbs, st);
+    ntt_forward_epilogue(t, limbset(conv->ptr, 2 * R, (std::size_t)limbs * N, limbs, limbs, L),
+                         moddown_epilogue(t, ol, al, addl), st);
     ctx.stats.ntt_limbs += (std::size_t)R * 2 * (K + limbs);
   }
   return outs;
@@ -262,8 +290,8 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
       outs.push_back(o);
     }
     moddown_conv(t, cl, zl, limbs, st);
-    ntt_forward(t, limbset(conv->ptr, 2 * R, (std::size_t)limbs * N, limbs, limbs, L), st);
-    moddown_finish(t, ol, al, cl, addl, limbs, st);
+    ntt_forward_epilogue(t, limbset(conv->ptr, 2 * R, (std::size_t)limbs * N, limbs, limbs, L),
+                         moddown_epilogue(t, ol, al, addl), st);
     ctx.stats.ntt_limbs += (std::size_t)R * 2 * (K + limbs);
     r0 += R;
   }
@@ -341,27 +369,8 @@ std::vector<Ciphertext> rotate_sum_many(Context& ctx, const std::vector<std::vec
 // ---------------------------------------------------------------- rescale
 Ciphertext rescale(Context& ctx, const Ciphertext& a) {
   require_valid(a, "rescale");
-  const int l = a.limbs;
-  if (l < 2) throw Error(ErrKind::depth_exhausted, "rescale: no limb left to drop");
-  const DevTables& t = ctx.dev();
-  cudaStream_t st = ctx.stream();
-  const std::size_t N = ctx.N();
-  BufPtr last = ctx.alloc(2 * N);
-  FHEON_CUDA(cudaMemcpyAsync(last->ptr, a.c0 + (std::size_t)(l - 1) * N, N * sizeof(u64), cudaMemcpyDeviceToDevice, st));
-  FHEON_CUDA(cudaMemcpyAsync(last->ptr + N, a.c1 + (std::size_t)(l - 1) * N, N * sizeof(u64),
-                             cudaMemcpyDeviceToDevice, st));
-  ntt_inverse(t, limbset(last->ptr, 2, N, 1, 1, ctx.L(), l - 1), st);
-  BufPtr r = ctx.alloc(2 * (std::size_t)(l - 1) * N);
-  u64* r0 = r->ptr;
-  u64* r1 = r->ptr + (std::size_t)(l - 1) * N;
-  rescale_lift(t, plist({r0, r1}), plist({last->ptr, last->ptr + N}), l, st);
-  ntt_forward(t, limbset(r->ptr, 2, (std::size_t)(l - 1) * N, l - 1, l - 1, ctx.L()), st);
-  Ciphertext out = ctx.new_ct(l - 1);
-  rescale_finish(t, plist({out.c0, out.c1}), plist({a.c0, a.c1}), plist({r0, r1}), l, st);
-  out.scale = a.scale;
-  ctx.stats.rescales++;
-  ctx.stats.ntt_limbs += 2 + 2 * (std::size_t)(l - 1);
-  return out;
+  if (a.limbs < 2) throw Error(ErrKind::depth_exhausted, "rescale: no limb left to drop");
+  return rescale_many(ctx, {a})[0];
 }
 
 // -------------------------------------------------------------- level down
@@ -761,8 +770,8 @@ std::vector<Ciphertext> rescale_many(Context& ctx, const std::vector<Ciphertext>
       outs.push_back(o);
     }
     rescale_lift(t, rl, ll, l, st);
-    ntt_forward(t, limbset(rb->ptr, 2 * R, (std::size_t)(l - 1) * N, l - 1, l - 1, ctx.L()), st);
-    rescale_finish(t, ol, al, rl, l, st);
+    ntt_forward_epilogue(t, limbset(rb->ptr, 2 * R, (std::size_t)(l - 1) * N, l - 1, l - 1, ctx.L()),
+                         rescale_epilogue(t, ol, al, l), st);
     ctx.stats.rescales += R;
     ctx.stats.ntt_limbs += (std::size_t)R * 2 * l;
   }

@@ -72,6 +72,19 @@ struct PolyList {
 // `src` (optional, same shape and primes): out-of-place -- the first phase reads
 // src and writes `set`, the second phase runs in place on `set`.
 void ntt_forward(const DevTables& t, const LimbSet& set, cudaStream_t st, const LimbSet* src = nullptr);
+// Forward NTT whose store writes, instead of v = NTT(set) for limb-poly p, limb t:
+//   out[p][t] = (src[p][t] - v) * c_t + sigma_{add_g[p]}(add[p])[t]      (add[p] may be null)
+// with c_t = cst[t * cst_stride] (value, Shoup at +1): ModDown's (acc - conv) P^-1 + sigma(c0)
+// and rescale's (a - lift) q_l^-1 without a separate pass over the limbs.
+struct NttEpilogue {
+  u64* out[kMaxPolys];
+  const u64* src[kMaxPolys];
+  const u64* add[kMaxPolys];
+  u64 add_g[kMaxPolys];
+  const u64* cst;
+  int cst_stride;
+};
+void ntt_forward_epilogue(const DevTables& t, const LimbSet& set, const NttEpilogue& epi, cudaStream_t st);
 void ntt_inverse(const DevTables& t, const LimbSet& set, cudaStream_t st, const LimbSet* src = nullptr);
 
 // ---- elementwise over the polys of a list, `limbs` limbs each, primes 0..limbs-1

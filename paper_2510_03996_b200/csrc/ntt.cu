@@ -84,10 +84,20 @@ __device__ __forceinline__ void pass_shape(int gi, int tp, int& b, int& nst, int
   base = ((tp >> b) << (b + 3)) | (tp & ((1 << b) - 1));
 }
 
-template <int LOGM, bool INV, bool COL, bool SMALL>
+struct NoEpilogue {};
+template <bool EPI>
+struct EpiArg {
+  using type = NoEpilogue;
+};
+template <>
+struct EpiArg<true> {
+  using type = NttEpilogue;
+};
+
+template <int LOGM, bool INV, bool COL, bool SMALL, bool EPI = false>
 __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
     ntt_phase_kernel(LimbSet set, LimbSet src, bool has_src, const PrimeConst* __restrict__ pc,
-                     const u64* __restrict__ tw, int logN, int n1, int n2) {
+                     const u64* __restrict__ tw, int logN, int n1, int n2, typename EpiArg<EPI>::type epi) {
   using G = Geometry<LOGM, COL, SMALL>;
   constexpr int E = G::E, T = G::T, LPC = G::LPC, LS = G::LS, NG = G::NG;
   // the phase that runs first (forward COL / inverse ROW) reads canonical input and
@@ -200,6 +210,29 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
     }
     x[e] = v;
   }
+  if constexpr (EPI) {  // forward ROW phase: fused ModDown / rescale finish
+    const int per_base = set.blocks_per_base * set.E;
+    const int bb = blockIdx.y / per_base;
+    const int rr = blockIdx.y - bb * per_base;
+    const int blk = rr / set.E;
+    const int tl = rr - blk * set.E;  // Q limb
+    const int pi = bb * set.blocks_per_base + blk;
+    const std::size_t off = (std::size_t)tl << logN;
+    const u64* srcp = epi.src[pi] + off;
+    const u64* addp = epi.add[pi] ? epi.add[pi] + off : nullptr;
+    const u64 g = epi.add_g[pi];
+    const u64 c = __ldg(epi.cst + (std::size_t)tl * epi.cst_stride);
+    const u64 csh = __ldg(epi.cst + (std::size_t)tl * epi.cst_stride + 1);
+    u64* outp = epi.out[pi] + off;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = (int)gaddr(base | (e << b));  // element index within the limb-poly
+      u64 v = shoup_mul(sub_mod(srcp[k], x[e], q), c, csh, q);
+      if (addp) v = add_mod(v, addp[(g == 1) ? (unsigned)k : auto_src((unsigned)k, g, logN)], q);
+      outp[k] = v;
+    }
+    return;
+  }
   if (!COL && b == 0) {  // 8 consecutive words per thread: 16-byte stores
     ulonglong2* dst = reinterpret_cast<ulonglong2*>(data + gaddr(base));
 #pragma unroll
@@ -210,20 +243,21 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
   }
 }
 
-template <int LOGM, bool INV, bool COL, bool SMALL>
-void launch_phase_g(const DevTables& t, const LimbSet& set, const LimbSet* src, cudaStream_t st) {
+template <int LOGM, bool INV, bool COL, bool SMALL, bool EPI = false>
+void launch_phase_g(const DevTables& t, const LimbSet& set, const LimbSet* src, cudaStream_t st,
+                    const typename EpiArg<EPI>::type& epi = {}) {
   using G = Geometry<LOGM, COL, SMALL>;
   const std::size_t smem = (std::size_t)G::LPC * G::LS * sizeof(u64);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(ntt_phase_kernel<LOGM, INV, COL, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(ntt_phase_kernel<LOGM, INV, COL, SMALL, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr_set = true;
   }
   const int lines = COL ? (1 << t.n2) : (1 << t.n1);
   dim3 grid(lines / G::LPC, set.count());
-  ntt_phase_kernel<LOGM, INV, COL, SMALL><<<grid, G::THREADS, smem, st>>>(set, src ? *src : set, src != nullptr,
-                                                                           t.pc, t.tw, t.logN, t.n1, t.n2);
+  ntt_phase_kernel<LOGM, INV, COL, SMALL, EPI><<<grid, G::THREADS, smem, st>>>(
+      set, src ? *src : set, src != nullptr, t.pc, t.tw, t.logN, t.n1, t.n2, epi);
   launch_check("ntt_phase_kernel");
 }
 
@@ -269,6 +303,19 @@ void ntt_forward(const DevTables& t, const LimbSet& set, cudaStream_t st, const 
   TimedScope ts(t, kNtt, st);
   dispatch<false, true>(t, set, src, st);
   dispatch<false, false>(t, set, nullptr, st);
+}
+
+void ntt_forward_epilogue(const DevTables& t, const LimbSet& set, const NttEpilogue& epi, cudaStream_t st) {
+  if (set.count() == 0) return;
+  TimedScope ts(t, kNtt, st);
+  dispatch<false, true>(t, set, nullptr, st);
+  switch (t.n2) {  // ROW phase with the fused store (small tiles)
+    case 5: launch_phase_g<5, false, false, true, true>(t, set, nullptr, st, epi); break;
+    case 6: launch_phase_g<6, false, false, true, true>(t, set, nullptr, st, epi); break;
+    case 7: launch_phase_g<7, false, false, true, true>(t, set, nullptr, st, epi); break;
+    case 8: launch_phase_g<8, false, false, true, true>(t, set, nullptr, st, epi); break;
+    default: throw std::runtime_error("unsupported NTT split " + std::to_string(t.n2));
+  }
 }
 
 void ntt_inverse(const DevTables& t, const LimbSet& set, cudaStream_t st, const LimbSet* src) {
