@@ -226,6 +226,32 @@ std::vector<Ciphertext> strided_sum_many(Context& ctx, const std::vector<Ciphert
                                          std::size_t stride) {
   if (span <= 1 || xs.empty()) return xs;
   const std::size_t B = xs.size();
+  // Hoisted stages: sum_{i < n1 n2} rot(x, i s) = sum_{g < n2} rot(sum_{b < n1} rot(x, b s), g n1 s);
+  // each stage is ONE rotate-and-sum per input (one ModUp, one ModDown, n-1 inner
+  // products) instead of log2(n) full key switches.  Fan-in <= 8 per stage.
+  constexpr std::size_t kFan = 8;
+  std::vector<std::size_t> stages;
+  for (std::size_t rest = span; rest > 1;) {
+    std::size_t f = std::min(rest, kFan);
+    while (rest % f != 0) --f;
+    if (f == 1) break;  // no factor <= 8 (prime > 8): doubling tree below
+    stages.push_back(f);
+    rest /= f;
+  }
+  std::size_t covered = 1;
+  for (std::size_t f : stages) covered *= f;
+  if (covered == span) {
+    std::vector<Ciphertext> cur = xs;
+    std::size_t step = stride;
+    for (std::size_t f : stages) {
+      std::vector<RotTerms> groups(B);
+      for (std::size_t i = 0; i < B; ++i)
+        for (std::size_t b = 0; b < f; ++b) groups[i].push_back({cur[i], (long)(b * step)});
+      cur = sum_rotations(ctx, groups);
+      step *= f;
+    }
+    return cur;
+  }
   std::vector<std::vector<Ciphertext>> pw{xs};  // pw[k] = sum_{i < 2^k} rot(x, i * stride)
   std::size_t p = 1;
   while (p * 2 <= span) {
