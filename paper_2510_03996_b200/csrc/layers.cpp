@@ -916,8 +916,12 @@ Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std
   rows.reserve(m);
   for (std::size_t i = 0; i < m; ++i) rows.push_back(pt_of(ctx, x, plain(ctx, std::vector<double>(w + i * n, w + (i + 1) * n))));
   std::vector<Ciphertext> y = mp_many(ctx, std::vector<Ciphertext>(m, x), rows);
-  for (std::size_t off = 1; off < p2; off <<= 1)
-    y = add_many(ctx, y, rotate_many(ctx, y, std::vector<long>(m, (long)off)));
+  if (ctx.fast_schedule()) {
+    y = strided_sum_many(ctx, y, p2, 1);  // hoisted rotate-and-sum stages
+  } else {
+    for (std::size_t off = 1; off < p2; off <<= 1)
+      y = add_many(ctx, y, rotate_many(ctx, y, std::vector<long>(m, (long)off)));
+  }
   const BufPtr head = pt_of(ctx, y[0], range_mask(ctx, 0, 1));
   const bool defer = ctx.fast_schedule();
   std::vector<Ciphertext> neurons = mp_many(ctx, y, std::vector<BufPtr>(m, head), defer);
