@@ -129,13 +129,14 @@ __global__ void __launch_bounds__(256) k_modup_bconv(PolyList ext, PolyList x, c
   }
 }
 
-// grid (N/256, E, jobs)
+// grid (jobs, N/256, E): the job index varies fastest, so CTAs of jobs that share
+// a key (same-key batches) run together and reuse its slices from L2
 __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int logN, int limbs, int L, int K,
                            DigitOwner dig) {
   const std::size_t N = (std::size_t)1 << logN;
-  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = blockIdx.y;
-  const int r = blockIdx.z;
+  const unsigned n = blockIdx.y * blockDim.x + threadIdx.x;
+  const int t = blockIdx.z;
+  const int r = blockIdx.x;
   const int E = limbs + K;
   const int pt = t < limbs ? t : L + (t - limbs);
   const PrimeConst P = pc[pt];
@@ -163,10 +164,12 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
 // 128-bit accumulator never exceeds q * 2^64; job results add mod q.
 __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc, const u64* __restrict__ md_q,
                                int logN, int limbs, int L, int K, DigitOwner dig) {
+  // grid (groups, N/256, E): groups vary fastest -- the groups of a hoisted stage
+  // use the same key list, so their CTAs share each key slice through L2
   const std::size_t N = (std::size_t)1 << logN;
-  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = blockIdx.y;
-  const int r = blockIdx.z;
+  const unsigned n = blockIdx.y * blockDim.x + threadIdx.x;
+  const int t = blockIdx.z;
+  const int r = blockIdx.x;
   const int E = limbs + K;
   const int pt = t < limbs ? t : L + (t - limbs);
   const PrimeConst P = pc[pt];
@@ -484,14 +487,16 @@ void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int
 void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.n == 0) return;
   TimedScope ts(t, kKsInner, st);
-  k_ks_inner<<<grid_for(t.N, limbs + t.K, jobs.n), kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K,
+  const dim3 grid(jobs.n, (unsigned)(t.N / kThreads), limbs + t.K);
+  k_ks_inner<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K,
                                                                        DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner");
 }
 void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.ngroups == 0) return;
   TimedScope ts(t, kKsInner, st);
-  k_ks_inner_sum<<<grid_for(t.N, limbs + t.K, jobs.ngroups), kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs,
+  const dim3 grid(jobs.ngroups, (unsigned)(t.N / kThreads), limbs + t.K);
+  k_ks_inner_sum<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs,
                                                                                  t.L, t.K, DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner_sum");
 }

@@ -11,7 +11,8 @@ from paper_2510_03996_b200 import api
 from paper_2510_03996_b200 import model as M
 
 ring = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
-spec = M.resnet20(ring=ring, depth_budget=12)
+depth = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+spec = M.resnet20(ring=ring, depth_budget=depth)
 ctx = fh.SlotContext(M.ckks_config(spec, True))
 info = api.bootstrap_info(ctx)
 S = ring // 2
