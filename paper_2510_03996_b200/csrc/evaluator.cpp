@@ -237,33 +237,71 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
   BufPtr ext = modup_all(ctx, inputs, limbs);
   std::vector<std::vector<const SumJob*>> by_group(ngroups);
   for (const SumJob& j : jobs) by_group[j.group].push_back(&j);
+  // every group = one input under the same key list (a hoisted stage)?
+  bool shared = ngroups > 1 && !by_group[0].empty() && (int)by_group[0].size() <= kMaxSharedKeys;
+  for (int r = 0; r < ngroups && shared; ++r) {
+    shared = by_group[r].size() == by_group[0].size();
+    for (std::size_t k = 0; k < by_group[r].size() && shared; ++k)
+      shared = by_group[r][k]->g == by_group[0][k]->g && by_group[r][k]->in == by_group[r][0]->in;
+  }
   std::vector<Ciphertext> outs;
   outs.reserve(ngroups);
-  int r0 = 0;
-  while (r0 < ngroups) {
-    // pack whole groups into one launch (<= kMaxSumGroups groups, <= kMaxSumJobs jobs)
-    KsSumJobs kj{};
-    int nj = 0, R = 0;
-    while (r0 + R < ngroups && R < kMaxSumGroups) {
-      const int gsz = (int)by_group[r0 + R].size();
-      if (gsz > kMaxSumJobs) throw Error(ErrKind::internal, "rotate_sum: group larger than one launch");
-      if (nj + gsz > kMaxSumJobs) break;
-      kj.begin[R] = nj;
-      for (const SumJob* j : by_group[r0 + R]) {
-        kj.key[nj] = ctx.key(j->g);
-        kj.ext[nj] = ext->ptr + (std::size_t)j->in * ext_words;
-        kj.d[nj] = inputs[j->in];
-        kj.c0[nj] = c0s[j->in];
-        kj.g[nj] = j->g;
-        ++nj;
+  // accumulators of all groups, [2][limbs+K][N] each
+  BufPtr accs = ctx.alloc((std::size_t)ngroups * 2 * E * N);
+  auto acc_of = [&](int r) { return accs->ptr + (std::size_t)r * 2 * E * N; };
+  if (shared) {
+    for (int r0 = 0; r0 < ngroups; r0 += kMaxSharedGroups) {
+      KsSharedJobs kj{};
+      kj.nkeys = (int)by_group[0].size();
+      for (int k = 0; k < kj.nkeys; ++k) {
+        kj.key[k] = ctx.key(by_group[0][k]->g);
+        kj.g[k] = by_group[0][k]->g;
       }
-      ++R;
+      kj.ngroups = std::min(kMaxSharedGroups, ngroups - r0);
+      for (int r = 0; r < kj.ngroups; ++r) {
+        const int in = by_group[r0 + r][0]->in;
+        kj.ext[r] = ext->ptr + (std::size_t)in * ext_words;
+        kj.d[r] = inputs[in];
+        kj.c0[r] = c0s[in];
+        kj.acc[r] = acc_of(r0 + r);
+      }
+      ks_inner_shared(t, kj, limbs, st);
     }
-    kj.begin[R] = nj;
-    kj.ngroups = R;
-    BufPtr acc = ctx.alloc((std::size_t)R * 2 * E * N);
-    for (int r = 0; r < R; ++r) kj.acc[r] = acc->ptr + (std::size_t)r * 2 * E * N;
-    ks_inner_sum(t, kj, limbs, st);
+  } else {
+    int r0 = 0;
+    while (r0 < ngroups) {
+      // pack whole groups into one launch (<= kMaxSumGroups groups, <= kMaxSumJobs jobs)
+      KsSumJobs kj{};
+      int nj = 0, R = 0;
+      while (r0 + R < ngroups && R < kMaxSumGroups) {
+        const int gsz = (int)by_group[r0 + R].size();
+        if (gsz > kMaxSumJobs) throw Error(ErrKind::internal, "rotate_sum: group larger than one launch");
+        if (nj + gsz > kMaxSumJobs) break;
+        kj.begin[R] = nj;
+        for (const SumJob* j : by_group[r0 + R]) {
+          kj.key[nj] = ctx.key(j->g);
+          kj.ext[nj] = ext->ptr + (std::size_t)j->in * ext_words;
+          kj.d[nj] = inputs[j->in];
+          kj.c0[nj] = c0s[j->in];
+          kj.g[nj] = j->g;
+          ++nj;
+        }
+        ++R;
+      }
+      kj.begin[R] = nj;
+      kj.ngroups = R;
+      for (int r = 0; r < R; ++r) kj.acc[r] = acc_of(r0 + r);
+      ks_inner_sum(t, kj, limbs, st);
+      r0 += R;
+    }
+  }
+  // ModDown of every group's accumulator, 32 groups (64 polys) per pipeline
+  for (int r0 = 0; r0 < ngroups; r0 += kMaxPolys / 2) {
+    const int R = std::min(kMaxPolys / 2, ngroups - r0);
+    struct {
+      u64* acc[kMaxPolys / 2];
+    } kj{};
+    for (int r = 0; r < R; ++r) kj.acc[r] = acc_of(r0 + r);
     LimbSet zs{};
     zs.nbase = R;
     for (int r = 0; r < R; ++r) zs.base[r] = kj.acc[r] + (std::size_t)limbs * N;
@@ -293,7 +331,6 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
     ntt_forward_epilogue(t, limbset(conv->ptr, 2 * R, (std::size_t)limbs * N, limbs, limbs, L),
                          moddown_epilogue(t, ol, al, addl), st);
     ctx.stats.ntt_limbs += (std::size_t)R * 2 * (K + limbs);
-    r0 += R;
   }
   return outs;
 }

@@ -150,6 +150,23 @@ struct KsSumJobs {
   int ngroups;
 };
 void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st);
+// Hoisted rotate-and-sum over many inputs sharing ONE key list (channel sums, FC
+// folds): acc_r = sum_j sigma_{g_j}(ext_r) key_j (+ P sigma_{g_j}(c0_r)); CTAs of
+// all groups walk the same keys together (grid: groups fastest), so each key
+// slice is read from HBM once per launch instead of once per group.
+constexpr int kMaxSharedKeys = 16;
+constexpr int kMaxSharedGroups = 40;
+struct KsSharedJobs {
+  const u64* key[kMaxSharedKeys];
+  u64 g[kMaxSharedKeys];
+  int nkeys;
+  const u64* ext[kMaxSharedGroups];
+  const u64* d[kMaxSharedGroups];
+  const u64* c0[kMaxSharedGroups];
+  u64* acc[kMaxSharedGroups];
+  int ngroups;
+};
+void ks_inner_shared(const DevTables& t, const KsSharedJobs& jobs, int limbs, cudaStream_t st);
 // ModDown front half: z[p] = coefficient-domain P limbs ([K][N], prime L+k);
 // conv[p] ([limbs][N]) = centred P-residue lifted to q_0..q_{limbs-1}
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);

@@ -199,6 +199,43 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
   acc[((std::size_t)E + t) * N + n] = s1;
 }
 
+// grid (groups, N/256, E): groups fastest (every group uses the same keys)
+__global__ void k_ks_inner_shared(KsSharedJobs jobs, const PrimeConst* __restrict__ pc,
+                                  const u64* __restrict__ md_q, int logN, int limbs, int L, int K, DigitOwner dig) {
+  const std::size_t N = (std::size_t)1 << logN;
+  const unsigned n = blockIdx.y * blockDim.x + threadIdx.x;
+  const int t = blockIdx.z;
+  const int r = blockIdx.x;
+  const int E = limbs + K;
+  const int pt = t < limbs ? t : L + (t - limbs);
+  const PrimeConst P = pc[pt];
+  const int beta = dig.beta;
+  const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;
+  const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;
+  const u64* ext = jobs.ext[r];
+  const u64* d = jobs.d[r];
+  const u64* c0 = jobs.c0[r];
+  u64 s0 = 0, s1 = 0;
+  for (int jb = 0; jb < jobs.nkeys; ++jb) {
+    const u64 g = jobs.g[jb];
+    const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
+    const u64* key = jobs.key[jb];
+    Acc128 a0, a1;
+    for (int j = 0; j < beta; ++j) {
+      const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+      const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
+      a0.mac(v, kj[n]);
+      a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
+    }
+    if (t < limbs) a0.mac(c0[(std::size_t)t * N + src], pm);
+    s0 = csub(s0 + redc(a0.hi, a0.lo, P.q, P.qinv_neg), P.q);
+    s1 = csub(s1 + redc(a1.hi, a1.lo, P.q, P.qinv_neg), P.q);
+  }
+  u64* acc = jobs.acc[r];
+  acc[(std::size_t)t * N + n] = s0;
+  acc[((std::size_t)E + t) * N + n] = s1;
+}
+
 // ModDown conversion with KK = K special limbs (compile time).
 // grid (N/256, ceil(limbs / kTC), npolys); the chunk's constants sit in smem.
 template <int KK>
@@ -499,6 +536,14 @@ void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStre
   k_ks_inner_sum<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs,
                                                                                  t.L, t.K, DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner_sum");
+}
+void ks_inner_shared(const DevTables& t, const KsSharedJobs& jobs, int limbs, cudaStream_t st) {
+  if (jobs.ngroups == 0) return;
+  TimedScope ts(t, kKsInner, st);
+  const dim3 grid(jobs.ngroups, (unsigned)(t.N / kThreads), limbs + t.K);
+  k_ks_inner_shared<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs, t.L, t.K,
+                                               DigitOwner{t.digit_owner, t.dig.beta(limbs)});
+  launch_check("k_ks_inner_shared");
 }
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
   if (conv.n == 0) return;
