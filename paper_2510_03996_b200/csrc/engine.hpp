@@ -260,7 +260,6 @@ Ciphertext encrypt_top(Context& ctx, const double* vals, std::size_t n);        
 void decrypt(Context& ctx, const Ciphertext& ct, double* out, double* out_im = nullptr);  // S slots
 Ciphertext rotate(Context& ctx, const Ciphertext& x, long t);
 std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& ts);
-std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t);
 // xs[i] rotated by ts[i]: one batched key-switch pipeline, shared ModUp for repeated inputs
 std::vector<Ciphertext> rotate_many(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<long>& ts);
 // out[r] = sum_k rot(x_rk, t_rk): rotate-and-sum, one ModDown per output (the

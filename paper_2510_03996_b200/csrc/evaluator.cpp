@@ -557,10 +557,6 @@ std::vector<Ciphertext> rotate_hoisted(Context& ctx, const Ciphertext& x, const 
   return rotate_many(ctx, std::vector<Ciphertext>(ts.size(), x), ts);
 }
 
-std::vector<Ciphertext> rotate_same(Context& ctx, const std::vector<Ciphertext>& xs, long t) {
-  return rotate_many(ctx, xs, std::vector<long>(xs.size(), t));
-}
-
 // complex conjugation of the slots: automorphism X -> X^{2N-1} + key switch
 std::vector<Ciphertext> conjugate_many(Context& ctx, const std::vector<Ciphertext>& xs) {
   const u64 g = 2 * (u64)ctx.N() - 1;

@@ -170,14 +170,10 @@ void ks_inner_shared(const DevTables& t, const KsSharedJobs& jobs, int limbs, cu
 // ModDown front half: z[p] = coefficient-domain P limbs ([K][N], prime L+k);
 // conv[p] ([limbs][N]) = centred P-residue lifted to q_0..q_{limbs-1}
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);
-// out[p] = (acc[p] - conv[p]) * P^{-1} + sigma_{add.g[p]}(add[p])   (add[p] may be null)
-void moddown_finish(const DevTables& t, const PolyList& out, const PolyList& acc, const PolyList& conv,
-                    const PolyList& add, int limbs, cudaStream_t st);
-// Rescale: last[p] coefficient-domain limb (limbs-1); r[p] ([limbs-1][N]) centred lift
+// (ModDown's back half (acc - conv) P^{-1} + sigma(add) runs in ntt_forward_epilogue.)
+// Rescale: last[p] coefficient-domain limb (limbs-1); r[p] ([limbs-1][N]) centred lift;
+// the back half (a - r) q_{limbs-1}^{-1} runs in ntt_forward_epilogue
 void rescale_lift(const DevTables& t, const PolyList& r, const PolyList& last, int limbs, cudaStream_t st);
-// out[p] = (a[p] - r[p]) * q_{limbs-1}^{-1}, limbs-1 limbs
-void rescale_finish(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& r, int limbs,
-                    cudaStream_t st);
 
 // ---- fused layer kernels
 // Multiply-accumulate of plaintext diagonals: for each output o,

@@ -43,6 +43,9 @@ namespace {
 #ifndef FHEON_NTT_ROW_THREADS
 #define FHEON_NTT_ROW_THREADS 256
 #endif
+#ifndef FHEON_NTT_RB
+#define FHEON_NTT_RB 3  // radix-2 stages per register pass (E = 2^RB elements per thread)
+#endif
 #ifndef FHEON_NTT_SMALL_CTAS
 #define FHEON_NTT_SMALL_CTAS 600
 #endif
@@ -57,31 +60,33 @@ __device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) { return
 template <int LOGM, bool COL, bool SMALL>
 struct Geometry {
   static constexpr int M = 1 << LOGM;
-  static constexpr int E = 8;        // elements per thread
+  static constexpr int E = 1 << FHEON_NTT_RB;  // elements per thread
   static constexpr int T = M / E;    // threads per line
   static constexpr int ROW_THREADS = SMALL ? FHEON_NTT_ROW_THREADS / 4 : FHEON_NTT_ROW_THREADS;
   static constexpr int ROWL = (ROW_THREADS / T) < 1 ? 1 : ((ROW_THREADS / T) < 32 ? (ROW_THREADS / T) : 32);
   static constexpr int LPC = COL ? (SMALL ? FHEON_NTT_COL_LINES / 4 : FHEON_NTT_COL_LINES) : ROWL;  // lines per CTA
   static constexpr int THREADS = LPC * T;
   static constexpr int LS = M + M / 8 + 1;  // padded line stride (words)
-  static constexpr int NG = (LOGM + 2) / 3;  // register passes
+  static constexpr int NG = (LOGM + FHEON_NTT_RB - 1) / FHEON_NTT_RB;  // register passes
 };
 
 // element positions of pass gi: idx(e) = base | (e << b)
 template <int LOGM, bool INV>
 __device__ __forceinline__ void pass_shape(int gi, int tp, int& b, int& nst, int& hb0, int& base) {
   if (!INV) {
-    const int top = LOGM - 1 - 3 * gi;
-    nst = top + 1 < 3 ? top + 1 : 3;
-    b = top - 2 > 0 ? top - 2 : 0;
+    constexpr int RB = FHEON_NTT_RB;
+    const int top = LOGM - 1 - RB * gi;
+    nst = top + 1 < RB ? top + 1 : RB;
+    b = top - (RB - 1) > 0 ? top - (RB - 1) : 0;
     hb0 = top;
   } else {
-    const int low = 3 * gi;
-    nst = LOGM - low < 3 ? LOGM - low : 3;
-    b = low < LOGM - 3 ? low : LOGM - 3;
+    constexpr int RB = FHEON_NTT_RB;
+    const int low = RB * gi;
+    nst = LOGM - low < RB ? LOGM - low : RB;
+    b = low < LOGM - RB ? low : LOGM - RB;
     hb0 = low;
   }
-  base = ((tp >> b) << (b + 3)) | (tp & ((1 << b) - 1));
+  base = ((tp >> b) << (b + FHEON_NTT_RB)) | (tp & ((1 << b) - 1));
 }
 
 struct NoEpilogue {};
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
       for (int e = 0; e < E; ++e) x[e] = lsm[pad8(base | (e << b))];
     }
 #pragma unroll
-    for (int st = 0; st < 3; ++st) {
+    for (int st = 0; st < FHEON_NTT_RB; ++st) {
       if (st < nst) {
         const int hb = INV ? hb0 + st : hb0 - st;
         const int eb = hb - b;

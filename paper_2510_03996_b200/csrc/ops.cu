@@ -285,24 +285,6 @@ __global__ void __launch_bounds__(256) k_moddown_conv(PolyList conv, PolyList z,
   }
 }
 
-// grid (N/256, limbs, npolys)
-__global__ void k_moddown_finish(PolyList out, PolyList acc, PolyList conv, PolyList add,
-                                 const PrimeConst* __restrict__ pc, const u64* __restrict__ md_q, int logN) {
-  const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
-  const int p = blockIdx.z;
-  const std::size_t o = ((std::size_t)i << logN) + n;
-  const u64 q = pc[i].q;
-  const u64* mq = md_q + (std::size_t)i * 4;
-  u64 v = shoup_mul(sub_mod(acc.p[p][o], conv.p[p][o], q), mq[2], mq[3], q);
-  if (add.p[p]) {
-    const u64 g = add.g[p];
-    const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
-    v = add_mod(v, add.p[p][((std::size_t)i << logN) + src], q);
-  }
-  out.p[p][o] = v;
-}
-
 // grid (N/256, npolys)
 __global__ void k_rescale_lift(PolyList r, PolyList last, const PrimeConst* __restrict__ pc,
                                const u64* __restrict__ rs, int logN, int limbs, int L) {
@@ -319,17 +301,6 @@ __global__ void k_rescale_lift(PolyList r, PolyList last, const PrimeConst* __re
     if (neg) x = sub_mod(x, rs[((std::size_t)l * L + i) * 4 + 2], P.q);
     out[(std::size_t)i * N + n] = x;
   }
-}
-
-// grid (N/256, limbs-1, npolys)
-__global__ void k_rescale_finish(PolyList out, PolyList a, PolyList r, const PrimeConst* __restrict__ pc,
-                                 const u64* __restrict__ rs, int logN, int limbs, int L) {
-  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
-  const int l = limbs - 1;
-  const u64 q = pc[i].q;
-  const u64* c = rs + ((std::size_t)l * L + i) * 4;
-  out.p[blockIdx.z][o] = shoup_mul(sub_mod(a.p[blockIdx.z][o], r.p[blockIdx.z][o], q), c[0], c[1], q);
 }
 
 // ------------------------------------------------------------ fused layer kernels
@@ -562,22 +533,10 @@ void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, i
 #undef FHEON_MDC
   launch_check("k_moddown_conv");
 }
-void moddown_finish(const DevTables& t, const PolyList& out, const PolyList& acc, const PolyList& conv,
-                    const PolyList& add, int limbs, cudaStream_t st) {
-  if (out.n == 0) return;
-  k_moddown_finish<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, acc, conv, add, t.pc, t.md_q, t.logN);
-  launch_check("k_moddown_finish");
-}
 void rescale_lift(const DevTables& t, const PolyList& r, const PolyList& last, int limbs, cudaStream_t st) {
   if (r.n == 0) return;
   k_rescale_lift<<<grid_for(t.N, 1, r.n), kThreads, 0, st>>>(r, last, t.pc, t.rs, t.logN, limbs, t.L);
   launch_check("k_rescale_lift");
-}
-void rescale_finish(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& r, int limbs,
-                    cudaStream_t st) {
-  if (out.n == 0) return;
-  k_rescale_finish<<<grid_for(t.N, limbs - 1, out.n), kThreads, 0, st>>>(out, a, r, t.pc, t.rs, t.logN, limbs, t.L);
-  launch_check("k_rescale_finish");
 }
 
 void modraise(const DevTables& t, const PolyList& out, const PolyList& in, int L, cudaStream_t st) {
