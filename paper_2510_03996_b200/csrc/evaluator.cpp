@@ -1017,8 +1017,17 @@ Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const 
       kc[(i * l + t) * 2 + 1] = shoup(v, h.q[t]);
     }
   }
+  // through a pinned staging slot: a pageable copy would serialise host and stream
+  if (kc.size() * sizeof(u64) > ctx.N() * sizeof(long long))
+    throw Error(ErrKind::capacity, "lincomb_const: constant table exceeds a staging slot");
   BufPtr kd = ctx.alloc(kc.size());
-  FHEON_CUDA(cudaMemcpyAsync(kd->ptr, kc.data(), kc.size() * sizeof(u64), cudaMemcpyHostToDevice, ctx.stream()));
+  {
+    cudaEvent_t* ev = nullptr;
+    long long* stage = ctx.staging_slot(&ev);
+    std::memcpy(stage, kc.data(), kc.size() * sizeof(u64));
+    FHEON_CUDA(cudaMemcpyAsync(kd->ptr, stage, kc.size() * sizeof(u64), cudaMemcpyHostToDevice, ctx.stream()));
+    FHEON_CUDA(cudaEventRecord(*ev, ctx.stream()));
+  }
   Ciphertext sum = ctx.new_ct(l);
   sum.scale = t_out * (double)h.q[l - 1];
   for (std::size_t i0 = 0; i0 < n; i0 += kMaxLincomb) {
