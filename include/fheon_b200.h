@@ -127,6 +127,12 @@ int fheon_ctx_set_weight_cache(fheon_ctx* ctx, uint64_t bytes);
 /* raw RNS words, layout [2][limbs][N] */
 int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* words, int limbs, double scale, fheon_ct** out);
 int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);
+/* non-blocking transfers on the context's copy streams (host buffers pinned and kept
+ * valid until fheon_ctx_wait_transfers): uploads of the next batch, compute of this
+ * one and downloads of the previous one overlap */
+int fheon_ct_upload_async(fheon_ctx* ctx, const uint64_t* words, int limbs, double scale, fheon_ct** out);
+int fheon_ct_download_async(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);
+int fheon_ctx_wait_transfers(fheon_ctx* ctx);
 
 /* ---- backend ops (backend.hpp:134-153) */
 int fheon_rotate(fheon_ctx* ctx, const fheon_ct* x, long t, fheon_ct** out);

@@ -267,6 +267,10 @@ class SlotContext:
             raise ShapeError(f'schedule must be one of {sorted(SCHEDULES)}, got "{schedule}"', 2)
         _check(_native.lib().fheon_ctx_set_schedule(self._h, SCHEDULES[schedule]))
 
+    def wait_transfers(self):
+        """Block until every asynchronous upload / download has completed."""
+        _check(_native.lib().fheon_ctx_wait_transfers(self._h))
+
     def set_weight_cache(self, nbytes: int):
         """HBM budget of resident weight plaintexts (weight_mode "preload"); 0 = "lazy"."""
         _check(_native.lib().fheon_ctx_set_weight_cache(self._h, int(nbytes)))
@@ -388,10 +392,19 @@ class SlotVector:
         return SlotVector(ctx, h)
 
     @staticmethod
-    def from_words(ctx: SlotContext, words: np.ndarray, scale: float) -> "SlotVector":
-        w = np.ascontiguousarray(words, np.uint64)
+    def from_words(ctx: SlotContext, words: np.ndarray, scale: float, async_copy: bool = False) -> "SlotVector":
+        """Upload raw RNS words [2][limbs][N].  async_copy: non-blocking copy on the
+        context's upload stream -- `words` must be a contiguous uint64 array (pinned
+        for overlap) that stays valid until SlotContext.wait_transfers()."""
+        if async_copy:
+            if words.dtype != np.uint64 or not words.flags.c_contiguous:
+                raise ShapeError("async upload needs a contiguous uint64 array", 2)
+            w = words
+        else:
+            w = np.ascontiguousarray(words, np.uint64)
         h = C.c_void_p()
-        _check(_native.lib().fheon_ct_upload(ctx._h, _u64ptr(w), w.shape[1], float(scale), C.byref(h)))
+        fn = _native.lib().fheon_ct_upload_async if async_copy else _native.lib().fheon_ct_upload
+        _check(fn(ctx._h, _u64ptr(w), w.shape[1], float(scale), C.byref(h)))
         return SlotVector(ctx, h)
 
     def valid(self) -> bool:
@@ -424,13 +437,18 @@ class SlotVector:
         _check(_native.lib().fheon_decrypt_complex(self._ctx._h, self._h, _dptr(re), _dptr(im), re.size))
         return re + 1j * im
 
-    def words(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+    def words(self, out: Optional[np.ndarray] = None, async_copy: bool = False) -> np.ndarray:
+        """Download raw RNS words.  async_copy: returns at once; `out` is filled on the
+        context's download stream and is valid after SlotContext.wait_transfers()."""
         shape = (2, self.limbs(), self._ctx.N)
         if out is None:
+            if async_copy:
+                raise ShapeError("async download needs a caller-owned output buffer", 2)
             out = np.zeros(shape, np.uint64)
         elif out.shape != shape or out.dtype != np.uint64 or not out.flags.c_contiguous:
             raise ShapeError(f"output buffer must be a contiguous uint64 array of shape {shape}", 2)
-        _check(_native.lib().fheon_ct_download(self._ctx._h, self._h, _u64ptr(out)))
+        fn = _native.lib().fheon_ct_download_async if async_copy else _native.lib().fheon_ct_download
+        _check(fn(self._ctx._h, self._h, _u64ptr(out)))
         return out
 
 

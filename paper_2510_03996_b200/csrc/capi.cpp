@@ -144,7 +144,10 @@ int fheon_ctx_info(const fheon_ctx* ctx, uint64_t* primes, double* scales, int* 
 void* fheon_ctx_stream(fheon_ctx* ctx) { return ctx ? static_cast<void*>(ctx->impl->stream()) : nullptr; }
 
 int fheon_ctx_sync(fheon_ctx* ctx) {
-  return guard([&] { FHEON_CUDA(cudaStreamSynchronize(ctx->impl->stream())); });
+  return guard([&] {
+    FHEON_CUDA(cudaStreamSynchronize(ctx->impl->stream()));
+    fheon::wait_transfers(*ctx->impl);
+  });
 }
 
 int fheon_ctx_stats(const fheon_ctx* ctx, uint64_t* o) {
@@ -277,6 +280,21 @@ int fheon_ct_upload(fheon_ctx* ctx, const uint64_t* w, int limbs, double scale, 
 }
 int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* w) {
   return guard([&] { fheon::download_ct(*ctx->impl, ct->ct, w); });
+}
+int fheon_ct_upload_async(fheon_ctx* ctx, const uint64_t* w, int limbs, double scale, fheon_ct** out) {
+  return guard([&] {
+    if (limbs < 1 || limbs > ctx->impl->L()) throw fheon::Error(fheon::ErrKind::shape, "upload: bad limb count");
+    *out = wrap(fheon::upload_ct_async(*ctx->impl, w, limbs, scale));
+  });
+}
+int fheon_ct_download_async(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* w) {
+  return guard([&] {
+    need(ct, "ciphertext");
+    fheon::download_ct_async(*ctx->impl, ct->ct, w);
+  });
+}
+int fheon_ctx_wait_transfers(fheon_ctx* ctx) {
+  return guard([&] { fheon::wait_transfers(*ctx->impl); });
 }
 
 int fheon_rotate(fheon_ctx* ctx, const fheon_ct* x, long t, fheon_ct** out) {

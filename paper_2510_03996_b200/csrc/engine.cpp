@@ -91,7 +91,46 @@ DevBuffer::~DevBuffer() {
   else cudaFree(ptr);
 }
 
+DevBuffer::DevBuffer(Context* c, std::size_t w, cudaStream_t alloc_stream)
+    : alive(c->alive), stream(c->stream()), words(w) {
+  if (w == 0) return;
+  FHEON_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), alloc_stream));
+}
+
 BufPtr Context::alloc(std::size_t words) { return std::make_shared<DevBuffer>(this, words); }
+
+cudaEvent_t Context::take_event() {
+  if (!event_pool_.empty()) {
+    cudaEvent_t e = event_pool_.back();
+    event_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  FHEON_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return e;
+}
+
+void Context::give_event(cudaEvent_t e) { event_pool_.push_back(e); }
+
+void Context::hold_until(cudaEvent_t done, BufPtr buf) {
+  reap_transfers(false);
+  held_.emplace_back(done, std::move(buf));
+}
+
+void Context::reap_transfers(bool wait) {
+  std::size_t k = 0;
+  for (auto& [e, b] : held_) {
+    if (wait) FHEON_CUDA(cudaEventSynchronize(e));
+    if (wait || cudaEventQuery(e) == cudaSuccess) {
+      give_event(e);
+      b.reset();
+    } else {
+      held_[k++] = {e, std::move(b)};
+    }
+  }
+  held_.resize(k);
+  cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error
+}
 
 Ciphertext Context::new_ct(int limbs) {
   Ciphertext c;
@@ -158,6 +197,8 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
   int dev = 0;
   FHEON_CUDA(cudaGetDevice(&dev));
   FHEON_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  FHEON_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+  FHEON_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   {
     cudaMemPool_t pool;
     FHEON_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -206,6 +247,13 @@ Context::~Context() {
     if (staging_[i]) cudaFreeHost(staging_[i]);
     if (staging_ev_[i]) cudaEventDestroy(staging_ev_[i]);
   }
+  if (h2d_) cudaStreamSynchronize(h2d_);
+  if (d2h_) cudaStreamSynchronize(d2h_);
+  for (auto& [e, b] : held_) cudaEventDestroy(e);
+  held_.clear();
+  for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 

@@ -67,6 +67,8 @@ struct DevBuffer {
   u64* ptr = nullptr;
   std::size_t words = 0;
   DevBuffer(Context* c, std::size_t w);
+  // allocated in `alloc_stream`'s order (e.g. the upload stream), freed in the context stream's
+  DevBuffer(Context* c, std::size_t w, cudaStream_t alloc_stream);
   ~DevBuffer();
   DevBuffer(const DevBuffer&) = delete;
   DevBuffer& operator=(const DevBuffer&) = delete;
@@ -187,12 +189,26 @@ class Context {
   // staging for host -> device copies of encoded coefficients
   long long* staging_slot(cudaEvent_t** ev);
 
+  // ---- asynchronous ciphertext transfers on dedicated copy streams (the
+  // host -> device copy of the next batch, the compute of this one and the
+  // device -> host copy of the previous one overlap)
+  cudaStream_t h2d_stream() const { return h2d_; }
+  cudaStream_t d2h_stream() const { return d2h_; }
+  cudaEvent_t take_event();
+  void give_event(cudaEvent_t e);
+  // keep `buf` alive until `done` has completed (a device -> host copy in flight)
+  void hold_until(cudaEvent_t done, BufPtr buf);
+  void reap_transfers(bool wait);  // release finished (or, with wait, all) held buffers
+
  private:
   void build_device_tables();
 
   HostTables ht_;
   DevTables dt_{};
   cudaStream_t stream_ = nullptr;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  std::vector<cudaEvent_t> event_pool_;
+  std::vector<std::pair<cudaEvent_t, BufPtr>> held_;
   int depth_budget_ = 0;
   std::uint64_t id_counter_ = 0;
   std::vector<void*> dev_allocs_;  // table allocations
@@ -283,5 +299,11 @@ Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d_as_c1, u64 key_id, u6
 // device <-> host for parity tests
 Ciphertext upload_ct(Context& ctx, const u64* host, int limbs, double scale);
 void download_ct(Context& ctx, const Ciphertext& ct, u64* host);
+// non-blocking variants (host buffers must stay valid -- and should be pinned --
+// until wait_transfers): the upload runs on the H2D stream and the context stream
+// waits for it; the download waits for the context stream and runs on the D2H stream
+Ciphertext upload_ct_async(Context& ctx, const u64* host, int limbs, double scale);
+void download_ct_async(Context& ctx, const Ciphertext& ct, u64* host);
+void wait_transfers(Context& ctx);
 
 }  // namespace fheon

@@ -1104,6 +1104,42 @@ Ciphertext upload_ct(Context& ctx, const u64* host, int limbs, double scale) {
   return ct;
 }
 
+Ciphertext upload_ct_async(Context& ctx, const u64* host, int limbs, double scale) {
+  const std::size_t words = 2 * (std::size_t)limbs * ctx.N();
+  Ciphertext ct;
+  ct.buf = std::make_shared<DevBuffer>(&ctx, words, ctx.h2d_stream());
+  ct.c0 = ct.buf->ptr;
+  ct.c1 = ct.buf->ptr + (std::size_t)limbs * ctx.N();
+  ct.limbs = limbs;
+  ct.id = ctx.next_id();
+  ct.scale = scale;
+  FHEON_CUDA(cudaMemcpyAsync(ct.c0, host, words * sizeof(u64), cudaMemcpyHostToDevice, ctx.h2d_stream()));
+  cudaEvent_t up = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(up, ctx.h2d_stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.stream(), up, 0));  // compute on it after the copy lands
+  ctx.give_event(up);  // safe: a recorded event may be re-recorded once waited on
+  return ct;
+}
+
+void download_ct_async(Context& ctx, const Ciphertext& ct, u64* host) {
+  const std::size_t LN = (std::size_t)ct.limbs * ctx.N();
+  cudaEvent_t ready = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(ready, ctx.stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.d2h_stream(), ready, 0));
+  ctx.give_event(ready);
+  FHEON_CUDA(cudaMemcpyAsync(host, ct.c0, LN * sizeof(u64), cudaMemcpyDeviceToHost, ctx.d2h_stream()));
+  FHEON_CUDA(cudaMemcpyAsync(host + LN, ct.c1, LN * sizeof(u64), cudaMemcpyDeviceToHost, ctx.d2h_stream()));
+  cudaEvent_t done = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(done, ctx.d2h_stream()));
+  ctx.hold_until(done, ct.buf);  // the buffer outlives the copy
+}
+
+void wait_transfers(Context& ctx) {
+  FHEON_CUDA(cudaStreamSynchronize(ctx.h2d_stream()));
+  FHEON_CUDA(cudaStreamSynchronize(ctx.d2h_stream()));
+  ctx.reap_transfers(true);
+}
+
 void download_ct(Context& ctx, const Ciphertext& ct, u64* host) {
   const std::size_t LN = (std::size_t)ct.limbs * ctx.N();
   FHEON_CUDA(cudaMemcpyAsync(host, ct.c0, LN * sizeof(u64), cudaMemcpyDeviceToHost, ctx.stream()));

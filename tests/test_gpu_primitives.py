@@ -323,3 +323,20 @@ def test_balanced_digits_keyswitch_bit_exact(L, t):
     want = orc.rotate_sum([ct, ct], [t, 1], [orc.rotation_key(t), orc.rotation_key(1)])
     assert np.array_equal(y.words(), want)
 
+
+
+def test_async_transfers_bit_exact(small):
+    """Asynchronous copy streams: uploads / downloads of several ciphertexts
+    overlapping compute give the same words as the blocking path."""
+    ctx, orc = small
+    rng = np.random.default_rng(77)
+    cts = [_oracle_ct(orc, rng, counter=60 + i)[1] for i in range(4)]
+    outs = [np.zeros_like(c) for c in cts]
+    for rep in range(2):
+        xs = [fh.SlotVector.from_words(ctx, c, orc.T[-1], async_copy=True) for c in cts]
+        ys = fh.rotate_many(xs, [1, 3, -2, 5])
+        for y, o in zip(ys, outs):
+            y.words(out=o, async_copy=True)
+        ctx.wait_transfers()
+        for c, t, o in zip(cts, [1, 3, -2, 5], outs):
+            assert np.array_equal(o, orc.rotate(c, t, orc.rotation_key(t)))
