@@ -89,6 +89,69 @@ __device__ __forceinline__ void pass_shape(int gi, int tp, int& b, int& nst, int
   base = ((tp >> b) << (b + FHEON_NTT_RB)) | (tp & ((1 << b) - 1));
 }
 
+// All register passes of one phase on E elements per thread: x holds pass 0's
+// layout on entry and the last pass's on exit (b, base describe it); re-layouts
+// go through the thread's line in shared memory (`lsm`).  SYNC: 1 = the line's
+// threads are one warp (__syncwarp), 2 = they span warps (__syncthreads).
+// row = -1 for column lines (twiddles independent of the line), else the row.
+template <int LOGM, bool INV, int SYNC>
+__device__ __forceinline__ void run_passes(u64 (&x)[1 << FHEON_NTT_RB], int tp, int row, u64* lsm,
+                                           const ulonglong2* __restrict__ twp, u64 q, int n1, int& b, int& nst,
+                                           int& hb0, int& base) {
+  constexpr int E = 1 << FHEON_NTT_RB;
+  constexpr int NG = (LOGM + FHEON_NTT_RB - 1) / FHEON_NTT_RB;
+  const u64 q2 = 2 * q;
+  pass_shape<LOGM, INV>(0, tp, b, nst, hb0, base);
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    if (gi > 0) {  // re-layout through shared memory
+      int pb, pn, ph, pbase;
+      pass_shape<LOGM, INV>(gi - 1, tp, pb, pn, ph, pbase);
+#pragma unroll
+      for (int e = 0; e < E; ++e) lsm[pad8(pbase | (e << pb))] = x[e];
+      if (SYNC == 2) __syncthreads();
+      else __syncwarp();
+      pass_shape<LOGM, INV>(gi, tp, b, nst, hb0, base);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = lsm[pad8(base | (e << b))];
+    }
+#pragma unroll
+    for (int st = 0; st < FHEON_NTT_RB; ++st) {
+      if (st < nst) {
+        const int hb = INV ? hb0 + st : hb0 - st;
+        const int eb = hb - b;
+        const int s = LOGM - 1 - hb;
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+          if (j < (E >> (eb + 1))) {
+            // twiddle of the butterflies whose e-bits above eb equal j
+            const int idx = base | ((j << (eb + 1)) << b);
+            const int sj = idx >> (hb + 1);
+            const ulonglong2 wv = __ldg(twp + (row < 0 ? (1 << s) + sj : (1 << (n1 + s)) + (row << s) + sj));
+#pragma unroll
+            for (int lo = 0; lo < (1 << eb); ++lo) {
+              const int e = (j << (eb + 1)) | lo;
+              const int e2 = e | (1 << eb);
+              if (!INV) {
+                u64 X = x[e];
+                X = X >= q2 ? X - q2 : X;
+                const u64 Tv = shoup_lazy(x[e2], wv.x, wv.y, q);
+                x[e] = X + Tv;
+                x[e2] = X - Tv + q2;
+              } else {
+                const u64 X = x[e], Y = x[e2];
+                const u64 sm2 = X + Y;
+                x[e] = sm2 >= q2 ? sm2 - q2 : sm2;
+                x[e2] = shoup_lazy(X - Y + q2, wv.x, wv.y, q);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 struct NoEpilogue {};
 template <bool EPI>
 struct EpiArg {
@@ -151,55 +214,7 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
     for (int e = 0; e < E; ++e) x[e] = in[gaddr(base | (e << b))];
   }
 
-#pragma unroll
-  for (int gi = 0; gi < NG; ++gi) {
-    if (gi > 0) {  // re-layout through shared memory
-      int pb, pn, ph, pbase;
-      pass_shape<LOGM, INV>(gi - 1, tp, pb, pn, ph, pbase);
-#pragma unroll
-      for (int e = 0; e < E; ++e) lsm[pad8(pbase | (e << pb))] = x[e];
-      if (COL) __syncthreads();
-      else __syncwarp();
-      pass_shape<LOGM, INV>(gi, tp, b, nst, hb0, base);
-#pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = lsm[pad8(base | (e << b))];
-    }
-#pragma unroll
-    for (int st = 0; st < FHEON_NTT_RB; ++st) {
-      if (st < nst) {
-        const int hb = INV ? hb0 + st : hb0 - st;
-        const int eb = hb - b;
-        const int s = LOGM - 1 - hb;
-#pragma unroll
-        for (int j = 0; j < E / 2; ++j) {
-          if (j < (E >> (eb + 1))) {
-            // twiddle of the butterflies whose e-bits above eb equal j
-            const int idx = base | ((j << (eb + 1)) << b);
-            const int sj = idx >> (hb + 1);
-            const ulonglong2 wv =
-                __ldg(twp + (COL ? (1 << s) + sj : (1 << (n1 + s)) + ((line0 + li) << s) + sj));
-#pragma unroll
-            for (int lo = 0; lo < (1 << eb); ++lo) {
-              const int e = (j << (eb + 1)) | lo;
-              const int e2 = e | (1 << eb);
-              if (!INV) {
-                u64 X = x[e];
-                X = X >= q2 ? X - q2 : X;
-                const u64 Tv = shoup_lazy(x[e2], wv.x, wv.y, q);
-                x[e] = X + Tv;
-                x[e2] = X - Tv + q2;
-              } else {
-                const u64 X = x[e], Y = x[e2];
-                const u64 sm2 = X + Y;
-                x[e] = sm2 >= q2 ? sm2 - q2 : sm2;
-                x[e2] = shoup_lazy(X - Y + q2, wv.x, wv.y, q);
-              }
-            }
-          }
-        }
-      }
-    }
-  }
+  run_passes<LOGM, INV, COL ? 2 : 1>(x, tp, COL ? -1 : line0 + li, lsm, twp, q, n1, b, nst, hb0, base);
 
   // ---- store the last pass's layout straight to global memory
 #pragma unroll
