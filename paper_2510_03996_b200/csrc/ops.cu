@@ -307,10 +307,13 @@ __global__ void k_rescale_lift(PolyList r, PolyList last, const PrimeConst* __re
 // grid (N/256, limbs, nout).  Accumulates up to 8 products in 128 bits, folds
 // with one REDC into an R^-1-domain sum, and converts back with a final REDC
 // by R^2: out = sum_j ct_j (*) pt_j mod q exactly.
+// grid (nout, N/256, limbs): outputs fastest, so the CTAs of outputs that share
+// their terms (a conv's taps, a BSGS level's baby steps) read each term tile
+// from L2 instead of HBM
 __global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN) {
-  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
-  const int z = blockIdx.z;
-  const PrimeConst P = pc[blockIdx.y];
+  const std::size_t o = ((std::size_t)blockIdx.z << logN) + blockIdx.y * blockDim.x + threadIdx.x;
+  const int z = blockIdx.x;
+  const PrimeConst P = pc[blockIdx.z];
   const int nt = jobs.nterm[z];
   u64 s0 = 0, s1 = 0;
   Acc128 a0, a1;
@@ -552,7 +555,8 @@ void mul_monomial_half(const DevTables& t, const PolyList& out, const PolyList& 
 }
 void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.nout == 0) return;
-  k_mac<<<grid_for(t.N, limbs, jobs.nout), kThreads, 0, st>>>(jobs, t.pc, t.logN);
+  const dim3 grid(jobs.nout, (unsigned)(t.N / kThreads), limbs);
+  k_mac<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN);
   launch_check("k_mac");
 }
 void encode_lincomb(const DevTables& t, u64* out, const LinComb& lc, double scale, int limbs, cudaStream_t st) {
