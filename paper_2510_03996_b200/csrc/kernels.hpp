@@ -122,6 +122,10 @@ void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int 
 // ModUp basis conversion. x[b]: coefficient-domain input [limbs][N];
 // ext[b]: [beta][limbs+K][N], written for every limb outside the digit's own range.
 void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st);
+// tensor-core basis conversions (bconv_tc.cu): ModUp of digit j, ModDown conversion
+void modup_bconv_tc(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, int j, cudaStream_t st);
+void moddown_conv_tc(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);
+bool bconv_tc_enabled();
 // Inner product with automorphism. For each job r: acc[r] ([2][limbs+K][N]) =
 //   sum_j sigma_g(D_j) (x) key_j   where D_j = d (own limbs, NTT c1) | ext (other limbs)
 struct KsJobs {

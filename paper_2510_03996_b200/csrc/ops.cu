@@ -477,6 +477,11 @@ void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int
   TimedScope ts(t, kModUp, st);
   const int E = limbs + t.K;
   for (int j = 0; j < beta; ++j) {
+    if (bconv_tc_enabled()) {
+      modup_bconv_tc(t, ext, x, limbs, j, st);
+      launch_check("k_bconv_tc<modup>");
+      continue;
+    }
     const int lo = t.dig.lo(j);
     const int a = t.dig.hi(j, limbs) - lo;
     const dim3 grid = grid_for(t.N, (E - a + kTC - 1) / kTC, x.n);
@@ -522,6 +527,11 @@ void ks_inner_shared(const DevTables& t, const KsSharedJobs& jobs, int limbs, cu
 void moddown_conv(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
   if (conv.n == 0) return;
   TimedScope ts(t, kModDown, st);
+  if (bconv_tc_enabled()) {
+    moddown_conv_tc(t, conv, z, limbs, st);
+    launch_check("k_bconv_tc<moddown>");
+    return;
+  }
   const dim3 grid = grid_for(t.N, (limbs + kTC - 1) / kTC, conv.n);
 #define FHEON_MDC(KK)                                                                                             \
   case KK:                                                                                                        \
