@@ -79,17 +79,25 @@ __device__ __forceinline__ u64 madw(uint32_t a, uint32_t b, u64 c) {
   asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
   return d;
 }
-// S = sum_s d[s] 2^(8s) with d[s] < 2^23 and S < 2^124 (hi exact mod 2^64).
-// The power-of-two multipliers come from opaque registers (m[]) so each step
-// stays ONE IMAD.WIDE.U32 instead of a shift/add/carry sequence.
-__device__ __forceinline__ void recombine(const uint32_t* d, const uint32_t* m, u64& hi, u64& lo) {
-  u64 x0 = madw(d[3], m[2], madw(d[2], m[1], madw(d[1], m[0], d[0])));
-  x0 += (u64)(d[5] * 256u + d[4]) << 32;
-  u64 x1 = madw(d[9], m[2], madw(d[8], m[1], madw(d[7], m[0], d[6])));
-  x1 += (u64)(d[11] * 256u + d[10]) << 32;
-  const u64 x2 = madw(d[14], m[1], madw(d[13], m[0], d[12]));
-  lo = x0 + (x1 << 48);
-  hi = (x1 >> 16) + (x2 << 32) + (lo < x0 ? 1ULL : 0ULL);
+// S = sum_s d[s] 2^(8s) with d[s] < 2^23, d[15] = 0 and S < 2^124:
+//   e_j = d_2j + 2^8 d_2j+1 < 2^32 (one IMAD), f_i = e_2i + 2^16 e_2i+1 < 2^49 (one
+//   IMAD.WIDE; m16 = 2^16 arrives as a kernel argument so ptxas keeps the
+//   multiply), S = f0 + 2^32 f1 + 2^64 f2 + 2^96 f3 (one carry chain).
+__device__ __forceinline__ void recombine(const uint32_t* d, uint32_t m16, u64& hi, u64& lo) {
+  uint32_t e[8];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) e[j] = d[2 * j + 1] * 256u + d[2 * j];
+  e[7] = d[14];
+  u64 f[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) f[i] = madw(e[2 * i + 1], m16, e[2 * i]);
+  uint32_t w1, w2, w3;
+  asm("add.cc.u32 %0, %3, %4;\n\taddc.cc.u32 %1, %5, %6;\n\taddc.u32 %2, %7, %8;"
+      : "=r"(w1), "=r"(w2), "=r"(w3)
+      : "r"((uint32_t)(f[0] >> 32)), "r"((uint32_t)f[1]), "r"((uint32_t)(f[1] >> 32)), "r"((uint32_t)f[2]),
+        "r"((uint32_t)(f[2] >> 32)), "r"((uint32_t)f[3]));
+  lo = ((u64)w1 << 32) | (uint32_t)f[0];
+  hi = ((u64)w3 << 32) | w2;
 }
 
 struct TcBconvArgs {
@@ -105,6 +113,7 @@ struct TcBconvArgs {
   int kin, T, tb;      // GEMM inputs, targets of this launch, first target
   int nin;             // inputs read from memory (ModDown folded: kin = nin + 2)
   int lo, j, tab;      // ModUp digit
+  uint32_t m16;        // 2^16 (opaque to ptxas, see recombine)
 };
 
 // MODE 0 = ModUp digit j.  MODE 1 = ModDown with the finish folded into the
@@ -122,7 +131,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
   __shared__ __align__(8) u64 full[2], empty[2], afree[2], afull[2], ufree[2];
   __shared__ u64 cst[kTcMaxT * 16];  // c[t][k]
   __shared__ u64 tq[kTcMaxT][4];     // q, qinv_neg, mode consts
-  __shared__ unsigned tdst[kTcMaxT]; // destination limb of each target
+  __shared__ u64 toff[kTcMaxT];      // destination limb offset (limb * N) of each target
   __shared__ u64 yin[16][4];         // per-input (w, w', q, add)
   __shared__ double ypinv[16];
   __shared__ u64 urow[2][128];       // ModDown overflow estimate per row
@@ -159,13 +168,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
       const int pt = tt < a.limbs ? tt : a.L + (tt - a.limbs);
       tq[i][0] = a.pc[pt].q;
       tq[i][1] = a.pc[pt].qinv_neg;
-      tdst[i] = (unsigned)tt;
+      toff[i] = (u64)tt << a.logN;
     } else {
       tq[i][0] = a.pc[t].q;
       tq[i][1] = a.pc[t].qinv_neg;
       tq[i][2] = a.md_q[(std::size_t)t * 4];
       tq[i][3] = a.md_q[(std::size_t)t * 4 + 1];
-      tdst[i] = (unsigned)t;
+      toff[i] = (u64)t << a.logN;
     }
   }
   if (tid < a.nin) {
@@ -307,10 +316,6 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
     const int par = warp >> 2;
     const int row = (warp & 3) * 32 + lane;
     const uint32_t lanebase = (uint32_t)((warp & 3) * 32) << 16;
-    uint32_t mul[3];
-    asm volatile("mov.u32 %0, 256;" : "=r"(mul[0]));
-    asm volatile("mov.u32 %0, 65536;" : "=r"(mul[1]));
-    asm volatile("mov.u32 %0, 16777216;" : "=r"(mul[2]));
     int use = 0, tl = 0;
     for (int g = blockIdx.x; g < tiles; g += gridDim.x, ++tl) {
       const int z = g / tiles_per_poly;
@@ -349,14 +354,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
             if (tt < nt) {
               const int t = t0 + tt;
               u64 hi, lo;
-              recombine(d[i], mul, hi, lo);
+              recombine(d[i], a.m16, hi, lo);
               const u64 q = tq[t][0], qn = tq[t][1];
               u64 r = redc(hi, lo, q, qn);
               if (MODE == 2) {
                 r = sub_mod(r, redc(mulhi(u, tq[t][2]), u * tq[t][2], q, qn), q);
                 r = sub_mod(r, tq[t][3], q);
               }
-              out[(std::size_t)tdst[t] * N + n] = r;
+              out[toff[t] + n] = r;
             }
           }
         }
@@ -418,6 +423,7 @@ bool bconv_tc_enabled() {
 
 void modup_bconv_tc(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, int j, cudaStream_t st) {
   TcBconvArgs a{};
+  a.m16 = 1u << 16;
   a.in = x;
   a.out = ext;
   a.pc = t.pc;
@@ -437,6 +443,7 @@ void modup_bconv_tc(const DevTables& t, const PolyList& ext, const PolyList& x, 
 
 void moddown_conv_tc(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
   TcBconvArgs a{};
+  a.m16 = 1u << 16;
   a.in = z;
   a.out = conv;
   a.pc = t.pc;
