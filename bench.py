@@ -15,6 +15,7 @@ full ModUp -> key inner product (automorphism fused) -> ModDown per rotation.
          download, every step
   roofline  the key-switch inner-product kernel (HBM-bound: streams the key)
          timed live with CUDA events inside the timed region
+  roofline_bconv  the tensor-core ModUp/ModDown basis conversions
   roofline_ntt  the NTT phases (the largest share of the step; integer-pipe
          bound): butterflies/s against the measured lazy-Shoup butterfly peak
   models  encrypted LeNet-5 / ResNet-20 s/image through the model runtime
@@ -222,6 +223,37 @@ def run_ours(args):
                     ntt_limbs // max(1, args.steps), "share_of_step": round(ntt_ms / ms_ntt_pass, 4),
                     "hbm_gbs": round(ntt_limbs * N * 8 * 4 / (ntt_ms / 1e3) / 1e9, 1)}
 
+    # ---- the tensor-core basis conversions (ModUp class 3, ModDown class 4),
+    # timed live in two more passes.  Algorithmic work: exact 64x64-bit
+    # products, per rotation sum_j (L + K - alpha_j) alpha_j (ModUp) + 2 L K
+    # (ModDown) per coefficient; each is 8 x 16 int8 MACs on the tensor cores.
+    bc_ms = {}
+    for cls in (3, 4):
+        ctx.timer_arm(cls)
+        for _ in range(args.steps):
+            keep = step()
+        torch.cuda.synchronize()
+        bc_ms[cls], _ = ctx.timer_read()
+        ctx.timer_arm(0)
+        del keep
+    alpha = (L + DNUM - 1) // DNUM
+    digs = [min(alpha, L - j * alpha) for j in range((L + alpha - 1) // alpha)]
+    macs_rot = (sum((L + K - a) * a for a in digs) + 2 * L * K) * N
+    bc_rate = macs_rot * args.steps * B / ((bc_ms[3] + bc_ms[4]) / 1e3)
+    int8_peak = 2 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] * 1e12 / 2 \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 2.25e15
+    roofline_bconv = {"kernel": "k_bconv_tc (ModUp + ModDown basis conversion, tcgen05.mma kind::i8)",
+                      "bound": "tensor", "achieved": round(bc_rate / 1e12, 3),
+                      "peak": round(int8_peak / 128 / 1e12, 3), "unit": "T exact 64-bit MAC/s",
+                      "frac": round(bc_rate / (int8_peak / 128), 4),
+                      "peak_source": "2 x measured bf16 dense (MEASURED_PEAKS.json) int8 MAC/s / 128 int8 MACs "
+                                     "per 64-bit product (8 bytes x 16 shift columns)",
+                      "cuda_core_roofline": 1.29,
+                      "cuda_core_roofline_note": "17.75 IMAD.WIDE.U32/clk/SM (profiles/int_peak.json) / 4 per "
+                                                 "64x64->128 product, 148 SMs at 1965 MHz",
+                      "share_of_step": round((bc_ms[3] + bc_ms[4]) / ms, 4),
+                      "macs_per_rotation": macs_rot}
+
     # ---- roofline of the key-switch inner product (per launch: one rotation)
     E = L + K
     beta = (L + (L + DNUM - 1) // DNUM - 1) // ((L + DNUM - 1) // DNUM)
@@ -298,6 +330,7 @@ def run_ours(args):
                      "launches_timed": ks_n,
                      "share_of_step": round(ks_ms / ms, 4)},
         "roofline_ntt": roofline_ntt,
+        "roofline_bconv": roofline_bconv,
         "clocks": clk.summary(),
     }
     if extras:

@@ -8,7 +8,7 @@ FHEON_PROFILE_RANGE=1 ncu --profile-from-start off --metrics gpu__time_duration.
   --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo list rc=$?
 FHEON_PROFILE_RANGE=1 ncu --profile-from-start off --set full --clock-control none --import-source on \
-  -k regex:"ntt_phase_kernel|k_ks_inner|k_modup_bconv|k_moddown_conv" -c 8 -o gpurun_out/prof_r1e $CMD \
+  -k regex:"ntt_phase_kernel|k_ks_inner|k_bconv_tc" -c 10 -o gpurun_out/prof_r1f $CMD \
   > gpurun_out/ncu_full.log 2>&1
 echo full rc=$?
 tail -3 gpurun_out/ncu_full.log

@@ -1,0 +1,28 @@
+"""One CSV row per profiled kernel of an ncu --set full report (the columns of
+profiles/r01_ncu_full_v*.csv): duration, DRAM bytes, pipe and issue activity,
+occupancy, the main stall ratios."""
+import csv
+import subprocess
+import sys
+
+COLS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
+raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr = rows[0]
+w = csv.writer(sys.stdout)
+w.writerow(["Kernel Name", "Grid Size", "Block Size"] + COLS)
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    w.writerow([d.get("Kernel Name", "")[:90], d.get("Grid Size", ""), d.get("Block Size", "")] +
+               [d.get(c, "") for c in COLS])
