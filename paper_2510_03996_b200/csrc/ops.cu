@@ -159,6 +159,21 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
   acc[((std::size_t)E + t) * N + n] = redc(a1.hi, a1.lo, P.q, P.qinv_neg);
 }
 
+// Lazy reduction across jobs: every product is < q^2 (canonical digit x
+// Montgomery key), so up to 32 of them stay below 32 q^2 < 2^125; REDC of
+// such a sum is < S / 2^64 + q < 3q (q < 2^60) and two conditional
+// subtractions make it canonical -- the same residue as one REDC per job.
+__device__ __forceinline__ int lazy_chunk(int beta) { return max(1, 32 / (beta + 1)); }
+__device__ __forceinline__ void lazy_flush(u64& s0, u64& s1, Acc128& a0, Acc128& a1, const PrimeConst& P) {
+  const u64 m0 = a0.lo * P.qinv_neg, m1 = a1.lo * P.qinv_neg;
+  const u64 t0 = a0.hi + mulhi(m0, P.q) + (a0.lo != 0 ? 1ULL : 0ULL);
+  const u64 t1 = a1.hi + mulhi(m1, P.q) + (a1.lo != 0 ? 1ULL : 0ULL);
+  s0 = add_mod(s0, csub(csub(t0, P.q), P.q), P.q);
+  s1 = add_mod(s1, csub(csub(t1, P.q), P.q), P.q);
+  a0 = Acc128{};
+  a1 = Acc128{};
+}
+
 // grid (N/256, E, groups): rotate-and-sum accumulation (kernels.hpp KsSumJobs).
 // Each job's digit sum (<= beta + 1 products < q^2) is REDC'd on its own so the
 // 128-bit accumulator never exceeds q * 2^64; job results add mod q.
@@ -177,13 +192,15 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
   const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;
   const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;  // P mod q_t, Montgomery form
   u64 s0 = 0, s1 = 0;
+  const int chunk = lazy_chunk(beta);
+  Acc128 a0, a1;
+  int cnt = 0;
   for (int jb = jobs.begin[r]; jb < jobs.begin[r + 1]; ++jb) {
     const u64 g = jobs.g[jb];
     const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
     const u64* key = jobs.key[jb];
     const u64* ext = jobs.ext[jb];
     const u64* d = jobs.d[jb];
-    Acc128 a0, a1;
     for (int j = 0; j < beta; ++j) {
       const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
       const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
@@ -191,9 +208,12 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
       a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
     }
     if (t < limbs) a0.mac(jobs.c0[jb][(std::size_t)t * N + src], pm);
-    s0 = csub(s0 + redc(a0.hi, a0.lo, P.q, P.qinv_neg), P.q);
-    s1 = csub(s1 + redc(a1.hi, a1.lo, P.q, P.qinv_neg), P.q);
+    if (++cnt == chunk) {
+      lazy_flush(s0, s1, a0, a1, P);
+      cnt = 0;
+    }
   }
+  if (cnt) lazy_flush(s0, s1, a0, a1, P);
   u64* acc = jobs.acc[r];
   acc[(std::size_t)t * N + n] = s0;
   acc[((std::size_t)E + t) * N + n] = s1;
@@ -216,11 +236,13 @@ __global__ void k_ks_inner_shared(KsSharedJobs jobs, const PrimeConst* __restric
   const u64* d = jobs.d[r];
   const u64* c0 = jobs.c0[r];
   u64 s0 = 0, s1 = 0;
+  const int chunk = lazy_chunk(beta);
+  Acc128 a0, a1;
+  int cnt = 0;
   for (int jb = 0; jb < jobs.nkeys; ++jb) {
     const u64 g = jobs.g[jb];
     const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
     const u64* key = jobs.key[jb];
-    Acc128 a0, a1;
     for (int j = 0; j < beta; ++j) {
       const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
       const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
@@ -228,9 +250,12 @@ __global__ void k_ks_inner_shared(KsSharedJobs jobs, const PrimeConst* __restric
       a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
     }
     if (t < limbs) a0.mac(c0[(std::size_t)t * N + src], pm);
-    s0 = csub(s0 + redc(a0.hi, a0.lo, P.q, P.qinv_neg), P.q);
-    s1 = csub(s1 + redc(a1.hi, a1.lo, P.q, P.qinv_neg), P.q);
+    if (++cnt == chunk) {
+      lazy_flush(s0, s1, a0, a1, P);
+      cnt = 0;
+    }
   }
+  if (cnt) lazy_flush(s0, s1, a0, a1, P);
   u64* acc = jobs.acc[r];
   acc[(std::size_t)t * N + n] = s0;
   acc[((std::size_t)E + t) * N + n] = s1;
@@ -304,7 +329,7 @@ __global__ void k_rescale_lift(PolyList r, PolyList last, const PrimeConst* __re
 }
 
 // ------------------------------------------------------------ fused layer kernels
-// grid (N/256, limbs, nout).  Accumulates up to 8 products in 128 bits, folds
+// grid (N/256, limbs, nout).  Accumulates up to 32 products in 128 bits, folds
 // with one REDC into an R^-1-domain sum, and converts back with a final REDC
 // by R^2: out = sum_j ct_j (*) pt_j mod q exactly.
 // grid (nout, N/256, limbs): outputs fastest, so the CTAs of outputs that share
@@ -317,17 +342,12 @@ __global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN)
   const int nt = jobs.nterm[z];
   u64 s0 = 0, s1 = 0;
   Acc128 a0, a1;
-  for (int j = 0; j < nt; ++j) {
+  for (int j = 0; j < nt; ++j) {  // nt <= kMacMaxTerms = 32 products < 32 q^2: one lazy flush
     const u64* c = jobs.ct[z][j];
     const u64 p = jobs.pt[z][j][o];
     a0.mac(c[o], p);
     a1.mac(c[jobs.c1_off[z][j] + o], p);
-    if ((j & 7) == 7 || j == nt - 1) {
-      s0 = add_mod(s0, redc(a0.hi, a0.lo, P.q, P.qinv_neg), P.q);
-      s1 = add_mod(s1, redc(a1.hi, a1.lo, P.q, P.qinv_neg), P.q);
-      a0 = Acc128{};
-      a1 = Acc128{};
-    }
+    if ((j & 31) == 31 || j == nt - 1) lazy_flush(s0, s1, a0, a1, P);
   }
   jobs.out0[z][o] = redc(mulhi(s0, P.r2), s0 * P.r2, P.q, P.qinv_neg);
   jobs.out1[z][o] = redc(mulhi(s1, P.r2), s1 * P.r2, P.q, P.qinv_neg);
