@@ -682,6 +682,12 @@ const double* Context::basis(const std::string& key, const std::vector<double>& 
   return reinterpret_cast<const double*>(b->ptr);
 }
 
+const double* Context::basis(const std::string& key, const std::function<std::vector<double>()>& make) {
+  auto it = basis_.find(key);
+  if (it != basis_.end()) return reinterpret_cast<const double*>(it->second->ptr);
+  return basis(key, make());
+}
+
 BufPtr Context::encode_lincomb(const LinComb& lc, int limbs, double scale) {
   BufPtr out = alloc((std::size_t)limbs * ht_.N);
   ++stats.encodes;

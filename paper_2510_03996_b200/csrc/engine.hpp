@@ -163,6 +163,8 @@ class Context {
   // device real-coefficient (unscaled, unrounded) encoding of a slot vector,
   // cached under `key` (block indicators of a layer geometry)
   const double* basis(const std::string& key, const std::vector<double>& slot_values);
+  // same, building the slot values only on a cache miss
+  const double* basis(const std::string& key, const std::function<std::vector<double>()>& make);
   // plaintext = round(scale * sum_b w_b basis_b), NTT domain over `limbs` limbs
   BufPtr encode_lincomb(const LinComb& lc, int limbs, double scale);
 

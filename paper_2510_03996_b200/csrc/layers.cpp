@@ -741,6 +741,123 @@ PackedTensor conv_generic(Context& ctx, const PackedTensor& x, const ConvConfig&
   return conv_core_generic(ctx, x, cfg, w);
 }
 
+namespace {
+// Fast-schedule special 3x3 convolution with C == F channels and 2 C m <= S:
+// the channel mixing as a diagonal (channel-rotation) transform instead of one
+// channel-sum rotate-and-sum per output channel.
+//   x_rep = clean(x) + rot(clean(x), -C m)       (level 1: the block mask the
+//                                                  reference spends on its cleanup)
+//   out[f m + p] = sum_{d < C, tap} w(f, (f+d) mod C, tap) mask_tap[p] x_rep[(f+d) m + p + o_tap]
+// With d = d1 + D d2, b(tap, d1) = rot(x_rep, o_tap + d1 m) (one hoisted set) and
+//   out = sum_d2 rot( sum_{tap,d1} Q(d2,tap,d1) (*) b(tap,d1), D d2 m )      (level 2)
+// where Q(d2,tap,d1) holds w(f, (f+d) mod C, tap) mask_tap at block f + D d2.
+// The giants are one rotate-and-sum (one ModDown) and the products one
+// unrescaled MAC + one rescale.  Same slot values and levels as the reference's
+// algorithm (taps, channel sums, cleanup, placement); C/D + 9D rotations instead of
+// 8 + F (2 log-stages + placement) -- e.g. 51 vs 968 inner products at C = 64.
+// baby range D: minimise a key-switch cost model (ModUp 3.3, ModDown 2.4, inner
+// product 1 -- measured ratios at N = 2^16): babies 9D-1 inner + ModDowns, giants
+// ceil(C/D)-1 ModUps + inner, plus the replication rotation and the hoisted ModUp
+std::size_t diag_baby_range(std::size_t C) {
+  std::size_t best = 1;
+  double best_cost = 1e300;
+  for (std::size_t D = 1; D <= std::min<std::size_t>(8, C); ++D) {
+    const double G = (double)((C + D - 1) / D);
+    const double cost = 3.3 * (1.0 + G) + 2.4 * (1.0 + 9.0 * D) + (9.0 * D + G - 1.0);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = D;
+    }
+  }
+  return best;
+}
+
+bool special3x3_diag_applies(const Context& ctx, std::size_t C, std::size_t F, std::size_t m) {
+  return ctx.fast_schedule() && C == F && C >= 8 && 2 * C * m <= (std::size_t)ctx.S() &&
+         C <= (std::size_t)kMaxBasis;
+}
+
+PackedTensor conv_special_3x3_diag(Context& ctx, const PackedTensor& x, const KernelTensor& w) {
+  const std::size_t W = x.width, C = x.channels, m = W * W;
+  const std::size_t D = diag_baby_range(C);
+  const std::size_t G = (C + D - 1) / D;  // giants d2 < G
+  // level 1: clean the input outside its C blocks, replicate it after itself
+  const BufPtr keep = pt_of(ctx, x.data, range_mask(ctx, 0, C * m));
+  const Ciphertext xc = mp_many(ctx, {x.data}, {keep})[0];
+  const Ciphertext xr = add(ctx, xc, rotate(ctx, xc, -(long)(C * m)));
+  // babies b(tap, d1) = rot(x_rep, o_tap + d1 m): one hoisted set
+  std::vector<long> offs;
+  for (std::size_t d1 = 0; d1 < D; ++d1)
+    for (std::size_t tap = 0; tap < 9; ++tap) {
+      const long o = ((long)(tap / 3) - 1) * (long)W + ((long)(tap % 3) - 1) + (long)(d1 * m);
+      if (o != 0) offs.push_back(o);
+    }
+  const std::vector<Ciphertext> rot = rotate_hoisted(ctx, xr, offs);
+  std::vector<Ciphertext> baby;  // index d1 * 9 + tap
+  {
+    std::size_t k = 0;
+    for (std::size_t d1 = 0; d1 < D; ++d1)
+      for (std::size_t tap = 0; tap < 9; ++tap) {
+        const long o = ((long)(tap / 3) - 1) * (long)W + ((long)(tap % 3) - 1) + (long)(d1 * m);
+        baby.push_back(o == 0 ? xr : rot[k++]);
+      }
+  }
+  const std::array<std::vector<double>, 9> masks = build_all_masks(m, 1, W);
+  // mask_tap restricted to block blk < 2C (same cache keys as the reference-schedule path)
+  std::vector<const double*> bases(9 * 2 * C);
+  for (std::size_t tap = 0; tap < 9; ++tap)
+    for (std::size_t blk = 0; blk < 2 * C; ++blk)
+      bases[tap * 2 * C + blk] =
+          ctx.basis("m3:" + std::to_string(W) + ":" + std::to_string(tap) + ":" + std::to_string(blk), [&] {
+            std::vector<double> v((blk + 1) * m, 0.0);
+            for (std::size_t i = 0; i < m; ++i) v[blk * m + i] = masks[tap][i];
+            return v;
+          });
+  const double ps = pt_scale_for(ctx, xr);
+  const std::string wk = weight_key("s3d", w, W);
+  std::vector<std::vector<Ciphertext>> terms(G);
+  std::vector<std::vector<BufPtr>> pts(G);
+  for (std::size_t d2 = 0; d2 < G; ++d2)
+    for (std::size_t d1 = 0; d1 < D; ++d1) {
+      const std::size_t d = d1 + D * d2;
+      if (d >= C) continue;
+      for (std::size_t tap = 0; tap < 9; ++tap) {
+        bool any = false;
+        for (std::size_t f = 0; f < C && !any; ++f) any = w.at(f, (f + d) % C, tap / 3, tap % 3) != 0.0;
+        if (!any) continue;
+        terms[d2].push_back(baby[d1 * 9 + tap]);
+        pts[d2].push_back(ctx.weight_pt(wk + ":" + std::to_string(d) + ":" + std::to_string(tap), xr.limbs, ps, [&] {
+          LinComb lc{};
+          for (std::size_t f = 0; f < C; ++f) {
+            const double wv = w.at(f, (f + d) % C, tap / 3, tap % 3);
+            if (wv == 0.0) continue;
+            lc.basis[lc.nb] = bases[tap * 2 * C + f + D * d2];
+            lc.w[lc.nb] = wv;
+            ++lc.nb;
+          }
+          return ctx.encode_lincomb(lc, xr.limbs, ps);
+        }));
+      }
+    }
+  // giants: one rotate-and-sum over d2 (rows unrescaled), one rescale
+  std::vector<std::vector<Ciphertext>> nz_terms;
+  std::vector<std::vector<BufPtr>> nz_pts;
+  std::vector<std::size_t> nz_d2;
+  for (std::size_t d2 = 0; d2 < G; ++d2)
+    if (!terms[d2].empty()) {
+      nz_terms.push_back(terms[d2]);
+      nz_pts.push_back(pts[d2]);
+      nz_d2.push_back(d2);
+    }
+  const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, nz_terms, nz_pts);
+  RotTerms giants;
+  for (std::size_t i = 0; i < rows.size(); ++i) giants.push_back({rows[i], (long)(D * nz_d2[i] * m)});
+  Ciphertext out = rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+  out = add_bias(ctx, out, w.bias, m);
+  return {out, C, W};
+}
+}  // namespace
+
 // conv_special_3x3 (layers_conv.cpp:435-502)
 PackedTensor conv_special_3x3(Context& ctx, const PackedTensor& x, const ConvConfig& cfg, const KernelTensor& w) {
   if (cfg.kernel != 3 || cfg.stride != 1 || cfg.padding != 1)
@@ -752,6 +869,7 @@ PackedTensor conv_special_3x3(Context& ctx, const PackedTensor& x, const ConvCon
   const std::size_t m = W * W;
   if (F * m > (std::size_t)ctx.S()) throw capacity_error("convolution output does not fit in the slot count");
   if (C > (std::size_t)kMaxBasis) throw capacity_error("too many input channels for one plaintext combination");
+  if (special3x3_diag_applies(ctx, C, F, m)) return conv_special_3x3_diag(ctx, x, w);
   const std::vector<Ciphertext> ud = rotate_hoisted(ctx, x.data, {-(long)W, (long)W});
   // the six +-1 shifts of up / x / down: one batched key switch (three hoisted pairs)
   const std::vector<Ciphertext> sh = rotate_many(ctx, {ud[0], ud[0], x.data, x.data, ud[1], ud[1]}, {-1, 1, -1, 1, -1, 1});

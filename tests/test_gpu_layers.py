@@ -103,6 +103,28 @@ def test_special3x3(env, W, C, F, s):
     check(out, ev, r, f"special3x3 W={W} C={C} F={F}", ctx.schedule())
 
 
+@pytest.mark.parametrize("W,C,garbage", [(8, 8, False), (4, 16, True), (8, 16, True)])
+def test_special3x3_channel_diagonal(env, W, C, garbage):
+    """C == F >= 8 with 2 C W^2 <= S: the fast schedule's channel-diagonal
+    transform (clean + replicate the input, baby-step/giant-step over channel
+    offsets); slots beyond the C blocks carry garbage that must not leak in."""
+    ctx, ref = env
+    rng = np.random.default_rng(C * 100 + W)
+    S = 1 << (LOGN - 1)
+    x = np.zeros(S)
+    x[:C * W * W] = rng.uniform(-1, 1, C * W * W)
+    if garbage:
+        x[C * W * W:] = rng.uniform(-1, 1, S - C * W * W)
+    w = rng.uniform(-1, 1, (C, C, 3, 3))
+    b = rng.uniform(-1, 1, C)
+    cfg = fh.ConvConfig(C, C, 3, 1, 1, fh.ConvMode.special3x3)
+    out, ev, r = run_both(ctx, lambda v: fh.convolution(fh.PackedTensor(v, C, W), cfg, fh.KernelTensor(w, b)).data,
+                          lambda v: ref.convolution(v, DEPTH, C, W, C, 3, 1, 1, 1, 0, w, b), x)
+    check(out, ev, r, f"special3x3 diagonal W={W} C={C}", ctx.schedule())
+    if ctx.schedule() == "fast":
+        assert sum(1 for e in ev if e[0] == "rotation") < sum(1 for e in r.events if e[0] == "rotation")
+
+
 @pytest.mark.parametrize("W,C,F,s", [c for c in cases(9003, 6) if c[1] >= 2][:3])
 def test_grouped_conv(env, W, C, F, s):
     ctx, ref = env
