@@ -303,6 +303,193 @@ std::vector<Ciphertext> channel_cursors(Context& ctx, const Ciphertext& x, std::
 std::vector<Ciphertext> stride_many(Context& ctx, const std::vector<Ciphertext>& a, std::size_t W, std::size_t S,
                                     std::size_t W_out, int variant);
 
+// One masked permutation of slots inside every block (nblk blocks of size blk):
+// out[c blk + dest] = x[c blk + src] for every move, zero elsewhere, as
+//   out = sum_g rot( sum_h M_{g,h} (*) rot(x, h), g ),   src - dest = g + h,
+// M_{g,h} = 1 where the moves with that (g, h) sit after the baby rotation
+// (c blk + src - h).  Babies one hoisted set, products one unrescaled MAC,
+// giants one rotate-and-sum, one rescale: one plaintext level.
+struct SlotMove {
+  std::size_t dest, src;
+  long g, h;
+};
+
+Ciphertext bsgs_moves(Context& ctx, const Ciphertext& x, const std::vector<SlotMove>& moves, std::size_t blk,
+                      std::size_t nblk, const std::string& key) {
+  std::vector<long> hs, gs;
+  for (const SlotMove& mv : moves) {
+    hs.push_back(mv.h);
+    gs.push_back(mv.g);
+  }
+  std::sort(hs.begin(), hs.end());
+  hs.erase(std::unique(hs.begin(), hs.end()), hs.end());
+  std::sort(gs.begin(), gs.end());
+  gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+  std::vector<long> nz;
+  for (long h : hs)
+    if (h != 0) nz.push_back(h);
+  const std::vector<Ciphertext> r = nz.empty() ? std::vector<Ciphertext>{} : rotate_hoisted(ctx, x, nz);
+  std::map<long, Ciphertext> baby;
+  {
+    std::size_t k = 0;
+    for (long h : hs) baby[h] = h == 0 ? x : r[k++];
+  }
+  const long Sl = ctx.S();
+  const double ps = pt_scale_for(ctx, x);
+  std::map<std::pair<long, long>, std::vector<std::size_t>> cls;  // (g, h) -> move indices
+  for (std::size_t i = 0; i < moves.size(); ++i) cls[{moves[i].g, moves[i].h}].push_back(i);
+  std::vector<std::vector<Ciphertext>> terms(gs.size());
+  std::vector<std::vector<BufPtr>> pts(gs.size());
+  for (const auto& [gh, idx] : cls) {
+    const std::size_t gi = (std::size_t)(std::lower_bound(gs.begin(), gs.end(), gh.first) - gs.begin());
+    terms[gi].push_back(baby[gh.second]);
+    pts[gi].push_back(ctx.encode_named(key + ":" + std::to_string(gh.first) + ":" + std::to_string(gh.second), [&] {
+      std::vector<double> v((std::size_t)Sl, 0.0);
+      for (std::size_t i : idx)
+        for (std::size_t c = 0; c < nblk; ++c) {
+          const long p = (((long)(c * blk + moves[i].src) - gh.second) % Sl + Sl) % Sl;
+          v[(std::size_t)p] = 1.0;
+        }
+      return v;
+    }, x.limbs, ps));
+  }
+  const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, terms, pts);
+  RotTerms giants;
+  for (std::size_t i = 0; i < rows.size(); ++i) giants.push_back({rows[i], gs[i]});
+  return rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+}
+
+// out[f mb + p] = sum_{q < nq} wfn(f, q) z[q mb + p] for f < F, with z periodic
+// (period nq mb over all S slots): diagonals d = (q - f) mod nq as a baby-step
+// giant-step sum, d = d1 + D d2, babies rot(z, d1 mb), giants rot(., D d2 mb);
+// plaintext Q(d2, d1) holds wfn(f, (f + d) mod nq) on block f + D d2.
+Ciphertext diag_mix(Context& ctx, const Ciphertext& z, std::size_t nq, std::size_t F, std::size_t mb,
+                    const std::function<double(std::size_t, std::size_t)>& wfn, const std::string& key) {
+  const std::size_t nblk = (std::size_t)ctx.S() / mb;
+  std::size_t D = 1;
+  double best = 1e300;
+  for (std::size_t d = 1; d <= std::min<std::size_t>(nq, 32); ++d) {
+    const double G = (double)((nq + d - 1) / d);
+    const double cost = 3.3 * G + 2.4 * (double)d + ((double)d - 1.0 + G - 1.0);
+    if (cost < best) {
+      best = cost;
+      D = d;
+    }
+  }
+  const std::size_t G = (nq + D - 1) / D;
+  std::vector<long> offs;
+  for (std::size_t d1 = 1; d1 < D; ++d1) offs.push_back((long)(d1 * mb));
+  std::vector<Ciphertext> baby{z};
+  if (!offs.empty()) {
+    const std::vector<Ciphertext> r = rotate_hoisted(ctx, z, offs);
+    baby.insert(baby.end(), r.begin(), r.end());
+  }
+  const double ps = pt_scale_for(ctx, z);
+  std::vector<std::vector<Ciphertext>> terms;
+  std::vector<std::vector<BufPtr>> pts;
+  std::vector<long> gsh;
+  for (std::size_t d2 = 0; d2 < G; ++d2) {
+    std::vector<Ciphertext> t;
+    std::vector<BufPtr> p;
+    for (std::size_t d1 = 0; d1 < D; ++d1) {
+      const std::size_t d = d1 + D * d2;
+      if (d >= nq) continue;
+      bool any = false;
+      for (std::size_t f = 0; f < F && !any; ++f) any = wfn(f, (f + d) % nq) != 0.0;
+      if (!any) continue;
+      t.push_back(baby[d1]);
+      p.push_back(ctx.weight_pt(key + ":" + std::to_string(d), z.limbs, ps, [&] {
+        LinComb lc{};
+        for (std::size_t f = 0; f < F; ++f) {
+          const double wv = wfn(f, (f + d) % nq);
+          if (wv == 0.0) continue;
+          lc.basis[lc.nb] = block_basis(ctx, mb, (f + D * d2) % nblk);
+          lc.w[lc.nb] = wv;
+          ++lc.nb;
+        }
+        return ctx.encode_lincomb(lc, z.limbs, ps);
+      }));
+    }
+    if (t.empty()) continue;
+    terms.push_back(std::move(t));
+    pts.push_back(std::move(p));
+    gsh.push_back((long)(D * d2 * mb));
+  }
+  const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, terms, pts);
+  RotTerms giants;
+  for (std::size_t i = 0; i < rows.size(); ++i) giants.push_back({rows[i], gsh[i]});
+  return rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+}
+
+std::size_t best_divisor_split(std::size_t n, std::size_t giants_per_unit) {
+  // babies B | n minimising (B - 1) baby key switches + (giants_per_unit n / B - 1) giant ones
+  std::size_t best = 1;
+  double bc = 1e300;
+  for (std::size_t b = 1; b <= n; ++b) {
+    if (n % b) continue;
+    const double c = 3.4 * (double)(b - 1) + 4.3 * (double)(giants_per_unit * n / b - 1);
+    if (c < bc) {
+      bc = c;
+      best = b;
+    }
+  }
+  return best;
+}
+
+// Fast-schedule 2x2 / stride-2 convolution (ResNet-20's downsampling convs) via
+// the polyphase decomposition: out[f][a][b] = sum_{c,i,j} w[f,c,i,j] x_ij[c][a][b]
+// with x_ij[c][a][b] = x[c][2a+i][2b+j].  Two masked permutations turn every
+// W x W channel block into its four W/2 x W/2 phase blocks (columns, then rows
+// and phases), the input is replicated to fill all slots, and the conv is a 1x1
+// channel mixing over the 4C phase blocks (diag_mix).  Three plaintext levels,
+// as the reference's MAC + cleanup + stride; a few dozen key switches instead of
+// a per-output-channel stride extraction.
+bool conv2x2s2_polyphase_applies(const Context& ctx, std::size_t C, std::size_t F, std::size_t W, std::size_t k,
+                                 std::size_t S) {
+  const std::size_t Sl = (std::size_t)ctx.S();
+  return ctx.fast_schedule() && k == 2 && S == 2 && W >= 4 && W % 2 == 0 && C * W * W <= Sl &&
+         Sl % (C * W * W) == 0 && F <= (std::size_t)kMaxBasis && F * (W / 2) * (W / 2) <= Sl && 4 * C >= 2;
+}
+
+PackedTensor conv_2x2s2_polyphase(Context& ctx, const PackedTensor& x, const KernelTensor& w) {
+  const std::size_t W = x.width, C = x.channels, F = w.out_channels;
+  const std::size_t Wo = W / 2, m = W * W, mo = Wo * Wo;
+  const std::size_t Sl = (std::size_t)ctx.S();
+  const std::string geo = std::to_string(W) + ":" + std::to_string(C);
+  // A: column de-interleave inside every row, s = 2b + j -> j Wo + b
+  std::vector<SlotMove> mA;
+  const std::size_t BA = best_divisor_split(Wo, 2);
+  for (std::size_t r = 0; r < W; ++r)
+    for (std::size_t j = 0; j < 2; ++j)
+      for (std::size_t b = 0; b < Wo; ++b) {
+        const long t = (long)b + (long)j * (1 - (long)Wo);
+        const long h = (long)(b % BA);
+        mA.push_back({r * W + j * Wo + b, r * W + 2 * b + j, t - h, h});
+      }
+  const Ciphertext za = bsgs_moves(ctx, x.data, mA, m, C, "pp-A:" + geo);
+  // B: rows and phases, row 2a + i, half j -> phase block 2i + j, row a
+  std::vector<SlotMove> mB;
+  const std::size_t BB = best_divisor_split(Wo, 4);
+  const long gstep = (long)(2 * W - Wo);
+  for (std::size_t a = 0; a < Wo; ++a)
+    for (std::size_t i = 0; i < 2; ++i)
+      for (std::size_t j = 0; j < 2; ++j)
+        for (std::size_t b = 0; b < Wo; ++b) {
+          const std::size_t src = (2 * a + i) * W + j * Wo + b, dest = (2 * i + j) * mo + a * Wo + b;
+          const long t = (long)src - (long)dest;
+          const long h = (long)(a % BB) * gstep;
+          mB.push_back({dest, src, t - h, h});
+        }
+  Ciphertext z = bsgs_moves(ctx, za, mB, m, C, "pp-B:" + geo);
+  // periodic over all slots (period C m): phase block q = 4c + 2i + j
+  for (std::size_t span = C * m; span < Sl; span *= 2) z = add(ctx, z, rotate(ctx, z, -(long)span));
+  Ciphertext out = diag_mix(ctx, z, 4 * C, F, mo,
+                            [&](std::size_t f, std::size_t q) { return w.at(f, q / 4, (q % 4) / 2, q % 2); },
+                            weight_key("pp", w, W));
+  out = add_bias(ctx, out, w.bias, mo);
+  return {out, F, Wo};
+}
+
 // conv_core_generic (layers_conv.cpp:117-180)
 PackedTensor conv_core_generic(Context& ctx, const PackedTensor& x, const ConvConfig& cfg, const KernelTensor& w) {
   const std::size_t W = x.width, C = x.channels;
@@ -318,6 +505,7 @@ PackedTensor conv_core_generic(Context& ctx, const PackedTensor& x, const ConvCo
     throw capacity_error("convolution output needs " + std::to_string(F * W_out * W_out) +
                          " slots but the context provides " + std::to_string(ctx.S()));
   if (C > (std::size_t)kMaxBasis) throw capacity_error("too many input channels for one plaintext combination");
+  if (conv2x2s2_polyphase_applies(ctx, C, F, W, k, S)) return conv_2x2s2_polyphase(ctx, x, w);
   const std::vector<Ciphertext> taps = tap_rotations(ctx, x.data, k, W);
   const double ps = pt_scale_for(ctx, taps[0]);
   // fused rotate-and-MAC: sum_f = sum_taps tap (*) repeated_kernel_vector(f, tap)

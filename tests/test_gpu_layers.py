@@ -103,6 +103,28 @@ def test_special3x3(env, W, C, F, s):
     check(out, ev, r, f"special3x3 W={W} C={C} F={F}", ctx.schedule())
 
 
+@pytest.mark.parametrize("W,C,F,garbage", [(8, 4, 8, True), (16, 8, 16, True), (4, 1, 3, False), (8, 2, 2, True)])
+def test_conv2x2_stride2_polyphase(env, W, C, F, garbage):
+    """2x2 / stride-2 generic convolution (ResNet-20's downsampling): the fast
+    schedule's polyphase path (two masked slot permutations, periodic
+    replication, 1x1 channel mixing over the 4C phase blocks)."""
+    ctx, ref = env
+    rng = np.random.default_rng(W * 1000 + C * 10 + F)
+    S = 1 << (LOGN - 1)
+    x = np.zeros(S)
+    x[:C * W * W] = rng.uniform(-1, 1, C * W * W)
+    if garbage:
+        x[C * W * W:] = rng.uniform(-1, 1, S - C * W * W)
+    w = rng.uniform(-1, 1, (F, C, 2, 2))
+    b = rng.uniform(-1, 1, F)
+    cfg = fh.ConvConfig(C, F, 2, 2, 0, fh.ConvMode.generic, fh.StrideVariant(0))
+    out, ev, r = run_both(ctx, lambda v: fh.convolution(fh.PackedTensor(v, C, W), cfg, fh.KernelTensor(w, b)).data,
+                          lambda v: ref.convolution(v, DEPTH, C, W, F, 2, 2, 0, 0, 0, w, b), x)
+    check(out, ev, r, f"2x2/s2 conv W={W} C={C} F={F}", ctx.schedule())
+    if ctx.schedule() == "fast" and W >= 8:
+        assert sum(1 for e in ev if e[0] == "rotation") < sum(1 for e in r.events if e[0] == "rotation")
+
+
 @pytest.mark.parametrize("W,C,garbage", [(8, 8, False), (4, 16, True), (8, 16, True)])
 def test_special3x3_channel_diagonal(env, W, C, garbage):
     """C == F >= 8 with 2 C W^2 <= S: the fast schedule's channel-diagonal
