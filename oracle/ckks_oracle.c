@@ -825,6 +825,103 @@ int ock_moddown(const ock_ctx* c, const u64* acc, int limbs, u64* out) {
   return 0;
 }
 
+/* ModDown by P' = P q_l, l = limbs - 1 (the fused relinearisation + rescale):
+ * z: [limbs+K][N] NTT domain over Q_limbs u P -> out [l][N] = round(z / P').
+ * Special limbs in this order: s = 0 is q_l, s = 1..K is p_{s-1}; the centred
+ * residue [z + h']_{P'} - h' (h' = (P'-1)/2) comes from the fast basis
+ * conversion with the FP64 overflow estimate summed in s order. */
+int ock_moddown_fused(const ock_ctx* c, const u64* z, int limbs, u64* out) {
+  const int L = c->L, K = c->K, l = limbs - 1, S = K + 1;
+  const size_t N = c->N;
+  if (l < 1) return -1;
+  int sp[MAXP];
+  sp[0] = l;
+  for (int k = 0; k < K; k++) sp[1 + k] = L + k;
+  u64* y = (u64*)malloc((size_t)S * N * sizeof(u64));
+  uint32_t* u = (uint32_t*)malloc(N * sizeof(uint32_t));
+  for (int s = 0; s < S; s++) {
+    const u64 m = c->q[sp[s]];
+    const size_t src = (s == 0) ? (size_t)l : (size_t)limbs + (size_t)(s - 1);
+    memcpy(y + (size_t)s * N, z + src * N, N * sizeof(u64));
+    ock_ntt_inv(c, sp[s], y + (size_t)s * N);
+    u64 hat = 1, Pp = 1;
+    for (int s2 = 0; s2 < S; s2++) {
+      Pp = mulmod(Pp, c->q[sp[s2]] % m, m);
+      if (s2 != s) hat = mulmod(hat, c->q[sp[s2]] % m, m);
+    }
+    const u64 hinv = invmod(hat, m);
+    const u64 hh = mulmod(submod(Pp, 1 % m, m), (m + 1) / 2, m);
+    for (size_t n = 0; n < N; n++)
+      y[(size_t)s * N + n] = mulmod(addmod(y[(size_t)s * N + n], hh, m), hinv, m);
+  }
+  for (size_t n = 0; n < N; n++) {
+    double v = 0.0;
+    for (int s = 0; s < S; s++) {
+      const double pinv = 1.0 / (double)c->q[sp[s]];
+      const double term = (double)y[(size_t)s * N + n] * pinv;
+      v = v + term;
+    }
+    u[n] = (uint32_t)v;
+  }
+#pragma omp parallel for
+  for (int i = 0; i < l; i++) {
+    const u64 qi = c->q[i];
+    u64 hm[MAXP];
+    u64 Pp = 1;
+    for (int s = 0; s < S; s++) {
+      u64 h = 1;
+      for (int s2 = 0; s2 < S; s2++) if (s2 != s) h = mulmod(h, c->q[sp[s2]] % qi, qi);
+      hm[s] = h;
+      Pp = mulmod(Pp, c->q[sp[s]] % qi, qi);
+    }
+    const u64 Ppinv = invmod(Pp, qi);
+    const u64 hq = mulmod(submod(Pp, 1 % qi, qi), (qi + 1) / 2, qi);
+    u64* conv = (u64*)malloc(N * sizeof(u64));
+    for (size_t n = 0; n < N; n++) {
+      u128 acc = 0;
+      for (int s = 0; s < S; s++) acc += (u128)y[(size_t)s * N + n] * hm[s];
+      u64 x = (u64)(acc % qi);
+      x = submod(x, mulmod((u64)u[n], Pp, qi), qi);
+      conv[n] = submod(x, hq, qi);
+    }
+    ock_ntt_fwd(c, i, conv);
+    for (size_t n = 0; n < N; n++)
+      out[(size_t)i * N + n] = mulmod(submod(z[(size_t)i * N + n], conv[n], qi), Ppinv, qi);
+    free(conv);
+  }
+  free(y);
+  free(u);
+  return 0;
+}
+
+/* key inner product of a key switch before its ModDown: acc_p over Q_limbs u P */
+static void ks_acc(const ock_ctx* c, const u64* d, int limbs, const u64* key, u64 g, u64* acc0, u64* acc1) {
+  const int K = c->K, E = limbs + K, LK = c->L + K;
+  const size_t N = c->N;
+  const int beta = digit_count(c, limbs);
+  u64* up = (u64*)malloc((size_t)beta * E * N * sizeof(u64));
+  ock_modup(c, d, limbs, up);
+  size_t* idx = (size_t*)malloc(N * sizeof(size_t));
+  for (size_t n = 0; n < N; n++) idx[n] = (g == 1) ? n : auto_index(c, n, g);
+#pragma omp parallel for
+  for (int t = 0; t < E; t++) {
+    const int pt = ext_prime(c, limbs, t);
+    const u64 m = c->q[pt];
+    for (size_t n = 0; n < N; n++) {
+      u128 s0 = 0, s1 = 0;
+      for (int j = 0; j < beta; j++) {
+        const u64 dv = up[((size_t)j * E + t) * N + idx[n]];
+        s0 += (u128)dv * key[(((size_t)j * 2 + 0) * LK + pt) * N + n];
+        s1 += (u128)dv * key[(((size_t)j * 2 + 1) * LK + pt) * N + n];
+      }
+      acc0[(size_t)t * N + n] = (u64)(s0 % m);
+      acc1[(size_t)t * N + n] = (u64)(s1 % m);
+    }
+  }
+  free(up);
+  free(idx);
+}
+
 int ock_keyswitch(const ock_ctx* c, const u64* d, int limbs, const u64* key,
                   u64 g, u64* ks0, u64* ks1) {
   const int L = c->L, K = c->K, E = limbs + K, LK = L + K;
@@ -998,9 +1095,13 @@ int ock_mult_plain(const ock_ctx* c, const u64* ct, int limbs, double ct_scale,
   return rc;
 }
 
+/* mult_cipher: tensor (d0, d1, d2), then the relinearisation and the rescale as
+ * ONE ModDown by P q_l: z_p = <ModUp(d2), rlk_p> + P d_p over Q u P, out_p =
+ * round(z_p / (P q_l)) on the remaining limbs (ock_moddown_fused). */
 int ock_mult_cipher(const ock_ctx* c, const u64* a, const u64* b, int limbs,
                     const u64* rk, u64* out) {
   if (limbs < 2) return -3;
+  const int L = c->L, K = c->K, E = limbs + K;
   const size_t N = c->N;
   const size_t P = (size_t)limbs * N;
   u64* d = (u64*)malloc(3 * P * sizeof(u64));
@@ -1013,12 +1114,24 @@ int ock_mult_cipher(const ock_ctx* c, const u64* a, const u64* b, int limbs,
       d[2 * P + o] = mulmod(a[P + o], b[P + o], q);
     }
   }
-  u64* ks = (u64*)malloc(2 * P * sizeof(u64));
-  ock_keyswitch(c, d + 2 * P, limbs, rk, 1, ks, ks + P);
-  ock_add(c, d, ks, 2, limbs, d);
-  const int rc = ock_rescale(c, d, limbs, out);
+  u64* z0 = (u64*)malloc((size_t)E * N * sizeof(u64));
+  u64* z1 = (u64*)malloc((size_t)E * N * sizeof(u64));
+  ks_acc(c, d + 2 * P, limbs, rk, 1, z0, z1);
+  for (int i = 0; i < limbs; i++) {
+    const u64 q = c->q[i];
+    u64 Pm = 1;
+    for (int k = 0; k < K; k++) Pm = mulmod(Pm, c->q[L + k] % q, q);
+    for (size_t n = 0; n < N; n++) {
+      const size_t o = (size_t)i * N + n;
+      z0[o] = addmod(z0[o], mulmod(d[o], Pm, q), q);
+      z1[o] = addmod(z1[o], mulmod(d[P + o], Pm, q), q);
+    }
+  }
+  int rc = ock_moddown_fused(c, z0, limbs, out);
+  if (!rc) rc = ock_moddown_fused(c, z1, limbs, out + (size_t)(limbs - 1) * N);
   free(d);
-  free(ks);
+  free(z0);
+  free(z1);
   return rc;
 }
 

@@ -113,6 +113,7 @@ struct TcBconvArgs {
   int kin, T, tb;      // GEMM inputs, targets of this launch, first target
   int nin;             // inputs read from memory (ModDown folded: kin = nin + 2)
   int lo, j, tab;      // ModUp digit
+  int s_ell, sp0;      // ModDown inputs: s < s_ell are Q limbs sp0 + s, the rest p_{s - s_ell}
   uint32_t m16;        // 2^16 (opaque to ptxas, see recombine)
 };
 
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
       const u64* c = a.md_pk + (std::size_t)tid * 4;
       yin[tid][0] = c[0];
       yin[tid][1] = c[1];
-      yin[tid][2] = a.pc[a.L + tid].q;
+      yin[tid][2] = a.pc[tid < a.s_ell ? a.sp0 + tid : a.L + (tid - a.s_ell)].q;
       yin[tid][3] = c[2];
       ypinv[tid] = a.md_pinv[tid];
     }
@@ -439,6 +440,34 @@ void modup_bconv_tc(const DevTables& t, const PolyList& ext, const PolyList& x, 
   a.j = j;
   a.tab = (limbs - 1) * t.dnum + j;
   dispatch_tc<0>(a, t.N, st);
+}
+
+void moddown_fused_conv_tc(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {
+  const int l = limbs - 1;
+  TcBconvArgs a{};
+  a.m16 = 1u << 16;
+  a.in = z;
+  a.out = conv;
+  a.pc = t.pc;
+  a.md_pk = t.md2_pk + (std::size_t)l * kMaxK * 4;
+  a.md_pinv = t.md2_pinv + (std::size_t)l * kMaxK;
+  a.md_phat = t.md2_phat + (std::size_t)l * t.L * kMaxK;
+  a.md_q = t.md2_q + (std::size_t)l * t.L * 4;
+  a.logN = t.logN;
+  a.limbs = l;
+  a.L = t.L;
+  a.K = t.K;
+  a.nin = t.K + 1;
+  a.T = l;
+  a.s_ell = 1;
+  a.sp0 = l;
+  if (a.nin + 2 <= 16) {
+    a.kin = (a.nin + 2 + 3) / 4 * 4;
+    dispatch_tc<1>(a, t.N, st);
+  } else {
+    a.kin = a.nin;
+    dispatch_tc<2>(a, t.N, st);
+  }
 }
 
 void moddown_conv_tc(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st) {

@@ -373,6 +373,47 @@ void Context::build_device_tables() {
   t.md_phat = upload(dev_allocs_, phat, stream_);
   t.md_q = upload(dev_allocs_, mq, stream_);
 
+  // Fused relinearisation + rescale tables: P' = P q_l, special s = 0: q_l, s >= 1: p_{s-1}
+  {
+    std::vector<u64> pk2((std::size_t)L * kMaxK * 4, 0);
+    std::vector<double> pinv2((std::size_t)L * kMaxK, 0.0);
+    std::vector<u64> phat2((std::size_t)L * L * kMaxK, 0);
+    std::vector<u64> mq2((std::size_t)L * L * 4, 0);
+    for (int l = 1; l < L && K + 1 <= kMaxK; ++l) {
+      auto sprime = [&](int sidx) { return sidx == 0 ? q[l] : q[L + sidx - 1]; };
+      auto Pp_mod = [&](u64 m) { return mulmod(prod_mod(q, L, L + K, -1, m), q[l] % m, m); };
+      auto half2 = [&](u64 m) { return mulmod(submod(Pp_mod(m), 1 % m, m), (m + 1) / 2, m); };
+      // P'/s mod m
+      auto hat = [&](int sidx, u64 m) {
+        return sidx == 0 ? prod_mod(q, L, L + K, -1, m) : mulmod(prod_mod(q, L, L + K, L + sidx - 1, m), q[l] % m, m);
+      };
+      for (int sidx = 0; sidx <= K; ++sidx) {
+        const u64 sv = sprime(sidx);
+        const u64 hinv = invmod(hat(sidx, sv), sv);
+        u64* c = pk2.data() + ((std::size_t)l * kMaxK + sidx) * 4;
+        c[0] = hinv;
+        c[1] = shoup(hinv, sv);
+        c[2] = half2(sv);
+        pinv2[(std::size_t)l * kMaxK + sidx] = 1.0 / (double)sv;
+      }
+      for (int i = 0; i < l; ++i) {
+        for (int sidx = 0; sidx <= K; ++sidx)
+          phat2[((std::size_t)l * L + i) * kMaxK + sidx] = to_mont(hat(sidx, q[i]), q[i]);
+        const u64 Pm = Pp_mod(q[i]);
+        const u64 Pinv = invmod(Pm, q[i]);
+        u64* c = mq2.data() + ((std::size_t)l * L + i) * 4;
+        c[0] = to_mont(Pm, q[i]);
+        c[1] = half2(q[i]);
+        c[2] = Pinv;
+        c[3] = shoup(Pinv, q[i]);
+      }
+    }
+    t.md2_pk = upload(dev_allocs_, pk2, stream_);
+    t.md2_pinv = upload(dev_allocs_, pinv2, stream_);
+    t.md2_phat = upload(dev_allocs_, phat2, stream_);
+    t.md2_q = upload(dev_allocs_, mq2, stream_);
+  }
+
   // Rescale tables
   std::vector<u64> rs((std::size_t)L * L * 4, 0);
   for (int l = 1; l < L; ++l)

@@ -216,6 +216,102 @@ std::vector<Ciphertext> keyswitch(Context& ctx, const std::vector<const u64*>& i
   return outs;
 }
 
+// Relinearisation fused with the rescale: for every job the
+// key inner product acc = <ModUp(d2), rlk> over Q u P, then z = acc + P (d0, d1)
+// is divided by P' = P q_l (l = limbs - 1) in ONE ModDown: the special limbs are
+// q_l and the K p's (z's q_l limb gets + P d_l, then the K + 1 limbs go to the
+// coefficient domain), the basis conversion runs over K + 1 inputs, and the
+// forward NTT's store computes (acc_i - conv_i) P'^-1 + d_i q_l^-1 = round(z / P')
+// on the l remaining limbs.  One rounding instead of ModDown + rescale, and no
+// rescale NTTs.  Mirrored by oracle/ckks_oracle.c ock_mult_cipher.
+std::vector<Ciphertext> keyswitch_relin_rescale(Context& ctx, const std::vector<const u64*>& inputs, int limbs,
+                                                const std::vector<KsJob>& jobs) {
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L(), K = ctx.K(), E = limbs + K;
+  const int l = limbs - 1;
+  const int beta = t.dig.beta(limbs);
+  ctx.stats.keyswitches += jobs.size();
+  const std::size_t ext_words = (std::size_t)beta * E * N;
+  BufPtr ext = modup_all(ctx, inputs, limbs);
+  std::vector<Ciphertext> outs;
+  outs.reserve(jobs.size());
+  constexpr int kChunk = kMaxPolys / 2;
+  for (std::size_t r0 = 0; r0 < jobs.size(); r0 += kChunk) {
+    const int R = (int)std::min<std::size_t>(kChunk, jobs.size() - r0);
+    BufPtr acc = ctx.alloc((std::size_t)R * 2 * E * N);
+    KsJobs kj{};
+    kj.n = R;
+    for (int r = 0; r < R; ++r) {
+      const int in = jobs[r0 + r].in;
+      kj.key[r] = ctx.key(jobs[r0 + r].key_id);
+      kj.ext[r] = ext->ptr + (std::size_t)in * ext_words;
+      kj.d[r] = inputs[in];
+      kj.acc[r] = acc->ptr + (std::size_t)r * 2 * E * N;
+      kj.g[r] = jobs[r0 + r].g;
+    }
+    ks_inner_product(t, kj, limbs, st);
+    // z_l = acc_l + P d_l on the dropped limb
+    PolyList za{}, dl{};
+    za.n = dl.n = 2 * R;
+    for (int r = 0; r < R; ++r)
+      for (int p = 0; p < 2; ++p) {
+        za.p[2 * r + p] = kj.acc[r] + (std::size_t)p * E * N + (std::size_t)l * N;
+        const KsJob& jb = jobs[r0 + r];
+        dl.p[2 * r + p] = const_cast<u64*>(p == 0 ? jb.add0 : jb.add1) + (std::size_t)l * N;
+      }
+    const HostTables& h = ctx.host();
+    u64 pm_l = 1;  // P mod q_l, Montgomery form
+    for (int k = 0; k < K; ++k) pm_l = mulmod(pm_l, h.q[L + k] % h.q[l], h.q[l]);
+    ew_axpy_limb(t, za, dl, to_mont(pm_l, h.q[l]), l, st);
+    // the K + 1 special limbs (q_l, p_0..p_K-1) to the coefficient domain
+    LimbSet zs{};
+    zs.nbase = R;
+    for (int r = 0; r < R; ++r) zs.base[r] = kj.acc[r] + (std::size_t)l * N;
+    zs.blocks_per_base = 2;
+    zs.block_stride = (long long)E * N;
+    zs.E = K + 1;
+    zs.ell = 1;
+    zs.p0 = l;
+    zs.L = L;
+    ntt_inverse(t, zs, st);
+    BufPtr conv = ctx.alloc((std::size_t)R * 2 * l * N);
+    PolyList cl{}, zl{}, al{}, ol{}, addl{};
+    cl.n = zl.n = al.n = ol.n = addl.n = 2 * R;
+    for (int r = 0; r < R; ++r) {
+      Ciphertext o = ctx.new_ct(l);
+      for (int p = 0; p < 2; ++p) {
+        const int i = 2 * r + p;
+        cl.p[i] = conv->ptr + (std::size_t)i * l * N;
+        zl.p[i] = kj.acc[r] + (std::size_t)p * E * N + (std::size_t)l * N;
+        al.p[i] = kj.acc[r] + (std::size_t)p * E * N;
+        ol.p[i] = p == 0 ? o.c0 : o.c1;
+        const KsJob& jb = jobs[r0 + r];
+        addl.p[i] = const_cast<u64*>(p == 0 ? jb.add0 : jb.add1);
+        addl.g[i] = 1;
+      }
+      outs.push_back(o);
+    }
+    moddown_fused_conv_tc(t, cl, zl, limbs, st);
+    NttEpilogue e{};
+    for (int i = 0; i < 2 * R; ++i) {
+      e.out[i] = ol.p[i];
+      e.src[i] = al.p[i];
+      e.add[i] = addl.p[i];
+      e.add_g[i] = 1;
+    }
+    e.cst = t.md2_q + (std::size_t)l * L * 4 + 2;  // P'^-1 mod q_i, Shoup
+    e.cst_stride = 4;
+    e.acst = t.rs + (std::size_t)l * L * 4;  // q_l^-1 mod q_i, Shoup
+    e.acst_stride = 4;
+    ntt_forward_epilogue(t, limbset(conv->ptr, 2 * R, (std::size_t)l * N, l, l, L), e, st);
+    ctx.stats.ntt_limbs += (std::size_t)R * 2 * (K + 1 + l);
+    ctx.stats.rescales += (std::size_t)R;
+  }
+  return outs;
+}
+
 // Rotate-and-sum: output r = sum over jobs of group r of rot(input, g), with
 // ONE ModDown per output (kernels.hpp KsSumJobs).  jobs[k].in indexes `inputs`
 // (c1 pointers, ModUp shared by repeated inputs), c0s[in] is that input's c0.
@@ -941,9 +1037,7 @@ std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphert
       jb.in = (int)k;
       jobs.push_back(jb);
     }
-    std::vector<Ciphertext> r = keyswitch(ctx, inputs, l, jobs);
-    for (Ciphertext& c : r) c.scale = 1.0;
-    std::vector<Ciphertext> rs = rescale_many(ctx, r);
+    std::vector<Ciphertext> rs = keyswitch_relin_rescale(ctx, inputs, l, jobs);
     for (std::size_t k = 0; k < idx.size(); ++k) {
       const std::size_t i = idx[k];
       rs[k].scale = A[i].scale * B[i].scale / (double)ctx.host().q[l - 1];

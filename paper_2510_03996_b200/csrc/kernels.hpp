@@ -38,6 +38,12 @@ struct DevTables {
   double* md_pinv = nullptr;      // [K] fl(1/p_k)
   u64* md_phat = nullptr;         // [L][kMaxK] (P/p_k) mod q_i, Montgomery form
   u64* md_q = nullptr;            // [L][4]: P mod q_i (Montgomery), (P-1)/2 mod q_i, P^{-1} mod q_i, shoup
+  // Fused relinearisation + rescale: ModDown by P' = P q_l (l = limbs - 1), special
+  // limbs s = 0: q_l, s = 1..K: p_{s-1}; same layouts as md_* per dropped limb l
+  u64* md2_pk = nullptr;          // [L][kMaxK][4]
+  double* md2_pinv = nullptr;     // [L][kMaxK]
+  u64* md2_phat = nullptr;        // [L][L][kMaxK]
+  u64* md2_q = nullptr;           // [L][L][4]
   // Rescale: [l][i][4]: q_l^{-1} mod q_i, shoup, q_l mod q_i, 0
   u64* rs = nullptr;
   // secret key, NTT domain standard form [L+K][N]
@@ -83,6 +89,8 @@ struct NttEpilogue {
   u64 add_g[kMaxPolys];
   const u64* cst;
   int cst_stride;
+  const u64* acst = nullptr;  // optional multiplier (value, Shoup) of `add` per limb
+  int acst_stride = 0;
 };
 void ntt_forward_epilogue(const DevTables& t, const LimbSet& set, const NttEpilogue& epi, cudaStream_t st);
 void ntt_inverse(const DevTables& t, const LimbSet& set, cudaStream_t st, const LimbSet* src = nullptr);
@@ -125,6 +133,12 @@ void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int
 // tensor-core basis conversions (bconv_tc.cu): ModUp of digit j, ModDown conversion
 void modup_bconv_tc(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, int j, cudaStream_t st);
 void moddown_conv_tc(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);
+// ModDown conversion by P' = P q_l for the fused relinearisation + rescale: z points at
+// limb l of each accumulator (q_l then the K special limbs, coefficient domain),
+// conv gets l = limbs - 1 limbs
+void moddown_fused_conv_tc(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);
+// acc[n] += x[n] * c (c Montgomery) on one limb (prime index `prime`) of every poly
+void ew_axpy_limb(const DevTables& t, const PolyList& acc, const PolyList& x, u64 c_mont, int prime, cudaStream_t st);
 bool bconv_tc_enabled();
 // Inner product with automorphism. For each job r: acc[r] ([2][limbs+K][N]) =
 //   sum_j sigma_g(D_j) (x) key_j   where D_j = d (own limbs, NTT c1) | ext (other limbs)

@@ -243,12 +243,19 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
     const u64 g = epi.add_g[pi];
     const u64 c = __ldg(epi.cst + (std::size_t)tl * epi.cst_stride);
     const u64 csh = __ldg(epi.cst + (std::size_t)tl * epi.cst_stride + 1);
+    const bool amul = epi.acst != nullptr;
+    const u64 ac = amul ? __ldg(epi.acst + (std::size_t)tl * epi.acst_stride) : 0;
+    const u64 acsh = amul ? __ldg(epi.acst + (std::size_t)tl * epi.acst_stride + 1) : 0;
     u64* outp = epi.out[pi] + off;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int k = (int)gaddr(base | (e << b));  // element index within the limb-poly
       u64 v = shoup_mul(sub_mod(srcp[k], x[e], q), c, csh, q);
-      if (addp) v = add_mod(v, addp[(g == 1) ? (unsigned)k : auto_src((unsigned)k, g, logN)], q);
+      if (addp) {
+        u64 av = addp[(g == 1) ? (unsigned)k : auto_src((unsigned)k, g, logN)];
+        if (amul) av = shoup_mul(av, ac, acsh, q);
+        v = add_mod(v, av, q);
+      }
       outp[k] = v;
     }
     return;

@@ -65,6 +65,14 @@ __global__ void k_lincomb_const(u64* out0, u64* out1, LincombTerms terms, const 
   (blockIdx.z ? out1 : out0)[o] = s;
 }
 
+// grid (N/256, npolys): acc[n] += x[n] * c (Montgomery constant) on one limb
+__global__ void k_axpy_limb(PolyList acc, PolyList x, u64 c, const PrimeConst* __restrict__ pc, int prime) {
+  const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst P = pc[prime];
+  u64* a = acc.p[blockIdx.y];
+  a[n] = add_mod(a[n], mont_mul(x.p[blockIdx.y][n], c, P), P.q);
+}
+
 __global__ void k_tensor(u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0, const u64* b1,
                          const PrimeConst* __restrict__ pc, int logN) {
   const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
@@ -480,6 +488,11 @@ void lincomb_const(const DevTables& t, u64* out0, u64* out1, const LincombTerms&
   if (terms.n == 0 || limbs == 0) return;
   k_lincomb_const<<<grid_for(t.N, limbs, 2), kThreads, 0, st>>>(out0, out1, terms, kc, t.pc, t.logN, limbs);
   launch_check("k_lincomb_const");
+}
+void ew_axpy_limb(const DevTables& t, const PolyList& acc, const PolyList& x, u64 c_mont, int prime, cudaStream_t st) {
+  if (acc.n == 0) return;
+  k_axpy_limb<<<dim3((unsigned)(t.N / kThreads), (unsigned)acc.n), kThreads, 0, st>>>(acc, x, c_mont, t.pc, prime);
+  launch_check("k_axpy_limb");
 }
 void ew_tensor(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
                const u64* b1, int limbs, cudaStream_t st) {
