@@ -211,9 +211,10 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
     FHEON_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const std::size_t ct_bytes = 2 * (std::size_t)(p.L + p.K) * ((std::size_t)1 << p.logN) * sizeof(u64);
     std::size_t want = std::min<std::size_t>(free_b / 4, 64 * ct_bytes * 3);
-    // resident weight plaintexts: up to a fifth of the free HBM (64 GiB cap); the
-    // keys, bootstrapping diagonals and masks need the rest
-    weight_cache_budget = std::min<std::size_t>(weight_cache_budget, free_b / 5);
+    // resident weight plaintexts: up to half of the free HBM (96 GiB cap); the keys
+    // (~40 GB for ResNet-20 at depth 25), the mask/diagonal cache (24 GiB) and the
+    // key-switch scratch pool need the rest
+    weight_cache_budget = std::min<std::size_t>(weight_cache_budget, free_b / 2);
     void* r = nullptr;
     if (want > 0 && cudaMallocAsync(&r, want, stream_) == cudaSuccess) cudaFreeAsync(r, stream_);
     cudaGetLastError();

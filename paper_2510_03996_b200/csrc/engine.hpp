@@ -159,7 +159,7 @@ class Context {
   // reference's weight_mode "preload" (model.hpp:46-48): built once by `make`
   // under `key`, then reused; past the budget new entries are built but not kept
   BufPtr weight_pt(const std::string& key, int limbs, double scale, const std::function<BufPtr()>& make);
-  std::size_t weight_cache_budget = (std::size_t)64 << 30;  // bytes (<= free HBM / 5 at creation); 0 disables
+  std::size_t weight_cache_budget = (std::size_t)96 << 30;  // bytes (<= free HBM / 2 at creation); 0 disables
   // device real-coefficient (unscaled, unrounded) encoding of a slot vector,
   // cached under `key` (block indicators of a layer geometry)
   const double* basis(const std::string& key, const std::vector<double>& slot_values);
