@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
@@ -315,7 +316,7 @@ struct SlotMove {
 };
 
 Ciphertext bsgs_moves(Context& ctx, const Ciphertext& x, const std::vector<SlotMove>& moves, std::size_t blk,
-                      std::size_t nblk, const std::string& key) {
+                      std::size_t nblk, const std::string& key, double value = 1.0) {
   std::vector<long> hs, gs;
   for (const SlotMove& mv : moves) {
     hs.push_back(mv.h);
@@ -348,7 +349,7 @@ Ciphertext bsgs_moves(Context& ctx, const Ciphertext& x, const std::vector<SlotM
       for (std::size_t i : idx)
         for (std::size_t c = 0; c < nblk; ++c) {
           const long p = (((long)(c * blk + moves[i].src) - gh.second) % Sl + Sl) % Sl;
-          v[(std::size_t)p] = 1.0;
+          v[(std::size_t)p] = value;
         }
       return v;
     }, x.limbs, ps));
@@ -1177,6 +1178,26 @@ PackedTensor avg_pool(Context& ctx, const PackedTensor& x, std::size_t k, std::s
 namespace {
 // merge_channel_slots (layers_misc.cpp:31-37): Horner chain by -1 (reference
 // schedule) or sum_c rot(piece_c, -c) as one batched key switch (fast)
+// Fast-schedule pooled-channel gather: out[c] = value * sums[c m] for c < C (zero
+// elsewhere), the head mask, channel cursors and -c placements of the reference
+// (layers_misc.cpp:159-165) as ONE masked slot permutation: shift c (m - 1)
+// split as baby (c mod B)(m - 1) + giant (c - c mod B)(m - 1) -- B - 1 hoisted
+// babies and ceil(C / B) - 1 giants instead of 2 (C - 1) rotations; one level.
+Ciphertext gather_block_heads(Context& ctx, const Ciphertext& sums, std::size_t C, std::size_t m, double value) {
+  std::size_t B = 1;
+  while (B * B < C) ++B;
+  std::vector<SlotMove> moves;
+  for (std::size_t c = 0; c < C; ++c) {
+    const long t = (long)(c * (m - 1));
+    const long h = (long)((c % B) * (m - 1));
+    moves.push_back({c, c * m, t - h, h});
+  }
+  char vk[32];
+  std::snprintf(vk, sizeof vk, "%.17g", value);
+  return bsgs_moves(ctx, sums, moves, (std::size_t)ctx.S(), 1,
+                    "heads:" + std::to_string(C) + ":" + std::to_string(m) + ":" + vk, value);
+}
+
 Ciphertext merge_channel_slots(Context& ctx, const std::vector<Ciphertext>& pieces) {
   if (ctx.fast_schedule()) return place_and_sum(ctx, pieces, 1);
   Ciphertext out = pieces.back();
@@ -1189,6 +1210,7 @@ Ciphertext merge_channel_slots(Context& ctx, const std::vector<Ciphertext>& piec
 Ciphertext global_avg_pool(Context& ctx, const PackedTensor& x) {
   const std::size_t W = x.width, C = x.channels, m = W * W;
   const Ciphertext sums = detail::block_sum(ctx, x.data, m);
+  if (ctx.fast_schedule() && C > 1) return gather_block_heads(ctx, sums, C, m, 1.0 / (double)m);
   const std::vector<Ciphertext> cur = channel_cursors(ctx, sums, C, m);
   const BufPtr head = pt_of(ctx, sums, range_mask(ctx, 0, 1, 1.0 / (double)m));
   const bool defer = ctx.fast_schedule();
@@ -1202,6 +1224,7 @@ Ciphertext whole_channel_pool(Context& ctx, const PackedTensor& x, std::size_t k
   const std::size_t W = x.width, C = x.channels, m = W * W;
   const Ciphertext v = mp(ctx, x.data, range_mask(ctx, 0, C * m, 1.0 / (double)(k * k)));
   const Ciphertext sums = detail::block_sum(ctx, v, m);
+  if (ctx.fast_schedule() && C > 1) return gather_block_heads(ctx, sums, C, m, 1.0);
   const std::vector<Ciphertext> cur = channel_cursors(ctx, sums, C, m);
   const BufPtr head = pt_of(ctx, sums, range_mask(ctx, 0, 1));
   const bool defer = ctx.fast_schedule();

@@ -196,6 +196,20 @@ def test_global_and_whole_channel_pool(env, W, C, F, s):
     check(out, ev, r, f"whole_channel W={W} C={C}", ctx.schedule())
 
 
+@pytest.mark.parametrize("W,C", [(4, 64), (8, 20), (6, 9), (2, 2)])
+def test_global_pool_many_channels(env, W, C):
+    """Wide channel counts (ResNet-20's 64 x 8 x 8 head): the fast schedule gathers
+    the C block heads as one baby-step giant-step slot permutation."""
+    ctx, ref = env
+    x = np.random.default_rng(9007 + C).uniform(-1, 1, (C, W, W))
+    out, ev, r = run_both(ctx, lambda v: fh.global_avg_pool(fh.PackedTensor(v, C, W)),
+                          lambda v: ref.pool(v, DEPTH, C, W, 1), x)
+    check(out, ev, r, f"global W={W} C={C}", ctx.schedule())
+    out, ev, r = run_both(ctx, lambda v: fh.whole_channel_pool(fh.PackedTensor(v, C, W), W),
+                          lambda v: ref.pool(v, DEPTH, C, W, 2, W), x)
+    check(out, ev, r, f"whole_channel W={W} C={C}", ctx.schedule())
+
+
 @pytest.mark.parametrize("W,C,F,s", cases(9006, 4))
 def test_fully_connected(env, W, C, F, s):
     ctx, ref = env
