@@ -33,6 +33,9 @@ struct BootParams {
   int cts_levels = 3;
   int stc_levels = 3;
   int cos_degree = 0;     // 0: chosen automatically
+  // linear transforms double-hoisted (babies kept over Q u P, one ModDown per
+  // giant); env FHEON_BOOT_DH=0 selects the single-hoisted schedule for A/B runs
+  bool double_hoist = true;
 };
 
 BootParams boot_params_of(const Params& p);
@@ -60,6 +63,7 @@ class Bootstrapper {
   struct Level {
     std::vector<long> babies;  // nonzero baby rotations
     std::vector<Giant> giants;
+    bool qp = false;           // plaintexts over Q u P (double-hoisted)
   };
   using Diag = std::vector<std::complex<double>>;
   using Mat = std::map<long, Diag>;

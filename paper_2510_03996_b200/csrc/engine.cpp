@@ -555,9 +555,10 @@ void encode_complex_coeffs_host(const HostTables& ht_, const double* re_in, cons
   }
 }
 
-BufPtr Context::encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale) {
+BufPtr Context::encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale,
+                               int special) {
   const std::size_t N = ht_.N;
-  BufPtr out = alloc((std::size_t)limbs * N);
+  BufPtr out = alloc((std::size_t)(limbs + special) * N);
   ++stats.encodes;
   cudaEvent_t* ev = nullptr;
   long long* h = staging_slot(&ev);
@@ -566,11 +567,14 @@ BufPtr Context::encode_complex(const double* re, const double* im, std::size_t n
   FHEON_CUDA(cudaMemcpyAsync(dcoef->ptr, h, N * sizeof(long long), cudaMemcpyHostToDevice, stream_));
   FHEON_CUDA(cudaEventRecord(*ev, stream_));
   coeffs_to_rns(dt_, out->ptr, reinterpret_cast<const long long*>(dcoef->ptr), limbs, stream_);
+  if (special > 0)
+    coeffs_to_rns(dt_, out->ptr + (std::size_t)limbs * N, reinterpret_cast<const long long*>(dcoef->ptr), special,
+                  stream_, ht_.p.L);
   LimbSet ls{};
   ls.base[0] = out->ptr;
   ls.nbase = 1;
   ls.blocks_per_base = 1;
-  ls.E = limbs;
+  ls.E = limbs + special;
   ls.ell = limbs;
   ls.L = ht_.p.L;
   ntt_forward(dt_, ls, stream_);

@@ -149,7 +149,8 @@ class Context {
   // encode `vals` at `scale` over `limbs` limbs into a device [limbs][N] NTT-domain buffer
   BufPtr encode(const double* vals, std::size_t n, int limbs, double scale);
   // complex slot values (re + i im), host special FFT
-  BufPtr encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale);
+  // special > 0: also the first `special` special primes (limbs + special rows, Q u P operands)
+  BufPtr encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale, int special = 0);
   // content-addressed cache over encode() (masks reused across a layer)
   BufPtr encode_cached(const std::vector<double>& vals, int limbs, double scale);
   // same cache keyed by a caller-chosen name (the slot values are built only on a miss)
@@ -284,6 +285,16 @@ std::vector<Ciphertext> rotate_many(Context& ctx, const std::vector<Ciphertext>&
 // rotated c0 terms are folded into the key-switch accumulator as P * c0)
 std::vector<Ciphertext> rotate_sum_many(Context& ctx,
                                         const std::vector<std::vector<std::pair<Ciphertext, long>>>& groups);
+// Double-hoisted baby-step giant-step linear transform (evaluator.cpp):
+// out = rescale(sum_g rot(sum_t pt_t (*) rot(x, babies[b_t]), rot_g)); a term's baby
+// index -1 is the identity; plaintexts are [limbs+K][N] over Q u P, encoded at
+// pt_scale_for(x) (at most 32 terms per giant)
+struct DhGiant {
+  long rot = 0;
+  std::vector<std::pair<int, BufPtr>> terms;
+};
+Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& babies,
+                               const std::vector<DhGiant>& giants);
 Ciphertext add(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext sub(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext add_plain(Context& ctx, const Ciphertext& a, const double* vals, std::size_t n);

@@ -320,13 +320,14 @@ struct SumJob {
   int in;
   int group;
 };
-std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*>& inputs,
-                                      const std::vector<const u64*>& c0s, int limbs, const std::vector<SumJob>& jobs,
-                                      int ngroups) {
+// Q u P accumulators of every group, [ngroups][2][limbs+K][N] (canonical, standard form):
+// acc_r = sum_{jobs of r} <sigma_g(ModUp(d)), key_g> + P sigma_g(c0) on the Q limbs
+BufPtr keyswitch_sum_accs(Context& ctx, const std::vector<const u64*>& inputs, const std::vector<const u64*>& c0s,
+                          int limbs, const std::vector<SumJob>& jobs, int ngroups) {
   const DevTables& t = ctx.dev();
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
-  const int L = ctx.L(), K = ctx.K(), E = limbs + K;
+  const int K = ctx.K(), E = limbs + K;
   const int beta = t.dig.beta(limbs);
   const std::size_t ext_words = (std::size_t)beta * E * N;
   ctx.stats.keyswitches += jobs.size();
@@ -340,8 +341,6 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
     for (std::size_t k = 0; k < by_group[r].size() && shared; ++k)
       shared = by_group[r][k]->g == by_group[0][k]->g && by_group[r][k]->in == by_group[r][0]->in;
   }
-  std::vector<Ciphertext> outs;
-  outs.reserve(ngroups);
   // accumulators of all groups, [2][limbs+K][N] each
   BufPtr accs = ctx.alloc((std::size_t)ngroups * 2 * E * N);
   auto acc_of = [&](int r) { return accs->ptr + (std::size_t)r * 2 * E * N; };
@@ -391,13 +390,25 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
       r0 += R;
     }
   }
-  // ModDown of every group's accumulator, 32 groups (64 polys) per pipeline
+  return accs;
+}
+
+// ModDown of Q u P accumulators ([2][limbs+K][N] each): round(acc / P) over the
+// Q limbs, 32 accumulators (64 polys) per pipeline
+std::vector<Ciphertext> moddown_accs(Context& ctx, const std::vector<u64*>& accp, int limbs) {
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L(), K = ctx.K(), E = limbs + K;
+  const int ngroups = (int)accp.size();
+  std::vector<Ciphertext> outs;
+  outs.reserve(ngroups);
   for (int r0 = 0; r0 < ngroups; r0 += kMaxPolys / 2) {
     const int R = std::min(kMaxPolys / 2, ngroups - r0);
     struct {
       u64* acc[kMaxPolys / 2];
     } kj{};
-    for (int r = 0; r < R; ++r) kj.acc[r] = acc_of(r0 + r);
+    for (int r = 0; r < R; ++r) kj.acc[r] = accp[r0 + r];
     LimbSet zs{};
     zs.nbase = R;
     for (int r = 0; r < R; ++r) zs.base[r] = kj.acc[r] + (std::size_t)limbs * N;
@@ -431,7 +442,100 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
   return outs;
 }
 
+std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*>& inputs,
+                                      const std::vector<const u64*>& c0s, int limbs, const std::vector<SumJob>& jobs,
+                                      int ngroups) {
+  BufPtr accs = keyswitch_sum_accs(ctx, inputs, c0s, limbs, jobs, ngroups);
+  const std::size_t stride = (std::size_t)2 * (limbs + ctx.K()) * ctx.N();
+  std::vector<u64*> accp(ngroups);
+  for (int r = 0; r < ngroups; ++r) accp[r] = accs->ptr + (std::size_t)r * stride;
+  return moddown_accs(ctx, accp, limbs);
+}
+
 }  // namespace
+
+// Double-hoisted baby-step giant-step transform:
+//   out = rescale( sum_g rot( ModDown( sum_t pt_{g,t} (*) B_{b(g,t)} ), G_g ) )
+// B_b = (P sigma_b(c0) + ks0_b, ks1_b) over Q u P is baby rotation b WITHOUT its
+// ModDown (one shared ModUp, one key inner product each); the identity baby is
+// (P c0, P c1) on Q and 0 on P.  The plaintexts live over Q u P, so each giant's
+// inner sum needs ONE ModDown instead of one per baby; the giant rotations are a
+// rotate-and-sum (one more ModDown) and the sum is rescaled once.
+Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& babies,
+                               const std::vector<DhGiant>& giants) {
+  require_valid(x, "linear transform");
+  require_depth(x, "linear transform");
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int limbs = x.limbs, K = ctx.K(), E = limbs + K, lv = limbs - 1;
+  const std::size_t accw = (std::size_t)2 * E * N;
+  const HostTables& h = ctx.host();
+  // baby accumulators
+  std::vector<SumJob> jobs;
+  for (std::size_t k = 0; k < babies.size(); ++k) {
+    ctx.record(0, babies[k]);
+    ctx.stats.rotations++;
+    const u64 g = ctx.galois(babies[k]);
+    if (g == 1) throw Error(ErrKind::internal, "double-hoisted transform: identity baby must be index -1");
+    jobs.push_back({g, 0, (int)k});
+  }
+  BufPtr accs = babies.empty() ? nullptr
+                               : keyswitch_sum_accs(ctx, {x.c1}, {x.c0}, limbs, jobs, (int)babies.size());
+  BufPtr ident;
+  bool need_ident = false;
+  for (const DhGiant& gi : giants)
+    for (const auto& [b, pt] : gi.terms) need_ident = need_ident || b < 0;
+  if (need_ident) {
+    ident = ctx.alloc(accw);
+    LimbConsts pc{};
+    for (int i = 0; i < limbs; ++i) {
+      u64 pm = 1 % h.q[i];
+      for (int k = 0; k < K; ++k) pm = mulmod(pm, h.q[ctx.L() + k] % h.q[i], h.q[i]);
+      pc.c[i] = pm;
+      pc.sh[i] = shoup(pm, h.q[i]);
+    }
+    ew_mul_const(t, plist({ident->ptr, ident->ptr + (std::size_t)E * N}), plist({x.c0, x.c1}), pc, limbs, st);
+    for (int p = 0; p < 2; ++p)
+      FHEON_CUDA(cudaMemsetAsync(ident->ptr + (std::size_t)p * E * N + (std::size_t)limbs * N, 0,
+                                 (std::size_t)K * N * sizeof(u64), st));
+  }
+  auto baby_ptr = [&](int b) { return b < 0 ? ident->ptr : accs->ptr + (std::size_t)b * accw; };
+  // inner sums over Q u P, one output accumulator per giant
+  BufPtr inner = ctx.alloc(giants.size() * accw);
+  for (std::size_t g0 = 0; g0 < giants.size(); g0 += kMacMaxOut) {
+    MacJobs jb{};
+    jb.nout = (int)std::min<std::size_t>(kMacMaxOut, giants.size() - g0);
+    for (int z = 0; z < jb.nout; ++z) {
+      const DhGiant& gi = giants[g0 + z];
+      if (gi.terms.empty() || gi.terms.size() > (std::size_t)kMacMaxTerms)
+        throw Error(ErrKind::internal, "double-hoisted transform: 1..32 terms per giant");
+      for (std::size_t j = 0; j < gi.terms.size(); ++j) {
+        jb.ct[z][j] = baby_ptr(gi.terms[j].first);
+        jb.c1_off[z][j] = (long long)E * (long long)N;
+        jb.pt[z][j] = gi.terms[j].second->ptr;
+      }
+      jb.nterm[z] = (int)gi.terms.size();
+      jb.out0[z] = inner->ptr + (g0 + z) * accw;
+      jb.out1[z] = jb.out0[z] + (std::size_t)E * N;
+    }
+    mac_pt(t, jb, E, st, limbs);
+  }
+  std::vector<u64*> accp(giants.size());
+  for (std::size_t g = 0; g < giants.size(); ++g) accp[g] = inner->ptr + g * accw;
+  std::vector<Ciphertext> rows = moddown_accs(ctx, accp, limbs);
+  const double sc = h.T[lv - 1] * (double)h.q[lv];  // plaintexts encoded at T_{lv-1} q_lv / scale(x)
+  std::vector<std::pair<Ciphertext, long>> terms;
+  for (std::size_t g = 0; g < giants.size(); ++g) {
+    rows[g].scale = sc;
+    terms.push_back({rows[g], giants[g].rot});
+    for (std::size_t j = 0; j < giants[g].terms.size(); ++j) {
+      ctx.stats.mult_plain++;
+      ctx.record(1, lv - 1);
+    }
+  }
+  return rescale_to_target(ctx, rotate_sum_many(ctx, {terms}))[0];
+}
 
 // out[r] = sum_k rot(groups[r][k].first, groups[r][k].second): every group's
 // rotations share one ModDown; repeated inputs share one ModUp.  All terms of

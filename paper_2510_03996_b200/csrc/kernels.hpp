@@ -208,7 +208,8 @@ struct MacJobs {
   int nterm[kMacMaxOut];
   int nout;
 };
-void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st);
+// ell >= 0: Q u P operands ([limbs][N], limbs ell.. on the special primes)
+void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st, int ell = -1);
 // Plaintext as a linear combination of cached real-coefficient basis vectors
 // (block-indicator encodings): coeff[k] = rint(scale * sum_b w_b basis_b[k]),
 // written as RNS limbs (coefficient domain, then forward NTT by the caller).
@@ -230,7 +231,7 @@ void mul_monomial_half(const DevTables& t, const PolyList& out, const PolyList& 
 
 // ---- encode / encrypt / keygen / decrypt
 // signed coefficients -> RNS coefficient domain [limbs][N]
-void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st);
+void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st, int p0 = 0);
 // CBD21 error polynomial for `stream_key` into limbs 0..nlimbs-1 (prime rule: i < ell ? i : L + i - ell)
 void sample_error(const DevTables& t, u64* out, u64 stream_key, int nlimbs, int ell, cudaStream_t st);
 // c1 = uniform(stream); c0 = m + e - c1 s (m, e NTT domain) over q_0..q_{limbs-1}

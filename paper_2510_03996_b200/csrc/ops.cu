@@ -343,10 +343,12 @@ __global__ void k_rescale_lift(PolyList r, PolyList last, const PrimeConst* __re
 // grid (nout, N/256, limbs): outputs fastest, so the CTAs of outputs that share
 // their terms (a conv's taps, a BSGS level's baby steps) read each term tile
 // from L2 instead of HBM
-__global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN) {
+// limb t < ell uses q_t, limb t >= ell the special prime p_{t - ell} (Q u P operands)
+__global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN, int ell, int L) {
   const std::size_t o = ((std::size_t)blockIdx.z << logN) + blockIdx.y * blockDim.x + threadIdx.x;
   const int z = blockIdx.x;
-  const PrimeConst P = pc[blockIdx.z];
+  const int t = (int)blockIdx.z;
+  const PrimeConst P = pc[t < ell ? t : L + (t - ell)];
   const int nt = jobs.nterm[z];
   u64 s0 = 0, s1 = 0;
   Acc128 a0, a1;
@@ -401,7 +403,7 @@ __global__ void k_mul_monomial_half(PolyList out, PolyList a, LimbConsts iq, con
 __global__ void k_coeffs_to_rns(u64* out, const long long* __restrict__ coeffs, const PrimeConst* __restrict__ pc,
                                 int logN) {
   const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
-  out[((std::size_t)blockIdx.y << logN) + n] = reduce_signed(coeffs[n], pc[blockIdx.y]);
+  out[((std::size_t)blockIdx.y << logN) + n] = reduce_signed(coeffs[n], pc[blockIdx.y]);  // pc offset by the launcher
 }
 __global__ void k_sample_error(u64* out, u64 key, const PrimeConst* __restrict__ pc, int logN, int ell, int L) {
   const std::size_t n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -596,18 +598,18 @@ void mul_monomial_half(const DevTables& t, const PolyList& out, const PolyList& 
   k_mul_monomial_half<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, iq, t.pc, t.logN);
   launch_check("k_mul_monomial_half");
 }
-void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st) {
+void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st, int ell) {
   if (jobs.nout == 0) return;
   const dim3 grid(jobs.nout, (unsigned)(t.N / kThreads), limbs);
-  k_mac<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN);
+  k_mac<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN, ell < 0 ? limbs : ell, t.L);
   launch_check("k_mac");
 }
 void encode_lincomb(const DevTables& t, u64* out, const LinComb& lc, double scale, int limbs, cudaStream_t st) {
   k_encode_lincomb<<<grid_for(t.N, 1), kThreads, 0, st>>>(out, lc, scale, t.pc, t.logN, limbs);
   launch_check("k_encode_lincomb");
 }
-void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st) {
-  k_coeffs_to_rns<<<grid_for(t.N, limbs), kThreads, 0, st>>>(out, coeffs, t.pc, t.logN);
+void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st, int p0) {
+  k_coeffs_to_rns<<<grid_for(t.N, limbs), kThreads, 0, st>>>(out, coeffs, t.pc + p0, t.logN);
   launch_check("k_coeffs_to_rns");
 }
 void sample_error(const DevTables& t, u64* out, u64 stream_key, int nlimbs, int ell, cudaStream_t st) {
