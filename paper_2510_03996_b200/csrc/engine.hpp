@@ -272,6 +272,9 @@ std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphert
 std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Ciphertext>& as, const std::vector<double>& cs);
 // sum_i cs[i] * xs[i] + c0 with one rescale (terms may sit at different levels)
 Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0);
+// the same landing exactly on (out_limbs, out_scale); every term needs >= out_limbs + 1 limbs
+Ciphertext lincomb_const_to(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0,
+                            int out_limbs, double out_scale);
 
 // ---------------------------------------------------------------- ops
 Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n);            // at the depth budget

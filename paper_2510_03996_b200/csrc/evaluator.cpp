@@ -1203,8 +1203,23 @@ Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const 
     require_depth(x, "mult_plain");
     l = std::min(l, x.limbs);
   }
+  return lincomb_const_to(ctx, xs, cs, c0, l - 1, ctx.host().T[l - 2]);
+}
+
+// The sum is formed at out_limbs + 1 limbs (terms' tails ignored), each constant
+// scaled by out_scale q_{out_limbs} / scale(x_i) and rounded, then ONE rescale:
+// the result lands exactly on (out_limbs, out_scale).
+Ciphertext lincomb_const_to(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0,
+                            int out_limbs, double out_scale) {
+  if (xs.empty() || xs.size() != cs.size()) throw Error(ErrKind::internal, "lincomb_const: bad term list");
+  const int l = out_limbs + 1;
+  for (const Ciphertext& x : xs) {
+    require_valid(x, "mult_plain");
+    require_depth(x, "mult_plain");
+    if (x.limbs < l) throw Error(ErrKind::internal, "lincomb_const: term below the target level");
+  }
   const HostTables& h = ctx.host();
-  const double t_out = h.T[l - 2];
+  const double t_out = out_scale;
   const std::size_t n = xs.size();
   std::vector<u64> kc(n * (std::size_t)l * 2);
   for (std::size_t i = 0; i < n; ++i) {

@@ -1384,9 +1384,18 @@ struct PsVal {
   double c = 0.0;  // constant part when ct is invalid
 };
 
-// evaluate node for every input; T[i][d] babies, G[i][j] giants
+// Evaluate a node for every input so that it lands EXACTLY on (tl[i] limbs,
+// scale ts[i]) -- no level alignment anywhere in the tree.  A split node
+// p = q G + r multiplies q, evaluated at (tl + 1, ts q_tl / scale(G)), by G
+// viewed at tl + 1 limbs (a zero-copy limb drop keeps G's scale), so the fused
+// relinearise-and-rescale lands on ts; r is evaluated at (tl, ts) directly and
+// the leaves are constant linear combinations of babies with per-term
+// constants c_d ts' q / scale(T_d) (one rescale).  Feasible whenever the node's
+// PS depth fits: the target level of a node of depth d is at most
+// level(x) - d (ps_cost).  T[i][d] babies, G[i][j] giants.
 std::vector<PsVal> ps_eval(Context& ctx, const PsNode& nd, std::vector<std::vector<Ciphertext>>& T,
-                           std::vector<std::vector<Ciphertext>>& G) {
+                           std::vector<std::vector<Ciphertext>>& G, const std::vector<int>& tl,
+                           const std::vector<double>& ts) {
   const std::size_t B = T.size();
   std::vector<PsVal> out(B);
   if (nd.leaf) {
@@ -1402,22 +1411,34 @@ std::vector<PsVal> ps_eval(Context& ctx, const PsNode& nd, std::vector<std::vect
           xs.push_back(T[i][d]);
           cs.push_back(nd.c[d]);
         }
-      out[i].ct = lincomb_const(ctx, xs, cs, nd.c[0]);
+      out[i].ct = lincomb_const_to(ctx, xs, cs, nd.c[0], tl[i], ts[i]);
     }
     return out;
   }
-  const std::vector<PsVal> q = ps_eval(ctx, *nd.q, T, G);
-  const std::vector<PsVal> r = ps_eval(ctx, *nd.r, T, G);
+  const HostTables& h = ctx.host();
+  std::vector<int> tq(B);
+  std::vector<double> sq(B);
+  std::vector<Ciphertext> gv(B);
+  for (std::size_t i = 0; i < B; ++i) {
+    gv[i] = G[i][nd.j - 1];
+    if (gv[i].limbs < tl[i] + 1) throw Error(ErrKind::internal, "Paterson-Stockmeyer: giant below its node");
+    gv[i].limbs = tl[i] + 1;  // zero-copy limb drop, scale kept
+    tq[i] = tl[i] + 1;
+    sq[i] = ts[i] * (double)h.q[tl[i]] / gv[i].scale;
+  }
+  const std::vector<PsVal> q = ps_eval(ctx, *nd.q, T, G, tq, sq);
+  const std::vector<PsVal> r = ps_eval(ctx, *nd.r, T, G, tl, ts);
   std::vector<Ciphertext> as, bs;
   for (std::size_t i = 0; i < B; ++i)
     if (q[i].ct.valid()) {
       as.push_back(q[i].ct);
-      bs.push_back(G[i][nd.j - 1]);
+      bs.push_back(gv[i]);
     }
   const std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
   std::size_t k = 0;
   for (std::size_t i = 0; i < B; ++i) {
-    Ciphertext p = q[i].ct.valid() ? prods[k++] : lincomb_const(ctx, {G[i][nd.j - 1]}, {q[i].c}, 0.0);
+    Ciphertext p = q[i].ct.valid() ? prods[k++] : lincomb_const_to(ctx, {G[i][nd.j - 1]}, {q[i].c}, 0.0, tl[i], ts[i]);
+    p.scale = ts[i];  // exact up to floating-point rounding of the scale bookkeeping
     out[i].ct = r[i].ct.valid() ? add(ctx, p, r[i].ct) : add_const(ctx, p, r[i].c);
   }
   return out;
@@ -1497,12 +1518,17 @@ std::vector<Ciphertext> cheb_eval_ps_many(Context& ctx, const std::vector<Cipher
     std::vector<Ciphertext> dbl = add_many(ctx, sq, sq);
     for (std::size_t i = 0; i < B; ++i) G[i].push_back(add_const(ctx, dbl[i], -1.0));
   }
-  const std::vector<PsVal> v = ps_eval(ctx, *best, T, G);
+  std::vector<int> tl(B);
+  std::vector<double> ts(B);
+  for (std::size_t i = 0; i < B; ++i) {
+    tl[i] = xs[i].limbs - want;
+    ts[i] = ctx.host().T[tl[i] - 1];
+  }
+  const std::vector<PsVal> v = ps_eval(ctx, *best, T, G, tl, ts);
   std::vector<Ciphertext> out(B);
   for (std::size_t i = 0; i < B; ++i) {
     out[i] = v[i].ct.valid() ? v[i].ct : add_const(ctx, sub(ctx, xs[i], xs[i]), v[i].c);
-    const int target = xs[i].limbs - want;
-    if (out[i].limbs > target) out[i] = level_down(ctx, out[i], target);
+    if (out[i].limbs > tl[i]) out[i] = level_down(ctx, out[i], tl[i]);
   }
   return out;
 }
