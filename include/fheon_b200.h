@@ -133,6 +133,16 @@ int fheon_ct_download(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);
 int fheon_ct_upload_async(fheon_ctx* ctx, const uint64_t* words, int limbs, double scale, fheon_ct** out);
 int fheon_ct_download_async(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* words);
 int fheon_ctx_wait_transfers(fheon_ctx* ctx);
+/* packed wire format (ciphertext serialization; the reference has none -- SURVEY 8(f) item 4,
+ * PAPER.md:541-566 describes the paper's serialized keys/ciphertexts): layout [2][limbs][N b_i / 64]
+ * uint64 words, limb i a little-endian bitstream of N canonical words of b_i = bit_length(q_i)
+ * bits.  At N = 2^16 with 60 + 23 x 50-bit limbs: 0.79 of the raw [2][limbs][N] words.  The
+ * (un)packing runs on the device, on the copy streams (async variants as above). */
+size_t fheon_ct_packed_words(const fheon_ctx* ctx, int limbs); /* 0 on a bad limb count */
+int fheon_ct_upload_packed(fheon_ctx* ctx, const uint64_t* packed, int limbs, double scale, fheon_ct** out);
+int fheon_ct_download_packed(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* packed);
+int fheon_ct_upload_packed_async(fheon_ctx* ctx, const uint64_t* packed, int limbs, double scale, fheon_ct** out);
+int fheon_ct_download_packed_async(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* packed);
 
 /* ---- backend ops (backend.hpp:134-153) */
 int fheon_rotate(fheon_ctx* ctx, const fheon_ct* x, long t, fheon_ct** out);

@@ -1160,3 +1160,57 @@ int ock_level_down(const ock_ctx* c, const u64* ct, int limbs, double scale,
   free(tmp);
   return rc;
 }
+
+/* ------------------------------------------------------------ packed wire format
+ * (the engine's fheon_ct_upload_packed / fheon_ct_download_packed, include/fheon_b200.h):
+ * [2][limbs] bitstreams, limb i = N canonical words of b_i = bit_length(q_i) bits each,
+ * coefficient k at stream bits [k b_i, (k+1) b_i), bit j of the stream = bit (j mod 64)
+ * of word j / 64.  Restated bit by bit (the device packs whole words). */
+static int bitlen64(u64 q) {
+  int b = 0;
+  while (b < 64 && (q >> b) != 0) ++b;
+  return b;
+}
+
+size_t ock_packed_words(const ock_ctx* c, int limbs) {
+  size_t w = 0;
+  for (int i = 0; i < limbs; ++i) w += c->N * (size_t)bitlen64(c->q[i]) / 64;
+  return 2 * w;
+}
+
+void ock_pack(const ock_ctx* c, const uint64_t* ct, int limbs, uint64_t* out) {
+  const size_t N = c->N;
+  memset(out, 0, ock_packed_words(c, limbs) * sizeof(u64));
+  size_t base = 0; /* bit position of the current limb's stream */
+  for (int p = 0; p < 2; ++p)
+    for (int i = 0; i < limbs; ++i) {
+      const int b = bitlen64(c->q[i]);
+      const u64* src = ct + ((size_t)p * limbs + i) * N;
+      for (size_t k = 0; k < N; ++k)
+        for (int j = 0; j < b; ++j)
+          if ((src[k] >> j) & 1u) {
+            const size_t bit = base + k * (size_t)b + (size_t)j;
+            out[bit / 64] |= (u64)1 << (bit % 64);
+          }
+      base += N * (size_t)b;
+    }
+}
+
+void ock_unpack(const ock_ctx* c, const uint64_t* in, int limbs, uint64_t* ct) {
+  const size_t N = c->N;
+  size_t base = 0;
+  for (int p = 0; p < 2; ++p)
+    for (int i = 0; i < limbs; ++i) {
+      const int b = bitlen64(c->q[i]);
+      u64* dst = ct + ((size_t)p * limbs + i) * N;
+      for (size_t k = 0; k < N; ++k) {
+        u64 v = 0;
+        for (int j = 0; j < b; ++j) {
+          const size_t bit = base + k * (size_t)b + (size_t)j;
+          v |= ((in[bit / 64] >> (bit % 64)) & 1u) << j;
+        }
+        dst[k] = v;
+      }
+      base += N * (size_t)b;
+    }
+}

@@ -104,6 +104,11 @@ int ock_level_down(const ock_ctx* c, const uint64_t* ct, int limbs,
                    double scale, int target_limbs, uint64_t* out,
                    double* out_scale);
 
+/* packed wire format of a [2][limbs][N] ciphertext (engine: fheon_ct_*_packed) */
+size_t ock_packed_words(const ock_ctx* c, int limbs);
+void ock_pack(const ock_ctx* c, const uint64_t* ct, int limbs, uint64_t* out);
+void ock_unpack(const ock_ctx* c, const uint64_t* in, int limbs, uint64_t* ct);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,10 @@ def lib():
         L.ock_mult_cipher.argtypes = [vp, _u64p, _u64p, C.c_int, _u64p, _u64p]
         L.ock_level_down.argtypes = [vp, _u64p, C.c_int, C.c_double, C.c_int, _u64p,
                                      C.POINTER(C.c_double)]
+        L.ock_packed_words.argtypes = [vp, C.c_int]
+        L.ock_packed_words.restype = C.c_size_t
+        L.ock_pack.argtypes = [vp, _u64p, C.c_int, _u64p]
+        L.ock_unpack.argtypes = [vp, _u64p, C.c_int, _u64p]
         _lib = L
     return _lib
 
@@ -239,6 +243,20 @@ class Oracle:
         tp = (C.c_long * n)(*[int(t) for t in ts])
         out = np.zeros((2, limbs, self.N), np.uint64)
         _chk(lib().ock_rotate_sum(self._c, cp, tp, n, limbs, kp, out), "rotate_sum")
+        return out
+
+    def pack(self, ct):
+        """packed wire format words of a [2][limbs][N] ciphertext"""
+        ct = np.ascontiguousarray(ct, np.uint64)
+        limbs = ct.shape[1]
+        out = np.zeros(lib().ock_packed_words(self._c, limbs), np.uint64)
+        lib().ock_pack(self._c, ct, limbs, out)
+        return out
+
+    def unpack(self, words, limbs):
+        words = np.ascontiguousarray(words, np.uint64)
+        out = np.zeros((2, limbs, self.N), np.uint64)
+        lib().ock_unpack(self._c, words, limbs, out)
         return out
 
     def rescale(self, ct):

@@ -100,6 +100,11 @@ SIGNATURES = {
     "fheon_rotate_sum": (C.c_int, [vp, pp, lp, C.c_size_t, pp]),
     "fheon_ct_upload_async": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
     "fheon_ct_download_async": (C.c_int, [vp, vp, u64p]),
+    "fheon_ct_packed_words": (C.c_size_t, [vp, C.c_int]),
+    "fheon_ct_upload_packed": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
+    "fheon_ct_download_packed": (C.c_int, [vp, vp, u64p]),
+    "fheon_ct_upload_packed_async": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
+    "fheon_ct_download_packed_async": (C.c_int, [vp, vp, u64p]),
     "fheon_ctx_wait_transfers": (C.c_int, [vp]),
     "fheon_add": (C.c_int, [vp, vp, vp, pp]),
     "fheon_sub": (C.c_int, [vp, vp, vp, pp]),

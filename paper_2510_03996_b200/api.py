@@ -267,6 +267,13 @@ class SlotContext:
             raise ShapeError(f'schedule must be one of {sorted(SCHEDULES)}, got "{schedule}"', 2)
         _check(_native.lib().fheon_ctx_set_schedule(self._h, SCHEDULES[schedule]))
 
+    def packed_words(self, limbs: int) -> int:
+        """uint64 words of one ciphertext with `limbs` limbs in the packed wire format."""
+        n = int(_native.lib().fheon_ct_packed_words(self._h, int(limbs)))
+        if n == 0:
+            raise ShapeError(f"bad limb count {limbs}", 2)
+        return n
+
     def wait_transfers(self):
         """Block until every asynchronous upload / download has completed."""
         _check(_native.lib().fheon_ctx_wait_transfers(self._h))
@@ -406,6 +413,33 @@ class SlotVector:
         fn = _native.lib().fheon_ct_upload_async if async_copy else _native.lib().fheon_ct_upload
         _check(fn(ctx._h, _u64ptr(w), w.shape[1], float(scale), C.byref(h)))
         return SlotVector(ctx, h)
+
+    @staticmethod
+    def from_packed(ctx: SlotContext, packed: np.ndarray, limbs: int, scale: float,
+                    async_copy: bool = False) -> "SlotVector":
+        """Upload a ciphertext in the packed wire format (include/fheon_b200.h:
+        fheon_ct_upload_packed): ctx.packed_words(limbs) uint64 words, unpacked on
+        the device.  async_copy as for from_words."""
+        want = ctx.packed_words(limbs)
+        if packed.dtype != np.uint64 or not packed.flags.c_contiguous or packed.size != want:
+            raise ShapeError(f"packed ciphertext must be {want} contiguous uint64 words", 2)
+        h = C.c_void_p()
+        fn = _native.lib().fheon_ct_upload_packed_async if async_copy else _native.lib().fheon_ct_upload_packed
+        _check(fn(ctx._h, _u64ptr(packed), int(limbs), float(scale), C.byref(h)))
+        return SlotVector(ctx, h)
+
+    def packed(self, out: Optional[np.ndarray] = None, async_copy: bool = False) -> np.ndarray:
+        """Download in the packed wire format (packed on the device)."""
+        want = self._ctx.packed_words(self.limbs())
+        if out is None:
+            if async_copy:
+                raise ShapeError("async download needs a caller-owned output buffer", 2)
+            out = np.zeros(want, np.uint64)
+        elif out.size != want or out.dtype != np.uint64 or not out.flags.c_contiguous:
+            raise ShapeError(f"output buffer must be {want} contiguous uint64 words", 2)
+        fn = _native.lib().fheon_ct_download_packed_async if async_copy else _native.lib().fheon_ct_download_packed
+        _check(fn(self._ctx._h, self._h, _u64ptr(out)))
+        return out
 
     def valid(self) -> bool:
         return bool(self._h)

@@ -293,6 +293,33 @@ int fheon_ct_download_async(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* w) {
     fheon::download_ct_async(*ctx->impl, ct->ct, w);
   });
 }
+size_t fheon_ct_packed_words(const fheon_ctx* ctx, int limbs) {
+  try {
+    return fheon::packed_words(*ctx->impl, limbs);
+  } catch (...) {
+    return 0;
+  }
+}
+int fheon_ct_upload_packed_async(fheon_ctx* ctx, const uint64_t* packed, int limbs, double scale, fheon_ct** out) {
+  return guard([&] {
+    if (limbs < 1 || limbs > ctx->impl->L()) throw fheon::Error(fheon::ErrKind::shape, "upload: bad limb count");
+    *out = wrap(fheon::upload_ct_packed_async(*ctx->impl, packed, limbs, scale));
+  });
+}
+int fheon_ct_download_packed_async(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* packed) {
+  return guard([&] {
+    need(ct, "ciphertext");
+    fheon::download_ct_packed_async(*ctx->impl, ct->ct, packed);
+  });
+}
+int fheon_ct_upload_packed(fheon_ctx* ctx, const uint64_t* packed, int limbs, double scale, fheon_ct** out) {
+  const int rc = fheon_ct_upload_packed_async(ctx, packed, limbs, scale, out);
+  return rc != 0 ? rc : fheon_ctx_wait_transfers(ctx);
+}
+int fheon_ct_download_packed(fheon_ctx* ctx, const fheon_ct* ct, uint64_t* packed) {
+  const int rc = fheon_ct_download_packed_async(ctx, ct, packed);
+  return rc != 0 ? rc : fheon_ctx_wait_transfers(ctx);
+}
 int fheon_ctx_wait_transfers(fheon_ctx* ctx) {
   return guard([&] { fheon::wait_transfers(*ctx->impl); });
 }

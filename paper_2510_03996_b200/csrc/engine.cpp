@@ -197,8 +197,14 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
   int dev = 0;
   FHEON_CUDA(cudaGetDevice(&dev));
   FHEON_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  FHEON_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
-  FHEON_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  // copy streams at the highest priority: their (un)pack kernels are scheduled ahead of
+  // the compute stream's grids, so the copy engines are not left waiting behind them
+  int prio_least = 0, prio_greatest = 0;
+  FHEON_CUDA(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+  FHEON_CUDA(cudaStreamCreateWithPriority(&h2d_, cudaStreamNonBlocking, prio_greatest));
+  FHEON_CUDA(cudaStreamCreateWithPriority(&d2h_, cudaStreamNonBlocking, prio_greatest));
+  FHEON_CUDA(cudaStreamCreateWithPriority(&unpack_, cudaStreamNonBlocking, prio_greatest));
+  FHEON_CUDA(cudaStreamCreateWithPriority(&pack_, cudaStreamNonBlocking, prio_greatest));
   {
     cudaMemPool_t pool;
     FHEON_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -250,11 +256,15 @@ Context::~Context() {
   }
   if (h2d_) cudaStreamSynchronize(h2d_);
   if (d2h_) cudaStreamSynchronize(d2h_);
+  if (unpack_) cudaStreamSynchronize(unpack_);
+  if (pack_) cudaStreamSynchronize(pack_);
   for (auto& [e, b] : held_) cudaEventDestroy(e);
   held_.clear();
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (d2h_) cudaStreamDestroy(d2h_);
+  if (unpack_) cudaStreamDestroy(unpack_);
+  if (pack_) cudaStreamDestroy(pack_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 

@@ -197,6 +197,10 @@ class Context {
   // device -> host copy of the previous one overlap)
   cudaStream_t h2d_stream() const { return h2d_; }
   cudaStream_t d2h_stream() const { return d2h_; }
+  // (un)pack kernels of the packed transfers: off the copy streams, so the copy
+  // engines stream back to back while the previous ciphertext is (un)packed
+  cudaStream_t unpack_stream() const { return unpack_; }
+  cudaStream_t pack_stream() const { return pack_; }
   cudaEvent_t take_event();
   void give_event(cudaEvent_t e);
   // keep `buf` alive until `done` has completed (a device -> host copy in flight)
@@ -209,7 +213,7 @@ class Context {
   HostTables ht_;
   DevTables dt_{};
   cudaStream_t stream_ = nullptr;
-  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr, unpack_ = nullptr, pack_ = nullptr;
   std::vector<cudaEvent_t> event_pool_;
   std::vector<std::pair<cudaEvent_t, BufPtr>> held_;
   int depth_budget_ = 0;
@@ -321,5 +325,10 @@ void download_ct(Context& ctx, const Ciphertext& ct, u64* host);
 Ciphertext upload_ct_async(Context& ctx, const u64* host, int limbs, double scale);
 void download_ct_async(Context& ctx, const Ciphertext& ct, u64* host);
 void wait_transfers(Context& ctx);
+// packed wire format (kernels.hpp PackLayout): [2][limbs][N b_i / 64] words, b_i = bit_length(q_i)
+PackLayout pack_layout(const Context& ctx, int limbs);
+std::size_t packed_words(const Context& ctx, int limbs);
+Ciphertext upload_ct_packed_async(Context& ctx, const u64* host, int limbs, double scale);
+void download_ct_packed_async(Context& ctx, const Ciphertext& ct, u64* host);
 
 }  // namespace fheon

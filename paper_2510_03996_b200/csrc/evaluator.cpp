@@ -1347,7 +1347,71 @@ void download_ct_async(Context& ctx, const Ciphertext& ct, u64* host) {
   ctx.hold_until(done, ct.buf);  // the buffer outlives the copy
 }
 
+// ---- packed wire format (kernels.hpp PackLayout)
+PackLayout pack_layout(const Context& ctx, int limbs) {
+  if (limbs < 1 || limbs > 64) throw Error(ErrKind::shape, "packed transfer: bad limb count");
+  PackLayout lay{};
+  lay.limbs = limbs;
+  lay.off[0] = 0;
+  for (int i = 0; i < limbs; ++i) {
+    lay.bits[i] = 64 - __builtin_clzll(ctx.host().q[i]);
+    lay.off[i + 1] = lay.off[i] + (long long)(ctx.N() * (std::size_t)lay.bits[i] / 64);
+  }
+  return lay;
+}
+
+std::size_t packed_words(const Context& ctx, int limbs) { return 2 * (std::size_t)pack_layout(ctx, limbs).off[limbs]; }
+
+Ciphertext upload_ct_packed_async(Context& ctx, const u64* host, int limbs, double scale) {
+  const PackLayout lay = pack_layout(ctx, limbs);
+  const std::size_t pw = 2 * (std::size_t)lay.off[limbs];
+  const std::size_t words = 2 * (std::size_t)limbs * ctx.N();
+  Ciphertext ct;
+  ct.buf = std::make_shared<DevBuffer>(&ctx, words, ctx.h2d_stream());
+  ct.c0 = ct.buf->ptr;
+  ct.c1 = ct.buf->ptr + (std::size_t)limbs * ctx.N();
+  ct.limbs = limbs;
+  ct.id = ctx.next_id();
+  ct.scale = scale;
+  BufPtr stage = std::make_shared<DevBuffer>(&ctx, pw, ctx.h2d_stream());
+  FHEON_CUDA(cudaMemcpyAsync(stage->ptr, host, pw * sizeof(u64), cudaMemcpyHostToDevice, ctx.h2d_stream()));
+  cudaEvent_t landed = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(landed, ctx.h2d_stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.unpack_stream(), landed, 0));
+  ctx.give_event(landed);
+  unpack_limbs(ctx.dev(), plist({ct.c0, ct.c1}), stage->ptr, lay, ctx.unpack_stream());
+  cudaEvent_t up = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(up, ctx.unpack_stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.stream(), up, 0));  // the staging buffer is freed after this point
+  ctx.give_event(up);
+  return ct;
+}
+
+void download_ct_packed_async(Context& ctx, const Ciphertext& ct, u64* host) {
+  const PackLayout lay = pack_layout(ctx, ct.limbs);
+  const std::size_t pw = 2 * (std::size_t)lay.off[ct.limbs];
+  cudaEvent_t ready = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(ready, ctx.stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.pack_stream(), ready, 0));
+  ctx.give_event(ready);
+  BufPtr stage = std::make_shared<DevBuffer>(&ctx, pw, ctx.pack_stream());
+  pack_limbs(ctx.dev(), stage->ptr, plist({ct.c0, ct.c1}), lay, ctx.pack_stream());
+  cudaEvent_t packed = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(packed, ctx.pack_stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.d2h_stream(), packed, 0));
+  ctx.give_event(packed);
+  FHEON_CUDA(cudaMemcpyAsync(host, stage->ptr, pw * sizeof(u64), cudaMemcpyDeviceToHost, ctx.d2h_stream()));
+  // one event per held buffer: reaping returns each event to the pool once
+  for (BufPtr held : {ct.buf, stage}) {
+    cudaEvent_t done = ctx.take_event();
+    FHEON_CUDA(cudaEventRecord(done, ctx.d2h_stream()));
+    ctx.hold_until(done, std::move(held));
+  }
+}
+
 void wait_transfers(Context& ctx) {
+  FHEON_CUDA(cudaStreamSynchronize(ctx.unpack_stream()));
+  FHEON_CUDA(cudaStreamSynchronize(ctx.pack_stream()));
   FHEON_CUDA(cudaStreamSynchronize(ctx.h2d_stream()));
   FHEON_CUDA(cudaStreamSynchronize(ctx.d2h_stream()));
   ctx.reap_transfers(true);

@@ -221,6 +221,18 @@ struct LinComb {
 };
 void encode_lincomb(const DevTables& t, u64* out, const LinComb& lc, double scale, int limbs, cudaStream_t st);
 
+// ---- packed wire format: every limb's N canonical words as a contiguous
+// bitstream of b_i = bit_length(q_i) bits per coefficient (N b_i / 64 words,
+// coefficient k at bits [k b_i, (k+1) b_i), little-endian within and across words)
+struct PackLayout {
+  int bits[64];             // b_i per limb
+  long long off[64 + 1];    // word offset of limb i within one packed poly; off[limbs] = poly words
+  int limbs;
+};
+// src polys ([limbs][N] each) -> dst ([npolys][off[limbs]] words)
+void pack_limbs(const DevTables& t, u64* dst, const PolyList& src, const PackLayout& lay, cudaStream_t st);
+void unpack_limbs(const DevTables& t, const PolyList& dst, const u64* src, const PackLayout& lay, cudaStream_t st);
+
 // ---- bootstrapping helpers
 // ModRaise: in[p] = coefficient-domain limb 0 (mod q_0); out[p] ([L][N]) = centred lift to q_0..q_{L-1}
 void modraise(const DevTables& t, const PolyList& out, const PolyList& in, int L, cudaStream_t st);

@@ -373,6 +373,41 @@ __global__ void k_encode_lincomb(u64* out, LinComb lc, double scale, const Prime
   for (int i = 0; i < limbs; ++i) out[((std::size_t)i << logN) + n] = reduce_signed(c, pc[i]);
 }
 
+// ------------------------------------------------------------ packed wire format
+// grid (words/256, limbs, npolys): one packed output word per thread
+__global__ void k_pack(u64* __restrict__ dst, PolyList src, PackLayout lay, int logN) {
+  const int i = blockIdx.y;
+  const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nw = lay.off[i + 1] - lay.off[i];
+  if (w >= nw) return;
+  const int b = lay.bits[i];
+  const u64* s = src.p[blockIdx.z] + ((std::size_t)i << logN);
+  const long long bit0 = w * 64;
+  long long k = bit0 / b;
+  const int o = (int)(bit0 - k * b);  // bits of coefficient k already in the previous word
+  u64 v = s[k] >> o;
+  int filled = b - o;
+  for (++k; filled < 64 && k < ((long long)1 << logN); ++k) {
+    v |= s[k] << filled;
+    filled += b;
+  }
+  dst[(std::size_t)blockIdx.z * lay.off[lay.limbs] + lay.off[i] + w] = v;
+}
+// grid (N/256, limbs, npolys): one coefficient per thread
+__global__ void k_unpack(PolyList dst, const u64* __restrict__ src, PackLayout lay, int logN) {
+  const int i = blockIdx.y;
+  const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = lay.bits[i];
+  const u64* s = src + (std::size_t)blockIdx.z * lay.off[lay.limbs] + lay.off[i];
+  const long long bit = (long long)k * b;
+  const long long w = bit >> 6;
+  const int o = (int)(bit & 63);
+  u64 v = s[w] >> o;
+  if (o + b > 64) v |= s[w + 1] << (64 - o);
+  if (b < 64) v &= (1ULL << b) - 1;
+  dst.p[blockIdx.z][((std::size_t)i << logN) + k] = v;
+}
+
 // ------------------------------------------------------------ bootstrapping
 // grid (N/256, npolys)
 __global__ void k_modraise(PolyList out, PolyList in, const PrimeConst* __restrict__ pc, int logN, int L) {
@@ -587,6 +622,19 @@ void rescale_lift(const DevTables& t, const PolyList& r, const PolyList& last, i
   launch_check("k_rescale_lift");
 }
 
+void pack_limbs(const DevTables& t, u64* dst, const PolyList& src, const PackLayout& lay, cudaStream_t st) {
+  if (src.n == 0 || lay.limbs == 0) return;
+  long long maxw = 0;
+  for (int i = 0; i < lay.limbs; ++i) maxw = std::max(maxw, lay.off[i + 1] - lay.off[i]);
+  const dim3 grid((unsigned)((maxw + kThreads - 1) / kThreads), lay.limbs, src.n);
+  k_pack<<<grid, kThreads, 0, st>>>(dst, src, lay, t.logN);
+  launch_check("k_pack");
+}
+void unpack_limbs(const DevTables& t, const PolyList& dst, const u64* src, const PackLayout& lay, cudaStream_t st) {
+  if (dst.n == 0 || lay.limbs == 0) return;
+  k_unpack<<<grid_for(t.N, lay.limbs, dst.n), kThreads, 0, st>>>(dst, src, lay, t.logN);
+  launch_check("k_unpack");
+}
 void modraise(const DevTables& t, const PolyList& out, const PolyList& in, int L, cudaStream_t st) {
   if (out.n == 0) return;
   k_modraise<<<grid_for(t.N, 1, out.n), kThreads, 0, st>>>(out, in, t.pc, t.logN, L);

@@ -340,3 +340,37 @@ def test_async_transfers_bit_exact(small):
         ctx.wait_transfers()
         for c, t, o in zip(cts, [1, 3, -2, 5], outs):
             assert np.array_equal(o, orc.rotate(c, t, orc.rotation_key(t)))
+
+
+@pytest.mark.parametrize("limbs", [1, 4, 6])
+def test_packed_transfers_bit_exact(small, limbs):
+    """Packed wire format (fheon_ct_*_packed): the device packs to exactly the
+    oracle's bitstream and unpacks it back to the same words (sync and async)."""
+    ctx, orc = small
+    rng = np.random.default_rng(90 + limbs)
+    ct = _oracle_ct(orc, rng, counter=70)[1][:, :limbs].copy()
+    packed = orc.pack(ct)
+    assert ctx.packed_words(limbs) == packed.size
+    x = fh.SlotVector.from_packed(ctx, packed, limbs, orc.T[limbs - 1])
+    assert np.array_equal(x.words(), ct)
+    assert np.array_equal(fh.SlotVector.from_words(ctx, ct, orc.T[limbs - 1]).packed(), packed)
+    out = np.zeros(packed.size, np.uint64)
+    y = fh.SlotVector.from_packed(ctx, packed, limbs, orc.T[limbs - 1], async_copy=True)
+    y.packed(out=out, async_copy=True)
+    ctx.wait_transfers()
+    assert np.array_equal(out, packed)
+
+
+def test_packed_transfers_config2_roundtrip():
+    """BASELINE configs[1] size (N=2^16, 60 + 23 x 50-bit limbs): packed size
+    0.79 of the raw words, device pack/unpack round trip bit-exact on a rotated
+    ciphertext (size-independent property: unpack(pack(x)) == x)."""
+    cfg = fh.ContextConfig(1 << 16, 1 << 15, 23, fh.CryptoMetadata(60, 50, 3), limbs=24, special_limbs=8,
+                           special_bits=60, seed=2001)
+    ctx = fh.SlotContext(cfg)
+    x = fh.rotate(fh.SlotVector.encode_top(ctx, np.random.default_rng(3).uniform(-1, 1, 1 << 15)), 5)
+    w = x.words()
+    p = x.packed()
+    bits = sum(int(q).bit_length() for q in ctx.primes[:24])
+    assert bits <= 60 + 23 * 51 and p.size == 2 * (1 << 16) * bits // 64
+    assert np.array_equal(fh.SlotVector.from_packed(ctx, p, 24, x.scale()).words(), w)

@@ -220,3 +220,36 @@ def test_constant_plaintext_is_degree_zero(small):
     o = small
     m = o.encode_coeffs(np.full(o.S, 0.375), 2.0 ** 40)
     assert m[0] == round(0.375 * 2 ** 40) and not m[1:].any()
+
+
+def test_packed_wire_format_definition(small):
+    """oracle pack == the definition with Python big integers: limb streams of
+    bit_length(q_i) bits per canonical word, concatenated little-endian
+    (N >= 1024, as the engine requires, so every limb stream is whole words)."""
+    o = small
+    rng = np.random.default_rng(5)
+    limbs = 3
+    ct = np.stack([np.stack([rng.integers(0, int(o.primes[i]), o.N, dtype=np.uint64) for i in range(limbs)])
+                   for _ in range(2)])
+    big, pos = 0, 0
+    for p in range(2):
+        for i in range(limbs):
+            b = _bits(o.primes[i])
+            for v in ct[p, i]:
+                big |= int(v) << pos
+                pos += b
+    words = o.pack(ct)
+    assert words.size * 64 == pos and pos == 2 * o.N * sum(_bits(o.primes[i]) for i in range(limbs))
+    assert [int(w) for w in words] == [(big >> (64 * k)) & ((1 << 64) - 1) for k in range(words.size)]
+    assert np.array_equal(o.unpack(words, limbs), ct)
+
+
+def test_packed_wire_format_extremes(small):
+    """all-zero and all-(q_i - 1) words survive the round trip (no bit bleeds
+    into the neighbouring coefficient)."""
+    o = small
+    for limbs in (1, 6):
+        top = np.stack([np.stack([np.full(o.N, int(o.primes[i]) - 1, np.uint64) for i in range(limbs)])
+                        for _ in range(2)])
+        for ct in (np.zeros_like(top), top):
+            assert np.array_equal(o.unpack(o.pack(ct), limbs), ct)
