@@ -187,10 +187,13 @@ __device__ __forceinline__ void lazy_flush(u64& s0, u64& s1, Acc128& a0, Acc128&
 // 128-bit accumulator never exceeds q * 2^64; job results add mod q.
 __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc, const u64* __restrict__ md_q,
                                int logN, int limbs, int L, int K, DigitOwner dig) {
-  // grid (groups, N/256, E): groups vary fastest -- the groups of a hoisted stage
-  // use the same key list, so their CTAs share each key slice through L2
+  // grid (groups, N/512, E): groups vary fastest -- the groups of a hoisted stage
+  // use the same key list, so their CTAs share each key slice through L2.  Two
+  // adjacent coefficients per thread: the per-job and per-CTA setup (constants,
+  // job pointers, digit owner) is amortised over both, key words and the
+  // accumulator move as 16-byte pairs; same products, same order per coefficient.
   const std::size_t N = (std::size_t)1 << logN;
-  const unsigned n = blockIdx.y * blockDim.x + threadIdx.x;
+  const unsigned n = 2 * (blockIdx.y * blockDim.x + threadIdx.x);
   const int t = blockIdx.z;
   const int r = blockIdx.x;
   const int E = limbs + K;
@@ -199,32 +202,48 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
   const int beta = dig.beta;
   const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;
   const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;  // P mod q_t, Montgomery form
-  u64 s0 = 0, s1 = 0;
+  const std::size_t LKN = (std::size_t)(L + K) * N;
+  u64 s0[2] = {0, 0}, s1[2] = {0, 0};
   const int chunk = lazy_chunk(beta);
-  Acc128 a0, a1;
+  Acc128 a0[2], a1[2];
   int cnt = 0;
   for (int jb = jobs.begin[r]; jb < jobs.begin[r + 1]; ++jb) {
     const u64 g = jobs.g[jb];
-    const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
+    unsigned src[2];
+    src[0] = (g == 1) ? n : auto_src(n, g, logN);
+    src[1] = (g == 1) ? n + 1 : auto_src(n + 1, g, logN);
     const u64* key = jobs.key[jb];
     const u64* ext = jobs.ext[jb];
     const u64* d = jobs.d[jb];
     for (int j = 0; j < beta; ++j) {
-      const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+      const u64* vb = j == jown ? d + (std::size_t)t * N : ext + ((std::size_t)j * E + t) * N;
       const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
-      a0.mac(v, kj[n]);
-      a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
+      const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(kj + n);
+      const ulonglong2 ka = *reinterpret_cast<const ulonglong2*>(kj + LKN + n);
+      const u64 v0 = vb[src[0]], v1 = vb[src[1]];
+      a0[0].mac(v0, kb.x);
+      a1[0].mac(v0, ka.x);
+      a0[1].mac(v1, kb.y);
+      a1[1].mac(v1, ka.y);
     }
-    if (t < limbs) a0.mac(jobs.c0[jb][(std::size_t)t * N + src], pm);
+    if (t < limbs) {
+      const u64* c0 = jobs.c0[jb] + (std::size_t)t * N;
+      a0[0].mac(c0[src[0]], pm);
+      a0[1].mac(c0[src[1]], pm);
+    }
     if (++cnt == chunk) {
-      lazy_flush(s0, s1, a0, a1, P);
+      lazy_flush(s0[0], s1[0], a0[0], a1[0], P);
+      lazy_flush(s0[1], s1[1], a0[1], a1[1], P);
       cnt = 0;
     }
   }
-  if (cnt) lazy_flush(s0, s1, a0, a1, P);
+  if (cnt) {
+    lazy_flush(s0[0], s1[0], a0[0], a1[0], P);
+    lazy_flush(s0[1], s1[1], a0[1], a1[1], P);
+  }
   u64* acc = jobs.acc[r];
-  acc[(std::size_t)t * N + n] = s0;
-  acc[((std::size_t)E + t) * N + n] = s1;
+  *reinterpret_cast<ulonglong2*>(acc + (std::size_t)t * N + n) = make_ulonglong2(s0[0], s0[1]);
+  *reinterpret_cast<ulonglong2*>(acc + ((std::size_t)E + t) * N + n) = make_ulonglong2(s1[0], s1[1]);
 }
 
 // grid (groups, N/256, E): groups fastest (every group uses the same keys)
@@ -581,7 +600,7 @@ void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStr
 void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.ngroups == 0) return;
   TimedScope ts(t, kKsInner, st);
-  const dim3 grid(jobs.ngroups, (unsigned)(t.N / kThreads), limbs + t.K);
+  const dim3 grid(jobs.ngroups, (unsigned)(t.N / (2 * kThreads)), limbs + t.K);
   k_ks_inner_sum<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs,
                                                                                  t.L, t.K, DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner_sum");
