@@ -453,6 +453,23 @@ def model_runs(args):
                "limbs": em.ctx.L, "bootstraps": em.n_boot, "rotations": r.stats["rotations"],
                "keyswitches": r.stats["keyswitches"], "gpu_launches": r.stats["launches"],
                "data": "synthetic seeded input, seeded random weights (no datasets/weights in the container)"}
+        if name == "resnet20_reference_spec":
+            # keyplan block mode (model_run.cpp:150 key_mode): keys of one block resident at a time
+            preload_key_bytes = em.ctx.key_bytes()
+            em.infer(x, key_mode="block")
+            rb = em.infer(x, key_mode="block", verify_keys=True)
+            est = M.keyplan.estimate_memory(rb.plan, em.memory_model())
+            ref_est = M.keyplan.estimate_memory(rb.plan, M.keyplan.MemoryModel.reference_model(
+                spec.ring_dimension, spec.depth_budget, 3))
+            rec["key_mode_block"] = {
+                "s_per_image": round(rb.wall_ms / 1e3, 4), "blocks": len(rb.plan.blocks),
+                "trace_check_ok": rb.trace_check.ok(), "rotations_checked": rb.trace_check.rotations_checked,
+                "keys_generated_per_image": rb.key_residency["generated"],
+                "peak_key_bytes": rb.key_residency["peak_key_bytes"], "preload_key_bytes": preload_key_bytes,
+                "estimate": {"total_keys": est.total_keys, "peak_resident_keys": est.resident_keys,
+                             "preload_bytes": est.preload_bytes, "peak_bytes": est.peak_bytes,
+                             "reference_memory_model_preload_bytes": ref_est.preload_bytes}}
+            em.infer(x)  # back to preload residency for the comparisons below
         if have_ref:
             path = spec.write(tempfile.mkdtemp())
             rl, rows, _, rwall = sref.infer(path, x)

@@ -99,6 +99,15 @@ int fheon_set_strict_keys(fheon_ctx* ctx, int strict); /* 1: missing key is an e
 /* key_id: 0 = relinearisation, else Galois element; out [dnum][2][L+K][N] standard form */
 int fheon_key_download(fheon_ctx* ctx, uint64_t key_id, uint64_t* out);
 size_t fheon_key_count(const fheon_ctx* ctx);
+/* key residency for keyplan block mode (keyplan.hpp:69-112 BlockPlan; model_run.cpp:150 key_mode):
+ * resident evaluation-key bytes; generate a block's rotation keys ahead of it (stream-ordered,
+ * no host sync); drop keys the next block does not use (freed after their last enqueued use,
+ * regenerated bit-identically on demand); counters of generations / drops since the last
+ * fheon_ctx_reset_stats */
+uint64_t fheon_key_bytes(const fheon_ctx* ctx);
+int fheon_prefetch_rotation_keys(fheon_ctx* ctx, const long* steps, size_t n);
+int fheon_drop_rotation_keys(fheon_ctx* ctx, const long* steps, size_t n);
+int fheon_key_events(const fheon_ctx* ctx, uint64_t* gens, uint64_t* drops);
 
 /* ---- ciphertexts (SlotVector, backend.hpp:108-132) */
 void fheon_ct_free(fheon_ct* ct);

@@ -61,6 +61,8 @@ def lib():
         L.sref_time_rotate.argtypes = [_sz, _sz, C.c_int, C.c_long, C.c_int, C.POINTER(C.c_double)]
         L.sref_infer.argtypes = [C.c_char_p, _dp, _sz, _dp, _sz, _szp, C.POINTER(C.c_double), _ip, _sz, _szp,
                                  C.c_char_p, _sz, _lp, _sz, _szp]
+        L.sref_layer_keys.argtypes = [C.c_char_p, _lp, _sz, _szp, _ip, _sz, _szp]
+        L.sref_plan.argtypes = [C.c_int, _sz, _lp, _sz, _ip, _lp, _sz, _lp, _sz, _lp, _sz, _szp, _lp]
         _lib = L
     return _lib
 
@@ -239,3 +241,42 @@ def conv_depth_cost(C_, F, k, stride, pad, mode, variant, W_in) -> int:
     if rc:
         raise RefError(lib().sref_last_error().decode(), rc)
     return out.value
+
+
+def layer_keys(spec_path: str):
+    """The reference's BuiltModel::layer_keys (model_spec.cpp:944-950) for a spec:
+    [(usage dict {index: count}, ends_block)] per top-level layer."""
+    cap = 1 << 16
+    ent = np.zeros(3 * cap, dtype=np.int64)
+    ends = np.zeros(4096, dtype=np.int32)
+    ne, nl = C.c_size_t(), C.c_size_t()
+    rc = lib().sref_layer_keys(spec_path.encode(), ent.ctypes.data_as(_lp), cap, C.byref(ne),
+                               ends.ctypes.data_as(_ip), 4096, C.byref(nl))
+    if rc:
+        raise RefError(lib().sref_last_error().decode(), rc)
+    out = [({}, bool(ends[i])) for i in range(nl.value)]
+    for m in range(ne.value):
+        out[int(ent[3 * m])][0][int(ent[3 * m + 1])] = int(ent[3 * m + 2])
+    return out
+
+
+def plan(mode: int, layers, ranges=(), events=()):
+    """The reference's plan_single_block (0) / plan_blocks (1) / plan_blocks(ranges) (2)
+    + verify_trace on `layers` [(usage dict, ends_block)] and `events` [(kind, value)]
+    (kind 0 rotation, 4 "layer:<value>" marker).  Returns (blocks [(first, last, nkeys)],
+    union size, peak resident, violations, unused keys, rotations checked)."""
+    ent = [(i, k, c) for i, (u, _) in enumerate(layers) for k, c in sorted(u.items())]
+    ent_a = np.array(ent if ent else [(0, 0, 0)], dtype=np.int64).reshape(-1)
+    ends = np.array([int(e) for _, e in layers] or [0], dtype=np.int32)
+    rg = np.array(list(ranges) or [(0, 0)], dtype=np.int64).reshape(-1)
+    ev = np.array(list(events) or [(1, 0)], dtype=np.int64).reshape(-1)
+    blocks = np.zeros(3 * 4096, dtype=np.int64)
+    nb = C.c_size_t()
+    out = np.zeros(5, dtype=np.int64)
+    rc = lib().sref_plan(mode, len(layers), ent_a.ctypes.data_as(_lp), len(ent), ends.ctypes.data_as(_ip),
+                         rg.ctypes.data_as(_lp), len(ranges), ev.ctypes.data_as(_lp), len(events),
+                         blocks.ctypes.data_as(_lp), 4096, C.byref(nb), out.ctypes.data_as(_lp))
+    if rc:
+        raise RefError(lib().sref_last_error().decode(), rc)
+    bl = [tuple(int(v) for v in blocks[3 * b:3 * b + 3]) for b in range(nb.value)]
+    return bl, int(out[0]), int(out[1]), int(out[2]), int(out[3]), int(out[4])

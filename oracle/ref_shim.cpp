@@ -20,6 +20,7 @@
 
 #include "slotcnn/backend.hpp"
 #include "slotcnn/chebyshev.hpp"
+#include "slotcnn/keyplan.hpp"
 #include "slotcnn/layers.hpp"
 #include "slotcnn/model.hpp"
 #include "slotcnn/packing.hpp"
@@ -346,6 +347,86 @@ int sref_infer(const char* spec_path, const double* input, std::size_t n_in,
       }
       *n_ev = m;
     }
+  });
+}
+
+// ----------------------------------------------------------------- keyplan
+// BuiltModel::layer_keys (model_spec.cpp:944-950) of a spec: entries (layer, index,
+// count) flattened, ends_block per layer.
+int sref_layer_keys(const char* spec_path, long* entries, std::size_t cap, std::size_t* n_entries,
+                    int* ends, std::size_t layer_cap, std::size_t* n_layers) {
+  return guard([&] {
+    const BuiltModel model = build_model(ModelSpec::from_json_file(spec_path));
+    const std::vector<LayerKeys> lk = model.layer_keys();
+    std::size_t m = 0;
+    for (std::size_t i = 0; i < lk.size(); ++i) {
+      if (i < layer_cap) ends[i] = lk[i].ends_block ? 1 : 0;
+      for (const auto& [idx, cnt] : lk[i].keys.usage) {
+        if (m < cap) {
+          entries[3 * m] = (long)i;
+          entries[3 * m + 1] = idx;
+          entries[3 * m + 2] = cnt;
+        }
+        ++m;
+      }
+    }
+    *n_entries = m;
+    *n_layers = lk.size();
+  });
+}
+
+// plan_single_block (mode 0) / plan_blocks (1) / plan_blocks with ranges (2)
+// (keyplan.cpp:319-368) over layers given as entries (layer, index, count), then
+// verify_trace (keyplan.cpp:370-421) of events (kind 0 rotation / 4 marker
+// "layer:<value>:x" / other, value).  blocks: 3 longs (first, last, keys) each;
+// out: union size, peak resident, violations, unused keys, rotations checked.
+int sref_plan(int mode, std::size_t n_layers, const long* entries, std::size_t n_entries, const int* ends,
+              const long* ranges, std::size_t n_ranges, const long* ev, std::size_t n_ev, long* blocks,
+              std::size_t block_cap, std::size_t* n_blocks, long* out) {
+  return guard([&] {
+    std::vector<LayerKeys> lk(n_layers);
+    for (std::size_t i = 0; i < n_layers; ++i) {
+      lk[i].name = "L" + std::to_string(i);
+      lk[i].ends_block = ends[i] != 0;
+    }
+    for (std::size_t m = 0; m < n_entries; ++m) lk[(std::size_t)entries[3 * m]].keys.add(entries[3 * m + 1], entries[3 * m + 2]);
+    BlockPlan plan;
+    if (mode == 0) {
+      plan = plan_single_block(lk);
+    } else if (mode == 1) {
+      plan = plan_blocks(lk);
+    } else {
+      std::vector<std::pair<std::size_t, std::size_t>> r;
+      for (std::size_t k = 0; k < n_ranges; ++k) r.push_back({(std::size_t)ranges[2 * k], (std::size_t)ranges[2 * k + 1]});
+      plan = plan_blocks(lk, r);
+    }
+    std::vector<TraceEvent> events;
+    for (std::size_t k = 0; k < n_ev; ++k) {
+      TraceEvent e{};
+      if (ev[2 * k] == 0) {
+        e.kind = TraceEvent::Kind::rotation;
+        e.rotation_index = ev[2 * k + 1];
+      } else if (ev[2 * k] == 4) {
+        e.kind = TraceEvent::Kind::marker;
+        e.label = "layer:" + std::to_string(ev[2 * k + 1]) + ":x";
+      } else {
+        e.kind = TraceEvent::Kind::mult_plain;
+        e.level_after = (int)ev[2 * k + 1];
+      }
+      events.push_back(e);
+    }
+    const TraceCheck tc = verify_trace(plan, events);
+    for (std::size_t b = 0; b < plan.blocks.size() && b < block_cap; ++b) {
+      blocks[3 * b] = (long)plan.blocks[b].first_layer;
+      blocks[3 * b + 1] = (long)plan.blocks[b].last_layer;
+      blocks[3 * b + 2] = (long)plan.blocks[b].keys.size();
+    }
+    *n_blocks = plan.blocks.size();
+    out[0] = (long)plan.union_keys.size();
+    out[1] = (long)plan.peak_resident_keys;
+    out[2] = (long)tc.violations.size();
+    out[3] = (long)tc.unused_keys.size();
+    out[4] = (long)tc.rotations_checked;
   });
 }
 

@@ -101,6 +101,10 @@ SIGNATURES = {
     "fheon_ct_upload_async": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
     "fheon_ct_download_async": (C.c_int, [vp, vp, u64p]),
     "fheon_ct_packed_words": (C.c_size_t, [vp, C.c_int]),
+    "fheon_key_bytes": (C.c_uint64, [vp]),
+    "fheon_prefetch_rotation_keys": (C.c_int, [vp, C.POINTER(C.c_long), C.c_size_t]),
+    "fheon_drop_rotation_keys": (C.c_int, [vp, C.POINTER(C.c_long), C.c_size_t]),
+    "fheon_key_events": (C.c_int, [vp, u64p, u64p]),
     "fheon_ct_upload_packed": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),
     "fheon_ct_download_packed": (C.c_int, [vp, vp, u64p]),
     "fheon_ct_upload_packed_async": (C.c_int, [vp, u64p, C.c_int, C.c_double, pp]),

@@ -309,6 +309,25 @@ class SlotContext:
     def set_strict_keys(self, strict: bool):
         _check(_native.lib().fheon_set_strict_keys(self._h, int(bool(strict))))
 
+    def key_bytes(self) -> int:
+        """HBM bytes of the resident evaluation keys."""
+        return int(_native.lib().fheon_key_bytes(self._h))
+
+    def prefetch_rotation_keys(self, steps: Sequence[int]):
+        """Generate the rotation keys of `steps` now (stream-ordered, no host sync)."""
+        arr = (C.c_long * max(1, len(steps)))(*[int(s) for s in steps])
+        _check(_native.lib().fheon_prefetch_rotation_keys(self._h, arr, len(steps)))
+
+    def drop_rotation_keys(self, steps: Sequence[int]):
+        """Evict the rotation keys of `steps` (regenerated bit-identically on demand)."""
+        arr = (C.c_long * max(1, len(steps)))(*[int(s) for s in steps])
+        _check(_native.lib().fheon_drop_rotation_keys(self._h, arr, len(steps)))
+
+    def key_events(self) -> Dict[str, int]:
+        g, d = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        _check(_native.lib().fheon_key_events(self._h, _u64ptr(g), _u64ptr(d)))
+        return {"generated": int(g[0]), "dropped": int(d[0])}
+
     def key_count(self) -> int:
         return int(_native.lib().fheon_key_count(self._h))
 

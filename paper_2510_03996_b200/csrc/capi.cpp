@@ -219,6 +219,32 @@ int fheon_set_strict_keys(fheon_ctx* ctx, int strict) {
   return guard([&] { ctx->impl->strict_keys = strict != 0; });
 }
 size_t fheon_key_count(const fheon_ctx* ctx) { return ctx->impl->num_keys(); }
+int fheon_key_events(const fheon_ctx* ctx, uint64_t* gens, uint64_t* drops) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (gens) *gens = ctx->impl->stats.key_gens;
+    if (drops) *drops = ctx->impl->stats.key_drops;
+  });
+}
+uint64_t fheon_key_bytes(const fheon_ctx* ctx) {
+  return (uint64_t)ctx->impl->num_keys() * ctx->impl->key_words() * sizeof(uint64_t);
+}
+int fheon_prefetch_rotation_keys(fheon_ctx* ctx, const long* steps, size_t n) {
+  return guard([&] {
+    for (size_t i = 0; i < n; ++i) {
+      const fheon::u64 g = ctx->impl->galois(steps[i]);
+      if (g != 1) ctx->impl->gen_key(g);  // stream-ordered, no host sync
+    }
+  });
+}
+int fheon_drop_rotation_keys(fheon_ctx* ctx, const long* steps, size_t n) {
+  return guard([&] {
+    for (size_t i = 0; i < n; ++i) {
+      const fheon::u64 g = ctx->impl->galois(steps[i]);
+      if (g != 1) ctx->impl->drop_key(g);  // freed in stream order after its last use
+    }
+  });
+}
 
 int fheon_key_download(fheon_ctx* ctx, uint64_t key_id, uint64_t* out) {
   return guard([&] {

@@ -497,6 +497,7 @@ const u64* Context::key(u64 key_id) {
 
 void Context::gen_key(u64 key_id) {
   if (keys_.count(key_id)) return;
+  ++stats.key_gens;
   const Params& p = ht_.p;
   const int L = p.L, K = p.K, NP = L + K;
   const std::size_t N = ht_.N, LN = (std::size_t)NP * N;

@@ -23,6 +23,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -98,6 +99,7 @@ struct TraceEvent {
 struct OpStats {
   std::uint64_t rotations = 0, keyswitches = 0, mult_plain = 0, mult_cipher = 0, rescales = 0, ntt_limbs = 0,
                 encodes = 0, adds = 0, launches = 0, bootstraps = 0;
+  std::uint64_t key_gens = 0, key_drops = 0;  // key residency (keyplan block mode)
 };
 
 struct KernelTimer {
@@ -139,6 +141,11 @@ class Context {
   void gen_key(u64 key_id);
   bool has_key(u64 key_id) const { return keys_.count(key_id) != 0; }
   void drop_keys() { keys_.clear(); }
+  // pinned keys (relinearisation, conjugation, bootstrapping rotations) are never dropped
+  void pin_key(u64 key_id) { pinned_keys_.insert(key_id); }
+  void drop_key(u64 key_id) {
+    if (!pinned_keys_.count(key_id) && keys_.erase(key_id)) ++stats.key_drops;
+  }
   std::size_t key_words() const;
   std::size_t num_keys() const { return keys_.size(); }
   bool strict_keys = false;
@@ -224,6 +231,7 @@ class Context {
 
  private:
   std::map<u64, BufPtr> keys_;
+  std::set<u64> pinned_keys_;
   std::map<std::string, BufPtr> basis_;
   struct PtEntry {
     std::vector<double> vals;

@@ -27,6 +27,7 @@ from typing import Dict, List, Optional, Tuple
 import numpy as np
 
 from . import api as fh
+from . import keyplan
 
 
 # ----------------------------------------------------------------- spec
@@ -641,6 +642,22 @@ def build(spec: ModelSpec) -> List[Built]:
     return layers
 
 
+def ends_block(b: Built) -> bool:
+    """BuiltLayer::ends_block (model_spec.cpp:521, 555, 577, 708-710): the layer
+    shrinks the spatial grid -- a strided conv or pool, a global reduction, or
+    a residual unit containing one."""
+    L = b.src
+    if b.type == "conv":
+        return int(L.params.get("stride", 1)) > 1
+    if b.type == "avg_pool":
+        return int(L.params.get("stride", 2)) > 1
+    if b.type in ("global_avg_pool", "whole_channel_pool"):
+        return True
+    if b.type == "residual":
+        return any(ends_block(c) for c in b.body) or (bool(b.downsample) and ends_block(b.downsample[0]))
+    return False
+
+
 def ledger_rows(layers: List[Built], budget: int) -> List[Tuple[str, int, int, bool]]:
     """Top-level (name, level_in, level_out, is_bootstrap) rows the built model
     will record (the reference infer()'s report rows), without running it."""
@@ -721,6 +738,11 @@ class InferResult:
     wall_ms: float
     layer_ms: Dict[str, float]
     stats: Dict[str, int]
+    # keyplan (model_run.cpp:148-153): the plan under the requested key mode, the
+    # trace replayed against it, and key residency observed on the engine
+    plan: Optional[keyplan.BlockPlan] = None
+    trace_check: Optional[keyplan.TraceCheck] = None
+    key_residency: Optional[Dict[str, int]] = None
 
 
 class EncryptedModel:
@@ -731,6 +753,8 @@ class EncryptedModel:
         self.layers = build(spec)
         self.n_boot = count_bootstraps(self.layers)
         self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule))
+        self._layer_keys: Optional[List[keyplan.LayerKeys]] = None
+        self._pinned_keys = self.ctx.key_count()  # relinearisation / bootstrapping keys made at creation
         if spec.weight_mode == "lazy":
             self.ctx.set_weight_cache(0)
         if self.ctx.depth_budget() != spec.depth_budget:
@@ -776,21 +800,86 @@ class EncryptedModel:
             timings[b.name] = timings.get(b.name, 0.0) + (time.perf_counter() - t0) * 1e3
         return out
 
-    def infer(self, x: np.ndarray, time_layers: bool = False) -> InferResult:
-        """Encrypt, run every layer on the GPU, decrypt the logits (model_run.cpp:100-159)."""
+    def layer_keys(self) -> List[keyplan.LayerKeys]:
+        """Per top-level layer, the rotation indices (with use counts) this engine
+        issues -- BuiltModel::layer_keys (model_spec.cpp:944-950), derived by one
+        recorded probe inference instead of the reference's derive_* algebra (the
+        rotation schedule depends on shapes only; under the reference schedule the
+        sets equal the reference's).  Cached."""
+        if self._layer_keys is None:
+            x = np.zeros((self.spec.input_channels, self.spec.input_width, self.spec.input_width))
+            rec = self.ctx.attach_recorder()
+            try:
+                v = fh.SlotVector.encode(self.ctx, x.reshape(-1))
+                out = []
+                for b in self.layers:
+                    rec.clear()
+                    v = self._run(b, v, None)
+                    ks = keyplan.KeySet()
+                    for t in rec.rotation_indices():
+                        ks.add(t)
+                    out.append(keyplan.LayerKeys(b.name, ks, ends_block(b)))
+            finally:
+                self.ctx.detach_recorder()
+            self._layer_keys = out
+        return self._layer_keys
+
+    def memory_model(self) -> keyplan.MemoryModel:
+        """MemoryModel::for_context with the engine's true key size; the keys made at
+        context creation (relinearisation, conjugation, bootstrapping) are the fixed part."""
+        c = self.ctx
+        return keyplan.MemoryModel.for_engine(c.N, c.L, c.K, c.dnum, self._pinned_keys)
+
+    def infer(self, x: np.ndarray, time_layers: bool = False, key_mode: str = "preload",
+              verify_keys: bool = False) -> InferResult:
+        """Encrypt, run every layer on the GPU, decrypt the logits (model_run.cpp:100-159).
+
+        key_mode (model.hpp:52 KeyMode, model_run.cpp:150): "preload" keeps every
+        rotation key resident (generated on first use); "block" makes the keys of
+        plan_blocks' block b resident before its first layer and drops, after its
+        last layer, those the next block does not use (pinned relinearisation /
+        bootstrapping keys stay) -- peak key memory = the largest block instead of
+        the union.  verify_keys records the trace with layer markers and replays it
+        against the plan (verify_trace)."""
+        if key_mode not in ("preload", "block"):
+            raise fh.ShapeError(f'key mode must be "preload" or "block", got "{key_mode}"', 2)
         x = np.asarray(x, np.float64)
         if x.shape != (self.spec.input_channels, self.spec.input_width, self.spec.input_width):
             raise fh.ShapeError(f"input tensor is {x.shape}, the model expects "
                                 f"{(self.spec.input_channels, self.spec.input_width, self.spec.input_width)}", 2)
+        plan = None
+        if key_mode == "block" or verify_keys:
+            lk = self.layer_keys()
+            plan = keyplan.plan_blocks(lk) if key_mode == "block" else keyplan.plan_single_block(lk)
+        rec = self.ctx.attach_recorder() if verify_keys else None
+        events: List[keyplan.TraceEvent] = []
         self.ctx.reset_stats()
+        peak_key_bytes = 0
         t0 = time.perf_counter()
         v = fh.SlotVector.encode(self.ctx, x.reshape(-1))
         ledger = []
         timings = {} if time_layers else None
-        for b in self.layers:
+        for i, b in enumerate(self.layers):
+            if key_mode == "block":
+                blk = plan.blocks[plan.block_of_layer(i)]
+                if blk.first_layer == i:
+                    if i == 0:  # "load block 0": nothing else of the plan stays resident
+                        self.ctx.drop_rotation_keys([t for t in plan.union_keys.indices() if not blk.keys.contains(t)])
+                    self.ctx.prefetch_rotation_keys(blk.keys.indices())
+                    peak_key_bytes = max(peak_key_bytes, self.ctx.key_bytes())
+            if rec is not None:
+                rec.clear()
+                events.append(keyplan.TraceEvent("marker", 0, f"layer:{i}:{b.name}"))
             lin = v.level()
             v = self._run(b, v, timings)
             lout = v.level()
+            if rec is not None:
+                events.extend(keyplan.TraceEvent(e.kind, e.value) for e in rec.snapshot())
+            if key_mode == "block":
+                bi = plan.block_of_layer(i)
+                if plan.blocks[bi].last_layer == i and bi + 1 < len(plan.blocks):
+                    nxt = plan.blocks[bi + 1].keys
+                    self.ctx.drop_rotation_keys([t for t in plan.blocks[bi].keys.indices() if not nxt.contains(t)])
             ledger.append((b.name, b.cost, lin, lout, b.type == "bootstrap"))
             if b.type == "bootstrap":
                 if lout != self.spec.depth_budget:
@@ -801,7 +890,12 @@ class EncryptedModel:
         count = C * W * W if packed else n
         logits = v.slots()[:count]
         wall = (time.perf_counter() - t0) * 1e3
-        return InferResult(logits, ledger, wall, timings or {}, self.ctx.stats())
+        if rec is not None:
+            self.ctx.detach_recorder()
+        residency = dict(self.ctx.key_events(), peak_key_bytes=max(peak_key_bytes, self.ctx.key_bytes()),
+                         resident_key_bytes=self.ctx.key_bytes())
+        check = keyplan.verify_trace(plan, events) if verify_keys else None
+        return InferResult(logits, ledger, wall, timings or {}, self.ctx.stats(), plan, check, residency)
 
 
 # ----------------------------------------------------------------- calibration

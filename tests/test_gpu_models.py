@@ -126,3 +126,47 @@ def test_lenet5_no_bootstrap_deep_budget():
     spec = M.lenet5(ring=8192, depth_budget=25)
     x = np.random.default_rng(3003).uniform(0, 1, (1, 28, 28))
     _compare(spec, x)
+
+
+def test_layer_keys_reference_schedule_equal_reference_derive():
+    """Under the reference rotation schedule the engine's probed per-layer key
+    sets equal the reference's derive_* sets (BuiltModel::layer_keys,
+    model_spec.cpp:944-950) for its own models/lenet5.json: same indices, same
+    use counts, same ends_block flags."""
+    from model_files import materialize
+    path = materialize("lenet5", tempfile.mkdtemp(), seed=4)
+    em = M.EncryptedModel(M.load_spec(path), schedule="reference")
+    ours = em.layer_keys()
+    want = sref.layer_keys(path)
+    assert [(lk.keys.usage, lk.ends_block) for lk in ours] == [(u, e) for u, e in want]
+
+
+@pytest.mark.parametrize("name", ["lenet5", "resnet20"])
+def test_block_key_mode_residency(name):
+    """key_mode "block" (model_run.cpp:150): the keys of plan_blocks' block b are
+    made resident before it and dropped after it when the next block does not
+    use them.  Same logits bit for bit (dropped keys regenerate identically),
+    the recorded trace replays cleanly against the plan, and the peak resident
+    key memory is below the preload run's.  Same logits within encryption noise
+    (every inference encrypts afresh)."""
+    from model_files import materialize
+    spec = M.load_spec(materialize(name, tempfile.mkdtemp(), seed=5))
+    shape = (spec.input_channels, spec.input_width, spec.input_width)
+
+    def prep(x):
+        return (x - 0.5) / 0.2887 if name == "resnet20" else x
+
+    spec = M.calibrate_relu_scales(spec, [prep(np.random.default_rng(600 + i).uniform(0, 1, shape))
+                                          for i in range(3)])
+    x = prep(np.random.default_rng(6).uniform(0, 1, shape))
+    em = M.EncryptedModel(spec)
+    pre = em.infer(x, verify_keys=True)
+    assert pre.trace_check.ok() and pre.trace_check.rotations_checked > 0
+    preload_bytes = em.ctx.key_bytes()
+    blk = em.infer(x, key_mode="block", verify_keys=True)
+    assert blk.trace_check.ok(), blk.trace_check.violations[:3]
+    assert np.abs(blk.logits - pre.logits).max() < 1e-3
+    assert len(blk.plan.blocks) > 1 and blk.key_residency["dropped"] > 0
+    assert blk.key_residency["peak_key_bytes"] < preload_bytes
+    est = M.keyplan.estimate_memory(blk.plan, em.memory_model())
+    assert est.peak_bytes < est.preload_bytes
