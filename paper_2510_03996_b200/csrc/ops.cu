@@ -141,30 +141,41 @@ __global__ void __launch_bounds__(256) k_modup_bconv(PolyList ext, PolyList x, c
 // a key (same-key batches) run together and reuse its slices from L2
 __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int logN, int limbs, int L, int K,
                            DigitOwner dig) {
+  // two adjacent coefficients per thread: 16-byte key and accumulator accesses,
+  // per-CTA setup amortised (as k_ks_inner_sum); same products per coefficient
   const std::size_t N = (std::size_t)1 << logN;
-  const unsigned n = blockIdx.y * blockDim.x + threadIdx.x;
+  const unsigned n = 2 * (blockIdx.y * blockDim.x + threadIdx.x);
   const int t = blockIdx.z;
   const int r = blockIdx.x;
   const int E = limbs + K;
   const int pt = t < limbs ? t : L + (t - limbs);
   const PrimeConst P = pc[pt];
   const u64 g = jobs.g[r];
-  const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
+  const unsigned src0 = (g == 1) ? n : auto_src(n, g, logN);
+  const unsigned src1 = (g == 1) ? n + 1 : auto_src(n + 1, g, logN);
   const int beta = dig.beta;
   const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;  // CTA-uniform: limb t's own digit passes d through
   const u64* key = jobs.key[r];
   const u64* ext = jobs.ext[r];
   const u64* d = jobs.d[r];
-  Acc128 a0, a1;
+  const std::size_t LKN = (std::size_t)(L + K) * N;
+  Acc128 a0[2], a1[2];
   for (int j = 0; j < beta; ++j) {
-    const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+    const u64* vb = j == jown ? d + (std::size_t)t * N : ext + ((std::size_t)j * E + t) * N;
     const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
-    a0.mac(v, kj[n]);
-    a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
+    const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(kj + n);
+    const ulonglong2 ka = *reinterpret_cast<const ulonglong2*>(kj + LKN + n);
+    const u64 v0 = vb[src0], v1 = vb[src1];
+    a0[0].mac(v0, kb.x);
+    a1[0].mac(v0, ka.x);
+    a0[1].mac(v1, kb.y);
+    a1[1].mac(v1, ka.y);
   }
   u64* acc = jobs.acc[r];
-  acc[(std::size_t)t * N + n] = redc(a0.hi, a0.lo, P.q, P.qinv_neg);
-  acc[((std::size_t)E + t) * N + n] = redc(a1.hi, a1.lo, P.q, P.qinv_neg);
+  *reinterpret_cast<ulonglong2*>(acc + (std::size_t)t * N + n) =
+      make_ulonglong2(redc(a0[0].hi, a0[0].lo, P.q, P.qinv_neg), redc(a0[1].hi, a0[1].lo, P.q, P.qinv_neg));
+  *reinterpret_cast<ulonglong2*>(acc + ((std::size_t)E + t) * N + n) =
+      make_ulonglong2(redc(a1[0].hi, a1[0].lo, P.q, P.qinv_neg), redc(a1[1].hi, a1[1].lo, P.q, P.qinv_neg));
 }
 
 // Lazy reduction across jobs: every product is < q^2 (canonical digit x
@@ -592,7 +603,7 @@ void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int
 void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.n == 0) return;
   TimedScope ts(t, kKsInner, st);
-  const dim3 grid(jobs.n, (unsigned)(t.N / kThreads), limbs + t.K);
+  const dim3 grid(jobs.n, (unsigned)(t.N / (2 * kThreads)), limbs + t.K);
   k_ks_inner<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN, limbs, t.L, t.K,
                                                                        DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner");
