@@ -165,6 +165,11 @@ int fheon_rotate_many(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts,
  * Replaces the reference's rotate + add accumulation loops (layers_conv.cpp:155-177,
  * layers_misc.cpp:132-142); one rotation trace event per term */
 int fheon_rotate_sum(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, size_t n, fheon_ct** out);
+/* several rotate-and-sum groups in one pipeline (terms flattened group by group, sizes[r] terms in
+ * group r); groups that rotate one input each under the same key list run as one hoisted stage
+ * (every key slice read once per launch) */
+int fheon_rotate_sum_many(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, const size_t* sizes,
+                          size_t ngroups, fheon_ct** outs);
 int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_sub(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_add_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, size_t n, fheon_ct** out);

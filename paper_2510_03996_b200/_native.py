@@ -102,6 +102,8 @@ SIGNATURES = {
     "fheon_ct_download_async": (C.c_int, [vp, vp, u64p]),
     "fheon_ct_packed_words": (C.c_size_t, [vp, C.c_int]),
     "fheon_key_bytes": (C.c_uint64, [vp]),
+    "fheon_rotate_sum_many": (C.c_int, [vp, C.c_void_p, C.POINTER(C.c_long), C.POINTER(C.c_size_t), C.c_size_t,
+                                        C.c_void_p]),
     "fheon_prefetch_rotation_keys": (C.c_int, [vp, C.POINTER(C.c_long), C.c_size_t]),
     "fheon_drop_rotation_keys": (C.c_int, [vp, C.POINTER(C.c_long), C.c_size_t]),
     "fheon_key_events": (C.c_int, [vp, u64p, u64p]),

@@ -16,7 +16,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 from enum import IntEnum
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -560,6 +560,21 @@ def rotate_many(xs: Sequence[SlotVector], ts: Sequence[int]) -> List[SlotVector]
     outs = (C.c_void_p * n)()
     _check(_native.lib().fheon_rotate_many(ctx._h, hs, arr, n, outs))
     return [SlotVector(ctx, C.c_void_p(outs[i])) for i in range(n)]
+
+
+def rotate_sum_many(groups: Sequence[Sequence[Tuple[SlotVector, int]]]) -> List[SlotVector]:
+    """[sum_k rotate(x_rk, t_rk) for every group r] in one key-switch pipeline."""
+    flat = [p for g in groups for p in g]
+    if not groups or any(len(g) == 0 for g in groups):
+        raise ShapeError("rotate_sum_many: every group needs at least one term", 2)
+    ctx = flat[0][0]._ctx
+    n = len(flat)
+    hs = (C.c_void_p * n)(*[x._h.value if isinstance(x._h, C.c_void_p) else x._h for x, _ in flat])
+    arr = (C.c_long * n)(*[int(t) for _, t in flat])
+    sizes = (C.c_size_t * len(groups))(*[len(g) for g in groups])
+    outs = (C.c_void_p * len(groups))()
+    _check(_native.lib().fheon_rotate_sum_many(ctx._h, hs, arr, sizes, len(groups), outs))
+    return [SlotVector(ctx, C.c_void_p(o)) for o in outs]
 
 
 def rotate_sum(xs: Sequence[SlotVector], ts: Sequence[int]) -> SlotVector:

@@ -388,6 +388,22 @@ int fheon_rotate_sum(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, 
     *out = wrap(fheon::rotate_sum_many(*ctx->impl, {g})[0]);
   });
 }
+int fheon_rotate_sum_many(fheon_ctx* ctx, const fheon_ct* const* xs, const long* ts, const size_t* sizes,
+                          size_t ngroups, fheon_ct** outs) {
+  return guard([&] {
+    std::vector<std::vector<std::pair<fheon::Ciphertext, long>>> groups(ngroups);
+    size_t k = 0;
+    for (size_t r = 0; r < ngroups; ++r) {
+      if (sizes[r] == 0) throw fheon::Error(fheon::ErrKind::shape, "rotate_sum needs at least one term per group");
+      for (size_t i = 0; i < sizes[r]; ++i, ++k) {
+        need(xs[k], "ciphertext");
+        groups[r].push_back({xs[k]->ct, ts[k]});
+      }
+    }
+    std::vector<fheon::Ciphertext> r = fheon::rotate_sum_many(*ctx->impl, groups);
+    for (size_t i = 0; i < ngroups; ++i) outs[i] = wrap(r[i]);
+  });
+}
 int fheon_add(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::add(*ctx->impl, a->ct, b->ct)); });
 }

@@ -260,8 +260,9 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
 // grid (groups, N/256, E): groups fastest (every group uses the same keys)
 __global__ void k_ks_inner_shared(KsSharedJobs jobs, const PrimeConst* __restrict__ pc,
                                   const u64* __restrict__ md_q, int logN, int limbs, int L, int K, DigitOwner dig) {
+  // two adjacent coefficients per thread (as k_ks_inner_sum)
   const std::size_t N = (std::size_t)1 << logN;
-  const unsigned n = blockIdx.y * blockDim.x + threadIdx.x;
+  const unsigned n = 2 * (blockIdx.y * blockDim.x + threadIdx.x);
   const int t = blockIdx.z;
   const int r = blockIdx.x;
   const int E = limbs + K;
@@ -272,31 +273,45 @@ __global__ void k_ks_inner_shared(KsSharedJobs jobs, const PrimeConst* __restric
   const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;
   const u64* ext = jobs.ext[r];
   const u64* d = jobs.d[r];
-  const u64* c0 = jobs.c0[r];
-  u64 s0 = 0, s1 = 0;
+  const u64* c0 = jobs.c0[r] + (std::size_t)t * N;
+  const std::size_t LKN = (std::size_t)(L + K) * N;
+  u64 s0[2] = {0, 0}, s1[2] = {0, 0};
   const int chunk = lazy_chunk(beta);
-  Acc128 a0, a1;
+  Acc128 a0[2], a1[2];
   int cnt = 0;
   for (int jb = 0; jb < jobs.nkeys; ++jb) {
     const u64 g = jobs.g[jb];
-    const unsigned src = (g == 1) ? n : auto_src(n, g, logN);
+    const unsigned src0 = (g == 1) ? n : auto_src(n, g, logN);
+    const unsigned src1 = (g == 1) ? n + 1 : auto_src(n + 1, g, logN);
     const u64* key = jobs.key[jb];
     for (int j = 0; j < beta; ++j) {
-      const u64 v = j == jown ? d[(std::size_t)t * N + src] : ext[((std::size_t)j * E + t) * N + src];
+      const u64* vb = j == jown ? d + (std::size_t)t * N : ext + ((std::size_t)j * E + t) * N;
       const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
-      a0.mac(v, kj[n]);
-      a1.mac(v, kj[(std::size_t)(L + K) * N + n]);
+      const ulonglong2 kb = *reinterpret_cast<const ulonglong2*>(kj + n);
+      const ulonglong2 ka = *reinterpret_cast<const ulonglong2*>(kj + LKN + n);
+      const u64 v0 = vb[src0], v1 = vb[src1];
+      a0[0].mac(v0, kb.x);
+      a1[0].mac(v0, ka.x);
+      a0[1].mac(v1, kb.y);
+      a1[1].mac(v1, ka.y);
     }
-    if (t < limbs) a0.mac(c0[(std::size_t)t * N + src], pm);
+    if (t < limbs) {
+      a0[0].mac(c0[src0], pm);
+      a0[1].mac(c0[src1], pm);
+    }
     if (++cnt == chunk) {
-      lazy_flush(s0, s1, a0, a1, P);
+      lazy_flush(s0[0], s1[0], a0[0], a1[0], P);
+      lazy_flush(s0[1], s1[1], a0[1], a1[1], P);
       cnt = 0;
     }
   }
-  if (cnt) lazy_flush(s0, s1, a0, a1, P);
+  if (cnt) {
+    lazy_flush(s0[0], s1[0], a0[0], a1[0], P);
+    lazy_flush(s0[1], s1[1], a0[1], a1[1], P);
+  }
   u64* acc = jobs.acc[r];
-  acc[(std::size_t)t * N + n] = s0;
-  acc[((std::size_t)E + t) * N + n] = s1;
+  *reinterpret_cast<ulonglong2*>(acc + (std::size_t)t * N + n) = make_ulonglong2(s0[0], s0[1]);
+  *reinterpret_cast<ulonglong2*>(acc + ((std::size_t)E + t) * N + n) = make_ulonglong2(s1[0], s1[1]);
 }
 
 // ModDown conversion with KK = K special limbs (compile time).
@@ -619,7 +634,7 @@ void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStre
 void ks_inner_shared(const DevTables& t, const KsSharedJobs& jobs, int limbs, cudaStream_t st) {
   if (jobs.ngroups == 0) return;
   TimedScope ts(t, kKsInner, st);
-  const dim3 grid(jobs.ngroups, (unsigned)(t.N / kThreads), limbs + t.K);
+  const dim3 grid(jobs.ngroups, (unsigned)(t.N / (2 * kThreads)), limbs + t.K);
   k_ks_inner_shared<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.md_q, t.logN, limbs, t.L, t.K,
                                                DigitOwner{t.digit_owner, t.dig.beta(limbs)});
   launch_check("k_ks_inner_shared");

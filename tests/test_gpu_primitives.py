@@ -374,3 +374,21 @@ def test_packed_transfers_config2_roundtrip():
     bits = sum(int(q).bit_length() for q in ctx.primes[:24])
     assert bits <= 60 + 23 * 51 and p.size == 2 * (1 << 16) * bits // 64
     assert np.array_equal(fh.SlotVector.from_packed(ctx, p, 24, x.scale()).words(), w)
+
+
+@pytest.mark.parametrize("shared", [True, False])
+def test_rotate_sum_many_groups_bit_exact(small, shared):
+    """Several rotate-and-sum groups in one pipeline.  shared=True: every group
+    rotates ONE input under the same key list -- the hoisted-stage kernel
+    (k_ks_inner_shared, every key slice read once per launch); False: distinct
+    key lists per group (k_ks_inner_sum).  Each output bit-exact against the
+    oracle's ock_rotate_sum."""
+    ctx, orc = small
+    rng = np.random.default_rng(410 + shared)
+    cts = [_oracle_ct(orc, rng, counter=80 + i)[1] for i in range(3)]
+    xs = [fh.SlotVector.from_words(ctx, c, orc.T[-1]) for c in cts]
+    lists = [[1, 3, -2]] * 3 if shared else [[1, 3, -2], [5, -1], [2, 7, 11, -9]]
+    outs = fh.rotate_sum_many([[(x, t) for t in ts] for x, ts in zip(xs, lists)])
+    for c, ts, o in zip(cts, lists, outs):
+        want = orc.rotate_sum([c] * len(ts), ts, [orc.rotation_key(t) for t in ts])
+        assert np.array_equal(o.words(), want)
