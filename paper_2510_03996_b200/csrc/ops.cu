@@ -390,22 +390,34 @@ __global__ void k_rescale_lift(PolyList r, PolyList last, const PrimeConst* __re
 // from L2 instead of HBM
 // limb t < ell uses q_t, limb t >= ell the special prime p_{t - ell} (Q u P operands)
 __global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN, int ell, int L) {
-  const std::size_t o = ((std::size_t)blockIdx.z << logN) + blockIdx.y * blockDim.x + threadIdx.x;
+  // two adjacent coefficients per thread, 16-byte loads and stores
+  const std::size_t o = ((std::size_t)blockIdx.z << logN) + 2 * (blockIdx.y * blockDim.x + threadIdx.x);
   const int z = blockIdx.x;
   const int t = (int)blockIdx.z;
   const PrimeConst P = pc[t < ell ? t : L + (t - ell)];
   const int nt = jobs.nterm[z];
-  u64 s0 = 0, s1 = 0;
-  Acc128 a0, a1;
+  u64 s0[2] = {0, 0}, s1[2] = {0, 0};
+  Acc128 a0[2], a1[2];
   for (int j = 0; j < nt; ++j) {  // nt <= kMacMaxTerms = 32 products < 32 q^2: one lazy flush
     const u64* c = jobs.ct[z][j];
-    const u64 p = jobs.pt[z][j][o];
-    a0.mac(c[o], p);
-    a1.mac(c[jobs.c1_off[z][j] + o], p);
-    if ((j & 31) == 31 || j == nt - 1) lazy_flush(s0, s1, a0, a1, P);
+    const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(jobs.pt[z][j] + o);
+    const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(c + o);
+    const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(c + jobs.c1_off[z][j] + o);
+    a0[0].mac(x0.x, p.x);
+    a1[0].mac(x1.x, p.x);
+    a0[1].mac(x0.y, p.y);
+    a1[1].mac(x1.y, p.y);
+    if ((j & 31) == 31 || j == nt - 1) {
+      lazy_flush(s0[0], s1[0], a0[0], a1[0], P);
+      lazy_flush(s0[1], s1[1], a0[1], a1[1], P);
+    }
   }
-  jobs.out0[z][o] = redc(mulhi(s0, P.r2), s0 * P.r2, P.q, P.qinv_neg);
-  jobs.out1[z][o] = redc(mulhi(s1, P.r2), s1 * P.r2, P.q, P.qinv_neg);
+  *reinterpret_cast<ulonglong2*>(jobs.out0[z] + o) =
+      make_ulonglong2(redc(mulhi(s0[0], P.r2), s0[0] * P.r2, P.q, P.qinv_neg),
+                      redc(mulhi(s0[1], P.r2), s0[1] * P.r2, P.q, P.qinv_neg));
+  *reinterpret_cast<ulonglong2*>(jobs.out1[z] + o) =
+      make_ulonglong2(redc(mulhi(s1[0], P.r2), s1[0] * P.r2, P.q, P.qinv_neg),
+                      redc(mulhi(s1[1], P.r2), s1[1] * P.r2, P.q, P.qinv_neg));
 }
 
 // grid (N/256, 1)
@@ -693,7 +705,7 @@ void mul_monomial_half(const DevTables& t, const PolyList& out, const PolyList& 
 }
 void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st, int ell) {
   if (jobs.nout == 0) return;
-  const dim3 grid(jobs.nout, (unsigned)(t.N / kThreads), limbs);
+  const dim3 grid(jobs.nout, (unsigned)(t.N / (2 * kThreads)), limbs);
   k_mac<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN, ell < 0 ? limbs : ell, t.L);
   launch_check("k_mac");
 }
