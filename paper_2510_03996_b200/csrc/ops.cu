@@ -53,16 +53,20 @@ __global__ void k_add_const(PolyList out, PolyList a, LimbConsts c, const PrimeC
 // grid (N/256, limbs, 2 polys)
 __global__ void k_lincomb_const(u64* out0, u64* out1, LincombTerms terms, const u64* __restrict__ kc,
                                 const PrimeConst* __restrict__ pc, int logN, int limbs) {
-  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  // two adjacent coefficients per thread (16-byte loads / stores)
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int t = blockIdx.y;
   const u64 q = pc[t].q;
-  u64 s = 0;
+  u64 s0 = 0, s1 = 0;
   for (int i = 0; i < terms.n; ++i) {
     const u64* x = terms.c0[i] + (blockIdx.z ? terms.c1_off[i] : 0);
     const u64* k = kc + ((std::size_t)i * limbs + t) * 2;
-    s = add_mod(s, shoup_mul(x[o], k[0], k[1], q), q);
+    const u64 kv = k[0], ksh = k[1];
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(x + o);
+    s0 = add_mod(s0, shoup_mul(v.x, kv, ksh, q), q);
+    s1 = add_mod(s1, shoup_mul(v.y, kv, ksh, q), q);
   }
-  (blockIdx.z ? out1 : out0)[o] = s;
+  *reinterpret_cast<ulonglong2*>((blockIdx.z ? out1 : out0) + o) = make_ulonglong2(s0, s1);
 }
 
 // grid (N/256, npolys): acc[n] += x[n] * c (Montgomery constant) on one limb
@@ -79,7 +83,12 @@ __global__ void k_tensor(u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1
   const PrimeConst P = pc[blockIdx.y];
   const u64 x0 = a0[o], x1 = a1[o], y0 = b0[o], y1 = b1[o];
   d0[o] = mul_mod(x0, y0, P);
-  d1[o] = add_mod(mul_mod(x0, y1, P), mul_mod(x1, y0, P), P.q);
+  // the cross term's two products (< 2 q^2 < q 2^64) share one REDC + conversion
+  Acc128 c;
+  c.mac(x0, y1);
+  c.mac(x1, y0);
+  const u64 tm = redc(c.hi, c.lo, P.q, P.qinv_neg);
+  d1[o] = redc(mulhi(tm, P.r2), tm * P.r2, P.q, P.qinv_neg);
   d2[o] = mul_mod(x1, y1, P);
 }
 __global__ void k_automorph(PolyList out, PolyList in, int logN) {
@@ -580,7 +589,7 @@ void ew_add_const(const DevTables& t, const PolyList& out, const PolyList& a, co
 void lincomb_const(const DevTables& t, u64* out0, u64* out1, const LincombTerms& terms, const u64* kc, int limbs,
                    cudaStream_t st) {
   if (terms.n == 0 || limbs == 0) return;
-  k_lincomb_const<<<grid_for(t.N, limbs, 2), kThreads, 0, st>>>(out0, out1, terms, kc, t.pc, t.logN, limbs);
+  k_lincomb_const<<<grid_for(t.N / 2, limbs, 2), kThreads, 0, st>>>(out0, out1, terms, kc, t.pc, t.logN, limbs);
   launch_check("k_lincomb_const");
 }
 void ew_axpy_limb(const DevTables& t, const PolyList& acc, const PolyList& x, u64 c_mont, int prime, cudaStream_t st) {
