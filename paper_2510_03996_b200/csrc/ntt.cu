@@ -247,6 +247,34 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
     const u64 ac = amul ? __ldg(epi.acst + (std::size_t)tl * epi.acst_stride) : 0;
     const u64 acsh = amul ? __ldg(epi.acst + (std::size_t)tl * epi.acst_stride + 1) : 0;
     u64* outp = epi.out[pi] + off;
+    if (!COL && b == 0) {  // the thread's E elements are consecutive: 16-byte accesses
+      const int k0 = (int)gaddr(base);
+#pragma unroll
+      for (int e = 0; e < E; e += 2) {
+        const ulonglong2 sv = *reinterpret_cast<const ulonglong2*>(srcp + k0 + e);
+        u64 v0 = shoup_mul(sub_mod(sv.x, x[e], q), c, csh, q);
+        u64 v1 = shoup_mul(sub_mod(sv.y, x[e + 1], q), c, csh, q);
+        if (addp) {
+          u64 a0, a1;
+          if (g == 1) {
+            const ulonglong2 av = *reinterpret_cast<const ulonglong2*>(addp + k0 + e);
+            a0 = av.x;
+            a1 = av.y;
+          } else {
+            a0 = addp[auto_src((unsigned)(k0 + e), g, logN)];
+            a1 = addp[auto_src((unsigned)(k0 + e + 1), g, logN)];
+          }
+          if (amul) {
+            a0 = shoup_mul(a0, ac, acsh, q);
+            a1 = shoup_mul(a1, ac, acsh, q);
+          }
+          v0 = add_mod(v0, a0, q);
+          v1 = add_mod(v1, a1, q);
+        }
+        *reinterpret_cast<ulonglong2*>(outp + k0 + e) = make_ulonglong2(v0, v1);
+      }
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int k = (int)gaddr(base | (e << b));  // element index within the limb-poly
