@@ -50,6 +50,34 @@ __global__ void k_add_const(PolyList out, PolyList a, LimbConsts c, const PrimeC
   const u64 q = pc[blockIdx.y].q;
   out.p[blockIdx.z][o] = add_mod(a.p[blockIdx.z][o], c.c[blockIdx.y], q);
 }
+// Two-coefficient (16-byte) variants of the elementwise kernels, used when every
+// pointer of the launch is 16-byte aligned (always, for ciphertext and key
+// buffers; checked per launch): grid (N/512, limbs, npolys)
+template <int OP>  // 0 add, 1 sub, 2 add_const, 3 mul_const
+__global__ void k_ew2(PolyList out, PolyList a, PolyList b, LimbConsts c, const PrimeConst* __restrict__ pc, int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const u64 q = pc[blockIdx.y].q;
+  const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a.p[blockIdx.z] + o);
+  ulonglong2 r;
+  if constexpr (OP == 0 || OP == 1) {
+    const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(b.p[blockIdx.z] + o);
+    r = OP == 0 ? make_ulonglong2(add_mod(x.x, y.x, q), add_mod(x.y, y.y, q))
+                : make_ulonglong2(sub_mod(x.x, y.x, q), sub_mod(x.y, y.y, q));
+  } else if constexpr (OP == 2) {
+    const u64 k = c.c[blockIdx.y];
+    r = make_ulonglong2(add_mod(x.x, k, q), add_mod(x.y, k, q));
+  } else {
+    const u64 k = c.c[blockIdx.y], ks = c.sh[blockIdx.y];
+    r = make_ulonglong2(shoup_mul(x.x, k, ks, q), shoup_mul(x.y, k, ks, q));
+  }
+  *reinterpret_cast<ulonglong2*>(out.p[blockIdx.z] + o) = r;
+}
+bool aligned16(const PolyList& l) {
+  for (int i = 0; i < l.n; ++i)
+    if (reinterpret_cast<std::uintptr_t>(l.p[i]) & 15u) return false;
+  return true;
+}
+
 // grid (N/256, limbs, 2 polys)
 __global__ void k_lincomb_const(u64* out0, u64* out1, LincombTerms terms, const u64* __restrict__ kc,
                                 const PrimeConst* __restrict__ pc, int logN, int limbs) {
@@ -556,11 +584,21 @@ __global__ void k_convert_mont(u64* out, const u64* in, const PrimeConst* __rest
 
 void ew_add(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& b, int limbs, cudaStream_t st) {
   if (out.n == 0 || limbs == 0) return;
+  if (aligned16(out) && aligned16(a) && aligned16(b)) {
+    k_ew2<0><<<grid_for(t.N / 2, limbs, out.n), kThreads, 0, st>>>(out, a, b, LimbConsts{}, t.pc, t.logN);
+    launch_check("k_add");
+    return;
+  }
   k_add<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, b, t.pc, t.logN);
   launch_check("k_add");
 }
 void ew_sub(const DevTables& t, const PolyList& out, const PolyList& a, const PolyList& b, int limbs, cudaStream_t st) {
   if (out.n == 0 || limbs == 0) return;
+  if (aligned16(out) && aligned16(a) && aligned16(b)) {
+    k_ew2<1><<<grid_for(t.N / 2, limbs, out.n), kThreads, 0, st>>>(out, a, b, LimbConsts{}, t.pc, t.logN);
+    launch_check("k_sub");
+    return;
+  }
   k_sub<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, b, t.pc, t.logN);
   launch_check("k_sub");
 }
@@ -577,12 +615,22 @@ void ew_mul_pt(const DevTables& t, const PolyList& out, const PolyList& a, const
 void ew_mul_const(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& c, int limbs,
                   cudaStream_t st) {
   if (out.n == 0 || limbs == 0) return;
+  if (aligned16(out) && aligned16(a)) {
+    k_ew2<3><<<grid_for(t.N / 2, limbs, out.n), kThreads, 0, st>>>(out, a, a, c, t.pc, t.logN);
+    launch_check("k_mul_const");
+    return;
+  }
   k_mul_const<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, c, t.pc, t.logN);
   launch_check("k_mul_const");
 }
 void ew_add_const(const DevTables& t, const PolyList& out, const PolyList& a, const LimbConsts& c, int limbs,
                   cudaStream_t st) {
   if (out.n == 0 || limbs == 0) return;
+  if (aligned16(out) && aligned16(a)) {
+    k_ew2<2><<<grid_for(t.N / 2, limbs, out.n), kThreads, 0, st>>>(out, a, a, c, t.pc, t.logN);
+    launch_check("k_add_const");
+    return;
+  }
   k_add_const<<<grid_for(t.N, limbs, out.n), kThreads, 0, st>>>(out, a, c, t.pc, t.logN);
   launch_check("k_add_const");
 }
