@@ -127,11 +127,7 @@ static int used(const ock_ctx* c, int n, u64 x) {
   return 0;
 }
 
-ock_ctx* ock_create(int logN, int L, int K, int dnum, int first_bits,
-                    int scale_bits, int special_bits, u64 seed) {
-  if (logN < 3 || logN > 17 || L < 1 || K < 1 || L + K > MAXP || dnum < 1 ||
-      first_bits > 61 || scale_bits > 61 || special_bits > 61)
-    return NULL;
+static ock_ctx* alloc_ctx(int logN, int L, int K, int dnum, u64 seed) {
   ock_ctx* c = (ock_ctx*)calloc(1, sizeof(ock_ctx));
   c->logN = logN;
   c->N = (size_t)1 << logN;
@@ -144,6 +140,69 @@ ock_ctx* ock_create(int logN, int L, int K, int dnum, int first_bits,
   for (int j = 0; j * c->alpha < L; j++) c->dig[c->ndig++] = j * c->alpha;
   c->dig[c->ndig] = L;
   c->seed = seed;
+  return c;
+}
+
+/* roots, twiddles (psi^brv by one running power per limb), encoder tables, secret */
+static ock_ctx* finish_ctx(ock_ctx* c) {
+  const int logN = c->logN, L = c->L, K = c->K;
+  const u64 M = 2 * (u64)c->N;
+  /* roots and twiddles */
+#pragma omp parallel for schedule(dynamic)
+  for (int i = 0; i < L + K; i++) {
+    const u64 q = c->q[i];
+    u64 psi = 0;
+    for (u64 g = 2;; g++) {
+      psi = powmod(g, (q - 1) / M, q);
+      if (powmod(psi, c->N, q) == q - 1) break;
+    }
+    c->psi[i] = psi;
+    const u64 ipsi = invmod(psi, q);
+    c->tw[i] = (u64*)malloc(c->N * sizeof(u64));
+    c->itw[i] = (u64*)malloc(c->N * sizeof(u64));
+    u64 pw = 1, ipw = 1; /* psi^e, psi^-e for e = 0, 1, ... */
+    for (size_t e = 0; e < c->N; e++) {
+      const unsigned k = brv((unsigned)e, logN);
+      c->tw[i][k] = pw;
+      c->itw[i][k] = ipw;
+      pw = mulmod(pw, psi, q);
+      ipw = mulmod(ipw, ipsi, q);
+    }
+    c->ninv[i] = invmod((u64)(c->N % q), q);
+  }
+  /* encoder tables */
+  c->rotgroup = (u64*)malloc(c->S * sizeof(u64));
+  {
+    u64 g = 1;
+    for (int j = 0; j < c->S; j++) { c->rotgroup[j] = g; g = (g * 5) % M; }
+  }
+  c->ksi_re = (double*)malloc((M + 1) * sizeof(double));
+  c->ksi_im = (double*)malloc((M + 1) * sizeof(double));
+  for (u64 k = 0; k <= M; k++) {
+    const double ang = 2.0 * 3.14159265358979323846 * (double)k / (double)M;
+    c->ksi_re[k] = cos(ang);
+    c->ksi_im[k] = sin(ang);
+  }
+  /* secret */
+  c->s = (int8_t*)malloc(c->N);
+  ock_secret(c, c->s);
+  c->s_ntt = (u64*)malloc((size_t)(L + K) * c->N * sizeof(u64));
+#pragma omp parallel for
+  for (int i = 0; i < L + K; i++) {
+    u64* d = c->s_ntt + (size_t)i * c->N;
+    for (size_t k = 0; k < c->N; k++) d[k] = reduce_signed(c->s[k], c->q[i]);
+    ock_ntt_fwd(c, i, d);
+  }
+  return c;
+}
+
+
+ock_ctx* ock_create(int logN, int L, int K, int dnum, int first_bits,
+                    int scale_bits, int special_bits, u64 seed) {
+  if (logN < 3 || logN > 17 || L < 1 || K < 1 || L + K > MAXP || dnum < 1 ||
+      first_bits > 61 || scale_bits > 61 || special_bits > 61)
+    return NULL;
+  ock_ctx* c = alloc_ctx(logN, L, K, dnum, seed);
   const u64 M = 2 * (u64)c->N;
   int np = 0;
   /* q_0: largest prime = 1 mod 2N below 2^first_bits */
@@ -192,49 +251,23 @@ ock_ctx* ock_create(int logN, int L, int K, int dnum, int first_bits,
       x -= M;
     }
   }
-  /* roots and twiddles */
-  for (int i = 0; i < L + K; i++) {
-    const u64 q = c->q[i];
-    u64 psi = 0;
-    for (u64 g = 2;; g++) {
-      psi = powmod(g, (q - 1) / M, q);
-      if (powmod(psi, c->N, q) == q - 1) break;
-    }
-    c->psi[i] = psi;
-    const u64 ipsi = invmod(psi, q);
-    c->tw[i] = (u64*)malloc(c->N * sizeof(u64));
-    c->itw[i] = (u64*)malloc(c->N * sizeof(u64));
-    for (size_t k = 0; k < c->N; k++) {
-      const unsigned e = brv((unsigned)k, logN);
-      c->tw[i][k] = powmod(psi, e, q);
-      c->itw[i][k] = powmod(ipsi, e, q);
-    }
-    c->ninv[i] = invmod((u64)(c->N % q), q);
-  }
-  /* encoder tables */
-  c->rotgroup = (u64*)malloc(c->S * sizeof(u64));
-  {
-    u64 g = 1;
-    for (int j = 0; j < c->S; j++) { c->rotgroup[j] = g; g = (g * 5) % M; }
-  }
-  c->ksi_re = (double*)malloc((M + 1) * sizeof(double));
-  c->ksi_im = (double*)malloc((M + 1) * sizeof(double));
-  for (u64 k = 0; k <= M; k++) {
-    const double ang = 2.0 * 3.14159265358979323846 * (double)k / (double)M;
-    c->ksi_re[k] = cos(ang);
-    c->ksi_im[k] = sin(ang);
-  }
-  /* secret */
-  c->s = (int8_t*)malloc(c->N);
-  ock_secret(c, c->s);
-  c->s_ntt = (u64*)malloc((size_t)(L + K) * c->N * sizeof(u64));
-#pragma omp parallel for
-  for (int i = 0; i < L + K; i++) {
-    u64* d = c->s_ntt + (size_t)i * c->N;
-    for (size_t k = 0; k < c->N; k++) d[k] = reduce_signed(c->s[k], c->q[i]);
-    ock_ntt_fwd(c, i, d);
-  }
-  return c;
+  return finish_ctx(c);
+}
+
+/* Context over an explicit chain (the engine's own primes and per-level scale
+ * targets, e.g. the model runtime's bootstrapping chains with mixed 55/40-bit
+ * levels): q_0..q_{L-1}, p_0..p_{K-1} in primes[L+K], T[L]; every prime must be
+ * = 1 mod 2N.  Everything after prime selection is shared with ock_create. */
+ock_ctx* ock_create_chain(int logN, int L, int K, int dnum, const u64* primes,
+                          const double* T, u64 seed) {
+  if (logN < 3 || logN > 17 || L < 1 || K < 1 || L + K > MAXP || dnum < 1) return NULL;
+  const u64 M = (u64)2 << logN;
+  for (int i = 0; i < L + K; i++)
+    if (primes[i] % M != 1 || !is_prime(primes[i]) || primes[i] >> 61) return NULL;
+  ock_ctx* c = alloc_ctx(logN, L, K, dnum, seed);
+  for (int i = 0; i < L + K; i++) c->q[i] = primes[i];
+  for (int i = 0; i < L; i++) c->T[i] = T[i];
+  return finish_ctx(c);
 }
 
 void ock_destroy(ock_ctx* c) {

@@ -32,6 +32,10 @@ typedef struct ock_ctx ock_ctx;
 
 ock_ctx* ock_create(int logN, int L, int K, int dnum, int first_bits,
                     int scale_bits, int special_bits, uint64_t seed);
+/* the same context over an explicit chain: primes[L+K] (q_0..q_{L-1}, p_0..p_{K-1},
+ * each = 1 mod 2N), T[L] per-level scale targets -- e.g. the engine's own chain */
+ock_ctx* ock_create_chain(int logN, int L, int K, int dnum, const uint64_t* primes,
+                          const double* T, uint64_t seed);
 void ock_destroy(ock_ctx* c);
 /* primes[L+K], psi[L+K], T[L] (scale target per level, level = limbs-1) */
 void ock_info(const ock_ctx* c, uint64_t* primes, uint64_t* psi, double* T);

@@ -30,6 +30,8 @@ def lib():
         vp = C.c_void_p
         L.ock_create.restype = vp
         L.ock_create.argtypes = [C.c_int] * 7 + [C.c_uint64]
+        L.ock_create_chain.restype = vp
+        L.ock_create_chain.argtypes = [C.c_int] * 4 + [_u64p, _dblp, C.c_uint64]
         L.ock_destroy.argtypes = [vp]
         L.ock_info.argtypes = [vp, _u64p, _u64p, _dblp]
         L.ock_ntt_fwd.argtypes = [vp, C.c_int, _u64p]
@@ -82,13 +84,18 @@ def _chk(rc, what):
 class Oracle:
     """CPU RNS-CKKS context mirroring the engine's parameter spec."""
 
-    def __init__(self, logN, L, K, dnum, first_bits, scale_bits, special_bits, seed=1, hamming_weight=0,
-                 digit_split=0):
+    def __init__(self, logN, L, K, dnum, first_bits=0, scale_bits=0, special_bits=0, seed=1, hamming_weight=0,
+                 digit_split=0, chain=None):
         self.logN, self.L, self.K, self.dnum = logN, L, K, dnum
         self.N = 1 << logN
         self.S = self.N // 2
         self.alpha = (L + dnum - 1) // dnum
-        self._c = lib().ock_create(logN, L, K, dnum, first_bits, scale_bits, special_bits, seed)
+        if chain is not None:
+            primes, T = chain
+            self._c = lib().ock_create_chain(logN, L, K, dnum, np.ascontiguousarray(primes, np.uint64),
+                                             np.ascontiguousarray(T, np.float64), seed)
+        else:
+            self._c = lib().ock_create(logN, L, K, dnum, first_bits, scale_bits, special_bits, seed)
         if not self._c:
             raise ValueError("invalid oracle parameters")
         self.primes = np.zeros(L + K, np.uint64)
@@ -99,6 +106,13 @@ class Oracle:
             lib().ock_set_hamming_weight(self._c, int(hamming_weight))
         if digit_split:
             _chk(lib().ock_set_digit_split(self._c, 1), "set_digit_split")
+
+    @classmethod
+    def from_chain(cls, logN, primes, T, L, K, dnum, seed=1, hamming_weight=0, digit_split=0):
+        """Oracle over an explicit prime chain (e.g. the engine context's own:
+        ctx.primes, ctx.scales) -- for the model runtime's mixed-width chains."""
+        return cls(logN, L, K, dnum, seed=seed, hamming_weight=hamming_weight, digit_split=digit_split,
+                   chain=(np.asarray(primes, np.uint64)[:L + K], np.asarray(T, np.float64)[:L]))
 
     def __del__(self):
         if getattr(self, "_c", None):

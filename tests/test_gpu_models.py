@@ -46,6 +46,16 @@ def test_lenet5_small_ring_with_bootstrapping(schedule):
     _compare(spec, x, schedule)
 
 
+def test_lenet5_config2_ring_depth25():
+    """LeNet-5 at BASELINE configs[2]: N = 2^15 (16384 slots), the reference's
+    preset depth budget 25 (backend.cpp:61-76), N(0, 0.1^2) weights, beta = 8
+    (models/lenet5.json relu scale), seeded U[0,1] input; bootstraps placed as
+    the reference places them."""
+    spec = M.lenet5(ring=32768, depth_budget=25)
+    x = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
+    _compare(spec, x, "fast")
+
+
 @pytest.mark.parametrize("schedule", ["reference", "fast"])
 def test_resnet20_full_ring_with_bootstrapping(schedule):
     """ResNet-20 (BASELINE configs[3]): N = 2^16, depth budget 12 -> 19 bootstraps,
