@@ -52,6 +52,15 @@ typedef struct {
   int bootstrap;      /* 1: enable CKKS bootstrapping (bootstrap() refreshes to depth_budget) */
   int boot_scale_bits;/* scale of the bootstrapping levels (0 = scale_bits) */
   int digit_split;    /* key-switching digits: 0 uniform ceil(limbs/dnum), 1 balanced by bit size */
+  /* bootstrapping with a dense secret (hamming_weight 0) runs the sparse-secret encapsulation:
+   * the level-0 ciphertext is switched to an ephemeral sparse secret of this Hamming weight
+   * (0 = 64) on q_0 and the special primes only, ModRaised, and switched back */
+  int boot_hamming_weight;
+  /* security: context creation refuses a chain whose log2(QP) exceeds the HE-standard bound
+   * (uniform ternary secret, classical) for N at min_security bits (0 = 128), or whose main
+   * secret is sparse, unless allow_insecure = 1 (the reference's presets need it) */
+  int min_security;
+  int allow_insecure;
 } fheon_params;
 
 /* ---- errors / version */
@@ -64,12 +73,18 @@ int fheon_version(void);
 int fheon_host_primes(const fheon_params* p, uint64_t* primes, double* scales);
 /* canonical-embedding encode of n <= N/2 slot values at `scale` -> N signed coefficients */
 int fheon_host_encode(const fheon_params* p, const double* values, size_t n, double scale, int64_t* coeffs);
+/* security disclosure of a parameter set: log2(QP) over the whole chain, the HE-standard level it
+ * meets (256/192/128; 0 below 128; -1 sparse main secret, not covered by the table) and the
+ * table's log2(QP) bound at min_security (homomorphicencryption.org 2018 Table 1, ternary) */
+int fheon_host_security(const fheon_params* p, double* log_qp, int* level, double* bound);
 /* Chebyshev interpolant coefficients of max(0, beta z) on [-1, 1] (chebyshev.cpp:33-50) */
 int fheon_cheb_relu_coefficients(double beta, int degree, double* coeffs);
 
 /* ---- context (SlotContext::create, backend.hpp:69) */
 int fheon_ctx_create(const fheon_params* p, fheon_ctx** out);
 void fheon_ctx_destroy(fheon_ctx* ctx);
+/* the context's log2(QP) and HE-standard security level (as fheon_host_security) */
+int fheon_ctx_security(const fheon_ctx* ctx, double* log_qp, int* level);
 /* primes[L+K], scales[L] (scale target per level), slots */
 int fheon_ctx_info(const fheon_ctx* ctx, uint64_t* primes, double* scales, int* slots);
 void* fheon_ctx_stream(fheon_ctx* ctx); /* cudaStream_t */

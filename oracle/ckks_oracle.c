@@ -45,6 +45,7 @@ struct ock_ctx {
   int h;          /* secret Hamming weight (0 = uniform ternary) */
   int8_t* s;      /* secret, coefficient domain */
   u64* s_ntt;     /* [L+K][N] */
+  u64* sb_ntt;    /* ephemeral sparse bootstrapping secret (sparse-secret encapsulation), or NULL */
 };
 
 /* ------------------------------------------------------------ arithmetic */
@@ -273,7 +274,7 @@ ock_ctx* ock_create_chain(int logN, int L, int K, int dnum, const u64* primes,
 void ock_destroy(ock_ctx* c) {
   if (!c) return;
   for (int i = 0; i < c->L + c->K; i++) { free(c->tw[i]); free(c->itw[i]); }
-  free(c->rotgroup); free(c->ksi_re); free(c->ksi_im); free(c->s); free(c->s_ntt);
+  free(c->rotgroup); free(c->ksi_re); free(c->ksi_im); free(c->s); free(c->s_ntt); free(c->sb_ntt);
   free(c);
 }
 
@@ -545,19 +546,39 @@ void ock_decode_coeffs(const ock_ctx* c, const double* coeffs, double scale, dou
 /* secret: uniform ternary (h = 0) or exactly h nonzero +-1 coefficients
  * (sparse, for bootstrapping): candidate j picks position prng(seed, 6, j) % N,
  * accepted when unused, sign from bit 0 of prng(seed, 7, j). */
+static void sparse_secret(const ock_ctx* c, int8_t* s, int h, u64 pos_stream) {
+  memset(s, 0, c->N);
+  int got = 0;
+  for (u64 j = 0; got < h; j++) {
+    const size_t pos = (size_t)(prng(c->seed, pos_stream, j) % c->N);
+    if (s[pos]) continue;
+    s[pos] = (prng(c->seed, pos_stream + 1, j) & 1) ? 1 : -1;
+    got++;
+  }
+}
+
 void ock_secret(const ock_ctx* c, int8_t* s) {
   if (c->h <= 0) {
     for (size_t k = 0; k < c->N; k++) s[k] = (int8_t)((int)(prng(c->seed, STREAM_SECRET, k) % 3) - 1);
     return;
   }
-  memset(s, 0, c->N);
-  int got = 0;
-  for (u64 j = 0; got < c->h; j++) {
-    const size_t pos = (size_t)(prng(c->seed, 6, j) % c->N);
-    if (s[pos]) continue;
-    s[pos] = (prng(c->seed, 7, j) & 1) ? 1 : -1;
-    got++;
+  sparse_secret(c, s, c->h, 6);
+}
+
+/* Sparse-secret encapsulation (engine Context::sse, evaluator.cpp mod_raise): the
+ * ephemeral sparse bootstrapping secret s_b with h_b nonzero coefficients from
+ * streams 8 (positions) / 9 (signs) -- the main secret's recipe on other streams. */
+void ock_set_boot_secret(ock_ctx* c, int hb) {
+  int8_t* sb = (int8_t*)malloc(c->N);
+  sparse_secret(c, sb, hb, 8);
+  if (!c->sb_ntt) c->sb_ntt = (u64*)malloc((size_t)(c->L + c->K) * c->N * sizeof(u64));
+#pragma omp parallel for
+  for (int i = 0; i < c->L + c->K; i++) {
+    u64* d = c->sb_ntt + (size_t)i * c->N;
+    for (size_t k = 0; k < c->N; k++) d[k] = reduce_signed(sb[k], c->q[i]);
+    ock_ntt_fwd(c, i, d);
   }
+  free(sb);
 }
 
 void ock_set_hamming_weight(ock_ctx* c, int h) {
@@ -580,9 +601,18 @@ static void error_ntt(const ock_ctx* c, u64 stream, int pi, u64* d) {
 int ock_keygen(const ock_ctx* c, u64 key_id, u64* key) {
   const int L = c->L, K = c->K, LK = L + K;
   const size_t N = c->N;
-  /* s' : s^2 (relinearisation, key_id 0) or sigma_g(s) (rotation, key_id g) */
+  /* s' : s^2 (relinearisation, key_id 0), sigma_g(s) (rotation, key_id g odd), or the
+   * sparse-secret encapsulation keys: 2 = s -> s_b (b = -a s_b + e + P s, on digit 0's
+   * q_0 and the special primes only: every other limb and digit is zero), 4 = s_b -> s */
   u64* sp = (u64*)malloc((size_t)LK * N * sizeof(u64));
-  if (key_id == 0) {
+  const u64* s_to = c->s_ntt;
+  const int to_sparse = key_id == 2, sse = key_id == 2 || key_id == 4;
+  if (sse && !c->sb_ntt) { free(sp); return -1; }
+  if (sse) {
+    memcpy(sp, to_sparse ? c->s_ntt : c->sb_ntt, (size_t)LK * N * sizeof(u64));
+    if (to_sparse) s_to = c->sb_ntt;
+    memset(key, 0, (size_t)c->dnum * 2 * LK * N * sizeof(u64));
+  } else if (key_id == 0) {
     for (int i = 0; i < LK; i++)
       for (size_t k = 0; k < N; k++) {
         const u64 v = c->s_ntt[(size_t)i * N + k];
@@ -592,12 +622,13 @@ int ock_keygen(const ock_ctx* c, u64 key_id, u64* key) {
     if ((key_id & 1) == 0) { free(sp); return -1; }
     ock_automorph_ntt(c, key_id, c->s_ntt, sp, LK);
   }
-  for (int j = 0; j < c->dnum; j++) { /* digits past ndig stay empty */
+  for (int j = 0; j < (to_sparse ? 1 : c->dnum); j++) { /* digits past ndig stay empty */
     const int lo = j < c->ndig ? c->dig[j] : L, hi = j < c->ndig ? c->dig[j + 1] : L;
     u64* b = key + ((size_t)j * 2 + 0) * LK * N;
     u64* a = key + ((size_t)j * 2 + 1) * LK * N;
 #pragma omp parallel for
     for (int i = 0; i < LK; i++) {
+      if (to_sparse && i >= 1 && i < L) continue;
       const u64 q = c->q[i];
       u64 Pmod = 1;
       for (int k = 0; k < K; k++) Pmod = mulmod(Pmod, c->q[L + k] % q, q);
@@ -606,7 +637,7 @@ int ock_keygen(const ock_ctx* c, u64 key_id, u64* key) {
       error_ntt(c, stream_key(key_id, j, 3), i, bi);
       for (size_t k = 0; k < N; k++) {
         ai[k] = uniform_mod(prng(c->seed, stream_key(key_id, j, 2), (u64)i * N + k), q);
-        u64 v = submod(bi[k], mulmod(ai[k], c->s_ntt[(size_t)i * N + k], q), q);
+        u64 v = submod(bi[k], mulmod(ai[k], s_to[(size_t)i * N + k], q), q);
         if (i >= lo && i < hi) v = addmod(v, mulmod(Pmod, sp[(size_t)i * N + k], q), q);
         bi[k] = v;
       }

@@ -70,6 +70,9 @@ void ock_decode_coeffs(const ock_ctx* c, const double* coeffs, double scale,
 void ock_secret(const ock_ctx* c, int8_t* s);
 /* switch to a sparse secret with exactly h nonzero coefficients (0 = uniform ternary) */
 void ock_set_hamming_weight(ock_ctx* c, int h);
+/* ephemeral sparse bootstrapping secret s_b (h_b nonzero) of the sparse-secret encapsulation;
+ * enables key ids 2 (s -> s_b, digit 0 on q_0 and P only) and 4 (s_b -> s) in ock_keygen */
+void ock_set_boot_secret(ock_ctx* c, int hb);
 int ock_keygen(const ock_ctx* c, uint64_t key_id, uint64_t* key);
 int ock_encrypt(const ock_ctx* c, const double* vals, size_t n,
                 uint64_t counter, uint64_t* ct);

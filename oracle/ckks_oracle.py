@@ -50,6 +50,7 @@ def lib():
         L.ock_secret.argtypes = [vp, _i8p]
         L.ock_set_hamming_weight.argtypes = [vp, C.c_int]
         L.ock_set_digit_split.argtypes = [vp, C.c_int]
+        L.ock_set_boot_secret.argtypes = [vp, C.c_int]
         L.ock_keygen.argtypes = [vp, C.c_uint64, _u64p]
         L.ock_encrypt.argtypes = [vp, _dblp, C.c_size_t, C.c_uint64, _u64p]
         L.ock_decrypt.argtypes = [vp, _u64p, C.c_int, C.c_double, _dblp]
@@ -190,6 +191,10 @@ class Oracle:
         s = np.zeros(self.N, np.int8)
         lib().ock_secret(self._c, s)
         return s
+
+    def set_boot_secret(self, hb=64):
+        """sparse-secret encapsulation: key ids 2 (s -> s_b) and 4 (s_b -> s)"""
+        lib().ock_set_boot_secret(self._c, int(hb))
 
     def keygen(self, key_id):
         key = np.zeros((self.dnum, 2, self.L + self.K, self.N), np.uint64)

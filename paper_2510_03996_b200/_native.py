@@ -32,6 +32,9 @@ class fheon_params(C.Structure):
         ("bootstrap", C.c_int),
         ("boot_scale_bits", C.c_int),
         ("digit_split", C.c_int),
+        ("boot_hamming_weight", C.c_int),
+        ("min_security", C.c_int),
+        ("allow_insecure", C.c_int),
     ]
 
 
@@ -60,6 +63,8 @@ SIGNATURES = {
     "fheon_last_error_kind": (C.c_int, []),
     "fheon_version": (C.c_int, []),
     "fheon_host_primes": (C.c_int, [C.POINTER(fheon_params), u64p, dp]),
+    "fheon_host_security": (C.c_int, [C.POINTER(fheon_params), dp, C.POINTER(C.c_int), dp]),
+    "fheon_ctx_security": (C.c_int, [vp, dp, C.POINTER(C.c_int)]),
     "fheon_host_encode": (C.c_int, [C.POINTER(fheon_params), dp, C.c_size_t, C.c_double, C.POINTER(C.c_int64)]),
     "fheon_cheb_relu_coefficients": (C.c_int, [C.c_double, C.c_int, dp]),
     "fheon_ctx_create": (C.c_int, [C.POINTER(fheon_params), pp]),

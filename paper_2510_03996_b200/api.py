@@ -121,6 +121,14 @@ class ContextConfig:
     bootstrap: bool = False   # build the CKKS bootstrapping pipeline
     boot_scale_bits: int = 0  # scale of the bootstrapping levels (0 = rescale_bits)
     digit_split: int = 0      # key-switching digits: 0 uniform, 1 balanced by prime bit size
+    # bootstrapping with a dense secret (hamming_weight 0): Hamming weight of the ephemeral
+    # sparse secret of the sparse-secret encapsulation (0 = the engine default, 64)
+    boot_hamming_weight: int = 0
+    # HE-standard security (homomorphicencryption.org 2018, uniform ternary secret): the engine
+    # refuses a chain whose log2(QP) exceeds the bound for N at `security` bits, or a sparse
+    # main secret, unless allow_insecure (toy rings, the reference's presets) is set
+    security: int = 128
+    allow_insecure: bool = False
     # layer rotation schedule: "fast" (hoisted / log-depth / baby-step giant-step,
     # same values and levels) or "reference" (the reference's exact rotation trace)
     schedule: str = "fast"
@@ -143,19 +151,24 @@ class ContextConfig:
     def preset(name: str) -> "ContextConfig":
         """Named parameter sets.  config1 = BASELINE configs[0] (N=2^14, 50/40-bit,
         depth 10, dnum 3); config2 = configs[1] (N=2^16, L=24 ~50-bit limbs, dnum 3);
-        lenet5 / large mirror the reference presets (backend.cpp:61-76)."""
+        lenet5 / large mirror the reference presets (backend.cpp:61-76).
+
+        Security (he_standard_security): config2 (log2 QP = 1690 <= 1747 at
+        N = 2^16) meets 128 bits; config1 (690 > 438 at N = 2^14) and the
+        reference's lenet5 / large presets (depth 25 at N = 2^14 / 2^15) cannot,
+        so those presets carry allow_insecure=True explicitly."""
         if name == "config1":
             return ContextConfig(16384, 8192, 10, CryptoMetadata(50, 40, 3), limbs=11, special_limbs=4,
-                                 special_bits=60)
+                                 special_bits=60, allow_insecure=True)
         if name == "config2":
             return ContextConfig(65536, 32768, 23, CryptoMetadata(60, 50, 3), limbs=24, special_limbs=8,
                                  special_bits=60)
         if name == "lenet5":
             return ContextConfig(16384, 8192, 25, CryptoMetadata(55, 40, 3), limbs=26, special_limbs=9,
-                                 special_bits=60)
+                                 special_bits=60, allow_insecure=True)
         if name == "large":
             return ContextConfig(32768, 16384, 25, CryptoMetadata(55, 40, 3), limbs=26, special_limbs=9,
-                                 special_bits=60)
+                                 special_bits=60, allow_insecure=True)
         raise ModelError(f'unknown context preset "{name}"', 2)
 
     def params(self) -> _native.fheon_params:
@@ -175,6 +188,9 @@ class ContextConfig:
         p.bootstrap = int(bool(self.bootstrap))
         p.boot_scale_bits = int(self.boot_scale_bits)
         p.digit_split = int(self.digit_split)
+        p.boot_hamming_weight = int(self.boot_hamming_weight)
+        p.min_security = int(self.security)
+        p.allow_insecure = int(bool(self.allow_insecure))
         return p
 
 
@@ -253,6 +269,12 @@ class SlotContext:
 
     def slots(self) -> int:
         return self._slots
+
+    def security(self) -> Dict[str, object]:
+        """log2(QP), ring dimension and the HE-standard security level of the chain."""
+        lq, lev = C.c_double(), C.c_int()
+        _check(_native.lib().fheon_ctx_security(self._h, C.byref(lq), C.byref(lev)))
+        return security_report(self.N, lq.value, lev.value, self.config)
 
     def depth_budget(self) -> int:
         """Levels of fresh encryptions and bootstrap outputs (resolved by the engine)."""
@@ -835,6 +857,28 @@ def host_primes(config: ContextConfig):
     scales = np.zeros(p.limbs, np.float64)
     _check(_native.lib().fheon_host_primes(C.byref(p), _u64ptr(primes), _dptr(scales)))
     return primes, scales
+
+
+def security_report(N: int, log_qp: float, level: int, config: ContextConfig) -> Dict[str, object]:
+    sparse = config.hamming_weight > 0
+    return {"ring_dimension": int(N), "log2_qp": round(float(log_qp), 1),
+            "he_standard_128_bound": {1 << 14: 438, 1 << 15: 881, 1 << 16: 1747}.get(int(N)),
+            "security_bits": None if level < 0 else int(level),
+            "meets_128": bool(level >= 128),
+            "secret": (f"sparse ternary h={config.hamming_weight} (not covered by the HE-standard table)" if sparse
+                       else "uniform ternary" + (f"; bootstrapping via sparse-secret encapsulation (ephemeral h="
+                                                 f"{config.boot_hamming_weight or 64} on q_0 and P only)"
+                                                 if config.bootstrap else "")),
+            "estimate": "HE standard (homomorphicencryption.org 2018) Table 1, uniform ternary, classical; "
+                        "N = 2^16 row as shipped by OpenFHE (1747 / 1224 / 956 bits)"}
+
+
+def host_security(config: ContextConfig) -> Dict[str, object]:
+    """The security disclosure of a parameter set, computed on the host (no GPU)."""
+    p = config.params()
+    lq, lev, bound = C.c_double(), C.c_int(), C.c_double()
+    _check(_native.lib().fheon_host_security(C.byref(p), C.byref(lq), C.byref(lev), C.byref(bound)))
+    return security_report(config.ring_dimension, lq.value, lev.value, config)
 
 
 def host_encode(config: ContextConfig, values, scale: float) -> np.ndarray:

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <set>
 
@@ -225,12 +226,18 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
   {
     std::vector<int> sizes = split(bp.cts_levels);
     std::vector<Mat> groups;
-    const double c = std::pow(1.0 / (2.0 * K1), 1.0 / bp.cts_levels);
+    // 1 / (2 (K + 1)) spread evenly over the levels -- or, when the first level's
+    // plaintexts (scale T_{L-2} q_{L-1} / q_0, about 2^65 on 60-bit bootstrapping
+    // levels) would overflow the encoder's 2^62, all on the first level
+    const double first_pt_scale = h.T[L - 2] * (double)h.q[L - 1] / (double)h.q[0];
+    const double c_even = std::pow(1.0 / (2.0 * K1), 1.0 / bp.cts_levels);
+    const bool front = first_pt_scale * c_even > std::ldexp(1.0, 60);
     long len = S_;
     for (int gsz : sizes) {
       Mat M = stage((int)len, true);
       len /= 2;
       for (int i = 1; i < gsz; ++i, len /= 2) M = mul(stage((int)len, true), M);
+      const double c = front ? (groups.empty() ? 1.0 / (2.0 * K1) : 1.0) : c_even;
       for (auto& [d, v] : M)
         for (auto& x : v) x *= c;
       groups.push_back(M);
@@ -263,6 +270,12 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
   ctx.gen_key(0);                 // relinearisation
   ctx.pin_key(2 * (u64)h.N - 1);
   ctx.pin_key(0);
+  if (ctx.sse()) {  // sparse-secret encapsulation keys
+    for (u64 id : {kKeyToSparse, kKeyFromSparse}) {
+      ctx.gen_key(id);
+      ctx.pin_key(id);
+    }
+  }
 }
 
 std::vector<long> Bootstrapper::rotation_steps() const {
@@ -346,18 +359,86 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0) {
     const HostTables& h = ctx_.host();
     Ciphertext x = x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0;
     const double corr = x.scale / h.T[0];
+    static const bool dbg = std::getenv("FHEON_BOOT_DEBUG") != nullptr;
+    const std::size_t S = (std::size_t)h.S;
+    std::vector<double> are(S), aim(S), bre(S), bim(S), cre(S), cim(S);
+    auto maxdiff = [&](const std::vector<double>& a, const std::vector<double>& b) {
+      double m = 0.0;
+      for (std::size_t i = 0; i < S; ++i) m = std::max(m, std::fabs(a[i] - b[i]));
+      return m;
+    };
     Ciphertext y = mod_raise(ctx_, x);
     for (const Level& lv : cts_) y = apply(y, lv);
     const Ciphertext yc = conjugate_many(ctx_, {y})[0];
     std::vector<Ciphertext> ys = {add(ctx_, y, yc), mul_by_i(ctx_, sub(ctx_, yc, y))};
+    std::vector<double> in0, in1;
+    if (dbg) {
+      decrypt(ctx_, y, are.data(), aim.data());
+      decrypt(ctx_, ys[0], bre.data(), bim.data());
+      decrypt(ctx_, ys[1], cre.data(), cim.data());
+      std::vector<double> t0(S), t1(S), z0(S, 0.0);
+      double mx = 0.0;
+      for (std::size_t i = 0; i < S; ++i) {
+        t0[i] = 2 * are[i];
+        t1[i] = 2 * aim[i];
+        mx = std::max(mx, std::fabs(are[i]) + std::fabs(aim[i]));
+      }
+      std::fprintf(stderr, "[boot] CtS out max|u| %.3e limbs %d scale 2^%.2f; split re err %.3e im-part %.3e; "
+                           "split im err %.3e im-part %.3e\n", mx, y.limbs, std::log2(y.scale), maxdiff(bre, t0),
+                   maxdiff(bim, z0), maxdiff(cre, t1), maxdiff(cim, z0));
+      in0 = bre;
+      in1 = cre;
+    }
     ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
+    if (dbg) {
+      decrypt(ctx_, ys[0], bre.data(), bim.data());
+      std::vector<double> w(S);
+      const double K1 = bp_.k_range + 1.0;
+      for (std::size_t i = 0; i < S; ++i) w[i] = std::cos(2.0 * kPi * (K1 * in0[i] / 2.0 - 0.25) / std::ldexp(1.0, bp_.double_angles));
+      std::fprintf(stderr, "[boot] cos poly out limbs %d scale 2^%.2f err %.3e\n", ys[0].limbs, std::log2(ys[0].scale),
+                   maxdiff(bre, w));
+    }
     for (int i = 0; i < bp_.double_angles; ++i) {
       std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
       ys = add_many(ctx_, sq, sq);
       for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
     }
+    if (dbg) {
+      decrypt(ctx_, ys[0], bre.data(), bim.data());
+      decrypt(ctx_, ys[1], cre.data(), cim.data());
+      std::vector<double> w0(S), w1(S);
+      const double K1 = bp_.k_range + 1.0;
+      for (std::size_t i = 0; i < S; ++i) {
+        w0[i] = std::sin(2.0 * kPi * K1 * in0[i] / 2.0);
+        w1[i] = std::sin(2.0 * kPi * K1 * in1[i] / 2.0);
+      }
+      double mo = 0.0;
+      for (std::size_t i = 0; i < S; ++i) mo = std::max(mo, std::fabs(w0[i]));
+      std::fprintf(stderr, "[boot] EvalMod out limbs %d scale 2^%.2f err re %.3e im %.3e (max|sin| %.3e)\n",
+                   ys[0].limbs, std::log2(ys[0].scale), maxdiff(bre, w0), maxdiff(cre, w1), mo);
+    }
     Ciphertext z = add(ctx_, ys[0], mul_by_i(ctx_, ys[1]));
+    std::vector<double> zre(S), zim(S);
+    if (dbg) decrypt(ctx_, z, zre.data(), zim.data());
     for (const Level& lv : stc_) z = apply(z, lv);
+    if (dbg) {
+      // expected StC output: the slots whose coefficients are (Re, Im) of z in bit-reversed
+      // order times q0 / (2 pi T_0)
+      const int logS = (int)std::lround(std::log2((double)S));
+      std::vector<double> co(2 * S), ore(S), oim(S), wre(S), wim(S);
+      const double c = (double)h.q[0] / (2.0 * kPi * h.T[0]);
+      for (std::size_t k = 0; k < S; ++k) {
+        const std::size_t b = bitrev((unsigned)k, logS);
+        co[k] = zre[b] * c;
+        co[k + S] = zim[b] * c;
+      }
+      ctx_.decode_coeffs(co.data(), 1.0, wre.data(), wim.data());
+      decrypt(ctx_, z, ore.data(), oim.data());
+      double zm = 0.0;
+      for (std::size_t i = 0; i < S; ++i) zm = std::max(zm, std::fabs(zre[i]) + std::fabs(zim[i]));
+      std::fprintf(stderr, "[boot] StC in max|z| %.3e; StC out limbs %d scale 2^%.2f err re %.3e im %.3e\n", zm,
+                   z.limbs, std::log2(z.scale), maxdiff(ore, wre), maxdiff(oim, wim));
+    }
     z.scale *= corr;
     if (z.level() > ctx_.depth_budget()) z = level_down(ctx_, z, ctx_.depth_budget() + 1);
     ctx_.set_tracing(tracing);

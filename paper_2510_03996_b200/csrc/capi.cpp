@@ -67,7 +67,27 @@ static fheon::Params to_params(const fheon_params* p) {
   prm.bootstrap = p->bootstrap;
   prm.boot_scale_bits = p->boot_scale_bits;
   prm.digit_split = p->digit_split;
+  if (p->boot_hamming_weight > 0) prm.boot_hamming_weight = p->boot_hamming_weight;
+  if (p->min_security > 0) prm.min_security = p->min_security;
+  prm.allow_insecure = p->allow_insecure;
   return prm;
+}
+
+int fheon_host_security(const fheon_params* p, double* log_qp, int* level, double* bound) {
+  return guard([&] {
+    need(p, "params");
+    fheon::HostTables h;
+    try {
+      h = fheon::make_tables(to_params(p));
+    } catch (const std::invalid_argument& e) {
+      throw fheon::Error(fheon::ErrKind::shape, e.what());
+    }
+    double b = 0.0;
+    for (std::size_t i = 0; i < h.q.size(); ++i) b += std::log2((double)h.q[i]);
+    if (log_qp) *log_qp = b;
+    if (level) *level = fheon::he_standard_security(h.p.logN, b, h.p.hamming_weight);
+    if (bound) *bound = fheon::he_standard_max_logqp(h.p.logN, h.p.min_security);
+  });
 }
 
 int fheon_host_primes(const fheon_params* p, uint64_t* primes, double* scales) {
@@ -127,6 +147,14 @@ void fheon_ctx_destroy(fheon_ctx* ctx) {
   if (!ctx) return;
   delete ctx->impl;
   delete ctx;
+}
+
+int fheon_ctx_security(const fheon_ctx* ctx, double* log_qp, int* level) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (log_qp) *log_qp = ctx->impl->log_qp();
+    if (level) *level = ctx->impl->security();
+  });
 }
 
 int fheon_ctx_info(const fheon_ctx* ctx, uint64_t* primes, double* scales, int* slots) {

@@ -192,8 +192,27 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
   depth_budget_ = p.depth_budget < 0 ? p.L - 1 : p.depth_budget;
   if (depth_budget_ < 1 || depth_budget_ > p.L - 1)
     throw Error(ErrKind::shape, "depth budget must lie in [1, L-1]");
-  if (p.bootstrap && p.hamming_weight <= 0)
-    throw Error(ErrKind::shape, "bootstrapping needs a sparse secret (hamming_weight > 0)");
+  if (p.bootstrap && p.hamming_weight <= 0 && p.boot_hamming_weight <= 0)
+    throw Error(ErrKind::shape, "bootstrapping with a dense secret needs boot_hamming_weight > 0 (sparse-secret "
+                                "encapsulation)");
+  {
+    double logqp = 0.0;
+    for (int i = 0; i < p.L + p.K; ++i) logqp += std::log2((double)ht_.q[i]);
+    log_qp_ = logqp;
+    security_ = he_standard_security(p.logN, logqp, p.hamming_weight);
+    const int want = p.min_security > 0 ? p.min_security : 128;
+    if (!p.allow_insecure && security_ < want) {
+      const double bound = he_standard_max_logqp(p.logN, want);
+      std::string why = p.hamming_weight > 0
+                            ? "a sparse main secret (hamming_weight " + std::to_string(p.hamming_weight) +
+                                  ") is not covered by the HE-standard table; use a dense secret (bootstrapping "
+                                  "then runs the sparse-secret encapsulation)"
+                            : "log2(QP) = " + std::to_string((int)std::ceil(logqp)) + " bits exceeds the HE-standard "
+                                  "bound of " + std::to_string((int)bound) + " bits for N = 2^" +
+                                  std::to_string(p.logN) + " at " + std::to_string(want) + "-bit security";
+      throw Error(ErrKind::shape, "insecure parameters: " + why + " (set allow_insecure to run them anyway)");
+    }
+  }
   int dev = 0;
   FHEON_CUDA(cudaGetDevice(&dev));
   FHEON_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -444,33 +463,45 @@ void Context::build_device_tables() {
     auto prng_h = [&](u64 stream, u64 idx) {
       return mix64(prng_stream_key(p.seed, stream) ^ (idx * 0xD1B54A32D192ED03ULL + 0x8CB92BA72F3D8DD7ULL));
     };
+    // sparse: candidate j -> position prng(pos_stream, j) % N if unused, sign bit 0 of
+    // prng(pos_stream + 1, j); main secret streams 6/7, bootstrapping secret 8/9
+    auto sparse = [&](std::vector<long long>& v, int h, u64 pos_stream) {
+      int got = 0;
+      for (u64 j = 0; got < h; ++j) {
+        const std::size_t pos = (std::size_t)(prng_h(pos_stream, j) % N);
+        if (v[pos]) continue;
+        v[pos] = (prng_h(pos_stream + 1, j) & 1) ? 1 : -1;
+        ++got;
+      }
+    };
     if (p.hamming_weight <= 0) {
       for (std::size_t k = 0; k < N; ++k) s[k] = (long long)(prng_h(kStreamSecret, k) % 3) - 1;
     } else {
-      // sparse: candidate j -> position prng(6, j) % N if unused, sign bit 0 of prng(7, j)
-      int got = 0;
-      for (u64 j = 0; got < p.hamming_weight; ++j) {
-        const std::size_t pos = (std::size_t)(prng_h(6, j) % N);
-        if (s[pos]) continue;
-        s[pos] = (prng_h(7, j) & 1) ? 1 : -1;
-        ++got;
-      }
+      sparse(s, p.hamming_weight, 6);
     }
-    long long* dcoef = upload(dev_allocs_, s, stream_);
-    u64* sntt = nullptr;
-    FHEON_CUDA(cudaMalloc(reinterpret_cast<void**>(&sntt), (std::size_t)NP * N * sizeof(u64)));
-    dev_allocs_.push_back(sntt);
-    coeffs_to_rns(dt_, sntt, dcoef, NP, stream_);
-    LimbSet ls{};
-    ls.base[0] = sntt;
-    ls.nbase = 1;
-    ls.blocks_per_base = 1;
-    ls.block_stride = 0;
-    ls.E = NP;
-    ls.ell = NP;
-    ls.L = L;
-    ntt_forward(dt_, ls, stream_);
-    t.s_ntt = sntt;
+    auto to_ntt = [&](const std::vector<long long>& v) {
+      long long* dcoef = upload(dev_allocs_, v, stream_);
+      u64* sntt = nullptr;
+      FHEON_CUDA(cudaMalloc(reinterpret_cast<void**>(&sntt), (std::size_t)NP * N * sizeof(u64)));
+      dev_allocs_.push_back(sntt);
+      coeffs_to_rns(dt_, sntt, dcoef, NP, stream_);
+      LimbSet ls{};
+      ls.base[0] = sntt;
+      ls.nbase = 1;
+      ls.blocks_per_base = 1;
+      ls.block_stride = 0;
+      ls.E = NP;
+      ls.ell = NP;
+      ls.L = L;
+      ntt_forward(dt_, ls, stream_);
+      return sntt;
+    };
+    t.s_ntt = to_ntt(s);
+    if (p.bootstrap && p.hamming_weight <= 0) {
+      std::vector<long long> sb(N, 0);
+      sparse(sb, p.boot_hamming_weight, 8);
+      t.sb_ntt = to_ntt(sb);
+    }
   }
   FHEON_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -503,8 +534,19 @@ void Context::gen_key(u64 key_id) {
   const std::size_t N = ht_.N, LN = (std::size_t)NP * N;
   BufPtr kb = alloc(key_words());
   BufPtr sp = alloc(LN);
+  // evk_j = (-a_j s_to + e_j + [i in D_j] P s_from, a_j): s_from = s^2 (relinearisation),
+  // sigma_g(s) (rotation), s (-> sparse) or s_b (<- sparse); s_to = s except for the
+  // switch to the sparse bootstrapping secret
+  const u64* s_to = dt_.s_ntt;
+  const bool sse_key = key_id == kKeyToSparse || key_id == kKeyFromSparse;
+  if (sse_key && !dt_.sb_ntt) throw Error(ErrKind::internal, "no sparse bootstrapping secret in this context");
   if (key_id == 0) {
     secret_square(dt_, sp->ptr, stream_);
+  } else if (key_id == kKeyToSparse) {
+    FHEON_CUDA(cudaMemcpyAsync(sp->ptr, dt_.s_ntt, LN * sizeof(u64), cudaMemcpyDeviceToDevice, stream_));
+    s_to = dt_.sb_ntt;
+  } else if (key_id == kKeyFromSparse) {
+    FHEON_CUDA(cudaMemcpyAsync(sp->ptr, dt_.sb_ntt, LN * sizeof(u64), cudaMemcpyDeviceToDevice, stream_));
   } else {
     if ((key_id & 1) == 0) throw Error(ErrKind::internal, "Galois element must be odd");
     PolyList o{}, in{};
@@ -527,14 +569,20 @@ void Context::gen_key(u64 key_id) {
   ls.E = NP;
   ls.ell = NP;
   ls.L = L;
-  for (int j = 0; j < p.dnum; ++j) {  // digits past ndig stay empty (lo = hi = L)
+  if (key_id == kKeyToSparse)  // only digit 0's q_0 and P limbs are ever read (level 0)
+    FHEON_CUDA(cudaMemsetAsync(kb->ptr, 0, key_words() * sizeof(u64), stream_));
+  for (int j = 0; j < (key_id == kKeyToSparse ? 1 : p.dnum); ++j) {  // digits past ndig stay empty (lo = hi = L)
     const int lo = j < ht_.ndig ? ht_.dig[j] : L, hi = j < ht_.ndig ? ht_.dig[j + 1] : L;
     sample_error(dt_, e->ptr, prng_stream_key(p.seed, stream_key(key_id, j, 3)), NP, NP, stream_);
     ntt_forward(dt_, ls, stream_);
     u64* b = kb->ptr + (std::size_t)(j * 2) * LN;
     u64* a = b + LN;
-    keygen_digit(dt_, b, a, e->ptr, sp->ptr, prng_stream_key(p.seed, stream_key(key_id, j, 2)), lo, hi, dpm->ptr,
-                 stream_);
+    keygen_digit(dt_, b, a, e->ptr, sp->ptr, s_to, prng_stream_key(p.seed, stream_key(key_id, j, 2)), lo, hi,
+                 dpm->ptr, stream_);
+    if (key_id == kKeyToSparse) {  // the sparse-secret sample exists on q_0 and P only
+      FHEON_CUDA(cudaMemsetAsync(b + N, 0, (std::size_t)(L - 1) * N * sizeof(u64), stream_));
+      FHEON_CUDA(cudaMemsetAsync(a + N, 0, (std::size_t)(L - 1) * N * sizeof(u64), stream_));
+    }
   }
   FHEON_CUDA(cudaStreamSynchronize(stream_));  // pmod host vector goes out of scope
   keys_[key_id] = kb;

@@ -130,6 +130,12 @@ class Context {
   int L() const { return ht_.p.L; }
   int K() const { return ht_.p.K; }
   int depth_budget() const { return depth_budget_; }
+  // security disclosure: log2(QP) of the whole chain and the HE-standard level it meets
+  // (he_standard_security: 128/192/256, 0 below 128, -1 sparse main secret)
+  double log_qp() const { return log_qp_; }
+  int security() const { return security_; }
+  // bootstrapping through the sparse-secret encapsulation (dense main secret)
+  bool sse() const { return ht_.p.bootstrap && ht_.p.hamming_weight <= 0; }
 
   BufPtr alloc(std::size_t words);
   Ciphertext new_ct(int limbs);
@@ -224,6 +230,8 @@ class Context {
   std::vector<cudaEvent_t> event_pool_;
   std::vector<std::pair<cudaEvent_t, BufPtr>> held_;
   int depth_budget_ = 0;
+  double log_qp_ = 0.0;
+  int security_ = 0;
   std::uint64_t id_counter_ = 0;
   std::vector<void*> dev_allocs_;  // table allocations
  public:

@@ -795,9 +795,31 @@ Ciphertext mul_by_i(Context& ctx, const Ciphertext& x) {
   return out;
 }
 
-// ModRaise of a level-0 ciphertext to all L limbs (decrypts to m + q_0 I)
+namespace {
+// key switch of x to the secret a key encapsulates: (c0 + ks0, ks1), automorphism-free
+Ciphertext switch_secret(Context& ctx, const Ciphertext& x, u64 key_id) {
+  KsJob jb{key_id, 1, x.c0, 1, nullptr};
+  Ciphertext y = keyswitch(ctx, {x.c1}, x.limbs, {jb})[0];
+  y.scale = x.scale;
+  return y;
+}
+Ciphertext mod_raise_raw(Context& ctx, const Ciphertext& x);
+}  // namespace
+
+// ModRaise of a level-0 ciphertext to all L limbs (decrypts to m + q_0 I).  With a
+// dense main secret (sparse-secret encapsulation, Bossuat et al. 2022) the level-0
+// ciphertext is first switched to the sparse bootstrapping secret s_b -- on q_0 only,
+// so |I| stays within the EvalMod range -- raised under s_b, and switched back to
+// the dense secret over the whole chain.
 Ciphertext mod_raise(Context& ctx, const Ciphertext& x) {
   if (x.limbs != 1) throw Error(ErrKind::internal, "mod_raise expects a level-0 ciphertext");
+  if (!ctx.sse()) return mod_raise_raw(ctx, x);
+  Ciphertext y = mod_raise_raw(ctx, switch_secret(ctx, x, kKeyToSparse));
+  return switch_secret(ctx, y, kKeyFromSparse);
+}
+
+namespace {
+Ciphertext mod_raise_raw(Context& ctx, const Ciphertext& x) {
   const DevTables& t = ctx.dev();
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
@@ -814,6 +836,7 @@ Ciphertext mod_raise(Context& ctx, const Ciphertext& x) {
   out.scale = (double)ctx.host().q[0];
   return out;
 }
+}  // namespace
 
 Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d, u64 key_id, u64 g) {
   std::vector<Ciphertext> r = keyswitch(ctx, {d.c1}, d.limbs, {{key_id, g, nullptr, 1, nullptr}});

@@ -48,6 +48,7 @@ struct DevTables {
   u64* rs = nullptr;
   // secret key, NTT domain standard form [L+K][N]
   u64* s_ntt = nullptr;
+  u64* sb_ntt = nullptr;  // ephemeral sparse bootstrapping secret (sparse-secret encapsulation), NTT over L+K
   // optional live kernel timer (owned by the Context)
   KernelTimer* timer = nullptr;
 };
@@ -250,8 +251,8 @@ void sample_error(const DevTables& t, u64* out, u64 stream_key, int nlimbs, int 
 void encrypt_combine(const DevTables& t, u64* c0, u64* c1, const u64* m, const u64* e, u64 stream_a, int limbs,
                      cudaStream_t st);
 // one key digit over all L+K limbs: a uniform, b = e - a s + [i in digit] (P mod q_i) sp; stored Montgomery
-void keygen_digit(const DevTables& t, u64* b, u64* a, const u64* e, const u64* sp, u64 stream_a, int lo, int hi,
-                  const u64* pmod, cudaStream_t st);
+void keygen_digit(const DevTables& t, u64* b, u64* a, const u64* e, const u64* sp, const u64* s_to, u64 stream_a,
+                  int lo, int hi, const u64* pmod, cudaStream_t st);
 // out = s^2 over all L+K limbs
 void secret_square(const DevTables& t, u64* out, cudaStream_t st);
 // m_i = c0_i + c1_i s_i, i < limbs

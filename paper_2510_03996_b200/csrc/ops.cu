@@ -783,9 +783,9 @@ void encrypt_combine(const DevTables& t, u64* c0, u64* c1, const u64* m, const u
   k_encrypt_combine<<<grid_for(t.N, limbs), kThreads, 0, st>>>(c0, c1, m, e, t.s_ntt, stream_a, t.pc, t.logN);
   launch_check("k_encrypt_combine");
 }
-void keygen_digit(const DevTables& t, u64* b, u64* a, const u64* e, const u64* sp, u64 stream_a, int lo, int hi,
-                  const u64* pmod, cudaStream_t st) {
-  k_keygen_digit<<<grid_for(t.N, t.L + t.K), kThreads, 0, st>>>(b, a, e, t.s_ntt, sp, stream_a, lo, hi, pmod, t.pc,
+void keygen_digit(const DevTables& t, u64* b, u64* a, const u64* e, const u64* sp, const u64* s_to, u64 stream_a,
+                  int lo, int hi, const u64* pmod, cudaStream_t st) {
+  k_keygen_digit<<<grid_for(t.N, t.L + t.K), kThreads, 0, st>>>(b, a, e, s_to, sp, stream_a, lo, hi, pmod, t.pc,
                                                                  t.logN);
 }
 void secret_square(const DevTables& t, u64* out, cudaStream_t st) {

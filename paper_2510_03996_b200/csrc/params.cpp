@@ -108,6 +108,25 @@ std::vector<int> balanced_digits(const std::vector<double>& bits, int dnum, int 
   return best;
 }
 
+// HE standard (Albrecht et al., "Homomorphic Encryption Security Standard",
+// homomorphicencryption.org 2018, Table 1, uniform ternary secret, classical
+// attacks): max log2(q) for N = 2^10 .. 2^15.  The standard stops at 2^15; the
+// 2^16 row is the extension libraries ship beside it (OpenFHE's HEStd tables).
+double he_standard_max_logqp(int logN, int bits) {
+  static const double tab[7][3] = {{27, 19, 14},    {54, 37, 29},    {109, 75, 58},   {218, 152, 118},
+                                   {438, 305, 237}, {881, 611, 476}, {1747, 1224, 956}};
+  if (logN < 10 || logN > 16) return 0.0;
+  const int col = bits <= 128 ? 0 : bits <= 192 ? 1 : 2;
+  return tab[logN - 10][col];
+}
+
+int he_standard_security(int logN, double log_qp, int hamming_weight) {
+  if (hamming_weight > 0) return -1;
+  for (int bits : {256, 192, 128})
+    if (log_qp <= he_standard_max_logqp(logN, bits)) return bits;
+  return 0;
+}
+
 HostTables make_tables(const Params& p) {
   if (p.logN < 10 || p.logN > 16) throw std::invalid_argument("logN must be in [10, 16]");
   if (p.L < 1 || p.K < 1 || p.L + p.K > kMaxPrimes || p.dnum < 1)
@@ -136,6 +155,12 @@ HostTables make_tables(const Params& p) {
   // to 2^scale_bits, so the raised ciphertext's linear transforms and the
   // modular-reduction polynomial run at full precision.
   std::vector<double> tbits(p.L, (double)p.scale_bits);
+  // "free" levels: the SlotsToCoeffs rescales when the bootstrapping levels are wider
+  // than 55 bits.  Those levels only ever multiply by plaintexts (encoded at
+  // T_{lv-1} q_lv / T_lv, bootstrap.cpp plan), so their primes need not follow
+  // T_lv^2 / T_{lv-1} -- which would exceed 2^61 on a steep 60 -> 40-bit ramp:
+  // q_lv is the prime nearest 4 T_{lv-1} and T_{lv-1} is the exact ramp target.
+  std::vector<char> free_level(p.L, 0);
   if (p.bootstrap && p.boot_scale_bits > p.scale_bits) {
     const int D = bootstrap_depth(p);
     const int lv_in = p.L - 1 - (D - p.boot_stc_levels);  // SlotsToCoeffs input level
@@ -145,6 +170,7 @@ HostTables make_tables(const Params& p) {
         const int k = lv_in - lv;  // 1..stc
         tbits[lv] = p.boot_scale_bits - (double)(p.boot_scale_bits - p.scale_bits) * k / p.boot_stc_levels;
       }
+      if (p.boot_scale_bits > 55 && lv <= lv_in && lv > lv_in - p.boot_stc_levels) free_level[lv] = 1;
     }
   }
   t.T.assign(p.L, 0.0);
@@ -153,7 +179,8 @@ HostTables make_tables(const Params& p) {
     double T = std::ldexp(1.0, (int)std::lround(tbits[p.L - 1]));
     t.T[p.L - 1] = T;
     for (int lv = p.L - 1; lv >= 1; --lv) {
-      const double target = (T * T) / std::ldexp(1.0, (int)std::lround(tbits[lv - 1]));
+      const double target = free_level[lv] ? std::exp2(tbits[lv - 1] + 2.0)
+                                            : (T * T) / std::ldexp(1.0, (int)std::lround(tbits[lv - 1]));
       if (!(target < std::ldexp(1.0, 61)) || !(target > std::ldexp(1.0, 20)))
         throw std::invalid_argument("scale schedule needs a prime outside [2^20, 2^61)");
       const u64 tgt = static_cast<u64>(target);
@@ -173,7 +200,7 @@ HostTables make_tables(const Params& p) {
         else if (ok(second)) pick = second;
       }
       chosen[lv] = pick;
-      T = (T * T) / static_cast<double>(pick);
+      T = free_level[lv] ? std::exp2(tbits[lv - 1]) : (T * T) / static_cast<double>(pick);
       t.T[lv - 1] = T;
     }
     for (int lv = 1; lv < p.L; ++lv) q.push_back(chosen[lv]);

@@ -41,7 +41,29 @@ struct Params {
   // digits balanced by bit size (the widest digit decides how many special primes
   // P needs, so a chain of mixed 40/55-bit primes wants unequal limb counts)
   int digit_split = 0;
+  // Sparse-secret encapsulation (bootstrapping with a DENSE main secret, hamming_weight = 0):
+  // the level-0 ciphertext is switched to an ephemeral sparse secret s_b with this many
+  // nonzero coefficients, ModRaised (|I| stays inside boot_k_range), and switched back to
+  // the dense secret at the top of the chain.  The s -> s_b key lives only on q_0 and the
+  // special primes.
+  int boot_hamming_weight = 64;
+  // HE-standard security (he_standard_max_logqp): context creation refuses a chain whose
+  // log2(QP) exceeds the bound for N at min_security bits unless allow_insecure is set
+  int min_security = 128;
+  int allow_insecure = 0;
 };
+
+// HE-standard (homomorphicencryption.org, 2018) maximum log2(QP) for a uniform
+// ternary secret at N = 2^logN and `bits` of classical security (128, 192, 256);
+// 0 when the table has no entry
+double he_standard_max_logqp(int logN, int bits);
+// security level (256/192/128) the chain meets under the table, 0 when below 128;
+// -1 when the main secret is sparse (not covered by the table)
+int he_standard_security(int logN, double log_qp, int hamming_weight);
+
+// key ids of the sparse-secret encapsulation keys (even: never a Galois element)
+constexpr std::uint64_t kKeyToSparse = 2;    // s -> s_b, on q_0 and P only
+constexpr std::uint64_t kKeyFromSparse = 4;  // s_b -> s, whole chain
 
 // contiguous split of per-limb bit sizes into at most `dnum` digits minimising the
 // widest digit's bit sum (each digit <= max_size limbs); returns boundaries 0 = d_0 < ... < d_n = L

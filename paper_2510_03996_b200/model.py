@@ -678,33 +678,69 @@ def count_bootstraps(layers: List[Built]) -> int:
 
 
 # ----------------------------------------------------------------- engine
-def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: str = "fast") -> fh.ContextConfig:
+def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: str = "fast",
+                security: int = 128) -> fh.ContextConfig:
     """RNS chain for the spec's ring and depth budget: 55-bit q0, 40-bit
-    application primes, 55-bit bootstrapping levels (+16 levels), dnum 3."""
+    application primes, 55-bit bootstrapping levels (+16 levels), digits
+    balanced by prime bit size, 60-bit special primes (the fewest whose product
+    exceeds the widest digit by 2 bits).
+
+    security > 0 (default 128): a uniform ternary secret (bootstrapping through
+    the sparse-secret encapsulation, its CoeffsToSlots / EvalMod levels at 60
+    bits: the dense secret's rounding noise is ~26x the h = 64 one, and the
+    SlotsToCoeffs map amplifies EvalMod noise by sqrt(S) q0 / (2 pi Delta_0);
+    the SlotsToCoeffs ramp 60 -> 40 bits runs on "free" plaintext-only levels,
+    params.cpp) and the fewest key-switching digits dnum >= 3
+    whose chain fits the HE-standard log2(QP) bound for N at `security` bits --
+    more digits mean a narrower widest digit, so fewer special primes.  Raises
+    ModelError when no dnum fits (e.g. the reference's depth budget 25 with
+    bootstrapping at N = 2^16: log2(Q) alone exceeds 1747).
+    security = 0: the round-1 chain kept for the reference's presets -- sparse
+    h = 64 main secret, dnum 3, allow_insecure (disclosed in host_security)."""
     N = spec.ring_dimension
     if spec.slot_count != N // 2:
         raise fh.ShapeError("the engine packs fully: slot_count must be ring_dimension / 2", 2)
     boot_depth = 16 if bootstrapping else 0
     L = spec.depth_budget + 1 + boot_depth
-    dnum = 3
+    secure = security > 0
 
-    def config(K):
+    def config(K, dnum):
         return fh.ContextConfig(N, N // 2, spec.depth_budget if not bootstrapping else -1,
                                 fh.CryptoMetadata(55, 40, dnum), limbs=L, special_limbs=K, special_bits=60, seed=seed,
-                                hamming_weight=64 if bootstrapping else 0, bootstrap=bootstrapping,
-                                boot_scale_bits=55 if bootstrapping else 0, schedule=schedule, digit_split=1)
+                                hamming_weight=0 if (secure or not bootstrapping) else 64, bootstrap=bootstrapping,
+                                boot_scale_bits=(60 if secure else 55) if bootstrapping else 0, schedule=schedule,
+                                digit_split=1,
+                                security=security if secure else 128, allow_insecure=not secure)
 
-    # digits balanced by bit size over the real Q chain (the special primes are
-    # chosen after it, so K does not change it); K = the fewest 60-bit special
-    # primes whose product exceeds the widest digit by 2 bits (the engine re-checks)
-    qbits = [math.log2(float(q)) for q in fh.host_primes(config(1))[0][:L]]
-    K = -(-int(balanced_widest(qbits, dnum) + 2.0) // 59) + 0
-    while True:
-        cfg = config(K)
-        pbits = sum(math.log2(float(q)) for q in fh.host_primes(cfg)[0][L:])
-        if pbits > balanced_widest(qbits, dnum):
+    def smallest_k(dnum):
+        # digits balanced by bit size over the real Q chain (the special primes are
+        # chosen after it, so K does not change it)
+        qbits = [math.log2(float(q)) for q in fh.host_primes(config(1, dnum))[0][:L]]
+        widest = balanced_widest(qbits, dnum)
+        K = max(1, -(-int(widest + 2.0) // 59))
+        while K < 16:
+            cfg = config(K, dnum)
+            pbits = sum(math.log2(float(q)) for q in fh.host_primes(cfg)[0][L:])
+            if pbits > widest:
+                return cfg
+            K += 1
+        return None
+
+    if not secure:
+        return smallest_k(3)
+    last = None
+    for dnum in range(3, min(L, 16) + 1):
+        cfg = smallest_k(dnum)
+        if cfg is None:
+            continue
+        sec = fh.host_security(cfg)
+        last = sec
+        if sec["security_bits"] is not None and sec["security_bits"] >= security:
             return cfg
-        K += 1
+    raise fh.ModelError(f"no {security}-bit chain for depth budget {spec.depth_budget} at N = {N}"
+                        + (" with bootstrapping" if bootstrapping else "")
+                        + (f": log2(QP) >= {last['log2_qp']} > {last['he_standard_128_bound']}" if last else "")
+                        + "; lower the depth budget or pass security=0 (insecure)", 2)
 
 
 def balanced_widest(bits: List[float], dnum: int, max_size: int = 15) -> float:
@@ -748,11 +784,15 @@ class InferResult:
 class EncryptedModel:
     """A built model bound to an engine context (keys generated on first use)."""
 
-    def __init__(self, spec: ModelSpec, seed: int = 1, schedule: str = "fast"):
+    def __init__(self, spec: ModelSpec, seed: int = 1, schedule: str = "fast", security: int = 128):
+        """security: HE-standard level the chain must meet (ckks_config); 0 runs
+        the insecure round-1 chain the reference's presets need (disclosed in
+        self.security)."""
         self.spec = spec
         self.layers = build(spec)
         self.n_boot = count_bootstraps(self.layers)
-        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule))
+        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule, security))
+        self.security = self.ctx.security()
         self._layer_keys: Optional[List[keyplan.LayerKeys]] = None
         self._pinned_keys = self.ctx.key_count()  # relinearisation / bootstrapping keys made at creation
         if spec.weight_mode == "lazy":

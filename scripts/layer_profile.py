@@ -15,7 +15,7 @@ from paper_2510_03996_b200 import model as M
 which = sys.argv[1] if len(sys.argv) > 1 else "conv2"
 depth = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 spec = M.resnet20(ring=65536, depth_budget=depth)
-ctx = fh.SlotContext(M.ckks_config(spec, True))
+ctx = fh.SlotContext(M.ckks_config(spec, True, security=int(__import__('os').environ.get('FHEON_SECURITY', '0'))))
 rng = np.random.default_rng(5)
 cudart = ctypes.CDLL("libcudart.so.12")
 

@@ -24,7 +24,7 @@ if which == "resnet20":
 else:
     spec = M.lenet5(ring=32768, depth_budget=depth)
     x = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
-em = M.EncryptedModel(spec)
+em = M.EncryptedModel(spec, security=int(__import__('os').environ.get('FHEON_SECURITY', '0')))
 em.infer(x)
 t0 = time.perf_counter()
 r = em.infer(x)

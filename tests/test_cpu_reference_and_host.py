@@ -193,3 +193,26 @@ def test_lenet_ledger_matches_reference(budget, tmp_path):
         assert r[1] == level
         level = budget if b.type == "bootstrap" else level - b.cost
         assert r[2] == level
+
+
+def test_security_disclosure_and_secure_chains():
+    """HE-standard security (homomorphicencryption.org 2018, uniform ternary):
+    configs[1] (log2 QP 1690 at N = 2^16) meets 128 bits; configs[0] (690 > 438
+    at N = 2^14) and the reference's presets do not (they carry allow_insecure);
+    the model runtime's default ResNet-20 chain at depth 12 meets 128 bits with a
+    dense secret, and refuses depth 25 (log2 Q alone exceeds the bound)."""
+    from paper_2510_03996_b200 import model as M
+    s2 = fh.host_security(fh.ContextConfig.preset("config2"))
+    assert s2["meets_128"] and s2["security_bits"] == 128 and abs(s2["log2_qp"] - 1690) < 5
+    s1 = fh.host_security(fh.ContextConfig.preset("config1"))
+    assert not s1["meets_128"] and s1["security_bits"] == 0
+    assert fh.ContextConfig.preset("config1").allow_insecure and fh.ContextConfig.preset("large").allow_insecure
+    cfg = M.ckks_config(M.resnet20(ring=65536, depth_budget=12), True)
+    sec = fh.host_security(cfg)
+    assert cfg.hamming_weight == 0 and sec["meets_128"] and sec["log2_qp"] <= 1747
+    assert "encapsulation" in sec["secret"]
+    with pytest.raises(fh.ModelError, match="no 128-bit chain"):
+        M.ckks_config(M.resnet20(ring=65536, depth_budget=25), True)
+    ins = M.ckks_config(M.resnet20(ring=65536, depth_budget=25), True, security=0)
+    si = fh.host_security(ins)
+    assert si["security_bits"] is None and not si["meets_128"] and si["log2_qp"] > 2600  # sparse h=64 main secret

@@ -17,10 +17,14 @@ LOGN, L = 12, 24
 N, S = 1 << LOGN, 1 << (LOGN - 1)
 
 
-@pytest.fixture(scope="module")
-def bctx():
+@pytest.fixture(scope="module", params=["sparse", "sse"])
+def bctx(request):
+    """sparse: the main secret itself sparse (h = 64); sse: a uniform ternary main
+    secret, bootstrapping through the sparse-secret encapsulation (level-0 switch
+    to an ephemeral h = 64 secret, ModRaise, switch back)."""
     cfg = fh.ContextConfig(N, S, -1, fh.CryptoMetadata(55, 40, 3), limbs=L, special_limbs=8, special_bits=60,
-                           seed=5, hamming_weight=64, bootstrap=True, boot_scale_bits=55)
+                           seed=5, hamming_weight=64 if request.param == "sparse" else 0, bootstrap=True,
+                           boot_scale_bits=55, allow_insecure=True)
     ctx = fh.SlotContext(cfg)
     M = 2 * N
     rot = np.array([pow(5, j, M) for j in range(S)], dtype=np.int64)
@@ -110,8 +114,35 @@ def test_bootstrap_from_higher_level(bctx):
 
 
 def test_bootstrap_requires_enabled_context():
-    cfg = fh.ContextConfig(4096, 2048, 5, fh.CryptoMetadata(50, 40, 3), limbs=6, special_limbs=2)
+    cfg = fh.ContextConfig(4096, 2048, 5, fh.CryptoMetadata(50, 40, 3), limbs=6, special_limbs=2,
+                           allow_insecure=True)
     ctx = fh.SlotContext(cfg)
     x = fh.SlotVector.encode(ctx, [1.0])
     with pytest.raises(fh.NotImplementedInEngine):
         fh.bootstrap(x)
+
+
+def test_sse_keys_and_switches_bit_exact():
+    """Sparse-secret encapsulation keys (ids 2: s -> s_b on q_0 and P only, 4:
+    s_b -> s) and the two key switches of ModRaise, bit-exact against the
+    oracle's restatement (ock_set_boot_secret / ock_keygen)."""
+    from oracle.ckks_oracle import Oracle
+    cfg = fh.ContextConfig(N, S, -1, fh.CryptoMetadata(55, 40, 3), limbs=L, special_limbs=8, special_bits=60,
+                           seed=6, bootstrap=True, boot_scale_bits=55, allow_insecure=True)
+    ctx = fh.SlotContext(cfg)
+    orc = Oracle.from_chain(LOGN, ctx.primes, ctx.scales, L, 8, 3, seed=6)
+    orc.set_boot_secret(64)
+    k2, k4 = orc.keygen(2), orc.keygen(4)
+    assert np.array_equal(ctx.download_key(2), k2)
+    assert np.array_equal(ctx.download_key(4), k4)
+    assert not k2[0, :, 1:L].any() and not k2[1:].any()  # the sparse sample lives on q_0 and P only
+    rng = np.random.default_rng(8)
+    ct = orc.encrypt(rng.uniform(-1, 1, S), 3)
+    x1 = fh.SlotVector.from_words(ctx, np.ascontiguousarray(ct[:, :1]), float(orc.T[0]))
+    ks = fh.keyswitch_raw(x1, 2, 1).words()
+    k0, k1 = orc.keyswitch(np.ascontiguousarray(ct[1, :1]), k2, 1)
+    assert np.array_equal(ks[0], k0) and np.array_equal(ks[1], k1)
+    xt = fh.SlotVector.from_words(ctx, ct, float(orc.T[-1]))
+    ks = fh.keyswitch_raw(xt, 4, 1).words()
+    k0, k1 = orc.keyswitch(ct[1], k4, 1)
+    assert np.array_equal(ks[0], k0) and np.array_equal(ks[1], k1)

@@ -18,7 +18,7 @@ N, S = 1 << LOGN, 1 << (LOGN - 1)
 @pytest.fixture(scope="module")
 def env():
     cfg = fh.ContextConfig(N, S, DEPTH, fh.CryptoMetadata(52, 40, 3), limbs=DEPTH + 1, special_limbs=3,
-                           special_bits=60, seed=77)
+                           special_bits=60, seed=77, allow_insecure=True)
     return fh.SlotContext(cfg), sref.Ref(N, S, DEPTH)
 
 

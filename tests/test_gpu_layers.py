@@ -26,7 +26,8 @@ def env(request):
     """Both rotation schedules: "reference" must replay the reference's trace
     multiset exactly; "fast" (the default) must give the same slots and levels."""
     cfg = fh.ContextConfig(1 << LOGN, 1 << (LOGN - 1), DEPTH, fh.CryptoMetadata(52, 40, 3), limbs=DEPTH + 1,
-                           special_limbs=4, special_bits=60, seed=9001, schedule=request.param)
+                           special_limbs=4, special_bits=60, seed=9001, schedule=request.param,
+                           allow_insecure=True)
     ctx = fh.SlotContext(cfg)
     return ctx, sref.Ref(1 << LOGN, 1 << (LOGN - 1), DEPTH)
 

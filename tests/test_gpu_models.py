@@ -14,10 +14,15 @@ from oracle import ref as sref
 pytestmark = pytest.mark.gpu
 
 
-def _compare(spec, x, schedule="reference"):
+def _compare(spec, x, schedule="reference", security=0):
+    """security=0: the insecure chains the reference's presets / toy rings need
+    (disclosed); security=128: the HE-standard 128-bit chain (dense secret,
+    sparse-secret encapsulation)."""
     path = spec.write(tempfile.mkdtemp())
     ref_logits, rows, ref_events, _ = sref.infer(path, x)
-    em = M.EncryptedModel(spec, schedule=schedule)
+    em = M.EncryptedModel(spec, schedule=schedule, security=security)
+    if security:
+        assert em.security["meets_128"] and em.security["log2_qp"] <= 1747
     rec = em.ctx.attach_recorder()
     r = em.infer(x)
     ev = [(e.kind, e.value) for e in rec.snapshot()]
@@ -56,8 +61,8 @@ def test_lenet5_config2_ring_depth25():
     _compare(spec, x, "fast")
 
 
-@pytest.mark.parametrize("schedule", ["reference", "fast"])
-def test_resnet20_full_ring_with_bootstrapping(schedule):
+@pytest.mark.parametrize("schedule,security", [("reference", 0), ("fast", 0), ("fast", 128)])
+def test_resnet20_full_ring_with_bootstrapping(schedule, security):
     """ResNet-20 (BASELINE configs[3]): N = 2^16, depth budget 12 -> 19 bootstraps,
     He-normal weights, calibrated frozen ReLU scales (beta = 8 diverges,
     SURVEY.md section 0 item 6), per-channel normalised U[0,1] input."""
@@ -68,7 +73,7 @@ def test_resnet20_full_ring_with_bootstrapping(schedule):
     cal = [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
     spec = M.calibrate_relu_scales(spec, cal)
     x = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
-    _compare(spec, x, schedule)
+    _compare(spec, x, schedule, security)
 
 
 def test_resnet20_reference_preset_depth25():
@@ -124,7 +129,7 @@ def test_batchnorm_explicit_bootstraps_end_to_end():
     json.dump(spec, open(path, "w"))
     x = np.random.default_rng(22).uniform(0, 1, (1, 8, 8))
     ref_logits, rows, ref_events, _ = sref.infer(path, x)
-    em = M.EncryptedModel(M.load_spec(path))
+    em = M.EncryptedModel(M.load_spec(path), security=0)
     r = em.infer(x)
     assert [(a[0], a[2], a[3]) for a in r.ledger] == [(b[0], b[1], b[2]) for b in rows]
     assert float(np.abs(r.logits - ref_logits).max()) < 1e-3
@@ -145,7 +150,7 @@ def test_layer_keys_reference_schedule_equal_reference_derive():
     use counts, same ends_block flags."""
     from model_files import materialize
     path = materialize("lenet5", tempfile.mkdtemp(), seed=4)
-    em = M.EncryptedModel(M.load_spec(path), schedule="reference")
+    em = M.EncryptedModel(M.load_spec(path), schedule="reference", security=0)
     ours = em.layer_keys()
     want = sref.layer_keys(path)
     assert [(lk.keys.usage, lk.ends_block) for lk in ours] == [(u, e) for u, e in want]
@@ -169,7 +174,7 @@ def test_block_key_mode_residency(name):
     spec = M.calibrate_relu_scales(spec, [prep(np.random.default_rng(600 + i).uniform(0, 1, shape))
                                           for i in range(3)])
     x = prep(np.random.default_rng(6).uniform(0, 1, shape))
-    em = M.EncryptedModel(spec)
+    em = M.EncryptedModel(spec, security=0)
     pre = em.infer(x, verify_keys=True)
     assert pre.trace_check.ok() and pre.trace_check.rotations_checked > 0
     preload_bytes = em.ctx.key_bytes()

@@ -18,7 +18,7 @@ SMALL = dict(logN=12, L=6, K=2, dnum=3, first=50, scale=40, special=60, seed=11)
 def make_pair(logN, L, K, dnum, first, scale, special, seed, depth=None, digit_split=0):
     cfg = fh.ContextConfig(1 << logN, 1 << (logN - 1), depth if depth is not None else L - 1,
                            fh.CryptoMetadata(first, scale, dnum), limbs=L, special_limbs=K, special_bits=special,
-                           seed=seed, digit_split=digit_split)
+                           seed=seed, digit_split=digit_split, allow_insecure=True)
     ctx = fh.SlotContext(cfg)
     orc = Oracle(logN, L, K, dnum, first, scale, special, seed, digit_split=digit_split)
     return ctx, orc

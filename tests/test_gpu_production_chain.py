@@ -40,7 +40,7 @@ def _digits(primes, L, dnum):
 
 @pytest.fixture(scope="module")
 def prod():
-    cfg = M.ckks_config(M.resnet20(ring=65536, depth_budget=25), True)
+    cfg = M.ckks_config(M.resnet20(ring=65536, depth_budget=25), True, security=0)
     ctx = fh.SlotContext(cfg)
     L, K = cfg.limbs, cfg.special_limbs
     orc = Oracle.from_chain(16, ctx.primes, ctx.scales, L, K, cfg.crypto.key_switch_digits, seed=cfg.seed,
@@ -153,7 +153,7 @@ def test_mode2_bconv_bit_exact(K):
     (K + 2 > 16) there.  Rotation, key switch and mult_cipher bit-exact."""
     logN, L, dnum = 12, 20, 2
     cfg = fh.ContextConfig(1 << logN, 1 << (logN - 1), L - 1, fh.CryptoMetadata(50, 40, dnum), limbs=L,
-                           special_limbs=K, special_bits=60, seed=31)
+                           special_limbs=K, special_bits=60, seed=31, allow_insecure=True)
     ctx = fh.SlotContext(cfg)
     orc = Oracle(logN, L, K, dnum, 50, 40, 60, 31)
     assert (orc.primes == ctx.primes).all()
@@ -170,3 +170,59 @@ def test_mode2_bconv_bit_exact(K):
         ys = fh.SlotVector.from_words(ctx, c2, float(orc.T[limbs - 1]))
         assert np.array_equal(fh.mult_cipher(xs, ys).words(), orc.mult_cipher(c, c2, orc.relin_key()))
         assert np.array_equal(fh.rotate(xs, -5).words(), orc.rotate(c, -5, orc.rotation_key(-5)))
+
+
+# ---- the 128-bit headline chain: ResNet-20 at depth budget 12, N = 2^16,
+# uniform ternary secret, sparse-secret encapsulation for bootstrapping, 60-bit
+# CoeffsToSlots / EvalMod levels, L = 29, K = 4, dnum = 8 (log2 QP = 1701 <= 1747,
+# model.ckks_config security=128)
+
+@pytest.fixture(scope="module")
+def secure():
+    cfg = M.ckks_config(M.resnet20(ring=65536, depth_budget=12), True)
+    ctx = fh.SlotContext(cfg)
+    sec = ctx.security()
+    assert sec["meets_128"] and sec["log2_qp"] <= 1747 and cfg.hamming_weight == 0
+    L, K = cfg.limbs, cfg.special_limbs
+    orc = Oracle.from_chain(16, ctx.primes, ctx.scales, L, K, cfg.crypto.key_switch_digits, seed=cfg.seed,
+                            digit_split=cfg.digit_split)
+    orc.set_boot_secret(64)
+    return ctx, orc, cfg
+
+
+def test_secure_chain_shape(secure):
+    ctx, orc, cfg = secure
+    assert (cfg.limbs, cfg.special_limbs, cfg.crypto.key_switch_digits) == (29, 4, 8)
+    assert len(_digits(ctx.primes, cfg.limbs, 8)) == 8
+    assert max(int(q).bit_length() for q in ctx.primes) == 61  # 60-bit-target bootstrapping primes
+
+
+@pytest.mark.parametrize("limbs", [29, 13, 1])
+def test_secure_rotation_and_mult_cipher_bit_exact(secure, limbs):
+    ctx, orc, _ = secure
+    a = np.ascontiguousarray(_ct(orc, 7800 + limbs, 20)[1][:, :limbs])
+    b = np.ascontiguousarray(_ct(orc, 7900 + limbs, 21)[1][:, :limbs])
+    sc = float(orc.T[limbs - 1])
+    x, y = fh.SlotVector.from_words(ctx, a, sc), fh.SlotVector.from_words(ctx, b, sc)
+    assert np.array_equal(fh.rotate(x, 3).words(), orc.rotate(a, 3, orc.rotation_key(3)))
+    if limbs > 1:
+        assert np.array_equal(fh.mult_cipher(x, y).words(), orc.mult_cipher(a, b, orc.relin_key()))
+        want = orc.rotate_sum([a, b], [3, -9], [orc.rotation_key(3), orc.rotation_key(-9)])
+        assert np.array_equal(fh.rotate_sum([x, y], [3, -9]).words(), want)
+
+
+def test_secure_sse_keys_bit_exact(secure):
+    ctx, orc, _ = secure
+    assert np.array_equal(ctx.download_key(2), orc.keygen(2))
+    assert np.array_equal(ctx.download_key(4), orc.keygen(4))
+
+
+def test_secure_bootstrap_precision(secure):
+    """Full-slot bootstrapping through the sparse-secret encapsulation at the
+    headline chain: lands on the depth budget within 1e-4."""
+    ctx, _, _ = secure
+    v = np.random.default_rng(31).uniform(-1, 1, ctx.slots())
+    x = fh.level_down(fh.SlotVector.encode(ctx, v), 1)
+    y = fh.bootstrap(x)
+    assert y.level() == ctx.depth_budget() == 12
+    assert np.abs(y.slots() - v).max() < 1e-4
