@@ -870,6 +870,26 @@ class EncryptedModel:
         c = self.ctx
         return keyplan.MemoryModel.for_engine(c.N, c.L, c.K, c.dnum, self._pinned_keys)
 
+    def output_count(self) -> int:
+        packed, C, W, n = self.layers[-1].out_shape
+        return C * W * W if packed else n
+
+    def encrypt_input(self, x: np.ndarray) -> fh.SlotVector:
+        """SlotVector::encode of the flattened input tensor at the depth budget."""
+        x = np.asarray(x, np.float64)
+        if x.shape != (self.spec.input_channels, self.spec.input_width, self.spec.input_width):
+            raise fh.ShapeError(f"input tensor is {x.shape}, the model expects "
+                                f"{(self.spec.input_channels, self.spec.input_width, self.spec.input_width)}", 2)
+        return fh.SlotVector.encode(self.ctx, x.reshape(-1))
+
+    def forward(self, v: fh.SlotVector) -> fh.SlotVector:
+        """The encrypted forward pass alone: an input ciphertext resident in HBM to
+        the logits ciphertext (preload key residency, no host synchronisation
+        beyond the engine's own)."""
+        for b in self.layers:
+            v = self._run(b, v, None)
+        return v
+
     def infer(self, x: np.ndarray, time_layers: bool = False, key_mode: str = "preload",
               verify_keys: bool = False) -> InferResult:
         """Encrypt, run every layer on the GPU, decrypt the logits (model_run.cpp:100-159).
