@@ -61,6 +61,11 @@ typedef struct {
    * secret is sparse, unless allow_insecure = 1 (the reference's presets need it) */
   int min_security;
   int allow_insecure;
+  /* 1: a SERVER context holding no secret key.  Evaluation keys (rotation, relinearisation,
+   * the bootstrapping set listed by fheon_required_key_ids) arrive by fheon_key_upload*;
+   * encrypt / decrypt / key generation fail.  The client creates a context with the same
+   * parameters (and seed) and generates / downloads the keys. */
+  int no_secret;
 } fheon_params;
 
 /* ---- errors / version */
@@ -114,6 +119,23 @@ int fheon_set_strict_keys(fheon_ctx* ctx, int strict); /* 1: missing key is an e
 /* key_id: 0 = relinearisation, else Galois element; out [dnum][2][L+K][N] standard form */
 int fheon_key_download(fheon_ctx* ctx, uint64_t key_id, uint64_t* out);
 size_t fheon_key_count(const fheon_ctx* ctx);
+/* evaluation-key serialization (PAPER.md:541-566 describes serialized keys; the reference has
+ * none): the packed wire format of the ciphertexts applied to the key's 2 dnum polys of L+K
+ * limbs, standard form.  Upload makes the key resident under key_id (replacing one of the same
+ * id); the _async variant copies on the context's upload stream and converts on the device,
+ * the compute stream waits for it, the pinned host buffer must stay valid until
+ * fheon_ctx_wait_transfers.  fheon_key_upload takes raw [dnum][2][L+K][N] standard-form words. */
+size_t fheon_key_packed_words(const fheon_ctx* ctx);
+int fheon_key_download_packed(fheon_ctx* ctx, uint64_t key_id, uint64_t* packed);
+int fheon_key_upload(fheon_ctx* ctx, uint64_t key_id, const uint64_t* words);
+int fheon_key_upload_packed(fheon_ctx* ctx, uint64_t key_id, const uint64_t* packed);
+int fheon_key_upload_packed_async(fheon_ctx* ctx, uint64_t key_id, const uint64_t* packed);
+/* ids of the keys the context needs beyond rotation keys: relinearisation (0), conjugation,
+ * the bootstrapping rotations and the encapsulation keys (2, 4) -- what a client uploads to a
+ * no_secret server context before the first bootstrap */
+int fheon_required_key_ids(const fheon_ctx* ctx, uint64_t* ids, size_t cap, size_t* n);
+/* keys received by upload (count, bytes) since the last fheon_ctx_reset_stats */
+int fheon_key_uploads(const fheon_ctx* ctx, uint64_t* count, uint64_t* bytes);
 /* key residency for keyplan block mode (keyplan.hpp:69-112 BlockPlan; model_run.cpp:150 key_mode):
  * resident evaluation-key bytes; generate a block's rotation keys ahead of it (stream-ordered,
  * no host sync); drop keys the next block does not use (freed after their last enqueued use,

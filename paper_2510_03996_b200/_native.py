@@ -35,6 +35,7 @@ class fheon_params(C.Structure):
         ("boot_hamming_weight", C.c_int),
         ("min_security", C.c_int),
         ("allow_insecure", C.c_int),
+        ("no_secret", C.c_int),
     ]
 
 
@@ -65,6 +66,13 @@ SIGNATURES = {
     "fheon_host_primes": (C.c_int, [C.POINTER(fheon_params), u64p, dp]),
     "fheon_host_security": (C.c_int, [C.POINTER(fheon_params), dp, C.POINTER(C.c_int), dp]),
     "fheon_ctx_security": (C.c_int, [vp, dp, C.POINTER(C.c_int)]),
+    "fheon_key_packed_words": (C.c_size_t, [vp]),
+    "fheon_key_download_packed": (C.c_int, [vp, C.c_uint64, u64p]),
+    "fheon_key_upload": (C.c_int, [vp, C.c_uint64, u64p]),
+    "fheon_key_upload_packed": (C.c_int, [vp, C.c_uint64, u64p]),
+    "fheon_key_upload_packed_async": (C.c_int, [vp, C.c_uint64, u64p]),
+    "fheon_required_key_ids": (C.c_int, [vp, u64p, C.c_size_t, szp]),
+    "fheon_key_uploads": (C.c_int, [vp, u64p, u64p]),
     "fheon_host_encode": (C.c_int, [C.POINTER(fheon_params), dp, C.c_size_t, C.c_double, C.POINTER(C.c_int64)]),
     "fheon_cheb_relu_coefficients": (C.c_int, [C.c_double, C.c_int, dp]),
     "fheon_ctx_create": (C.c_int, [C.POINTER(fheon_params), pp]),

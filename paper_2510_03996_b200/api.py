@@ -129,6 +129,9 @@ class ContextConfig:
     # main secret, unless allow_insecure (toy rings, the reference's presets) is set
     security: int = 128
     allow_insecure: bool = False
+    # a server context without the secret key: evaluation keys arrive by upload
+    # (SlotContext.key_upload), encrypt / decrypt are refused
+    no_secret: bool = False
     # layer rotation schedule: "fast" (hoisted / log-depth / baby-step giant-step,
     # same values and levels) or "reference" (the reference's exact rotation trace)
     schedule: str = "fast"
@@ -191,6 +194,7 @@ class ContextConfig:
         p.boot_hamming_weight = int(self.boot_hamming_weight)
         p.min_security = int(self.security)
         p.allow_insecure = int(bool(self.allow_insecure))
+        p.no_secret = int(bool(self.no_secret))
         return p
 
 
@@ -299,6 +303,7 @@ class SlotContext:
     def wait_transfers(self):
         """Block until every asynchronous upload / download has completed."""
         _check(_native.lib().fheon_ctx_wait_transfers(self._h))
+        self._keep = []
 
     def set_weight_cache(self, nbytes: int):
         """HBM budget of resident weight plaintexts (weight_mode "preload"); 0 = "lazy"."""
@@ -359,6 +364,47 @@ class SlotContext:
         return out
 
     # ---- misc
+    # ---- evaluation-key serialization / upload (client -> server, keyplan streaming)
+    def key_packed_words(self) -> int:
+        return int(_native.lib().fheon_key_packed_words(self._h))
+
+    def key_download_packed(self, key_id: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """The key's packed wire-format words (standard form, every limb at its prime's bit width)."""
+        if out is None:
+            out = np.zeros(self.key_packed_words(), np.uint64)
+        _check(_native.lib().fheon_key_download_packed(self._h, int(key_id), _u64ptr(out)))
+        return out
+
+    def key_upload(self, key_id: int, words: np.ndarray, packed: bool = True, async_copy: bool = False):
+        """Make an evaluation key resident from host words (packed wire format, or raw
+        [dnum][2][L+K][N] standard form).  async_copy: on the upload stream (keep the
+        pinned host buffer alive until wait_transfers)."""
+        w = np.ascontiguousarray(words, np.uint64)
+        if async_copy:
+            if not packed:
+                raise ShapeError("asynchronous key upload takes the packed format", 2)
+            self._keep = getattr(self, "_keep", [])
+            self._keep.append(w)
+            _check(_native.lib().fheon_key_upload_packed_async(self._h, int(key_id), _u64ptr(w)))
+        elif packed:
+            _check(_native.lib().fheon_key_upload_packed(self._h, int(key_id), _u64ptr(w)))
+        else:
+            _check(_native.lib().fheon_key_upload(self._h, int(key_id), _u64ptr(w)))
+
+    def required_key_ids(self) -> List[int]:
+        """Relinearisation, conjugation, bootstrapping rotations and encapsulation keys
+        the context needs beyond rotation keys (what a client uploads to a server)."""
+        n = C.c_size_t()
+        _check(_native.lib().fheon_required_key_ids(self._h, None, 0, C.byref(n)))
+        ids = np.zeros(n.value, np.uint64)
+        _check(_native.lib().fheon_required_key_ids(self._h, _u64ptr(ids), n.value, C.byref(n)))
+        return [int(i) for i in ids]
+
+    def key_uploads(self) -> Dict[str, int]:
+        c, b = C.c_uint64(), C.c_uint64()
+        _check(_native.lib().fheon_key_uploads(self._h, C.byref(c), C.byref(b)))
+        return {"uploads": c.value, "bytes": b.value}
+
     def stream(self) -> int:
         return int(_native.lib().fheon_ctx_stream(self._h) or 0)
 

@@ -262,17 +262,19 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
     stc_limbs_ = stc_limbs;
     stc_ = plan(groups, stc_limbs, h.T[stc_limbs - 1]);
   }
-  for (long s : rotation_steps()) {
-    ctx.gen_key(ctx.galois(s));
+  for (long s : rotation_steps()) {  // a server context (no secret) receives them by upload
+    if (ctx.has_secret()) ctx.gen_key(ctx.galois(s));
     ctx.pin_key(ctx.galois(s));
   }
-  ctx.gen_key(2 * (u64)h.N - 1);  // conjugation
-  ctx.gen_key(0);                 // relinearisation
+  if (ctx.has_secret()) {
+    ctx.gen_key(2 * (u64)h.N - 1);  // conjugation
+    ctx.gen_key(0);                 // relinearisation
+  }
   ctx.pin_key(2 * (u64)h.N - 1);
   ctx.pin_key(0);
   if (ctx.sse()) {  // sparse-secret encapsulation keys
     for (u64 id : {kKeyToSparse, kKeyFromSparse}) {
-      ctx.gen_key(id);
+      if (ctx.has_secret()) ctx.gen_key(id);
       ctx.pin_key(id);
     }
   }

@@ -70,6 +70,7 @@ static fheon::Params to_params(const fheon_params* p) {
   if (p->boot_hamming_weight > 0) prm.boot_hamming_weight = p->boot_hamming_weight;
   if (p->min_security > 0) prm.min_security = p->min_security;
   prm.allow_insecure = p->allow_insecure;
+  prm.no_secret = p->no_secret;
   return prm;
 }
 
@@ -271,6 +272,56 @@ int fheon_drop_rotation_keys(fheon_ctx* ctx, const long* steps, size_t n) {
       const fheon::u64 g = ctx->impl->galois(steps[i]);
       if (g != 1) ctx->impl->drop_key(g);  // freed in stream order after its last use
     }
+  });
+}
+
+size_t fheon_key_packed_words(const fheon_ctx* ctx) {
+  try {
+    return fheon::key_packed_words(*ctx->impl);
+  } catch (...) {
+    return 0;
+  }
+}
+int fheon_key_download_packed(fheon_ctx* ctx, uint64_t key_id, uint64_t* packed) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(packed, "packed");
+    fheon::download_key_packed(*ctx->impl, key_id, packed);
+  });
+}
+int fheon_key_upload(fheon_ctx* ctx, uint64_t key_id, const uint64_t* words) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(words, "words");
+    fheon::upload_key_async(*ctx->impl, key_id, words, false);
+    fheon::wait_transfers(*ctx->impl);
+  });
+}
+int fheon_key_upload_packed_async(fheon_ctx* ctx, uint64_t key_id, const uint64_t* packed) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(packed, "packed");
+    fheon::upload_key_async(*ctx->impl, key_id, packed, true);
+  });
+}
+int fheon_key_upload_packed(fheon_ctx* ctx, uint64_t key_id, const uint64_t* packed) {
+  const int rc = fheon_key_upload_packed_async(ctx, key_id, packed);
+  if (rc) return rc;
+  return guard([&] { fheon::wait_transfers(*ctx->impl); });
+}
+int fheon_required_key_ids(const fheon_ctx* ctx, uint64_t* ids, size_t cap, size_t* n) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const std::vector<fheon::u64> v = ctx->impl->pinned_keys();
+    if (n) *n = v.size();
+    for (size_t i = 0; i < v.size() && i < cap && ids; ++i) ids[i] = v[i];
+  });
+}
+int fheon_key_uploads(const fheon_ctx* ctx, uint64_t* count, uint64_t* bytes) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (count) *count = ctx->impl->stats.key_uploads;
+    if (bytes) *bytes = ctx->impl->stats.key_upload_bytes;
   });
 }
 

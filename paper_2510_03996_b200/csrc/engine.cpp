@@ -458,7 +458,7 @@ void Context::build_device_tables() {
   t.rs = upload(dev_allocs_, rs, stream_);
 
   // secret key: ternary from the counter PRNG, NTT domain over all L+K primes
-  {
+  if (!p.no_secret) {
     std::vector<long long> s(N, 0);
     auto prng_h = [&](u64 stream, u64 idx) {
       return mix64(prng_stream_key(p.seed, stream) ^ (idx * 0xD1B54A32D192ED03ULL + 0x8CB92BA72F3D8DD7ULL));
@@ -526,8 +526,19 @@ const u64* Context::key(u64 key_id) {
   return keys_.at(key_id)->ptr;
 }
 
+void Context::require_secret(const char* what) const {
+  if (!has_secret())
+    throw Error(ErrKind::internal, std::string(what) + ": this context holds no secret key (no_secret); upload "
+                                                      "the evaluation keys (fheon_key_upload*) and encrypt / "
+                                                      "decrypt on the client");
+}
+
 void Context::gen_key(u64 key_id) {
   if (keys_.count(key_id)) return;
+  if (!has_secret())
+    throw Error(ErrKind::internal, "evaluation key " + std::to_string(key_id) +
+                                       " is not resident and this context holds no secret to generate it: upload "
+                                       "it (fheon_key_upload*)");
   ++stats.key_gens;
   const Params& p = ht_.p;
   const int L = p.L, K = p.K, NP = L + K;

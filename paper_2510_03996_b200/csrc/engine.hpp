@@ -100,6 +100,7 @@ struct OpStats {
   std::uint64_t rotations = 0, keyswitches = 0, mult_plain = 0, mult_cipher = 0, rescales = 0, ntt_limbs = 0,
                 encodes = 0, adds = 0, launches = 0, bootstraps = 0;
   std::uint64_t key_gens = 0, key_drops = 0;  // key residency (keyplan block mode)
+  std::uint64_t key_uploads = 0, key_upload_bytes = 0;  // keys received over PCIe (fheon_key_upload*)
 };
 
 struct KernelTimer {
@@ -149,11 +150,18 @@ class Context {
   void drop_keys() { keys_.clear(); }
   // pinned keys (relinearisation, conjugation, bootstrapping rotations) are never dropped
   void pin_key(u64 key_id) { pinned_keys_.insert(key_id); }
+  // the pinned set: relinearisation, conjugation, bootstrapping rotations, encapsulation keys
+  std::vector<u64> pinned_keys() const { return {pinned_keys_.begin(), pinned_keys_.end()}; }
   void drop_key(u64 key_id) {
     if (!pinned_keys_.count(key_id) && keys_.erase(key_id)) ++stats.key_drops;
   }
   std::size_t key_words() const;
   std::size_t num_keys() const { return keys_.size(); }
+  // make an uploaded key (Montgomery form, [dnum][2][L+K][N]) resident under key_id
+  void put_key(u64 key_id, BufPtr kb) { keys_[key_id] = std::move(kb); }
+  // a server context (Params::no_secret) cannot generate keys, encrypt or decrypt
+  bool has_secret() const { return dt_.s_ntt != nullptr; }
+  void require_secret(const char* what) const;
   bool strict_keys = false;
 
   // ---- encoder (host special FFT)
@@ -345,6 +353,15 @@ void wait_transfers(Context& ctx);
 PackLayout pack_layout(const Context& ctx, int limbs);
 std::size_t packed_words(const Context& ctx, int limbs);
 Ciphertext upload_ct_packed_async(Context& ctx, const u64* host, int limbs, double scale);
+// evaluation-key transfer (client -> server, keyplan streaming): standard-form words
+// [dnum][2][L+K][N], raw or in the packed wire format (every limb b_i = bit_length of
+// its prime, the ciphertext layout applied to the 2 dnum polys of L+K limbs)
+std::size_t key_packed_words(const Context& ctx);
+void download_key_packed(Context& ctx, u64 key_id, u64* host);
+// upload on the context's upload stream; the compute stream waits for it, the host
+// buffer must stay valid (and should be pinned) until the copy completes
+// (fheon_ctx_wait_transfers); replaces a resident key of the same id
+void upload_key_async(Context& ctx, u64 key_id, const u64* host, bool packed);
 void download_ct_packed_async(Context& ctx, const Ciphertext& ct, u64* host);
 
 }  // namespace fheon

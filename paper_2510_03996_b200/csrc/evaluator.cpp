@@ -640,6 +640,7 @@ void align(Context& ctx, Ciphertext& a, Ciphertext& b) {
 
 // --------------------------------------------------------------- encrypt
 Ciphertext encrypt_top(Context& ctx, const double* vals, std::size_t n) {
+  ctx.require_secret("encrypt");
   const int L = ctx.L();
   const std::size_t N = ctx.N();
   const DevTables& t = ctx.dev();
@@ -666,6 +667,7 @@ Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n) {
 
 void decrypt(Context& ctx, const Ciphertext& ct, double* out, double* out_im) {
   require_valid(ct, "decrypt");
+  ctx.require_secret("decrypt");
   const std::size_t N = ctx.N();
   const int use = ct.limbs >= 2 ? 2 : 1;
   const DevTables& t = ctx.dev();
@@ -1408,6 +1410,67 @@ Ciphertext upload_ct_packed_async(Context& ctx, const u64* host, int limbs, doub
   FHEON_CUDA(cudaStreamWaitEvent(ctx.stream(), up, 0));  // the staging buffer is freed after this point
   ctx.give_event(up);
   return ct;
+}
+
+std::size_t key_packed_words(const Context& ctx) {
+  const int NP = ctx.L() + ctx.K();
+  return (std::size_t)ctx.host().p.dnum * 2 * (std::size_t)pack_layout(ctx, NP).off[NP];
+}
+
+void download_key_packed(Context& ctx, u64 key_id, u64* host) {
+  const int NP = ctx.L() + ctx.K();
+  const std::size_t LN = (std::size_t)NP * ctx.N();
+  const std::size_t nblk = (std::size_t)ctx.host().p.dnum * 2;
+  const u64* k = ctx.key(key_id);
+  BufPtr std_form = ctx.alloc(nblk * LN);
+  for (std::size_t b = 0; b < nblk; ++b)
+    convert_mont(ctx.dev(), std_form->ptr + b * LN, k + b * LN, NP, NP, false, ctx.stream());
+  const PackLayout lay = pack_layout(ctx, NP);
+  BufPtr stage = ctx.alloc(key_packed_words(ctx));
+  PolyList src{};
+  for (std::size_t b0 = 0; b0 < nblk; b0 += kMaxPolys) {
+    src.n = (int)std::min<std::size_t>(kMaxPolys, nblk - b0);
+    for (int i = 0; i < src.n; ++i) src.p[i] = std_form->ptr + (b0 + i) * LN;
+    pack_limbs(ctx.dev(), stage->ptr + b0 * lay.off[NP], src, lay, ctx.stream());
+  }
+  FHEON_CUDA(cudaMemcpyAsync(host, stage->ptr, key_packed_words(ctx) * sizeof(u64), cudaMemcpyDeviceToHost,
+                             ctx.stream()));
+  FHEON_CUDA(cudaStreamSynchronize(ctx.stream()));
+}
+
+void upload_key_async(Context& ctx, u64 key_id, const u64* host, bool packed) {
+  if (key_id != 0 && (key_id & 1) == 0 && key_id != kKeyToSparse && key_id != kKeyFromSparse)
+    throw Error(ErrKind::internal, "key upload: key id " + std::to_string(key_id) +
+                                       " is neither 0 (relinearisation), a Galois element nor an encapsulation key");
+  const int NP = ctx.L() + ctx.K();
+  const std::size_t LN = (std::size_t)NP * ctx.N();
+  const std::size_t nblk = (std::size_t)ctx.host().p.dnum * 2;
+  const std::size_t words = packed ? key_packed_words(ctx) : nblk * LN;
+  BufPtr kb = std::make_shared<DevBuffer>(&ctx, nblk * LN, ctx.h2d_stream());
+  BufPtr stage = packed ? std::make_shared<DevBuffer>(&ctx, words, ctx.h2d_stream()) : kb;
+  FHEON_CUDA(cudaMemcpyAsync(stage->ptr, host, words * sizeof(u64), cudaMemcpyHostToDevice, ctx.h2d_stream()));
+  cudaEvent_t landed = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(landed, ctx.h2d_stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.unpack_stream(), landed, 0));
+  ctx.give_event(landed);
+  if (packed) {
+    const PackLayout lay = pack_layout(ctx, NP);
+    PolyList dst{};
+    for (std::size_t b0 = 0; b0 < nblk; b0 += kMaxPolys) {
+      dst.n = (int)std::min<std::size_t>(kMaxPolys, nblk - b0);
+      for (int i = 0; i < dst.n; ++i) dst.p[i] = kb->ptr + (b0 + i) * LN;
+      unpack_limbs(ctx.dev(), dst, stage->ptr + b0 * lay.off[NP], lay, ctx.unpack_stream());
+    }
+  }
+  for (std::size_t b = 0; b < nblk; ++b)  // standard -> Montgomery form, in place
+    convert_mont(ctx.dev(), kb->ptr + b * LN, kb->ptr + b * LN, NP, NP, true, ctx.unpack_stream());
+  cudaEvent_t ready = ctx.take_event();
+  FHEON_CUDA(cudaEventRecord(ready, ctx.unpack_stream()));
+  FHEON_CUDA(cudaStreamWaitEvent(ctx.stream(), ready, 0));  // later uses (and the frees) follow on the compute stream
+  ctx.give_event(ready);
+  ctx.put_key(key_id, kb);
+  ctx.stats.key_uploads++;
+  ctx.stats.key_upload_bytes += words * sizeof(u64);
 }
 
 void download_ct_packed_async(Context& ctx, const Ciphertext& ct, u64* host) {

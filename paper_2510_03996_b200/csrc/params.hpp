@@ -51,6 +51,9 @@ struct Params {
   // log2(QP) exceeds the bound for N at min_security bits unless allow_insecure is set
   int min_security = 128;
   int allow_insecure = 0;
+  // 1: a server context holding NO secret key -- evaluation keys must be uploaded
+  // (fheon_key_upload*), encrypt / decrypt / key generation are refused
+  int no_secret = 0;
 };
 
 // HE-standard (homomorphicencryption.org, 2018) maximum log2(QP) for a uniform

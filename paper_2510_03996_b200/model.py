@@ -870,6 +870,27 @@ class EncryptedModel:
         c = self.ctx
         return keyplan.MemoryModel.for_engine(c.N, c.L, c.K, c.dnum, self._pinned_keys)
 
+    def enable_key_streaming(self):
+        """Keyplan block mode WITHOUT regenerating keys on the device: every rotation
+        key of the plan is serialized once (packed wire format) into pinned host
+        memory, and infer(key_mode="block") then uploads each block's missing keys
+        from there on the upload stream (fheon_key_upload_packed_async) -- the
+        deployment shape where the server does not hold the secret.  Keys are
+        strict while streaming: a key outside the plan is an error, not a silent
+        regeneration."""
+        import torch
+        plan = keyplan.plan_blocks(self.layer_keys())
+        store = {}
+        for t in plan.union_keys.indices():
+            g = self.ctx.galois_element(t)
+            if g == 1:
+                continue
+            self.ctx.prefetch_rotation_keys([t])
+            buf = torch.empty(self.ctx.key_packed_words(), dtype=torch.uint64, pin_memory=True)
+            store[t] = self.ctx.key_download_packed(g, out=buf.numpy())
+        self._key_store = store
+        self._streamed = set(store)  # resident right now
+
     def output_count(self) -> int:
         packed, C, W, n = self.layers[-1].out_shape
         return C * W * W if packed else n
@@ -913,7 +934,10 @@ class EncryptedModel:
             plan = keyplan.plan_blocks(lk) if key_mode == "block" else keyplan.plan_single_block(lk)
         rec = self.ctx.attach_recorder() if verify_keys else None
         events: List[keyplan.TraceEvent] = []
+        store = getattr(self, "_key_store", None) if key_mode == "block" else None
         self.ctx.reset_stats()
+        if store is not None:
+            self.ctx.set_strict_keys(True)
         peak_key_bytes = 0
         t0 = time.perf_counter()
         v = fh.SlotVector.encode(self.ctx, x.reshape(-1))
@@ -924,8 +948,17 @@ class EncryptedModel:
                 blk = plan.blocks[plan.block_of_layer(i)]
                 if blk.first_layer == i:
                     if i == 0:  # "load block 0": nothing else of the plan stays resident
-                        self.ctx.drop_rotation_keys([t for t in plan.union_keys.indices() if not blk.keys.contains(t)])
-                    self.ctx.prefetch_rotation_keys(blk.keys.indices())
+                        drop = [t for t in plan.union_keys.indices() if not blk.keys.contains(t)]
+                        self.ctx.drop_rotation_keys(drop)
+                        if store is not None:
+                            self._streamed -= set(drop)
+                    if store is not None:  # stream the block's missing keys from pinned host memory
+                        for t in blk.keys.indices():
+                            if t in store and t not in self._streamed:
+                                self.ctx.key_upload(self.ctx.galois_element(t), store[t], async_copy=True)
+                                self._streamed.add(t)
+                    else:
+                        self.ctx.prefetch_rotation_keys(blk.keys.indices())
                     peak_key_bytes = max(peak_key_bytes, self.ctx.key_bytes())
             if rec is not None:
                 rec.clear()
@@ -939,7 +972,10 @@ class EncryptedModel:
                 bi = plan.block_of_layer(i)
                 if plan.blocks[bi].last_layer == i and bi + 1 < len(plan.blocks):
                     nxt = plan.blocks[bi + 1].keys
-                    self.ctx.drop_rotation_keys([t for t in plan.blocks[bi].keys.indices() if not nxt.contains(t)])
+                    drop = [t for t in plan.blocks[bi].keys.indices() if not nxt.contains(t)]
+                    self.ctx.drop_rotation_keys(drop)
+                    if store is not None:
+                        self._streamed -= set(drop)
             ledger.append((b.name, b.cost, lin, lout, b.type == "bootstrap"))
             if b.type == "bootstrap":
                 if lout != self.spec.depth_budget:
@@ -952,8 +988,12 @@ class EncryptedModel:
         wall = (time.perf_counter() - t0) * 1e3
         if rec is not None:
             self.ctx.detach_recorder()
+        if store is not None:
+            self.ctx.wait_transfers()
+            self.ctx.set_strict_keys(False)
+        up = self.ctx.key_uploads()
         residency = dict(self.ctx.key_events(), peak_key_bytes=max(peak_key_bytes, self.ctx.key_bytes()),
-                         resident_key_bytes=self.ctx.key_bytes())
+                         resident_key_bytes=self.ctx.key_bytes(), uploaded=up["uploads"], uploaded_bytes=up["bytes"])
         check = keyplan.verify_trace(plan, events) if verify_keys else None
         return InferResult(logits, ledger, wall, timings or {}, self.ctx.stats(), plan, check, residency)
 

@@ -216,3 +216,25 @@ def test_security_disclosure_and_secure_chains():
     ins = M.ckks_config(M.resnet20(ring=65536, depth_budget=25), True, security=0)
     si = fh.host_security(ins)
     assert si["security_bits"] is None and not si["meets_128"] and si["log2_qp"] > 2600  # sparse h=64 main secret
+
+
+def test_integration_seam_links_the_engine_not_the_simulator():
+    """integration/_build/libslotcnn_b200.so: the reference core compiled against
+    integration/include/slotcnn/backend.hpp -- its backend entry points are
+    defined by backend_b200.cpp and call the C ABI (fheon_*), and the reference
+    simulator's backend.cpp is not in it."""
+    import subprocess
+    lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration", "_build",
+                       "libslotcnn_b200.so")
+    if not os.path.exists(lib):
+        pytest.skip("integration not built (needs /root/reference: make -C integration)")
+    syms = subprocess.run(["nm", "-DC", lib], capture_output=True, text=True).stdout
+    defined = {ln.split(" ", 2)[-1] for ln in syms.splitlines() if " T " in ln}
+    undefined = {ln.split()[-1] for ln in syms.splitlines() if " U " in ln}
+    for fn in ("slotcnn::rotate(slotcnn::SlotVector const&, long)", "slotcnn::bootstrap(slotcnn::SlotVector const&)",
+               "slotcnn::convolution(slotcnn::PackedTensor const&, slotcnn::ConvConfig const&, "
+               "slotcnn::KernelTensor const&)"):
+        assert fn in defined, fn
+    for fn in ("fheon_rotate", "fheon_mult_cipher", "fheon_bootstrap", "fheon_ctx_create"):
+        assert fn in undefined, fn
+    assert "slotcnn::SlotVector::slots() const" in defined  # decrypt-on-read (backend_b200.cpp)

@@ -185,3 +185,25 @@ def test_block_key_mode_residency(name):
     assert blk.key_residency["peak_key_bytes"] < preload_bytes
     est = M.keyplan.estimate_memory(blk.plan, em.memory_model())
     assert est.peak_bytes < est.preload_bytes
+
+
+def test_block_key_mode_streamed_from_host():
+    """key_mode "block" with the keys streamed from pinned host memory (packed
+    wire format, upload stream) instead of regenerated on the device: no key is
+    generated during the inference, every block's missing keys are uploaded, the
+    trace replays cleanly against the plan, and the logits match the reference."""
+    from model_files import materialize
+    path = materialize("lenet5", tempfile.mkdtemp(), seed=5)
+    spec = M.load_spec(path)
+    spec = M.calibrate_relu_scales(spec, [np.random.default_rng(600 + i).uniform(0, 1, (1, 28, 28))
+                                          for i in range(3)])
+    x = np.random.default_rng(6).uniform(0, 1, (1, 28, 28))
+    em = M.EncryptedModel(spec, security=0)
+    em.enable_key_streaming()
+    for _ in range(2):
+        r = em.infer(x, key_mode="block", verify_keys=True)
+        assert r.trace_check.ok() and r.key_residency["generated"] == 0
+        assert r.key_residency["uploaded"] > 0
+        assert r.key_residency["uploaded_bytes"] == r.key_residency["uploaded"] * em.ctx.key_packed_words() * 8
+    ref_logits, _, _, _ = sref.infer(spec.write(tempfile.mkdtemp()), x)
+    assert float(np.abs(r.logits - ref_logits).max()) < 1e-3
