@@ -81,9 +81,44 @@ TimedScope::~TimedScope() {
 }
 
 // ------------------------------------------------------------- buffers
+namespace {
+// stream-ordered allocation; on out-of-memory the context's plaintext caches are
+// released (their buffers return to the pool once the compute stream passes their
+// last use) and the allocation is retried once
+u64* device_alloc(Context* c, std::size_t words, cudaStream_t st) {
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), st);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    if (c->release_caches() > 0) {
+      FHEON_CUDA(cudaStreamSynchronize(c->stream()));
+      e = cudaMallocAsync(&p, words * sizeof(u64), st);
+    }
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(ErrKind::cuda, std::string("CUDA error: ") + cudaGetErrorString(e) + " allocating " +
+                                   std::to_string(words * sizeof(u64)) + " bytes (resident keys and caches exceed HBM)");
+  }
+  return static_cast<u64*>(p);
+}
+}  // namespace
+
+std::size_t Context::release_caches() {
+  std::size_t bytes = weightcache_bytes_ + ptcache_words_ * sizeof(u64);
+  // the resident set did not fit beside the keys: keep at most half of it from now on
+  if (weightcache_bytes_ > 0) weight_cache_budget = std::min(weight_cache_budget, weightcache_bytes_ / 2);
+  weightcache_.clear();
+  weightcache_bytes_ = 0;
+  ptcache_.clear();
+  namedcache_.clear();
+  ptcache_words_ = 0;
+  return bytes;
+}
+
 DevBuffer::DevBuffer(Context* c, std::size_t w) : alive(c->alive), stream(c->stream()), words(w) {
   if (w == 0) return;
-  FHEON_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), stream));
+  ptr = device_alloc(c, w, stream);
 }
 DevBuffer::~DevBuffer() {
   if (!ptr) return;
@@ -94,7 +129,7 @@ DevBuffer::~DevBuffer() {
 DevBuffer::DevBuffer(Context* c, std::size_t w, cudaStream_t alloc_stream)
     : alive(c->alive), stream(c->stream()), words(w) {
   if (w == 0) return;
-  FHEON_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), w * sizeof(u64), alloc_stream));
+  ptr = device_alloc(c, w, alloc_stream);
 }
 
 BufPtr Context::alloc(std::size_t words) { return std::make_shared<DevBuffer>(this, words); }

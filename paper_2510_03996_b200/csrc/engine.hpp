@@ -182,6 +182,10 @@ class Context {
   // under `key`, then reused; past the budget new entries are built but not kept
   BufPtr weight_pt(const std::string& key, int limbs, double scale, const std::function<BufPtr()>& make);
   std::size_t weight_cache_budget = (std::size_t)96 << 30;  // bytes (<= free HBM / 2 at creation); 0 disables
+  // drop the resident plaintext caches (weights, masks, diagonals); buffers still in
+  // use stay alive through their handles.  Called when a device allocation fails
+  // (HBM shared with the lazily generated keys), before the allocation is retried.
+  std::size_t release_caches();
   // device real-coefficient (unscaled, unrounded) encoding of a slot vector,
   // cached under `key` (block indicators of a layer geometry)
   const double* basis(const std::string& key, const std::vector<double>& slot_values);

@@ -214,7 +214,7 @@ void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st,
 // Plaintext as a linear combination of cached real-coefficient basis vectors
 // (block-indicator encodings): coeff[k] = rint(scale * sum_b w_b basis_b[k]),
 // written as RNS limbs (coefficient domain, then forward NTT by the caller).
-constexpr int kMaxBasis = 64;
+constexpr int kMaxBasis = 128;  // LinComb is a kernel parameter: 128 x 16 B + count (< 4 KiB)
 struct LinComb {
   const double* basis[kMaxBasis];
   double w[kMaxBasis];

@@ -71,15 +71,18 @@ BufPtr pt_of(Context& ctx, const Ciphertext& like, const std::vector<double>& fu
   return ctx.encode_cached(full, like.limbs, pt_scale_for(ctx, like));
 }
 
-// FNV-1a over a weight tensor's bit patterns (keys the resident weight plaintexts)
+// 128-bit content key of a weight tensor (keys the resident weight plaintexts): FNV-1a
+// and an independent multiply-xorshift chain over the bit patterns, plus the shape --
+// a hit on another layer's plaintexts would need both 64-bit hashes to collide
 std::string weight_key(const char* tag, const KernelTensor& w, std::size_t W) {
-  u64 h = 1469598103934665603ULL;
+  u64 h = 1469598103934665603ULL, g = 0x9E3779B97F4A7C15ULL;
   for (double v : w.weights) {
     u64 b;
     std::memcpy(&b, &v, 8);
     h = (h ^ b) * 1099511628211ULL;
+    g = mix64(g ^ (b + 0x632BE59BD9B4E019ULL));
   }
-  return std::string(tag) + ":" + std::to_string(h) + ":" + std::to_string(w.out_channels) + "x" +
+  return std::string(tag) + ":" + std::to_string(h) + ":" + std::to_string(g) + ":" + std::to_string(w.out_channels) + "x" +
          std::to_string(w.in_channels) + "x" + std::to_string(w.kernel) + ":" + std::to_string(W);
 }
 
@@ -214,9 +217,26 @@ std::vector<Ciphertext> sum_rotations(Context& ctx, const std::vector<RotTerms>&
 
 // out = sum_f rot(r_f, -f * block): placement rotations share one ModDown
 Ciphertext place_and_sum(Context& ctx, const std::vector<Ciphertext>& r, std::size_t block) {
-  RotTerms g;
-  for (std::size_t f = 0; f < r.size(); ++f) g.push_back({r[f], -(long)(f * block)});
-  return sum_rotations(ctx, {g})[0];
+  // Up to 64 placements: one rotate-and-sum with one key per placement (the
+  // reference's multiset).  More (FC layers of 1024 outputs) under the fast
+  // schedule: baby-step giant-step, sum_G rot(sum_b rot(r_{G nb + b}, -b block),
+  // -G nb block) -- about 2 sqrt(n) keys instead of n (each key is 100-200 MB at
+  // N = 2^16), the same terms, one more ModDown per giant.
+  constexpr std::size_t kMaxPlacementKeys = 64;
+  const std::size_t n = r.size();
+  if (n <= kMaxPlacementKeys || !ctx.fast_schedule()) {
+    RotTerms g;
+    for (std::size_t f = 0; f < n; ++f) g.push_back({r[f], -(long)(f * block)});
+    return sum_rotations(ctx, {g})[0];
+  }
+  std::size_t nb = 1;
+  while (nb * nb < n) nb <<= 1;
+  std::vector<RotTerms> babies((n + nb - 1) / nb);
+  for (std::size_t f = 0; f < n; ++f) babies[f / nb].push_back({r[f], -(long)((f % nb) * block)});
+  const std::vector<Ciphertext> inner = sum_rotations(ctx, babies);
+  RotTerms giants;
+  for (std::size_t G = 0; G < inner.size(); ++G) giants.push_back({inner[G], -(long)(G * nb * block)});
+  return sum_rotations(ctx, {giants})[0];
 }
 
 // sum_{i < span} rot(x, i * stride) for every x (fast schedule): a doubling

@@ -405,6 +405,32 @@ def vgg16(seed: int = 5001, ring: int = 65536, depth_budget: int = 25) -> ModelS
     return ModelSpec("vgg16", ring, ring // 2, depth_budget, 3, 32, layers)
 
 
+def vgg16_paper(seed: int = 5001, ring: int = 65536, depth_budget: int = 11) -> ModelSpec:
+    """VGG-16 at the FHEON paper's own widths (the network behind
+    its 42.3 GB / 2232 s figure): 3x32x32 input; 3x3 / pad-1 convs 16-16 | 32-32 |
+    64-64-64 | 128-128-128 | 128-128-128, 2x2 average pooling after each block,
+    then three FC layers.  The table gives FC 1024->1024->1024->10, but after five
+    poolings the tensor is 128x1x1, so the first FC takes the 128 flattened
+    values: FC 128->1024, 1024->1024, 1024->10.  The first block's 16x32x32 output
+    fits one 32768-slot ciphertext.  He-normal weights, bias 0; degree-59
+    Chebyshev ReLU after every conv and the two hidden FC layers."""
+    rng = np.random.default_rng(seed)
+    layers, C = [], 3
+    for block, (F, n) in enumerate(((16, 2), (32, 2), (64, 3), (128, 3), (128, 3)), start=1):
+        for u in range(n):
+            layers.append(_conv(f"conv{block}_{u + 1}", F, C, 3, rng, math.sqrt(2.0 / (C * 9)), padding=1,
+                                mode="special3x3", bias=False))
+            layers.append(Layer("relu", f"relu{block}_{u + 1}", {"degree": 59, "scale": 8.0}))
+            C = F
+        layers.append(Layer("avg_pool", f"pool{block}", {"kernel": 2, "stride": 2}))
+    n_in = C
+    for i, (m, n) in enumerate(((1024, n_in), (1024, 1024), (10, 1024)), start=1):
+        layers.append(Layer("fc", f"fc{i}", {"outputs": m}, rng.normal(0, math.sqrt(2.0 / n), (m, n)), np.zeros(m)))
+        if i < 3:
+            layers.append(Layer("relu", f"relu_fc{i}", {"degree": 59, "scale": 8.0}))
+    return ModelSpec("vgg16_paper", ring, ring // 2, depth_budget, 3, 32, layers)
+
+
 # ----------------------------------------------------------------- build
 @dataclass
 class Built:
@@ -1067,3 +1093,76 @@ def calibrate_relu_scales(spec: ModelSpec, batch: List[np.ndarray], safety: floa
 
     assign(spec.layers)
     return spec
+
+
+# ----------------------------------------------------------------- run report
+@dataclass
+class RunReport:
+    """RunReport (model.hpp:211-231): one encrypted inference with its float
+    (true-ReLU) reference, per-logit deltas, argmax agreement, ledger, key plan,
+    trace check and memory estimate -- plus what the engine adds: the chain's
+    security disclosure and its op / launch counters."""
+    model_name: str
+    kernels: str
+    logits: List[float]
+    reference_logits: List[float]
+    deltas: List[float]
+    max_abs_delta: float
+    argmax: int
+    reference_argmax: int
+    argmax_match: bool
+    ledger: List[Tuple[str, int, int, int, bool]]
+    plan: keyplan.BlockPlan
+    trace_check: keyplan.TraceCheck
+    memory: keyplan.MemoryEstimate
+    rotation_count: int
+    wall_ms: float
+    notes: List[str]
+    security: Dict[str, object]
+    engine: Dict[str, object]
+
+    def to_json(self) -> str:
+        """The reference's RunReport::to_json layout (model_run.cpp:440-492), same keys
+        and nesting, plus "security" and "engine"."""
+        j = {"model": self.model_name, "kernels": self.kernels, "logits": list(map(float, self.logits)),
+             "reference_logits": list(map(float, self.reference_logits)), "deltas": list(map(float, self.deltas)),
+             "max_abs_delta": float(self.max_abs_delta), "argmax": int(self.argmax),
+             "reference_argmax": int(self.reference_argmax), "argmax_match": bool(self.argmax_match),
+             "rotations": int(self.rotation_count), "wall_ms": float(self.wall_ms),
+             "ledger": [{"layer": n, "declared_levels": d, "level_in": li, "level_out": lo, "bootstrap": b}
+                        for n, d, li, lo, b in self.ledger],
+             "plan": {"blocks": [{"first_layer": b.first_layer, "last_layer": b.last_layer, "keys": b.keys.size()}
+                                 for b in self.plan.blocks],
+                      "total_keys": self.plan.union_keys.size(), "peak_resident_keys": self.plan.peak_resident_keys,
+                      "residency": list(self.plan.residency_events)},
+             "trace_check": {"ok": self.trace_check.ok(),
+                             "violations": [{"event": v.event_index, "rotation_index": v.rotation_index,
+                                             "reason": v.reason} for v in self.trace_check.violations],
+                             "unused_keys": list(self.trace_check.unused_keys)},
+             "memory": {"total_keys": self.memory.total_keys, "resident_keys": self.memory.resident_keys,
+                        "preload_bytes": self.memory.preload_bytes, "peak_bytes": self.memory.peak_bytes,
+                        "assumptions": self.memory.assumptions},
+             "notes": list(self.notes), "security": self.security, "engine": self.engine}
+        return json.dumps(j, indent=2)
+
+
+def run_with_report(em: EncryptedModel, x: np.ndarray, key_mode: str = "preload") -> RunReport:
+    """run_with_report (model_run.cpp:407-437): infer with the trace verified against
+    the key plan, the float true-ReLU reference on the same input, and the
+    memory estimate under the engine's true key size."""
+    r = em.infer(x, key_mode=key_mode, verify_keys=True)
+    ref = _forward_float(em.spec, np.asarray(x, np.float64), [])
+    n = min(len(r.logits), len(ref))
+    deltas = np.abs(np.asarray(r.logits[:n]) - np.asarray(ref[:n]))
+    am = int(np.argmax(r.logits)) if len(r.logits) else 0
+    ram = int(np.argmax(ref)) if len(ref) else 0
+    mem = keyplan.estimate_memory(r.plan, em.memory_model())
+    notes = [f"{em.n_boot} bootstraps placed ({em.spec.bootstrap_policy} policy)",
+             f"rotation schedule: {em.ctx.schedule()}"]
+    engine = {"ring_dimension": em.spec.ring_dimension, "limbs": em.ctx.L, "special_limbs": em.ctx.K,
+              "dnum": em.ctx.dnum, "key_mode": key_mode, "key_residency": r.key_residency,
+              "ops": {k: int(v) for k, v in r.stats.items()}}
+    return RunReport(em.spec.name, "b200 rns-ckks (sm_100a kernels, libfheon_b200.so)", list(r.logits), list(ref),
+                     deltas.tolist(), float(deltas.max()) if n else 0.0, am, ram, am == ram,
+                     [(a, b, c, d, e) for a, b, c, d, e in r.ledger], r.plan, r.trace_check, mem,
+                     r.trace_check.rotations_checked, r.wall_ms, notes, em.security, engine)

@@ -22,6 +22,10 @@ if which == "resnet20":
     spec = M.calibrate_relu_scales(spec, [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32)))
                                           for i in range(6)])
     x = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
+elif which == "vgg16":
+    spec = M.calibrate_relu_scales(M.vgg16_paper(ring=65536, depth_budget=depth),
+                                   [norm(np.random.default_rng(5002 + i).uniform(0, 1, (3, 32, 32))) for i in range(4)])
+    x = norm(np.random.default_rng(5001).uniform(0, 1, (3, 32, 32)))
 else:
     ring = int(sys.argv[5]) if len(sys.argv) > 5 else 32768
     spec = M.lenet5(ring=ring, depth_budget=depth)

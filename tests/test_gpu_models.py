@@ -207,3 +207,40 @@ def test_block_key_mode_streamed_from_host():
         assert r.key_residency["uploaded_bytes"] == r.key_residency["uploaded"] * em.ctx.key_packed_words() * 8
     ref_logits, _, _, _ = sref.infer(spec.write(tempfile.mkdtemp()), x)
     assert float(np.abs(r.logits - ref_logits).max()) < 1e-3
+
+
+def test_run_report_json_matches_reference_layout():
+    """RunReport / to_json (model_run.cpp:407-492): same top-level keys and nested
+    layout as the reference's report, the logits equal to infer()'s within noise,
+    deltas against the float true-ReLU reference, clean trace check."""
+    import json
+    spec = M.lenet5(ring=8192, depth_budget=12)
+    x = np.random.default_rng(3002).uniform(0, 1, (1, 28, 28))
+    em = M.EncryptedModel(spec, security=0)
+    rep = M.run_with_report(em, x, key_mode="block")
+    j = json.loads(rep.to_json())
+    ref_keys = {"model", "kernels", "logits", "reference_logits", "deltas", "max_abs_delta", "argmax",
+                "reference_argmax", "argmax_match", "rotations", "wall_ms", "ledger", "plan", "trace_check",
+                "memory", "notes"}
+    assert ref_keys <= set(j) and {"security", "engine"} <= set(j)
+    assert set(j["ledger"][0]) == {"layer", "declared_levels", "level_in", "level_out", "bootstrap"}
+    assert set(j["plan"]) == {"blocks", "total_keys", "peak_resident_keys", "residency"}
+    assert set(j["trace_check"]) == {"ok", "violations", "unused_keys"} and j["trace_check"]["ok"]
+    assert set(j["memory"]) == {"total_keys", "resident_keys", "preload_bytes", "peak_bytes", "assumptions"}
+    assert len(j["deltas"]) == 10 and abs(j["max_abs_delta"] - max(j["deltas"])) < 1e-15
+    assert j["rotations"] > 0 and len(j["plan"]["blocks"]) >= 2
+    ref_logits, _, _, _ = sref.infer(spec.write(tempfile.mkdtemp()), x)
+    assert float(np.abs(np.asarray(j["logits"]) - ref_logits).max()) < 1e-3
+
+
+def test_vgg16_paper_widths_128bit():
+    """VGG-16 (BASELINE configs[4]) at the FHEON paper's widths (PAPER.md:844-865,
+    model.vgg16_paper) on the 128-bit N = 2^16 chain: thirteen 3x3 convs, five
+    poolings, three FC layers, bootstraps placed as the reference places them;
+    decrypted logits within 1e-3 of the reference's infer()."""
+    def norm(x):
+        return (x - 0.5) / 0.2887
+
+    cal = [norm(np.random.default_rng(5002 + i).uniform(0, 1, (3, 32, 32))) for i in range(4)]
+    spec = M.calibrate_relu_scales(M.vgg16_paper(ring=65536, depth_budget=11), cal)
+    _compare(spec, norm(np.random.default_rng(5001).uniform(0, 1, (3, 32, 32))), "fast", 128)
