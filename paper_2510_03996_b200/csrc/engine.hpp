@@ -297,6 +297,7 @@ std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a,
 std::vector<Ciphertext> conjugate_many(Context& ctx, const std::vector<Ciphertext>& xs);
 Ciphertext mul_by_i(Context& ctx, const Ciphertext& x);
 Ciphertext mod_raise(Context& ctx, const Ciphertext& x);
+Ciphertext encrypt_at(Context& ctx, const double* vals, std::size_t n, int limbs);
 // add an encoded plaintext (encoded at a's level and scale)
 Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt);
 std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphertext>& as,

@@ -618,6 +618,14 @@ Ciphertext level_down(Context& ctx, const Ciphertext& a, int target) {
   const int keep = target + 1;
   const HostTables& h = ctx.host();
   const double c = h.T[target - 1] * (double)h.q[target] / a.scale;
+  // the integer constant k carries the scale change; below 2^30 its rounding would move
+  // the result off T_{target-1} by more than 2^-31 relative (an unrescaled product
+  // reaching add/sub, say), above 2^62 it does not fit a signed word -- both are bugs
+  // of the caller, not something to absorb silently
+  if (!(c >= 1073741824.0) || !(c < 4.6e18))
+    throw Error(ErrKind::internal, "level_down: scale 2^" + std::to_string(std::log2(a.scale)) + " at " +
+                                       std::to_string(a.limbs) + " limbs cannot be brought to the target scale of " +
+                                       std::to_string(target) + " limbs with an integer constant (rescale first)");
   const long long k = std::llround(c);
   LimbConsts lc{};
   for (int i = 0; i < keep; ++i) {
@@ -639,9 +647,13 @@ void align(Context& ctx, Ciphertext& a, Ciphertext& b) {
 }  // namespace
 
 // --------------------------------------------------------------- encrypt
-Ciphertext encrypt_top(Context& ctx, const double* vals, std::size_t n) {
+Ciphertext encrypt_top(Context& ctx, const double* vals, std::size_t n) { return encrypt_at(ctx, vals, n, ctx.L()); }
+
+// secret-key encryption over the first L limbs at the level's scale target (the same
+// randomness streams as a top-level encryption restricted to those limbs)
+Ciphertext encrypt_at(Context& ctx, const double* vals, std::size_t n, int L) {
   ctx.require_secret("encrypt");
-  const int L = ctx.L();
+  if (L < 1 || L > ctx.L()) throw Error(ErrKind::internal, "encrypt: bad limb count");
   const std::size_t N = ctx.N();
   const DevTables& t = ctx.dev();
   cudaStream_t st = ctx.stream();
@@ -661,8 +673,10 @@ Ciphertext encrypt(Context& ctx, const double* vals, std::size_t n) {
   if (n > (std::size_t)ctx.S())
     throw Error(ErrKind::capacity, "payload of " + std::to_string(n) + " values does not fit in " +
                                        std::to_string(ctx.S()) + " slots");
-  Ciphertext ct = encrypt_top(ctx, vals, n);
-  return level_down(ctx, ct, ctx.depth_budget() + 1);
+  // directly at the depth budget: a top-level encryption brought down by level_down
+  // would carry its scale change in a small integer constant (2^22 on 60-bit
+  // bootstrapping chains) and lose precision
+  return encrypt_at(ctx, vals, n, ctx.depth_budget() + 1);
 }
 
 void decrypt(Context& ctx, const Ciphertext& ct, double* out, double* out_im) {
