@@ -560,6 +560,28 @@ def primitives(ctx, fh):
         out[f"hoisted{r}_rot_per_s"] = round(r / (ms / 1e3), 1)
     ntt_bytes = 2 * L * N * 8 * 2
     out["ntt_hbm_gbs"] = round(ntt_bytes / (out["ntt_ms_per_ct"] / 1e3) / 1e9, 1)
+    # ---- the SURVEY 8(d) C2 sweep
+    peak, _ = measured_peak_hbm()
+    alpha = (L + DNUM - 1) // DNUM
+    beta = (L + alpha - 1) // alpha
+    key_bytes = 16 * beta * (L + K) * N
+    sweep = {}
+    for B in (1, 2, 4, 8, 16, 32, 64):  # same key across B ciphertexts: one key read per launch
+        ms = ctx.microbench(8, B, L, 1, 5)
+        alg = B * 32 * L * N + key_bytes  # B 32 l N + 16 beta (l + K) N
+        sweep[str(B)] = {"rot_per_s": round(B / (ms / 1e3), 1), "ms": round(ms, 4),
+                         "hbm_frac_of_algorithmic": round(alg / (ms / 1e3) / 1e9 / peak, 4)}
+    out["same_key_batched_rotation"] = {
+        "by_batch": sweep, "hbm_roofline_rot_per_s_at_64": round(64 / ((64 * 32 * L * N + key_bytes) / (peak * 1e9)), 1),
+        "note": "rot/s of B distinct ciphertexts rotated by one step; roofline = algorithmic bytes "
+                "B 32 l N + 16 beta (l + K) N at the measured HBM peak (SURVEY 8(d))"}
+    out["mac_fused_ms"] = {str(k): round(ctx.microbench(9, 1, L, k, 10), 5) for k in (1, 9, 25)}
+    out["mac_fused_hbm_frac"] = {k: round((int(k) * 24 * L * N + 16 * L * N) / (v / 1e3) / 1e9 / peak, 4)
+                                 for k, v in out["mac_fused_ms"].items()}
+    n_auto = S - 1
+    ms_all = ctx.microbench(10, 1, L, 1, n_auto)  # every t in [1, S), one launch each
+    out["automorphism_all_steps"] = {"steps": n_auto, "mean_ms": round(ms_all, 5),
+                                     "hbm_gbs": round(2 * 2 * L * N * 8 / (ms_all / 1e3) / 1e9, 1)}
     # integer roofline of the NTT: (N/2) log2 N butterflies per limb-poly, 2L limb-polys
     bfly = (N // 2) * LOGN * 2 * L
     achieved = bfly / (out["ntt_ms_per_ct"] / 1e3)
@@ -667,6 +689,16 @@ def model_runs(args):
             est = M.keyplan.estimate_memory(rb.plan, em.memory_model())
             ref_est = M.keyplan.estimate_memory(rb.plan, M.keyplan.MemoryModel.reference_model(
                 spec.ring_dimension, spec.depth_budget, 3))
+            # the same plan with the keys streamed from pinned host memory (packed wire format,
+            # upload stream) instead of regenerated: the PCIe key traffic is inside s/image
+            em.enable_key_streaming()
+            em.infer(x, key_mode="block")
+            rs = em.infer(x, key_mode="block", verify_keys=True)
+            rec["key_mode_block_streamed"] = {
+                "s_per_image": round(rs.wall_ms / 1e3, 4), "keys_uploaded_per_image": rs.key_residency["uploaded"],
+                "key_bytes_uploaded_per_image": rs.key_residency["uploaded_bytes"],
+                "keys_generated_per_image": rs.key_residency["generated"], "trace_check_ok": rs.trace_check.ok(),
+                "pcie_gbs_implied": round(rs.key_residency["uploaded_bytes"] / (rs.wall_ms / 1e3) / 1e9, 2)}
             rec["key_mode_block"] = {
                 "s_per_image": round(rb.wall_ms / 1e3, 4), "blocks": len(rb.plan.blocks),
                 "trace_check_ok": rb.trace_check.ok(), "rotations_checked": rb.trace_check.rotations_checked,

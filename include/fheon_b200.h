@@ -230,7 +230,10 @@ int fheon_automorph_host(fheon_ctx* ctx, uint64_t* words, int npolys, int nlimbs
 /* ---- device-resident microbench (config 2): times `iters` launches of a
  * primitive with CUDA events on the context stream; returns mean ms.
  * kind: 0 NTT fwd, 1 iNTT, 2 automorphism, 3 rotation (single key switch),
- * 4 hoisted rotations (n_rot), 5 pt x ct MAC term, 6 rescale, 7 add */
+ * 4 hoisted rotations (n_rot), 5 pt x ct MAC term, 6 rescale, 7 add,
+ * 8 batch of `batch` (<= 64) ciphertexts rotated by the same step (one key),
+ * 9 fused MAC of k = n_rot terms sum_j pt_j (*) ct_j + rescale,
+ * 10 automorphism cycling through every step t in [1, S) one per launch */
 int fheon_microbench(fheon_ctx* ctx, int kind, int batch, int limbs, int n_rot, int iters, double* ms);
 
 /* ---- layers (layers.hpp:83-158).  Tensors are packed channel-major

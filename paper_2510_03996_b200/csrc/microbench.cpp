@@ -10,7 +10,7 @@ namespace fheon {
 
 double microbench(Context& ctx, int kind, int batch, int limbs, int n_rot, int iters) {
   if (limbs < 2 || limbs > ctx.L()) throw Error(ErrKind::shape, "microbench: limbs out of range");
-  if (batch < 1 || batch > kMaxBases) throw Error(ErrKind::shape, "microbench: batch out of range");
+  if (batch < 1 || batch > (kind == 8 ? 64 : kMaxBases)) throw Error(ErrKind::shape, "microbench: batch out of range");
   cudaStream_t st = ctx.stream();
   const DevTables& t = ctx.dev();
   const std::size_t N = ctx.N();
@@ -19,12 +19,22 @@ double microbench(Context& ctx, int kind, int batch, int limbs, int n_rot, int i
   std::uniform_real_distribution<double> u(-1.0, 1.0);
   for (double& v : vals) v = u(rng);
   std::vector<Ciphertext> cts;
-  for (int b = 0; b < batch; ++b) cts.push_back(level_down(ctx, encrypt_top(ctx, vals.data(), vals.size()), limbs));
+  const int ncts = kind == 9 ? std::max(batch, n_rot) : batch;  // MAC: k distinct terms
+  for (int b = 0; b < ncts; ++b) cts.push_back(encrypt_at(ctx, vals.data(), vals.size(), limbs));
   BufPtr pt = ctx.encode(vals.data(), vals.size(), limbs, ctx.host().T[limbs - 1]);
   std::vector<long> steps;
   for (int r = 0; r < std::max(1, n_rot); ++r) steps.push_back(1L << (r % 15));
-  if (kind == 3 || kind == 4)
+  if (kind == 3 || kind == 4 || kind == 8)
     for (long s : steps) ctx.gen_key(ctx.galois(s));
+  // kind 9: the fused MAC sum_j pt_j (*) ct_j over k = n_rot terms (distinct plaintexts)
+  std::vector<BufPtr> mac_pts;
+  if (kind == 9)
+    for (int j = 0; j < std::max(1, n_rot); ++j) {
+      for (double& v : vals) v = u(rng);
+      mac_pts.push_back(ctx.encode(vals.data(), vals.size(), limbs, pt_scale_for(ctx, cts[0])));
+    }
+  // kind 10: the automorphism for every rotation step t in [1, S) (keyless permutation)
+  long auto_t = 1;
   std::vector<Ciphertext> keep;
   auto run = [&]() {
     keep.clear();
@@ -88,6 +98,27 @@ double microbench(Context& ctx, int kind, int batch, int limbs, int n_rot, int i
       case 7:
         for (int b = 0; b < batch; ++b) keep.push_back(add(ctx, cts[b], cts[(b + 1) % batch]));
         break;
+      case 8:  // batch of `batch` distinct ciphertexts rotated by the SAME step: one key read per launch
+        keep = rotate_many(ctx, cts, std::vector<long>(batch, steps[0]));
+        break;
+      case 9: {
+        std::vector<Ciphertext> terms(cts.begin(), cts.begin() + std::max(1, n_rot));
+        keep = mac_plain_many(ctx, {terms}, {mac_pts});
+        break;
+      }
+      case 10: {
+        PolyList o{}, in{};
+        BufPtr out = ctx.alloc(2 * (std::size_t)limbs * N);
+        for (int p = 0; p < 2; ++p) {
+          in.p[p] = p ? cts[0].c1 : cts[0].c0;
+          o.p[p] = out->ptr + (std::size_t)p * limbs * N;
+          o.g[p] = ctx.galois(auto_t);
+        }
+        o.n = in.n = 2;
+        automorph(t, o, in, limbs, st);
+        auto_t = auto_t % (ctx.S() - 1) + 1;
+        break;
+      }
       default:
         throw Error(ErrKind::shape, "microbench: unknown kind");
     }

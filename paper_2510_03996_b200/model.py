@@ -906,16 +906,16 @@ class EncryptedModel:
         regeneration."""
         import torch
         plan = keyplan.plan_blocks(self.layer_keys())
-        store = {}
+        store = {}  # by Galois element: rotation steps t and t - S share a key
         for t in plan.union_keys.indices():
             g = self.ctx.galois_element(t)
-            if g == 1:
+            if g == 1 or g in store:
                 continue
             self.ctx.prefetch_rotation_keys([t])
             buf = torch.empty(self.ctx.key_packed_words(), dtype=torch.uint64, pin_memory=True)
-            store[t] = self.ctx.key_download_packed(g, out=buf.numpy())
+            store[g] = self.ctx.key_download_packed(g, out=buf.numpy())
         self._key_store = store
-        self._streamed = set(store)  # resident right now
+        self._streamed = set(store)  # Galois elements resident right now
 
     def output_count(self) -> int:
         packed, C, W, n = self.layers[-1].out_shape
@@ -974,15 +974,17 @@ class EncryptedModel:
                 blk = plan.blocks[plan.block_of_layer(i)]
                 if blk.first_layer == i:
                     if i == 0:  # "load block 0": nothing else of the plan stays resident
-                        drop = [t for t in plan.union_keys.indices() if not blk.keys.contains(t)]
+                        keep = {self.ctx.galois_element(t) for t in blk.keys.indices()}
+                        drop = [t for t in plan.union_keys.indices() if self.ctx.galois_element(t) not in keep]
                         self.ctx.drop_rotation_keys(drop)
                         if store is not None:
-                            self._streamed -= set(drop)
+                            self._streamed -= {self.ctx.galois_element(t) for t in drop}
                     if store is not None:  # stream the block's missing keys from pinned host memory
                         for t in blk.keys.indices():
-                            if t in store and t not in self._streamed:
-                                self.ctx.key_upload(self.ctx.galois_element(t), store[t], async_copy=True)
-                                self._streamed.add(t)
+                            g = self.ctx.galois_element(t)
+                            if g in store and g not in self._streamed:
+                                self.ctx.key_upload(g, store[g], async_copy=True)
+                                self._streamed.add(g)
                     else:
                         self.ctx.prefetch_rotation_keys(blk.keys.indices())
                     peak_key_bytes = max(peak_key_bytes, self.ctx.key_bytes())
@@ -997,11 +999,11 @@ class EncryptedModel:
             if key_mode == "block":
                 bi = plan.block_of_layer(i)
                 if plan.blocks[bi].last_layer == i and bi + 1 < len(plan.blocks):
-                    nxt = plan.blocks[bi + 1].keys
-                    drop = [t for t in plan.blocks[bi].keys.indices() if not nxt.contains(t)]
+                    nxt = {self.ctx.galois_element(t) for t in plan.blocks[bi + 1].keys.indices()}
+                    drop = [t for t in plan.blocks[bi].keys.indices() if self.ctx.galois_element(t) not in nxt]
                     self.ctx.drop_rotation_keys(drop)
                     if store is not None:
-                        self._streamed -= set(drop)
+                        self._streamed -= {self.ctx.galois_element(t) for t in drop}
             ledger.append((b.name, b.cost, lin, lout, b.type == "bootstrap"))
             if b.type == "bootstrap":
                 if lout != self.spec.depth_budget:
