@@ -526,6 +526,32 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def host_cpu():
+    """The GPU box's host: lscpu model name and logical core count."""
+    model = None
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
+
+
+def reference_config1_conv():
+    """BASELINE configs[0] through the reference's own convolution() (layers_conv.cpp:577-594,
+    oracle/_ref) on this host, same seeded input / weights as our config-1 layer: mean of 50."""
+    from oracle import ref as sref
+    r = sref.Ref(16384, 8192, 10)
+    x = np.random.default_rng(1001).uniform(0, 1, (1, 28, 28))
+    w = np.random.default_rng(1002).normal(0, 0.1, (6, 1, 5, 5))
+    r.convolution(x, 10, 1, 28, 6, 5, 1, 0, 0, 0, w, None)
+    t0 = time.perf_counter()
+    for _ in range(50):
+        r.convolution(x, 10, 1, 28, 6, 5, 1, 0, 0, 0, w, None)
+    return round((time.perf_counter() - t0) / 50 * 1e3, 3)
+
+
 def cpu_baseline_reference(spec, x, depth):
     """The reference's own infer() (oracle/_ref, the unmodified slotcnn core) on the
     same spec, weights and input: one image on one host core."""
@@ -542,7 +568,8 @@ def cpu_baseline_reference(spec, x, depth):
     return {"value": round(dt, 4), "unit": "s/image", "cores": 1, "kind": "reference",
             "sample": f"one ResNet-20 image through the reference's infer() (slotcnn cleartext slot simulator, "
                       f"N=2^16 depth {depth}, {sum(1 for r in rows if r[3])} top-level bootstraps)",
-            "reference_internal_wall_s": round(rwall / 1e3, 4),
+            "reference_internal_wall_s": round(rwall / 1e3, 4), "host": host_cpu(),
+            "reference_config1_conv_ms_1core": reference_config1_conv(),
             "_logit_err_fn": lambda lg: float(np.abs(np.asarray(lg)[:rl.size] - rl).max())}
 
 
@@ -795,6 +822,8 @@ def run_reference(args):
         "e2e": {"value": round(value, 4), "unit": "s/image", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "all_core_throughput": {"images": cores, "threads": cores, "wall_s": round(par, 3),
                                 "s_per_image": round(par / cores, 4)},
+        "host": host_cpu(),
+        "reference_config1_conv_ms_1core": reference_config1_conv(),
         "rep_times_s": [round(t, 4) for t in times],
         "note": "the reference's backend is a cleartext slot simulator (backend.cpp:165-249: rotate is a memcpy, "
                 "bootstrap a level reset) -- it does no cryptography; the paper's OpenFHE CPU figure for "
