@@ -88,6 +88,11 @@ int fheon_cheb_relu_coefficients(double beta, int degree, double* coeffs);
 /* ---- context (SlotContext::create, backend.hpp:69) */
 int fheon_ctx_create(const fheon_params* p, fheon_ctx** out);
 void fheon_ctx_destroy(fheon_ctx* ctx);
+/* a second context over the same parameters and secret that SHARES the parent's resident
+ * evaluation keys (read-only device buffers; keys made later are per-context): its own CUDA
+ * stream, pools and caches, so several images are in flight on one GPU (one host thread per
+ * context) without duplicating the tens of GB of keys.  Ciphertexts are bit-compatible. */
+int fheon_ctx_clone(const fheon_ctx* parent, fheon_ctx** out);
 /* the context's log2(QP) and HE-standard security level (as fheon_host_security) */
 int fheon_ctx_security(const fheon_ctx* ctx, double* log_qp, int* level);
 /* primes[L+K], scales[L] (scale target per level), slots */

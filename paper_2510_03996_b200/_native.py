@@ -66,6 +66,7 @@ SIGNATURES = {
     "fheon_host_primes": (C.c_int, [C.POINTER(fheon_params), u64p, dp]),
     "fheon_host_security": (C.c_int, [C.POINTER(fheon_params), dp, C.POINTER(C.c_int), dp]),
     "fheon_ctx_security": (C.c_int, [vp, dp, C.POINTER(C.c_int)]),
+    "fheon_ctx_clone": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
     "fheon_key_packed_words": (C.c_size_t, [vp]),
     "fheon_key_download_packed": (C.c_int, [vp, C.c_uint64, u64p]),
     "fheon_key_upload": (C.c_int, [vp, C.c_uint64, u64p]),

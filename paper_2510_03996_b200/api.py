@@ -237,12 +237,15 @@ class TraceRecorder:
 class SlotContext:
     """SlotContext::create (backend.hpp:66-93): owns the device context."""
 
-    def __init__(self, config: ContextConfig):
+    def __init__(self, config: ContextConfig, _share_keys_from: Optional["SlotContext"] = None):
         self.config = config
         L = _native.lib()
         p = config.params()
         h = C.c_void_p()
-        _check(L.fheon_ctx_create(C.byref(p), C.byref(h)))
+        if _share_keys_from is None:
+            _check(L.fheon_ctx_create(C.byref(p), C.byref(h)))
+        else:
+            _check(L.fheon_ctx_clone(_share_keys_from._h, C.byref(h)))
         self._h = h
         self.L = p.limbs
         self.K = p.special_limbs
@@ -261,6 +264,12 @@ class SlotContext:
     @staticmethod
     def create(config: ContextConfig) -> "SlotContext":
         return SlotContext(config)
+
+    def clone(self) -> "SlotContext":
+        """A second context (own CUDA stream, pools, caches) over the same parameters and
+        secret that shares this one's resident evaluation keys: several images in flight
+        on one GPU, one host thread per context, without duplicating the keys."""
+        return SlotContext(self.config, _share_keys_from=self)
 
     def __del__(self):
         h = getattr(self, "_h", None)

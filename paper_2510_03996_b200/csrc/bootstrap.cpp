@@ -263,10 +263,10 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
     stc_ = plan(groups, stc_limbs, h.T[stc_limbs - 1]);
   }
   for (long s : rotation_steps()) {  // a server context (no secret) receives them by upload
-    if (ctx.has_secret()) ctx.gen_key(ctx.galois(s));
+    if (ctx.has_secret() && !ctx.inheriting_keys) ctx.gen_key(ctx.galois(s));
     ctx.pin_key(ctx.galois(s));
   }
-  if (ctx.has_secret()) {
+  if (ctx.has_secret() && !ctx.inheriting_keys) {
     ctx.gen_key(2 * (u64)h.N - 1);  // conjugation
     ctx.gen_key(0);                 // relinearisation
   }
@@ -274,7 +274,7 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
   ctx.pin_key(0);
   if (ctx.sse()) {  // sparse-secret encapsulation keys
     for (u64 id : {kKeyToSparse, kKeyFromSparse}) {
-      if (ctx.has_secret()) ctx.gen_key(id);
+      if (ctx.has_secret() && !ctx.inheriting_keys) ctx.gen_key(id);
       ctx.pin_key(id);
     }
   }

@@ -150,6 +150,16 @@ void fheon_ctx_destroy(fheon_ctx* ctx) {
   delete ctx;
 }
 
+int fheon_ctx_clone(const fheon_ctx* parent, fheon_ctx** out) {
+  return guard([&] {
+    need(parent, "parent");
+    need(out, "out");
+    *out = new fheon_ctx{new fheon::Context(parent->impl->host().p, *parent->impl)};
+    (*out)->impl->schedule = parent->impl->schedule;
+    (*out)->impl->weight_cache_budget = parent->impl->weight_cache_budget;
+  });
+}
+
 int fheon_ctx_security(const fheon_ctx* ctx, double* log_qp, int* level) {
   return guard([&] {
     need(ctx, "ctx");

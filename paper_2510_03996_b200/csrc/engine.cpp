@@ -204,7 +204,14 @@ u64 prod_mod(const std::vector<u64>& primes, int lo, int hi, int skip, u64 m) {
 
 }  // namespace
 
-Context::Context(const Params& p) : ht_(make_tables(p)) {
+Context::Context(const Params& p, const Context* parent) : ht_(make_tables(p)) {
+  if (parent) {
+    const Params& pp = parent->host().p;
+    if (pp.logN != p.logN || pp.L != p.L || pp.K != p.K || pp.dnum != p.dnum || pp.seed != p.seed ||
+        pp.hamming_weight != p.hamming_weight || parent->host().q != ht_.q)
+      throw Error(ErrKind::internal, "key-sharing context: parameters differ from the parent's");
+    inheriting_keys = true;  // the bootstrapper pins the parent's keys instead of generating
+  }
   if (ht_.alpha > kMaxAlpha - 1) throw Error(ErrKind::shape, "a key-switching digit must hold < 16 limbs");
   if (ht_.ndig > kMaxDigits) throw Error(ErrKind::shape, "at most 16 key-switching digits");
   if (p.K > kMaxK - 1) throw Error(ErrKind::shape, "K must be < 16");
@@ -292,7 +299,15 @@ Context::Context(const Params& p) : ht_(make_tables(p)) {
       throw Error(ErrKind::shape, "depth budget " + std::to_string(p.depth_budget) +
                                       " exceeds the levels left after bootstrapping (" + std::to_string(after) + ")");
   }
+  if (parent) {
+    keys_ = parent->keys_;  // shared read-only device buffers
+    for (u64 id : parent->pinned_keys_) pinned_keys_.insert(id);
+    inheriting_keys = false;
+  }
 }
+
+Context::Context(const Params& p) : Context(p, nullptr) {}
+Context::Context(const Params& p, const Context& parent) : Context(p, &parent) {}
 
 Context::~Context() {
   boot.reset();

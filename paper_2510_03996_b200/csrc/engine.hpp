@@ -119,6 +119,13 @@ struct KernelTimer {
 class Context {
  public:
   explicit Context(const Params& p);
+  // (delegation target of both public constructors)
+  Context(const Params& p, const Context* share_keys_from);
+  // a second context over the same parameters and secret that SHARES the parent's
+  // resident evaluation keys (read-only device buffers) instead of generating its
+  // own: its own stream, pools' streams, caches and counters, so two images can be
+  // in flight on one GPU without doubling the key memory
+  Context(const Params& p, const Context& share_keys_from);
   ~Context();
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
@@ -161,6 +168,8 @@ class Context {
   void put_key(u64 key_id, BufPtr kb) { keys_[key_id] = std::move(kb); }
   // a server context (Params::no_secret) cannot generate keys, encrypt or decrypt
   bool has_secret() const { return dt_.s_ntt != nullptr; }
+  // true while a key-sharing clone is being built (its keys come from the parent)
+  bool inheriting_keys = false;
   void require_secret(const char* what) const;
   bool strict_keys = false;
 

@@ -896,6 +896,15 @@ class EncryptedModel:
         c = self.ctx
         return keyplan.MemoryModel.for_engine(c.N, c.L, c.K, c.dnum, self._pinned_keys)
 
+    def clone(self) -> "EncryptedModel":
+        """The same built model on a key-sharing context clone (SlotContext.clone):
+        run it from a second host thread to keep two images in flight on the GPU."""
+        twin = EncryptedModel.__new__(EncryptedModel)
+        twin.__dict__.update(self.__dict__)
+        twin.ctx = self.ctx.clone()
+        twin._key_store = None
+        return twin
+
     def enable_key_streaming(self):
         """Keyplan block mode WITHOUT regenerating keys on the device: every rotation
         key of the plan is serialized once (packed wire format) into pinned host

@@ -84,3 +84,36 @@ def test_server_bootstraps_with_uploaded_keys():
     assert y.level() == client.depth_budget()
     assert np.abs(y.slots() - v).max() < 1e-4
     assert np.array_equal(sy.words(), fh.bootstrap(fh.SlotVector.from_words(client, x.words(), x.scale())).words())
+
+
+def test_key_sharing_clone_runs_concurrently_bit_exact():
+    """SlotContext.clone: a second context over the same keys (no new key memory),
+    own stream; two host threads drive both at once and each result is bit-exact
+    with the same ops on the parent alone."""
+    import threading
+    cfg = fh.ContextConfig(N, S, -1, fh.CryptoMetadata(55, 40, 3), limbs=24, special_limbs=8, special_bits=60,
+                           seed=47, bootstrap=True, boot_scale_bits=55, allow_insecure=True)
+    parent = fh.SlotContext(cfg)
+    parent.keygen_rotations([1, 5])
+    kb = parent.key_bytes()
+    twin = parent.clone()
+    assert twin.key_bytes() == kb and twin.key_count() == parent.key_count()
+    v = np.random.default_rng(3).uniform(-1, 1, S)
+    x = fh.level_down(fh.SlotVector.encode(parent, v), 1)
+    words, scale = x.words(), x.scale()
+
+    def pipeline(ctx):
+        y = fh.SlotVector.from_words(ctx, words, scale)
+        y = fh.bootstrap(y)
+        return fh.mult_cipher(fh.rotate(y, 1), fh.rotate(y, 5)).words()
+
+    want = pipeline(parent)
+    got = {}
+    th = [threading.Thread(target=lambda c, k: got.__setitem__(k, pipeline(c)), args=(c, k))
+          for k, c in (("a", parent), ("b", twin))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert np.array_equal(got["a"], want) and np.array_equal(got["b"], want)
+    assert twin.key_bytes() == kb  # nothing was generated on the clone
