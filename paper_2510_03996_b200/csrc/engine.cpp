@@ -374,6 +374,9 @@ void Context::build_device_tables() {
     c.pad = 0;
   }
   t.pc = upload(dev_allocs_, pcs, stream_);
+  t.rotgroup = upload(dev_allocs_, ht_.rotgroup, stream_);
+  t.ksi_re = upload(dev_allocs_, ht_.ksi_re, stream_);
+  t.ksi_im = upload(dev_allocs_, ht_.ksi_im, stream_);
 
   // twiddles [NP][4][N]
   std::vector<u64> tw((std::size_t)NP * 4 * N);
@@ -680,12 +683,7 @@ BufPtr Context::encode_complex(const double* re, const double* im, std::size_t n
   const std::size_t N = ht_.N;
   BufPtr out = alloc((std::size_t)(limbs + special) * N);
   ++stats.encodes;
-  cudaEvent_t* ev = nullptr;
-  long long* h = staging_slot(&ev);
-  encode_complex_coeffs_host(ht_, re, im, n, scale, h);
-  BufPtr dcoef = alloc(N);
-  FHEON_CUDA(cudaMemcpyAsync(dcoef->ptr, h, N * sizeof(long long), cudaMemcpyHostToDevice, stream_));
-  FHEON_CUDA(cudaEventRecord(*ev, stream_));
+  BufPtr dcoef = encode_device(re, im, n, scale);
   coeffs_to_rns(dt_, out->ptr, reinterpret_cast<const long long*>(dcoef->ptr), limbs, stream_);
   if (special > 0)
     coeffs_to_rns(dt_, out->ptr + (std::size_t)limbs * N, reinterpret_cast<const long long*>(dcoef->ptr), special,
@@ -947,6 +945,36 @@ bool constant_value(const double* vals, std::size_t n, int S, double* c) {
 }
 }  // namespace
 
+// slot values -> N signed coefficients on the device (encode.cu): the values ride the
+// pinned staging ring to the device, the special FFT runs there
+BufPtr Context::encode_device(const double* re, const double* im, std::size_t n, double scale) {
+  const std::size_t N = ht_.N, S = (std::size_t)ht_.S;
+  if (n > S) throw Error(ErrKind::capacity, "payload exceeds the slot count");
+  // every coefficient is an average of the slot values times unit roots: |c| <= max|v| * scale
+  double mx = 0.0;
+  for (std::size_t i = 0; i < n; ++i) {
+    mx = std::max(mx, std::fabs(re[i]));
+    if (im) mx = std::max(mx, std::fabs(im[i]));
+  }
+  if (!(mx * std::fabs(scale) < 4611686018427387904.0))
+    throw Error(ErrKind::capacity, "encoded value exceeds the 2^62 coefficient range");
+  BufPtr work = alloc(N);  // [re S][im S] doubles
+  FHEON_CUDA(cudaMemsetAsync(work->ptr, 0, N * sizeof(u64), stream_));
+  cudaEvent_t* ev = nullptr;
+  long long* h = staging_slot(&ev);
+  double* hd = reinterpret_cast<double*>(h);
+  std::memcpy(hd, re, n * sizeof(double));
+  if (im) std::memcpy(hd + S, im, n * sizeof(double));
+  FHEON_CUDA(cudaMemcpyAsync(work->ptr, hd, n * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  if (im)
+    FHEON_CUDA(cudaMemcpyAsync(work->ptr + S, hd + S, n * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  FHEON_CUDA(cudaEventRecord(*ev, stream_));
+  BufPtr dcoef = alloc(N);
+  encode_fft_device(dt_, reinterpret_cast<long long*>(dcoef->ptr), reinterpret_cast<double*>(work->ptr), scale,
+                    stream_);
+  return dcoef;
+}
+
 BufPtr Context::encode(const double* vals, std::size_t n, int limbs, double scale) {
   const std::size_t N = ht_.N;
   BufPtr out = alloc((std::size_t)limbs * N);
@@ -968,12 +996,7 @@ BufPtr Context::encode(const double* vals, std::size_t n, int limbs, double scal
     ew_add_const(dt_, o, o, lc, limbs, stream_);
     return out;
   }
-  cudaEvent_t* ev = nullptr;
-  long long* h = staging_slot(&ev);
-  encode_coeffs(vals, n, scale, h);
-  BufPtr dcoef = alloc(N);
-  FHEON_CUDA(cudaMemcpyAsync(dcoef->ptr, h, N * sizeof(long long), cudaMemcpyHostToDevice, stream_));
-  FHEON_CUDA(cudaEventRecord(*ev, stream_));
+  BufPtr dcoef = encode_device(vals, nullptr, n, scale);
   coeffs_to_rns(dt_, out->ptr, reinterpret_cast<const long long*>(dcoef->ptr), limbs, stream_);
   LimbSet ls{};
   ls.base[0] = out->ptr;

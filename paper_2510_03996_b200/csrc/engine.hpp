@@ -178,6 +178,8 @@ class Context {
   void decode_coeffs(const double* coeffs, double scale, double* out, double* out_im = nullptr) const;
   // encode `vals` at `scale` over `limbs` limbs into a device [limbs][N] NTT-domain buffer
   BufPtr encode(const double* vals, std::size_t n, int limbs, double scale);
+  // the N signed coefficients of round(scale * canonical-embedding preimage), computed on the device
+  BufPtr encode_device(const double* re, const double* im, std::size_t n, double scale);
   // complex slot values (re + i im), host special FFT
   // special > 0: also the first `special` special primes (limbs + special rows, Q u P operands)
   BufPtr encode_complex(const double* re, const double* im, std::size_t n, int limbs, double scale, int special = 0);

@@ -49,6 +49,10 @@ struct DevTables {
   // secret key, NTT domain standard form [L+K][N]
   u64* s_ntt = nullptr;
   u64* sb_ntt = nullptr;  // ephemeral sparse bootstrapping secret (sparse-secret encapsulation), NTT over L+K
+  // encoder (special FFT on the device, encode.cu): 5^j mod 2N (j < S), e^{2 pi i k / 2N} (k <= 2N)
+  u64* rotgroup = nullptr;
+  double* ksi_re = nullptr;
+  double* ksi_im = nullptr;
   // optional live kernel timer (owned by the Context)
   KernelTimer* timer = nullptr;
 };
@@ -245,6 +249,9 @@ void mul_monomial_half(const DevTables& t, const PolyList& out, const PolyList& 
 // ---- encode / encrypt / keygen / decrypt
 // signed coefficients -> RNS coefficient domain [limbs][N]
 void coeffs_to_rns(const DevTables& t, u64* out, const long long* coeffs, int limbs, cudaStream_t st, int p0 = 0);
+// canonical-embedding encode on the device: work = [re S][im S] slot values (zero-padded),
+// overwritten; coeffs [N] = llround(scale * special_fft_inv / S), bit-identical to the host
+void encode_fft_device(const DevTables& t, long long* coeffs, double* work, double scale, cudaStream_t st);
 // CBD21 error polynomial for `stream_key` into limbs 0..nlimbs-1 (prime rule: i < ell ? i : L + i - ell)
 void sample_error(const DevTables& t, u64* out, u64 stream_key, int nlimbs, int ell, cudaStream_t st);
 // c1 = uniform(stream); c0 = m + e - c1 s (m, e NTT domain) over q_0..q_{limbs-1}
