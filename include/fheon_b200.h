@@ -66,6 +66,10 @@ typedef struct {
    * encrypt / decrypt / key generation fail.  The client creates a context with the same
    * parameters (and seed) and generates / downloads the keys. */
   int no_secret;
+  /* EvalMod range K of bootstrapping: |I| <= K for the ModRaise overflow (0 = 16).  With the
+   * encapsulation secret at h_b = 32 (sigma(I) = 1.66) K = 12 is a 7-sigma margin and lowers
+   * the cosine's degree -- one bootstrapping level less */
+  int boot_k_range;
 } fheon_params;
 
 /* ---- errors / version */
@@ -82,6 +86,8 @@ int fheon_host_encode(const fheon_params* p, const double* values, size_t n, dou
  * meets (256/192/128; 0 below 128; -1 sparse main secret, not covered by the table) and the
  * table's log2(QP) bound at min_security (homomorphicencryption.org 2018 Table 1, ternary) */
 int fheon_host_security(const fheon_params* p, double* log_qp, int* level, double* bound);
+/* levels bootstrapping consumes for these parameters (CtS + EvalMod + StC) */
+int fheon_host_bootstrap_depth(const fheon_params* p, int* depth);
 /* Chebyshev interpolant coefficients of max(0, beta z) on [-1, 1] (chebyshev.cpp:33-50) */
 int fheon_cheb_relu_coefficients(double beta, int degree, double* coeffs);
 

@@ -36,6 +36,7 @@ class fheon_params(C.Structure):
         ("min_security", C.c_int),
         ("allow_insecure", C.c_int),
         ("no_secret", C.c_int),
+        ("boot_k_range", C.c_int),
     ]
 
 
@@ -65,6 +66,7 @@ SIGNATURES = {
     "fheon_version": (C.c_int, []),
     "fheon_host_primes": (C.c_int, [C.POINTER(fheon_params), u64p, dp]),
     "fheon_host_security": (C.c_int, [C.POINTER(fheon_params), dp, C.POINTER(C.c_int), dp]),
+    "fheon_host_bootstrap_depth": (C.c_int, [C.POINTER(fheon_params), C.POINTER(C.c_int)]),
     "fheon_ctx_security": (C.c_int, [vp, dp, C.POINTER(C.c_int)]),
     "fheon_ctx_clone": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
     "fheon_key_packed_words": (C.c_size_t, [vp]),

@@ -132,6 +132,8 @@ class ContextConfig:
     # a server context without the secret key: evaluation keys arrive by upload
     # (SlotContext.key_upload), encrypt / decrypt are refused
     no_secret: bool = False
+    # bootstrapping EvalMod range K (|I| <= K); 0 = the engine default, 16
+    boot_k_range: int = 0
     # layer rotation schedule: "fast" (hoisted / log-depth / baby-step giant-step,
     # same values and levels) or "reference" (the reference's exact rotation trace)
     schedule: str = "fast"
@@ -195,6 +197,7 @@ class ContextConfig:
         p.min_security = int(self.security)
         p.allow_insecure = int(bool(self.allow_insecure))
         p.no_secret = int(bool(self.no_secret))
+        p.boot_k_range = int(self.boot_k_range)
         return p
 
 
@@ -922,10 +925,19 @@ def security_report(N: int, log_qp: float, level: int, config: ContextConfig) ->
             "meets_128": bool(level >= 128),
             "secret": (f"sparse ternary h={config.hamming_weight} (not covered by the HE-standard table)" if sparse
                        else "uniform ternary" + (f"; bootstrapping via sparse-secret encapsulation (ephemeral h="
-                                                 f"{config.boot_hamming_weight or 64} on q_0 and P only)"
+                                                 f"{config.boot_hamming_weight or 64} on q_0 and P only, EvalMod "
+                                                 f"range {config.boot_k_range or 16})"
                                                  if config.bootstrap else "")),
             "estimate": "HE standard (homomorphicencryption.org 2018) Table 1, uniform ternary, classical; "
                         "N = 2^16 row as shipped by OpenFHE (1747 / 1224 / 956 bits)"}
+
+
+def host_bootstrap_depth(config: ContextConfig) -> int:
+    """Levels bootstrapping consumes under this configuration (CtS + EvalMod + StC)."""
+    p = config.params()
+    d = C.c_int()
+    _check(_native.lib().fheon_host_bootstrap_depth(C.byref(p), C.byref(d)))
+    return d.value
 
 
 def host_security(config: ContextConfig) -> Dict[str, object]:

@@ -71,7 +71,16 @@ static fheon::Params to_params(const fheon_params* p) {
   if (p->min_security > 0) prm.min_security = p->min_security;
   prm.allow_insecure = p->allow_insecure;
   prm.no_secret = p->no_secret;
+  if (p->boot_k_range > 0) prm.boot_k_range = p->boot_k_range;
   return prm;
+}
+
+int fheon_host_bootstrap_depth(const fheon_params* p, int* depth) {
+  return guard([&] {
+    need(p, "params");
+    need(depth, "depth");
+    *depth = fheon::bootstrap_depth(to_params(p));
+  });
 }
 
 int fheon_host_security(const fheon_params* p, double* log_qp, int* level, double* bound) {

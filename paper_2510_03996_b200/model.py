@@ -726,17 +726,25 @@ def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: s
     N = spec.ring_dimension
     if spec.slot_count != N // 2:
         raise fh.ShapeError("the engine packs fully: slot_count must be ring_dimension / 2", 2)
-    boot_depth = 16 if bootstrapping else 0
-    L = spec.depth_budget + 1 + boot_depth
     secure = security > 0
+    # 128-bit chains: the encapsulation's ephemeral secret at h_b = 32 (sigma(I) = 1.66) with
+    # EvalMod range K = 12 (7.2 sigma): a lower-degree cosine, one bootstrapping level less
+    boot_hw, boot_kr = (32, 12) if secure else (0, 0)
 
-    def config(K, dnum):
+    def config(K, dnum, L=1):
         return fh.ContextConfig(N, N // 2, spec.depth_budget if not bootstrapping else -1,
                                 fh.CryptoMetadata(55, 40, dnum), limbs=L, special_limbs=K, special_bits=60, seed=seed,
                                 hamming_weight=0 if (secure or not bootstrapping) else 64, bootstrap=bootstrapping,
                                 boot_scale_bits=(60 if secure else 55) if bootstrapping else 0, schedule=schedule,
-                                digit_split=1,
+                                digit_split=1, boot_hamming_weight=boot_hw, boot_k_range=boot_kr,
                                 security=security if secure else 128, allow_insecure=not secure)
+
+    boot_depth = fh.host_bootstrap_depth(config(1, 3)) if bootstrapping else 0
+    L = spec.depth_budget + 1 + boot_depth
+    _config = config
+
+    def config(K, dnum):  # noqa: F811 -- the chain's limb count fixed from here on
+        return _config(K, dnum, L)
 
     def smallest_k(dnum):
         # digits balanced by bit size over the real Q chain (the special primes are

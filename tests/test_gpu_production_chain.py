@@ -172,9 +172,9 @@ def test_mode2_bconv_bit_exact(K):
         assert np.array_equal(fh.rotate(xs, -5).words(), orc.rotate(c, -5, orc.rotation_key(-5)))
 
 
-# ---- the 128-bit headline chain: ResNet-20 at depth budget 12, N = 2^16,
-# uniform ternary secret, sparse-secret encapsulation for bootstrapping, 60-bit
-# CoeffsToSlots / EvalMod levels, L = 29, K = 4, dnum = 8 (log2 QP = 1701 <= 1747,
+# ---- a 128-bit chain: ResNet-20 at depth budget 12, N = 2^16, uniform ternary
+# secret, sparse-secret encapsulation (h_b = 32, EvalMod range 12) for bootstrapping,
+# 60-bit CoeffsToSlots / EvalMod levels, L = 28, K = 5, dnum = 6 (log2 QP <= 1747,
 # model.ckks_config security=128)
 
 @pytest.fixture(scope="module")
@@ -186,18 +186,19 @@ def secure():
     L, K = cfg.limbs, cfg.special_limbs
     orc = Oracle.from_chain(16, ctx.primes, ctx.scales, L, K, cfg.crypto.key_switch_digits, seed=cfg.seed,
                             digit_split=cfg.digit_split)
-    orc.set_boot_secret(64)
+    orc.set_boot_secret(cfg.boot_hamming_weight or 64)
     return ctx, orc, cfg
 
 
 def test_secure_chain_shape(secure):
     ctx, orc, cfg = secure
-    assert (cfg.limbs, cfg.special_limbs, cfg.crypto.key_switch_digits) == (29, 4, 8)
-    assert len(_digits(ctx.primes, cfg.limbs, 8)) == 8
+    dnum = cfg.crypto.key_switch_digits
+    assert cfg.limbs == 12 + 1 + 15 and dnum > 3  # 15 bootstrapping levels (EvalMod range 12)
+    assert len(_digits(ctx.primes, cfg.limbs, dnum)) == dnum
     assert max(int(q).bit_length() for q in ctx.primes) == 61  # 60-bit-target bootstrapping primes
 
 
-@pytest.mark.parametrize("limbs", [29, 13, 1])
+@pytest.mark.parametrize("limbs", [28, 13, 1])
 def test_secure_rotation_and_mult_cipher_bit_exact(secure, limbs):
     ctx, orc, _ = secure
     a = np.ascontiguousarray(_ct(orc, 7800 + limbs, 20)[1][:, :limbs])
