@@ -70,6 +70,9 @@ typedef struct {
    * encapsulation secret at h_b = 32 (sigma(I) = 1.66) K = 12 is a 7-sigma margin and lowers
    * the cosine's degree -- one bootstrapping level less */
   int boot_k_range;
+  /* levels of the bootstrapping linear transforms (0 = 3 each): CoeffsToSlots, SlotsToCoeffs */
+  int boot_cts_levels;
+  int boot_stc_levels;
 } fheon_params;
 
 /* ---- errors / version */

@@ -37,6 +37,8 @@ class fheon_params(C.Structure):
         ("allow_insecure", C.c_int),
         ("no_secret", C.c_int),
         ("boot_k_range", C.c_int),
+        ("boot_cts_levels", C.c_int),
+        ("boot_stc_levels", C.c_int),
     ]
 
 

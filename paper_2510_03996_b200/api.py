@@ -134,6 +134,9 @@ class ContextConfig:
     no_secret: bool = False
     # bootstrapping EvalMod range K (|I| <= K); 0 = the engine default, 16
     boot_k_range: int = 0
+    # levels of the bootstrapping linear transforms (0 = 3 each)
+    boot_cts_levels: int = 0
+    boot_stc_levels: int = 0
     # layer rotation schedule: "fast" (hoisted / log-depth / baby-step giant-step,
     # same values and levels) or "reference" (the reference's exact rotation trace)
     schedule: str = "fast"
@@ -198,6 +201,8 @@ class ContextConfig:
         p.allow_insecure = int(bool(self.allow_insecure))
         p.no_secret = int(bool(self.no_secret))
         p.boot_k_range = int(self.boot_k_range)
+        p.boot_cts_levels = int(self.boot_cts_levels)
+        p.boot_stc_levels = int(self.boot_stc_levels)
         return p
 
 

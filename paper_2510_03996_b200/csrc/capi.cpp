@@ -72,6 +72,8 @@ static fheon::Params to_params(const fheon_params* p) {
   prm.allow_insecure = p->allow_insecure;
   prm.no_secret = p->no_secret;
   if (p->boot_k_range > 0) prm.boot_k_range = p->boot_k_range;
+  if (p->boot_cts_levels > 0) prm.boot_cts_levels = p->boot_cts_levels;
+  if (p->boot_stc_levels > 0) prm.boot_stc_levels = p->boot_stc_levels;
   return prm;
 }
 

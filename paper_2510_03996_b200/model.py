@@ -705,7 +705,7 @@ def count_bootstraps(layers: List[Built]) -> int:
 
 # ----------------------------------------------------------------- engine
 def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: str = "fast",
-                security: int = 128) -> fh.ContextConfig:
+                security: int = 128, boot_levels: Tuple[int, int] = (0, 0)) -> fh.ContextConfig:
     """RNS chain for the spec's ring and depth budget: 55-bit q0, 40-bit
     application primes, 55-bit bootstrapping levels (+16 levels), digits
     balanced by prime bit size, 60-bit special primes (the fewest whose product
@@ -737,6 +737,7 @@ def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: s
                                 hamming_weight=0 if (secure or not bootstrapping) else 64, bootstrap=bootstrapping,
                                 boot_scale_bits=(60 if secure else 55) if bootstrapping else 0, schedule=schedule,
                                 digit_split=1, boot_hamming_weight=boot_hw, boot_k_range=boot_kr,
+                                boot_cts_levels=boot_levels[0], boot_stc_levels=boot_levels[1],
                                 security=security if secure else 128, allow_insecure=not secure)
 
     boot_depth = fh.host_bootstrap_depth(config(1, 3)) if bootstrapping else 0
@@ -818,14 +819,15 @@ class InferResult:
 class EncryptedModel:
     """A built model bound to an engine context (keys generated on first use)."""
 
-    def __init__(self, spec: ModelSpec, seed: int = 1, schedule: str = "fast", security: int = 128):
+    def __init__(self, spec: ModelSpec, seed: int = 1, schedule: str = "fast", security: int = 128,
+                 boot_levels: Tuple[int, int] = (0, 0)):
         """security: HE-standard level the chain must meet (ckks_config); 0 runs
         the insecure round-1 chain the reference's presets need (disclosed in
         self.security)."""
         self.spec = spec
         self.layers = build(spec)
         self.n_boot = count_bootstraps(self.layers)
-        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule, security))
+        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule, security, boot_levels))
         self.security = self.ctx.security()
         self._layer_keys: Optional[List[keyplan.LayerKeys]] = None
         self._pinned_keys = self.ctx.key_count()  # relinearisation / bootstrapping keys made at creation
