@@ -374,6 +374,7 @@ def rotation_bench(args):
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(args)
     del cts, ctx
+    fh.api.release_memory()
     return line
 
 
@@ -549,7 +550,8 @@ def run_ours(args):
         "roofline": roofline,
         "clocks": clk.summary(),
     }
-    del em, ems, ctx, xin, xins
+    del em, ems, ctx, xin, xins, streams
+    fh.api.release_memory()
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_reference(spec, x, depth)
         line["logits_max_abs_err_vs_reference"] = line["cpu_baseline"].pop("_logit_err_fn")(logits_dev)
@@ -691,6 +693,7 @@ def model_runs(args):
     N = 2^15, where bootstrapping alone needs more modulus than the 881-bit
     bound) run with security=0 and say so."""
     import tempfile
+    import paper_2510_03996_b200 as fh
     from paper_2510_03996_b200 import model as M
     try:
         from oracle import ref as sref
@@ -731,7 +734,7 @@ def model_runs(args):
     for name, spec, x, security, ref_schedule_only in cases:
         em = M.EncryptedModel(spec, security=security, schedule="reference" if ref_schedule_only else "fast")
         reps = 1 if ref_schedule_only else args.model_reps
-        for _ in range(1 if ref_schedule_only else 2):  # warm-up: lazy keys, plaintext caches, pool growth
+        for _ in range(1 if ref_schedule_only else 3):  # warm-up: lazy keys, plaintext caches, pool growth
             em.infer(x)
         times = []
         for _ in range(reps):

@@ -101,7 +101,10 @@ void fheon_ctx_destroy(fheon_ctx* ctx);
  * evaluation keys (read-only device buffers; keys made later are per-context): its own CUDA
  * stream, pools and caches, so several images are in flight on one GPU (one host thread per
  * context) without duplicating the tens of GB of keys.  Ciphertexts are bit-compatible. */
-int fheon_ctx_clone(const fheon_ctx* parent, fheon_ctx** out);
+int fheon_ctx_clone(fheon_ctx* parent, fheon_ctx** out);
+/* synchronise the device and return the stream-ordered pool's unused memory to the system
+ * (between workloads: contexts destroyed, their buffers released) */
+int fheon_release_memory(void);
 /* the context's log2(QP) and HE-standard security level (as fheon_host_security) */
 int fheon_ctx_security(const fheon_ctx* ctx, double* log_qp, int* level);
 /* primes[L+K], scales[L] (scale target per level), slots */

@@ -71,6 +71,7 @@ SIGNATURES = {
     "fheon_host_bootstrap_depth": (C.c_int, [C.POINTER(fheon_params), C.POINTER(C.c_int)]),
     "fheon_ctx_security": (C.c_int, [vp, dp, C.POINTER(C.c_int)]),
     "fheon_ctx_clone": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
+    "fheon_release_memory": (C.c_int, []),
     "fheon_key_packed_words": (C.c_size_t, [vp]),
     "fheon_key_download_packed": (C.c_int, [vp, C.c_uint64, u64p]),
     "fheon_key_upload": (C.c_int, [vp, C.c_uint64, u64p]),

@@ -937,6 +937,13 @@ def security_report(N: int, log_qp: float, level: int, config: ContextConfig) ->
                         "N = 2^16 row as shipped by OpenFHE (1747 / 1224 / 956 bits)"}
 
 
+def release_memory():
+    """Synchronise and return the engine pool's unused device memory (between workloads)."""
+    import gc
+    gc.collect()
+    _check(_native.lib().fheon_release_memory())
+
+
 def host_bootstrap_depth(config: ContextConfig) -> int:
     """Levels bootstrapping consumes under this configuration (CtS + EvalMod + StC)."""
     p = config.params()

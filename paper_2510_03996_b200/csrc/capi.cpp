@@ -161,13 +161,28 @@ void fheon_ctx_destroy(fheon_ctx* ctx) {
   delete ctx;
 }
 
-int fheon_ctx_clone(const fheon_ctx* parent, fheon_ctx** out) {
+int fheon_ctx_clone(fheon_ctx* parent, fheon_ctx** out) {
   return guard([&] {
     need(parent, "parent");
     need(out, "out");
     *out = new fheon_ctx{new fheon::Context(parent->impl->host().p, *parent->impl)};
     (*out)->impl->schedule = parent->impl->schedule;
-    (*out)->impl->weight_cache_budget = parent->impl->weight_cache_budget;
+    // the keys are shared, the resident weight plaintexts are not: split the parent's
+    // budget so the two caches together stay within what the parent alone was given
+    const std::size_t half = parent->impl->weight_cache_budget / 2;
+    parent->impl->weight_cache_budget = half;
+    (*out)->impl->weight_cache_budget = half;
+  });
+}
+
+int fheon_release_memory(void) {
+  return guard([&] {
+    int dev = 0;
+    FHEON_CUDA(cudaGetDevice(&dev));
+    FHEON_CUDA(cudaDeviceSynchronize());
+    cudaMemPool_t pool;
+    FHEON_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    FHEON_CUDA(cudaMemPoolTrimTo(pool, 0));
   });
 }
 

@@ -21,10 +21,15 @@ if which == "resnet20":
     spec = M.calibrate_relu_scales(spec, [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32)))
                                           for i in range(6)])
     x = norm(np.random.default_rng(4001).uniform(0, 1, (3, 32, 32)))
+elif which == "vgg16":
+    spec = M.calibrate_relu_scales(M.vgg16_paper(ring=65536, depth_budget=depth),
+                                   [norm(np.random.default_rng(5002 + i).uniform(0, 1, (3, 32, 32))) for i in range(4)])
+    x = norm(np.random.default_rng(5001).uniform(0, 1, (3, 32, 32)))
 else:
     spec = M.lenet5(ring=32768, depth_budget=depth)
     x = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
 em = M.EncryptedModel(spec, security=int(__import__('os').environ.get('FHEON_SECURITY', '0')))
+em.infer(x)
 em.infer(x)
 t0 = time.perf_counter()
 r = em.infer(x)
