@@ -1254,12 +1254,91 @@ Ciphertext whole_channel_pool(Context& ctx, const PackedTensor& x, std::size_t k
 
 // ------------------------------------------------------------- FC
 // fully_connected (layers_misc.cpp:197-255): neurons batched
+namespace {
+// y = W x (m x n, row-major) as a baby-step giant-step sum of GENERALISED diagonals (fast
+// schedule): y_i = sum_{k < n + m - 1} diag_k[i] x[i + k - (m - 1)] with diag_k[i] =
+// W[i][i + k - (m - 1)] where i < m and the column lies in [0, n), 0 elsewhere.  The zero
+// entries make every product ignore the slots of x outside [0, n) (post-ReLU p(0), say)
+// and leave [m, S) exactly zero -- the reference FC's output layout -- in ONE level.
+// Babies rot(x, k0 + b) (one hoisted set), giants g: rot(sum_b diag'_{g n1 + b} (*) baby_b,
+// g n1) with the diagonals pre-rotated by -g n1, one fused MAC per giant, one
+// rotate-and-sum, one rescale.  n1 = 32 (the MAC's terms per output): a 1024 x 1024 layer
+// is 32 + 64 key switches and 2047 plaintext products instead of 1024 neurons x log2(1024)
+// folds.  The diagonals are resident weight plaintexts.
+Ciphertext fc_diagonal(Context& ctx, const Ciphertext& x, std::size_t n, std::size_t m, const double* w) {
+  const long S = ctx.S();
+  const std::size_t D = n + m - 1;
+  const long k0 = -(long)(m - 1);
+  const std::size_t n1 = std::min<std::size_t>((std::size_t)kMacMaxTerms, D);
+  const std::size_t G = (D + n1 - 1) / n1;
+  auto norm = [S](long t) {
+    long r = t % S;
+    return r < 0 ? r + S : r;
+  };
+  std::vector<long> offs;
+  for (std::size_t b = 0; b < n1; ++b)
+    if (norm(k0 + (long)b) != 0) offs.push_back(k0 + (long)b);
+  const std::vector<Ciphertext> rot = rotate_hoisted(ctx, x, offs);
+  std::vector<Ciphertext> baby;
+  {
+    std::size_t r = 0;
+    for (std::size_t b = 0; b < n1; ++b) baby.push_back(norm(k0 + (long)b) == 0 ? x : rot[r++]);
+  }
+  // 128-bit content key of the weight matrix (as weight_key for kernel tensors)
+  u64 h = 1469598103934665603ULL, g2 = 0x9E3779B97F4A7C15ULL;
+  for (std::size_t i = 0; i < m * n; ++i) {
+    u64 bits;
+    std::memcpy(&bits, w + i, 8);
+    h = (h ^ bits) * 1099511628211ULL;
+    g2 = mix64(g2 ^ (bits + 0x632BE59BD9B4E019ULL));
+  }
+  const std::string wk = "fcd:" + std::to_string(h) + ":" + std::to_string(g2) + ":" + std::to_string(m) + "x" +
+                         std::to_string(n);
+  const double ps = pt_scale_for(ctx, x);
+  std::vector<std::vector<Ciphertext>> terms;
+  std::vector<std::vector<BufPtr>> pts;
+  std::vector<long> gofs;
+  for (std::size_t g = 0; g < G; ++g) {
+    std::vector<Ciphertext> tg;
+    std::vector<BufPtr> pg;
+    for (std::size_t b = 0; b < n1 && g * n1 + b < D; ++b) {
+      const std::size_t k = g * n1 + b;
+      tg.push_back(baby[b]);
+      pg.push_back(ctx.weight_pt(wk + ":" + std::to_string(k), x.limbs, ps, [&] {
+        std::vector<double> v((std::size_t)S, 0.0);
+        for (std::size_t i = 0; i < m; ++i) {
+          const long c = (long)i + k0 + (long)k;
+          if (c >= 0 && c < (long)n) v[(std::size_t)norm((long)i + (long)(g * n1))] = w[i * n + (std::size_t)c];
+        }
+        return ctx.encode(v.data(), v.size(), x.limbs, ps);
+      }));
+    }
+    terms.push_back(tg);
+    pts.push_back(pg);
+    gofs.push_back((long)(g * n1));
+  }
+  const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, terms, pts);
+  RotTerms giants;
+  for (std::size_t g = 0; g < rows.size(); ++g) giants.push_back({rows[g], gofs[g]});
+  return rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+}
+}  // namespace
+
 Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std::size_t m, std::size_t B,
                            const double* w, const double* bias) {
   if (n == 0 || m == 0) throw shape_error("fully-connected layer needs positive input/output sizes");
   if (n > (std::size_t)ctx.S() || m > (std::size_t)ctx.S())
     throw capacity_error("fully-connected layer does not fit in the slot count");
   if (B == 0) throw shape_error("merge budget must be >= 1");
+  if (ctx.fast_schedule() && m >= 64 && n + m - 1 <= (std::size_t)ctx.S() && x.limbs >= 3) {
+    Ciphertext y = fc_diagonal(ctx, x, n, m, w);
+    // the reference's FC consumes two levels (row product + head mask); the diagonal
+    // form needs one, the second is an exact level drop so the ledger is unchanged
+    y = level_down(ctx, y, y.limbs - 1);
+    std::vector<double> b(m, 0.0);
+    if (bias) std::copy(bias, bias + m, b.begin());
+    return add_plain(ctx, y, b.data(), b.size());
+  }
   const std::size_t p2 = std::bit_ceil(n);
   std::vector<BufPtr> rows;
   rows.reserve(m);

@@ -226,6 +226,24 @@ def test_fully_connected(env, W, C, F, s):
     check(out, ev, r, f"fc n={n} m={m} B={B}", ctx.schedule())
 
 
+@pytest.mark.parametrize("n,m", [(256, 100), (128, 300), (400, 64)])
+def test_fully_connected_wide(env, n, m):
+    """Wide FC layers (m >= 64): under the fast schedule the generalised-diagonal
+    baby-step giant-step product (layers.cpp fc_diagonal).  Garbage in the input's
+    slots beyond n (post-ReLU p(0), say) must be ignored as the reference's row
+    products ignore it; output zeros beyond m; same two levels."""
+    ctx, ref = env
+    rng = np.random.default_rng(n + m)
+    S = ctx.slots()
+    x = rng.uniform(-1, 1, S)  # n inputs + garbage in [n, S)
+    w = rng.uniform(-1, 1, (m, n)) / np.sqrt(n)
+    b = rng.uniform(-1, 1, m)
+    out, ev, r = run_both(ctx, lambda v: fh.fully_connected(v, fh.FcConfig(n, m, 1), fh.FcWeights(w, b)),
+                          lambda v: ref.fully_connected(v, DEPTH, n, m, 1, w, b), x)
+    check(out, ev, r, f"fc wide n={n} m={m}", ctx.schedule())
+    assert np.abs(out.slots()[m:]).max() < 1e-3
+
+
 @pytest.mark.parametrize("W,C,F,s", cases(9007, 3))
 def test_pad_input(env, W, C, F, s):
     ctx, ref = env
