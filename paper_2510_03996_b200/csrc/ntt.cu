@@ -162,8 +162,12 @@ struct EpiArg<true> {
   using type = NttEpilogue;
 };
 
+#ifndef FHEON_NTT_OCC
+#define FHEON_NTT_OCC 1024  // resident threads per SM the register budget is sized for
+#endif
 template <int LOGM, bool INV, bool COL, bool SMALL, bool EPI = false>
-__global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS)
+__global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS,
+                                  FHEON_NTT_OCC / Geometry<LOGM, COL, SMALL>::THREADS)
     ntt_phase_kernel(LimbSet set, LimbSet src, bool has_src, const PrimeConst* __restrict__ pc,
                      const u64* __restrict__ tw, int logN, int n1, int n2, typename EpiArg<EPI>::type epi) {
   using G = Geometry<LOGM, COL, SMALL>;
