@@ -732,6 +732,7 @@ def model_runs(args):
                           M.calibrate_relu_scales(M.vgg16_paper(ring=65536, depth_budget=args.depth), calv), xv,
                           128, False))
     for name, spec, x, security, ref_schedule_only in cases:
+        fh.api.release_memory()  # each case starts from a trimmed pool (VGG-16's keys alone are ~90 GB)
         em = M.EncryptedModel(spec, security=security, schedule="reference" if ref_schedule_only else "fast")
         reps = 1 if ref_schedule_only else args.model_reps
         for _ in range(1 if ref_schedule_only else 3):  # warm-up: lazy keys, plaintext caches, pool growth
