@@ -101,6 +101,8 @@ class ClockSampler:
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        if os.environ.get("FHEON_NO_CLOCKS"):
+            return self
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
@@ -373,6 +375,7 @@ def rotation_bench(args):
         line["primitives"] = extras
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(args)
+    ctx.close()
     del cts, ctx
     fh.api.release_memory()
     return line
@@ -550,12 +553,14 @@ def run_ours(args):
         "roofline": roofline,
         "clocks": clk.summary(),
     }
+    for e in ems:  # the keys (~31 GB) must not outlive the headline: the model cases need the HBM
+        e.ctx.close()
     del em, ems, ctx, xin, xins, streams
     fh.api.release_memory()
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_reference(spec, x, depth)
         line["logits_max_abs_err_vs_reference"] = line["cpu_baseline"].pop("_logit_err_fn")(logits_dev)
-    if not args.quick:
+    if not args.quick and not args.no_rotations:
         rot = rotation_bench(args)
         if rank == 0:
             line["rotations"] = rot
@@ -683,15 +688,64 @@ def primitives(ctx, fh):
     return out
 
 
-def model_runs(args):
-    """Encrypted inference s/image of the other BASELINE networks and chains through
-    the model runtime (host image -> encrypt -> every layer and bootstrap on the
-    GPU -> decrypt), with the decrypted logits compared against the reference's
-    own infer() on the same spec / weights / input (timed beside it on one core)
-    and the chain's security disclosure.  Chains that cannot reach 128 bits (the
-    reference's presets: depth 25 at N = 2^14 / 2^15; LeNet-5 at configs[2]'s
-    N = 2^15, where bootstrapping alone needs more modulus than the 881-bit
-    bound) run with security=0 and say so."""
+def model_cases(args, want=None):
+    """The model cases of the bench: (name, spec, input, security, reference-schedule-only).
+    Encrypted inference s/image of the other BASELINE networks and chains through the
+    model runtime (host image -> encrypt -> every layer and bootstrap on the GPU ->
+    decrypt), with the decrypted logits compared against the reference's own infer()
+    on the same spec / weights / input (timed beside it on one core) and the chain's
+    security disclosure.  Chains that cannot reach 128 bits (the reference's presets:
+    depth 25 at N = 2^14 / 2^15; LeNet-5 at configs[2]'s N = 2^15, where bootstrapping
+    alone needs more modulus than the 881-bit bound) run with security=0 and say so.
+    want: build only that case (the others are returned as names with None)."""
+    import tempfile
+    from paper_2510_03996_b200 import model as M
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from model_files import materialize
+
+    def norm(x):
+        return (x - 0.5) / 0.2887
+
+    def lenet_ref():
+        spec = M.load_spec(materialize("lenet5", tempfile.mkdtemp(), seed=9))
+        spec = M.calibrate_relu_scales(spec, [np.random.default_rng(500 + i).uniform(0, 1, (1, 28, 28))
+                                              for i in range(4)])
+        return spec, np.random.default_rng(501).uniform(0, 1, (1, 28, 28))
+
+    def resnet_cal():
+        return [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
+
+    xl = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
+    builders = [("lenet5_configs2_n15_d25", lambda: (M.lenet5(ring=32768, depth_budget=25), xl), 0, False),
+                ("lenet5_n16_d10_128bit", lambda: (M.lenet5(ring=65536, depth_budget=10), xl), 128, False),
+                ("lenet5_reference_spec", lenet_ref, 0, False)]
+    if not args.no_resnet:
+        if not args.no_reference_schedule:
+            builders.append((f"resnet20_n16_d{args.depth}_128bit_reference_schedule", lambda: head_spec(args.depth),
+                             128, True))
+        builders.append(("resnet20_reference_spec", lambda: (M.calibrate_relu_scales(
+            M.load_spec(materialize("resnet20", tempfile.mkdtemp(), seed=9)), resnet_cal()), head_spec(args.depth)[1]),
+            0, False))
+        builders.append(("resnet20_n16_d25_insecure", lambda: (M.calibrate_relu_scales(
+            M.resnet20(ring=65536, depth_budget=25), resnet_cal()), head_spec(args.depth)[1]), 0, False))
+        if not args.no_vgg:
+            builders.append(("vgg16_paper_widths_n16_128bit", lambda: (M.calibrate_relu_scales(
+                M.vgg16_paper(ring=65536, depth_budget=args.depth),
+                [norm(np.random.default_rng(5002 + i).uniform(0, 1, (3, 32, 32))) for i in range(4)]),
+                norm(np.random.default_rng(5001).uniform(0, 1, (3, 32, 32)))), 128, False))
+    cases = []
+    for name, build_fn, security, ref_only in builders:
+        if want is not None and name != want:
+            cases.append((name, None, None, security, ref_only))
+            continue
+        spec, x = build_fn()
+        cases.append((name, spec, x, security, ref_only))
+    return cases
+
+
+def run_model_case(args, case):
+    """One model case (built by model_cases) timed in THIS process: encrypted s/image with
+    clocks sampled, the logit error against the reference's infer(), key residency."""
     import tempfile
     import paper_2510_03996_b200 as fh
     from paper_2510_03996_b200 import model as M
@@ -700,91 +754,88 @@ def model_runs(args):
         have_ref = sref.available()
     except Exception:
         have_ref = False
-
-    def norm(x):
-        return (x - 0.5) / 0.2887
-
-    out = {}
-    xl = np.random.default_rng(3001).uniform(0, 1, (1, 28, 28))
-    # name, spec, input, security, also time the reference's exact rotation schedule
-    cases = [("lenet5_configs2_n15_d25", M.lenet5(ring=32768, depth_budget=25), xl, 0, False),
-             ("lenet5_n16_d10_128bit", M.lenet5(ring=65536, depth_budget=10), xl, 128, False)]
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from model_files import materialize
-    refspec = M.load_spec(materialize("lenet5", tempfile.mkdtemp(), seed=9))
-    refspec = M.calibrate_relu_scales(refspec, [np.random.default_rng(500 + i).uniform(0, 1, (1, 28, 28))
-                                                for i in range(4)])
-    cases.append(("lenet5_reference_spec", refspec, np.random.default_rng(501).uniform(0, 1, (1, 28, 28)), 0,
-                  False))
-    if not args.no_resnet:
-        spec, xr = head_spec(args.depth)
-        if not args.no_reference_schedule:
-            cases.append((f"resnet20_n16_d{args.depth}_128bit_reference_schedule", spec, xr, 128, True))
-        cal = [norm(np.random.default_rng(4002 + i).uniform(0, 1, (3, 32, 32))) for i in range(6)]
-        refspec = M.calibrate_relu_scales(M.load_spec(materialize("resnet20", tempfile.mkdtemp(), seed=9)), cal)
-        cases.append(("resnet20_reference_spec", refspec, xr, 0, False))
-        cases.append(("resnet20_n16_d25_insecure", M.calibrate_relu_scales(M.resnet20(ring=65536, depth_budget=25),
-                                                                           cal), xr, 0, False))
-        if not args.no_vgg and hasattr(M, "vgg16_paper"):
-            xv = norm(np.random.default_rng(5001).uniform(0, 1, (3, 32, 32)))
-            calv = [norm(np.random.default_rng(5002 + i).uniform(0, 1, (3, 32, 32))) for i in range(4)]
-            cases.append(("vgg16_paper_widths_n16_128bit",
-                          M.calibrate_relu_scales(M.vgg16_paper(ring=65536, depth_budget=args.depth), calv), xv,
-                          128, False))
-    for name, spec, x, security, ref_schedule_only in cases:
-        fh.api.release_memory()  # each case starts from a trimmed pool (VGG-16's keys alone are ~90 GB)
-        em = M.EncryptedModel(spec, security=security, schedule="reference" if ref_schedule_only else "fast")
-        reps = 1 if ref_schedule_only else args.model_reps
-        for _ in range(1 if ref_schedule_only else 3):  # warm-up: lazy keys, plaintext caches, pool growth
-            em.infer(x)
-        times = []
+    name, spec, x, security, ref_schedule_only = case
+    em = M.EncryptedModel(spec, security=security, schedule="reference" if ref_schedule_only else "fast")
+    reps = 1 if ref_schedule_only else args.model_reps
+    for _ in range(1 if ref_schedule_only else 3):  # warm-up: lazy keys, plaintext caches, pool growth
+        em.infer(x)
+    times = []
+    with ClockSampler(0) as clk:
         for _ in range(reps):
             r = em.infer(x)
             times.append(r.wall_ms / 1e3)
-        rec = {"s_per_image": round(float(np.median(times)), 4), "reps": reps,
-               "schedule": "reference (the reference's exact rotation sequence)" if ref_schedule_only else "fast",
-               "rep_times_s": [round(t, 4) for t in times],
-               "spec": ("the reference's models/%s.json (preset, seeded weights)" % name.split("_")[0]
-                        if name.endswith("reference_spec") else "paper_2510_03996_b200.model." + name.split("_")[0]),
-               "ring_dimension": spec.ring_dimension, "depth_budget": spec.depth_budget, "security": em.security,
-               "limbs": em.ctx.L, "special_limbs": em.ctx.K, "dnum": em.ctx.dnum, "bootstraps": em.n_boot,
-               "rotations": r.stats["rotations"], "keyswitches": r.stats["keyswitches"],
-               "gpu_launches": r.stats["launches"], "key_bytes": em.ctx.key_bytes(),
-               "data": "synthetic seeded input, seeded random weights (no datasets/weights in the container)"}
-        if name == "resnet20_reference_spec":
-            # keyplan block mode (model_run.cpp:150 key_mode): keys of one block resident at a time
-            preload_key_bytes = em.ctx.key_bytes()
-            em.infer(x, key_mode="block")
-            rb = em.infer(x, key_mode="block", verify_keys=True)
-            est = M.keyplan.estimate_memory(rb.plan, em.memory_model())
-            ref_est = M.keyplan.estimate_memory(rb.plan, M.keyplan.MemoryModel.reference_model(
-                spec.ring_dimension, spec.depth_budget, 3))
-            # the same plan with the keys streamed from pinned host memory (packed wire format,
-            # upload stream) instead of regenerated: the PCIe key traffic is inside s/image
-            em.enable_key_streaming()
-            em.infer(x, key_mode="block")
-            rs = em.infer(x, key_mode="block", verify_keys=True)
-            rec["key_mode_block_streamed"] = {
-                "s_per_image": round(rs.wall_ms / 1e3, 4), "keys_uploaded_per_image": rs.key_residency["uploaded"],
-                "key_bytes_uploaded_per_image": rs.key_residency["uploaded_bytes"],
-                "keys_generated_per_image": rs.key_residency["generated"], "trace_check_ok": rs.trace_check.ok(),
-                "pcie_gbs_implied": round(rs.key_residency["uploaded_bytes"] / (rs.wall_ms / 1e3) / 1e9, 2)}
-            rec["key_mode_block"] = {
-                "s_per_image": round(rb.wall_ms / 1e3, 4), "blocks": len(rb.plan.blocks),
-                "trace_check_ok": rb.trace_check.ok(), "rotations_checked": rb.trace_check.rotations_checked,
-                "keys_generated_per_image": rb.key_residency["generated"],
-                "peak_key_bytes": rb.key_residency["peak_key_bytes"], "preload_key_bytes": preload_key_bytes,
-                "estimate": {"total_keys": est.total_keys, "peak_resident_keys": est.resident_keys,
-                             "preload_bytes": est.preload_bytes, "peak_bytes": est.peak_bytes,
-                             "reference_memory_model_preload_bytes": ref_est.preload_bytes}}
-        if have_ref:
-            path = spec.write(tempfile.mkdtemp())
-            rl, rows, _, rwall = sref.infer(path, x)
-            rec["max_abs_logit_err_vs_reference"] = float(np.abs(r.logits - rl).max())
-            rec["argmax_match"] = bool(int(np.argmax(r.logits)) == int(np.argmax(rl)))
-            rec["reference_sim_s_per_image_1core"] = round(rwall / 1e3, 4)
-        del em
-        out[name] = rec
+    rec = {"s_per_image": round(float(np.median(times)), 4), "reps": reps,
+           "schedule": "reference (the reference's exact rotation sequence)" if ref_schedule_only else "fast",
+           "rep_times_s": [round(t, 4) for t in times],
+           "spec": ("the reference's models/%s.json (preset, seeded weights)" % name.split("_")[0]
+                    if name.endswith("reference_spec") else "paper_2510_03996_b200.model." + name.split("_")[0]),
+           "ring_dimension": spec.ring_dimension, "depth_budget": spec.depth_budget, "security": em.security,
+           "limbs": em.ctx.L, "special_limbs": em.ctx.K, "dnum": em.ctx.dnum, "bootstraps": em.n_boot,
+           "rotations": r.stats["rotations"], "keyswitches": r.stats["keyswitches"],
+           "gpu_launches": r.stats["launches"], "key_bytes": em.ctx.key_bytes(), "clocks": clk.summary(),
+           "data": "synthetic seeded input, seeded random weights (no datasets/weights in the container)"}
+    if name == "resnet20_reference_spec":
+        # keyplan block mode (model_run.cpp:150 key_mode): keys of one block resident at a time
+        preload_key_bytes = em.ctx.key_bytes()
+        em.infer(x, key_mode="block")
+        rb = em.infer(x, key_mode="block", verify_keys=True)
+        est = M.keyplan.estimate_memory(rb.plan, em.memory_model())
+        ref_est = M.keyplan.estimate_memory(rb.plan, M.keyplan.MemoryModel.reference_model(
+            spec.ring_dimension, spec.depth_budget, 3))
+        # the same plan with the keys streamed from pinned host memory (packed wire format,
+        # upload stream) instead of regenerated: the PCIe key traffic is inside s/image
+        em.enable_key_streaming()
+        em.infer(x, key_mode="block")
+        rs = em.infer(x, key_mode="block", verify_keys=True)
+        rec["key_mode_block_streamed"] = {
+            "s_per_image": round(rs.wall_ms / 1e3, 4), "keys_uploaded_per_image": rs.key_residency["uploaded"],
+            "key_bytes_uploaded_per_image": rs.key_residency["uploaded_bytes"],
+            "keys_generated_per_image": rs.key_residency["generated"], "trace_check_ok": rs.trace_check.ok(),
+            "pcie_gbs_implied": round(rs.key_residency["uploaded_bytes"] / (rs.wall_ms / 1e3) / 1e9, 2)}
+        rec["key_mode_block"] = {
+            "s_per_image": round(rb.wall_ms / 1e3, 4), "blocks": len(rb.plan.blocks),
+            "trace_check_ok": rb.trace_check.ok(), "rotations_checked": rb.trace_check.rotations_checked,
+            "keys_generated_per_image": rb.key_residency["generated"],
+            "peak_key_bytes": rb.key_residency["peak_key_bytes"], "preload_key_bytes": preload_key_bytes,
+            "estimate": {"total_keys": est.total_keys, "peak_resident_keys": est.resident_keys,
+                         "preload_bytes": est.preload_bytes, "peak_bytes": est.peak_bytes,
+                         "reference_memory_model_preload_bytes": ref_est.preload_bytes}}
+    if have_ref:
+        path = spec.write(tempfile.mkdtemp())
+        rl, rows, _, rwall = sref.infer(path, x)
+        rec["max_abs_logit_err_vs_reference"] = float(np.abs(r.logits - rl).max())
+        rec["argmax_match"] = bool(int(np.argmax(r.logits)) == int(np.argmax(rl)))
+        rec["reference_sim_s_per_image_1core"] = round(rwall / 1e3, 4)
+    del em
+    return rec
+
+
+def model_runs(args):
+    """Every model case in a FRESH process (`bench.py --model-case NAME`): each starts from
+    an empty device and pool, as a deployment running that model would -- one
+    process's earlier workloads measurably slowed later ones (VGG-16 0.70 s alone,
+    1.1 s after the headline section in the same process)."""
+    out = {}
+    try:
+        import torch
+        free, total = torch.cuda.mem_get_info()
+        out["_parent_device_memory_free_gb"] = round(free / 1e9, 1)
+    except Exception:
+        pass
+    names = [c[0] for c in model_cases(args, want="")]
+    only = [c for c in (args.models or "").split(",") if c]
+    for name in names:
+        if only and not any(name.startswith(c) for c in only):
+            continue
+        cmd = [sys.executable, os.path.abspath(__file__), "--model-case", name, "--depth", str(args.depth),
+               "--model-reps", str(args.model_reps)]
+        if args.no_reference_schedule:
+            cmd.append("--no-reference-schedule")
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        try:
+            out[name] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception:
+            out[name] = {"error": (r.stderr or r.stdout)[-800:]}
     return out
 
 
@@ -891,12 +942,21 @@ def main():
     ap.add_argument("--no-vgg", action="store_true", help="skip VGG-16")
     ap.add_argument("--depth", type=int, default=HEAD_DEPTH, help="ResNet-20 depth budget of the headline chain")
     ap.add_argument("--in-flight", type=int, default=2, help="images in flight per GPU (key-sharing contexts)")
+    ap.add_argument("--models", default="", help="comma-separated name prefixes of the model cases to run")
+    ap.add_argument("--no-rotations", action="store_true", help="skip the configs[1] rotation block")
+    ap.add_argument("--model-case", default="", help=argparse.SUPPRESS)
     ap.add_argument("--model-reps", type=int, default=3)
     ap.add_argument("--no-reference-schedule", action="store_true",
                     help="skip the models' reference-rotation-schedule timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.model_case:
+        case = [c for c in model_cases(args, want=args.model_case) if c[0] == args.model_case]
+        if not case:
+            raise SystemExit(f"unknown model case {args.model_case}")
+        print(json.dumps(run_model_case(args, case[0])), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -280,6 +280,11 @@ class SlotContext:
         return SlotContext(self.config, _share_keys_from=self)
 
     def __del__(self):
+        self.close()
+
+    def close(self):
+        """Destroy the engine context now (keys, pools, caches) instead of at garbage
+        collection; ciphertexts of this context must not be used afterwards."""
         h = getattr(self, "_h", None)
         if h:
             try:
