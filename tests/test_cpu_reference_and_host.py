@@ -238,3 +238,53 @@ def test_integration_seam_links_the_engine_not_the_simulator():
     for fn in ("fheon_rotate", "fheon_mult_cipher", "fheon_bootstrap", "fheon_ctx_create"):
         assert fn in undefined, fn
     assert "slotcnn::SlotVector::slots() const" in defined  # decrypt-on-read (backend_b200.cpp)
+
+
+def test_he_standard_table_and_chain_properties():
+    """The HE-standard bounds the engine enforces (homomorphicencryption.org 2018 Table 1,
+    ternary, classical; 2^16 as OpenFHE ships it), and the 128-bit chains the model
+    runtime builds: dense secret, encapsulation h_b = 32 with EvalMod range 12 (a
+    15-level bootstrap), log2 QP under the bound, the fewest digits that fit."""
+    from paper_2510_03996_b200 import model as M
+    for logn, bound in ((14, 438), (15, 881), (16, 1747)):
+        cfg = fh.ContextConfig(1 << logn, 1 << (logn - 1), 5, fh.CryptoMetadata(50, 40, 3), limbs=6,
+                               special_limbs=2, allow_insecure=True)
+        assert fh.host_security(cfg)["he_standard_128_bound"] == bound
+    prev_dnum = None
+    for depth in (9, 10, 11, 12):
+        cfg = M.ckks_config(M.resnet20(ring=65536, depth_budget=depth), True)
+        sec = fh.host_security(cfg)
+        assert sec["meets_128"] and sec["log2_qp"] <= 1747
+        assert cfg.hamming_weight == 0 and cfg.boot_hamming_weight == 32 and cfg.boot_k_range == 12
+        assert fh.host_bootstrap_depth(cfg) == 15 and cfg.limbs == depth + 1 + 15
+        prev_dnum = cfg.crypto.key_switch_digits
+    assert prev_dnum is not None
+
+
+def test_oracle_encapsulation_keys_structure():
+    """The oracle's restatement of the sparse-secret encapsulation keys: key 2 (s -> s_b)
+    exists only on digit 0's q_0 limb and the special primes, and switching a level-0
+    ciphertext with it and back (key 4 at level 0) preserves the decryption."""
+    o = Oracle(12, 6, 2, 3, 50, 40, 60, 9)
+    o.set_boot_secret(32)
+    k2, k4 = o.keygen(2), o.keygen(4)
+    assert not k2[1:].any() and not k2[0, :, 1:6].any() and k2[0, :, 0].any() and k2[0, :, 6:].any()
+    assert k4[0, :, 0].any() and k4[2].any()
+    rng = np.random.default_rng(2)
+    v = rng.uniform(-1, 1, o.S)
+    ct = o.encrypt(v, 0)
+    c1 = np.ascontiguousarray(ct[:, :1])
+    ks0, ks1 = o.keyswitch(np.ascontiguousarray(c1[1]), k2, 1)  # now under s_b
+    y = np.stack([(c1[0].astype(object) + ks0.astype(object)) % int(o.primes[0]), ks1.astype(object)])
+    y = np.ascontiguousarray(y.astype(np.uint64))
+    back0, back1 = o.keyswitch(np.ascontiguousarray(y[1]), k4, 1)  # s_b -> s
+    z = np.stack([(y[0].astype(object) + back0.astype(object)) % int(o.primes[0]), back1.astype(object)])
+    z = np.ascontiguousarray(z.astype(np.uint64))
+    assert np.abs(o.decrypt(z, float(o.T[0])) - o.decrypt(c1, float(o.T[0]))).max() < 1e-6
+
+
+def test_bench_arms_print_the_same_config():
+    """The two bench arms' `config` dicts are built by one function (same_config)."""
+    import bench
+    assert bench.head_config(11) == bench.head_config(11)
+    assert bench.head_config(11)["workload"].startswith("configs[3]")
