@@ -73,6 +73,9 @@ typedef struct {
   /* levels of the bootstrapping linear transforms (0 = 3 each): CoeffsToSlots, SlotsToCoeffs */
   int boot_cts_levels;
   int boot_stc_levels;
+  /* sparse-slot bootstrapping variants over n = S/2, S/4, ..., S/2^boot_sparse slots, built at
+   * context creation (their rotation keys join the pinned set); fheon_bootstrap_active picks one */
+  int boot_sparse;
 } fheon_params;
 
 /* ---- errors / version */
@@ -230,6 +233,11 @@ int fheon_add_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, siz
 int fheon_mult_plain(fheon_ctx* ctx, const fheon_ct* a, const double* values, size_t n, fheon_ct** out);
 int fheon_mult_cipher(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheon_ct** out);
 int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out);
+/* bootstrap() when only slots [0, active_slots) matter (a packed tensor's active region): runs the
+ * smallest sparse-slot variant (fheon_params.boot_sparse) holding them -- the input must sit above
+ * level 0, its last level takes the mask -- else the full pipeline.  Same level accounting and
+ * trace event as fheon_bootstrap; output slots [0, active_slots) = input, the rest 0 (sparse) */
+int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, fheon_ct** out);
 /* bootstrapping stage probes (tests): 1 CoeffsToSlots, 2 EvalMod, 3 SlotsToCoeffs, 4 ModRaise;
  * info (may be NULL): [depth, k_range, double_angles, stc_input_limbs] */
 int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out);

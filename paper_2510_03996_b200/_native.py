@@ -39,6 +39,7 @@ class fheon_params(C.Structure):
         ("boot_k_range", C.c_int),
         ("boot_cts_levels", C.c_int),
         ("boot_stc_levels", C.c_int),
+        ("boot_sparse", C.c_int),
     ]
 
 
@@ -137,6 +138,7 @@ SIGNATURES = {
     "fheon_mult_plain": (C.c_int, [vp, vp, dp, C.c_size_t, pp]),
     "fheon_mult_cipher": (C.c_int, [vp, vp, vp, pp]),
     "fheon_bootstrap": (C.c_int, [vp, vp, pp]),
+    "fheon_bootstrap_active": (C.c_int, [vp, vp, C.c_size_t, pp]),
     "fheon_bootstrap_stage": (C.c_int, [vp, vp, C.c_int, pp]),
     "fheon_bootstrap_info": (C.c_int, [vp, C.POINTER(C.c_int), dp, C.c_size_t, szp]),
     "fheon_rescale": (C.c_int, [vp, vp, pp]),

@@ -137,6 +137,9 @@ class ContextConfig:
     # levels of the bootstrapping linear transforms (0 = 3 each)
     boot_cts_levels: int = 0
     boot_stc_levels: int = 0
+    # sparse-slot bootstrapping variants over S/2, ..., S/2^boot_sparse slots (0 = none;
+    # bootstrap(v, active_slots) uses them)
+    boot_sparse: int = 0
     # layer rotation schedule: "fast" (hoisted / log-depth / baby-step giant-step,
     # same values and levels) or "reference" (the reference's exact rotation trace)
     schedule: str = "fast"
@@ -203,6 +206,7 @@ class ContextConfig:
         p.boot_k_range = int(self.boot_k_range)
         p.boot_cts_levels = int(self.boot_cts_levels)
         p.boot_stc_levels = int(self.boot_stc_levels)
+        p.boot_sparse = int(self.boot_sparse)
         return p
 
 
@@ -702,8 +706,13 @@ def mult_cipher(a: SlotVector, b: SlotVector) -> SlotVector:
     return _wrap(a._ctx, _native.lib().fheon_mult_cipher, a._h, b._h)
 
 
-def bootstrap(a: SlotVector) -> SlotVector:
-    return _wrap(a._ctx, _native.lib().fheon_bootstrap, a._h)
+def bootstrap(a: SlotVector, active_slots: Optional[int] = None) -> SlotVector:
+    """backend.cpp:233-249: refresh to the depth budget.  With `active_slots`, only
+    slots [0, active_slots) are kept (a sparse-slot variant when the context has
+    one that fits and the input sits above level 0; the rest become 0)."""
+    if active_slots is None:
+        return _wrap(a._ctx, _native.lib().fheon_bootstrap, a._h)
+    return _wrap(a._ctx, _native.lib().fheon_bootstrap_active, a._h, int(active_slots))
 
 
 def bootstrap_stage(a: SlotVector, stage: int) -> SlotVector:

@@ -205,8 +205,10 @@ BootParams boot_params_of(const Params& p) {
 Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(bp) {
   const HostTables& h = ctx.host();
   S_ = h.S;
+  n_ = bp.log_slots > 0 ? (1L << bp.log_slots) : (long)S_;
+  if (n_ > S_ || n_ < 4) throw Error(ErrKind::shape, "bootstrapping: sparse slot count must lie in [4, S]");
   const int L = h.p.L;
-  const long logS = ilog2(S_);
+  const long logS = ilog2(n_);
   const double K1 = bp.k_range + 1.0;
   const int r = bp.double_angles;
   const int deg = bp.cos_degree > 0 ? bp.cos_degree : evalmod_degree(bp.k_range, r);
@@ -222,29 +224,41 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
     for (int i = 0; i < (int)(logS % levels); ++i) sizes[i]++;
     return sizes;
   };
-  // CoeffsToSlots: inverse stages len = S .. 2 (first applied first)
+  // CoeffsToSlots: inverse stages len = n .. 2 (first applied first).  Sparse: the
+  // smaller group first (fewer diagonals on the top level, and the lower groups
+  // then hold the same stages as the full pipeline's)
+  const long g = S_ / n_;
   {
     std::vector<int> sizes = split(bp.cts_levels);
+    if (sparse()) std::reverse(sizes.begin(), sizes.end());
     std::vector<Mat> groups;
     // 1 / (2 (K + 1)) spread evenly over the levels -- or, when the first level's
     // plaintexts (scale T_{L-2} q_{L-1} / q_0, about 2^65 on 60-bit bootstrapping
-    // levels) would overflow the encoder's 2^62, all on the first level
+    // levels) would overflow the encoder's 2^62, all on the first level.  Sparse:
+    // the trace's factor g is divided out on the first level too
     const double first_pt_scale = h.T[L - 2] * (double)h.q[L - 1] / (double)h.q[0];
     const double c_even = std::pow(1.0 / (2.0 * K1), 1.0 / bp.cts_levels);
     const bool front = first_pt_scale * c_even > std::ldexp(1.0, 60);
-    long len = S_;
+    long len = n_;
     for (int gsz : sizes) {
       Mat M = stage((int)len, true);
       len /= 2;
       for (int i = 1; i < gsz; ++i, len /= 2) M = mul(stage((int)len, true), M);
-      const double c = front ? (groups.empty() ? 1.0 / (2.0 * K1) : 1.0) : c_even;
+      double c = front ? (groups.empty() ? 1.0 / (2.0 * K1) : 1.0) : c_even;
+      if (groups.empty()) c /= (double)g;
       for (auto& [d, v] : M)
         for (auto& x : v) x *= c;
       groups.push_back(M);
     }
+    if (sparse()) {  // pack: slots k mod 2n < n keep z, the others take -i z (v + conj v = [2 Re | 2 Im])
+      Diag dv(S_);
+      for (long k = 0; k < S_; ++k) dv[k] = (k % (2 * n_)) < n_ ? std::complex<double>(1.0, 0.0)
+                                                                : std::complex<double>(0.0, -1.0);
+      groups.back() = mul(Mat{{0, dv}}, groups.back());
+    }
     cts_ = plan(groups, L, (double)h.q[0]);
   }
-  // SlotsToCoeffs: forward stages len = 2 .. S, scaled by q0 / (2 pi Delta_0)
+  // SlotsToCoeffs: forward stages len = 2 .. n, scaled by q0 / (2 pi Delta_0)
   {
     std::vector<int> sizes = split(bp.stc_levels);
     std::vector<Mat> groups;
@@ -258,10 +272,25 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
         for (auto& x : v) x *= c;
       groups.push_back(M);
     }
+    if (sparse()) {
+      // unpack: z_k = w_k + i w_{k+n} (k mod 2n < n), w_{k-n} + i w_k (otherwise)
+      Diag da(S_), db(S_);
+      for (long k = 0; k < S_; ++k) {
+        const bool lo = (k % (2 * n_)) < n_;
+        da[k] = lo ? std::complex<double>(1.0, 0.0) : std::complex<double>(0.0, 1.0);
+        db[k] = lo ? std::complex<double>(0.0, 1.0) : std::complex<double>(1.0, 0.0);
+      }
+      groups.front() = mul(groups.front(), Mat{{0, da}, {signed_off(n_, S_), db}});
+      Diag mask(S_);
+      for (long k = 0; k < S_; ++k) mask[k] = k < n_ ? 1.0 : 0.0;
+      groups.back() = mul(Mat{{0, mask}}, groups.back());
+    }
     const int stc_limbs = L - bp.cts_levels - cheb_eval_depth(deg) - r;
     stc_limbs_ = stc_limbs;
     stc_ = plan(groups, stc_limbs, h.T[stc_limbs - 1]);
   }
+  if (sparse())
+    for (long j = 1; j < g; ++j) sub_steps_.push_back(j * n_);
   for (long s : rotation_steps()) {  // a server context (no secret) receives them by upload
     if (ctx.has_secret() && !ctx.inheriting_keys) ctx.gen_key(ctx.galois(s));
     ctx.pin_key(ctx.galois(s));
@@ -282,6 +311,7 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
 
 std::vector<long> Bootstrapper::rotation_steps() const {
   std::set<long> s;
+  for (long t : sub_steps_) s.insert(t);
   for (const auto* v : {&cts_, &stc_})
     for (const Level& lv : *v) {
       for (long b : lv.babies) s.insert(b);
@@ -354,11 +384,52 @@ Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {
   throw Error(ErrKind::internal, "debug_stage: unknown stage");
 }
 
+Ciphertext Bootstrapper::subsum(const Ciphertext& x) {
+  if (sub_steps_.empty()) return x;
+  std::vector<std::pair<Ciphertext, long>> terms = {{x, 0}};
+  for (long t : sub_steps_) terms.push_back({x, t});
+  return rotate_sum_many(ctx_, {terms})[0];
+}
+
 Ciphertext Bootstrapper::run(const Ciphertext& x0) {
   const bool tracing = ctx_.tracing();
   ctx_.set_tracing(false);
   try {
     const HostTables& h = ctx_.host();
+    if (sparse()) {
+      if (x0.limbs < 2)
+        throw Error(ErrKind::internal, "sparse-slot bootstrapping needs an input above level 0 (the mask)");
+      // mask to [0, n) on the last level, replicate n-periodically, raise, trace
+      Ciphertext x = x0.limbs > 2 ? level_down(ctx_, x0, 2) : x0;
+      const long n = n_, S = S_;
+      BufPtr mask = ctx_.encode_named("boot_mask_" + std::to_string(n),
+                                      [n, S] {
+                                        std::vector<double> m((std::size_t)S, 0.0);
+                                        std::fill(m.begin(), m.begin() + n, 1.0);
+                                        return m;
+                                      },
+                                      x.limbs, pt_scale_for(ctx_, x));
+      x = mac_plain_many(ctx_, {{x}}, {{mask}})[0];
+      x = subsum(x);
+      const double corr = x.scale / h.T[0];
+      Ciphertext y = subsum(mod_raise(ctx_, x));
+      for (const Level& lv : cts_) y = apply(y, lv);
+      std::vector<Ciphertext> ys = {add(ctx_, y, conjugate_many(ctx_, {y})[0])};
+      ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
+      for (int i = 0; i < bp_.double_angles; ++i) {
+        std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
+        ys = add_many(ctx_, sq, sq);
+        for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
+      }
+      Ciphertext z = ys[0];
+      for (const Level& lv : stc_) z = apply(z, lv);
+      z.scale *= corr;
+      if (z.level() > ctx_.depth_budget()) z = level_down(ctx_, z, ctx_.depth_budget() + 1);
+      ctx_.set_tracing(tracing);
+      ctx_.record(3, z.level());
+      ctx_.stats.bootstraps++;
+      return z;
+    }
     Ciphertext x = x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0;
     const double corr = x.scale / h.T[0];
     static const bool dbg = std::getenv("FHEON_BOOT_DEBUG") != nullptr;

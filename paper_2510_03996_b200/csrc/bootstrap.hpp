@@ -17,6 +17,20 @@
 //   SlotsToCoeffs  U (stages F_2 .. F_S), with q0 / (2 pi Delta_0) folded in
 //
 // The output lands on the context's depth budget with the input's slot values.
+//
+// Sparse-slot variant (BootParams::log_slots = log2 n, n < S): for inputs whose
+// slots [n, S) carry nothing the caller needs (a packed tensor's inactive
+// region).  The input is masked to [0, n) on its last level and replicated
+// n-periodically (one hoisted rotate-and-sum at one limb), so its plaintext
+// lies in the subring Z[X^{S/n}]; after ModRaise the same rotate-and-sum over
+// the raised ciphertext (the trace to the subring, divided by g = S/n inside
+// CtS) projects q0 I there as well.  CtS and StC then run the n-point special
+// FFT (stages n..2 / 2..n: fewer diagonals), the real and imaginary halves of
+// the 2n coefficients are packed into ONE real ciphertext (D = [1 | -i] folded
+// into CtS's last factor, one conjugation), so EvalMod runs once instead of
+// twice, and StC's first factor unpacks them (P = [1 | i] + [i | 1] rot_n) while
+// its last factor masks the output to [0, n).  Same levels as the full
+// pipeline; output slots [0, n) = input, [n, S) = 0.
 #pragma once
 
 #include <complex>
@@ -36,6 +50,7 @@ struct BootParams {
   // linear transforms double-hoisted (babies kept over Q u P, one ModDown per
   // giant); env FHEON_BOOT_DH=0 selects the single-hoisted schedule for A/B runs
   bool double_hoist = true;
+  int log_slots = 0;      // sparse-slot variant over n = 2^log_slots < S slots (0: full)
 };
 
 BootParams boot_params_of(const Params& p);
@@ -45,7 +60,10 @@ class Bootstrapper {
   Bootstrapper(Context& ctx, const BootParams& bp = {});
   // levels consumed between ModRaise (top) and the output
   int depth() const { return depth_; }
+  // full: any level; sparse: x must hold >= 2 limbs (the mask takes one level)
   Ciphertext run(const Ciphertext& x);
+  long slots() const { return n_; }
+  bool sparse() const { return n_ < S_; }
   // stage probes for tests: 1 CoeffsToSlots on x (scale reinterpreted as q0),
   // 2 EvalMod of x (slots u -> sin(2 pi (K+1) u)), 3 SlotsToCoeffs on x,
   // 4 ModRaise of x
@@ -72,10 +90,14 @@ class Bootstrapper {
   Mat mul(const Mat& A, const Mat& B) const;
   std::vector<Level> plan(const std::vector<Mat>& groups, int limbs_in, double scale_in);
   Ciphertext apply(const Ciphertext& x, const Level& lv);
+  // sum_{j < S/n} rot(x, j n): one hoisted rotate-and-sum
+  Ciphertext subsum(const Ciphertext& x);
 
   Context& ctx_;
   BootParams bp_;
   int S_ = 0;
+  long n_ = 0;  // slots the pipeline carries (S_ for the full variant)
+  std::vector<long> sub_steps_;  // sparse: the trace rotations j n, 0 < j < S / n
   int depth_ = 0;
   int stc_limbs_ = 0;
   std::vector<Level> cts_, stc_;

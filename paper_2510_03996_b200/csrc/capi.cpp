@@ -74,6 +74,7 @@ static fheon::Params to_params(const fheon_params* p) {
   if (p->boot_k_range > 0) prm.boot_k_range = p->boot_k_range;
   if (p->boot_cts_levels > 0) prm.boot_cts_levels = p->boot_cts_levels;
   if (p->boot_stc_levels > 0) prm.boot_stc_levels = p->boot_stc_levels;
+  prm.boot_sparse = p->boot_sparse > 0 ? p->boot_sparse : 0;
   return prm;
 }
 
@@ -536,6 +537,9 @@ int fheon_mult_cipher(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheo
 }
 int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::bootstrap(*ctx->impl, a->ct)); });
+}
+int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::bootstrap_active(*ctx->impl, a->ct, active_slots)); });
 }
 int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out) {
   return guard([&] {

@@ -298,6 +298,13 @@ Context::Context(const Params& p, const Context* parent) : ht_(make_tables(p)) {
     else if (p.depth_budget > after)
       throw Error(ErrKind::shape, "depth budget " + std::to_string(p.depth_budget) +
                                       " exceeds the levels left after bootstrapping (" + std::to_string(after) + ")");
+    for (int k = 1; k <= p.boot_sparse && (ht_.S >> k) >= 4; ++k) {
+      BootParams bp = boot_params_of(p);
+      int ls = 0;
+      while ((1L << ls) < (long)(ht_.S >> k)) ++ls;
+      bp.log_slots = ls;
+      boot_sparse.push_back(std::make_unique<Bootstrapper>(*this, bp));
+    }
   }
   if (parent) {
     keys_ = parent->keys_;  // shared read-only device buffers
@@ -311,6 +318,7 @@ Context::Context(const Params& p, const Context& parent) : Context(p, &parent) {
 
 Context::~Context() {
   boot.reset();
+  boot_sparse.clear();
   keys_.clear();
   basis_.clear();
   ptcache_.clear();

@@ -224,6 +224,8 @@ class Context {
   KernelTimer timer;
   std::uint64_t enc_counter = 0;
   std::unique_ptr<Bootstrapper> boot;  // present when Params::bootstrap
+  // sparse-slot variants: boot_sparse[k - 1] carries n = S >> k slots (Params::boot_sparse)
+  std::vector<std::unique_ptr<Bootstrapper>> boot_sparse;
 
   // staging for host -> device copies of encoded coefficients
   long long* staging_slot(cudaEvent_t** ev);
@@ -352,6 +354,10 @@ Ciphertext mult_cipher(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext level_down(Context& ctx, const Ciphertext& a, int target_limbs);
 Ciphertext rescale(Context& ctx, const Ciphertext& a);
 Ciphertext bootstrap(Context& ctx, const Ciphertext& a);
+// bootstrap when only slots [0, active) matter: the smallest sparse-slot variant
+// holding them (input above level 0), else the full pipeline.  Output slots
+// [0, active) = input (the rest 0 for a sparse variant, the input's for the full one)
+Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t active);
 // raw key switch of one polynomial d ([limbs][N], NTT) for parity tests:
 // returns (ks0, ks1) as a 2-poly ciphertext without scale meaning
 Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d_as_c1, u64 key_id, u64 g);

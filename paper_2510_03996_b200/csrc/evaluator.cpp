@@ -1346,6 +1346,19 @@ Ciphertext bootstrap(Context& ctx, const Ciphertext& a) {
   return ctx.boot->run(a);
 }
 
+Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t active) {
+  require_valid(a, "bootstrap");
+  if (!ctx.boot) return bootstrap(ctx, a);
+  if (active == 0 || active > (std::size_t)ctx.S())
+    throw Error(ErrKind::shape, "bootstrap: active slot count " + std::to_string(active) + " outside [1, " +
+                                    std::to_string(ctx.S()) + "]");
+  Bootstrapper* best = nullptr;
+  if (a.limbs >= 2)
+    for (auto& b : ctx.boot_sparse)
+      if ((std::size_t)b->slots() >= active && (!best || b->slots() < best->slots())) best = b.get();
+  return best ? best->run(a) : ctx.boot->run(a);
+}
+
 // -------------------------------------------------------------- raw access
 Ciphertext upload_ct(Context& ctx, const u64* host, int limbs, double scale) {
   Ciphertext ct = ctx.new_ct(limbs);

@@ -37,6 +37,9 @@ struct Params {
   int boot_double_angles = 3;
   int boot_cts_levels = 3;
   int boot_stc_levels = 3;
+  // sparse-slot bootstrapping variants over n = S/2, S/4, ..., S/2^boot_sparse slots
+  // (bootstrap_active picks the smallest that holds the active slots; 0 = none)
+  int boot_sparse = 0;
   // key-switching digits: 0 = uniform alpha = ceil(L / dnum) limbs each; 1 = contiguous
   // digits balanced by bit size (the widest digit decides how many special primes
   // P needs, so a chain of mixed 40/55-bit primes wants unequal limb counts)

@@ -705,7 +705,7 @@ def count_bootstraps(layers: List[Built]) -> int:
 
 # ----------------------------------------------------------------- engine
 def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: str = "fast",
-                security: int = 128, boot_levels: Tuple[int, int] = (0, 0)) -> fh.ContextConfig:
+                security: int = 128, boot_levels: Tuple[int, int] = (0, 0), boot_sparse: int = 3) -> fh.ContextConfig:
     """RNS chain for the spec's ring and depth budget: 55-bit q0, 40-bit
     application primes, 55-bit bootstrapping levels (+16 levels), digits
     balanced by prime bit size, 60-bit special primes (the fewest whose product
@@ -722,7 +722,9 @@ def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: s
     ModelError when no dnum fits (e.g. the reference's depth budget 25 with
     bootstrapping at N = 2^16: log2(Q) alone exceeds 1747).
     security = 0: the round-1 chain kept for the reference's presets -- sparse
-    h = 64 main secret, dnum 3, allow_insecure (disclosed in host_security)."""
+    h = 64 main secret, dnum 3, allow_insecure (disclosed in host_security).
+    boot_sparse: sparse-slot bootstrapping variants over S/2 .. S/2^boot_sparse
+    slots (the model's bootstraps carry only the tensor's active slots)."""
     N = spec.ring_dimension
     if spec.slot_count != N // 2:
         raise fh.ShapeError("the engine packs fully: slot_count must be ring_dimension / 2", 2)
@@ -738,6 +740,7 @@ def ckks_config(spec: ModelSpec, bootstrapping: bool, seed: int = 1, schedule: s
                                 boot_scale_bits=(60 if secure else 55) if bootstrapping else 0, schedule=schedule,
                                 digit_split=1, boot_hamming_weight=boot_hw, boot_k_range=boot_kr,
                                 boot_cts_levels=boot_levels[0], boot_stc_levels=boot_levels[1],
+                                boot_sparse=boot_sparse if bootstrapping else 0,
                                 security=security if secure else 128, allow_insecure=not secure)
 
     boot_depth = fh.host_bootstrap_depth(config(1, 3)) if bootstrapping else 0
@@ -820,14 +823,16 @@ class EncryptedModel:
     """A built model bound to an engine context (keys generated on first use)."""
 
     def __init__(self, spec: ModelSpec, seed: int = 1, schedule: str = "fast", security: int = 128,
-                 boot_levels: Tuple[int, int] = (0, 0)):
+                 boot_levels: Tuple[int, int] = (0, 0), boot_sparse: int = 3):
         """security: HE-standard level the chain must meet (ckks_config); 0 runs
         the insecure round-1 chain the reference's presets need (disclosed in
-        self.security)."""
+        self.security).  boot_sparse: sparse-slot bootstrapping variants (0 = every
+        bootstrap runs the full-slot pipeline)."""
         self.spec = spec
         self.layers = build(spec)
         self.n_boot = count_bootstraps(self.layers)
-        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule, security, boot_levels))
+        self.ctx = fh.SlotContext(ckks_config(spec, self.n_boot > 0, seed, schedule, security, boot_levels,
+                                              boot_sparse))
         self.security = self.ctx.security()
         self._layer_keys: Optional[List[keyplan.LayerKeys]] = None
         self._pinned_keys = self.ctx.key_count()  # relinearisation / bootstrapping keys made at creation
@@ -860,7 +865,8 @@ class EncryptedModel:
             active = C * W * W if packed else n
             out = fh.secure_relu(v, fh.ReluConfig(L.params.get("scale", 1.0), L.params.get("degree", 59), active))
         elif b.type == "bootstrap":
-            out = fh.bootstrap(v)
+            # only the tensor's active slots survive (a sparse-slot variant when one fits)
+            out = fh.bootstrap(v, C * W * W if packed else n)
         elif b.type == "residual":
             body = v
             for c in b.body:

@@ -146,3 +146,52 @@ def test_sse_keys_and_switches_bit_exact():
     ks = fh.keyswitch_raw(xt, 4, 1).words()
     k0, k1 = orc.keyswitch(ct[1], k4, 1)
     assert np.array_equal(ks[0], k0) and np.array_equal(ks[1], k1)
+
+
+@pytest.fixture(scope="module", params=["sparse", "sse"])
+def sctx(request):
+    """Contexts with the sparse-slot variants (n = S/2, S/4, S/8)."""
+    cfg = fh.ContextConfig(N, S, -1, fh.CryptoMetadata(55, 40, 3), limbs=L, special_limbs=8, special_bits=60,
+                           seed=7, hamming_weight=64 if request.param == "sparse" else 0, bootstrap=True,
+                           boot_scale_bits=55, allow_insecure=True, boot_sparse=3)
+    return fh.SlotContext(cfg)
+
+
+@pytest.mark.parametrize("active", [S // 2, 700, S // 8, 3, S // 2 + 1])
+def test_bootstrap_active_sparse_slots(sctx, active):
+    """bootstrap(v, active): the smallest sparse-slot variant n >= active keeps
+    slots [0, n) (the input's), zeroes [n, S), lands on the depth budget with one
+    bootstrap trace event -- the reference's bootstrap() on the slots that matter."""
+    n = S
+    for k in (1, 2, 3):
+        if active <= S >> k:
+            n = S >> k
+    rng = np.random.default_rng(active)
+    v = rng.uniform(-1, 1, S)
+    x = fh.level_down(fh.SlotVector.encode(sctx, v), 2)  # level 1
+    rec = sctx.attach_recorder()
+    y = fh.bootstrap(x, active)
+    ev = [(e.kind, e.value) for e in rec.snapshot()]
+    sctx.detach_recorder()
+    assert y.level() == sctx.depth_budget()
+    assert ev == [("bootstrap", sctx.depth_budget())]
+    out = y.slots()
+    assert np.abs(out[:n] - v[:n]).max() < 1e-4
+    if n < S:
+        assert np.abs(out[n:]).max() < 1e-4
+    else:
+        assert np.abs(out - v).max() < 1e-4
+    # refreshed ciphertexts compute again
+    z = fh.mult_plain(y, np.full(S, 0.5))
+    assert np.abs(z.slots()[:active] - 0.5 * v[:active]).max() < 1e-4
+
+
+def test_bootstrap_active_level0_runs_full(sctx):
+    """At level 0 there is no level for the mask: the full pipeline runs."""
+    rng = np.random.default_rng(11)
+    v = rng.uniform(-1, 1, S)
+    x = fh.level_down(fh.SlotVector.encode(sctx, v), 1)  # level 0
+    y = fh.bootstrap(x, 100)
+    assert np.abs(y.slots() - v).max() < 1e-4
+    with pytest.raises(fh.ShapeError):
+        fh.bootstrap(x, S + 1)
