@@ -2,6 +2,7 @@
 #include "bootstrap.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -86,6 +87,24 @@ Bootstrapper::Mat Bootstrapper::mul(const Mat& A, const Mat& B) const {
       for (long k = 0; k < S; ++k) dst[k] += da[k] * db[(k + a % S + S) % S];
     }
   // drop all-zero diagonals
+  for (auto it = out.begin(); it != out.end();) {
+    bool nz = false;
+    for (const auto& v : it->second) nz = nz || std::abs(v) > 1e-300;
+    it = nz ? std::next(it) : out.erase(it);
+  }
+  return out;
+}
+
+Bootstrapper::Mat Bootstrapper::reduce_period(const Mat& M, long period) const {
+  if (period >= S_) return M;
+  Mat out;
+  for (const auto& [d, v] : M) {
+    long r = ((d % period) + period) % period;
+    if (r > period / 2) r -= period;
+    Diag& dst = out[r];
+    if (dst.empty()) dst.assign(S_, 0.0);
+    for (long k = 0; k < S_; ++k) dst[k] += v[k];
+  }
   for (auto it = out.begin(); it != out.end();) {
     bool nz = false;
     for (const auto& v : it->second) nz = nz || std::abs(v) > 1e-300;
@@ -255,6 +274,8 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
       for (long k = 0; k < S_; ++k) dv[k] = (k % (2 * n_)) < n_ ? std::complex<double>(1.0, 0.0)
                                                                 : std::complex<double>(0.0, -1.0);
       groups.back() = mul(Mat{{0, dv}}, groups.back());
+      // every CtS input is n-periodic (the trace's output and the stages' images)
+      for (Mat& M : groups) M = reduce_period(M, n_);
     }
     cts_ = plan(groups, L, (double)h.q[0]);
   }
@@ -284,6 +305,8 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
       Diag mask(S_);
       for (long k = 0; k < S_; ++k) mask[k] = k < n_ ? 1.0 : 0.0;
       groups.back() = mul(Mat{{0, mask}}, groups.back());
+      // the first factor reads the 2n-periodic EvalMod output, the others n-periodic images
+      for (std::size_t i = 0; i < groups.size(); ++i) groups[i] = reduce_period(groups[i], i == 0 ? 2 * n_ : n_);
     }
     const int stc_limbs = L - bp.cts_levels - cheb_eval_depth(deg) - r;
     stc_limbs_ = stc_limbs;
@@ -291,6 +314,17 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
   }
   if (sparse())
     for (long j = 1; j < g; ++j) sub_steps_.push_back(j * n_);
+  if (std::getenv("FHEON_BOOT_TIMING")) {
+    for (const auto* v : {&cts_, &stc_}) {
+      std::fprintf(stderr, "[boot n=%ld] %s:", n_, v == &cts_ ? "CtS" : "StC");
+      for (const Level& lv : *v) {
+        std::size_t terms = 0;
+        for (const Giant& gi : lv.giants) terms += gi.terms.size();
+        std::fprintf(stderr, " (%zu babies, %zu giants, %zu diagonals)", lv.babies.size(), lv.giants.size(), terms);
+      }
+      std::fprintf(stderr, "\n");
+    }
+  }
   for (long s : rotation_steps()) {  // a server context (no secret) receives them by upload
     if (ctx.has_secret() && !ctx.inheriting_keys) ctx.gen_key(ctx.galois(s));
     ctx.pin_key(ctx.galois(s));
@@ -400,6 +434,17 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0) {
       if (x0.limbs < 2)
         throw Error(ErrKind::internal, "sparse-slot bootstrapping needs an input above level 0 (the mask)");
       // mask to [0, n) on the last level, replicate n-periodically, raise, trace
+      static const bool timing = std::getenv("FHEON_BOOT_TIMING") != nullptr;
+      auto t_last = std::chrono::steady_clock::now();
+      auto lap = [&](const char* what) {
+        if (!timing) return;
+        FHEON_CUDA(cudaStreamSynchronize(ctx_.stream()));
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[boot n=%ld] %-10s %8.3f ms\n", n_, what,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+      };
+      lap("start");
       Ciphertext x = x0.limbs > 2 ? level_down(ctx_, x0, 2) : x0;
       const long n = n_, S = S_;
       BufPtr mask = ctx_.encode_named("boot_mask_" + std::to_string(n),
@@ -411,18 +456,31 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0) {
                                       x.limbs, pt_scale_for(ctx_, x));
       x = mac_plain_many(ctx_, {{x}}, {{mask}})[0];
       x = subsum(x);
+      lap("mask+rep");
       const double corr = x.scale / h.T[0];
-      Ciphertext y = subsum(mod_raise(ctx_, x));
-      for (const Level& lv : cts_) y = apply(y, lv);
+      Ciphertext y = mod_raise(ctx_, x);
+      lap("modraise");
+      y = subsum(y);
+      lap("trace");
+      for (const Level& lv : cts_) {
+        y = apply(y, lv);
+        lap("cts");
+      }
       std::vector<Ciphertext> ys = {add(ctx_, y, conjugate_many(ctx_, {y})[0])};
+      lap("conj");
       ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
+      lap("cos");
       for (int i = 0; i < bp_.double_angles; ++i) {
         std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
         ys = add_many(ctx_, sq, sq);
         for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
       }
+      lap("dbl-angle");
       Ciphertext z = ys[0];
-      for (const Level& lv : stc_) z = apply(z, lv);
+      for (const Level& lv : stc_) {
+        z = apply(z, lv);
+        lap("stc");
+      }
       z.scale *= corr;
       if (z.level() > ctx_.depth_budget()) z = level_down(ctx_, z, ctx_.depth_budget() + 1);
       ctx_.set_tracing(tracing);

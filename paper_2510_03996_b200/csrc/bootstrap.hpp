@@ -88,6 +88,8 @@ class Bootstrapper {
 
   Mat stage(int len, bool inverse) const;
   Mat mul(const Mat& A, const Mat& B) const;
+  // offsets taken mod `period` (the input is period-periodic): coinciding diagonals merge
+  Mat reduce_period(const Mat& M, long period) const;
   std::vector<Level> plan(const std::vector<Mat>& groups, int limbs_in, double scale_in);
   Ciphertext apply(const Ciphertext& x, const Level& lv);
   // sum_{j < S/n} rot(x, j n): one hoisted rotate-and-sum

@@ -1483,8 +1483,8 @@ struct PsVal {
   double c = 0.0;  // constant part when ct is invalid
 };
 
-// Evaluate a node for every input so that it lands EXACTLY on (tl[i] limbs,
-// scale ts[i]) -- no level alignment anywhere in the tree.  A split node
+// Evaluate the tree for every input so that each node lands EXACTLY on (tl[i]
+// limbs, scale ts[i]) -- no level alignment anywhere in the tree.  A split node
 // p = q G + r multiplies q, evaluated at (tl + 1, ts q_tl / scale(G)), by G
 // viewed at tl + 1 limbs (a zero-copy limb drop keeps G's scale), so the fused
 // relinearise-and-rescale lands on ts; r is evaluated at (tl, ts) directly and
@@ -1492,29 +1492,30 @@ struct PsVal {
 // constants c_d ts' q / scale(T_d) (one rescale).  Feasible whenever the node's
 // PS depth fits: the target level of a node of depth d is at most
 // level(x) - d (ps_cost).  T[i][d] babies, G[i][j] giants.
-std::vector<PsVal> ps_eval(Context& ctx, const PsNode& nd, std::vector<std::vector<Ciphertext>>& T,
-                           std::vector<std::vector<Ciphertext>>& G, const std::vector<int>& tl,
-                           const std::vector<double>& ts) {
-  const std::size_t B = T.size();
-  std::vector<PsVal> out(B);
-  if (nd.leaf) {
-    for (std::size_t i = 0; i < B; ++i) {
-      if (!nonconst(nd.c)) {
-        out[i].c = nd.c.empty() ? 0.0 : nd.c[0];
-        continue;
-      }
-      std::vector<Ciphertext> xs;
-      std::vector<double> cs;
-      for (std::size_t d = 1; d < nd.c.size(); ++d)
-        if (nd.c[d] != 0.0) {
-          xs.push_back(T[i][d]);
-          cs.push_back(nd.c[d]);
-        }
-      out[i].ct = lincomb_const_to(ctx, xs, cs, nd.c[0], tl[i], ts[i]);
-    }
-    return out;
-  }
+//
+// Targets are assigned top-down first; the products then run bottom-up, ALL
+// nodes of one height (and every input) in one batched relinearisation, so the
+// serial key-switch chain is the tree's height, not its node count.
+struct PsTask {
+  const PsNode* nd = nullptr;
+  std::vector<int> tl;
+  std::vector<double> ts;
+  std::vector<Ciphertext> gv;  // G_{j-1} viewed at tl + 1 limbs
+  int height = 0;
+  int q = -1, r = -1;          // child tasks
+  std::vector<PsVal> val;
+};
+
+int ps_plan(Context& ctx, const PsNode& nd, std::vector<std::vector<Ciphertext>>& G, const std::vector<int>& tl,
+            const std::vector<double>& ts, std::vector<PsTask>& tasks) {
+  const int id = (int)tasks.size();
+  tasks.emplace_back();
+  tasks[id].nd = &nd;
+  tasks[id].tl = tl;
+  tasks[id].ts = ts;
+  if (nd.leaf) return id;
   const HostTables& h = ctx.host();
+  const std::size_t B = tl.size();
   std::vector<int> tq(B);
   std::vector<double> sq(B);
   std::vector<Ciphertext> gv(B);
@@ -1525,22 +1526,66 @@ std::vector<PsVal> ps_eval(Context& ctx, const PsNode& nd, std::vector<std::vect
     tq[i] = tl[i] + 1;
     sq[i] = ts[i] * (double)h.q[tl[i]] / gv[i].scale;
   }
-  const std::vector<PsVal> q = ps_eval(ctx, *nd.q, T, G, tq, sq);
-  const std::vector<PsVal> r = ps_eval(ctx, *nd.r, T, G, tl, ts);
-  std::vector<Ciphertext> as, bs;
-  for (std::size_t i = 0; i < B; ++i)
-    if (q[i].ct.valid()) {
-      as.push_back(q[i].ct);
-      bs.push_back(gv[i]);
+  const int q = ps_plan(ctx, *nd.q, G, tq, sq, tasks);
+  const int r = ps_plan(ctx, *nd.r, G, tl, ts, tasks);
+  tasks[id].gv = std::move(gv);
+  tasks[id].q = q;
+  tasks[id].r = r;
+  tasks[id].height = std::max(tasks[q].height, tasks[r].height) + 1;
+  return id;
+}
+
+std::vector<PsVal> ps_eval(Context& ctx, const PsNode& root, std::vector<std::vector<Ciphertext>>& T,
+                           std::vector<std::vector<Ciphertext>>& G, const std::vector<int>& tl,
+                           const std::vector<double>& ts) {
+  const std::size_t B = T.size();
+  std::vector<PsTask> tasks;
+  ps_plan(ctx, root, G, tl, ts, tasks);
+  int H = 0;
+  for (PsTask& t : tasks) {
+    H = std::max(H, t.height);
+    if (!t.nd->leaf) continue;
+    t.val.resize(B);
+    for (std::size_t i = 0; i < B; ++i) {
+      if (!nonconst(t.nd->c)) {
+        t.val[i].c = t.nd->c.empty() ? 0.0 : t.nd->c[0];
+        continue;
+      }
+      std::vector<Ciphertext> xs;
+      std::vector<double> cs;
+      for (std::size_t d = 1; d < t.nd->c.size(); ++d)
+        if (t.nd->c[d] != 0.0) {
+          xs.push_back(T[i][d]);
+          cs.push_back(t.nd->c[d]);
+        }
+      t.val[i].ct = lincomb_const_to(ctx, xs, cs, t.nd->c[0], t.tl[i], t.ts[i]);
     }
-  const std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
-  std::size_t k = 0;
-  for (std::size_t i = 0; i < B; ++i) {
-    Ciphertext p = q[i].ct.valid() ? prods[k++] : lincomb_const_to(ctx, {G[i][nd.j - 1]}, {q[i].c}, 0.0, tl[i], ts[i]);
-    p.scale = ts[i];  // exact up to floating-point rounding of the scale bookkeeping
-    out[i].ct = r[i].ct.valid() ? add(ctx, p, r[i].ct) : add_const(ctx, p, r[i].c);
   }
-  return out;
+  for (int ht = 1; ht <= H; ++ht) {
+    std::vector<Ciphertext> as, bs;
+    for (const PsTask& t : tasks)
+      if (t.height == ht)
+        for (std::size_t i = 0; i < B; ++i)
+          if (tasks[t.q].val[i].ct.valid()) {
+            as.push_back(tasks[t.q].val[i].ct);
+            bs.push_back(t.gv[i]);
+          }
+    const std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
+    std::size_t k = 0;
+    for (PsTask& t : tasks) {
+      if (t.height != ht) continue;
+      const int j = t.nd->j;
+      t.val.resize(B);
+      for (std::size_t i = 0; i < B; ++i) {
+        const PsVal& q = tasks[t.q].val[i];
+        const PsVal& r = tasks[t.r].val[i];
+        Ciphertext p = q.ct.valid() ? prods[k++] : lincomb_const_to(ctx, {G[i][j - 1]}, {q.c}, 0.0, t.tl[i], t.ts[i]);
+        p.scale = t.ts[i];  // exact up to floating-point rounding of the scale bookkeeping
+        t.val[i].ct = r.ct.valid() ? add(ctx, p, r.ct) : add_const(ctx, p, r.c);
+      }
+    }
+  }
+  return tasks[0].val;
 }
 }  // namespace
 
