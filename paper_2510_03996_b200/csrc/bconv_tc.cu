@@ -113,6 +113,10 @@ struct TcBconvArgs {
   int kin, T, tb;      // GEMM inputs, targets of this launch, first target
   int nin;             // inputs read from memory (ModDown folded: kin = nin + 2)
   int lo, j, tab;      // ModUp digit
+  // ModUp, every digit in one launch (ndig > 0): CTAs [cta0[d], cta0[d+1]) convert digit d
+  int ndig;
+  int dlo[kMaxDigits], dkin[kMaxDigits], dT[kMaxDigits], dj[kMaxDigits], dtab[kMaxDigits];
+  int cta0[kMaxDigits + 1];
   int s_ell, sp0;      // ModDown inputs: s < s_ell are Q limbs sp0 + s, the rest p_{s - s_ell}
   uint32_t m16;        // 2^16 (opaque to ptxas, see recombine)
 };
@@ -139,19 +143,32 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
   unsigned char* A = smem;           // [2][ABYTES]
   unsigned char* B = smem + 2 * ABYTES;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int KIN = a.kin, T = a.T;
+  int KIN = a.kin, T = a.T, nin = a.nin, lo = a.lo, jd = a.j, tab = a.tab, tb = a.tb;
+  int bx = blockIdx.x, gx = gridDim.x;
+  if (MODE == 0 && a.ndig > 0) {  // this CTA's digit
+    int d = 0;
+    while (d + 1 < a.ndig && (int)blockIdx.x >= a.cta0[d + 1]) ++d;
+    lo = a.dlo[d];
+    KIN = nin = a.dkin[d];
+    T = a.dT[d];
+    jd = a.dj[d];
+    tab = a.dtab[d];
+    tb = 0;
+    bx = (int)blockIdx.x - a.cta0[d];
+    gx = a.cta0[d + 1] - a.cta0[d];
+  }
   const int Tp = (T + kTcTargets - 1) / kTcTargets * kTcTargets;
   const std::size_t N = (std::size_t)1 << a.logN;
   const int E = a.limbs + a.K;
 
   // ---- per-launch tables
   for (int z = tid; z < T * KIN; z += blockDim.x) {
-    const int t = a.tb + z / KIN, k = z % KIN;
+    const int t = tb + z / KIN, k = z % KIN;
     if (MODE == 0) {
-      const int tt = t < a.lo ? t : t + KIN;
+      const int tt = t < lo ? t : t + KIN;
       const int pt = tt < a.limbs ? tt : a.L + (tt - a.limbs);
-      cst[z] = a.qhat[((std::size_t)a.tab * (a.L + a.K) + pt) * kMaxAlpha + k];
-    } else if (MODE == 2 || k < a.nin) {
+      cst[z] = a.qhat[((std::size_t)tab * (a.L + a.K) + pt) * kMaxAlpha + k];
+    } else if (MODE == 2 || k < nin) {
       cst[z] = a.md_phat[(std::size_t)t * kMaxK + k];
     } else if (k >= KIN - 2) {  // folded finish in the last two columns
       const PrimeConst P = a.pc[t];
@@ -163,9 +180,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
     }
   }
   for (int i = tid; i < T; i += blockDim.x) {
-    const int t = a.tb + i;
+    const int t = tb + i;
     if (MODE == 0) {
-      const int tt = t < a.lo ? t : t + KIN;
+      const int tt = t < lo ? t : t + KIN;
       const int pt = tt < a.limbs ? tt : a.L + (tt - a.limbs);
       tq[i][0] = a.pc[pt].q;
       tq[i][1] = a.pc[pt].qinv_neg;
@@ -178,12 +195,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
       toff[i] = (u64)t << a.logN;
     }
   }
-  if (tid < a.nin) {
+  if (tid < nin) {
     if (MODE == 0) {
-      const u64* h = a.qhinv + ((std::size_t)a.tab * kMaxAlpha + tid) * 2;
+      const u64* h = a.qhinv + ((std::size_t)tab * kMaxAlpha + tid) * 2;
       yin[tid][0] = h[0];
       yin[tid][1] = h[1];
-      yin[tid][2] = a.pc[a.lo + tid].q;
+      yin[tid][2] = a.pc[lo + tid].q;
       yin[tid][3] = 0;
     } else {
       const u64* c = a.md_pk + (std::size_t)tid * 4;
@@ -233,32 +250,32 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
     // ---- loaders: warp 8 + i fills rows 32 i .. 32 i + 31, one row per lane;
     // lane k < nin prefetches its limb's 256-byte slice of the tile two ahead into L2
     const int r = (warp - 8) * 32 + lane;
-    const int xoff = MODE == 0 ? a.lo : 0;
+    const int xoff = MODE == 0 ? lo : 0;
     auto slice = [&](int g, int k) {
       return a.in.p[g / tiles_per_poly] + (std::size_t)(xoff + k) * N + (std::size_t)(g % tiles_per_poly) * 128 +
              (warp - 8) * 32;
     };
-    if (lane < a.nin)
+    if (lane < nin)
       for (int d = 0; d < 2; ++d) {
-        const int g = blockIdx.x + d * gridDim.x;
+        const int g = bx + d * gx;
         if (g < tiles) asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(slice(g, lane)) : "memory");
       }
     int tl = 0;
-    for (int g = blockIdx.x; g < tiles; g += gridDim.x, ++tl) {
+    for (int g = bx; g < tiles; g += gx, ++tl) {
       const int ab = tl & 1;
-      const int gp = g + 2 * gridDim.x;
-      if (lane < a.nin && gp < tiles)
+      const int gp = g + 2 * gx;
+      if (lane < nin && gp < tiles)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(slice(gp, lane)) : "memory");
       u64 xr[KINP];
       {
         const u64* x = slice(g, 0) + lane;
 #pragma unroll
-        for (int k = 0; k < KINP; ++k) xr[k] = k < a.nin ? x[(std::size_t)k * N] : 0;
+        for (int k = 0; k < KINP; ++k) xr[k] = k < nin ? x[(std::size_t)k * N] : 0;
       }
       double v = 0.0;  // y_k computed in place of the inputs
 #pragma unroll
       for (int k = 0; k < KINP; ++k) {
-        if (k < a.nin) {
+        if (k < nin) {
           const u64 q = yin[k][2];
           if (MODE == 0) {
             xr[k] = shoup_mul(xr[k], yin[k][0], yin[k][1], q);
@@ -288,7 +305,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
   } else if (warp == kTcMmaWarp) {
     // ---- MMA issuer
     int use = 0, tl = 0;
-    for (int g = blockIdx.x; g < tiles; g += gridDim.x, ++tl) {
+    for (int g = bx; g < tiles; g += gx, ++tl) {
       const int ab = tl & 1;
       const uint32_t abase = smem_u32(A + ab * ABYTES);
       if (lane == 0) {
@@ -318,10 +335,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
     const int row = (warp & 3) * 32 + lane;
     const uint32_t lanebase = (uint32_t)((warp & 3) * 32) << 16;
     int use = 0, tl = 0;
-    for (int g = blockIdx.x; g < tiles; g += gridDim.x, ++tl) {
+    for (int g = bx; g < tiles; g += gx, ++tl) {
       const int z = g / tiles_per_poly;
       const std::size_t n = (std::size_t)(g % tiles_per_poly) * 128 + row;
-      u64* out = a.out.p[z] + (MODE == 0 ? (std::size_t)a.j * E * N : 0);
+      u64* out = a.out.p[z] + (MODE == 0 ? (std::size_t)jd * E * N : 0);
       u64 u = 0;
       if (MODE == 2) {  // the tile's overflow estimates: read, then release the slot
         mbar_wait(&afull[tl & 1], (tl >> 1) & 1);
@@ -385,7 +402,7 @@ int sm_count() {
 }
 
 template <int KINP, int MODE>
-void launch_tc(const TcBconvArgs& a, std::size_t N, cudaStream_t st) {
+void launch_tc(const TcBconvArgs& a, std::size_t N, cudaStream_t st, int grid_override = 0) {
   const int Tp = (a.T + kTcTargets - 1) / kTcTargets * kTcTargets;
   const std::size_t smem = (std::size_t)2 * 128 * KINP * 8 + (std::size_t)Tp * 16 * KINP * 8;
   static int configured = 0;
@@ -394,7 +411,7 @@ void launch_tc(const TcBconvArgs& a, std::size_t N, cudaStream_t st) {
     configured = 1;
   }
   const int tiles = (int)(N / 128) * a.in.n;
-  const int grid = std::min(tiles, 2 * sm_count());
+  const int grid = grid_override > 0 ? grid_override : std::min(tiles, 2 * sm_count());
   k_bconv_tc<KINP, MODE><<<grid, kTcThreads, smem, st>>>(a);
 }
 
@@ -420,6 +437,46 @@ bool bconv_tc_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+bool modup_bconv_tc_all(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st) {
+  const int beta = t.dig.beta(limbs);
+  if (beta < 2) return false;
+  TcBconvArgs a{};
+  a.m16 = 1u << 16;
+  a.in = x;
+  a.out = ext;
+  a.pc = t.pc;
+  a.qhinv = t.modup_qhinv;
+  a.qhat = t.modup_qhat;
+  a.logN = t.logN;
+  a.limbs = limbs;
+  a.L = t.L;
+  a.K = t.K;
+  a.ndig = beta;
+  int kmax = 0, tmax = 0;
+  for (int j = 0; j < beta; ++j) {
+    a.dlo[j] = t.dig.lo(j);
+    a.dkin[j] = t.dig.hi(j, limbs) - a.dlo[j];
+    a.dT[j] = limbs + t.K - a.dkin[j];
+    a.dj[j] = j;
+    a.dtab[j] = (limbs - 1) * t.dnum + j;
+    kmax = std::max(kmax, a.dkin[j]);
+    tmax = std::max(tmax, a.dT[j]);
+  }
+  if (tmax > kTcMaxT || kmax > 16) return false;
+  // the widest digit's targets size the shared B (the others use a prefix)
+  a.kin = a.nin = kmax;
+  a.T = tmax;
+  const int tiles = (int)(t.N / 128) * x.n;
+  const int per = std::max(1, std::min(tiles, 2 * sm_count() / beta));
+  for (int j = 0; j <= beta; ++j) a.cta0[j] = j * per;
+  const std::size_t N = t.N;
+  if (kmax <= 4) launch_tc<4, 0>(a, N, st, beta * per);
+  else if (kmax <= 8) launch_tc<8, 0>(a, N, st, beta * per);
+  else if (kmax <= 12) launch_tc<12, 0>(a, N, st, beta * per);
+  else launch_tc<16, 0>(a, N, st, beta * per);
+  return true;
 }
 
 void modup_bconv_tc(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, int j, cudaStream_t st) {

@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cuda_profiler_api.h>
+#include <string>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -113,58 +115,81 @@ Bootstrapper::Mat Bootstrapper::reduce_period(const Mat& M, long period) const {
   return out;
 }
 
-std::vector<Bootstrapper::Level> Bootstrapper::plan(const std::vector<Mat>& groups, int limbs_in, double scale_in) {
+std::vector<Bootstrapper::Level> Bootstrapper::plan(const std::vector<Mat>& groups, int limbs_in, double scale_in,
+                                                   const std::vector<long>& periods) {
   const HostTables& h = ctx_.host();
   const long S = S_;
   std::vector<Level> out;
   int limbs = limbs_in;
   double scale = scale_in;
-  for (const Mat& M : groups) {
-    long u = S;
-    for (const auto& [d, v] : M)
-      if (d != 0) u = std::min(u, std::labs(d) & -std::labs(d));  // lowest set bit
-    if (u == S) u = 1;
-    std::vector<long> ks;
-    for (const auto& [d, v] : M) ks.push_back(d / u);
+  for (std::size_t gi_ = 0; gi_ < groups.size(); ++gi_) {
+    const Mat& M = groups[gi_];
+    const long period = gi_ < periods.size() ? periods[gi_] : S;
+    // offset representations: signed (-S/2, S/2]; for a period-periodic input also
+    // [0, period) -- the diagonals then fit under fewer giants (rot(x, d) = rot(x, d - period))
+    std::vector<int> reps = {0};
+    if (period < S) reps.push_back(1);
+    auto rep_of = [&](long d, int rep) {
+      if (rep == 0) return d;
+      return ((d % period) + period) % period;
+    };
     // baby-step size: minimise the key-switch cost.  Single hoisting: every baby
     // and giant is a full key switch (cost 1 each).  Double hoisting: a baby is one
     // key inner product (1), a giant its inner sum's ModDown + a ModUp + an inner
-    // product (6.7; measured ratios ModUp 3.3, ModDown 2.4, inner 1 at N = 2^16),
-    // and at most 32 MAC terms per giant
+    // product (8.5, measured best of 5 / 6.7 / 8.5 / 12 / 20 on the 128-bit chain), the
+    // unrotated giant its ModDown only; at most 32 MAC terms per giant
     const bool dh = bp_.double_hoist;
     static const double gcost = [] {
       const char* e = std::getenv("FHEON_DH_GCOST");
-      return e ? std::atof(e) : 6.7;
+      return e ? std::atof(e) : 8.5;
     }();
-    long best_n1 = 1;
+    static const double g0cost = [] {
+      const char* e = std::getenv("FHEON_DH_G0COST");
+      return e ? std::atof(e) : 2.4;
+    }();
+    long best_n1 = 1, best_u = 1;
+    int best_rep = 0;
     double best_cost = 1e300;
-    for (long n1 = 1; n1 <= 64; n1 *= 2) {
-      std::set<long> bs, gs;
-      std::map<long, int> per_giant;
-      for (long k : ks) {
-        const long g = (long)std::floor((double)k / (double)n1);
-        bs.insert(k - g * n1);
-        gs.insert(g);
-        per_giant[g]++;
+    for (int rep : reps) {
+      long u = S;
+      for (const auto& [d0, v] : M) {
+        const long d = rep_of(d0, rep);
+        if (d != 0) u = std::min(u, std::labs(d) & -std::labs(d));  // lowest set bit
       }
-      int maxterms = 0;
-      for (const auto& [g, c] : per_giant) maxterms = std::max(maxterms, c);
-      if (dh && maxterms > kMacMaxTerms) continue;
-      const double nb = (double)(bs.size() - (bs.count(0) ? 1 : 0)), ng = (double)gs.size();
-      const double cost = dh ? nb + gcost * ng : nb + ng - (gs.count(0) ? 1.0 : 0.0);
-      if (cost < best_cost) {
-        best_cost = cost;
-        best_n1 = n1;
+      if (u == S) u = 1;
+      std::vector<long> ks;
+      for (const auto& [d0, v] : M) ks.push_back(rep_of(d0, rep) / u);
+      for (long n1 = 1; n1 <= 64; n1 *= 2) {
+        std::set<long> bs, gs;
+        std::map<long, int> per_giant;
+        for (long k : ks) {
+          const long g = (long)std::floor((double)k / (double)n1);
+          bs.insert(k - g * n1);
+          gs.insert(g);
+          per_giant[g]++;
+        }
+        int maxterms = 0;
+        for (const auto& [g, c] : per_giant) maxterms = std::max(maxterms, c);
+        if (dh && maxterms > kMacMaxTerms) continue;
+        const double nb = (double)(bs.size() - (bs.count(0) ? 1 : 0)), ng = (double)gs.size();
+        const double g0 = gs.count(0) ? 1.0 : 0.0;
+        const double cost = dh ? nb + gcost * (ng - g0) + g0cost * g0 : nb + ng - g0;
+        if (cost < best_cost - 1e-9) {
+          best_cost = cost;
+          best_n1 = n1;
+          best_u = u;
+          best_rep = rep;
+        }
       }
     }
-    const long n1 = best_n1;
+    const long n1 = best_n1, u = best_u;
     const int lv = limbs - 1;
     const double pt_scale = h.T[lv - 1] * (double)h.q[lv] / scale;
     Level L;
     std::map<long, Giant> giants;
     std::set<long> babies;
-    for (const auto& [d, diag] : M) {
-      const long k = d / u;
+    for (const auto& [d0, diag] : M) {
+      const long k = rep_of(d0, best_rep) / u;
       const long g = (long)std::floor((double)k / (double)n1);
       const long b = k - g * n1;
       const long G = g * n1 * u;
@@ -277,7 +302,7 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
       // every CtS input is n-periodic (the trace's output and the stages' images)
       for (Mat& M : groups) M = reduce_period(M, n_);
     }
-    cts_ = plan(groups, L, (double)h.q[0]);
+    cts_ = plan(groups, L, (double)h.q[0], std::vector<long>(groups.size(), n_));
   }
   // SlotsToCoeffs: forward stages len = 2 .. n, scaled by q0 / (2 pi Delta_0)
   {
@@ -310,7 +335,9 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
     }
     const int stc_limbs = L - bp.cts_levels - cheb_eval_depth(deg) - r;
     stc_limbs_ = stc_limbs;
-    stc_ = plan(groups, stc_limbs, h.T[stc_limbs - 1]);
+    std::vector<long> periods(groups.size(), n_);
+    periods[0] = std::min<long>(2 * n_, S_);  // the EvalMod output is 2n-periodic
+    stc_ = plan(groups, stc_limbs, h.T[stc_limbs - 1], periods);
   }
   if (sparse())
     for (long j = 1; j < g; ++j) sub_steps_.push_back(j * n_);
@@ -468,7 +495,11 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0) {
       }
       std::vector<Ciphertext> ys = {add(ctx_, y, conjugate_many(ctx_, {y})[0])};
       lap("conj");
+      static const char* prof = std::getenv("FHEON_BOOT_PROFILE");  // ncu range: "cos"
+      const bool prof_cos = prof && std::string(prof) == "cos";
+      if (prof_cos) FHEON_CUDA(cudaProfilerStart());
       ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
+      if (prof_cos) FHEON_CUDA(cudaProfilerStop());
       lap("cos");
       for (int i = 0; i < bp_.double_angles; ++i) {
         std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);

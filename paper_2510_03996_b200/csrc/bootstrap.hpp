@@ -90,7 +90,9 @@ class Bootstrapper {
   Mat mul(const Mat& A, const Mat& B) const;
   // offsets taken mod `period` (the input is period-periodic): coinciding diagonals merge
   Mat reduce_period(const Mat& M, long period) const;
-  std::vector<Level> plan(const std::vector<Mat>& groups, int limbs_in, double scale_in);
+  // periods[i]: group i's input is periods[i]-periodic (S: no structure)
+  std::vector<Level> plan(const std::vector<Mat>& groups, int limbs_in, double scale_in,
+                          const std::vector<long>& periods);
   Ciphertext apply(const Ciphertext& x, const Level& lv);
   // sum_{j < S/n} rot(x, j n): one hoisted rotate-and-sum
   Ciphertext subsum(const Ciphertext& x);

@@ -137,6 +137,8 @@ void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int 
 void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st);
 // tensor-core basis conversions (bconv_tc.cu): ModUp of digit j, ModDown conversion
 void modup_bconv_tc(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, int j, cudaStream_t st);
+// every digit of the ModUp in one launch; false when the shape needs the per-digit launches
+bool modup_bconv_tc_all(const DevTables& t, const PolyList& ext, const PolyList& x, int limbs, cudaStream_t st);
 void moddown_conv_tc(const DevTables& t, const PolyList& conv, const PolyList& z, int limbs, cudaStream_t st);
 // ModDown conversion by P' = P q_l for the fused relinearisation + rescale: z points at
 // limb l of each accumulator (q_l then the K special limbs, coefficient domain),

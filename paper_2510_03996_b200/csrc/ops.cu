@@ -660,6 +660,10 @@ void modup_bconv(const DevTables& t, const PolyList& ext, const PolyList& x, int
   const int beta = t.dig.beta(limbs);
   TimedScope ts(t, kModUp, st);
   const int E = limbs + t.K;
+  if (bconv_tc_enabled() && modup_bconv_tc_all(t, ext, x, limbs, st)) {  // every digit in one launch
+    launch_check("k_bconv_tc<modup>");
+    return;
+  }
   for (int j = 0; j < beta; ++j) {
     if (bconv_tc_enabled()) {
       modup_bconv_tc(t, ext, x, limbs, j, st);
