@@ -416,7 +416,7 @@ Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv) {
   std::vector<Ciphertext> inner = mac_plain_many_unrescaled(ctx_, terms, pts);
   std::vector<std::pair<Ciphertext, long>> g;
   for (std::size_t i = 0; i < lv.giants.size(); ++i) g.push_back({inner[i], lv.giants[i].rot});
-  return rescale_to_target(ctx_, rotate_sum_many(ctx_, {g}))[0];
+  return rotate_sum_to_target(ctx_, {g})[0];
 }
 
 Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {

@@ -304,6 +304,12 @@ std::vector<Ciphertext> mac_plain_many(Context& ctx, const std::vector<std::vect
 // over such outputs needs one rescale instead of one per term); trace as above
 std::vector<Ciphertext> mac_plain_many_unrescaled(Context& ctx, const std::vector<std::vector<Ciphertext>>& terms,
                                                   const std::vector<std::vector<BufPtr>>& pts);
+// rescale_to_target(rotate_sum_many(groups)) with each group's rescale folded into its
+// ModDown (one rounding by P q_l); identity terms join before the division
+// (record_identity: trace the t = 0 terms as rotations, as rotate_sum_many does)
+std::vector<Ciphertext> rotate_sum_to_target(Context& ctx,
+                                             const std::vector<std::vector<std::pair<Ciphertext, long>>>& groups,
+                                             bool record_identity = true);
 // rescale unrescaled MAC outputs onto the next level's target scale
 std::vector<Ciphertext> rescale_to_target(Context& ctx, const std::vector<Ciphertext>& prods);
 std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b);

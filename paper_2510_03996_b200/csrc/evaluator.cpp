@@ -442,6 +442,79 @@ std::vector<Ciphertext> moddown_accs(Context& ctx, const std::vector<u64*>& accp
   return outs;
 }
 
+// ModDown of Q u P accumulators with the rescale folded in (as keyswitch_relin_rescale):
+// z = acc + P add (add: the group's unrotated terms, or none) divided by P' = P q_l,
+// l = limbs - 1, in ONE rounding -- round(z / P') on the l remaining limbs, no
+// rescale NTTs.  Outputs [2][l][N], scale left to the caller.
+std::vector<Ciphertext> moddown_rescale_accs(Context& ctx, const std::vector<u64*>& accp,
+                                             const std::vector<Ciphertext>& adds, int limbs) {
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L(), K = ctx.K(), E = limbs + K;
+  const int l = limbs - 1;
+  const HostTables& h = ctx.host();
+  u64 pm_l = 1;  // P mod q_l
+  for (int k = 0; k < K; ++k) pm_l = mulmod(pm_l, h.q[L + k] % h.q[l], h.q[l]);
+  const u64 pm_mont = to_mont(pm_l, h.q[l]);
+  const int ngroups = (int)accp.size();
+  std::vector<Ciphertext> outs;
+  outs.reserve(ngroups);
+  constexpr int kChunk = kMaxPolys / 2;
+  for (int r0 = 0; r0 < ngroups; r0 += kChunk) {
+    const int R = std::min(kChunk, ngroups - r0);
+    // z_l = acc_l + P add_l on the dropped limb
+    PolyList za{}, dl{};
+    for (int r = 0; r < R; ++r) {
+      const Ciphertext& a = adds[r0 + r];
+      if (!a.valid()) continue;
+      for (int p = 0; p < 2; ++p) {
+        za.p[za.n++] = accp[r0 + r] + (std::size_t)p * E * N + (std::size_t)l * N;
+        dl.p[dl.n++] = (p == 0 ? a.c0 : a.c1) + (std::size_t)l * N;
+      }
+    }
+    if (za.n) ew_axpy_limb(t, za, dl, pm_mont, l, st);
+    // the K + 1 special limbs (q_l, p_0..p_K-1) to the coefficient domain
+    LimbSet zs{};
+    zs.nbase = R;
+    for (int r = 0; r < R; ++r) zs.base[r] = accp[r0 + r] + (std::size_t)l * N;
+    zs.blocks_per_base = 2;
+    zs.block_stride = (long long)E * N;
+    zs.E = K + 1;
+    zs.ell = 1;
+    zs.p0 = l;
+    zs.L = L;
+    ntt_inverse(t, zs, st);
+    BufPtr conv = ctx.alloc((std::size_t)R * 2 * l * N);
+    PolyList cl{}, zl{};
+    cl.n = zl.n = 2 * R;
+    NttEpilogue e{};
+    for (int r = 0; r < R; ++r) {
+      Ciphertext o = ctx.new_ct(l);
+      const Ciphertext& a = adds[r0 + r];
+      for (int p = 0; p < 2; ++p) {
+        const int i = 2 * r + p;
+        cl.p[i] = conv->ptr + (std::size_t)i * l * N;
+        zl.p[i] = accp[r0 + r] + (std::size_t)p * E * N + (std::size_t)l * N;
+        e.out[i] = p == 0 ? o.c0 : o.c1;
+        e.src[i] = accp[r0 + r] + (std::size_t)p * E * N;
+        e.add[i] = a.valid() ? (p == 0 ? a.c0 : a.c1) : nullptr;
+        e.add_g[i] = 1;
+      }
+      outs.push_back(o);
+    }
+    moddown_fused_conv_tc(t, cl, zl, limbs, st);
+    e.cst = t.md2_q + (std::size_t)l * L * 4 + 2;  // P'^-1 mod q_i, Shoup
+    e.cst_stride = 4;
+    e.acst = t.rs + (std::size_t)l * L * 4;  // q_l^-1 mod q_i, Shoup
+    e.acst_stride = 4;
+    ntt_forward_epilogue(t, limbset(conv->ptr, 2 * R, (std::size_t)l * N, l, l, L), e, st);
+    ctx.stats.ntt_limbs += (std::size_t)R * 2 * (K + 1 + l);
+    ctx.stats.rescales += (std::size_t)R;
+  }
+  return outs;
+}
+
 std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*>& inputs,
                                       const std::vector<const u64*>& c0s, int limbs, const std::vector<SumJob>& jobs,
                                       int ngroups) {
@@ -534,7 +607,7 @@ Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vec
       ctx.record(1, lv - 1);
     }
   }
-  return rescale_to_target(ctx, rotate_sum_many(ctx, {terms}))[0];
+  return rotate_sum_to_target(ctx, {terms})[0];
 }
 
 // out[r] = sum_k rot(groups[r][k].first, groups[r][k].second): every group's
@@ -600,6 +673,89 @@ std::vector<Ciphertext> rotate_sum_many(Context& ctx, const std::vector<std::vec
   }
   for (std::size_t r = 0; r < groups.size(); ++r)
     for (const Ciphertext& d : direct[r]) outs[r] = outs[r].valid() ? add(ctx, outs[r], d) : d;
+  return outs;
+}
+
+// rescale_to_target(rotate_sum_many(groups)) with the rescale folded into each group's
+// ModDown (moddown_rescale_accs): one rounding by P q_l, no rescale NTTs.  Every term
+// of a group shares level and scale (the unrescaled MAC outputs of a layer or a
+// linear transform); outputs land on T_{l-1}.  Records one rotation event per term.
+std::vector<Ciphertext> rotate_sum_to_target(Context& ctx,
+                                             const std::vector<std::vector<std::pair<Ciphertext, long>>>& groups,
+                                             bool record_identity) {
+  if (groups.empty()) return {};
+  const long S = ctx.S();
+  const int limbs = groups[0].at(0).first.limbs;
+  bool fused = limbs >= 2 && bconv_tc_enabled() && ctx.K() + 1 + 2 <= 16;
+  for (const auto& g : groups) {
+    if (g.empty()) throw Error(ErrKind::internal, "rotate_sum: empty group");
+    for (const auto& [x, tt] : g) fused = fused && x.limbs == limbs;
+  }
+  if (!fused) return rescale_to_target(ctx, rotate_sum_many(ctx, groups));
+  std::vector<const u64*> inputs, c0s;
+  std::map<const u64*, int> slot;
+  std::vector<SumJob> jobs;
+  std::vector<int> gidx(groups.size(), -1);  // group -> accumulator
+  std::vector<Ciphertext> direct(groups.size());
+  int nacc = 0;
+  for (std::size_t r = 0; r < groups.size(); ++r) {
+    const Ciphertext& x0 = groups[r][0].first;
+    int in_group = 0;
+    for (const auto& [x, tt] : groups[r]) {
+      require_valid(x, "rotate");
+      if (tt <= -S || tt >= S)
+        throw Error(ErrKind::invalid_rotation,
+                    "rotation amount " + std::to_string(tt) + " out of range for " + std::to_string(S) + " slots");
+      check_scales(x, x0, "rotate_sum");
+      const u64 g = ctx.galois(tt);
+      if (g != 1 || record_identity) {
+        ctx.record(0, tt);
+        ctx.stats.rotations++;
+      }
+      if (g == 1) {
+        direct[r] = direct[r].valid() ? add(ctx, direct[r], x) : x;
+        continue;
+      }
+      ++in_group;
+    }
+    if (in_group > kMaxSumJobs) return rescale_to_target(ctx, rotate_sum_many(ctx, groups));
+    if (in_group == 0) continue;
+    gidx[r] = nacc++;
+    for (const auto& [x, tt] : groups[r]) {
+      const u64 g = ctx.galois(tt);
+      if (g == 1) continue;
+      auto it = slot.find(x.c1);
+      int in;
+      if (it == slot.end()) {
+        in = (int)inputs.size();
+        slot[x.c1] = in;
+        inputs.push_back(x.c1);
+        c0s.push_back(x.c0);
+      } else {
+        in = it->second;
+      }
+      jobs.push_back({g, in, gidx[r]});
+    }
+  }
+  const int lv = limbs - 1;
+  std::vector<Ciphertext> outs(groups.size());
+  if (nacc > 0) {
+    BufPtr accs = keyswitch_sum_accs(ctx, inputs, c0s, limbs, jobs, nacc);
+    const std::size_t stride = (std::size_t)2 * (limbs + ctx.K()) * ctx.N();
+    std::vector<u64*> accp(nacc);
+    std::vector<Ciphertext> adds(nacc);
+    for (std::size_t r = 0; r < groups.size(); ++r)
+      if (gidx[r] >= 0) {
+        accp[gidx[r]] = accs->ptr + (std::size_t)gidx[r] * stride;
+        adds[gidx[r]] = direct[r];
+      }
+    std::vector<Ciphertext> rs = moddown_rescale_accs(ctx, accp, adds, limbs);
+    for (std::size_t r = 0; r < groups.size(); ++r)
+      if (gidx[r] >= 0) outs[r] = rs[gidx[r]];
+  }
+  for (std::size_t r = 0; r < groups.size(); ++r)
+    if (gidx[r] < 0) outs[r] = rescale_many(ctx, {direct[r]})[0];
+  for (Ciphertext& o : outs) o.scale = ctx.host().T[lv - 1];
   return outs;
 }
 

@@ -215,6 +215,16 @@ std::vector<Ciphertext> sum_rotations(Context& ctx, const std::vector<RotTerms>&
   return outs;
 }
 
+// rescale_to_target(sum_rotations(groups)) with the rescale folded into the ModDowns
+// when every group is uniform (rotate_sum_to_target); the same events
+std::vector<Ciphertext> sum_rotations_to_target(Context& ctx, const std::vector<RotTerms>& groups) {
+  bool uniform = !groups.empty();
+  for (const RotTerms& g : groups) uniform = uniform && !g.empty() && same_level_and_scale(g);
+  for (const RotTerms& g : groups) uniform = uniform && g[0].first.limbs == groups[0][0].first.limbs;
+  if (uniform) return rotate_sum_to_target(ctx, groups, false);
+  return rescale_to_target(ctx, sum_rotations(ctx, groups));
+}
+
 // out = sum_f rot(r_f, -f * block): placement rotations share one ModDown
 Ciphertext place_and_sum(Context& ctx, const std::vector<Ciphertext>& r, std::size_t block) {
   // Up to 64 placements: one rotate-and-sum with one key per placement (the
@@ -377,7 +387,7 @@ Ciphertext bsgs_moves(Context& ctx, const Ciphertext& x, const std::vector<SlotM
   const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, terms, pts);
   RotTerms giants;
   for (std::size_t i = 0; i < rows.size(); ++i) giants.push_back({rows[i], gs[i]});
-  return rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+  return sum_rotations_to_target(ctx, {giants})[0];
 }
 
 // out[f mb + p] = sum_{q < nq} wfn(f, q) z[q mb + p] for f < F, with z periodic
@@ -439,7 +449,7 @@ Ciphertext diag_mix(Context& ctx, const Ciphertext& z, std::size_t nq, std::size
   const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, terms, pts);
   RotTerms giants;
   for (std::size_t i = 0; i < rows.size(); ++i) giants.push_back({rows[i], gsh[i]});
-  return rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+  return sum_rotations_to_target(ctx, {giants})[0];
 }
 
 std::size_t best_divisor_split(std::size_t n, std::size_t giants_per_unit) {
@@ -748,7 +758,7 @@ std::vector<Ciphertext> stride_bsgs_many(Context& ctx, const std::vector<Ciphert
   std::vector<RotTerms> giants(B);
   for (std::size_t i = 0; i < B; ++i)
     for (std::size_t a = 0; a < W_out; ++a) giants[i].push_back({rows[i * W_out + a], (long)(a * (S * W - W_out))});
-  return rescale_to_target(ctx, sum_rotations(ctx, giants));
+  return sum_rotations_to_target(ctx, giants);
 }
 }  // namespace
 
@@ -1061,7 +1071,7 @@ PackedTensor conv_special_3x3_diag(Context& ctx, const PackedTensor& x, const Ke
   const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, nz_terms, nz_pts);
   RotTerms giants;
   for (std::size_t i = 0; i < rows.size(); ++i) giants.push_back({rows[i], (long)(D * nz_d2[i] * m)});
-  Ciphertext out = rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+  Ciphertext out = sum_rotations_to_target(ctx, {giants})[0];
   out = add_bias(ctx, out, w.bias, m);
   return {out, C, W};
 }
@@ -1320,7 +1330,7 @@ Ciphertext fc_diagonal(Context& ctx, const Ciphertext& x, std::size_t n, std::si
   const std::vector<Ciphertext> rows = mac_plain_many_unrescaled(ctx, terms, pts);
   RotTerms giants;
   for (std::size_t g = 0; g < rows.size(); ++g) giants.push_back({rows[g], gofs[g]});
-  return rescale_to_target(ctx, sum_rotations(ctx, {giants}))[0];
+  return sum_rotations_to_target(ctx, {giants})[0];
 }
 }  // namespace
 
