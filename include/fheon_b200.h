@@ -236,8 +236,11 @@ int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out);
 /* bootstrap() when only slots [0, active_slots) matter (a packed tensor's active region): runs the
  * smallest sparse-slot variant (fheon_params.boot_sparse) holding them -- the input must sit above
  * level 0, its last level takes the mask -- else the full pipeline.  Same level accounting and
- * trace event as fheon_bootstrap; output slots [0, active_slots) = input, the rest 0 (sparse) */
-int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, fheon_ct** out);
+ * trace event as fheon_bootstrap; output slots [0, active_slots) = input, the rest 0 (sparse).
+ * flags bit 0 (FHEON_BOOT_CLEAN): the caller asserts slots [active_slots, S) of the input are
+ * zero (a convolution's output): no mask, so a level-0 input takes a sparse variant too */
+#define FHEON_BOOT_CLEAN 1
+int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, int flags, fheon_ct** out);
 /* bootstrapping stage probes (tests): 1 CoeffsToSlots, 2 EvalMod, 3 SlotsToCoeffs, 4 ModRaise;
  * info (may be NULL): [depth, k_range, double_angles, stc_input_limbs] */
 int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out);

@@ -138,7 +138,7 @@ SIGNATURES = {
     "fheon_mult_plain": (C.c_int, [vp, vp, dp, C.c_size_t, pp]),
     "fheon_mult_cipher": (C.c_int, [vp, vp, vp, pp]),
     "fheon_bootstrap": (C.c_int, [vp, vp, pp]),
-    "fheon_bootstrap_active": (C.c_int, [vp, vp, C.c_size_t, pp]),
+    "fheon_bootstrap_active": (C.c_int, [vp, vp, C.c_size_t, C.c_int, pp]),
     "fheon_bootstrap_stage": (C.c_int, [vp, vp, C.c_int, pp]),
     "fheon_bootstrap_info": (C.c_int, [vp, C.POINTER(C.c_int), dp, C.c_size_t, szp]),
     "fheon_rescale": (C.c_int, [vp, vp, pp]),

@@ -706,13 +706,14 @@ def mult_cipher(a: SlotVector, b: SlotVector) -> SlotVector:
     return _wrap(a._ctx, _native.lib().fheon_mult_cipher, a._h, b._h)
 
 
-def bootstrap(a: SlotVector, active_slots: Optional[int] = None) -> SlotVector:
+def bootstrap(a: SlotVector, active_slots: Optional[int] = None, clean: bool = False) -> SlotVector:
     """backend.cpp:233-249: refresh to the depth budget.  With `active_slots`, only
     slots [0, active_slots) are kept (a sparse-slot variant when the context has
-    one that fits and the input sits above level 0; the rest become 0)."""
+    one that fits and the input sits above level 0 -- or at any level when `clean`:
+    the caller asserts slots past active_slots are zero; the rest become 0)."""
     if active_slots is None:
         return _wrap(a._ctx, _native.lib().fheon_bootstrap, a._h)
-    return _wrap(a._ctx, _native.lib().fheon_bootstrap_active, a._h, int(active_slots))
+    return _wrap(a._ctx, _native.lib().fheon_bootstrap_active, a._h, int(active_slots), int(bool(clean)))
 
 
 def bootstrap_stage(a: SlotVector, stage: int) -> SlotVector:

@@ -452,13 +452,13 @@ Ciphertext Bootstrapper::subsum(const Ciphertext& x) {
   return rotate_sum_many(ctx_, {terms})[0];
 }
 
-Ciphertext Bootstrapper::run(const Ciphertext& x0) {
+Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
   const bool tracing = ctx_.tracing();
   ctx_.set_tracing(false);
   try {
     const HostTables& h = ctx_.host();
     if (sparse()) {
-      if (x0.limbs < 2)
+      if (x0.limbs < 2 && !clean)
         throw Error(ErrKind::internal, "sparse-slot bootstrapping needs an input above level 0 (the mask)");
       // mask to [0, n) on the last level, replicate n-periodically, raise, trace
       static const bool timing = std::getenv("FHEON_BOOT_TIMING") != nullptr;
@@ -472,16 +472,21 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0) {
         t_last = t;
       };
       lap("start");
-      Ciphertext x = x0.limbs > 2 ? level_down(ctx_, x0, 2) : x0;
-      const long n = n_, S = S_;
-      BufPtr mask = ctx_.encode_named("boot_mask_" + std::to_string(n),
-                                      [n, S] {
-                                        std::vector<double> m((std::size_t)S, 0.0);
-                                        std::fill(m.begin(), m.begin() + n, 1.0);
-                                        return m;
-                                      },
-                                      x.limbs, pt_scale_for(ctx_, x));
-      x = mac_plain_many(ctx_, {{x}}, {{mask}})[0];
+      Ciphertext x;
+      if (clean) {  // slots [n, S) already zero: no mask
+        x = x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0;
+      } else {
+        x = x0.limbs > 2 ? level_down(ctx_, x0, 2) : x0;
+        const long n = n_, S = S_;
+        BufPtr mask = ctx_.encode_named("boot_mask_" + std::to_string(n),
+                                        [n, S] {
+                                          std::vector<double> m((std::size_t)S, 0.0);
+                                          std::fill(m.begin(), m.begin() + n, 1.0);
+                                          return m;
+                                        },
+                                        x.limbs, pt_scale_for(ctx_, x));
+        x = mac_plain_many(ctx_, {{x}}, {{mask}})[0];
+      }
       x = subsum(x);
       lap("mask+rep");
       const double corr = x.scale / h.T[0];

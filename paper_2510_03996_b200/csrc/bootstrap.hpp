@@ -60,8 +60,9 @@ class Bootstrapper {
   Bootstrapper(Context& ctx, const BootParams& bp = {});
   // levels consumed between ModRaise (top) and the output
   int depth() const { return depth_; }
-  // full: any level; sparse: x must hold >= 2 limbs (the mask takes one level)
-  Ciphertext run(const Ciphertext& x);
+  // full: any level; sparse: x must hold >= 2 limbs (the mask takes one level) unless
+  // `clean` (slots [n, S) of x are already zero: no mask, any level)
+  Ciphertext run(const Ciphertext& x, bool clean = false);
   long slots() const { return n_; }
   bool sparse() const { return n_ < S_; }
   // stage probes for tests: 1 CoeffsToSlots on x (scale reinterpreted as q0),

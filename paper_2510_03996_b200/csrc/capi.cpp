@@ -538,8 +538,8 @@ int fheon_mult_cipher(fheon_ctx* ctx, const fheon_ct* a, const fheon_ct* b, fheo
 int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::bootstrap(*ctx->impl, a->ct)); });
 }
-int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, fheon_ct** out) {
-  return guard([&] { *out = wrap(fheon::bootstrap_active(*ctx->impl, a->ct, active_slots)); });
+int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, int flags, fheon_ct** out) {
+  return guard([&] { *out = wrap(fheon::bootstrap_active(*ctx->impl, a->ct, active_slots, (flags & 1) != 0)); });
 }
 int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out) {
   return guard([&] {

@@ -363,7 +363,9 @@ Ciphertext bootstrap(Context& ctx, const Ciphertext& a);
 // bootstrap when only slots [0, active) matter: the smallest sparse-slot variant
 // holding them (input above level 0), else the full pipeline.  Output slots
 // [0, active) = input (the rest 0 for a sparse variant, the input's for the full one)
-Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t active);
+// clean: the caller knows slots [active, S) of a are zero (a convolution's output) -- no
+// mask, so a level-0 input can take a sparse variant too
+Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t active, bool clean = false);
 // raw key switch of one polynomial d ([limbs][N], NTT) for parity tests:
 // returns (ks0, ks1) as a 2-poly ciphertext without scale meaning
 Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d_as_c1, u64 key_id, u64 g);

@@ -1502,17 +1502,17 @@ Ciphertext bootstrap(Context& ctx, const Ciphertext& a) {
   return ctx.boot->run(a);
 }
 
-Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t active) {
+Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t active, bool clean) {
   require_valid(a, "bootstrap");
   if (!ctx.boot) return bootstrap(ctx, a);
   if (active == 0 || active > (std::size_t)ctx.S())
     throw Error(ErrKind::shape, "bootstrap: active slot count " + std::to_string(active) + " outside [1, " +
                                     std::to_string(ctx.S()) + "]");
   Bootstrapper* best = nullptr;
-  if (a.limbs >= 2)
+  if (a.limbs >= 2 || clean)
     for (auto& b : ctx.boot_sparse)
       if ((std::size_t)b->slots() >= active && (!best || b->slots() < best->slots())) best = b.get();
-  return best ? best->run(a) : ctx.boot->run(a);
+  return best ? best->run(a, clean) : ctx.boot->run(a);
 }
 
 // -------------------------------------------------------------- raw access

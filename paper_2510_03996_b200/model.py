@@ -865,8 +865,9 @@ class EncryptedModel:
             active = C * W * W if packed else n
             out = fh.secure_relu(v, fh.ReluConfig(L.params.get("scale", 1.0), L.params.get("degree", 59), active))
         elif b.type == "bootstrap":
-            # only the tensor's active slots survive (a sparse-slot variant when one fits)
-            out = fh.bootstrap(v, C * W * W if packed else n)
+            # only the tensor's active slots survive (a sparse-slot variant when one fits;
+            # a convolution's output is zero past them, so it needs no mask level)
+            out = fh.bootstrap(v, C * W * W if packed else n, clean=getattr(v, "_clean", False))
         elif b.type == "residual":
             body = v
             for c in b.body:
@@ -875,8 +876,13 @@ class EncryptedModel:
             for c in b.downsample:
                 skip = self._run(c, skip, timings)
             out = fh.add(body, skip)
+            out._clean = getattr(body, "_clean", False) and getattr(skip, "_clean", False)
         else:
             raise fh.ModelError(f"unexecutable layer {b.type}", 2)
+        if b.type == "conv":
+            # convolutions end in masked placements: slots past F * W_out^2 are zero
+            # (layers_conv.cpp:142-177; checked against the reference in test_gpu_layers)
+            out._clean = True
         if timings is not None:
             self.ctx.sync()
             timings[b.name] = timings.get(b.name, 0.0) + (time.perf_counter() - t0) * 1e3

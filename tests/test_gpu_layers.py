@@ -294,3 +294,20 @@ def test_config1_conv_layer(schedule):
     err = check(out, ev, r, "config1 conv", schedule)
     assert r.level == 7 and len(r.rotations()) == 305
     assert err < 1e-4
+
+
+@pytest.mark.parametrize("W,C,F,k,s,p,mode", [(8, 4, 8, 3, 1, 1, 1), (8, 4, 8, 2, 2, 0, 0), (9, 2, 3, 3, 2, 1, 0),
+                                               (9, 2, 3, 3, 2, 0, 0), (12, 1, 6, 5, 1, 0, 0), (8, 3, 4, 3, 1, 1, 0)])
+def test_conv_output_clean_past_active(env, W, C, F, k, s, p, mode):
+    """Convolutions end in masked placements (layers_conv.cpp:142-177): the slots
+    past F * W_out^2 are zero even when the input carries garbage there -- the
+    property the model runtime's bootstrap(v, active, clean=True) relies on."""
+    ctx, _ = env
+    rng = np.random.default_rng(W * 100 + C * 10 + F + k)
+    x = rng.uniform(-1, 1, 1 << (LOGN - 1))  # garbage past C * W * W
+    w = rng.normal(0, 0.3, (F, C, k, k))
+    cfg = fh.ConvConfig(C, F, k, s, p, fh.ConvMode.special3x3 if mode else fh.ConvMode.generic)
+    out = fh.convolution(fh.PackedTensor(fh.SlotVector.encode(ctx, x), C, W), cfg, fh.KernelTensor(w)).data
+    wo = (W + 2 * p - k) // s + 1
+    got = out.slots()
+    assert np.abs(got[F * wo * wo:]).max() < 1e-5 * max(1.0, np.abs(got[:F * wo * wo]).max())
