@@ -157,6 +157,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_bconv_tc(TcBconvArgs a) {
     bx = (int)blockIdx.x - a.cta0[d];
     gx = a.cta0[d + 1] - a.cta0[d];
   }
+  FHEON_DCHECK(T >= 1 && T <= kTcMaxT && KIN >= 1 && KIN <= KINP && nin <= KIN && (MODE != 0 || a.ndig <= kMaxDigits) &&
+               bx >= 0 && gx >= 1);
   const int Tp = (T + kTcTargets - 1) / kTcTargets * kTcTargets;
   const std::size_t N = (std::size_t)1 << a.logN;
   const int E = a.limbs + a.K;

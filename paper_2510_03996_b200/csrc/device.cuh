@@ -12,6 +12,9 @@
 #pragma once
 
 #include <cstdint>
+#ifdef FHEON_DEVICE_CHECKS
+#include <cstdio>
+#endif
 
 namespace fheon {
 
@@ -78,6 +81,25 @@ struct LimbSet {
 
 #ifdef __CUDACC__
 
+// Device bounds checks (the checked build, make CHECKS=1 -> FHEON_DEVICE_CHECKS): an
+// index outside its buffer prints the kernel's file:line and traps the launch, so
+// the host call fails loudly instead of reading or corrupting neighbouring words.
+// compute-sanitizer is closed on this GPU pool; this is what stands in.
+#ifdef FHEON_DEVICE_CHECKS
+#define FHEON_DCHECK(cond)                                                                                 \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("FHEON_DCHECK failed: %s at %s:%d (block %d,%d,%d thread %d)\n", #cond, __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x);                           \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define FHEON_DCHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
+
 __device__ __forceinline__ u64 mulhi(u64 a, u64 b) { return __umul64hi(a, b); }
 
 __device__ __forceinline__ u64 csub(u64 x, u64 q) { return x >= q ? x - q : x; }
@@ -139,8 +161,10 @@ __device__ __forceinline__ bool limbset_get(const LimbSet& s, int idx, std::size
     const int j = blk % s.skip_digits;
     if (t >= s.dig.lo(j) && t < s.dig.hi(j, s.ell)) return false;
   }
+  FHEON_DCHECK(b >= 0 && b < s.nbase && b < kMaxBases && blk < s.blocks_per_base && t < s.E);
   ptr = s.base[b] + (long long)blk * s.block_stride + (long long)t * (long long)N;
   prime = t < s.ell ? s.p0 + t : s.L + (t - s.ell);
+  FHEON_DCHECK(ptr != nullptr && prime >= 0 && prime < 64 + 16);
   return true;
 }
 
@@ -166,6 +190,7 @@ __device__ __forceinline__ unsigned auto_src(unsigned i, u64 g, int logN) {
   const u64 M = 2ULL << logN;
   const u64 e = 2ULL * brev_bits(i, logN) + 1ULL;
   const u64 eg = (e * g) & (M - 1);
+  FHEON_DCHECK((g & 1) == 1 && i < (1u << logN));  // Galois elements are odd
   return brev_bits((unsigned)((eg - 1) >> 1), logN);
 }
 

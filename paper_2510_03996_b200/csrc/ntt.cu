@@ -199,7 +199,9 @@ __global__ void __launch_bounds__(Geometry<LOGM, COL, SMALL>::THREADS,
   const int tp = COL ? (int)(threadIdx.x / LPC) : (int)(threadIdx.x % T);
   u64* lsm = sm + li * LS;
   auto gaddr = [&](int k) -> std::size_t {
-    return COL ? (std::size_t)k * N2 + line0 + li : (std::size_t)(line0 + li) * N2 + k;
+    const std::size_t a = COL ? (std::size_t)k * N2 + line0 + li : (std::size_t)(line0 + li) * N2 + k;
+    FHEON_DCHECK(a < N && k < G::M && li < LPC);
+    return a;
   };
 
   u64 x[E];

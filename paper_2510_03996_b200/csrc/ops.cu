@@ -192,6 +192,7 @@ __global__ void k_ks_inner(KsJobs jobs, const PrimeConst* __restrict__ pc, int l
   const unsigned src1 = (g == 1) ? n + 1 : auto_src(n + 1, g, logN);
   const int beta = dig.beta;
   const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;  // CTA-uniform: limb t's own digit passes d through
+  FHEON_DCHECK(r < jobs.n && t < E && beta >= 1 && beta <= kMaxDigits && jown < beta && n + 1 < N);
   const u64* key = jobs.key[r];
   const u64* ext = jobs.ext[r];
   const u64* d = jobs.d[r];
@@ -251,6 +252,9 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
   const int jown = t < limbs ? (int)__ldg(dig.owner + t) : -1;
   const u64 pm = t < limbs ? md_q[(std::size_t)t * 4] : 0;  // P mod q_t, Montgomery form
   const std::size_t LKN = (std::size_t)(L + K) * N;
+  FHEON_DCHECK(r < jobs.ngroups && r < kMaxSumGroups && t < E && beta >= 1 && beta <= kMaxDigits && jown < beta &&
+               n + 1 < N && jobs.begin[r] >= 0 && jobs.begin[r + 1] <= kMaxSumJobs &&
+               jobs.begin[r] <= jobs.begin[r + 1]);
   u64 s0[2] = {0, 0}, s1[2] = {0, 0};
   const int chunk = lazy_chunk(beta);
   Acc128 a0[2], a1[2];
@@ -433,6 +437,7 @@ __global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN,
   const int t = (int)blockIdx.z;
   const PrimeConst P = pc[t < ell ? t : L + (t - ell)];
   const int nt = jobs.nterm[z];
+  FHEON_DCHECK(z < jobs.nout && z < kMacMaxOut && nt >= 1 && nt <= kMacMaxTerms);
   u64 s0[2] = {0, 0}, s1[2] = {0, 0};
   Acc128 a0[2], a1[2];
   for (int j = 0; j < nt; ++j) {  // nt <= kMacMaxTerms = 32 products < 32 q^2: one lazy flush
