@@ -356,6 +356,14 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
     if (ctx.has_secret() && !ctx.inheriting_keys) ctx.gen_key(ctx.galois(s));
     ctx.pin_key(ctx.galois(s));
   }
+  if (sparse()) {  // conj o rot_G for the last CtS level's giant steps
+    const u64 twoN = 2 * (u64)h.N;
+    for (const Giant& gi : cts_.back().giants) {
+      const u64 gc = (ctx.galois(gi.rot) * (twoN - 1)) % twoN;
+      if (ctx.has_secret() && !ctx.inheriting_keys) ctx.gen_key(gc);
+      ctx.pin_key(gc);
+    }
+  }
   if (ctx.has_secret() && !ctx.inheriting_keys) {
     ctx.gen_key(2 * (u64)h.N - 1);  // conjugation
     ctx.gen_key(0);                 // relinearisation
@@ -382,7 +390,7 @@ std::vector<long> Bootstrapper::rotation_steps() const {
   return std::vector<long>(s.begin(), s.end());
 }
 
-Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv) {
+Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv, bool with_conj) {
   if (lv.qp) {
     std::map<long, int> idx;
     for (std::size_t i = 0; i < lv.babies.size(); ++i) idx[lv.babies[i]] = (int)i;
@@ -393,7 +401,7 @@ Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv) {
       for (const auto& [b, pt] : g.terms) d.terms.push_back({b == 0 ? -1 : idx.at(b), pt});
       gs.push_back(std::move(d));
     }
-    return bsgs_double_hoisted(ctx_, x, lv.babies, gs);
+    return bsgs_double_hoisted(ctx_, x, lv.babies, gs, with_conj);
   }
   std::vector<Ciphertext> rot = rotate_hoisted(ctx_, x, lv.babies);
   std::map<long, Ciphertext> by_b;
@@ -416,7 +424,7 @@ Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv) {
   std::vector<Ciphertext> inner = mac_plain_many_unrescaled(ctx_, terms, pts);
   std::vector<std::pair<Ciphertext, long>> g;
   for (std::size_t i = 0; i < lv.giants.size(); ++i) g.push_back({inner[i], lv.giants[i].rot});
-  return rotate_sum_to_target(ctx_, {g})[0];
+  return rotate_sum_to_target(ctx_, {g}, true, with_conj)[0];
 }
 
 Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {
@@ -494,12 +502,13 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
       lap("modraise");
       y = subsum(y);
       lap("trace");
-      for (const Level& lv : cts_) {
-        y = apply(y, lv);
+      // the last CtS level returns y + conj(y) directly: its giant steps enter twice, as
+      // rot_G and conj o rot_G, in one ModDown (no separate conjugation key switch)
+      for (std::size_t i = 0; i < cts_.size(); ++i) {
+        y = apply(y, cts_[i], i + 1 == cts_.size());
         lap("cts");
       }
-      std::vector<Ciphertext> ys = {add(ctx_, y, conjugate_many(ctx_, {y})[0])};
-      lap("conj");
+      std::vector<Ciphertext> ys = {y};
       static const char* prof = std::getenv("FHEON_BOOT_PROFILE");  // ncu range: "cos"
       const bool prof_cos = prof && std::string(prof) == "cos";
       if (prof_cos) FHEON_CUDA(cudaProfilerStart());

@@ -94,7 +94,8 @@ class Bootstrapper {
   // periods[i]: group i's input is periods[i]-periodic (S: no structure)
   std::vector<Level> plan(const std::vector<Mat>& groups, int limbs_in, double scale_in,
                           const std::vector<long>& periods);
-  Ciphertext apply(const Ciphertext& x, const Level& lv);
+  // with_conj: returns T x + conj(T x) (the conjugated giant steps join the same ModDown)
+  Ciphertext apply(const Ciphertext& x, const Level& lv, bool with_conj = false);
   // sum_{j < S/n} rot(x, j n): one hoisted rotate-and-sum
   Ciphertext subsum(const Ciphertext& x);
 

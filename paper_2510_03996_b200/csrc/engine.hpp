@@ -307,9 +307,11 @@ std::vector<Ciphertext> mac_plain_many_unrescaled(Context& ctx, const std::vecto
 // rescale_to_target(rotate_sum_many(groups)) with each group's rescale folded into its
 // ModDown (one rounding by P q_l); identity terms join before the division
 // (record_identity: trace the t = 0 terms as rotations, as rotate_sum_many does)
+// with_conj: every term also enters conjugated (Galois element -5^t: the sum becomes
+// out + conj(out) in the same ModDown; keys for conj o rot_t must be resident)
 std::vector<Ciphertext> rotate_sum_to_target(Context& ctx,
                                              const std::vector<std::vector<std::pair<Ciphertext, long>>>& groups,
-                                             bool record_identity = true);
+                                             bool record_identity = true, bool with_conj = false);
 // rescale unrescaled MAC outputs onto the next level's target scale
 std::vector<Ciphertext> rescale_to_target(Context& ctx, const std::vector<Ciphertext>& prods);
 std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b);
@@ -349,7 +351,7 @@ struct DhGiant {
   std::vector<std::pair<int, BufPtr>> terms;
 };
 Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& babies,
-                               const std::vector<DhGiant>& giants);
+                               const std::vector<DhGiant>& giants, bool with_conj = false);
 Ciphertext add(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext sub(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext add_plain(Context& ctx, const Ciphertext& a, const double* vals, std::size_t n);

@@ -535,7 +535,7 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
 // inner sum needs ONE ModDown instead of one per baby; the giant rotations are a
 // rotate-and-sum (one more ModDown) and the sum is rescaled once.
 Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& babies,
-                               const std::vector<DhGiant>& giants) {
+                               const std::vector<DhGiant>& giants, bool with_conj) {
   require_valid(x, "linear transform");
   require_depth(x, "linear transform");
   const DevTables& t = ctx.dev();
@@ -607,7 +607,7 @@ Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vec
       ctx.record(1, lv - 1);
     }
   }
-  return rotate_sum_to_target(ctx, {terms})[0];
+  return rotate_sum_to_target(ctx, {terms}, true, with_conj)[0];
 }
 
 // out[r] = sum_k rot(groups[r][k].first, groups[r][k].second): every group's
@@ -682,7 +682,7 @@ std::vector<Ciphertext> rotate_sum_many(Context& ctx, const std::vector<std::vec
 // linear transform); outputs land on T_{l-1}.  Records one rotation event per term.
 std::vector<Ciphertext> rotate_sum_to_target(Context& ctx,
                                              const std::vector<std::vector<std::pair<Ciphertext, long>>>& groups,
-                                             bool record_identity) {
+                                             bool record_identity, bool with_conj) {
   if (groups.empty()) return {};
   const long S = ctx.S();
   const int limbs = groups[0].at(0).first.limbs;
@@ -690,6 +690,13 @@ std::vector<Ciphertext> rotate_sum_to_target(Context& ctx,
   for (const auto& g : groups) {
     if (g.empty()) throw Error(ErrKind::internal, "rotate_sum: empty group");
     for (const auto& [x, tt] : g) fused = fused && x.limbs == limbs;
+  }
+  const u64 conj = 2 * (u64)ctx.N() - 1;
+  const u64 twoN = 2 * (u64)ctx.N();
+  if (!fused && with_conj) {  // out + conj(out) the plain way
+    std::vector<Ciphertext> o = rescale_to_target(ctx, rotate_sum_many(ctx, groups));
+    std::vector<Ciphertext> c = conjugate_many(ctx, o);
+    return add_many(ctx, o, c);
   }
   if (!fused) return rescale_to_target(ctx, rotate_sum_many(ctx, groups));
   std::vector<const u64*> inputs, c0s;
@@ -712,18 +719,25 @@ std::vector<Ciphertext> rotate_sum_to_target(Context& ctx,
         ctx.record(0, tt);
         ctx.stats.rotations++;
       }
+      if (with_conj) ++in_group;  // the conjugated term is always key-switched
       if (g == 1) {
         direct[r] = direct[r].valid() ? add(ctx, direct[r], x) : x;
         continue;
       }
       ++in_group;
     }
-    if (in_group > kMaxSumJobs) return rescale_to_target(ctx, rotate_sum_many(ctx, groups));
+    if (in_group > kMaxSumJobs) {
+      if (with_conj) {
+        std::vector<Ciphertext> o = rescale_to_target(ctx, rotate_sum_many(ctx, groups));
+        return add_many(ctx, o, conjugate_many(ctx, o));
+      }
+      return rescale_to_target(ctx, rotate_sum_many(ctx, groups));
+    }
     if (in_group == 0) continue;
     gidx[r] = nacc++;
     for (const auto& [x, tt] : groups[r]) {
       const u64 g = ctx.galois(tt);
-      if (g == 1) continue;
+      if (g == 1 && !with_conj) continue;
       auto it = slot.find(x.c1);
       int in;
       if (it == slot.end()) {
@@ -734,7 +748,8 @@ std::vector<Ciphertext> rotate_sum_to_target(Context& ctx,
       } else {
         in = it->second;
       }
-      jobs.push_back({g, in, gidx[r]});
+      if (g != 1) jobs.push_back({g, in, gidx[r]});
+      if (with_conj) jobs.push_back({(g * conj) % twoN, in, gidx[r]});  // conj o rot_t
     }
   }
   const int lv = limbs - 1;
