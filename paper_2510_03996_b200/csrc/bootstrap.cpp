@@ -515,9 +515,8 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
       ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
       if (prof_cos) FHEON_CUDA(cudaProfilerStop());
       lap("cos");
-      for (int i = 0; i < bp_.double_angles; ++i) {
-        std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
-        ys = add_many(ctx_, sq, sq);
+      for (int i = 0; i < bp_.double_angles; ++i) {  // y <- 2 y^2 - 1
+        ys = mult_cipher_cheb_many(ctx_, ys, ys, std::vector<Ciphertext>(ys.size()));
         for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
       }
       lap("dbl-angle");
@@ -574,9 +573,8 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
       std::fprintf(stderr, "[boot] cos poly out limbs %d scale 2^%.2f err %.3e\n", ys[0].limbs, std::log2(ys[0].scale),
                    maxdiff(bre, w));
     }
-    for (int i = 0; i < bp_.double_angles; ++i) {
-      std::vector<Ciphertext> sq = mult_cipher_many(ctx_, ys, ys);
-      ys = add_many(ctx_, sq, sq);
+    for (int i = 0; i < bp_.double_angles; ++i) {  // y <- 2 y^2 - 1
+      ys = mult_cipher_cheb_many(ctx_, ys, ys, std::vector<Ciphertext>(ys.size()));
       for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
     }
     if (dbg) {

@@ -323,6 +323,10 @@ Ciphertext encrypt_at(Context& ctx, const double* vals, std::size_t n, int limbs
 Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt);
 std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphertext>& as,
                                          const std::vector<Ciphertext>& bs);
+// 2 a_i b_i - subs_i (subs_i may be invalid: 2 a_i b_i), the Chebyshev recurrence step,
+// in one relinearise-and-rescale (the subtrahend joins before the rescale)
+std::vector<Ciphertext> mult_cipher_cheb_many(Context& ctx, const std::vector<Ciphertext>& as,
+                                              const std::vector<Ciphertext>& bs, const std::vector<Ciphertext>& subs);
 std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Ciphertext>& as, const std::vector<double>& cs);
 // sum_i cs[i] * xs[i] + c0 with one rescale (terms may sit at different levels)
 Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0);

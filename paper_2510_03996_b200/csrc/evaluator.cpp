@@ -1363,6 +1363,75 @@ std::vector<Ciphertext> mult_cipher_many(Context& ctx, const std::vector<Ciphert
   return outs;
 }
 
+// 2 a_i b_i - s_i (s_i invalid: 2 a_i b_i) with the subtraction and the doubling folded
+// into the tensor product, ahead of ONE relinearise-and-rescale: the Chebyshev
+// recurrence step T_{a+b} = 2 T_a T_b - T_{a-b} without bringing T_{a-b} down a level
+// (no level_down rescale).  s_i is read at the product's limbs (zero-copy drop) and
+// multiplied by the integer k = round(scale(a) scale(b) / scale(s)) (>= 2^30 -- the
+// same rounding level_down applies).  Same trace events as mult_cipher_many.
+std::vector<Ciphertext> mult_cipher_cheb_many(Context& ctx, const std::vector<Ciphertext>& as,
+                                              const std::vector<Ciphertext>& bs, const std::vector<Ciphertext>& subs) {
+  if (as.size() != bs.size() || as.size() != subs.size())
+    throw Error(ErrKind::internal, "mult_cipher_cheb_many: size mismatch");
+  std::vector<Ciphertext> outs(as.size());
+  if (as.empty()) return outs;
+  std::vector<Ciphertext> A(as.size()), B(bs.size());
+  for (std::size_t i = 0; i < as.size(); ++i) {
+    require_valid(as[i], "mult_cipher");
+    require_valid(bs[i], "mult_cipher");
+    require_depth(as[i], "mult_cipher");
+    require_depth(bs[i], "mult_cipher");
+    A[i] = as[i];
+    B[i] = bs[i];
+    align(ctx, A[i], B[i]);
+  }
+  std::map<int, std::vector<std::size_t>> by_level;
+  for (std::size_t i = 0; i < A.size(); ++i) by_level[A[i].limbs].push_back(i);
+  const std::size_t N = ctx.N();
+  const HostTables& h = ctx.host();
+  for (auto& [l, idx] : by_level) {
+    const std::size_t P = (std::size_t)l * N;
+    BufPtr d = ctx.alloc(3 * P * idx.size());
+    std::vector<const u64*> inputs;
+    std::vector<KsJob> jobs;
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      const std::size_t i = idx[k];
+      u64* d0 = d->ptr + 3 * P * k;
+      const Ciphertext& s = subs[i];
+      LimbConsts kc{};
+      const u64 *s0 = nullptr, *s1 = nullptr;
+      if (s.valid()) {
+        if (s.limbs < l) throw Error(ErrKind::internal, "mult_cipher_cheb: subtrahend below the product");
+        const double c = A[i].scale * B[i].scale / s.scale;
+        if (!(c >= 1073741824.0) || !(c < 4.6e18))
+          throw Error(ErrKind::internal, "mult_cipher_cheb: subtrahend scale out of range");
+        const long long kk = std::llround(c);
+        for (int q = 0; q < l; ++q) {
+          kc.c[q] = signed_mod(kk, h.q[q]);
+          kc.sh[q] = shoup(kc.c[q], h.q[q]);
+        }
+        s0 = s.c0;
+        s1 = s.c1;
+      }
+      ew_tensor_cheb(ctx.dev(), d0, d0 + P, d0 + 2 * P, A[i].c0, A[i].c1, B[i].c0, B[i].c1, s0, s1, kc, l,
+                     ctx.stream());
+      inputs.push_back(d0 + 2 * P);
+      KsJob jb{0, 1, d0, 1, d0 + P};
+      jb.in = (int)k;
+      jobs.push_back(jb);
+    }
+    std::vector<Ciphertext> rs = keyswitch_relin_rescale(ctx, inputs, l, jobs);
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      const std::size_t i = idx[k];
+      rs[k].scale = A[i].scale * B[i].scale / (double)h.q[l - 1];
+      outs[i] = rs[k];
+      ctx.stats.mult_cipher++;
+    }
+  }
+  for (const Ciphertext& o : outs) ctx.record(2, o.level());
+  return outs;
+}
+
 // a_i * c_i (constant vectors) with one batched rescale per level
 std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Ciphertext>& as, const std::vector<double>& cs) {
   std::vector<Ciphertext> outs(as.size());

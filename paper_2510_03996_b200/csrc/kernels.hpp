@@ -128,6 +128,10 @@ void lincomb_const(const DevTables& t, u64* out0, u64* out1, const LincombTerms&
 // (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1)
 void ew_tensor(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
                const u64* b1, int limbs, cudaStream_t st);
+// d = 2 (a (x) b) - k (s0, s1, 0): the Chebyshev step 2 T_a T_b - T_{a-b} before its
+// relinearise-and-rescale (s0 = nullptr: doubling only)
+void ew_tensor_cheb(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
+                    const u64* b1, const u64* s0, const u64* s1, const LimbConsts& kc, int limbs, cudaStream_t st);
 // out[p] = sigma_{g[p]}(in[p]) in the NTT domain
 void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int limbs, cudaStream_t st);
 

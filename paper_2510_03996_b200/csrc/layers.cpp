@@ -1645,20 +1645,21 @@ std::vector<Ciphertext> cheb_eval_ps_many(Context& ctx, const std::vector<Cipher
   };
   for (int lo = 2; lo <= nb; lo = lo * 2 - 1) {
     const int hi = std::min(nb, 2 * lo - 2 > lo ? 2 * lo - 2 : lo);
-    std::vector<Ciphertext> as, bs;
+    // T_d = 2 T_a T_b - T_{a-b}: T_1 (odd d) is subtracted inside the product's
+    // relinearise-and-rescale (mult_cipher_cheb_many), T_0 = 1 (even d) afterwards
+    std::vector<Ciphertext> as, bs, subs;
     for (std::size_t i = 0; i < B; ++i)
       for (int d = lo; d <= hi; ++d) {
         const int a = (d + 1) / 2, b = d / 2;
         const int l = std::min(T[i][a].limbs, T[i][b].limbs);
         as.push_back(at(i, a, l));
         bs.push_back(at(i, b, l));
+        subs.push_back(d % 2 == 0 ? Ciphertext{} : T[i][1]);
       }
-    std::vector<Ciphertext> prods = mult_cipher_many(ctx, as, bs);
-    std::vector<Ciphertext> doubled = add_many(ctx, prods, prods);
+    std::vector<Ciphertext> prods = mult_cipher_cheb_many(ctx, as, bs, subs);
     std::size_t j = 0;
     for (std::size_t i = 0; i < B; ++i)
-      for (int d = lo; d <= hi; ++d, ++j)
-        T[i][d] = (d % 2 == 0) ? add_const(ctx, doubled[j], -1.0) : sub(ctx, doubled[j], at(i, 1, doubled[j].limbs));
+      for (int d = lo; d <= hi; ++d, ++j) T[i][d] = (d % 2 == 0) ? add_const(ctx, prods[j], -1.0) : prods[j];
     if (hi == nb) break;
   }
   // giants G_0 = T_k, G_j = 2 G_{j-1}^2 - 1
@@ -1668,8 +1669,7 @@ std::vector<Ciphertext> cheb_eval_ps_many(Context& ctx, const std::vector<Cipher
   for (int j = 1; j < best_m; ++j) {
     std::vector<Ciphertext> g;
     for (std::size_t i = 0; i < B; ++i) g.push_back(G[i].back());
-    std::vector<Ciphertext> sq = mult_cipher_many(ctx, g, g);
-    std::vector<Ciphertext> dbl = add_many(ctx, sq, sq);
+    std::vector<Ciphertext> dbl = mult_cipher_cheb_many(ctx, g, g, std::vector<Ciphertext>(g.size()));
     for (std::size_t i = 0; i < B; ++i) G[i].push_back(add_const(ctx, dbl[i], -1.0));
   }
   std::vector<int> tl(B);

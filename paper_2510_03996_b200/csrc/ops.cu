@@ -119,6 +119,33 @@ __global__ void k_tensor(u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1
   d1[o] = redc(mulhi(tm, P.r2), tm * P.r2, P.q, P.qinv_neg);
   d2[o] = mul_mod(x1, y1, P);
 }
+// Chebyshev step 2 a (x) b - k s before the relinearise-and-rescale: d = 2 (a (x) b)
+// on all three parts, minus k s on d0 / d1 (s: the step's subtrahend T_{a-b} viewed
+// at these limbs, k ~ scale(a) scale(b) / scale(s) so it lands on the product's scale)
+__global__ void k_tensor_cheb(u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0, const u64* b1,
+                              const u64* s0, const u64* s1, LimbConsts kc, const PrimeConst* __restrict__ pc,
+                              int logN) {
+  const std::size_t o = ((std::size_t)blockIdx.y << logN) + blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst P = pc[blockIdx.y];
+  const u64 x0 = a0[o], x1 = a1[o], y0 = b0[o], y1 = b1[o];
+  u64 t0 = mul_mod(x0, y0, P);
+  Acc128 c;
+  c.mac(x0, y1);
+  c.mac(x1, y0);
+  const u64 tm = redc(c.hi, c.lo, P.q, P.qinv_neg);
+  u64 t1 = redc(mulhi(tm, P.r2), tm * P.r2, P.q, P.qinv_neg);
+  const u64 t2 = mul_mod(x1, y1, P);
+  t0 = add_mod(t0, t0, P.q);
+  t1 = add_mod(t1, t1, P.q);
+  if (s0 != nullptr) {
+    const u64 k = kc.c[blockIdx.y], ksh = kc.sh[blockIdx.y];
+    t0 = sub_mod(t0, shoup_mul(s0[o], k, ksh, P.q), P.q);
+    t1 = sub_mod(t1, shoup_mul(s1[o], k, ksh, P.q), P.q);
+  }
+  d0[o] = t0;
+  d1[o] = t1;
+  d2[o] = add_mod(t2, t2, P.q);
+}
 __global__ void k_automorph(PolyList out, PolyList in, int logN) {
   const unsigned n = blockIdx.x * blockDim.x + threadIdx.x;
   const std::size_t base = (std::size_t)blockIdx.y << logN;
@@ -654,6 +681,11 @@ void ew_tensor(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, con
                const u64* b1, int limbs, cudaStream_t st) {
   k_tensor<<<grid_for(t.N, limbs), kThreads, 0, st>>>(d0, d1, d2, a0, a1, b0, b1, t.pc, t.logN);
   launch_check("k_tensor");
+}
+void ew_tensor_cheb(const DevTables& t, u64* d0, u64* d1, u64* d2, const u64* a0, const u64* a1, const u64* b0,
+                    const u64* b1, const u64* s0, const u64* s1, const LimbConsts& kc, int limbs, cudaStream_t st) {
+  k_tensor_cheb<<<grid_for(t.N, limbs), kThreads, 0, st>>>(d0, d1, d2, a0, a1, b0, b1, s0, s1, kc, t.pc, t.logN);
+  launch_check("k_tensor_cheb");
 }
 void automorph(const DevTables& t, const PolyList& out, const PolyList& in, int limbs, cudaStream_t st) {
   if (out.n == 0 || limbs == 0) return;
