@@ -331,6 +331,15 @@ std::vector<Ciphertext> mult_const_many(Context& ctx, const std::vector<Cipherte
 // sum_i cs[i] * xs[i] + c0 with one rescale (terms may sit at different levels)
 Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0);
 // the same landing exactly on (out_limbs, out_scale); every term needs >= out_limbs + 1 limbs
+struct LincombItem {
+  std::vector<Ciphertext> xs;
+  std::vector<double> cs;
+  double c0 = 0.0;
+  int out_limbs = 0;
+  double out_scale = 0.0;
+};
+// several lincomb_const_to at once: the rescales of one level batched
+std::vector<Ciphertext> lincomb_const_to_many(Context& ctx, const std::vector<LincombItem>& items);
 Ciphertext lincomb_const_to(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0,
                             int out_limbs, double out_scale);
 

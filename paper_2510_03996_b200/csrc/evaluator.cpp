@@ -1488,8 +1488,11 @@ Ciphertext lincomb_const(Context& ctx, const std::vector<Ciphertext>& xs, const 
 // The sum is formed at out_limbs + 1 limbs (terms' tails ignored), each constant
 // scaled by out_scale q_{out_limbs} / scale(x_i) and rounded, then ONE rescale:
 // the result lands exactly on (out_limbs, out_scale).
-Ciphertext lincomb_const_to(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0,
-                            int out_limbs, double out_scale) {
+namespace {
+// sum_i k_i x_i at out_limbs + 1 limbs with k_i = round(c_i out_scale q_{out_limbs} / scale(x_i)):
+// the unrescaled part of lincomb_const_to
+Ciphertext lincomb_const_sum(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs,
+                             int out_limbs, double out_scale) {
   if (xs.empty() || xs.size() != cs.size()) throw Error(ErrKind::internal, "lincomb_const: bad term list");
   const int l = out_limbs + 1;
   for (const Ciphertext& x : xs) {
@@ -1538,11 +1541,40 @@ Ciphertext lincomb_const_to(Context& ctx, const std::vector<Ciphertext>& xs, con
              ctx.stream());
     }
   }
-  Ciphertext out = rescale(ctx, sum);
-  out.scale = t_out;
-  ctx.stats.mult_plain += n;
-  for (std::size_t i = 0; i < n; ++i) ctx.record(1, out.level());
+  return sum;
+}
+
+Ciphertext lincomb_finish(Context& ctx, Ciphertext out, std::size_t nterms, double c0, double out_scale) {
+  out.scale = out_scale;
+  ctx.stats.mult_plain += nterms;
+  for (std::size_t i = 0; i < nterms; ++i) ctx.record(1, out.level());
   return c0 != 0.0 ? add_const(ctx, out, c0) : out;
+}
+}  // namespace
+
+Ciphertext lincomb_const_to(Context& ctx, const std::vector<Ciphertext>& xs, const std::vector<double>& cs, double c0,
+                            int out_limbs, double out_scale) {
+  Ciphertext sum = lincomb_const_sum(ctx, xs, cs, out_limbs, out_scale);
+  return lincomb_finish(ctx, rescale(ctx, sum), xs.size(), c0, out_scale);
+}
+
+std::vector<Ciphertext> lincomb_const_to_many(Context& ctx, const std::vector<LincombItem>& items) {
+  std::vector<Ciphertext> sums(items.size()), outs(items.size());
+  std::map<int, std::vector<std::size_t>> by_level;
+  for (std::size_t i = 0; i < items.size(); ++i) {
+    sums[i] = lincomb_const_sum(ctx, items[i].xs, items[i].cs, items[i].out_limbs, items[i].out_scale);
+    by_level[sums[i].limbs].push_back(i);
+  }
+  for (auto& [l, idx] : by_level) {  // one batched rescale per level
+    std::vector<Ciphertext> in;
+    for (std::size_t i : idx) in.push_back(sums[i]);
+    std::vector<Ciphertext> r = rescale_many(ctx, in);
+    for (std::size_t k = 0; k < idx.size(); ++k) {
+      const LincombItem& it = items[idx[k]];
+      outs[idx[k]] = lincomb_finish(ctx, r[k], it.xs.size(), it.c0, it.out_scale);
+    }
+  }
+  return outs;
 }
 
 std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a, const std::vector<Ciphertext>& b) {

@@ -1552,7 +1552,11 @@ std::vector<PsVal> ps_eval(Context& ctx, const PsNode& root, std::vector<std::ve
   std::vector<PsTask> tasks;
   ps_plan(ctx, root, G, tl, ts, tasks);
   int H = 0;
-  for (PsTask& t : tasks) {
+  // every leaf (constant linear combination of babies) at once: one rescale per level
+  std::vector<LincombItem> items;
+  std::vector<std::pair<std::size_t, std::size_t>> where;  // (task, input)
+  for (std::size_t k = 0; k < tasks.size(); ++k) {
+    PsTask& t = tasks[k];
     H = std::max(H, t.height);
     if (!t.nd->leaf) continue;
     t.val.resize(B);
@@ -1561,16 +1565,21 @@ std::vector<PsVal> ps_eval(Context& ctx, const PsNode& root, std::vector<std::ve
         t.val[i].c = t.nd->c.empty() ? 0.0 : t.nd->c[0];
         continue;
       }
-      std::vector<Ciphertext> xs;
-      std::vector<double> cs;
+      LincombItem it;
       for (std::size_t d = 1; d < t.nd->c.size(); ++d)
         if (t.nd->c[d] != 0.0) {
-          xs.push_back(T[i][d]);
-          cs.push_back(t.nd->c[d]);
+          it.xs.push_back(T[i][d]);
+          it.cs.push_back(t.nd->c[d]);
         }
-      t.val[i].ct = lincomb_const_to(ctx, xs, cs, t.nd->c[0], t.tl[i], t.ts[i]);
+      it.c0 = t.nd->c[0];
+      it.out_limbs = t.tl[i];
+      it.out_scale = t.ts[i];
+      items.push_back(std::move(it));
+      where.push_back({k, i});
     }
   }
+  const std::vector<Ciphertext> leaves = lincomb_const_to_many(ctx, items);
+  for (std::size_t m = 0; m < leaves.size(); ++m) tasks[where[m].first].val[where[m].second].ct = leaves[m];
   for (int ht = 1; ht <= H; ++ht) {
     std::vector<Ciphertext> as, bs;
     for (const PsTask& t : tasks)
