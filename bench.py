@@ -941,7 +941,7 @@ def main():
     ap.add_argument("--no-resnet", action="store_true", help="skip the ResNet-20 / VGG-16 model variants")
     ap.add_argument("--no-vgg", action="store_true", help="skip VGG-16")
     ap.add_argument("--depth", type=int, default=HEAD_DEPTH, help="ResNet-20 depth budget of the headline chain")
-    ap.add_argument("--in-flight", type=int, default=3, help="images in flight per GPU (key-sharing contexts)")
+    ap.add_argument("--in-flight", type=int, default=4, help="images in flight per GPU (key-sharing contexts)")
     ap.add_argument("--models", default="", help="comma-separated name prefixes of the model cases to run")
     ap.add_argument("--no-rotations", action="store_true", help="skip the configs[1] rotation block")
     ap.add_argument("--model-case", default="", help=argparse.SUPPRESS)

@@ -378,6 +378,10 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
   }
 }
 
+Bootstrapper::Bootstrapper(Context& ctx, const Bootstrapper& o)
+    : ctx_(ctx), bp_(o.bp_), S_(o.S_), n_(o.n_), sub_steps_(o.sub_steps_), depth_(o.depth_), stc_limbs_(o.stc_limbs_),
+      cts_(o.cts_), stc_(o.stc_), cos_coeffs_(o.cos_coeffs_) {}
+
 std::vector<long> Bootstrapper::rotation_steps() const {
   std::set<long> s;
   for (long t : sub_steps_) s.insert(t);

@@ -58,6 +58,9 @@ BootParams boot_params_of(const Params& p);
 class Bootstrapper {
  public:
   Bootstrapper(Context& ctx, const BootParams& bp = {});
+  // a key-sharing clone's bootstrapper: the parent's plan and encoded diagonals
+  // (read-only device buffers) shared, operations issued on `ctx`
+  Bootstrapper(Context& ctx, const Bootstrapper& parent);
   // levels consumed between ModRaise (top) and the output
   int depth() const { return depth_; }
   // full: any level; sparse: x must hold >= 2 limbs (the mask takes one level) unless

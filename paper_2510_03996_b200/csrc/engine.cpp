@@ -291,7 +291,14 @@ Context::Context(const Params& p, const Context* parent) : ht_(make_tables(p)) {
     FHEON_CUDA(cudaEventCreateWithFlags(&staging_ev_[i], cudaEventDisableTiming));
   }
   build_device_tables();
-  if (p.bootstrap) {
+  if (p.bootstrap && parent && parent->boot) {
+    // a clone shares the parent's bootstrapping plans and encoded diagonals (read-only);
+    // the parent's stream has finished writing them before this context reads them
+    FHEON_CUDA(cudaStreamSynchronize(parent->stream()));
+    boot = std::make_unique<Bootstrapper>(*this, *parent->boot);
+    for (const auto& b : parent->boot_sparse) boot_sparse.push_back(std::make_unique<Bootstrapper>(*this, *b));
+    depth_budget_ = parent->depth_budget();
+  } else if (p.bootstrap) {
     boot = std::make_unique<Bootstrapper>(*this, boot_params_of(p));
     const int after = p.L - 1 - boot->depth();
     if (p.depth_budget < 0) depth_budget_ = after;
