@@ -484,6 +484,9 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
         t_last = t;
       };
       lap("start");
+      static const char* prof_env = std::getenv("FHEON_BOOT_PROFILE");  // ncu range: "all" | "cos"
+      const bool prof_all = prof_env && std::string(prof_env) == "all";
+      if (prof_all) FHEON_CUDA(cudaProfilerStart());
       Ciphertext x;
       if (clean) {  // slots [n, S) already zero: no mask
         x = x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0;
@@ -513,8 +516,7 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
         lap("cts");
       }
       std::vector<Ciphertext> ys = {y};
-      static const char* prof = std::getenv("FHEON_BOOT_PROFILE");  // ncu range: "cos"
-      const bool prof_cos = prof && std::string(prof) == "cos";
+      const bool prof_cos = prof_env && std::string(prof_env) == "cos";
       if (prof_cos) FHEON_CUDA(cudaProfilerStart());
       ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
       if (prof_cos) FHEON_CUDA(cudaProfilerStop());
@@ -531,6 +533,7 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
       }
       z.scale *= corr;
       if (z.level() > ctx_.depth_budget()) z = level_down(ctx_, z, ctx_.depth_budget() + 1);
+      if (prof_all) FHEON_CUDA(cudaProfilerStop());
       ctx_.set_tracing(tracing);
       ctx_.record(3, z.level());
       ctx_.stats.bootstraps++;
