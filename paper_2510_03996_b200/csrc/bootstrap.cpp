@@ -371,7 +371,9 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
   ctx.pin_key(2 * (u64)h.N - 1);
   ctx.pin_key(0);
   if (ctx.sse()) {  // sparse-secret encapsulation keys
-    for (u64 id : {kKeyToSparse, kKeyFromSparse}) {
+    std::vector<u64> ids = {kKeyToSparse, kKeyFromSparse};
+    for (long t : sub_steps_) ids.push_back(key_from_sparse_rot(ctx.galois(t)));  // trace + switch back
+    for (u64 id : ids) {
       if (ctx.has_secret() && !ctx.inheriting_keys) ctx.gen_key(id);
       ctx.pin_key(id);
     }
@@ -505,10 +507,8 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
       x = subsum(x);
       lap("mask+rep");
       const double corr = x.scale / h.T[0];
-      Ciphertext y = mod_raise(ctx_, x);
-      lap("modraise");
-      y = subsum(y);
-      lap("trace");
+      Ciphertext y = mod_raise_trace(ctx_, x, n_);
+      lap("modraise+trace");
       // the last CtS level returns y + conj(y) directly: its giant steps enter twice, as
       // rot_G and conj o rot_G, in one ModDown (no separate conjugation key switch)
       for (std::size_t i = 0; i < cts_.size(); ++i) {

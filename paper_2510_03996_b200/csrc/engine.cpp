@@ -617,7 +617,7 @@ void Context::gen_key(u64 key_id) {
   // sigma_g(s) (rotation), s (-> sparse) or s_b (<- sparse); s_to = s except for the
   // switch to the sparse bootstrapping secret
   const u64* s_to = dt_.s_ntt;
-  const bool sse_key = key_id == kKeyToSparse || key_id == kKeyFromSparse;
+  const bool sse_key = key_id == kKeyToSparse || key_id == kKeyFromSparse || is_key_from_sparse_rot(key_id);
   if (sse_key && !dt_.sb_ntt) throw Error(ErrKind::internal, "no sparse bootstrapping secret in this context");
   if (key_id == 0) {
     secret_square(dt_, sp->ptr, stream_);
@@ -626,6 +626,14 @@ void Context::gen_key(u64 key_id) {
     s_to = dt_.sb_ntt;
   } else if (key_id == kKeyFromSparse) {
     FHEON_CUDA(cudaMemcpyAsync(sp->ptr, dt_.sb_ntt, LN * sizeof(u64), cudaMemcpyDeviceToDevice, stream_));
+  } else if (is_key_from_sparse_rot(key_id)) {  // sigma_g(s_b) -> s
+    PolyList o{}, in{};
+    o.p[0] = sp->ptr;
+    o.g[0] = key_id >> 4;
+    o.n = 1;
+    in.p[0] = dt_.sb_ntt;
+    in.n = 1;
+    automorph(dt_, o, in, NP, stream_);
   } else {
     if ((key_id & 1) == 0) throw Error(ErrKind::internal, "Galois element must be odd");
     PolyList o{}, in{};

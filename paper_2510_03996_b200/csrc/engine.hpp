@@ -318,6 +318,9 @@ std::vector<Ciphertext> add_many(Context& ctx, const std::vector<Ciphertext>& a,
 std::vector<Ciphertext> conjugate_many(Context& ctx, const std::vector<Ciphertext>& xs);
 Ciphertext mul_by_i(Context& ctx, const Ciphertext& x);
 Ciphertext mod_raise(Context& ctx, const Ciphertext& x);
+// ModRaise + the sparse-slot trace sum_{j < S/n} rot(., j n), the encapsulation's switch back
+// folded into the trace's key switches (keys key_from_sparse_rot)
+Ciphertext mod_raise_trace(Context& ctx, const Ciphertext& x, long n);
 Ciphertext encrypt_at(Context& ctx, const double* vals, std::size_t n, int limbs);
 // add an encoded plaintext (encoded at a's level and scale)
 Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt);

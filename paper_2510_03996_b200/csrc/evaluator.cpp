@@ -319,6 +319,9 @@ struct SumJob {
   u64 g;
   int in;
   int group;
+  u64 key_id = kNoKeyOverride;  // the key to read when it is not the Galois element's own
+  static constexpr u64 kNoKeyOverride = ~0ULL;
+  u64 key() const { return key_id == kNoKeyOverride ? g : key_id; }
 };
 // Q u P accumulators of every group, [ngroups][2][limbs+K][N] (canonical, standard form):
 // acc_r = sum_{jobs of r} <sigma_g(ModUp(d)), key_g> + P sigma_g(c0) on the Q limbs
@@ -336,6 +339,7 @@ BufPtr keyswitch_sum_accs(Context& ctx, const std::vector<const u64*>& inputs, c
   for (const SumJob& j : jobs) by_group[j.group].push_back(&j);
   // every group = one input under the same key list (a hoisted stage)?
   bool shared = ngroups > 1 && !by_group[0].empty() && (int)by_group[0].size() <= kMaxSharedKeys;
+  for (const SumJob& j : jobs) shared = shared && j.key_id == SumJob::kNoKeyOverride;
   for (int r = 0; r < ngroups && shared; ++r) {
     shared = by_group[r].size() == by_group[0].size();
     for (std::size_t k = 0; k < by_group[r].size() && shared; ++k)
@@ -374,7 +378,7 @@ BufPtr keyswitch_sum_accs(Context& ctx, const std::vector<const u64*>& inputs, c
         if (nj + gsz > kMaxSumJobs) break;
         kj.begin[R] = nj;
         for (const SumJob* j : by_group[r0 + R]) {
-          kj.key[nj] = ctx.key(j->g);
+          kj.key[nj] = ctx.key(j->key());
           kj.ext[nj] = ext->ptr + (std::size_t)j->in * ext_words;
           kj.d[nj] = inputs[j->in];
           kj.c0[nj] = c0s[j->in];
@@ -992,6 +996,36 @@ Ciphertext switch_secret(Context& ctx, const Ciphertext& x, u64 key_id) {
 }
 Ciphertext mod_raise_raw(Context& ctx, const Ciphertext& x);
 }  // namespace
+
+// ModRaise followed by the trace sum_{j < S/n} rot(., j n) of sparse-slot bootstrapping.
+// Under the encapsulation (dense main secret) the raised ciphertext is under s_b; each
+// trace term is key-switched from sigma_{5^{jn}}(s_b) straight to s (j = 0: the plain
+// switch back), so the switch back costs no key switch of its own: one ModUp, S/n key
+// inner products, one ModDown.
+Ciphertext mod_raise_trace(Context& ctx, const Ciphertext& x, long n) {
+  const long S = ctx.S();
+  if (x.limbs != 1) throw Error(ErrKind::internal, "mod_raise expects a level-0 ciphertext");
+  if (n <= 0 || S % n != 0) throw Error(ErrKind::internal, "mod_raise_trace: n must divide the slot count");
+  if (!ctx.sse()) {
+    Ciphertext y = mod_raise_raw(ctx, x);
+    if (n == S) return y;
+    std::vector<std::pair<Ciphertext, long>> terms;
+    for (long j = 0; j < S / n; ++j) terms.push_back({y, j * n});
+    return rotate_sum_many(ctx, {terms})[0];
+  }
+  Ciphertext y = mod_raise_raw(ctx, switch_secret(ctx, x, kKeyToSparse));
+  std::vector<SumJob> jobs;
+  for (long j = 0; j < S / n; ++j) {
+    const u64 g = ctx.galois(j * n);
+    SumJob jb{g, 0, 0};
+    jb.key_id = j == 0 ? kKeyFromSparse : key_from_sparse_rot(g);
+    jobs.push_back(jb);
+    if (j > 0) ctx.stats.rotations++;
+  }
+  Ciphertext out = keyswitch_sum(ctx, {y.c1}, {y.c0}, y.limbs, jobs, 1)[0];
+  out.scale = y.scale;
+  return out;
+}
 
 // ModRaise of a level-0 ciphertext to all L limbs (decrypts to m + q_0 I).  With a
 // dense main secret (sparse-secret encapsulation, Bossuat et al. 2022) the level-0
@@ -1738,7 +1772,8 @@ void download_key_packed(Context& ctx, u64 key_id, u64* host) {
 }
 
 void upload_key_async(Context& ctx, u64 key_id, const u64* host, bool packed) {
-  if (key_id != 0 && (key_id & 1) == 0 && key_id != kKeyToSparse && key_id != kKeyFromSparse)
+  if (key_id != 0 && (key_id & 1) == 0 && key_id != kKeyToSparse && key_id != kKeyFromSparse &&
+      !is_key_from_sparse_rot(key_id))
     throw Error(ErrKind::internal, "key upload: key id " + std::to_string(key_id) +
                                        " is neither 0 (relinearisation), a Galois element nor an encapsulation key");
   const int NP = ctx.L() + ctx.K();

@@ -70,6 +70,11 @@ int he_standard_security(int logN, double log_qp, int hamming_weight);
 // key ids of the sparse-secret encapsulation keys (even: never a Galois element)
 constexpr std::uint64_t kKeyToSparse = 2;    // s -> s_b, on q_0 and P only
 constexpr std::uint64_t kKeyFromSparse = 4;  // s_b -> s, whole chain
+// sigma_g(s_b) -> s, whole chain: the encapsulation's switch back merged into the sparse-slot
+// bootstrapping trace (id = g << 4 | 6, g an odd Galois element)
+constexpr std::uint64_t kKeyFromSparseRotTag = 6;
+constexpr std::uint64_t key_from_sparse_rot(std::uint64_t g) { return (g << 4) | kKeyFromSparseRotTag; }
+constexpr bool is_key_from_sparse_rot(std::uint64_t id) { return (id & 15) == kKeyFromSparseRotTag && id > 15; }
 
 // contiguous split of per-limb bit sizes into at most `dnum` digits minimising the
 // widest digit's bit sum (each digit <= max_size limbs); returns boundaries 0 = d_0 < ... < d_n = L
