@@ -90,6 +90,8 @@ u64* device_alloc(Context* c, std::size_t words, cudaStream_t st) {
   cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), st);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
+    static const bool dbg = std::getenv("FHEON_ALLOC_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "[fheon] allocation of %zu bytes failed: releasing plaintext caches\n", words * 8);
     if (c->release_caches() > 0) {
       FHEON_CUDA(cudaStreamSynchronize(c->stream()));
       e = cudaMallocAsync(&p, words * sizeof(u64), st);
