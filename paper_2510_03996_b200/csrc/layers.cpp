@@ -62,13 +62,18 @@ std::vector<double> range_mask(const Context& ctx, std::size_t begin, std::size_
   return plain(ctx, v);
 }
 
-Ciphertext mp(Context& ctx, const Ciphertext& x, const std::vector<double>& full) {
-  return mult_plain(ctx, x, full.data(), full.size());
-}
-
 // plaintext for `like` from slot values (content-cached host encode)
 BufPtr pt_of(Context& ctx, const Ciphertext& like, const std::vector<double>& full) {
   return ctx.encode_cached(full, like.limbs, pt_scale_for(ctx, like));
+}
+
+// mult_plain by a slot vector through the content-keyed plaintext cache (masks repeat
+// across layers and inferences: encoded once); one mult_plain event, one rescale
+Ciphertext mp(Context& ctx, const Ciphertext& x, const std::vector<double>& full) {
+  if (x.level() < 1)
+    throw Error(ErrKind::depth_exhausted, "mult_plain: no multiplicative depth left (level " +
+                                              std::to_string(x.level()) + ")");
+  return mac_plain_many(ctx, {{x}}, {{pt_of(ctx, x, full)}})[0];
 }
 
 // 128-bit content key of a weight tensor (keys the resident weight plaintexts): FNV-1a
