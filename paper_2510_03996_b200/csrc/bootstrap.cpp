@@ -307,6 +307,13 @@ Bootstrapper::Bootstrapper(Context& ctx, const BootParams& bp) : ctx_(ctx), bp_(
   // SlotsToCoeffs: forward stages len = 2 .. n, scaled by q0 / (2 pi Delta_0)
   {
     std::vector<int> sizes = split(bp.stc_levels);
+    // sparse: the smaller groups first as well -- StC's first factor also carries the
+    // unpacking P (twice the diagonals) and runs on StC's highest level
+    static const bool stc_small_first = [] {
+      const char* e = std::getenv("FHEON_STC_SMALL_FIRST");
+      return !(e && e[0] == '0');
+    }();
+    if (sparse() && stc_small_first) std::reverse(sizes.begin(), sizes.end());
     std::vector<Mat> groups;
     const double c = std::pow((double)h.q[0] / (2.0 * kPi * h.T[0]), 1.0 / bp.stc_levels);
     long len = 2;
