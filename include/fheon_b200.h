@@ -241,6 +241,13 @@ int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out);
  * zero (a convolution's output): no mask, so a level-0 input takes a sparse variant too */
 #define FHEON_BOOT_CLEAN 1
 int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, int flags, fheon_ct** out);
+/* fheon_bootstrap_active on n ciphertexts in lockstep (the images of a batched inference,
+ * model_run.cpp:100-159 run once per image): inputs on one level go through the sparse-slot
+ * pipeline together, so each evaluation key and encoded diagonal is read from HBM once per batch
+ * and every NTT / basis-conversion launch carries n times the limbs.  outs[i] is bit-identical
+ * to fheon_bootstrap_active(as[i]); one bootstrap trace event per input. */
+int fheon_bootstrap_active_many(fheon_ctx* ctx, const fheon_ct* const* as, size_t n, size_t active_slots, int flags,
+                                fheon_ct** outs);
 /* bootstrapping stage probes (tests): 1 CoeffsToSlots, 2 EvalMod, 3 SlotsToCoeffs, 4 ModRaise;
  * info (may be NULL): [depth, k_range, double_angles, stc_input_limbs] */
 int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out);
@@ -285,6 +292,11 @@ int fheon_fully_connected(fheon_ctx* ctx, const fheon_ct* x, size_t inputs, size
 /* secure_relu (layers_misc.cpp:268-295): Chebyshev interpolant of max(0, scale*z), degree */
 int fheon_secure_relu(fheon_ctx* ctx, const fheon_ct* x, double scale, int degree, size_t active_slots,
                       fheon_ct** out);
+/* secure_relu on n ciphertexts in lockstep (the images of a batched inference): one polynomial
+ * evaluation whose relinearisations and rescales carry every input; outs[i] bit-identical to
+ * fheon_secure_relu(xs[i]) */
+int fheon_secure_relu_many(fheon_ctx* ctx, const fheon_ct* const* xs, size_t n, double scale, int degree,
+                           size_t active_slots, fheon_ct** outs);
 /* stride stage (layers_conv.cpp:285-421): variant 0 extract (v1), 1 masked (v2); w_out 0 = default */
 int fheon_stride(fheon_ctx* ctx, const fheon_ct* x, size_t width, size_t stride, size_t w_out, int variant,
                  fheon_ct** out);

@@ -139,6 +139,7 @@ SIGNATURES = {
     "fheon_mult_cipher": (C.c_int, [vp, vp, vp, pp]),
     "fheon_bootstrap": (C.c_int, [vp, vp, pp]),
     "fheon_bootstrap_active": (C.c_int, [vp, vp, C.c_size_t, C.c_int, pp]),
+    "fheon_bootstrap_active_many": (C.c_int, [vp, pp, C.c_size_t, C.c_size_t, C.c_int, pp]),
     "fheon_bootstrap_stage": (C.c_int, [vp, vp, C.c_int, pp]),
     "fheon_bootstrap_info": (C.c_int, [vp, C.POINTER(C.c_int), dp, C.c_size_t, szp]),
     "fheon_rescale": (C.c_int, [vp, vp, pp]),
@@ -153,6 +154,7 @@ SIGNATURES = {
                              szp]),
     "fheon_fully_connected": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.c_size_t, dp, dp, pp]),
     "fheon_secure_relu": (C.c_int, [vp, vp, C.c_double, C.c_int, C.c_size_t, pp]),
+    "fheon_secure_relu_many": (C.c_int, [vp, pp, C.c_size_t, C.c_double, C.c_int, C.c_size_t, pp]),
     "fheon_stride": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, pp]),
     "fheon_pad_input": (C.c_int, [vp, vp, C.c_size_t, C.c_size_t, C.c_size_t, pp]),
     "fheon_conv_depth_cost": (C.c_int, [C.POINTER(fheon_conv_cfg), C.c_size_t, C.POINTER(C.c_int)]),

@@ -716,6 +716,20 @@ def bootstrap(a: SlotVector, active_slots: Optional[int] = None, clean: bool = F
     return _wrap(a._ctx, _native.lib().fheon_bootstrap_active, a._h, int(active_slots), int(bool(clean)))
 
 
+def bootstrap_many(xs: Sequence[SlotVector], active_slots: int, clean: bool = False) -> List[SlotVector]:
+    """bootstrap(x, active_slots, clean) of every x in lockstep (the images of a
+    batched inference): inputs on one level share each stage's launches, so keys and
+    encoded diagonals leave HBM once per batch.  Bit-identical to the single calls."""
+    n = len(xs)
+    if n == 0:
+        return []
+    ctx = xs[0]._ctx
+    hs = (C.c_void_p * n)(*[x._h.value if isinstance(x._h, C.c_void_p) else x._h for x in xs])
+    outs = (C.c_void_p * n)()
+    _check(_native.lib().fheon_bootstrap_active_many(ctx._h, hs, n, int(active_slots), int(bool(clean)), outs))
+    return [SlotVector(ctx, C.c_void_p(outs[i])) for i in range(n)]
+
+
 def bootstrap_stage(a: SlotVector, stage: int) -> SlotVector:
     """Bootstrapping stage probe: 1 CoeffsToSlots, 2 EvalMod, 3 SlotsToCoeffs, 4 ModRaise."""
     return _wrap(a._ctx, _native.lib().fheon_bootstrap_stage, a._h, int(stage))
@@ -911,6 +925,20 @@ def secure_relu(x, cfg: ReluConfig):
         return PackedTensor(v, x.channels, x.width)
     return _wrap(x._ctx, _native.lib().fheon_secure_relu, x._h, float(cfg.scale), int(cfg.degree),
                  int(cfg.active_slots))
+
+
+def secure_relu_many(xs: Sequence[SlotVector], cfg: ReluConfig) -> List[SlotVector]:
+    """secure_relu(x, cfg) of every x in lockstep (one polynomial evaluation carrying
+    the whole batch); bit-identical to the single calls."""
+    n = len(xs)
+    if n == 0:
+        return []
+    ctx = xs[0]._ctx
+    hs = (C.c_void_p * n)(*[x._h.value if isinstance(x._h, C.c_void_p) else x._h for x in xs])
+    outs = (C.c_void_p * n)()
+    _check(_native.lib().fheon_secure_relu_many(ctx._h, hs, n, float(cfg.scale), int(cfg.degree),
+                                                int(cfg.active_slots), outs))
+    return [SlotVector(ctx, C.c_void_p(outs[i])) for i in range(n)]
 
 
 def stride_extract_v1(a: SlotVector, W: int, S: int, W_out: int = 0) -> SlotVector:

@@ -403,19 +403,26 @@ std::vector<long> Bootstrapper::rotation_steps() const {
   return std::vector<long>(s.begin(), s.end());
 }
 
-Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv, bool with_conj) {
-  if (lv.qp) {
-    std::map<long, int> idx;
-    for (std::size_t i = 0; i < lv.babies.size(); ++i) idx[lv.babies[i]] = (int)i;
-    std::vector<DhGiant> gs;
-    for (const Giant& g : lv.giants) {
-      DhGiant d;
-      d.rot = g.rot;
-      for (const auto& [b, pt] : g.terms) d.terms.push_back({b == 0 ? -1 : idx.at(b), pt});
-      gs.push_back(std::move(d));
-    }
-    return bsgs_double_hoisted(ctx_, x, lv.babies, gs, with_conj);
+std::vector<Ciphertext> Bootstrapper::apply_many(const std::vector<Ciphertext>& xs, const Level& lv, bool with_conj) {
+  if (!lv.qp) {
+    std::vector<Ciphertext> out;
+    for (const Ciphertext& x : xs) out.push_back(apply(x, lv, with_conj));
+    return out;
   }
+  std::map<long, int> idx;
+  for (std::size_t i = 0; i < lv.babies.size(); ++i) idx[lv.babies[i]] = (int)i;
+  std::vector<DhGiant> gs;
+  for (const Giant& g : lv.giants) {
+    DhGiant d;
+    d.rot = g.rot;
+    for (const auto& [b, pt] : g.terms) d.terms.push_back({b == 0 ? -1 : idx.at(b), pt});
+    gs.push_back(std::move(d));
+  }
+  return bsgs_double_hoisted_many(ctx_, xs, lv.babies, gs, with_conj);
+}
+
+Ciphertext Bootstrapper::apply(const Ciphertext& x, const Level& lv, bool with_conj) {
+  if (lv.qp) return apply_many({x}, lv, with_conj)[0];
   std::vector<Ciphertext> rot = rotate_hoisted(ctx_, x, lv.babies);
   std::map<long, Ciphertext> by_b;
   by_b[0] = x;
@@ -466,42 +473,66 @@ Ciphertext Bootstrapper::debug_stage(const Ciphertext& x0, int what) {
   throw Error(ErrKind::internal, "debug_stage: unknown stage");
 }
 
-Ciphertext Bootstrapper::subsum(const Ciphertext& x) {
-  if (sub_steps_.empty()) return x;
-  std::vector<std::pair<Ciphertext, long>> terms = {{x, 0}};
-  for (long t : sub_steps_) terms.push_back({x, t});
-  return rotate_sum_many(ctx_, {terms})[0];
+std::vector<Ciphertext> Bootstrapper::subsum_many(const std::vector<Ciphertext>& xs) {
+  if (sub_steps_.empty()) return xs;
+  std::vector<std::vector<std::pair<Ciphertext, long>>> groups;
+  for (const Ciphertext& x : xs) {
+    std::vector<std::pair<Ciphertext, long>> terms = {{x, 0}};
+    for (long t : sub_steps_) terms.push_back({x, t});
+    groups.push_back(std::move(terms));
+  }
+  return rotate_sum_many(ctx_, groups);
 }
 
 Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
+  if (sparse()) return run_many({x0}, clean)[0];
+  return run_full(x0);
+}
+
+// Sparse-slot pipeline on several ciphertexts of one level in lockstep (the images of a
+// batched inference): every stage is one batched call, so keys and encoded diagonals are
+// read once per batch and the NTT / basis-conversion launches carry B times the limbs.
+// Per input the operations are those of the single-input pipeline (bit-identical outputs).
+std::vector<Ciphertext> Bootstrapper::run_many(const std::vector<Ciphertext>& xs0, bool clean) {
+  if (xs0.empty()) return {};
+  if (!sparse()) {
+    std::vector<Ciphertext> out;
+    for (const Ciphertext& x : xs0) out.push_back(run_full(x));
+    return out;
+  }
+  for (const Ciphertext& x : xs0)
+    if (x.limbs != xs0[0].limbs) throw Error(ErrKind::internal, "bootstrap_many: inputs at different levels");
   const bool tracing = ctx_.tracing();
   ctx_.set_tracing(false);
   try {
     const HostTables& h = ctx_.host();
-    if (sparse()) {
-      if (x0.limbs < 2 && !clean)
-        throw Error(ErrKind::internal, "sparse-slot bootstrapping needs an input above level 0 (the mask)");
-      // mask to [0, n) on the last level, replicate n-periodically, raise, trace
-      static const bool timing = std::getenv("FHEON_BOOT_TIMING") != nullptr;
-      auto t_last = std::chrono::steady_clock::now();
-      auto lap = [&](const char* what) {
-        if (!timing) return;
-        FHEON_CUDA(cudaStreamSynchronize(ctx_.stream()));
-        const auto t = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[boot n=%ld] %-10s %8.3f ms\n", n_, what,
-                     std::chrono::duration<double, std::milli>(t - t_last).count());
-        t_last = t;
-      };
-      lap("start");
-      static const char* prof_env = std::getenv("FHEON_BOOT_PROFILE");  // ncu range: "all" | "cos"
-      const bool prof_all = prof_env && std::string(prof_env) == "all";
-      if (prof_all) FHEON_CUDA(cudaProfilerStart());
-      Ciphertext x;
-      if (clean) {  // slots [n, S) already zero: no mask
-        x = x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0;
-      } else {
-        x = x0.limbs > 2 ? level_down(ctx_, x0, 2) : x0;
-        const long n = n_, S = S_;
+    const std::size_t B = xs0.size();
+    if (xs0[0].limbs < 2 && !clean)
+      throw Error(ErrKind::internal, "sparse-slot bootstrapping needs an input above level 0 (the mask)");
+    // mask to [0, n) on the last level, replicate n-periodically, raise, trace
+    static const bool timing = std::getenv("FHEON_BOOT_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!timing) return;
+      FHEON_CUDA(cudaStreamSynchronize(ctx_.stream()));
+      const auto t = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[boot n=%ld x%zu] %-10s %8.3f ms\n", n_, B, what,
+                   std::chrono::duration<double, std::milli>(t - t_last).count());
+      t_last = t;
+    };
+    lap("start");
+    static const char* prof_env = std::getenv("FHEON_BOOT_PROFILE");  // ncu range: "all" | "cos"
+    const bool prof_all = prof_env && std::string(prof_env) == "all";
+    if (prof_all) FHEON_CUDA(cudaProfilerStart());
+    std::vector<Ciphertext> xs(B);
+    if (clean) {  // slots [n, S) already zero: no mask
+      for (std::size_t i = 0; i < B; ++i) xs[i] = xs0[i].limbs > 1 ? level_down(ctx_, xs0[i], 1) : xs0[i];
+    } else {
+      const long n = n_, S = S_;
+      std::vector<std::vector<Ciphertext>> terms;
+      std::vector<std::vector<BufPtr>> pts;
+      for (std::size_t i = 0; i < B; ++i) {
+        const Ciphertext x = xs0[i].limbs > 2 ? level_down(ctx_, xs0[i], 2) : xs0[i];
         BufPtr mask = ctx_.encode_named("boot_mask_" + std::to_string(n),
                                         [n, S] {
                                           std::vector<double> m((std::size_t)S, 0.0);
@@ -509,43 +540,58 @@ Ciphertext Bootstrapper::run(const Ciphertext& x0, bool clean) {
                                           return m;
                                         },
                                         x.limbs, pt_scale_for(ctx_, x));
-        x = mac_plain_many(ctx_, {{x}}, {{mask}})[0];
+        terms.push_back({x});
+        pts.push_back({mask});
       }
-      x = subsum(x);
-      lap("mask+rep");
-      const double corr = x.scale / h.T[0];
-      Ciphertext y = mod_raise_trace(ctx_, x, n_);
-      lap("modraise+trace");
-      // the last CtS level returns y + conj(y) directly: its giant steps enter twice, as
-      // rot_G and conj o rot_G, in one ModDown (no separate conjugation key switch)
-      for (std::size_t i = 0; i < cts_.size(); ++i) {
-        y = apply(y, cts_[i], i + 1 == cts_.size());
-        lap("cts");
-      }
-      std::vector<Ciphertext> ys = {y};
-      const bool prof_cos = prof_env && std::string(prof_env) == "cos";
-      if (prof_cos) FHEON_CUDA(cudaProfilerStart());
-      ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
-      if (prof_cos) FHEON_CUDA(cudaProfilerStop());
-      lap("cos");
-      for (int i = 0; i < bp_.double_angles; ++i) {  // y <- 2 y^2 - 1
-        ys = mult_cipher_cheb_many(ctx_, ys, ys, std::vector<Ciphertext>(ys.size()));
-        for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
-      }
-      lap("dbl-angle");
-      Ciphertext z = ys[0];
-      for (const Level& lv : stc_) {
-        z = apply(z, lv);
-        lap("stc");
-      }
-      z.scale *= corr;
+      xs = mac_plain_many(ctx_, terms, pts);
+    }
+    xs = subsum_many(xs);
+    lap("mask+rep");
+    std::vector<double> corr(B);
+    for (std::size_t i = 0; i < B; ++i) corr[i] = xs[i].scale / h.T[0];
+    std::vector<Ciphertext> ys = mod_raise_trace_many(ctx_, xs, n_);
+    lap("modraise+trace");
+    // the last CtS level returns y + conj(y) directly: its giant steps enter twice, as
+    // rot_G and conj o rot_G, in one ModDown (no separate conjugation key switch)
+    for (std::size_t i = 0; i < cts_.size(); ++i) {
+      ys = apply_many(ys, cts_[i], i + 1 == cts_.size());
+      lap("cts");
+    }
+    const bool prof_cos = prof_env && std::string(prof_env) == "cos";
+    if (prof_cos) FHEON_CUDA(cudaProfilerStart());
+    ys = cheb_eval_many(ctx_, ys, cos_coeffs_, true);
+    if (prof_cos) FHEON_CUDA(cudaProfilerStop());
+    lap("cos");
+    for (int i = 0; i < bp_.double_angles; ++i) {  // y <- 2 y^2 - 1
+      ys = mult_cipher_cheb_many(ctx_, ys, ys, std::vector<Ciphertext>(ys.size()));
+      for (Ciphertext& c : ys) c = add_const(ctx_, c, -1.0);
+    }
+    lap("dbl-angle");
+    for (const Level& lv : stc_) {
+      ys = apply_many(ys, lv);
+      lap("stc");
+    }
+    if (prof_all) FHEON_CUDA(cudaProfilerStop());
+    ctx_.set_tracing(tracing);
+    for (std::size_t i = 0; i < B; ++i) {
+      Ciphertext& z = ys[i];
+      z.scale *= corr[i];
       if (z.level() > ctx_.depth_budget()) z = level_down(ctx_, z, ctx_.depth_budget() + 1);
-      if (prof_all) FHEON_CUDA(cudaProfilerStop());
-      ctx_.set_tracing(tracing);
       ctx_.record(3, z.level());
       ctx_.stats.bootstraps++;
-      return z;
     }
+    return ys;
+  } catch (...) {
+    ctx_.set_tracing(tracing);
+    throw;
+  }
+}
+
+Ciphertext Bootstrapper::run_full(const Ciphertext& x0) {
+  const bool tracing = ctx_.tracing();
+  ctx_.set_tracing(false);
+  try {
+    const HostTables& h = ctx_.host();
     Ciphertext x = x0.limbs > 1 ? level_down(ctx_, x0, 1) : x0;
     const double corr = x.scale / h.T[0];
     static const bool dbg = std::getenv("FHEON_BOOT_DEBUG") != nullptr;

@@ -66,6 +66,9 @@ class Bootstrapper {
   // full: any level; sparse: x must hold >= 2 limbs (the mask takes one level) unless
   // `clean` (slots [n, S) of x are already zero: no mask, any level)
   Ciphertext run(const Ciphertext& x, bool clean = false);
+  // several ciphertexts of one level in lockstep (sparse variants: every stage batched, keys
+  // and diagonals read once per batch; full variant: one after the other); bit-identical to run
+  std::vector<Ciphertext> run_many(const std::vector<Ciphertext>& xs, bool clean = false);
   long slots() const { return n_; }
   bool sparse() const { return n_ < S_; }
   // stage probes for tests: 1 CoeffsToSlots on x (scale reinterpreted as q0),
@@ -99,8 +102,10 @@ class Bootstrapper {
                           const std::vector<long>& periods);
   // with_conj: returns T x + conj(T x) (the conjugated giant steps join the same ModDown)
   Ciphertext apply(const Ciphertext& x, const Level& lv, bool with_conj = false);
-  // sum_{j < S/n} rot(x, j n): one hoisted rotate-and-sum
-  Ciphertext subsum(const Ciphertext& x);
+  std::vector<Ciphertext> apply_many(const std::vector<Ciphertext>& xs, const Level& lv, bool with_conj = false);
+  // sum_{j < S/n} rot(x, j n): one hoisted rotate-and-sum (all inputs in one pipeline)
+  std::vector<Ciphertext> subsum_many(const std::vector<Ciphertext>& xs);
+  Ciphertext run_full(const Ciphertext& x);
 
   Context& ctx_;
   BootParams bp_;

@@ -541,6 +541,19 @@ int fheon_bootstrap(fheon_ctx* ctx, const fheon_ct* a, fheon_ct** out) {
 int fheon_bootstrap_active(fheon_ctx* ctx, const fheon_ct* a, size_t active_slots, int flags, fheon_ct** out) {
   return guard([&] { *out = wrap(fheon::bootstrap_active(*ctx->impl, a->ct, active_slots, (flags & 1) != 0)); });
 }
+int fheon_bootstrap_active_many(fheon_ctx* ctx, const fheon_ct* const* as, size_t n, size_t active_slots, int flags,
+                                fheon_ct** outs) {
+  return guard([&] {
+    std::vector<fheon::Ciphertext> in;
+    in.reserve(n);
+    for (size_t i = 0; i < n; ++i) {
+      need(as[i], "ciphertext");
+      in.push_back(as[i]->ct);
+    }
+    std::vector<fheon::Ciphertext> r = fheon::bootstrap_active_many(*ctx->impl, in, active_slots, (flags & 1) != 0);
+    for (size_t i = 0; i < n; ++i) outs[i] = wrap(r[i]);
+  });
+}
 int fheon_bootstrap_stage(fheon_ctx* ctx, const fheon_ct* a, int stage, fheon_ct** out) {
   return guard([&] {
     if (!ctx->impl->boot) throw fheon::Error(fheon::ErrKind::not_implemented, "context has no bootstrapper");
@@ -666,6 +679,20 @@ int fheon_secure_relu(fheon_ctx* ctx, const fheon_ct* x, double scale, int degre
   return guard([&] {
     need(x, "ciphertext");
     *out = wrap(fheon::secure_relu(*ctx->impl, x->ct, scale, degree, active));
+  });
+}
+
+int fheon_secure_relu_many(fheon_ctx* ctx, const fheon_ct* const* xs, size_t n, double scale, int degree,
+                           size_t active, fheon_ct** outs) {
+  return guard([&] {
+    std::vector<fheon::Ciphertext> in;
+    in.reserve(n);
+    for (size_t i = 0; i < n; ++i) {
+      need(xs[i], "ciphertext");
+      in.push_back(xs[i]->ct);
+    }
+    std::vector<fheon::Ciphertext> r = fheon::secure_relu_many(*ctx->impl, in, scale, degree, active);
+    for (size_t i = 0; i < n; ++i) outs[i] = wrap(r[i]);
   });
 }
 

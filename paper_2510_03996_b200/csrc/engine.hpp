@@ -321,6 +321,7 @@ Ciphertext mod_raise(Context& ctx, const Ciphertext& x);
 // ModRaise + the sparse-slot trace sum_{j < S/n} rot(., j n), the encapsulation's switch back
 // folded into the trace's key switches (keys key_from_sparse_rot)
 Ciphertext mod_raise_trace(Context& ctx, const Ciphertext& x, long n);
+std::vector<Ciphertext> mod_raise_trace_many(Context& ctx, const std::vector<Ciphertext>& xs, long n);
 Ciphertext encrypt_at(Context& ctx, const double* vals, std::size_t n, int limbs);
 // add an encoded plaintext (encoded at a's level and scale)
 Ciphertext add_plain_pt(Context& ctx, const Ciphertext& a, const BufPtr& pt);
@@ -368,6 +369,11 @@ struct DhGiant {
 };
 Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& babies,
                                const std::vector<DhGiant>& giants, bool with_conj = false);
+// the same transform on several ciphertexts of one level and scale in lockstep (keys and
+// plaintext diagonals read once per batch); outputs bit-identical to the single-input call
+std::vector<Ciphertext> bsgs_double_hoisted_many(Context& ctx, const std::vector<Ciphertext>& xs,
+                                                 const std::vector<long>& babies, const std::vector<DhGiant>& giants,
+                                                 bool with_conj = false);
 Ciphertext add(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext sub(Context& ctx, const Ciphertext& a, const Ciphertext& b);
 Ciphertext add_plain(Context& ctx, const Ciphertext& a, const double* vals, std::size_t n);
@@ -384,6 +390,8 @@ Ciphertext bootstrap(Context& ctx, const Ciphertext& a);
 // clean: the caller knows slots [active, S) of a are zero (a convolution's output) -- no
 // mask, so a level-0 input can take a sparse variant too
 Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t active, bool clean = false);
+std::vector<Ciphertext> bootstrap_active_many(Context& ctx, const std::vector<Ciphertext>& as, std::size_t active,
+                                              bool clean = false);
 // raw key switch of one polynomial d ([limbs][N], NTT) for parity tests:
 // returns (ks0, ks1) as a 2-poly ciphertext without scale meaning
 Ciphertext keyswitch_raw(Context& ctx, const Ciphertext& d_as_c1, u64 key_id, u64 g);

@@ -540,31 +540,56 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
 // rotate-and-sum (one more ModDown) and the sum is rescaled once.
 Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vector<long>& babies,
                                const std::vector<DhGiant>& giants, bool with_conj) {
-  require_valid(x, "linear transform");
-  require_depth(x, "linear transform");
+  return bsgs_double_hoisted_many(ctx, {x}, babies, giants, with_conj)[0];
+}
+
+// The same transform on several ciphertexts of one level and scale (lockstep images of a
+// batched inference): accumulator groups are ordered baby-major / giant-major with the
+// inputs innermost, so the CTAs that run side by side (grid x = group / output) read the
+// same key slice or plaintext diagonal and every key and diagonal leaves HBM once per
+// batch instead of once per input.  Per input the operations and their order are those of
+// the single-input transform: outputs are bit-identical.
+std::vector<Ciphertext> bsgs_double_hoisted_many(Context& ctx, const std::vector<Ciphertext>& xs,
+                                                 const std::vector<long>& babies, const std::vector<DhGiant>& giants,
+                                                 bool with_conj) {
+  if (xs.empty()) return {};
+  const int B = (int)xs.size();
+  for (const Ciphertext& x : xs) {
+    require_valid(x, "linear transform");
+    require_depth(x, "linear transform");
+    if (x.limbs != xs[0].limbs) throw Error(ErrKind::internal, "linear transform: inputs at different levels");
+    check_scales(x, xs[0], "linear transform");
+  }
   const DevTables& t = ctx.dev();
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
-  const int limbs = x.limbs, K = ctx.K(), E = limbs + K, lv = limbs - 1;
+  const int limbs = xs[0].limbs, K = ctx.K(), E = limbs + K, lv = limbs - 1;
   const std::size_t accw = (std::size_t)2 * E * N;
   const HostTables& h = ctx.host();
-  // baby accumulators
+  const int nb = (int)babies.size(), ng = (int)giants.size();
+  // baby accumulators: group k * B + i = baby k of input i
   std::vector<SumJob> jobs;
-  for (std::size_t k = 0; k < babies.size(); ++k) {
-    ctx.record(0, babies[k]);
-    ctx.stats.rotations++;
+  for (int k = 0; k < nb; ++k) {
     const u64 g = ctx.galois(babies[k]);
     if (g == 1) throw Error(ErrKind::internal, "double-hoisted transform: identity baby must be index -1");
-    jobs.push_back({g, 0, (int)k});
+    for (int i = 0; i < B; ++i) {
+      ctx.record(0, babies[k]);
+      ctx.stats.rotations++;
+      jobs.push_back({g, i, k * B + i});
+    }
   }
-  BufPtr accs = babies.empty() ? nullptr
-                               : keyswitch_sum_accs(ctx, {x.c1}, {x.c0}, limbs, jobs, (int)babies.size());
+  std::vector<const u64*> c1s, c0s;
+  for (const Ciphertext& x : xs) {
+    c1s.push_back(x.c1);
+    c0s.push_back(x.c0);
+  }
+  BufPtr accs = babies.empty() ? nullptr : keyswitch_sum_accs(ctx, c1s, c0s, limbs, jobs, nb * B);
   BufPtr ident;
   bool need_ident = false;
   for (const DhGiant& gi : giants)
     for (const auto& [b, pt] : gi.terms) need_ident = need_ident || b < 0;
   if (need_ident) {
-    ident = ctx.alloc(accw);
+    ident = ctx.alloc((std::size_t)B * accw);
     LimbConsts pc{};
     for (int i = 0; i < limbs; ++i) {
       u64 pm = 1 % h.q[i];
@@ -572,46 +597,55 @@ Ciphertext bsgs_double_hoisted(Context& ctx, const Ciphertext& x, const std::vec
       pc.c[i] = pm;
       pc.sh[i] = shoup(pm, h.q[i]);
     }
-    ew_mul_const(t, plist({ident->ptr, ident->ptr + (std::size_t)E * N}), plist({x.c0, x.c1}), pc, limbs, st);
-    for (int p = 0; p < 2; ++p)
-      FHEON_CUDA(cudaMemsetAsync(ident->ptr + (std::size_t)p * E * N + (std::size_t)limbs * N, 0,
-                                 (std::size_t)K * N * sizeof(u64), st));
+    for (int i = 0; i < B; ++i) {
+      u64* id = ident->ptr + (std::size_t)i * accw;
+      ew_mul_const(t, plist({id, id + (std::size_t)E * N}), plist({xs[i].c0, xs[i].c1}), pc, limbs, st);
+      for (int p = 0; p < 2; ++p)
+        FHEON_CUDA(cudaMemsetAsync(id + (std::size_t)p * E * N + (std::size_t)limbs * N, 0,
+                                   (std::size_t)K * N * sizeof(u64), st));
+    }
   }
-  auto baby_ptr = [&](int b) { return b < 0 ? ident->ptr : accs->ptr + (std::size_t)b * accw; };
-  // inner sums over Q u P, one output accumulator per giant
-  BufPtr inner = ctx.alloc(giants.size() * accw);
-  for (std::size_t g0 = 0; g0 < giants.size(); g0 += kMacMaxOut) {
+  auto baby_ptr = [&](int b, int i) {
+    return b < 0 ? ident->ptr + (std::size_t)i * accw : accs->ptr + ((std::size_t)b * B + i) * accw;
+  };
+  // inner sums over Q u P, one output accumulator per (giant, input): output g * B + i
+  const std::size_t nout = (std::size_t)ng * B;
+  BufPtr inner = ctx.alloc(nout * accw);
+  for (std::size_t o0 = 0; o0 < nout; o0 += kMacMaxOut) {
     MacJobs jb{};
-    jb.nout = (int)std::min<std::size_t>(kMacMaxOut, giants.size() - g0);
+    jb.nout = (int)std::min<std::size_t>(kMacMaxOut, nout - o0);
     for (int z = 0; z < jb.nout; ++z) {
-      const DhGiant& gi = giants[g0 + z];
+      const DhGiant& gi = giants[(o0 + z) / B];
+      const int i = (int)((o0 + z) % B);
       if (gi.terms.empty() || gi.terms.size() > (std::size_t)kMacMaxTerms)
         throw Error(ErrKind::internal, "double-hoisted transform: 1..32 terms per giant");
       for (std::size_t j = 0; j < gi.terms.size(); ++j) {
-        jb.ct[z][j] = baby_ptr(gi.terms[j].first);
+        jb.ct[z][j] = baby_ptr(gi.terms[j].first, i);
         jb.c1_off[z][j] = (long long)E * (long long)N;
         jb.pt[z][j] = gi.terms[j].second->ptr;
       }
       jb.nterm[z] = (int)gi.terms.size();
-      jb.out0[z] = inner->ptr + (g0 + z) * accw;
+      jb.out0[z] = inner->ptr + (o0 + z) * accw;
       jb.out1[z] = jb.out0[z] + (std::size_t)E * N;
     }
     mac_pt(t, jb, E, st, limbs);
   }
-  std::vector<u64*> accp(giants.size());
-  for (std::size_t g = 0; g < giants.size(); ++g) accp[g] = inner->ptr + g * accw;
+  std::vector<u64*> accp(nout);
+  for (std::size_t o = 0; o < nout; ++o) accp[o] = inner->ptr + o * accw;
   std::vector<Ciphertext> rows = moddown_accs(ctx, accp, limbs);
   const double sc = h.T[lv - 1] * (double)h.q[lv];  // plaintexts encoded at T_{lv-1} q_lv / scale(x)
-  std::vector<std::pair<Ciphertext, long>> terms;
-  for (std::size_t g = 0; g < giants.size(); ++g) {
-    rows[g].scale = sc;
-    terms.push_back({rows[g], giants[g].rot});
-    for (std::size_t j = 0; j < giants[g].terms.size(); ++j) {
-      ctx.stats.mult_plain++;
-      ctx.record(1, lv - 1);
+  std::vector<std::vector<std::pair<Ciphertext, long>>> terms(B);
+  for (int i = 0; i < B; ++i)
+    for (int g = 0; g < ng; ++g) {
+      Ciphertext& row = rows[(std::size_t)g * B + i];
+      row.scale = sc;
+      terms[i].push_back({row, giants[g].rot});
+      for (std::size_t j = 0; j < giants[g].terms.size(); ++j) {
+        ctx.stats.mult_plain++;
+        ctx.record(1, lv - 1);
+      }
     }
-  }
-  return rotate_sum_to_target(ctx, {terms}, true, with_conj)[0];
+  return rotate_sum_to_target(ctx, terms, true, with_conj);
 }
 
 // out[r] = sum_k rot(groups[r][k].first, groups[r][k].second): every group's
@@ -987,14 +1021,25 @@ Ciphertext mul_by_i(Context& ctx, const Ciphertext& x) {
 }
 
 namespace {
-// key switch of x to the secret a key encapsulates: (c0 + ks0, ks1), automorphism-free
+// key switch of every x to the secret a key encapsulates: (c0 + ks0, ks1), automorphism-free
+std::vector<Ciphertext> switch_secret_many(Context& ctx, const std::vector<Ciphertext>& xs, u64 key_id) {
+  std::vector<const u64*> inputs;
+  std::vector<KsJob> jobs;
+  for (std::size_t i = 0; i < xs.size(); ++i) {
+    inputs.push_back(xs[i].c1);
+    KsJob jb{key_id, 1, xs[i].c0, 1, nullptr};
+    jb.in = (int)i;
+    jobs.push_back(jb);
+  }
+  std::vector<Ciphertext> ys = keyswitch(ctx, inputs, xs[0].limbs, jobs);
+  for (std::size_t i = 0; i < xs.size(); ++i) ys[i].scale = xs[i].scale;
+  return ys;
+}
 Ciphertext switch_secret(Context& ctx, const Ciphertext& x, u64 key_id) {
-  KsJob jb{key_id, 1, x.c0, 1, nullptr};
-  Ciphertext y = keyswitch(ctx, {x.c1}, x.limbs, {jb})[0];
-  y.scale = x.scale;
-  return y;
+  return switch_secret_many(ctx, {x}, key_id)[0];
 }
 Ciphertext mod_raise_raw(Context& ctx, const Ciphertext& x);
+std::vector<Ciphertext> mod_raise_raw_many(Context& ctx, const std::vector<Ciphertext>& xs);
 }  // namespace
 
 // ModRaise followed by the trace sum_{j < S/n} rot(., j n) of sparse-slot bootstrapping.
@@ -1003,28 +1048,42 @@ Ciphertext mod_raise_raw(Context& ctx, const Ciphertext& x);
 // switch back), so the switch back costs no key switch of its own: one ModUp, S/n key
 // inner products, one ModDown.
 Ciphertext mod_raise_trace(Context& ctx, const Ciphertext& x, long n) {
+  return mod_raise_trace_many(ctx, {x}, n)[0];
+}
+
+// several level-0 ciphertexts in lockstep (one group per input under the same key list)
+std::vector<Ciphertext> mod_raise_trace_many(Context& ctx, const std::vector<Ciphertext>& xs, long n) {
   const long S = ctx.S();
-  if (x.limbs != 1) throw Error(ErrKind::internal, "mod_raise expects a level-0 ciphertext");
+  if (xs.empty()) return {};
+  for (const Ciphertext& x : xs)
+    if (x.limbs != 1) throw Error(ErrKind::internal, "mod_raise expects a level-0 ciphertext");
   if (n <= 0 || S % n != 0) throw Error(ErrKind::internal, "mod_raise_trace: n must divide the slot count");
+  const int B = (int)xs.size();
   if (!ctx.sse()) {
-    Ciphertext y = mod_raise_raw(ctx, x);
-    if (n == S) return y;
-    std::vector<std::pair<Ciphertext, long>> terms;
-    for (long j = 0; j < S / n; ++j) terms.push_back({y, j * n});
-    return rotate_sum_many(ctx, {terms})[0];
+    std::vector<Ciphertext> ys = mod_raise_raw_many(ctx, xs);
+    if (n == S) return ys;
+    std::vector<std::vector<std::pair<Ciphertext, long>>> groups(B);
+    for (int i = 0; i < B; ++i)
+      for (long j = 0; j < S / n; ++j) groups[i].push_back({ys[i], j * n});
+    return rotate_sum_many(ctx, groups);
   }
-  Ciphertext y = mod_raise_raw(ctx, switch_secret(ctx, x, kKeyToSparse));
+  std::vector<Ciphertext> ys = mod_raise_raw_many(ctx, switch_secret_many(ctx, xs, kKeyToSparse));
   std::vector<SumJob> jobs;
-  for (long j = 0; j < S / n; ++j) {
-    const u64 g = ctx.galois(j * n);
-    SumJob jb{g, 0, 0};
-    jb.key_id = j == 0 ? kKeyFromSparse : key_from_sparse_rot(g);
-    jobs.push_back(jb);
-    if (j > 0) ctx.stats.rotations++;
+  std::vector<const u64*> c1s, c0s;
+  for (int i = 0; i < B; ++i) {
+    c1s.push_back(ys[i].c1);
+    c0s.push_back(ys[i].c0);
+    for (long j = 0; j < S / n; ++j) {
+      const u64 g = ctx.galois(j * n);
+      SumJob jb{g, i, i};
+      jb.key_id = j == 0 ? kKeyFromSparse : key_from_sparse_rot(g);
+      jobs.push_back(jb);
+      if (j > 0) ctx.stats.rotations++;
+    }
   }
-  Ciphertext out = keyswitch_sum(ctx, {y.c1}, {y.c0}, y.limbs, jobs, 1)[0];
-  out.scale = y.scale;
-  return out;
+  std::vector<Ciphertext> outs = keyswitch_sum(ctx, c1s, c0s, ys[0].limbs, jobs, B);
+  for (int i = 0; i < B; ++i) outs[i].scale = ys[i].scale;
+  return outs;
 }
 
 // ModRaise of a level-0 ciphertext to all L limbs (decrypts to m + q_0 I).  With a
@@ -1040,22 +1099,49 @@ Ciphertext mod_raise(Context& ctx, const Ciphertext& x) {
 }
 
 namespace {
-Ciphertext mod_raise_raw(Context& ctx, const Ciphertext& x) {
+Ciphertext mod_raise_raw(Context& ctx, const Ciphertext& x) { return mod_raise_raw_many(ctx, {x})[0]; }
+
+std::vector<Ciphertext> mod_raise_raw_many(Context& ctx, const std::vector<Ciphertext>& xs) {
   const DevTables& t = ctx.dev();
   cudaStream_t st = ctx.stream();
   const std::size_t N = ctx.N();
   const int L = ctx.L();
-  BufPtr coef = ctx.alloc(2 * N);
-  LimbSet dst = limbset(coef->ptr, 2, N, 1, 1, L);
-  LimbSet src = dst;
-  src.base[0] = x.c0;
-  src.block_stride = (long long)(x.c1 - x.c0);
-  ntt_inverse(t, dst, st, &src);
-  Ciphertext out = ctx.new_ct(L);
-  modraise(t, plist({out.c0, out.c1}), plist({coef->ptr, coef->ptr + N}), L, st);
-  ntt_forward(t, limbset(out.c0, 2, (std::size_t)(out.c1 - out.c0), L, L, L), st);
-  out.scale = (double)ctx.host().q[0];
-  return out;
+  std::vector<Ciphertext> outs;
+  for (std::size_t i0 = 0; i0 < xs.size(); i0 += kMaxBases) {
+    const int B = (int)std::min<std::size_t>(kMaxBases, xs.size() - i0);
+    BufPtr coef = ctx.alloc((std::size_t)B * 2 * N);
+    LimbSet dst = limbset(coef->ptr, 2 * B, N, 1, 1, L);
+    LimbSet src = dst;
+    src.nbase = B;
+    src.blocks_per_base = 2;
+    const long long cstride = (long long)(xs[i0].c1 - xs[i0].c0);
+    src.block_stride = cstride;
+    for (int i = 0; i < B; ++i) {
+      const Ciphertext& x = xs[i0 + i];
+      if ((long long)(x.c1 - x.c0) != cstride) throw Error(ErrKind::internal, "mod_raise: mixed ciphertext strides");
+      src.base[i] = x.c0;
+    }
+    ntt_inverse(t, dst, st, &src);
+    LimbSet fw{};
+    long long ostride = 0;
+    for (int i = 0; i < B; ++i) {
+      Ciphertext out = ctx.new_ct(L);
+      modraise(t, plist({out.c0, out.c1}),
+               plist({coef->ptr + (std::size_t)(2 * i) * N, coef->ptr + (std::size_t)(2 * i + 1) * N}), L, st);
+      if (i == 0) {
+        ostride = (long long)(out.c1 - out.c0);
+        fw = limbset(out.c0, 2, (std::size_t)ostride, L, L, L);
+      } else if ((long long)(out.c1 - out.c0) != ostride) {
+        throw Error(ErrKind::internal, "mod_raise: mixed ciphertext strides");
+      }
+      fw.base[i] = out.c0;
+      out.scale = (double)ctx.host().q[0];
+      outs.push_back(out);
+    }
+    fw.nbase = B;
+    ntt_forward(t, fw, st);
+  }
+  return outs;
 }
 }  // namespace
 
@@ -1663,6 +1749,29 @@ Ciphertext bootstrap_active(Context& ctx, const Ciphertext& a, std::size_t activ
     for (auto& b : ctx.boot_sparse)
       if ((std::size_t)b->slots() >= active && (!best || b->slots() < best->slots())) best = b.get();
   return best ? best->run(a, clean) : ctx.boot->run(a);
+}
+
+// bootstrap_active on several ciphertexts (the images of a batched inference) in lockstep:
+// inputs of one level take the sparse-slot variant together (Bootstrapper::run_many),
+// anything else runs one after the other.  Outputs bit-identical to bootstrap_active.
+std::vector<Ciphertext> bootstrap_active_many(Context& ctx, const std::vector<Ciphertext>& as, std::size_t active,
+                                              bool clean) {
+  for (const Ciphertext& a : as) require_valid(a, "bootstrap");
+  std::vector<Ciphertext> outs;
+  bool same = !as.empty() && ctx.boot != nullptr;
+  for (const Ciphertext& a : as) same = same && a.limbs == as[0].limbs;
+  if (!same) {
+    for (const Ciphertext& a : as) outs.push_back(bootstrap_active(ctx, a, active, clean));
+    return outs;
+  }
+  if (active == 0 || active > (std::size_t)ctx.S())
+    throw Error(ErrKind::shape, "bootstrap: active slot count " + std::to_string(active) + " outside [1, " +
+                                    std::to_string(ctx.S()) + "]");
+  Bootstrapper* best = nullptr;
+  if (as[0].limbs >= 2 || clean)
+    for (auto& b : ctx.boot_sparse)
+      if ((std::size_t)b->slots() >= active && (!best || b->slots() < best->slots())) best = b.get();
+  return best ? best->run_many(as, clean) : ctx.boot->run_many(as);
 }
 
 // -------------------------------------------------------------- raw access

@@ -1778,17 +1778,25 @@ std::vector<Ciphertext> cheb_eval_many(Context& ctx, const std::vector<Ciphertex
 
 // secure_relu (layers_misc.cpp:268-295)
 Ciphertext secure_relu(Context& ctx, const Ciphertext& x, double scale, int degree, std::size_t active_slots) {
+  return secure_relu_many(ctx, {x}, scale, degree, active_slots)[0];
+}
+
+// The same activation on several ciphertexts (the images of a batched inference): one
+// polynomial evaluation whose relinearisations, rescales and constant combinations carry
+// every input (cheb_eval_many).  Per input bit-identical to secure_relu.
+std::vector<Ciphertext> secure_relu_many(Context& ctx, const std::vector<Ciphertext>& xs, double scale, int degree,
+                                         std::size_t active_slots) {
   if (degree < 0) throw shape_error("activation degree must be >= 0");
   const bool scaled = scale > 1.0;
   const double beta = scaled ? scale : 1.0;
-  Ciphertext v = x;
+  std::vector<Ciphertext> vs = xs;
   if (scaled) {
     if (active_slots == 0) throw shape_error("scaled activation requires the active slot count");
     if (active_slots > (std::size_t)ctx.S()) throw capacity_error("active slot count exceeds the context");
-    v = mp(ctx, x, range_mask(ctx, 0, active_slots, 1.0 / beta));
+    for (Ciphertext& v : vs) v = mp(ctx, v, range_mask(ctx, 0, active_slots, 1.0 / beta));
   }
   const auto f = [beta](double z) { return z < 0.0 ? 0.0 : beta * z; };
-  return cheb_eval(ctx, v, cheb_coefficients(f, degree));
+  return cheb_eval_many(ctx, vs, cheb_coefficients(f, degree));
 }
 
 // ------------------------------------------------------------- depth costs

@@ -59,6 +59,8 @@ Ciphertext whole_channel_pool(Context& ctx, const PackedTensor& x, std::size_t k
 Ciphertext fully_connected(Context& ctx, const Ciphertext& x, std::size_t n, std::size_t m, std::size_t merge_budget,
                            const double* w, const double* bias);
 Ciphertext secure_relu(Context& ctx, const Ciphertext& x, double scale, int degree, std::size_t active_slots);
+std::vector<Ciphertext> secure_relu_many(Context& ctx, const std::vector<Ciphertext>& xs, double scale, int degree,
+                                         std::size_t active_slots);
 
 // ---- Chebyshev (chebyshev.cpp)
 std::vector<double> cheb_coefficients(const std::function<double(double)>& f, int degree);

@@ -835,6 +835,7 @@ class EncryptedModel:
                                               boot_sparse))
         self.security = self.ctx.security()
         self._layer_keys: Optional[List[keyplan.LayerKeys]] = None
+        self.batch_relu = True  # forward_batch: activations of a batch in one polynomial evaluation
         self._pinned_keys = self.ctx.key_count()  # relinearisation / bootstrapping keys made at creation
         if spec.weight_mode == "lazy":
             self.ctx.set_weight_cache(0)
@@ -887,6 +888,51 @@ class EncryptedModel:
             self.ctx.sync()
             timings[b.name] = timings.get(b.name, 0.0) + (time.perf_counter() - t0) * 1e3
         return out
+
+    def _run_batch(self, b: Built, vs: List, timings=None) -> List:
+        """One layer on the images of a batch in lockstep (model_run.cpp:100-159 once
+        per image): bootstraps run together through bootstrap_many, so each
+        bootstrapping key and encoded diagonal is read from HBM once per batch and the
+        NTT / basis-conversion launches carry the whole batch; the other layers run
+        image by image on the same stream.  Per image the operations are those of
+        _run (outputs bit-identical)."""
+        packed, C, W, n = b.in_shape
+        if b.type == "bootstrap":
+            clean = all(getattr(v, "_clean", False) for v in vs)
+            return fh.bootstrap_many(vs, C * W * W if packed else n, clean=clean)
+        if b.type == "relu" and self.batch_relu:
+            L = b.src
+            active = C * W * W if packed else n
+            return fh.secure_relu_many(vs, fh.ReluConfig(L.params.get("scale", 1.0), L.params.get("degree", 59),
+                                                         active))
+        if b.type == "residual":
+            body = vs
+            for c in b.body:
+                body = self._run_batch(c, body, timings)
+            skip = vs
+            for c in b.downsample:
+                skip = self._run_batch(c, skip, timings)
+            outs = []
+            for bd, sk in zip(body, skip):
+                o = fh.add(bd, sk)
+                o._clean = getattr(bd, "_clean", False) and getattr(sk, "_clean", False)
+                outs.append(o)
+            return outs
+        return [self._run(b, v, timings) for v in vs]
+
+    def forward_batch(self, vs: List[fh.SlotVector]) -> List[fh.SlotVector]:
+        """forward() on several encrypted images in lockstep (one stream, one host
+        thread): see _run_batch."""
+        vs = list(vs)
+        for b in self.layers:
+            vs = self._run_batch(b, vs)
+        return vs
+
+    def infer_batch(self, xs: List[np.ndarray]) -> List[np.ndarray]:
+        """Encrypt every image, forward_batch, decrypt: the logits per image."""
+        outs = self.forward_batch([self.encrypt_input(x) for x in xs])
+        m = self.output_count()
+        return [o.slots()[:m].copy() for o in outs]
 
     def layer_keys(self) -> List[keyplan.LayerKeys]:
         """Per top-level layer, the rotation indices (with use counts) this engine

@@ -195,3 +195,41 @@ def test_bootstrap_active_level0_runs_full(sctx):
     assert np.abs(y.slots() - v).max() < 1e-4
     with pytest.raises(fh.ShapeError):
         fh.bootstrap(x, S + 1)
+
+
+@pytest.mark.parametrize("active,clean,level", [(S // 4, False, 2), (S // 8, True, 1), (S // 2, False, 3)])
+def test_bootstrap_many_bit_identical(sctx, active, clean, level):
+    """bootstrap_many (the images of a batched inference in lockstep: keys and
+    diagonals read once per batch) returns, per input, the very words of
+    bootstrap(x, active, clean) -- and one bootstrap trace event per input."""
+    rng = np.random.default_rng(100 + active)
+    vs = [rng.uniform(-1, 1, S) for _ in range(3)]
+    if clean:
+        for v in vs:
+            v[active:] = 0.0
+    xs = [fh.level_down(fh.SlotVector.encode(sctx, v), level) for v in vs]
+    singles = [fh.bootstrap(x, active, clean=clean) for x in xs]
+    rec = sctx.attach_recorder()
+    many = fh.bootstrap_many(xs, active, clean=clean)
+    ev = [(e.kind, e.value) for e in rec.snapshot()]
+    sctx.detach_recorder()
+    assert ev == [("bootstrap", sctx.depth_budget())] * 3
+    for s, m, v in zip(singles, many, vs):
+        assert m.level() == s.level() == sctx.depth_budget()
+        assert np.array_equal(m.words(), s.words())
+        assert np.abs(m.slots()[:active] - v[:active]).max() < 1e-4
+
+
+def test_bootstrap_many_mixed_levels_and_full(sctx):
+    """Inputs on different levels (or no sparse variant: level 0 without `clean`)
+    run one after the other with the same results."""
+    rng = np.random.default_rng(77)
+    vs = [rng.uniform(-1, 1, S) for _ in range(2)]
+    xs = [fh.level_down(fh.SlotVector.encode(sctx, vs[0]), 2), fh.level_down(fh.SlotVector.encode(sctx, vs[1]), 3)]
+    many = fh.bootstrap_many(xs, S // 4)
+    for x, m in zip(xs, many):
+        assert np.array_equal(m.words(), fh.bootstrap(x, S // 4).words())
+    x0 = [fh.level_down(fh.SlotVector.encode(sctx, v), 1) for v in vs]  # level 0: full pipeline
+    for m, v in zip(fh.bootstrap_many(x0, 100), vs):
+        assert np.abs(m.slots() - v).max() < 1e-4
+    assert fh.bootstrap_many([], 10) == []

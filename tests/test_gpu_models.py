@@ -244,3 +244,25 @@ def test_vgg16_paper_widths_128bit():
     cal = [norm(np.random.default_rng(5002 + i).uniform(0, 1, (3, 32, 32))) for i in range(4)]
     spec = M.calibrate_relu_scales(M.vgg16_paper(ring=65536, depth_budget=11), cal)
     _compare(spec, norm(np.random.default_rng(5001).uniform(0, 1, (3, 32, 32))), "fast", 128)
+
+
+def test_forward_batch_bit_identical_to_forward():
+    """forward_batch (images in lockstep, bootstraps through bootstrap_many) yields,
+    per image, the very ciphertext words of forward(): LeNet-5 on a 2^13 ring with
+    five bootstraps, three images; and the bootstrap count scales with the batch."""
+    spec = M.lenet5(ring=8192, depth_budget=12)
+    em = M.EncryptedModel(spec, security=0)
+    xs = [np.random.default_rng(3100 + i).uniform(0, 1, (1, 28, 28)) for i in range(3)]
+    vs = [em.encrypt_input(x) for x in xs]  # ciphertexts are immutable: both paths read the same inputs
+    singles = [em.forward(v) for v in vs]
+    rec = em.ctx.attach_recorder()
+    many = em.forward_batch(vs)
+    boots = sum(1 for e in rec.snapshot() if e.kind == "bootstrap")
+    em.ctx.detach_recorder()
+    assert boots == 3 * em.n_boot
+    for s, m in zip(singles, many):
+        assert m.level() == s.level()
+        assert np.array_equal(m.words(), s.words())
+    m = em.output_count()
+    for x, lg, s in zip(xs, em.infer_batch(xs), singles):
+        assert np.abs(lg - s.slots()[:m]).max() < 1e-5
