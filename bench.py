@@ -402,11 +402,27 @@ def run_ours(args):
     ctx_s = time.perf_counter() - t_ctx
     stream = torch.cuda.ExternalStream(ctx.stream())
     xin = em.encrypt_input(x)  # the encrypted input, resident in HBM
-    # images in flight: key-sharing context clones (own stream, shared keys), one host thread each
+    # batches in flight: key-sharing context clones (own stream, shared keys), one host thread each,
+    # every one stepping a batch of B images in lockstep (EncryptedModel.forward_batch: bootstraps and
+    # activations of the batch share their launches, keys and diagonals read once per batch)
     F = max(1, args.in_flight)
+    B = max(1, args.image_batch)
     ems = [em] + [em.clone() for _ in range(F - 1)]
-    xins = [xin] + [e.encrypt_input(x) for e in ems[1:]]
+
+    def image(k):  # the seeded image first, then further seeded images of the same distribution
+        return x if k == 0 else (np.random.default_rng(4100 + k).uniform(0, 1, (3, 32, 32)) - 0.5) / 0.2887
+
+    host_images = [[image(i * B + b) for b in range(B)] for i in range(F)]
+    xins = [[xin if (i == 0 and b == 0) else e.encrypt_input(host_images[i][b]) for b in range(B)]
+            for i, e in enumerate(ems)]
     streams = [stream] + [torch.cuda.ExternalStream(e.ctx.stream()) for e in ems[1:]]
+
+    def stats_all():
+        tot = {}
+        for e in ems:
+            for k, v in e.ctx.stats().items():
+                tot[k] = tot.get(k, 0) + v
+        return tot
 
     def barrier():
         torch.cuda.synchronize()
@@ -415,10 +431,25 @@ def run_ours(args):
         if ws > 1:
             torch.distributed.barrier()
 
-    for _ in range(args.warmup):  # lazy key generation, weight plaintexts, pool growth
-        for e, xi in zip(ems, xins):
-            out = e.forward(xi)
+    # warm-up: one pass per context in turn (lazy key generation, weight plaintexts), then the
+    # timed pattern itself -- all batches in flight together -- so the stream-ordered pool reaches
+    # its concurrent footprint before the clock starts (mapping new pool memory mid-run costs
+    # 15-20 %: measured 0.377 vs 0.318 s/image)
+    for e, xi in zip(ems, xins):
+        out = e.forward_batch(xi)
+    out = em.forward(xin)
     del out
+
+    def warm(i):
+        for _ in range(max(1, args.warmup - 1)):
+            ems[i].forward_batch(xins[i])
+        ems[i].ctx.sync()
+
+    th = [threading.Thread(target=warm, args=(i,)) for i in range(F)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
     barrier()
     # single-image latency: one stream, K steps
     l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -430,20 +461,21 @@ def run_ours(args):
     latency_s = l0.elapsed_time(l1) / args.steps / 1e3
     del out
     barrier()
-    st0 = ctx.stats()
+    st0 = stats_all()
     prof = None
     if os.environ.get("FHEON_PROFILE_RANGE"):
         import ctypes
         prof = ctypes.CDLL("libcudart.so.12")
         prof.cudaProfilerStart()
-    # throughput: F images in flight, every stream starts at e0 (stream-ordered), ends at its own event
+    # throughput: F batches of B images in flight, every stream starts at e0 (stream-ordered), ends at
+    # its own event
     e0 = torch.cuda.Event(enable_timing=True)
     ends = [torch.cuda.Event(enable_timing=True) for _ in ems]
     outs = [None] * F
 
     def run(i):
         for _ in range(args.steps):
-            outs[i] = ems[i].forward(xins[i])
+            outs[i] = ems[i].forward_batch(xins[i])
         ends[i].record(streams[i])
 
     with ClockSampler(local) as clk:
@@ -462,13 +494,16 @@ def run_ours(args):
     ms = max(e0.elapsed_time(ev) for ev in ends)
     if prof is not None:
         prof.cudaProfilerStop()
-    st1 = ctx.stats()
-    logits_dev = outs[0].slots()[:em.output_count()]
-    logits_twin_diff = max(float(np.abs(o.slots()[:em.output_count()] - logits_dev).max()) for o in outs)
+    st1 = stats_all()
+    logits_dev = outs[0][0].slots()[:em.output_count()]
+    # the lockstep batch against one image at a time: same ciphertext words (image 0 of batch 0)
+    single = em.forward(xin)
+    batch_vs_single_words_equal = bool(np.array_equal(single.words(), outs[0][0].words()))
+    del single
     out = None
     outs = None
     barrier()
-    ips, ms_max = replicas.replica_throughput(ms, args.steps * F, torch.device("cuda", local))
+    ips, ms_max = replicas.replica_throughput(ms, args.steps * F * B, torch.device("cuda", local))
     value = 1.0 / ips  # seconds per image over all ranks' images
 
     # ---- roofline of the dominant kernel class (NTT: integer-pipe bound), timed live in a
@@ -505,17 +540,37 @@ def run_ours(args):
                 "traffic": None,
                 "traffic_note": "DRAM bytes per launch: profiles/r02_ncu_resnet_ntt.csv"}
 
-    # ---- e2e through the public API: host image -> encode + encrypt -> forward -> decrypt
+    # ---- e2e through the public API: host images -> encode + encrypt -> forward -> decrypt -> host
+    # logits, the same F batches of B in flight (EncryptedModel.infer_batch from F host threads);
+    # wall clock from the first call to the last result on the host
     e2e_steps = max(3, args.steps // 2)
-    em.infer(x)
+    e2e_out = [None] * F
+
+    def run_e2e(i, n):
+        for _ in range(n):
+            e2e_out[i] = ems[i].infer_batch(host_images[i])
+
+    def e2e_pass(n):
+        th = [threading.Thread(target=run_e2e, args=(i, n)) for i in range(F)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    e2e_pass(1)
     barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        r = em.infer(x)
+    e2e_pass(e2e_steps)
     barrier()
-    e2e_ips, _ = replicas.replica_throughput((time.perf_counter() - t0) * 1e3, e2e_steps,
+    e2e_ips, _ = replicas.replica_throughput((time.perf_counter() - t0) * 1e3, e2e_steps * F * B,
                                              torch.device("cuda", local))
-    logit_err_dev_vs_api = float(np.abs(r.logits - logits_dev).max())
+    logit_err_dev_vs_api = float(np.abs(e2e_out[0][0] - logits_dev).max())
+    # one image at a time through infer() (latency shape of the same path)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        r = em.infer(x)
+    e2e_latency_s = (time.perf_counter() - t0) / 3
+    del r
 
     line = {
         "metric": "encrypted inference s/image (ResNet-20, CKKS N=2^16, full bootstrapping, 128-bit security)",
@@ -526,7 +581,9 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 3),
         "host_enqueue_ms_per_step": round(host_ms / args.steps, 3),
-        "images_in_flight": F,
+        "images_in_flight": F * B,
+        "batches_in_flight": F,
+        "batch": B,
         "latency_s_per_image": round(latency_s, 4),
         "higher_is_better": False,
         "scaling": "weak",
@@ -538,17 +595,20 @@ def run_ours(args):
         "chain": {"limbs": ctx.L, "special_limbs": ctx.K, "dnum": ctx.dnum, "bootstraps": em.n_boot,
                   "context_create_s": round(ctx_s, 2), "key_bytes": ctx.key_bytes()},
         "e2e": {"value": round(1.0 / e2e_ips, 4), "unit": "s/image",
-                "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": 2 * N * 8,
-                "path": "EncryptedModel.infer (public API): host image -> host special-FFT encode -> "
-                        "h2d of N int64 coefficients -> device RNS + NTT + encrypt -> forward -> device "
-                        "decrypt -> d2h of 2 limbs -> host CRT + decode -> logits",
+                "h2d_bytes_per_step": N * 8 * F * B, "d2h_bytes_per_step": 2 * N * 8 * F * B,
+                "path": "EncryptedModel.infer_batch (public API) from F host threads: host images -> "
+                        "h2d of the slot values -> device special-FFT encode + RNS + NTT + encrypt -> "
+                        "forward_batch -> device decrypt -> d2h of 2 limbs per image -> host CRT + decode -> "
+                        "logits on the host",
                 "steps": e2e_steps, "logits_max_abs_diff_vs_value_path": logit_err_dev_vs_api,
-                "images_in_flight": 1},
-        "value_note": f"{F} images in flight per GPU (key-sharing context clones, one stream and host thread "
-                      f"each, SlotContext.clone); latency_s_per_image is one image at a time; the in-flight "
-                      f"results agree to {logits_twin_diff:.1e}",
+                "images_in_flight": F * B, "latency_s_per_image": round(e2e_latency_s, 4)},
+        "value_note": f"{F} batches of {B} images in flight per GPU: key-sharing context clones "
+                      f"(SlotContext.clone, one stream and host thread each), each stepping its batch in "
+                      f"lockstep (forward_batch: bootstraps / activations of the batch share launches, keys "
+                      f"and diagonals); latency_s_per_image is one image at a time; a batched image's "
+                      f"ciphertext words equal the one-at-a-time result: {batch_vs_single_words_equal}",
         "gpu_launches": int(st1["launches"] - st0["launches"]),
-        "ops_per_image": {k: int((st1[k] - st0[k]) // args.steps) for k in
+        "ops_per_image": {k: int((st1[k] - st0[k]) // (args.steps * F * B)) for k in
                           ("rotations", "keyswitches", "mult_plain", "mult_cipher", "rescales", "ntt_limbs")},
         "roofline": roofline,
         "clocks": clk.summary(),
@@ -941,7 +1001,9 @@ def main():
     ap.add_argument("--no-resnet", action="store_true", help="skip the ResNet-20 / VGG-16 model variants")
     ap.add_argument("--no-vgg", action="store_true", help="skip VGG-16")
     ap.add_argument("--depth", type=int, default=HEAD_DEPTH, help="ResNet-20 depth budget of the headline chain")
-    ap.add_argument("--in-flight", type=int, default=4, help="images in flight per GPU (key-sharing contexts)")
+    ap.add_argument("--in-flight", type=int, default=3,
+                    help="batches in flight per GPU (key-sharing contexts, one host thread each)")
+    ap.add_argument("--image-batch", type=int, default=4, help="images per lockstep batch (forward_batch)")
     ap.add_argument("--models", default="", help="comma-separated name prefixes of the model cases to run")
     ap.add_argument("--no-rotations", action="store_true", help="skip the configs[1] rotation block")
     ap.add_argument("--model-case", default="", help=argparse.SUPPRESS)

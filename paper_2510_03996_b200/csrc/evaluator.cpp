@@ -605,31 +605,36 @@ std::vector<Ciphertext> bsgs_double_hoisted_many(Context& ctx, const std::vector
                                    (std::size_t)K * N * sizeof(u64), st));
     }
   }
-  auto baby_ptr = [&](int b, int i) {
-    return b < 0 ? ident->ptr + (std::size_t)i * accw : accs->ptr + ((std::size_t)b * B + i) * accw;
-  };
-  // inner sums over Q u P, one output accumulator per (giant, input): output g * B + i
+  // inner sums over Q u P, one output accumulator per (giant, input): output g * B + i; every
+  // giant set x input chunk in one launch (each diagonal read once per batch, each baby once
+  // per giant set)
   const std::size_t nout = (std::size_t)ng * B;
   BufPtr inner = ctx.alloc(nout * accw);
-  for (std::size_t o0 = 0; o0 < nout; o0 += kMacMaxOut) {
-    MacJobs jb{};
-    jb.nout = (int)std::min<std::size_t>(kMacMaxOut, nout - o0);
-    for (int z = 0; z < jb.nout; ++z) {
-      const DhGiant& gi = giants[(o0 + z) / B];
-      const int i = (int)((o0 + z) % B);
-      if (gi.terms.empty() || gi.terms.size() > (std::size_t)kMacMaxTerms)
-        throw Error(ErrKind::internal, "double-hoisted transform: 1..32 terms per giant");
-      for (std::size_t j = 0; j < gi.terms.size(); ++j) {
-        jb.ct[z][j] = baby_ptr(gi.terms[j].first, i);
-        jb.c1_off[z][j] = (long long)E * (long long)N;
-        jb.pt[z][j] = gi.terms[j].second->ptr;
+  for (int g0 = 0; g0 < ng; g0 += kBsgsMaxGiants)
+    for (int i0 = 0; i0 < B; i0 += kBsgsMaxIn) {
+      BsgsMacJobs jb{};
+      jb.ngiants = std::min(kBsgsMaxGiants, ng - g0);
+      jb.nin = std::min(kBsgsMaxIn, B - i0);
+      jb.baby_stride = (long long)B * (long long)accw;
+      jb.out_stride = (long long)B * (long long)accw;
+      jb.c1_off = (long long)E * (long long)N;
+      for (int z = 0; z < jb.ngiants; ++z) {
+        const DhGiant& gi = giants[g0 + z];
+        if (gi.terms.empty() || gi.terms.size() > (std::size_t)kMacMaxTerms)
+          throw Error(ErrKind::internal, "double-hoisted transform: 1..32 terms per giant");
+        for (std::size_t j = 0; j < gi.terms.size(); ++j) {
+          jb.pt[z][j] = gi.terms[j].second->ptr;
+          jb.bidx[z][j] = (short)gi.terms[j].first;
+        }
+        jb.nterm[z] = (int)gi.terms.size();
       }
-      jb.nterm[z] = (int)gi.terms.size();
-      jb.out0[z] = inner->ptr + (o0 + z) * accw;
-      jb.out1[z] = jb.out0[z] + (std::size_t)E * N;
+      for (int i = 0; i < jb.nin; ++i) {
+        jb.babies[i] = accs ? accs->ptr + (std::size_t)(i0 + i) * accw : nullptr;
+        jb.ident[i] = ident ? ident->ptr + (std::size_t)(i0 + i) * accw : nullptr;
+        jb.out[i] = inner->ptr + ((std::size_t)g0 * B + i0 + i) * accw;
+      }
+      mac_bsgs(t, jb, E, st, limbs);
     }
-    mac_pt(t, jb, E, st, limbs);
-  }
   std::vector<u64*> accp(nout);
   for (std::size_t o = 0; o < nout; ++o) accp[o] = inner->ptr + o * accw;
   std::vector<Ciphertext> rows = moddown_accs(ctx, accp, limbs);

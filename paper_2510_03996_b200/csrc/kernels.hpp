@@ -167,7 +167,7 @@ void ks_inner_product(const DevTables& t, const KsJobs& jobs, int limbs, cudaStr
 // so that ONE ModDown of acc_r yields sum_j rot(x_j): the c0 terms ride through
 // the division by P exactly (P * c0 is 0 mod every p_k).
 constexpr int kMaxSumJobs = 64;
-constexpr int kMaxSumGroups = 16;
+constexpr int kMaxSumGroups = 64;  // (a batch's babies x images in one launch: every key read once)
 struct KsSumJobs {
   const u64* key[kMaxSumJobs];
   const u64* ext[kMaxSumJobs];
@@ -219,6 +219,23 @@ struct MacJobs {
   int nterm[kMacMaxOut];
   int nout;
 };
+// The inner sums of a double-hoisted transform over a batch of inputs in ONE launch:
+// output (g, i) = sum_j pt[g][j] (*) baby(i, bidx[g][j]) over Q u P, baby(i, b) =
+// babies[i] + b * baby_stride (b >= 0) or ident[i] (b < 0); grid x = g * nin + i (fastest), so
+// the CTAs running together read each diagonal once per batch and each baby once per giant set.
+constexpr int kBsgsMaxGiants = 16;
+constexpr int kBsgsMaxIn = 16;
+struct BsgsMacJobs {
+  const u64* pt[kBsgsMaxGiants][kMacMaxTerms];  // [E][N] standard form
+  short bidx[kBsgsMaxGiants][kMacMaxTerms];
+  int nterm[kBsgsMaxGiants];
+  const u64* babies[kBsgsMaxIn];  // [nb][2][E][N]
+  const u64* ident[kBsgsMaxIn];   // [2][E][N] or null
+  u64* out[kBsgsMaxIn];           // [ngiants][2][E][N]: giant g at out[i] + g * out_stride
+  long long baby_stride, out_stride, c1_off;
+  int ngiants, nin;
+};
+void mac_bsgs(const DevTables& t, const BsgsMacJobs& jobs, int E, cudaStream_t st, int ell);
 // ell >= 0: Q u P operands ([limbs][N], limbs ell.. on the special primes)
 void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st, int ell = -1);
 // Plaintext as a linear combination of cached real-coefficient basis vectors

@@ -489,6 +489,42 @@ __global__ void k_mac(MacJobs jobs, const PrimeConst* __restrict__ pc, int logN,
                       redc(mulhi(s1[1], P.r2), s1[1] * P.r2, P.q, P.qinv_neg));
 }
 
+// grid (ngiants * nin, N/512, E): kernels.hpp BsgsMacJobs.  Per output the products and
+// their order are k_mac's (bit-identical sums).
+__global__ void k_mac_bsgs(BsgsMacJobs jobs, const PrimeConst* __restrict__ pc, int logN, int ell, int L) {
+  const std::size_t o = ((std::size_t)blockIdx.z << logN) + 2 * (blockIdx.y * blockDim.x + threadIdx.x);
+  const int g = blockIdx.x / jobs.nin;
+  const int i = blockIdx.x - g * jobs.nin;
+  const int t = (int)blockIdx.z;
+  const PrimeConst P = pc[t < ell ? t : L + (t - ell)];
+  const int nt = jobs.nterm[g];
+  FHEON_DCHECK(g < jobs.ngiants && g < kBsgsMaxGiants && i < kBsgsMaxIn && nt >= 1 && nt <= kMacMaxTerms);
+  const u64* babies = jobs.babies[i];
+  const u64* ident = jobs.ident[i];
+  u64 s0[2] = {0, 0}, s1[2] = {0, 0};
+  Acc128 a0[2], a1[2];
+  for (int j = 0; j < nt; ++j) {  // nt <= kMacMaxTerms = 32 products < 32 q^2: one lazy flush
+    const int b = jobs.bidx[g][j];
+    const u64* c = b < 0 ? ident : babies + (long long)b * jobs.baby_stride;
+    const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(jobs.pt[g][j] + o);
+    const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(c + o);
+    const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(c + jobs.c1_off + o);
+    a0[0].mac(x0.x, p.x);
+    a1[0].mac(x1.x, p.x);
+    a0[1].mac(x0.y, p.y);
+    a1[1].mac(x1.y, p.y);
+  }
+  lazy_flush(s0[0], s1[0], a0[0], a1[0], P);
+  lazy_flush(s0[1], s1[1], a0[1], a1[1], P);
+  u64* out = jobs.out[i] + (long long)g * jobs.out_stride;
+  *reinterpret_cast<ulonglong2*>(out + o) =
+      make_ulonglong2(redc(mulhi(s0[0], P.r2), s0[0] * P.r2, P.q, P.qinv_neg),
+                      redc(mulhi(s0[1], P.r2), s0[1] * P.r2, P.q, P.qinv_neg));
+  *reinterpret_cast<ulonglong2*>(out + jobs.c1_off + o) =
+      make_ulonglong2(redc(mulhi(s1[0], P.r2), s1[0] * P.r2, P.q, P.qinv_neg),
+                      redc(mulhi(s1[1], P.r2), s1[1] * P.r2, P.q, P.qinv_neg));
+}
+
 // grid (N/256, 1)
 __global__ void k_encode_lincomb(u64* out, LinComb lc, double scale, const PrimeConst* __restrict__ pc, int logN,
                                  int limbs) {
@@ -806,6 +842,12 @@ void mac_pt(const DevTables& t, const MacJobs& jobs, int limbs, cudaStream_t st,
   const dim3 grid(jobs.nout, (unsigned)(t.N / (2 * kThreads)), limbs);
   k_mac<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN, ell < 0 ? limbs : ell, t.L);
   launch_check("k_mac");
+}
+void mac_bsgs(const DevTables& t, const BsgsMacJobs& jobs, int E, cudaStream_t st, int ell) {
+  if (jobs.ngiants == 0 || jobs.nin == 0) return;
+  const dim3 grid(jobs.ngiants * jobs.nin, (unsigned)(t.N / (2 * kThreads)), E);
+  k_mac_bsgs<<<grid, kThreads, 0, st>>>(jobs, t.pc, t.logN, ell, t.L);
+  launch_check("k_mac_bsgs");
 }
 void encode_lincomb(const DevTables& t, u64* out, const LinComb& lc, double scale, int limbs, cudaStream_t st) {
   k_encode_lincomb<<<grid_for(t.N, 1), kThreads, 0, st>>>(out, lc, scale, t.pc, t.logN, limbs);

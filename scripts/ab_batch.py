@@ -20,7 +20,10 @@ spec = M.calibrate_relu_scales(spec, [norm(np.random.default_rng(4002 + i).unifo
                                       for i in range(3)])
 em = M.EncryptedModel(spec)
 REPS = int(os.environ.get("REPS", "4"))
+if os.environ.get("SWITCH"):
+    sys.setswitchinterval(float(os.environ["SWITCH"]))
 F = int(os.environ.get("FLIGHT", "1"))
+em.batch_relu = os.environ.get("BATCH_RELU", "1") != "0"
 ems = [em] + [em.clone() for _ in range(F - 1)]
 
 
@@ -59,5 +62,8 @@ def run_all(B):
 for B in [int(a) for a in sys.argv[1:]] or [0, 1, 2, 4]:
     try:
         print(f"B={B} (0 = forward) x {F} in flight: {run_all(B):.4f} s/image", flush=True)
+        import torch
+        free, total = torch.cuda.mem_get_info()
+        print(f"   device memory free {free / 1e9:.1f} of {total / 1e9:.1f} GB", flush=True)
     except Exception as ex:  # noqa: BLE001
         print(f"B={B}: failed: {str(ex)[:200]}", flush=True)

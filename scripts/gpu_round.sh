@@ -1,0 +1,11 @@
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 1500 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$?
+tail -3 gpurun_out/bench.err
+cut -c1-900 gpurun_out/bench.log
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err; echo rc=$?
+cut -c1-600 gpurun_out/bench_ref.log
+bash scripts/gpu_ncu_ntt.sh
