@@ -39,11 +39,14 @@ def timed(fn, reps=REPS, warm=2):
 
 
 def run_all(B):
+    STEPS = int(os.environ.get("STEPS", "1"))  # forward passes per thread between synchronisations
+
     def work(e, vs):
-        if B == 0:
-            e.forward(vs[0])
-        else:
-            e.forward_batch(vs)
+        for _ in range(STEPS):
+            if B == 0:
+                e.forward(vs[0])
+            else:
+                e.forward_batch(vs)
         e.ctx.sync()
     ins = []
     for k, e in enumerate(ems):
@@ -56,7 +59,7 @@ def run_all(B):
             t.start()
         for t in th:
             t.join()
-    return timed(once) / (max(B, 1) * F)
+    return timed(once) / (max(B, 1) * F * STEPS)
 
 
 for B in [int(a) for a in sys.argv[1:]] or [0, 1, 2, 4]:
