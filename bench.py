@@ -441,17 +441,6 @@ def run_ours(args):
     out = em.forward(xin)
     del out
 
-    def warm(i):
-        for _ in range(max(1, args.warmup - 1)):
-            ems[i].forward_batch(xins[i])
-        ems[i].ctx.sync()
-
-    th = [threading.Thread(target=warm, args=(i,)) for i in range(F)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    barrier()
     # single-image latency: one stream, K steps
     l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0.record(stream)
@@ -461,6 +450,18 @@ def run_ours(args):
     l1.synchronize()
     latency_s = l0.elapsed_time(l1) / args.steps / 1e3
     del out
+    barrier()
+
+    def warm(i):  # the timed pattern, untimed (same per-batch synchronisation)
+        for _ in range(max(1, args.warmup - 1)):
+            ems[i].forward_batch(xins[i])
+            ems[i].ctx.sync()
+
+    th = [threading.Thread(target=warm, args=(i,)) for i in range(F)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
     barrier()
     st0 = stats_all()
     prof = None

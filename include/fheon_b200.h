@@ -292,7 +292,8 @@ int fheon_fully_connected(fheon_ctx* ctx, const fheon_ct* x, size_t inputs, size
 /* secure_relu (layers_misc.cpp:268-295): Chebyshev interpolant of max(0, scale*z), degree */
 int fheon_secure_relu(fheon_ctx* ctx, const fheon_ct* x, double scale, int degree, size_t active_slots,
                       fheon_ct** out);
-/* secure_relu on n ciphertexts in lockstep (the images of a batched inference): one polynomial
+/* secure_relu (layers_misc.cpp:268-295) on n ciphertexts in lockstep (the images of a batched
+ * inference, model_run.cpp:100-159 once per image): one polynomial
  * evaluation whose relinearisations and rescales carry every input; outs[i] bit-identical to
  * fheon_secure_relu(xs[i]) */
 int fheon_secure_relu_many(fheon_ctx* ctx, const fheon_ct* const* xs, size_t n, double scale, int degree,

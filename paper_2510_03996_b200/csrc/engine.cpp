@@ -85,16 +85,19 @@ namespace {
 // stream-ordered allocation; on out-of-memory the context's plaintext caches are
 // released (their buffers return to the pool once the compute stream passes their
 // last use) and the allocation is retried once
+cudaError_t pool_alloc(Context* c, void** p, std::size_t bytes, cudaStream_t st) {
+  return c->mem_pool() ? cudaMallocFromPoolAsync(p, bytes, c->mem_pool(), st) : cudaMallocAsync(p, bytes, st);
+}
 u64* device_alloc(Context* c, std::size_t words, cudaStream_t st) {
   void* p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), st);
+  cudaError_t e = pool_alloc(c, &p, words * sizeof(u64), st);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     static const bool dbg = std::getenv("FHEON_ALLOC_DEBUG") != nullptr;
     if (dbg) std::fprintf(stderr, "[fheon] allocation of %zu bytes failed: releasing plaintext caches\n", words * 8);
     if (c->release_caches() > 0) {
       FHEON_CUDA(cudaStreamSynchronize(c->stream()));
-      e = cudaMallocAsync(&p, words * sizeof(u64), st);
+      e = pool_alloc(c, &p, words * sizeof(u64), st);
     }
   }
   if (e != cudaSuccess) {
@@ -269,8 +272,24 @@ Context::Context(const Params& p, const Context* parent) : ht_(make_tables(p)) {
   FHEON_CUDA(cudaStreamCreateWithPriority(&unpack_, cudaStreamNonBlocking, prio_greatest));
   FHEON_CUDA(cudaStreamCreateWithPriority(&pack_, cudaStreamNonBlocking, prio_greatest));
   {
+    // One stream-ordered pool PER CONTEXT: contexts in flight (key-sharing clones, one stream and
+    // host thread each) must not recycle each other's blocks -- a block freed on one stream and
+    // handed to another makes the allocator either insert a dependency between the streams (they
+    // serialise at random points) or map new memory mid-run; both showed as a bimodal 0.31-0.38
+    // s/image with batches in flight.  FHEON_PRIVATE_POOL=0: the device's default pool (A/B).
     cudaMemPool_t pool;
-    FHEON_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    const char* pp = std::getenv("FHEON_PRIVATE_POOL");
+    if (pp && std::atoi(pp) == 0) {
+      FHEON_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    } else {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      FHEON_CUDA(cudaMemPoolCreate(&pool_, &props));
+      pool = pool_;
+    }
     std::uint64_t thr = UINT64_MAX;
     FHEON_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     // Pre-grow the stream-ordered pool so steady-state key switching never
@@ -285,7 +304,7 @@ Context::Context(const Params& p, const Context* parent) : ht_(make_tables(p)) {
     // key-switch scratch pool need the rest
     weight_cache_budget = std::min<std::size_t>(weight_cache_budget, free_b / 2);
     void* r = nullptr;
-    if (want > 0 && cudaMallocAsync(&r, want, stream_) == cudaSuccess) cudaFreeAsync(r, stream_);
+    if (want > 0 && pool_alloc(this, &r, want, stream_) == cudaSuccess) cudaFreeAsync(r, stream_);
     cudaGetLastError();
   }
   for (int i = 0; i < kStaging; ++i) {
@@ -352,6 +371,11 @@ Context::~Context() {
   if (unpack_) cudaStreamDestroy(unpack_);
   if (pack_) cudaStreamDestroy(pack_);
   if (stream_) cudaStreamDestroy(stream_);
+  // released once the last outstanding allocation (a handle that outlives the context) is freed
+  if (pool_) {
+    cudaMemPoolTrimTo(pool_, 0);
+    cudaMemPoolDestroy(pool_);
+  }
 }
 
 void Context::build_device_tables() {

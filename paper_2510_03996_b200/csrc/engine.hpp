@@ -133,6 +133,8 @@ class Context {
   const HostTables& host() const { return ht_; }
   const DevTables& dev() const { return dt_; }
   cudaStream_t stream() const { return stream_; }
+  // this context's own stream-ordered pool (null: the device's default pool)
+  cudaMemPool_t mem_pool() const { return pool_; }
   std::size_t N() const { return ht_.N; }
   int S() const { return ht_.S; }
   int L() const { return ht_.p.L; }
@@ -251,6 +253,7 @@ class Context {
   HostTables ht_;
   DevTables dt_{};
   cudaStream_t stream_ = nullptr;
+  cudaMemPool_t pool_ = nullptr;
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr, unpack_ = nullptr, pack_ = nullptr;
   std::vector<cudaEvent_t> event_pool_;
   std::vector<std::pair<cudaEvent_t, BufPtr>> held_;

@@ -277,6 +277,29 @@ def test_secure_relu(env, degree, scale):
     check(out, ev, r, f"relu degree={degree} scale={scale}", ctx.schedule())
 
 
+@pytest.mark.parametrize("degree,scale", [(27, 1.0), (59, 8.0)])
+def test_secure_relu_many_bit_identical(env, degree, scale):
+    """secure_relu_many (the activations of a batch in one polynomial evaluation): per
+    input the very words of secure_relu, under both schedules, and the same events thrice."""
+    ctx, ref = env
+    rng = np.random.default_rng(degree + 1)
+    n = 40
+    cfg = fh.ReluConfig(scale, degree, n)
+    xs = [fh.SlotVector.encode(ctx, rng.uniform(-1, 1, n) * scale) for _ in range(3)]
+    rec = ctx.attach_recorder()
+    singles = [fh.secure_relu(x, cfg) for x in xs]
+    ev1 = sorted((e.kind, e.value) for e in rec.snapshot())
+    rec.clear()
+    many = fh.secure_relu_many(xs, cfg)
+    evm = sorted((e.kind, e.value) for e in rec.snapshot())
+    ctx.detach_recorder()
+    assert evm == ev1
+    for s_, m in zip(singles, many):
+        assert m.level() == s_.level()
+        assert np.array_equal(m.words(), s_.words())
+    assert fh.secure_relu_many([], cfg) == []
+
+
 @pytest.mark.parametrize("schedule", ["reference", "fast"])
 def test_config1_conv_layer(schedule):
     """BASELINE configs[0]: N=2^14, 8192 slots, 50-bit q0 + 40-bit scaling, depth 10, dnum 3;
