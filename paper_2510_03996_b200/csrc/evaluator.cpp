@@ -320,6 +320,11 @@ struct SumJob {
   int in;
   int group;
   u64 key_id = kNoKeyOverride;  // the key to read when it is not the Galois element's own
+  // Q u P mode (every job of a call or none): c0qp = the job's c0 as a [limbs+K][N] polynomial
+  // over Q u P, added as sigma_g(c0qp) on every limb (the c0 half of an accumulator that was
+  // never ModDown'd); direct_c1 != null: no key switch at all, (c0qp, direct_c1) join as they are
+  const u64* c0qp = nullptr;
+  const u64* direct_c1 = nullptr;
   static constexpr u64 kNoKeyOverride = ~0ULL;
   u64 key() const { return key_id == kNoKeyOverride ? g : key_id; }
 };
@@ -338,7 +343,10 @@ BufPtr keyswitch_sum_accs(Context& ctx, const std::vector<const u64*>& inputs, c
   std::vector<std::vector<const SumJob*>> by_group(ngroups);
   for (const SumJob& j : jobs) by_group[j.group].push_back(&j);
   // every group = one input under the same key list (a hoisted stage)?
-  bool shared = ngroups > 1 && !by_group[0].empty() && (int)by_group[0].size() <= kMaxSharedKeys;
+  const bool qp = !jobs.empty() && jobs[0].c0qp != nullptr;
+  for (const SumJob& j : jobs)
+    if ((j.c0qp != nullptr) != qp) throw Error(ErrKind::internal, "rotate_sum: mixed Q and Q u P c0 terms");
+  bool shared = !qp && ngroups > 1 && !by_group[0].empty() && (int)by_group[0].size() <= kMaxSharedKeys;
   for (const SumJob& j : jobs) shared = shared && j.key_id == SumJob::kNoKeyOverride;
   for (int r = 0; r < ngroups && shared; ++r) {
     shared = by_group[r].size() == by_group[0].size();
@@ -378,10 +386,15 @@ BufPtr keyswitch_sum_accs(Context& ctx, const std::vector<const u64*>& inputs, c
         if (nj + gsz > kMaxSumJobs) break;
         kj.begin[R] = nj;
         for (const SumJob* j : by_group[r0 + R]) {
-          kj.key[nj] = ctx.key(j->key());
-          kj.ext[nj] = ext->ptr + (std::size_t)j->in * ext_words;
-          kj.d[nj] = inputs[j->in];
-          kj.c0[nj] = c0s[j->in];
+          if (j->direct_c1) {
+            kj.direct[nj] = 1;
+            kj.d[nj] = j->direct_c1;
+          } else {
+            kj.key[nj] = ctx.key(j->key());
+            kj.ext[nj] = ext->ptr + (std::size_t)j->in * ext_words;
+            kj.d[nj] = inputs[j->in];
+          }
+          kj.c0[nj] = qp ? j->c0qp : c0s[j->in];
           kj.g[nj] = j->g;
           ++nj;
         }
@@ -389,6 +402,7 @@ BufPtr keyswitch_sum_accs(Context& ctx, const std::vector<const u64*>& inputs, c
       }
       kj.begin[R] = nj;
       kj.ngroups = R;
+      kj.c0_qp = qp ? 1 : 0;
       for (int r = 0; r < R; ++r) kj.acc[r] = acc_of(r0 + r);
       ks_inner_sum(t, kj, limbs, st);
       r0 += R;
@@ -531,6 +545,54 @@ std::vector<Ciphertext> keyswitch_sum(Context& ctx, const std::vector<const u64*
 
 }  // namespace
 
+namespace {
+// ModDown of the c1 half alone of Q u P accumulators ([2][limbs+K][N] each): [n][limbs][N]
+BufPtr moddown_c1(Context& ctx, const std::vector<u64*>& accp, int limbs) {
+  const DevTables& t = ctx.dev();
+  cudaStream_t st = ctx.stream();
+  const std::size_t N = ctx.N();
+  const int L = ctx.L(), K = ctx.K(), E = limbs + K;
+  const int n = (int)accp.size();
+  BufPtr out = ctx.alloc((std::size_t)n * limbs * N);
+  for (int r0 = 0; r0 < n; r0 += kMaxBases) {
+    const int R = std::min(kMaxBases, n - r0);
+    // the special limbs go to the coefficient domain OUT of place: the accumulator stays whole
+    // (an unrotated giant that also enters conjugated is added as it is afterwards)
+    BufPtr z = ctx.alloc((std::size_t)R * K * N);
+    LimbSet zs = limbset(z->ptr, R, (std::size_t)K * N, K, 0, L);
+    LimbSet src = zs;
+    src.nbase = R;
+    src.blocks_per_base = 1;
+    for (int r = 0; r < R; ++r) src.base[r] = accp[r0 + r] + (std::size_t)E * N + (std::size_t)limbs * N;
+    ntt_inverse(t, zs, st, &src);
+    BufPtr conv = ctx.alloc((std::size_t)R * limbs * N);
+    PolyList cl{}, zl{}, al{}, ol{}, addl{};
+    cl.n = zl.n = al.n = ol.n = addl.n = R;
+    for (int r = 0; r < R; ++r) {
+      cl.p[r] = conv->ptr + (std::size_t)r * limbs * N;
+      zl.p[r] = z->ptr + (std::size_t)r * K * N;
+      al.p[r] = accp[r0 + r] + (std::size_t)E * N;
+      ol.p[r] = out->ptr + (std::size_t)(r0 + r) * limbs * N;
+      addl.p[r] = nullptr;
+      addl.g[r] = 1;
+    }
+    moddown_conv(t, cl, zl, limbs, st);
+    ntt_forward_epilogue(t, limbset(conv->ptr, R, (std::size_t)limbs * N, limbs, limbs, L),
+                         moddown_epilogue(t, ol, al, addl), st);
+    ctx.stats.ntt_limbs += (std::size_t)R * (K + limbs);
+  }
+  return out;
+}
+
+bool dh_c0qp_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FHEON_DH_C0QP");
+    return e ? std::atoi(e) != 0 : true;  // FHEON_DH_C0QP=0: the two-ModDown form, for A/B runs
+  }();
+  return on;
+}
+}  // namespace
+
 // Double-hoisted baby-step giant-step transform:
 //   out = rescale( sum_g rot( ModDown( sum_t pt_{g,t} (*) B_{b(g,t)} ), G_g ) )
 // B_b = (P sigma_b(c0) + ks0_b, ks1_b) over Q u P is baby rotation b WITHOUT its
@@ -637,6 +699,59 @@ std::vector<Ciphertext> bsgs_double_hoisted_many(Context& ctx, const std::vector
     }
   std::vector<u64*> accp(nout);
   for (std::size_t o = 0; o < nout; ++o) accp[o] = inner->ptr + o * accw;
+  const bool fused_tail = limbs >= 2 && bconv_tc_enabled() && K + 1 + 2 <= 16;
+  if (dh_c0qp_enabled() && fused_tail && (with_conj ? 2 : 1) * ng <= kMaxSumJobs) {
+    // Giant steps on the un-ModDown'd inner sums: only the c1 half of a giant is brought down to Q
+    // (the key switch decomposes it); its c0 half stays over Q u P and joins the rotate-and-sum
+    // accumulator as sigma_G(c0) on every limb, and the unrotated giant joins whole, with no key
+    // switch and no ModDown of its own.  Half the giants' ModDown work, and one rounding fewer
+    // on c0 (the result differs from the two-ModDown form by rounding only).
+    const u64 conj = 2 * (u64)ctx.N() - 1, twoN = 2 * (u64)ctx.N();
+    std::vector<int> slot_of(nout, -1);  // (g, i) -> c1 input index
+    std::vector<u64*> need;
+    for (int g = 0; g < ng; ++g) {
+      const bool ident_g = ctx.galois(giants[g].rot) == 1;
+      for (int i = 0; i < B; ++i)
+        if (!ident_g || with_conj) {
+          slot_of[(std::size_t)g * B + i] = (int)need.size();
+          need.push_back(accp[(std::size_t)g * B + i]);
+        }
+    }
+    BufPtr c1q = need.empty() ? nullptr : moddown_c1(ctx, need, limbs);
+    std::vector<const u64*> inputs, c0s;
+    for (std::size_t k = 0; k < need.size(); ++k) {
+      inputs.push_back(c1q->ptr + k * (std::size_t)limbs * N);
+      c0s.push_back(nullptr);
+    }
+    std::vector<SumJob> sj;
+    for (int i = 0; i < B; ++i)
+      for (int g = 0; g < ng; ++g) {
+        const u64 ge = ctx.galois(giants[g].rot);
+        const u64* acc = accp[(std::size_t)g * B + i];
+        const int in = slot_of[(std::size_t)g * B + i];
+        ctx.record(0, giants[g].rot);
+        ctx.stats.rotations++;
+        for (std::size_t j = 0; j < giants[g].terms.size(); ++j) {
+          ctx.stats.mult_plain++;
+          ctx.record(1, lv - 1);
+        }
+        SumJob a{ge, in, i};
+        a.c0qp = acc;
+        if (ge == 1) a.direct_c1 = acc + (std::size_t)E * N;
+        sj.push_back(a);
+        if (with_conj) {
+          SumJob c{(ge * conj) % twoN, in, i};
+          c.c0qp = acc;
+          sj.push_back(c);
+        }
+      }
+    BufPtr accs2 = keyswitch_sum_accs(ctx, inputs, c0s, limbs, sj, B);
+    std::vector<u64*> ap(B);
+    for (int i = 0; i < B; ++i) ap[i] = accs2->ptr + (std::size_t)i * accw;
+    std::vector<Ciphertext> outs = moddown_rescale_accs(ctx, ap, std::vector<Ciphertext>(B), limbs);
+    for (Ciphertext& o : outs) o.scale = h.T[lv - 1];
+    return outs;
+  }
   std::vector<Ciphertext> rows = moddown_accs(ctx, accp, limbs);
   const double sc = h.T[lv - 1] * (double)h.q[lv];  // plaintexts encoded at T_{lv-1} q_lv / scale(x)
   std::vector<std::vector<std::pair<Ciphertext, long>>> terms(B);

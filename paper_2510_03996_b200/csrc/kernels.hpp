@@ -177,6 +177,11 @@ struct KsSumJobs {
   int begin[kMaxSumGroups + 1];
   u64* acc[kMaxSumGroups];  // [2][limbs+K][N]
   int ngroups;
+  // c0_qp: c0[j] is a Q u P polynomial ([limbs+K][N], already P-scaled: the c0 half of an
+  // un-ModDown'd accumulator) added as sigma_g(c0) on every limb instead of P sigma_g(c0) on Q.
+  // direct[j] (c0_qp only): no key switch -- c0[j] and d[j] ([limbs+K][N] each) are added as they are.
+  int c0_qp;
+  unsigned char direct[kMaxSumJobs];
 };
 void ks_inner_sum(const DevTables& t, const KsSumJobs& jobs, int limbs, cudaStream_t st);
 // Hoisted rotate-and-sum over many inputs sharing ONE key list (channel sums, FC

@@ -294,6 +294,17 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
     const u64* key = jobs.key[jb];
     const u64* ext = jobs.ext[jb];
     const u64* d = jobs.d[jb];
+    if (jobs.c0_qp) {  // CTA-uniform
+      const u64* c0 = jobs.c0[jb] + (std::size_t)t * N;
+      s0[0] = add_mod(s0[0], c0[src[0]], P.q);
+      s0[1] = add_mod(s0[1], c0[src[1]], P.q);
+      if (jobs.direct[jb]) {
+        const u64* c1 = d + (std::size_t)t * N;
+        s1[0] = add_mod(s1[0], c1[src[0]], P.q);
+        s1[1] = add_mod(s1[1], c1[src[1]], P.q);
+        continue;
+      }
+    }
     for (int j = 0; j < beta; ++j) {
       const u64* vb = j == jown ? d + (std::size_t)t * N : ext + ((std::size_t)j * E + t) * N;
       const u64* kj = key + ((std::size_t)(j * 2) * (L + K) + pt) * N;
@@ -305,7 +316,7 @@ __global__ void k_ks_inner_sum(KsSumJobs jobs, const PrimeConst* __restrict__ pc
       a0[1].mac(v1, kb.y);
       a1[1].mac(v1, ka.y);
     }
-    if (t < limbs) {
+    if (t < limbs && !jobs.c0_qp) {
       const u64* c0 = jobs.c0[jb] + (std::size_t)t * N;
       a0[0].mac(c0[src[0]], pm);
       a0[1].mac(c0[src[1]], pm);

@@ -1,19 +1,8 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_primitives.py tests/test_gpu_layers.py tests/test_gpu_keys_client_server.py -x -q -m gpu 2>&1 | tail -3
-for rep in 1 2; do
-  timeout 900 python bench.py --quick --no-cpu-baseline --no-rotations > gpurun_out/bq_$rep.log 2> gpurun_out/bq_$rep.err; echo rc=$?
-  tail -2 gpurun_out/bq_$rep.err
-  python - <<P
-import json
-d=json.loads(open("gpurun_out/bq_$rep.log").read().strip().splitlines()[-1])
-print("$rep", {k:d[k] for k in ("value","latency_s_per_image","ms_per_step")}, "e2e", d["e2e"]["value"])
-P
-done
-timeout 900 python bench.py --quick --no-cpu-baseline --no-rotations --in-flight 3 > gpurun_out/bq_3.log 2> gpurun_out/bq_3.err; echo rc=$?
-python - <<P
-import json
-d=json.loads(open("gpurun_out/bq_3.log").read().strip().splitlines()[-1])
-print("F3", {k:d[k] for k in ("value","latency_s_per_image","ms_per_step")}, "e2e", d["e2e"]["value"])
-P
-nvidia-smi --query-gpu=memory.used --format=csv
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 1500 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$?
+tail -3 gpurun_out/bench.err
+cut -c1-400 gpurun_out/bench.log
