@@ -1,8 +1,11 @@
 set -x
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
-timeout 1500 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$?
-tail -3 gpurun_out/bench.err
-cut -c1-400 gpurun_out/bench.log
+for mode in noclk 2000 500; do
+  if [ $mode = noclk ]; then export FHEON_NO_CLOCKS=1; else unset FHEON_NO_CLOCKS; export FHEON_CLOCKS_MS=$mode; fi
+  timeout 900 python bench.py --quick --no-cpu-baseline --no-rotations > gpurun_out/bq_$mode.log 2> gpurun_out/bq_$mode.err; echo rc=$?
+  python - <<P
+import json
+d=json.loads(open("gpurun_out/bq_$mode.log").read().strip().splitlines()[-1])
+print("$mode", {k:d[k] for k in ("value","latency_s_per_image","ms_per_step")}, "e2e", d["e2e"]["value"], d["clocks"])
+P
+done
