@@ -1,9 +1,11 @@
+# One GPU call of a round: smoke, the whole -m gpu suite, the default bench and the reference arm.
 set -x
 mkdir -p gpurun_out
-for B in 1 4; do
-FHEON_BOOT_PROFILE=all ACTIVES=4096 REPS=1 timeout 1200 ncu --profile-from-start off --set full --clock-control none \
-  -k regex:"k_ks_inner_sum|k_mac_bsgs" --launch-skip 3 -c 5 -o /tmp/prof_b$B python scripts/boot_batch_time.py $B > gpurun_out/ncu_b$B.log 2>&1
-echo rc=$?
-python scripts/ncu_kernel_traffic.py /tmp/prof_b$B.ncu-rep > gpurun_out/ncu_boot_batch_b$B.csv
-cat gpurun_out/ncu_boot_batch_b$B.csv
-done
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 1500 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$?
+tail -3 gpurun_out/bench.err
+cut -c1-400 gpurun_out/bench.log
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err; echo rc=$?
+cut -c1-300 gpurun_out/bench_ref.log
