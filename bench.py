@@ -1015,9 +1015,9 @@ def main():
     ap.add_argument("--no-resnet", action="store_true", help="skip the ResNet-20 / VGG-16 model variants")
     ap.add_argument("--no-vgg", action="store_true", help="skip VGG-16")
     ap.add_argument("--depth", type=int, default=HEAD_DEPTH, help="ResNet-20 depth budget of the headline chain")
-    ap.add_argument("--in-flight", type=int, default=2,
+    ap.add_argument("--in-flight", type=int, default=3,
                     help="batches in flight per GPU (key-sharing contexts, one host thread each)")
-    ap.add_argument("--image-batch", type=int, default=4, help="images per lockstep batch (forward_batch)")
+    ap.add_argument("--image-batch", type=int, default=3, help="images per lockstep batch (forward_batch)")
     ap.add_argument("--models", default="", help="comma-separated name prefixes of the model cases to run")
     ap.add_argument("--no-rotations", action="store_true", help="skip the configs[1] rotation block")
     ap.add_argument("--model-case", default="", help=argparse.SUPPRESS)

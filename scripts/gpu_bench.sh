@@ -1,6 +1,5 @@
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 mkdir -p gpurun_out
-timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$?
+timeout 1500 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$?
 tail -3 gpurun_out/bench.err
-cat gpurun_out/bench.log
+cut -c1-400 gpurun_out/bench.log
